@@ -1,0 +1,207 @@
+/*
+ * mars_b200.h -- C ABI of the B200-native MARS scheduling step.
+ *
+ * The reference (arXiv 2604.26963, /root/reference/pkg/src/agentsched) has no
+ * FFI: its pluggable boundary is the Python PolicyBase object
+ * (baselines.py:56-101) plus the module-level balance_and_admit
+ * (control.py:166-208).  These entry points are what a ctypes/cffi binding of
+ * that boundary needs; every one names the reference interface it replaces.
+ * The Python mirror of the plugin API (paper_2604_26963_b200/policy.py,
+ * admission.py) sits on top of exactly this surface.
+ *
+ * Conventions
+ *   - plain pointers and sizes, no framework types; every function returns
+ *     MARS_OK (0) or an error category (mars_last_error() has the text).
+ *     MARS_ERR_CONTRACT maps to agentsched ContractViolation (engine.py:30),
+ *     everything else to RuntimeError.
+ *   - one host thread per context; all device work is ordered on the
+ *     context's stream (mars_set_stream), calls marked "sync" return after the
+ *     stream drained.
+ *   - row = slot index in the device session table, 0 <= row < max_rows.
+ *     rank = dense lexicographic rank of the session-id string (the
+ *     reference's final tie-break, baselines.py:374-377).
+ */
+#ifndef MARS_B200_H
+#define MARS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MARS_OK 0
+#define MARS_ERR_CONTRACT 1
+#define MARS_ERR_CUDA 2
+#define MARS_ERR_CAPACITY 3
+#define MARS_ERR_ARG 4
+
+#define MARS_ABI_VERSION 1
+
+/* phase codes: agentsched/engine.py:250-256 */
+#define MARS_WAITING_ADMISSION 0
+#define MARS_PREFILL 1
+#define MARS_DECODE 2
+#define MARS_TOOL 3
+#define MARS_WAITING_RESUME 4
+#define MARS_DONE 5
+#define MARS_EMPTY 7
+
+/* row flag bits */
+#define MARS_F_ACTIVE 1u   /* admitted, not finished (sim.py:133 `active`) */
+#define MARS_F_QUEUED 2u   /* in the admission queue (sim.py:132) */
+#define MARS_F_PINNED 4u   /* in the pin registry (baselines.py:349) */
+#define MARS_F_BOUNDARY 8u /* S2 retention requested this step */
+#define MARS_F_LONG 16u    /* QueueEntry.is_long_session (control.py:91) */
+
+/* journal op codes (KvPool observer ops, engine.py:129-143 + evict) */
+#define MARS_J_ALLOC 1
+#define MARS_J_EVICT_RUNNING 2
+#define MARS_J_EVICT_PINNED 3
+#define MARS_J_EXPIRE 4
+
+typedef struct mars_ctx mars_ctx;
+
+/* All constants of GpuModel, MlfqConfig, RetentionConfig, PressureConfig,
+ * ControllerConfig and the MarsPolicy ablation switches.  Infinite level
+ * boundaries / quotas are INT64_MAX.  mars_config_default() fills the
+ * reference defaults (engine.py:24-27, scheduler.py:34-41,
+ * telemetry.py:14-19, control.py:20-27). */
+typedef struct mars_config {
+  int32_t block_size;          /* engine.py:26 */
+  int32_t token_budget;        /* engine.py:24 */
+  double tick_duration_s;      /* engine.py:25 */
+  int32_t num_levels;          /* scheduler.py:34 (<= 4) */
+  int32_t max_promotions;      /* scheduler.py:50 */
+  int32_t max_decode_slots;    /* scheduler.py:38 */
+  int32_t window_size;         /* scheduler.py:61-63 (<= 128) */
+  int64_t level_bounds[4];     /* scheduler.py:35 */
+  int64_t level_quotas[4];     /* scheduler.py:36 */
+  double promotion_wait_s;     /* scheduler.py:37 */
+  double deadline_slack;       /* scheduler.py:39 */
+  double max_pin_horizon_s;    /* scheduler.py:40 */
+  double pressure_weight_clip; /* scheduler.py:41 */
+  double cpu_high_fraction, cpu_low_fraction;   /* telemetry.py:16-17 */
+  double kv_high_watermark, kv_low_watermark;   /* telemetry.py:18-19 */
+  int32_t hysteresis_window;                    /* telemetry.py:15 */
+  double ema_smoothing;                         /* telemetry.py:14 */
+  double initial_tool_estimate_s;               /* telemetry.py:56 */
+  int32_t w_min;                                /* control.py:20 */
+  double aimd_increase, aimd_decrease;          /* control.py:21-22 */
+  double control_interval_s;                    /* control.py:23 */
+  double initial_window;                        /* control.py:24 */
+  double cpu_oversubscription;                  /* control.py:25 */
+  double reserve_fraction;                      /* control.py:26 */
+  double long_session_fraction;                 /* control.py:27 */
+  int32_t enable_coordinator;                   /* baselines.py:339 */
+  int32_t enable_coscheduler;                   /* baselines.py:340 */
+} mars_config;
+
+/* Structure-of-arrays column pointers (host side).  NULL = column not
+ * transferred.  Widths are the minimal exact widths of the reference values
+ * (SURVEY.md §8 canonical SoA). */
+typedef struct mars_cols {
+  uint8_t *phase, *flags, *level, *promos, *plevel;
+  double *ready_since, *wait_since, *deadline, *arrival;
+  int32_t *context, *kv, *rem_decode, *pinned_blocks, *req_blocks, *r0_prefill, *r0_decode,
+      *preempt;
+  int64_t *served;
+  uint32_t *rank;
+} mars_cols;
+
+/* Device-resident scalar state: KvPool counters, the Telemetry value
+ * (telemetry.py:66-96) and ControllerState (control.py:52-61). */
+typedef struct mars_scalars {
+  int64_t total_blocks, free_blocks;
+  double w_adm, last_update;
+  int32_t cpu_overloaded, kv_overloaded;
+  int32_t cpu_high_streak, cpu_low_streak, kv_high_streak, kv_low_streak;
+  int32_t has_ema_tool, has_ema_blocks, has_blocks_seed;
+  double ema_tool, ema_blocks, blocks_seed;
+  double last_w_adm, last_window_update;
+  int32_t has_last_w_adm;
+  int64_t available_kv;
+  double kv_usage_ratio;
+  int64_t active_sessions;
+  int32_t active_tools, queued_tools;
+  int64_t queue_len;
+} mars_scalars;
+
+typedef struct mars_step_in {
+  double now;
+  int32_t control_due;     /* sim.py:329: run refresh_pressure + balance_and_admit */
+  int32_t active_tools;    /* ToolPlane.active_count() at the probe (sim.py:327) */
+  int32_t queued_tools;    /* ToolPlane.queued_count() */
+  int32_t worker_slots;    /* ToolPlane.worker_slots */
+  int32_t skip_expiry;     /* drop-in mode: the sim evicts expired pins itself */
+} mars_step_in;
+
+/* Step result.  Pointers refer to pinned host buffers owned by the context,
+ * valid until the next call on it. */
+typedef struct mars_step_out {
+  int32_t status;          /* 0 ok */
+  int32_t n_expired, n_admitted, n_window, n_decode, n_prefill, n_evict, n_journal, n_retention;
+  int32_t n_ready, n_promoted, pack_mode;
+  int64_t total_tokens;
+  int64_t free_after_expiry, free_blocks;
+  int64_t limit, slots;
+  const uint32_t *expired_rows; const int32_t *expired_blocks;   /* rank order */
+  const uint32_t *admitted_rows;                                 /* packed order */
+  const uint32_t *window_rows;                                   /* priority order */
+  const uint32_t *decode_rows;
+  const uint32_t *prefill_rows; const int32_t *prefill_grants;
+  const uint32_t *evict_rows; const uint8_t *evict_kind; const int32_t *evict_blocks;
+  const uint8_t *journal_op; const uint32_t *journal_row; const int32_t *journal_n;
+  const uint32_t *ret_rows; const uint8_t *ret_pin;
+  const double *ret_benefit, *ret_cost, *ret_deadline;
+} mars_step_out;
+
+/* ---- lifecycle ------------------------------------------------------- */
+int mars_abi_version(void);
+void mars_config_default(mars_config* cfg);
+int mars_create(const mars_config* cfg, int device, int64_t max_rows, int64_t max_queue,
+                mars_ctx** out);
+int mars_destroy(mars_ctx* ctx);
+const char* mars_last_error(mars_ctx* ctx);
+int mars_set_stream(mars_ctx* ctx, void* cuda_stream);
+
+/* ---- session-state store (replaces Call/PriorityState/PinnedSession/QueueEntry
+ *      objects: engine.py:259-319, scheduler.py:78-84,165-172, control.py:64-73) */
+int mars_set_rows(mars_ctx* ctx, int64_t n_rows);                 /* live row count */
+int mars_upsert_rows(mars_ctx* ctx, int64_t n, const int64_t* rows, const mars_cols* cols);
+int mars_read_rows(mars_ctx* ctx, int64_t n, const int64_t* rows, mars_cols* out);   /* sync */
+/* admission list (sim.py:132 admission_queue; control.py:190 persistent order) */
+int mars_set_queue(mars_ctx* ctx, int64_t n, const uint32_t* rows, const int32_t* req_blocks,
+                   const uint8_t* is_long);
+int mars_get_queue(mars_ctx* ctx, int64_t cap, uint32_t* rows, int64_t* n);          /* sync */
+int mars_set_scalars(mars_ctx* ctx, const mars_scalars* s);
+int mars_get_scalars(mars_ctx* ctx, mars_scalars* s);                               /* sync */
+
+/* ---- the step (S1-S5): replaces one tick's sim.py:324-342 scheduling half:
+ *      MarsPolicy.expired_pins + evictions, Telemetry.probe, refresh_pressure,
+ *      balance_and_admit + admit, decide_retention for BOUNDARY rows,
+ *      MarsPolicy.plan_tick (promote_waiting + build_plan + reclaim). */
+int mars_step(mars_ctx* ctx, const mars_step_in* in, mars_step_out* out);          /* sync */
+int mars_step_enqueue(mars_ctx* ctx, const mars_step_in* in);   /* async, device-resident */
+int mars_step_fetch(mars_ctx* ctx, mars_step_out* out);          /* sync, after enqueue */
+
+/* decide_retention (scheduler.py:190-213) for explicit inputs; elementwise f64
+ * on the device, bit-exact (no FMA contraction). */
+int mars_retention_batch(mars_ctx* ctx, int64_t n, const int32_t* context, const int32_t* kv,
+                         int64_t total_blocks, double kv_usage_ratio, double ema_tool,
+                         double now, uint8_t* pin, double* benefit, double* cost,
+                         double* deadline);                                         /* sync */
+
+/* ---- checkpoint / resume of the whole device state (for replay and bench) */
+int mars_checkpoint(mars_ctx* ctx);
+int mars_restore(mars_ctx* ctx);
+/* write `bytes` of scratch to evict L2 between timed steps */
+int mars_flush_l2(mars_ctx* ctx, int64_t bytes);
+
+/* number of kernel launches issued by the last step (incl. early-exit ones) */
+int mars_last_launch_count(mars_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MARS_B200_H */

@@ -59,6 +59,8 @@ class World:
         self.tel.ema_tool_duration = snap.ema_tool
         self.tel.ema_blocks_per_session = snap.ema_blocks
         self.tel.blocks_seed = snap.blocks_seed
+        for k, v in getattr(snap, "telemetry", {}).items():
+            setattr(self.tel, k, v)
         self.ctl = controller or adm.Controller(initial_window=snap.initial_window)
         self.sessions: List[Session] = []
         self.row_of: Dict[str, int] = {}

@@ -1,0 +1,717 @@
+// C ABI of the B200 MARS step (include/mars_b200.h): context lifecycle,
+// device allocation of the session-state store, uploads/downloads, the step.
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "mars_internal.cuh"
+#include "mars_launch.h"
+
+namespace {
+
+struct ColSpec {
+  size_t host_off;  // offset of the pointer inside mars_cols
+  void** dev;       // address of the device pointer inside Tab
+  int esz;
+  void* ckpt;       // checkpoint copy
+};
+
+}  // namespace
+
+struct mars_ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr, side = nullptr;
+  bool own_stream = true;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  mars_config hcfg;
+  Cfg cfg;
+  i64 max_rows = 0, max_queue = 0, n_rows = 0;
+  Tab tab;
+  Queue queue;
+  Lsd qlsd, xlsd;
+  Work* work = nullptr;
+  Bufs bufs;
+  mars_scalars* sc = nullptr;
+  i32* qsel = nullptr;
+  std::vector<ColSpec> cols;
+  // host staging
+  mars_step_in* h_in = nullptr;
+  Work* h_work = nullptr;
+  mars_scalars* h_sc = nullptr;
+  unsigned char* h_out = nullptr;  // pinned output arena
+  size_t h_out_bytes = 0;
+  // device staging for row scatter/gather
+  unsigned char* d_stage = nullptr;
+  i64* d_rows = nullptr;
+  // checkpoint
+  bool have_ckpt = false;
+  void* ck_q[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  mars_scalars* ck_sc = nullptr;
+  i32* ck_qsel = nullptr;
+  i64 ck_q_upper = 0;
+  int ck_q_maxreq = 0;
+  // host knowledge of the queue (launch-shape decisions only)
+  i64 q_upper = 0;
+  int q_maxreq = 0;
+  i64 pinned_upper = 0;
+  int last_launches = 0;
+  unsigned flush_salt = 1;
+  std::string err;
+};
+
+static int fail(mars_ctx* c, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return code;
+}
+
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(ctx, MARS_ERR_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                    \
+  } while (0)
+
+static Cfg make_cfg(const mars_config& h) {
+  Cfg c;
+  memset(&c, 0, sizeof c);
+  c.bs = h.block_size;
+  c.budget = h.token_budget;
+  c.window = h.window_size;
+  c.max_dec = h.max_decode_slots;
+  c.num_levels = h.num_levels;
+  c.max_promos = h.max_promotions;
+  c.hyst = h.hysteresis_window;
+  c.w_min = h.w_min;
+  c.coord = h.enable_coordinator;
+  c.cosched = h.enable_coscheduler;
+  for (int i = 0; i < 4; ++i) {
+    c.bounds[i] = h.level_bounds[i];
+    c.quotas[i] = h.level_quotas[i];
+  }
+  c.tick_s = h.tick_duration_s;
+  c.prefill_rate = (double)h.token_budget / h.tick_duration_s;  // engine.py:240-242
+  c.promo_wait = h.promotion_wait_s;
+  c.slack = h.deadline_slack;
+  c.horizon = h.max_pin_horizon_s;
+  c.pw_clip = h.pressure_weight_clip;
+  c.cpu_hi = h.cpu_high_fraction;
+  c.cpu_lo = h.cpu_low_fraction;
+  c.kv_hi = h.kv_high_watermark;
+  c.kv_lo = h.kv_low_watermark;
+  c.ema_alpha = h.ema_smoothing;
+  c.tool_prior = h.initial_tool_estimate_s;
+  c.ai = h.aimd_increase;
+  c.md = h.aimd_decrease;
+  c.ctl_interval = h.control_interval_s;
+  c.init_window = h.initial_window;
+  c.oversub = h.cpu_oversubscription;
+  c.reserve = h.reserve_fraction;
+  c.long_frac = h.long_session_fraction;
+  return c;
+}
+
+extern "C" {
+
+int mars_abi_version(void) { return MARS_ABI_VERSION; }
+
+void mars_config_default(mars_config* h) {
+  memset(h, 0, sizeof *h);
+  h->block_size = 16;
+  h->token_budget = 512;
+  h->tick_duration_s = 0.064;
+  h->num_levels = 4;
+  h->max_promotions = 3;
+  h->max_decode_slots = 64;
+  h->window_size = 128;
+  const int64_t inf = INT64_MAX;
+  int64_t b[4] = {4000, 32000, 128000, inf}, q[4] = {2000, 8000, 32000, inf};
+  for (int i = 0; i < 4; ++i) {
+    h->level_bounds[i] = b[i];
+    h->level_quotas[i] = q[i];
+  }
+  h->promotion_wait_s = 10.0;
+  h->deadline_slack = 2.0;
+  h->max_pin_horizon_s = 60.0;
+  h->pressure_weight_clip = 100.0;
+  h->cpu_high_fraction = 0.90;
+  h->cpu_low_fraction = 0.70;
+  h->kv_high_watermark = 0.90;
+  h->kv_low_watermark = 0.70;
+  h->hysteresis_window = 3;
+  h->ema_smoothing = 0.3;
+  h->initial_tool_estimate_s = 5.0;
+  h->w_min = 2;
+  h->aimd_increase = 1.0;
+  h->aimd_decrease = 0.5;
+  h->control_interval_s = 2.0;
+  h->initial_window = 8.0;
+  h->cpu_oversubscription = 1.5;
+  h->reserve_fraction = 0.10;
+  h->long_session_fraction = 0.25;
+  h->enable_coordinator = 1;
+  h->enable_coscheduler = 1;
+}
+
+const char* mars_last_error(mars_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int mars_last_launch_count(mars_ctx* ctx) { return ctx ? ctx->last_launches : -1; }
+
+static int alloc(mars_ctx* ctx, void** p, size_t bytes) {
+  CK(cudaMalloc(p, bytes ? bytes : 16));
+  return MARS_OK;
+}
+
+#define ALLOC(ptr, bytes)                                      \
+  do {                                                         \
+    int rc_ = alloc(ctx, (void**)&(ptr), (size_t)(bytes));     \
+    if (rc_) {                                                 \
+      mars_destroy(ctx);                                       \
+      return rc_;                                              \
+    }                                                          \
+  } while (0)
+
+int mars_create(const mars_config* hcfg, int device, int64_t max_rows, int64_t max_queue,
+                mars_ctx** out) {
+  if (!hcfg || !out || max_rows < 1 || max_queue < 0) return MARS_ERR_ARG;
+  if (hcfg->window_size < 1 || hcfg->window_size > WIN_MAX || hcfg->num_levels < 1 ||
+      hcfg->num_levels > 4 || hcfg->block_size < 1 || hcfg->token_budget < 1 ||
+      hcfg->max_decode_slots < 0)
+    return MARS_ERR_ARG;
+  if (max_rows >= (1ll << 31)) return MARS_ERR_ARG;
+  mars_ctx* ctx = new mars_ctx();
+  ctx->device = device;
+  ctx->hcfg = *hcfg;
+  ctx->cfg = make_cfg(*hcfg);
+  ctx->max_rows = max_rows;
+  ctx->max_queue = max_queue < 1 ? 1 : max_queue;
+  CK(cudaSetDevice(device));
+  CK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
+  CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+  {
+    int rc = mars_kernels_init();
+    if (rc) return fail(ctx, MARS_ERR_CUDA, "kernel init: %s", cudaGetErrorString((cudaError_t)rc));
+  }
+  const i64 R = max_rows, Qc = ctx->max_queue;
+  Tab& t = ctx->tab;
+  memset(&t, 0, sizeof t);
+  t.cap = R;
+  ALLOC(t.phase, R);
+  ALLOC(t.flags, R);
+  ALLOC(t.level, R);
+  ALLOC(t.promos, R);
+  ALLOC(t.plevel, R);
+  ALLOC(t.rs, R * 8);
+  ALLOC(t.ws, R * 8);
+  ALLOC(t.dl, R * 8);
+  ALLOC(t.arr, R * 8);
+  ALLOC(t.ctx, R * 4);
+  ALLOC(t.kv, R * 4);
+  ALLOC(t.rem, R * 4);
+  ALLOC(t.pb, R * 4);
+  ALLOC(t.req, R * 4);
+  ALLOC(t.r0p, R * 4);
+  ALLOC(t.r0d, R * 4);
+  ALLOC(t.pre, R * 4);
+  ALLOC(t.served, R * 8);
+  ALLOC(t.rank, R * 4);
+  ALLOC(t.winpos, R * 2);
+  CK(cudaMemset(t.winpos, 0xff, R * 2));
+  CK(cudaMemset(t.phase, MARS_EMPTY, R));
+  CK(cudaMemset(t.flags, 0, R));
+  Queue& q = ctx->queue;
+  q.cap = Qc;
+  for (int i = 0; i < 2; ++i) {
+    ALLOC(q.row[i], Qc * 4);
+    ALLOC(q.req[i], Qc * 4);
+    ALLOC(q.lng[i], Qc);
+  }
+  i64 Lc = Qc > R ? Qc : R;
+  Lsd* ls[2] = {&ctx->qlsd, &ctx->xlsd};
+  for (int j = 0; j < 2; ++j) {
+    ls[j]->cap = Lc;
+    for (int i = 0; i < 2; ++i) {
+      ALLOC(ls[j]->k[i], Lc * 8);
+      ALLOC(ls[j]->v[i], Lc * 4);
+    }
+    ALLOC(ls[j]->cnt, (size_t)LSD_G * 256 * 4);
+  }
+  ALLOC(ctx->work, sizeof(Work));
+  ALLOC(ctx->sc, sizeof(mars_scalars));
+  ALLOC(ctx->qsel, sizeof(i32));
+  CK(cudaMemset(ctx->qsel, 0, sizeof(i32)));
+  Bufs& b = ctx->bufs;
+  memset(&b, 0, sizeof b);
+  ALLOC(b.exp_row, R * 4);
+  ALLOC(b.exp_blk, R * 4);
+  ALLOC(b.exp_rank, R * 4);
+  ALLOC(b.exp_row_sorted, R * 4);
+  ALLOC(b.exp_blk_sorted, R * 4);
+  ALLOC(b.wc_hi, R * 8);
+  ALLOC(b.wc_lo, R * 8);
+  ALLOC(b.wc_row, R * 4);
+  ALLOC(b.vc_key, R * 8);
+  ALLOC(b.vc_whi, R * 8);
+  ALLOC(b.vc_wlo, R * 8);
+  ALLOC(b.vc_row, R * 4);
+  ALLOC(b.vc_blk, R * 4);
+  ALLOC(b.ret_row, R * 4);
+  ALLOC(b.ret_pin, R);
+  ALLOC(b.ret_b, R * 8);
+  ALLOC(b.ret_c, R * 8);
+  ALLOC(b.ret_d, R * 8);
+  ALLOC(b.admitted, Qc * 4);
+  ALLOC(b.win_rows, WIN_MAX * 4);
+  ALLOC(b.dec_rows, WIN_MAX * 4);
+  ALLOC(b.pre_rows, WIN_MAX * 4);
+  ALLOC(b.pre_grant, WIN_MAX * 4);
+  b.ev_cap = R;
+  ALLOC(b.ev_row, R * 4);
+  ALLOC(b.ev_kind, R);
+  ALLOC(b.ev_blk, R * 4);
+  b.j_cap = R + 2 * WIN_MAX;
+  ALLOC(b.j_op, b.j_cap);
+  ALLOC(b.j_row, b.j_cap * 4);
+  ALLOC(b.j_n, b.j_cap * 4);
+  ALLOC(ctx->d_stage, R * 8);
+  ALLOC(ctx->d_rows, R * 8);
+  // host pinned
+  CK(cudaMallocHost((void**)&ctx->h_in, sizeof(mars_step_in)));
+  CK(cudaMallocHost((void**)&ctx->h_work, sizeof(Work)));
+  CK(cudaMallocHost((void**)&ctx->h_sc, sizeof(mars_scalars)));
+  ctx->h_out_bytes = (size_t)R * 48 + (size_t)Qc * 4 + (size_t)b.j_cap * 9 + 4 * WIN_MAX * 4 + 4096;
+  CK(cudaMallocHost((void**)&ctx->h_out, ctx->h_out_bytes));
+  memset(ctx->h_in, 0, sizeof(mars_step_in));
+  // scalars: empty pool of one block until mars_set_scalars
+  mars_scalars s0;
+  memset(&s0, 0, sizeof s0);
+  s0.total_blocks = 1;
+  s0.free_blocks = 1;
+  s0.available_kv = 1;
+  s0.w_adm = hcfg->initial_window;
+  CK(cudaMemcpy(ctx->sc, &s0, sizeof s0, cudaMemcpyHostToDevice));
+  // column table
+  auto add = [&](size_t off, void** dev, int esz) { ctx->cols.push_back({off, dev, esz, nullptr}); };
+  add(offsetof(mars_cols, phase), (void**)&t.phase, 1);
+  add(offsetof(mars_cols, flags), (void**)&t.flags, 1);
+  add(offsetof(mars_cols, level), (void**)&t.level, 1);
+  add(offsetof(mars_cols, promos), (void**)&t.promos, 1);
+  add(offsetof(mars_cols, plevel), (void**)&t.plevel, 1);
+  add(offsetof(mars_cols, ready_since), (void**)&t.rs, 8);
+  add(offsetof(mars_cols, wait_since), (void**)&t.ws, 8);
+  add(offsetof(mars_cols, deadline), (void**)&t.dl, 8);
+  add(offsetof(mars_cols, arrival), (void**)&t.arr, 8);
+  add(offsetof(mars_cols, context), (void**)&t.ctx, 4);
+  add(offsetof(mars_cols, kv), (void**)&t.kv, 4);
+  add(offsetof(mars_cols, rem_decode), (void**)&t.rem, 4);
+  add(offsetof(mars_cols, pinned_blocks), (void**)&t.pb, 4);
+  add(offsetof(mars_cols, req_blocks), (void**)&t.req, 4);
+  add(offsetof(mars_cols, r0_prefill), (void**)&t.r0p, 4);
+  add(offsetof(mars_cols, r0_decode), (void**)&t.r0d, 4);
+  add(offsetof(mars_cols, preempt), (void**)&t.pre, 4);
+  add(offsetof(mars_cols, served), (void**)&t.served, 8);
+  add(offsetof(mars_cols, rank), (void**)&t.rank, 4);
+  CK(cudaDeviceSynchronize());
+  *out = ctx;
+  return MARS_OK;
+}
+
+int mars_destroy(mars_ctx* ctx) {
+  if (!ctx) return MARS_OK;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  Tab& t = ctx->tab;
+  void* ps[] = {t.phase, t.flags, t.level, t.promos, t.plevel, t.rs, t.ws, t.dl, t.arr, t.ctx,
+                t.kv, t.rem, t.pb, t.req, t.r0p, t.r0d, t.pre, t.served, t.rank, t.winpos};
+  for (void* p : ps) cudaFree(p);
+  for (int i = 0; i < 2; ++i) {
+    cudaFree(ctx->queue.row[i]);
+    cudaFree(ctx->queue.req[i]);
+    cudaFree(ctx->queue.lng[i]);
+    cudaFree(ctx->qlsd.k[i]);
+    cudaFree(ctx->qlsd.v[i]);
+    cudaFree(ctx->xlsd.k[i]);
+    cudaFree(ctx->xlsd.v[i]);
+  }
+  cudaFree(ctx->qlsd.cnt);
+  cudaFree(ctx->xlsd.cnt);
+  cudaFree(ctx->work);
+  cudaFree(ctx->sc);
+  cudaFree(ctx->qsel);
+  Bufs& b = ctx->bufs;
+  void* bs[] = {b.exp_row, b.exp_blk, b.exp_rank, b.exp_row_sorted, b.exp_blk_sorted, b.wc_hi,
+                b.wc_lo, b.wc_row, b.vc_key, b.vc_whi, b.vc_wlo, b.vc_row, b.vc_blk, b.ret_row,
+                b.ret_pin, b.ret_b, b.ret_c, b.ret_d, b.admitted, b.win_rows, b.dec_rows,
+                b.pre_rows, b.pre_grant, b.ev_row, b.ev_kind, b.ev_blk, b.j_op, b.j_row, b.j_n,
+                b.flush};
+  for (void* p : bs) cudaFree(p);
+  cudaFree(ctx->d_stage);
+  cudaFree(ctx->d_rows);
+  for (auto& cs : ctx->cols) cudaFree(cs.ckpt);
+  for (void* p : ctx->ck_q) cudaFree(p);
+  cudaFree(ctx->ck_sc);
+  cudaFree(ctx->ck_qsel);
+  cudaFreeHost(ctx->h_in);
+  cudaFreeHost(ctx->h_work);
+  cudaFreeHost(ctx->h_sc);
+  cudaFreeHost(ctx->h_out);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
+  delete ctx;
+  return MARS_OK;
+}
+
+int mars_set_stream(mars_ctx* ctx, void* stream) {
+  if (!ctx) return MARS_ERR_ARG;
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  ctx->stream = (cudaStream_t)stream;
+  ctx->own_stream = false;
+  return MARS_OK;
+}
+
+int mars_set_rows(mars_ctx* ctx, int64_t n) {
+  if (!ctx || n < 0 || n > ctx->max_rows) return fail(ctx, MARS_ERR_CAPACITY, "rows %lld", (long long)n);
+  ctx->n_rows = n;
+  return MARS_OK;
+}
+
+int mars_upsert_rows(mars_ctx* ctx, int64_t n, const int64_t* rows, const mars_cols* cols) {
+  if (!ctx || !cols || n < 0) return MARS_ERR_ARG;
+  if (n == 0) return MARS_OK;
+  CK(cudaSetDevice(ctx->device));
+  if (!rows) {
+    if (n > ctx->max_rows) return fail(ctx, MARS_ERR_CAPACITY, "upsert %lld rows", (long long)n);
+    for (auto& cs : ctx->cols) {
+      const void* hp = *(void* const*)((const char*)cols + cs.host_off);
+      if (!hp) continue;
+      CK(cudaMemcpyAsync(*cs.dev, hp, (size_t)n * cs.esz, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    if (n > ctx->n_rows) ctx->n_rows = n;
+  } else {
+    for (int64_t i = 0; i < n; ++i)
+      if (rows[i] < 0 || rows[i] >= ctx->max_rows)
+        return fail(ctx, MARS_ERR_CAPACITY, "row %lld out of range", (long long)rows[i]);
+    if (n > ctx->max_rows) return MARS_ERR_CAPACITY;
+    CK(cudaMemcpyAsync(ctx->d_rows, rows, (size_t)n * 8, cudaMemcpyHostToDevice, ctx->stream));
+    for (auto& cs : ctx->cols) {
+      const void* hp = *(void* const*)((const char*)cols + cs.host_off);
+      if (!hp) continue;
+      CK(cudaMemcpyAsync(ctx->d_stage, hp, (size_t)n * cs.esz, cudaMemcpyHostToDevice, ctx->stream));
+      int rc = mars_enqueue_scatter(ctx->stream, *cs.dev, ctx->d_stage, ctx->d_rows, n, cs.esz);
+      if (rc) return fail(ctx, MARS_ERR_CUDA, "scatter: %s", cudaGetErrorString((cudaError_t)rc));
+    }
+    for (int64_t i = 0; i < n; ++i)
+      if (rows[i] + 1 > ctx->n_rows) ctx->n_rows = rows[i] + 1;
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  return MARS_OK;
+}
+
+int mars_read_rows(mars_ctx* ctx, int64_t n, const int64_t* rows, mars_cols* out) {
+  if (!ctx || !out || n < 0) return MARS_ERR_ARG;
+  if (n == 0) return MARS_OK;
+  CK(cudaSetDevice(ctx->device));
+  if (!rows) {
+    if (n > ctx->max_rows) return MARS_ERR_CAPACITY;
+    for (auto& cs : ctx->cols) {
+      void* hp = *(void**)((char*)out + cs.host_off);
+      if (!hp) continue;
+      CK(cudaMemcpyAsync(hp, *cs.dev, (size_t)n * cs.esz, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+  } else {
+    if (n > ctx->max_rows) return MARS_ERR_CAPACITY;
+    CK(cudaMemcpyAsync(ctx->d_rows, rows, (size_t)n * 8, cudaMemcpyHostToDevice, ctx->stream));
+    for (auto& cs : ctx->cols) {
+      void* hp = *(void**)((char*)out + cs.host_off);
+      if (!hp) continue;
+      int rc = mars_enqueue_gather(ctx->stream, ctx->d_stage, *cs.dev, ctx->d_rows, n, cs.esz);
+      if (rc) return fail(ctx, MARS_ERR_CUDA, "gather: %s", cudaGetErrorString((cudaError_t)rc));
+      CK(cudaMemcpyAsync(hp, ctx->d_stage, (size_t)n * cs.esz, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  return MARS_OK;
+}
+
+int mars_set_queue(mars_ctx* ctx, int64_t n, const uint32_t* rows, const int32_t* req,
+                   const uint8_t* lng) {
+  if (!ctx || n < 0) return MARS_ERR_ARG;
+  if (n > ctx->max_queue) return fail(ctx, MARS_ERR_CAPACITY, "queue %lld > %lld", (long long)n,
+                                      (long long)ctx->max_queue);
+  CK(cudaSetDevice(ctx->device));
+  int mx = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    if (req[i] < 1) return fail(ctx, MARS_ERR_CONTRACT, "queue entry needs req_blocks >= 1");
+    if (req[i] > mx) mx = req[i];
+  }
+  CK(cudaMemsetAsync(ctx->qsel, 0, sizeof(i32), ctx->stream));
+  if (n) {
+    CK(cudaMemcpyAsync(ctx->queue.row[0], rows, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->queue.req[0], req, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->queue.lng[0], lng, n, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  // queue_len lives in the device scalars
+  CK(cudaMemcpyAsync(&ctx->sc->queue_len, &n, sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->q_upper = n;
+  ctx->q_maxreq = mx;
+  return MARS_OK;
+}
+
+int mars_get_queue(mars_ctx* ctx, int64_t cap, uint32_t* rows, int64_t* n) {
+  if (!ctx || !n) return MARS_ERR_ARG;
+  CK(cudaSetDevice(ctx->device));
+  int64_t len = 0;
+  i32 sel = 0;
+  CK(cudaMemcpyAsync(&len, &ctx->sc->queue_len, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(&sel, ctx->qsel, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  *n = len;
+  if (rows && len) {
+    int64_t m = len < cap ? len : cap;
+    CK(cudaMemcpy(rows, ctx->queue.row[sel], m * 4, cudaMemcpyDeviceToHost));
+  }
+  ctx->q_upper = len;
+  return MARS_OK;
+}
+
+int mars_set_scalars(mars_ctx* ctx, const mars_scalars* s) {
+  if (!ctx || !s) return MARS_ERR_ARG;
+  if (s->total_blocks < 1 || s->free_blocks < 0 || s->free_blocks > s->total_blocks)
+    return fail(ctx, MARS_ERR_CONTRACT, "bad pool counters");
+  CK(cudaSetDevice(ctx->device));
+  *ctx->h_sc = *s;
+  CK(cudaMemcpyAsync(ctx->sc, ctx->h_sc, sizeof(mars_scalars), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->q_upper = s->queue_len;
+  return MARS_OK;
+}
+
+int mars_get_scalars(mars_ctx* ctx, mars_scalars* s) {
+  if (!ctx || !s) return MARS_ERR_ARG;
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaMemcpyAsync(ctx->h_sc, ctx->sc, sizeof(mars_scalars), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  *s = *ctx->h_sc;
+  return MARS_OK;
+}
+
+static LaunchArgs launch_args(mars_ctx* ctx, const mars_step_in* in) {
+  LaunchArgs a;
+  a.stream = ctx->stream;
+  a.side = ctx->side;
+  a.ev_fork = ctx->ev_fork;
+  a.ev_join = ctx->ev_join;
+  a.tab = ctx->tab;
+  a.cfg = ctx->cfg;
+  a.work = ctx->work;
+  a.bufs = ctx->bufs;
+  a.sc = ctx->sc;
+  a.queue = ctx->queue;
+  a.qlsd = ctx->qlsd;
+  a.xlsd = ctx->xlsd;
+  a.qsel = ctx->qsel;
+  a.host_in = ctx->h_in;
+  a.n_rows = ctx->n_rows;
+  a.num_sms = ctx->num_sms;
+  a.control_possible = in->control_due ? 1 : 0;
+  a.queue_upper = ctx->q_upper;
+  int passes = 0;
+  if (ctx->q_upper > SORT_CAP) {
+    unsigned mx = (unsigned)(ctx->q_maxreq > 0 ? ctx->q_maxreq : 1);
+    passes = 1;
+    while (passes < 4 && (mx >> (8 * passes)) != 0) passes++;
+  }
+  a.queue_passes = passes;
+  a.exp_may_be_big = (in->skip_expiry == 0 && ctx->n_rows > SORT_CAP) ? 1 : 0;
+  return a;
+}
+
+int mars_step_enqueue(mars_ctx* ctx, const mars_step_in* in) {
+  if (!ctx || !in) return MARS_ERR_ARG;
+  CK(cudaSetDevice(ctx->device));
+  *ctx->h_in = *in;
+  LaunchArgs a = launch_args(ctx, in);
+  ctx->last_launches = mars_enqueue_step(&a);
+  CK(cudaGetLastError());
+  return MARS_OK;
+}
+
+// copy a device array into the pinned arena and return its host address
+static const void* pull(mars_ctx* ctx, size_t& off, const void* dev, size_t bytes) {
+  off = (off + 15) & ~(size_t)15;
+  if (off + bytes > ctx->h_out_bytes) return nullptr;
+  void* h = ctx->h_out + off;
+  if (bytes) cudaMemcpyAsync(h, dev, bytes, cudaMemcpyDeviceToHost, ctx->stream);
+  off += bytes;
+  return h;
+}
+
+int mars_step_fetch(mars_ctx* ctx, mars_step_out* o) {
+  if (!ctx || !o) return MARS_ERR_ARG;
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaMemcpyAsync(ctx->h_work, ctx->work, sizeof(Work), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  const Work& w = *ctx->h_work;
+  memset(o, 0, sizeof *o);
+  o->status = w.status;
+  o->n_expired = w.n_exp;
+  o->n_admitted = (int32_t)w.take;
+  o->n_window = w.n_window;
+  o->n_decode = w.n_dec;
+  o->n_prefill = w.n_pre;
+  o->n_evict = w.n_evict;
+  o->n_journal = w.n_journal;
+  o->n_retention = w.n_ret;
+  o->n_ready = w.n_ready;
+  o->n_promoted = w.n_promoted;
+  o->pack_mode = w.pack_mode;
+  o->total_tokens = w.total_tokens;
+  o->free_after_expiry = w.free_after_expiry;
+  o->limit = w.limit;
+  o->slots = w.slots;
+  const Bufs& b = ctx->bufs;
+  size_t off = 0;
+  o->expired_rows = (const uint32_t*)pull(ctx, off, b.exp_row_sorted, (size_t)w.n_exp * 4);
+  o->expired_blocks = (const int32_t*)pull(ctx, off, b.exp_blk_sorted, (size_t)w.n_exp * 4);
+  o->admitted_rows = (const uint32_t*)pull(ctx, off, b.admitted, (size_t)w.take * 4);
+  o->window_rows = (const uint32_t*)pull(ctx, off, b.win_rows, (size_t)w.n_window * 4);
+  o->decode_rows = (const uint32_t*)pull(ctx, off, b.dec_rows, (size_t)w.n_dec * 4);
+  o->prefill_rows = (const uint32_t*)pull(ctx, off, b.pre_rows, (size_t)w.n_pre * 4);
+  o->prefill_grants = (const int32_t*)pull(ctx, off, b.pre_grant, (size_t)w.n_pre * 4);
+  int ne = w.n_evict < b.ev_cap ? w.n_evict : (int)b.ev_cap;
+  o->evict_rows = (const uint32_t*)pull(ctx, off, b.ev_row, (size_t)ne * 4);
+  o->evict_kind = (const uint8_t*)pull(ctx, off, b.ev_kind, (size_t)ne);
+  o->evict_blocks = (const int32_t*)pull(ctx, off, b.ev_blk, (size_t)ne * 4);
+  int nj = w.n_journal < b.j_cap ? w.n_journal : (int)b.j_cap;
+  o->journal_op = (const uint8_t*)pull(ctx, off, b.j_op, (size_t)nj);
+  o->journal_row = (const uint32_t*)pull(ctx, off, b.j_row, (size_t)nj * 4);
+  o->journal_n = (const int32_t*)pull(ctx, off, b.j_n, (size_t)nj * 4);
+  o->ret_rows = (const uint32_t*)pull(ctx, off, b.ret_row, (size_t)w.n_ret * 4);
+  o->ret_pin = (const uint8_t*)pull(ctx, off, b.ret_pin, (size_t)w.n_ret);
+  o->ret_benefit = (const double*)pull(ctx, off, b.ret_b, (size_t)w.n_ret * 8);
+  o->ret_cost = (const double*)pull(ctx, off, b.ret_c, (size_t)w.n_ret * 8);
+  o->ret_deadline = (const double*)pull(ctx, off, b.ret_d, (size_t)w.n_ret * 8);
+  CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaGetLastError());
+  // free_blocks after the plan
+  int64_t fb = 0;
+  CK(cudaMemcpy(&fb, &ctx->sc->free_blocks, 8, cudaMemcpyDeviceToHost));
+  o->free_blocks = fb;
+  ctx->q_upper -= w.take;
+  if (ctx->q_upper < 0) ctx->q_upper = 0;
+  return MARS_OK;
+}
+
+int mars_step(mars_ctx* ctx, const mars_step_in* in, mars_step_out* out) {
+  int rc = mars_step_enqueue(ctx, in);
+  if (rc) return rc;
+  return mars_step_fetch(ctx, out);
+}
+
+int mars_retention_batch(mars_ctx* ctx, int64_t n, const int32_t* context, const int32_t* kv,
+                         int64_t total_blocks, double usage, double ema, double now,
+                         uint8_t* pin, double* benefit, double* cost, double* deadline) {
+  if (!ctx || n < 0) return MARS_ERR_ARG;
+  if (n == 0) return MARS_OK;
+  if (n > ctx->max_rows) return MARS_ERR_CAPACITY;
+  if (total_blocks < 1) return fail(ctx, MARS_ERR_CONTRACT, "total_blocks must be >= 1");
+  CK(cudaSetDevice(ctx->device));
+  // staging: ctx[n] | kv[n] in d_stage (8 B per row), outputs in the retention buffers
+  i32* dctx = (i32*)ctx->d_stage;
+  i32* dkv = dctx + n;
+  CK(cudaMemcpyAsync(dctx, context, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(dkv, kv, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+  const Bufs& b = ctx->bufs;
+  int rc = mars_enqueue_retention(ctx->cfg, ctx->stream, n, dctx, dkv, total_blocks, usage, ema,
+                                  now, b.ret_pin, b.ret_b, b.ret_c, b.ret_d);
+  if (rc) return fail(ctx, MARS_ERR_CUDA, "retention: %s", cudaGetErrorString((cudaError_t)rc));
+  CK(cudaMemcpyAsync(pin, b.ret_pin, n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(benefit, b.ret_b, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(cost, b.ret_c, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(deadline, b.ret_d, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return MARS_OK;
+}
+
+int mars_checkpoint(mars_ctx* ctx) {
+  if (!ctx) return MARS_ERR_ARG;
+  CK(cudaSetDevice(ctx->device));
+  const i64 R = ctx->max_rows, Qc = ctx->max_queue;
+  for (auto& cs : ctx->cols) {
+    if (!cs.ckpt) CK(cudaMalloc(&cs.ckpt, (size_t)R * cs.esz));
+    CK(cudaMemcpyAsync(cs.ckpt, *cs.dev, (size_t)ctx->n_rows * cs.esz, cudaMemcpyDeviceToDevice,
+                       ctx->stream));
+  }
+  size_t qs[6] = {(size_t)Qc * 4, (size_t)Qc * 4, (size_t)Qc, (size_t)Qc * 4, (size_t)Qc * 4,
+                  (size_t)Qc};
+  void* qp[6] = {ctx->queue.row[0], ctx->queue.req[0], ctx->queue.lng[0], ctx->queue.row[1],
+                 ctx->queue.req[1], ctx->queue.lng[1]};
+  for (int i = 0; i < 6; ++i) {
+    if (!ctx->ck_q[i]) CK(cudaMalloc(&ctx->ck_q[i], qs[i]));
+    CK(cudaMemcpyAsync(ctx->ck_q[i], qp[i], qs[i], cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  if (!ctx->ck_sc) CK(cudaMalloc((void**)&ctx->ck_sc, sizeof(mars_scalars)));
+  if (!ctx->ck_qsel) CK(cudaMalloc((void**)&ctx->ck_qsel, sizeof(i32)));
+  CK(cudaMemcpyAsync(ctx->ck_sc, ctx->sc, sizeof(mars_scalars), cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->ck_qsel, ctx->qsel, sizeof(i32), cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->ck_q_upper = ctx->q_upper;
+  ctx->ck_q_maxreq = ctx->q_maxreq;
+  ctx->have_ckpt = true;
+  return MARS_OK;
+}
+
+int mars_restore(mars_ctx* ctx) {
+  if (!ctx) return MARS_ERR_ARG;
+  if (!ctx->have_ckpt) return fail(ctx, MARS_ERR_ARG, "no checkpoint");
+  CK(cudaSetDevice(ctx->device));
+  const i64 Qc = ctx->max_queue;
+  for (auto& cs : ctx->cols)
+    CK(cudaMemcpyAsync(*cs.dev, cs.ckpt, (size_t)ctx->n_rows * cs.esz, cudaMemcpyDeviceToDevice,
+                       ctx->stream));
+  size_t qs[6] = {(size_t)Qc * 4, (size_t)Qc * 4, (size_t)Qc, (size_t)Qc * 4, (size_t)Qc * 4,
+                  (size_t)Qc};
+  void* qp[6] = {ctx->queue.row[0], ctx->queue.req[0], ctx->queue.lng[0], ctx->queue.row[1],
+                 ctx->queue.req[1], ctx->queue.lng[1]};
+  for (int i = 0; i < 6; ++i)
+    CK(cudaMemcpyAsync(qp[i], ctx->ck_q[i], qs[i], cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->sc, ctx->ck_sc, sizeof(mars_scalars), cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->qsel, ctx->ck_qsel, sizeof(i32), cudaMemcpyDeviceToDevice, ctx->stream));
+  ctx->q_upper = ctx->ck_q_upper;
+  ctx->q_maxreq = ctx->ck_q_maxreq;
+  return MARS_OK;
+}
+
+int mars_flush_l2(mars_ctx* ctx, int64_t bytes) {
+  if (!ctx || bytes < 0) return MARS_ERR_ARG;
+  CK(cudaSetDevice(ctx->device));
+  if (bytes > ctx->bufs.flush_bytes) {
+    cudaFree(ctx->bufs.flush);
+    ctx->bufs.flush = nullptr;
+    CK(cudaMalloc((void**)&ctx->bufs.flush, (size_t)bytes));
+    ctx->bufs.flush_bytes = bytes;
+  }
+  int rc = mars_enqueue_flush(ctx->stream, ctx->bufs.flush, bytes, ctx->flush_salt++);
+  if (rc) return fail(ctx, MARS_ERR_CUDA, "flush: %s", cudaGetErrorString((cudaError_t)rc));
+  return MARS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,217 @@
+// Internal device-side layout of the B200 MARS step.  See DESIGN.md for the
+// data layout and the kernel pipeline; include/mars_b200.h for the C ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/mars_b200.h"
+
+typedef uint8_t u8;
+typedef uint16_t u16;
+typedef uint32_t u32;
+typedef uint64_t u64;
+typedef int32_t i32;
+typedef int64_t i64;
+
+#define HIST_BINS 4096
+#define WIN_MAX 128
+#define SORT_CAP 4096         // bitonic sort capacity of the single-CTA selector
+#define VSEL 1024             // victim-stream target length (prefix of reclaim order)
+#define VSTREAM_CAP 2048      // victim stream entries kept in shared memory
+#define LSD_G 148             // CTAs of the multi-CTA LSD radix sort
+#define MAXH 0x0FFFFFFFull    // 28-bit complement base for -blocks in victim keys
+
+// pack modes (control.py:101-122)
+#define PACK_ASC 0
+#define PACK_DESC 1
+#define PACK_FF 2
+
+// step status bits
+#define ST_OK 0
+#define ST_QUEUE_MISMATCH 1
+#define ST_WALK_OVERFLOW 2
+#define ST_BAD_INPUT 4
+
+// device copy of the configuration (mars_config + derived)
+struct Cfg {
+  i32 bs, budget, window, max_dec, num_levels, max_promos, hyst, w_min;
+  i32 coord, cosched;
+  i64 bounds[4], quotas[4];
+  double tick_s, prefill_rate, promo_wait, slack, horizon, pw_clip;
+  double cpu_hi, cpu_lo, kv_hi, kv_lo, ema_alpha, tool_prior;
+  double ai, md, ctl_interval, init_window, oversub, reserve, long_frac;
+};
+
+// device column pointers (the session-state store, SoA in HBM)
+struct Tab {
+  u8 *phase, *flags, *level, *promos, *plevel;
+  double *rs, *ws, *dl, *arr;
+  i32 *ctx, *kv, *rem, *pb, *req, *r0p, *r0d, *pre;
+  i64 *served;
+  u32 *rank;
+  int16_t *winpos;  // row -> window index during the walk, -1 otherwise
+  i64 cap;
+};
+
+// queue (admission list), double-buffered: q[sel] is current
+struct Queue {
+  u32 *row[2];
+  i32 *req[2];
+  u8 *lng[2];
+  i64 cap;
+};
+
+// generic multi-CTA LSD radix sort scratch (u64 keys, u32 vals)
+struct Lsd {
+  u64 *k[2];
+  u32 *v[2];
+  u32 *cnt;      // [256][LSD_G] counts, then offsets
+  i64 cap;
+};
+
+// fixed-size per-step work area (device memory, zeroed at step start)
+struct Work {
+  mars_step_in in;
+  // K_A accumulators
+  u32 ticket;
+  u32 ticket_ap;
+  unsigned long long exp_blocks;
+  i32 n_exp, n_active, n_queued, n_long_q, n_ready, n_promoted, n_victims, n_boundary;
+  i32 max_req, min_req;
+  u32 tmin_win, tmin_vic;
+  u32 hist_win[HIST_BINS];
+  u32 hist_vic[HIST_BINS];
+  // thresholds
+  i32 t_win, t_vic;
+  i32 n_win_cand_expected, n_vic_cand_expected;
+  // candidate counts (K_C / K_AP appends)
+  i32 n_wc, n_vc, n_ret;
+  // control plane
+  i32 pack_mode, need_seed, big_queue;
+  i64 qlen;
+  double ff_median;
+  i32 lsd_cur, lsd_skip[8], lsd_in[8];
+  u64 lsd_maxkey;
+  i32 lsd_big, lsd_n;
+  i32 xlsd_cur, xlsd_skip[8], xlsd_in[8];
+  u64 xlsd_maxkey;
+  i32 xlsd_big, xlsd_n;
+  i64 limit, slots, take;
+  long long projected;
+  // plan
+  i32 n_window, n_dec, n_pre, n_evict, n_journal;
+  i64 total_tokens;
+  i64 free_after_expiry;
+  i32 status;
+  i32 walk_slow;
+};
+
+// variable-length step buffers
+struct Bufs {
+  // expired pins (K_A append, K_X sorts by rank)
+  u32 *exp_row; i32 *exp_blk; u32 *exp_rank;
+  u32 *exp_row_sorted; i32 *exp_blk_sorted;
+  // window candidates
+  u64 *wc_hi, *wc_lo; u32 *wc_row;
+  // victim candidates
+  u64 *vc_key, *vc_whi, *vc_wlo; u32 *vc_row; i32 *vc_blk;
+  // retention results
+  u32 *ret_row; u8 *ret_pin; double *ret_b, *ret_c, *ret_d;
+  // admission
+  u32 *admitted;
+  // plan outputs
+  u32 *win_rows, *dec_rows, *pre_rows; i32 *pre_grant;
+  u32 *ev_row; u8 *ev_kind; i32 *ev_blk;
+  u8 *j_op; u32 *j_row; i32 *j_n;
+  i64 ev_cap, j_cap;
+  // flush scratch
+  u8 *flush; i64 flush_bytes;
+};
+
+// ---------------------------------------------------------------------------
+// key helpers
+// ---------------------------------------------------------------------------
+
+// total order on finite doubles as an unsigned integer; -0.0 folds onto +0.0
+// (Python compares them equal, the session-id tie-break then decides)
+__device__ __forceinline__ u64 ord_f64(double x) {
+  x = x + 0.0;
+  u64 b = (u64)__double_as_longlong(x);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// window order key (baselines.py:374-377): (level, ready_since, session_id) or,
+// coordinator off, (arrival_time, session_id).  98 significant bits.
+__device__ __forceinline__ void window_key(u32 level, double t, u32 rank, u64& hi, u64& lo) {
+  u64 o = ord_f64(t);
+  hi = ((u64)level << 62) | (o >> 2);
+  lo = ((o & 3ull) << 62) | (u64)rank;
+}
+
+// monotone 12-bit digit of the window key
+__device__ __forceinline__ u32 window_digit(u32 level, double t, double scale) {
+  double y = t * scale;
+  u32 b = (y >= 1023.0) ? 1023u : (y > 0.0 ? (u32)y : 0u);
+  return (level << 10) | b;
+}
+
+// monotone non-decreasing 8-bit bucket of a block count
+__device__ __forceinline__ u32 blocks_bucket(i64 h) {
+  if (h <= 0) return 0;
+  if (h >= (1ll << 31)) return 255;
+  u32 x = (u32)h;
+  int e = 31 - __clz(x);
+  if (e < 3) return x;
+  return 8u * (u32)(e - 2) + ((x >> (e - 3)) & 7u);
+}
+
+// reclaim order (scheduler.py:249-259): pinned before running, expired pins
+// first, then lowest level (largest level value) first, then largest
+// footprint, then session id.
+__device__ __forceinline__ u64 victim_key(bool running, bool nonexp, u32 level, i64 blocks,
+                                          u32 rank) {
+  u64 b = (blocks > (i64)MAXH) ? MAXH : (u64)blocks;
+  return ((u64)running << 63) | ((u64)(nonexp ? 1 : 0) << 62) | ((u64)(3u - level) << 60) |
+         ((MAXH - b) << 32) | (u64)rank;
+}
+
+__device__ __forceinline__ u32 victim_digit(bool running, bool nonexp, u32 level, i64 blocks) {
+  return ((running ? 1u : 0u) << 11) | ((nonexp ? 1u : 0u) << 10) | ((3u - level) << 8) |
+         (255u - blocks_bucket(blocks));
+}
+
+__device__ __forceinline__ i64 ceil_div64(i64 a, i64 b) { return (a + b - 1) / b; }
+
+__device__ __forceinline__ bool key_lt(u64 ah, u64 al, u64 bh, u64 bl) {
+  return ah < bh || (ah == bh && al < bl);
+}
+
+// initial_level (scheduler.py:87-97)
+__device__ __forceinline__ u32 initial_level(const Cfg& c, i64 tokens) {
+  for (int i = 0; i < c.num_levels; ++i)
+    if (tokens <= c.bounds[i]) return (u32)i;
+  return (u32)(c.num_levels - 1);
+}
+
+// pressure_weight + decide_retention (scheduler.py:183-213).  Operation order
+// is the reference's, and this file is compiled with --fmad=false, so the
+// results are bit-identical to CPython's IEEE doubles.
+__device__ __forceinline__ void decide_retention(const Cfg& c, i64 context, i64 kv,
+                                                 i64 total_blocks, double usage, double ema,
+                                                 double now, u8& pin, double& benefit,
+                                                 double& cost, double& deadline) {
+  benefit = (double)context / c.prefill_rate;
+  i64 foot = ceil_div64(kv, c.bs);
+  double pw;
+  if (usage >= 1.0) {
+    pw = c.pw_clip;
+  } else {
+    double inv = 1.0 / (1.0 - usage);
+    pw = (c.pw_clip < inv) ? c.pw_clip : inv;
+  }
+  cost = ((double)foot / (double)total_blocks) * ema * pw;
+  pin = (benefit > cost && ema <= c.horizon) ? 1 : 0;
+  double d = ema * c.slack;
+  deadline = now + ((c.horizon < d) ? c.horizon : d);
+}

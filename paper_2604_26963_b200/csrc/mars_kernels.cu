@@ -1,0 +1,1812 @@
+// B200 (sm_100a) kernels of the MARS scheduling step.
+//
+// Pipeline, one CUDA stream + one side stream:
+//   k_scan        multi-CTA pass over the session table: pin expiry, MLFQ aging
+//                 (promote_waiting), counters, per-CTA key histograms; the
+//                 last CTA finalises pool/telemetry scalars, refresh_pressure,
+//                 and the exact global top-k thresholds.
+//   k_compact     [side] second pass: window / victim candidates at the exact
+//                 thresholds, S2 retention for BOUNDARY rows.
+//   k_exp_*       [side] expired pins in session-id (rank) order.
+//   k_pack_small  control plane: pack_queue for small queues (bitonic) and the
+//                 first-fit mode; k_lsd_* multi-CTA stable LSD sort for big ones.
+//   k_admit_apply update_window + triple clamp, admit() of the packed prefix,
+//                 residual queue, admitted rows join the window candidates.
+//   k_walk        single CTA: window top-k, build_plan decode/prefill passes
+//                 with try_fit and reclamation (victim stream or exact
+//                 full-table fallback), plan + ordered journal.
+//
+// Compiled with --fmad=false: every f64 expression keeps CPython's IEEE
+// rounding so retention / admission scalars are bit-identical.
+
+#include <cuda_runtime.h>
+#include <stdio.h>
+
+#include "mars_internal.cuh"
+#include "mars_launch.h"
+
+#define FULL 0xffffffffu
+
+// ---------------------------------------------------------------------------
+// block utilities
+// ---------------------------------------------------------------------------
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    T x = __shfl_xor_sync(FULL, v, o);
+    v = x > v ? x : v;
+  }
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_min(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    T x = __shfl_xor_sync(FULL, v, o);
+    v = x < v ? x : v;
+  }
+  return v;
+}
+
+// block-wide sum; `sh` needs 32 slots; all threads get the result
+template <typename T>
+__device__ T block_sum(T v, T* sh) {
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  T r = (threadIdx.x < nw) ? sh[threadIdx.x] : (T)0;
+  if (wid == 0) r = warp_sum(r);
+  if (threadIdx.x == 0) sh[0] = r;
+  __syncthreads();
+  r = sh[0];
+  __syncthreads();
+  return r;
+}
+
+template <typename T>
+__device__ T block_max(T v, T* sh, T lowest) {
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  v = warp_max(v);
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  T r = (threadIdx.x < nw) ? sh[threadIdx.x] : lowest;
+  if (wid == 0) r = warp_max(r);
+  if (threadIdx.x == 0) sh[0] = r;
+  __syncthreads();
+  r = sh[0];
+  __syncthreads();
+  return r;
+}
+
+template <typename T>
+__device__ T block_min(T v, T* sh, T highest) {
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  v = warp_min(v);
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  T r = (threadIdx.x < nw) ? sh[threadIdx.x] : highest;
+  if (wid == 0) r = warp_min(r);
+  if (threadIdx.x == 0) sh[0] = r;
+  __syncthreads();
+  r = sh[0];
+  __syncthreads();
+  return r;
+}
+
+// Smallest bin d with cumsum(h[0..d]) >= k over `nb` bins (nb multiple of
+// blockDim.x); returns nb-1 if the total is below k.  *below = cumsum(h[0..d-1]),
+// *upto = cumsum(h[0..d]).  `sh` needs blockDim.x + 32 u32 slots.
+__device__ void block_threshold(const u32* h, int nb, u32 k, u32* sh, int* out_d, u32* below,
+                                u32* upto) {
+  int per = nb / blockDim.x;
+  int base = threadIdx.x * per;
+  u32 s = 0;
+  for (int i = 0; i < per; ++i) s += h[base + i];
+  // inclusive scan of per-thread sums
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int off = 1; off < (int)blockDim.x; off <<= 1) {
+    u32 x = (threadIdx.x >= (unsigned)off) ? sh[threadIdx.x - off] : 0u;
+    __syncthreads();
+    sh[threadIdx.x] += x;
+    __syncthreads();
+  }
+  u32 incl = sh[threadIdx.x];
+  u32 excl = incl - s;
+  u32 total = sh[blockDim.x - 1];
+  __shared__ int s_d;
+  __shared__ u32 s_below, s_upto;
+  if (threadIdx.x == 0) {
+    s_d = nb - 1;
+    s_below = total - h[nb - 1];
+    s_upto = total;
+  }
+  __syncthreads();
+  if (total >= k && excl < k && incl >= k) {
+    u32 c = excl;
+    for (int i = 0; i < per; ++i) {
+      u32 nc = c + h[base + i];
+      if (nc >= k) {
+        s_d = base + i;
+        s_below = c;
+        s_upto = nc;
+        break;
+      }
+      c = nc;
+    }
+  }
+  __syncthreads();
+  *out_d = s_d;
+  *below = s_below;
+  *upto = s_upto;
+  __syncthreads();
+}
+
+// warp-aggregated append: returns the slot for lanes with pred, -1 otherwise
+__device__ __forceinline__ int warp_append(int* counter, bool pred) {
+  u32 m = __ballot_sync(__activemask(), pred);
+  if (!m) return -1;
+  int lane = threadIdx.x & 31;
+  int leader = __ffs(m) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(counter, __popc(m));
+  base = __shfl_sync(__activemask(), base, leader);
+  if (!pred) return -1;
+  return base + __popc(m & ((1u << lane) - 1u));
+}
+
+// ---------------------------------------------------------------------------
+// K_A: scan (expiry, aging, counters, histograms); last CTA finalises
+// ---------------------------------------------------------------------------
+
+#define SCAN_TPB 512
+
+__global__ void __launch_bounds__(SCAN_TPB) k_scan(Tab t, Cfg c, Work* w, Bufs b,
+                                                   mars_scalars* sc, i64 n_rows) {
+  __shared__ u32 hw[HIST_BINS];
+  __shared__ u32 hv[HIST_BINS];
+  __shared__ u32 shu[SCAN_TPB + 32];
+  __shared__ long long shl[32];
+  __shared__ int shi[32];
+  __shared__ bool s_last;
+
+  for (int i = threadIdx.x; i < HIST_BINS; i += blockDim.x) hw[i] = hv[i] = 0;
+  __syncthreads();
+
+  const double now = w->in.now;
+  const bool do_exp = !w->in.skip_expiry;
+  const double scale = (now > 0.0 && now < 1e300) ? 1024.0 / now : 0.0;
+  const i64 chunk = (n_rows + gridDim.x - 1) / gridDim.x;
+  const i64 start = (i64)blockIdx.x * chunk;
+  i64 end = start + chunk;
+  if (end > n_rows) end = n_rows;
+
+  long long exp_blocks = 0;
+  int n_active = 0, n_queued = 0, n_long = 0, n_ready = 0, n_prom = 0, n_vic = 0, n_bnd = 0;
+  int max_req = 0, min_req = 0x7fffffff;
+
+  for (i64 r0 = start; r0 < end; r0 += blockDim.x) {
+    i64 r = r0 + threadIdx.x;
+    bool valid = r < end;
+    u8 f = valid ? t.flags[r] : 0;
+    u8 ph = valid ? t.phase[r] : MARS_EMPTY;
+    bool expire = false;
+    i32 pbk = 0;
+    if (f & MARS_F_ACTIVE) n_active++;
+    if (f & MARS_F_QUEUED) {
+      n_queued++;
+      if (f & MARS_F_LONG) n_long++;
+      i32 q = t.req[r];
+      max_req = q > max_req ? q : max_req;
+      min_req = q < min_req ? q : min_req;
+    }
+    if (f & MARS_F_BOUNDARY) n_bnd++;
+    if (f & MARS_F_PINNED) {
+      double d = t.dl[r];
+      bool exp_ = d < now;
+      pbk = t.pb[r];
+      if (do_exp && exp_) {
+        expire = true;
+        t.flags[r] = f & ~MARS_F_PINNED;
+        t.kv[r] = 0;
+        exp_blocks += pbk;
+      } else {
+        u32 plv = t.plevel[r];
+        atomicAdd(&hv[victim_digit(false, !exp_, plv, pbk)], 1u);
+        n_vic++;
+      }
+    }
+    int slot = warp_append(&w->n_exp, expire);
+    if (slot >= 0) {
+      b.exp_row[slot] = (u32)r;
+      b.exp_blk[slot] = pbk;
+      b.exp_rank[slot] = t.rank[r];
+    }
+    if ((f & MARS_F_ACTIVE) && (ph == MARS_PREFILL || ph == MARS_DECODE)) {
+      n_ready++;
+      u32 lv = t.level[r];
+      if (c.coord) {
+        if (lv != 0 && t.promos[r] < (u32)c.max_promos) {
+          double ws = t.ws[r];
+          if (now - ws >= c.promo_wait) {  // scheduler.py:123
+            lv -= 1;
+            t.level[r] = (u8)lv;
+            t.promos[r] = t.promos[r] + 1;
+            t.ws[r] = now;
+            n_prom++;
+          }
+        }
+        atomicAdd(&hw[window_digit(lv, t.rs[r], scale)], 1u);
+      } else {
+        atomicAdd(&hw[window_digit(0, t.arr[r], scale)], 1u);
+      }
+      i32 kvv = t.kv[r];
+      if (kvv > 0) {
+        atomicAdd(&hv[victim_digit(true, false, c.coord ? lv : 0u, ceil_div64(kvv, c.bs))], 1u);
+        n_vic++;
+      }
+    }
+  }
+  __syncthreads();
+
+  // local thresholds: only bins at or below them can hold a global top-k key
+  int tw, tv;
+  u32 bl, up;
+  block_threshold(hw, HIST_BINS, (u32)c.window, shu, &tw, &bl, &up);
+  block_threshold(hv, HIST_BINS, (u32)VSEL, shu, &tv, &bl, &up);
+  for (int i = threadIdx.x; i <= tw; i += blockDim.x)
+    if (hw[i]) atomicAdd(&w->hist_win[i], hw[i]);
+  for (int i = threadIdx.x; i <= tv; i += blockDim.x)
+    if (hv[i]) atomicAdd(&w->hist_vic[i], hv[i]);
+  if (threadIdx.x == 0) {
+    atomicMin(&w->tmin_win, (u32)tw);
+    atomicMin(&w->tmin_vic, (u32)tv);
+  }
+
+  long long eb = block_sum<long long>(exp_blocks, shl);
+  int a0 = block_sum<int>(n_active, shi);
+  int a1 = block_sum<int>(n_queued, shi);
+  int a2 = block_sum<int>(n_long, shi);
+  int a3 = block_sum<int>(n_ready, shi);
+  int a4 = block_sum<int>(n_prom, shi);
+  int a5 = block_sum<int>(n_vic, shi);
+  int a6 = block_sum<int>(n_bnd, shi);
+  int mx = block_max<int>(max_req, shi, 0);
+  int mn = block_min<int>(min_req, shi, 0x7fffffff);
+  if (threadIdx.x == 0) {
+    atomicAdd(&w->exp_blocks, (unsigned long long)eb);
+    atomicAdd(&w->n_active, a0);
+    atomicAdd(&w->n_queued, a1);
+    atomicAdd(&w->n_long_q, a2);
+    atomicAdd(&w->n_ready, a3);
+    atomicAdd(&w->n_promoted, a4);
+    atomicAdd(&w->n_victims, a5);
+    atomicAdd(&w->n_boundary, a6);
+    atomicMax(&w->max_req, mx);
+    atomicMin(&w->min_req, mn);
+    __threadfence();
+    u32 tk = atomicAdd(&w->ticket, 1u);
+    s_last = (tk == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+
+  // ---- last CTA: finalise ------------------------------------------------
+  volatile Work* vw = w;
+  // global thresholds over the exact prefix of the merged histograms
+  for (int i = threadIdx.x; i < HIST_BINS; i += blockDim.x) {
+    hw[i] = (i <= (int)vw->tmin_win) ? vw->hist_win[i] : 0u;
+    hv[i] = (i <= (int)vw->tmin_vic) ? vw->hist_vic[i] : 0u;
+  }
+  __syncthreads();
+  int gw, gv;
+  u32 wb, wu, vb, vu;
+  block_threshold(hw, HIST_BINS, (u32)c.window, shu, &gw, &wb, &wu);
+  block_threshold(hv, HIST_BINS, (u32)VSEL, shu, &gv, &vb, &vu);
+  if (threadIdx.x == 0) {
+    if (gw > (int)vw->tmin_win) gw = (int)vw->tmin_win;
+    if (gv > (int)vw->tmin_vic) gv = (int)vw->tmin_vic;
+    w->t_win = gw;
+    w->t_vic = gv;
+    w->n_win_cand_expected = (i32)wu;
+    w->n_vic_cand_expected = (i32)vu;
+    // Telemetry.probe (telemetry.py:152-158) after the expiry evictions
+    i64 total = sc->total_blocks;
+    i64 freeb = sc->free_blocks + (i64)vw->exp_blocks;
+    sc->free_blocks = freeb;
+    w->free_after_expiry = freeb;
+    sc->available_kv = freeb;
+    sc->kv_usage_ratio = (double)(total - freeb) / (double)total;
+    sc->active_sessions = vw->n_active;
+    sc->active_tools = w->in.active_tools;
+    sc->queued_tools = w->in.queued_tools;
+    i64 qlen = sc->queue_len;
+    w->qlen = qlen;
+    if ((i64)vw->n_queued != qlen) w->status |= ST_QUEUE_MISMATCH;
+    if (w->in.control_due) {
+      // refresh_pressure (telemetry.py:174-208)
+      double slots = (double)w->in.worker_slots;
+      int at = sc->active_tools, qt = sc->queued_tools;
+      bool hi = ((double)at >= c.cpu_hi * slots) || qt > 0;
+      bool lo = ((double)at < c.cpu_lo * slots) && qt == 0;
+      int hs = hi ? sc->cpu_high_streak + 1 : 0;
+      int ls = lo ? sc->cpu_low_streak + 1 : 0;
+      int on = sc->cpu_overloaded;
+      if (!on && hs >= c.hyst) {
+        on = 1;
+        ls = 0;
+      } else if (on && ls >= c.hyst) {
+        on = 0;
+        hs = 0;
+      }
+      sc->cpu_overloaded = on;
+      sc->cpu_high_streak = hs;
+      sc->cpu_low_streak = ls;
+      double u = sc->kv_usage_ratio;
+      hi = u >= c.kv_hi;
+      lo = u < c.kv_lo;
+      hs = hi ? sc->kv_high_streak + 1 : 0;
+      ls = lo ? sc->kv_low_streak + 1 : 0;
+      on = sc->kv_overloaded;
+      if (!on && hs >= c.hyst) {
+        on = 1;
+        ls = 0;
+      } else if (on && ls >= c.hyst) {
+        on = 0;
+        hs = 0;
+      }
+      sc->kv_overloaded = on;
+      sc->kv_high_streak = hs;
+      sc->kv_low_streak = ls;
+      // pack_queue mode (control.py:109-122)
+      int mode = sc->cpu_overloaded ? PACK_DESC
+                                    : ((qlen > 0 && (i64)vw->n_long_q == qlen) ? PACK_FF : PACK_ASC);
+      w->pack_mode = mode;
+      w->need_seed = (!sc->has_ema_blocks && !sc->has_blocks_seed && qlen > 0) ? 1 : 0;
+      int big = (qlen > SORT_CAP && mode != PACK_FF) ? 1 : 0;
+      w->big_queue = big;
+      w->lsd_big = big;
+      w->lsd_n = (i32)qlen;
+      w->lsd_maxkey = (mode == PACK_ASC) ? (u64)vw->max_req : (u64)(vw->max_req - vw->min_req);
+    }
+    int ne = vw->n_exp;
+    w->xlsd_big = ne > SORT_CAP ? 1 : 0;
+    w->xlsd_n = ne;
+    w->xlsd_maxkey = 0xffffffffull;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K_C: candidates at the exact thresholds + S2 retention (boundary rows)
+// ---------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(SCAN_TPB) k_compact(Tab t, Cfg c, Work* w, Bufs b,
+                                                      mars_scalars* sc, i64 n_rows) {
+  const double now = w->in.now;
+  const double scale = (now > 0.0 && now < 1e300) ? 1024.0 / now : 0.0;
+  const u32 tw = (u32)w->t_win, tv = (u32)w->t_vic;
+  const i64 total = sc->total_blocks;
+  const double usage = sc->kv_usage_ratio;
+  const double ema = sc->has_ema_tool ? sc->ema_tool : c.tool_prior;
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  const i64 lim = ((n_rows + 31) / 32) * 32;
+  for (i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x; r < lim + 0; r += stride) {
+    bool valid = r < n_rows;
+    u8 f = valid ? t.flags[r] : 0;
+    u8 ph = valid ? t.phase[r] : MARS_EMPTY;
+    bool ready = (f & MARS_F_ACTIVE) && (ph == MARS_PREFILL || ph == MARS_DECODE);
+    bool wcand = false, vcand = false, bnd = (f & MARS_F_BOUNDARY) != 0;
+    u64 whi = 0, wlo = 0, vk = 0;
+    i32 blk = 0;
+    if (ready) {
+      u32 lv = c.coord ? (u32)t.level[r] : 0u;
+      double tt = c.coord ? t.rs[r] : t.arr[r];
+      u32 rk = t.rank[r];
+      window_key(lv, tt, rk, whi, wlo);
+      wcand = window_digit(lv, tt, scale) <= tw;
+      i32 kvv = t.kv[r];
+      if (kvv > 0) {
+        i64 h = ceil_div64(kvv, c.bs);
+        if (victim_digit(true, false, lv, h) <= tv) {
+          vcand = true;
+          vk = victim_key(true, false, lv, h, rk);
+          blk = (i32)h;
+        }
+      }
+    } else if (f & MARS_F_PINNED) {
+      bool nonexp = !(t.dl[r] < now);
+      u32 plv = (u32)t.plevel[r];
+      i32 pbk = t.pb[r];
+      if (victim_digit(false, nonexp, plv, pbk) <= tv) {
+        vcand = true;
+        vk = victim_key(false, nonexp, plv, pbk, t.rank[r]);
+        blk = pbk;
+      }
+    }
+    int s = warp_append(&w->n_wc, wcand);
+    if (s >= 0) {
+      b.wc_hi[s] = whi;
+      b.wc_lo[s] = wlo;
+      b.wc_row[s] = (u32)r;
+    }
+    s = warp_append(&w->n_vc, vcand);
+    if (s >= 0) {
+      b.vc_key[s] = vk;
+      b.vc_whi[s] = whi;
+      b.vc_wlo[s] = wlo;
+      b.vc_row[s] = (u32)r;
+      b.vc_blk[s] = blk;
+    }
+    s = warp_append(&w->n_ret, bnd);
+    if (s >= 0) {
+      u8 pin;
+      double bb, cc, dd;
+      decide_retention(c, t.ctx[r], t.kv[r], total, usage, ema, now, pin, bb, cc, dd);
+      b.ret_row[s] = (u32)r;
+      b.ret_pin[s] = pin;
+      b.ret_b[s] = bb;
+      b.ret_c[s] = cc;
+      b.ret_d[s] = dd;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// single-CTA bitonic sort in shared memory: keys (hi, lo) + u32 payload
+// ---------------------------------------------------------------------------
+
+__device__ void bitonic_sort(u64* kh, u64* kl, u32* pv, int n2) {
+  for (int k = 2; k <= n2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+        int p = i ^ j;
+        if (p > i) {
+          bool up = (i & k) == 0;
+          u64 ah = kh[i], al = kl[i], bh = kh[p], bl = kl[p];
+          bool gt = key_lt(bh, bl, ah, al);
+          if (gt == up) {
+            kh[i] = bh;
+            kl[i] = bl;
+            kh[p] = ah;
+            kl[p] = al;
+            u32 tv = pv[i];
+            pv[i] = pv[p];
+            pv[p] = tv;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__device__ __forceinline__ int next_pow2(int n) {
+  int p = 1;
+  while (p < n) p <<= 1;
+  return p;
+}
+
+// ---------------------------------------------------------------------------
+// generic multi-CTA stable LSD radix sort (u64 keys, u32 values, 8-bit digits)
+// control words live in Work (queue: lsd_*, expired: xlsd_*)
+// ---------------------------------------------------------------------------
+
+struct LsdView {
+  i32* cur;
+  i32* skip;
+  i32* in;
+  u64* maxkey;
+  i32* big;
+  i32* n;
+};
+
+__device__ __forceinline__ LsdView lsd_view(Work* w, int which) {
+  LsdView v;
+  if (which == 0) {
+    v.cur = &w->lsd_cur; v.skip = w->lsd_skip; v.in = w->lsd_in; v.maxkey = &w->lsd_maxkey;
+    v.big = &w->lsd_big; v.n = &w->lsd_n;
+  } else {
+    v.cur = &w->xlsd_cur; v.skip = w->xlsd_skip; v.in = w->xlsd_in; v.maxkey = &w->xlsd_maxkey;
+    v.big = &w->xlsd_big; v.n = &w->xlsd_n;
+  }
+  return v;
+}
+
+__global__ void __launch_bounds__(256) k_lsd_hist(Lsd L, Work* w, int which, int pass) {
+  LsdView v = lsd_view(w, which);
+  if (!*v.big) return;
+  int shift = 8 * pass;
+  if (pass > 0 && ((*v.maxkey) >> shift) == 0) return;
+  int n = *v.n;
+  int cur = *v.cur;
+  __shared__ u32 h[256];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  int chunk = (n + gridDim.x - 1) / gridDim.x;
+  int s = blockIdx.x * chunk, e = min(n, s + chunk);
+  for (int i = s + threadIdx.x; i < e; i += blockDim.x)
+    atomicAdd(&h[(L.k[cur][i] >> shift) & 255u], 1u);
+  __syncthreads();
+  L.cnt[blockIdx.x * 256 + threadIdx.x] = h[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(256) k_lsd_scan(Lsd L, Work* w, int which, int pass, int G) {
+  LsdView v = lsd_view(w, which);
+  if (!*v.big) return;
+  int shift = 8 * pass;
+  if (pass > 0 && ((*v.maxkey) >> shift) == 0) {
+    if (threadIdx.x == 0) v.skip[pass] = 1;
+    return;
+  }
+  __shared__ u32 sh[256];
+  int d = threadIdx.x;
+  u32 tot = 0;
+  for (int cta = 0; cta < G; ++cta) tot += L.cnt[cta * 256 + d];
+  sh[d] = tot;
+  __syncthreads();
+  for (int off = 1; off < 256; off <<= 1) {
+    u32 x = d >= off ? sh[d - off] : 0;
+    __syncthreads();
+    sh[d] += x;
+    __syncthreads();
+  }
+  u32 run = sh[d] - tot;
+  for (int cta = 0; cta < G; ++cta) {
+    u32 x = L.cnt[cta * 256 + d];
+    L.cnt[cta * 256 + d] = run;
+    run += x;
+  }
+  if (d == 0) {
+    v.skip[pass] = 0;
+    v.in[pass] = *v.cur;
+    *v.cur = 1 - *v.cur;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_lsd_scatter(Lsd L, Work* w, int which, int pass) {
+  LsdView v = lsd_view(w, which);
+  if (!*v.big || v.skip[pass]) return;
+  int shift = 8 * pass;
+  int n = *v.n;
+  int in = v.in[pass], out = 1 - in;
+  __shared__ u32 off[256];
+  __shared__ u32 wc[8][256];
+  __shared__ u32 tt[256];
+  int d = threadIdx.x;
+  off[d] = L.cnt[blockIdx.x * 256 + d];
+  for (int q = 0; q < 8; ++q) wc[q][d] = 0;
+  __syncthreads();
+  int chunk = (n + gridDim.x - 1) / gridDim.x;
+  int s = blockIdx.x * chunk, e = min(n, s + chunk);
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int base = s; base < e; base += 256) {
+    int i = base + threadIdx.x;
+    bool valid = i < e;
+    u64 key = valid ? L.k[in][i] : 0;
+    u32 val = valid ? L.v[in][i] : 0;
+    u32 dig = valid ? (u32)((key >> shift) & 255u) : (256u + (u32)lane);
+    u32 peers = __match_any_sync(FULL, dig);
+    u32 rk = __popc(peers & ((1u << lane) - 1u));
+    if (valid && rk == 0) wc[wid][dig] = __popc(peers);
+    __syncthreads();
+    u32 acc = 0;
+    for (int q = 0; q < 8; ++q) {
+      u32 x = wc[q][d];
+      wc[q][d] = acc;
+      acc += x;
+    }
+    tt[d] = acc;
+    __syncthreads();
+    if (valid) {
+      u32 pos = off[dig] + wc[wid][dig] + rk;
+      L.k[out][pos] = key;
+      L.v[out][pos] = val;
+    }
+    __syncthreads();
+    off[d] += tt[d];
+    for (int q = 0; q < 8; ++q) wc[q][d] = 0;
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// expired pins in rank order (side stream)
+// ---------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(1024) k_exp_small(Work* w, Bufs b, Lsd L) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  int n = w->n_exp;
+  if (n > SORT_CAP) {
+    // big: seed the LSD buffers (key = rank, value = index)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      L.k[0][i] = b.exp_rank[i];
+      L.v[0][i] = (u32)i;
+    }
+    if (threadIdx.x == 0) w->xlsd_cur = 0;
+    return;
+  }
+  int n2 = next_pow2(n > 1 ? n : 1);
+  u64* kh = (u64*)smem;
+  u64* kl = kh + n2;
+  u32* pv = (u32*)(kl + n2);
+  for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+    kh[i] = i < n ? (u64)b.exp_rank[i] : ~0ull;
+    kl[i] = (u64)i;
+    pv[i] = (u32)i;
+  }
+  __syncthreads();
+  bitonic_sort(kh, kl, pv, n2);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    u32 j = pv[i];
+    b.exp_row_sorted[i] = b.exp_row[j];
+    b.exp_blk_sorted[i] = b.exp_blk[j];
+  }
+}
+
+__global__ void k_exp_gather(Work* w, Bufs b, Lsd L) {
+  if (!w->xlsd_big) return;
+  int n = w->xlsd_n;
+  int cur = w->xlsd_cur;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    u32 j = L.v[cur][i];
+    b.exp_row_sorted[i] = b.exp_row[j];
+    b.exp_blk_sorted[i] = b.exp_blk[j];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K_Q: pack_queue (control.py:101-122) -- small / first-fit part, one CTA
+// ---------------------------------------------------------------------------
+
+// k-th smallest (0-based) of a[0..n) by MSD radix select, one CTA
+__device__ i32 cta_kth_i32(const i32* a, int n, int k, u32* hist /*256*/, u32* sh) {
+  u32 prefix = 0, mask = 0;
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      u32 x = (u32)a[i] ^ 0x80000000u;
+      if ((x & mask) == prefix) atomicAdd(&hist[(x >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    __shared__ int s_bin, s_k;
+    if (threadIdx.x == 0) {
+      u32 cum = 0;
+      int bin = 255;
+      for (int i = 0; i < 256; ++i) {
+        if (cum + hist[i] > (u32)k) {
+          bin = i;
+          break;
+        }
+        cum += hist[i];
+      }
+      s_bin = bin;
+      s_k = k - (int)cum;
+    }
+    __syncthreads();
+    prefix |= ((u32)s_bin) << shift;
+    mask |= 255u << shift;
+    k = s_k;
+    __syncthreads();
+  }
+  return (i32)(prefix ^ 0x80000000u);
+}
+
+__global__ void __launch_bounds__(1024) k_pack_small(Work* w, Queue Q, Lsd L,
+                                                     mars_scalars* sc, i32* qsel_p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  if (!w->in.control_due) return;
+  int qlen = (int)w->qlen;
+  if (qlen <= 0) return;
+  int sel = *qsel_p;
+  const i32* req = Q.req[sel];
+  int mode = w->pack_mode;
+  __shared__ u32 shu[1024 + 32];
+  __shared__ u32 hist[256];
+  if (mode == PACK_FF) {
+    // first fit against available_kv, in current list order; fits, then deferred
+    __shared__ long long s_cap;
+    __shared__ int s_cursor, s_found, s_nfit;
+    if (threadIdx.x == 0) {
+      s_cap = sc->available_kv;
+      s_nfit = 0;
+    }
+    u32* fit = L.v[1];  // scratch flags (reuse LSD buffer)
+    __syncthreads();
+    for (int base = 0; base < qlen; base += blockDim.x) {
+      int i = base + threadIdx.x;
+      i32 rq = i < qlen ? req[i] : 0;
+      if (i < qlen) fit[i] = 0;
+      if (threadIdx.x == 0) s_cursor = base;
+      __syncthreads();
+      while (true) {
+        long long cap = s_cap;
+        int cand = (i < qlen && i >= s_cursor && (long long)rq <= cap) ? i : 0x7fffffff;
+        __shared__ int shmin[32];
+        int m = block_min<int>(cand, shmin, 0x7fffffff);
+        if (m == 0x7fffffff) break;
+        if (threadIdx.x == 0) {
+          fit[m] = 1;
+          s_cap -= req[m];
+          s_cursor = m + 1;
+          s_nfit++;
+        }
+        __syncthreads();
+      }
+      __syncthreads();
+    }
+    int nfit = s_nfit;
+    // stable partition by block scan over chunks
+    __shared__ int s_fit_run, s_def_run;
+    if (threadIdx.x == 0) {
+      s_fit_run = 0;
+      s_def_run = nfit;
+    }
+    __syncthreads();
+    for (int base = 0; base < qlen; base += blockDim.x) {
+      int i = base + threadIdx.x;
+      u32 isfit = (i < qlen) ? fit[i] : 0;
+      u32 isdef = (i < qlen) ? (1u - isfit) : 0;
+      // scan of isfit (and isdef = valid - isfit)
+      shu[threadIdx.x] = isfit;
+      __syncthreads();
+      for (int off = 1; off < (int)blockDim.x; off <<= 1) {
+        u32 x = threadIdx.x >= (unsigned)off ? shu[threadIdx.x - off] : 0;
+        __syncthreads();
+        shu[threadIdx.x] += x;
+        __syncthreads();
+      }
+      u32 incl = shu[threadIdx.x];
+      u32 tot = shu[blockDim.x - 1];
+      int nvalid = min((int)blockDim.x, qlen - base);
+      if (i < qlen) {
+        int pos = isfit ? (s_fit_run + (int)incl - 1)
+                        : (s_def_run + (int)(threadIdx.x + 1 - incl) - 1);
+        L.v[0][pos] = (u32)i;
+      }
+      (void)isdef;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        s_fit_run += (int)tot;
+        s_def_run += nvalid - (int)tot;
+      }
+      __syncthreads();
+    }
+    if (w->need_seed) {
+      i32 a = cta_kth_i32(req, qlen, (qlen - 1) / 2, hist, shu);
+      i32 bq = cta_kth_i32(req, qlen, qlen / 2, hist, shu);
+      if (threadIdx.x == 0) w->ff_median = (qlen & 1) ? (double)a : (double)((i64)a + (i64)bq) / 2.0;
+    }
+    if (threadIdx.x == 0) w->lsd_cur = 0;
+    return;
+  }
+  i32 mr = w->max_req;
+  if (qlen > SORT_CAP) {
+    // big queue: seed LSD keys (stable sort by req asc, or by -req via max-req)
+    for (int i = threadIdx.x; i < qlen; i += blockDim.x) {
+      i32 rq = req[i];
+      L.k[0][i] = (u64)(mode == PACK_ASC ? rq : (mr - rq));
+      L.v[0][i] = (u32)i;
+    }
+    if (threadIdx.x == 0) w->lsd_cur = 0;
+    return;
+  }
+  int n2 = next_pow2(qlen);
+  u64* kh = (u64*)smem;
+  u64* kl = kh + n2;
+  u32* pv = (u32*)(kl + n2);
+  for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+    if (i < qlen) {
+      i32 rq = req[i];
+      kh[i] = (u64)(mode == PACK_ASC ? rq : (mr - rq));
+    } else {
+      kh[i] = ~0ull;
+    }
+    kl[i] = (u64)i;  // list position: makes the sort stable
+    pv[i] = (u32)i;
+  }
+  __syncthreads();
+  bitonic_sort(kh, kl, pv, n2);
+  for (int i = threadIdx.x; i < qlen; i += blockDim.x) L.v[0][i] = pv[i];
+  if (threadIdx.x == 0) w->lsd_cur = 0;
+}
+
+// ---------------------------------------------------------------------------
+// K_AP: update_window + clamp + admit prefix + residual queue
+// ---------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(SCAN_TPB) k_admit_apply(Tab t, Cfg c, Work* w, Bufs b, Queue Q,
+                                                          Lsd L, mars_scalars* sc, i32* qsel_p) {
+  if (!w->in.control_due) return;
+  __shared__ long long shl[32];
+  __shared__ bool s_last;
+  const double now = w->in.now;
+  const i64 qlen = w->qlen;
+  const int sel = *qsel_p;
+  const u32* perm = L.v[w->lsd_cur];
+  const int mode = w->pack_mode;
+  // balance_and_admit scalars (control.py:181-190), computed redundantly per CTA
+  bool has_seed = sc->has_blocks_seed;
+  double seed = sc->blocks_seed;
+  if (w->need_seed) {
+    has_seed = true;
+    if (mode == PACK_FF) {
+      seed = w->ff_median;
+    } else {
+      i32 r1 = Q.req[sel][perm[(qlen - 1) / 2]];
+      i32 r2 = Q.req[sel][perm[qlen / 2]];
+      seed = (qlen & 1) ? (double)r1 : (double)((i64)r1 + (i64)r2) / 2.0;
+    }
+  }
+  double wadm = sc->w_adm, last = sc->last_update;
+  if (now - last >= c.ctl_interval) {  // update_window (control.py:154-160)
+    if (sc->cpu_overloaded || sc->kv_overloaded) {
+      double x = wadm * c.md;
+      wadm = (x > (double)c.w_min) ? x : (double)c.w_min;
+    } else if (sc->kv_usage_ratio < c.kv_lo) {
+      wadm = wadm + c.ai;
+    }
+    last = now;
+  }
+  double raw = (double)w->in.worker_slots * c.oversub - (double)sc->queued_tools;
+  double cpu = (raw > (double)c.w_min) ? raw : (double)c.w_min;
+  double eff = sc->has_ema_blocks ? sc->ema_blocks : (has_seed ? seed : 1.0);
+  double per = (1.0 > eff) ? 1.0 : eff;
+  i64 cap = (i64)floor((double)sc->available_kv * (1.0 - c.reserve) / per);
+  i64 act = sc->active_sessions;
+  double kvl = ((double)(cap + act) > (double)c.w_min) ? (double)(cap + act) : (double)c.w_min;
+  double m = wadm;
+  if (cpu < m) m = cpu;
+  if (kvl < m) m = kvl;
+  i64 limit = (i64)m;
+  i64 slots = limit - act;
+  i64 take = slots > 0 ? (slots < qlen ? slots : qlen) : 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    w->limit = limit;
+    w->slots = slots;
+    w->take = take;
+  }
+  // admit() of the packed prefix (sim.py:148-166 + MarsPolicy.on_admit)
+  const double scale = (now > 0.0 && now < 1e300) ? 1024.0 / now : 0.0;
+  const u32 tw = (u32)w->t_win;
+  long long proj = 0;
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  const i64 lim = ((take + 31) / 32) * 32;
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < lim; i += stride) {
+    bool valid = i < take;
+    bool wc = false;
+    u64 whi = 0, wlo = 0;
+    u32 row = 0;
+    if (valid) {
+      u32 pos = perm[i];
+      row = Q.row[sel][pos];
+      i32 r0p = t.r0p[row];
+      i32 kvv = t.kv[row];
+      i64 cn = (i64)t.ctx[row] + r0p;
+      t.ctx[row] = (i32)cn;
+      t.rem[row] = t.r0d[row];
+      t.rs[row] = now;
+      t.ws[row] = now;
+      t.phase[row] = MARS_PREFILL;
+      t.flags[row] = (t.flags[row] | MARS_F_ACTIVE) & ~MARS_F_QUEUED;
+      u32 lv = initial_level(c, r0p);
+      t.level[row] = (u8)lv;
+      t.promos[row] = 0;
+      t.served[row] = 0;
+      proj += ceil_div64(cn, c.bs) - ceil_div64(kvv, c.bs);
+      b.admitted[i] = row;
+      u32 kl = c.coord ? lv : 0u;
+      double tt = c.coord ? now : t.arr[row];
+      window_key(kl, tt, t.rank[row], whi, wlo);
+      wc = window_digit(kl, tt, scale) <= tw;
+    }
+    int s = warp_append(&w->n_wc, wc);
+    if (s >= 0) {
+      b.wc_hi[s] = whi;
+      b.wc_lo[s] = wlo;
+      b.wc_row[s] = row;
+    }
+  }
+  // residual queue, in packed order (control.py:190)
+  for (i64 j = (i64)blockIdx.x * blockDim.x + threadIdx.x; j < qlen - take; j += stride) {
+    u32 pos = perm[take + j];
+    Q.row[1 - sel][j] = Q.row[sel][pos];
+    Q.req[1 - sel][j] = Q.req[sel][pos];
+    Q.lng[1 - sel][j] = Q.lng[sel][pos];
+  }
+  long long ps = block_sum<long long>(proj, shl);
+  if (threadIdx.x == 0) {
+    atomicAdd((unsigned long long*)&w->projected, (unsigned long long)ps);
+    __threadfence();
+    u32 tk = atomicAdd(&w->ticket_ap, 1u);
+    s_last = tk == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    __threadfence();
+    volatile Work* vw = w;
+    sc->w_adm = wadm;
+    sc->last_update = last;
+    if (w->need_seed) {
+      sc->has_blocks_seed = 1;
+      sc->blocks_seed = seed;
+    }
+    sc->last_w_adm = wadm;  // telemetry.record("window_update") (telemetry.py:326-327)
+    sc->has_last_w_adm = 1;
+    sc->last_window_update = now;
+    sc->available_kv -= (i64)vw->projected;  // gpu_submit debits (telemetry.py:324-325)
+    sc->queue_len = qlen - take;
+    *qsel_p = 1 - sel;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K_D: the window walk (scheduler.py:283-371 with baselines.py:406-438)
+// ---------------------------------------------------------------------------
+
+#define WALK_TPB 1024
+
+// victim stream entry (prefix of the reclaim order, scheduler.py:259)
+struct VEnt {
+  u64 key, whi, wlo;
+  u32 row;
+  i32 blk;
+  int16_t wi;   // window index or -1
+  u8 pinned, dead;
+};
+
+enum { REQ_NONE = 0, REQ_DONE = 1, REQ_SORT = 2, REQ_FULLSCAN = 3 };
+enum { CL_TRUE = 1, CL_FALSE = 0, CL_NEED_SORT = 2, CL_NEED_FULL = 3 };
+
+#define FS_CAP 4096  // victims one full-scan claim may return
+
+struct WalkShared {
+  // window
+  u64 whi[WIN_MAX], wlo[WIN_MAX];
+  u32 wrow[WIN_MAX];
+  i32 wkv[WIN_MAX], wctx[WIN_MAX], wrem[WIN_MAX];
+  u8 wph[WIN_MAX], wplanned[WIN_MAX];
+  int nwin;
+  // walk state
+  int pass, idx, sub, request, ndec, npre, nev, nj;
+  long long total, freeb;
+  int stream_ready, stream_len, stream_complete, stream_first;
+  int fs_ready, fs_need_i, fs_b, fs_n;
+  long long fs_need;
+  int status;
+  // fast path results
+  int fast_ok;
+};
+
+__device__ __forceinline__ void jpush(Bufs& b, WalkShared& S, u8 op, u32 row, i32 n) {
+  int j = S.nj++;
+  if (j < b.j_cap) {
+    b.j_op[j] = op;
+    b.j_row[j] = row;
+    b.j_n[j] = n;
+  } else {
+    S.status |= ST_WALK_OVERFLOW;
+  }
+}
+
+// evict one victim (sim.py:168-188) -- thread 0 only
+__device__ void walk_evict(Tab& t, Bufs& b, WalkShared& S, u32 row, bool pinned, i32 blk) {
+  if (pinned) {
+    t.flags[row] = t.flags[row] & ~MARS_F_PINNED;
+  } else {
+    t.pre[row] = t.pre[row] + 1;
+    if (t.phase[row] == MARS_DECODE) t.phase[row] = MARS_PREFILL;
+  }
+  t.kv[row] = 0;
+  S.freeb += blk;
+  int e = S.nev++;
+  if (e < b.ev_cap) {
+    b.ev_row[e] = row;
+    b.ev_kind[e] = pinned ? 1 : 0;
+    b.ev_blk[e] = blk;
+  } else {
+    S.status |= ST_WALK_OVERFLOW;
+  }
+  jpush(b, S, pinned ? MARS_J_EVICT_PINNED : MARS_J_EVICT_RUNNING, row, blk);
+  int wi = t.winpos[row];
+  if (wi >= 0) {
+    S.wkv[wi] = 0;
+    if (S.wph[wi] == MARS_DECODE) S.wph[wi] = MARS_PREFILL;
+  }
+}
+
+// is running row `e` (stream entry) an eligible victim for beneficiary bi
+__device__ __forceinline__ bool run_eligible(const Cfg& c, const WalkShared& S, u32 row, u64 ehi,
+                                             u64 elo, int ewi, int bi) {
+  if (row == S.wrow[bi]) return false;
+  if (ewi >= 0 && S.wplanned[ewi]) return false;
+  if (c.coord) return key_lt(S.whi[bi], S.wlo[bi], ehi, elo);
+  // coordinator off: arrival_time strictly greater (baselines.py:431); the
+  // key's time part is ord(arrival)
+  u64 ev = (ehi << 2) | (elo >> 62), bv = (S.whi[bi] << 2) | (S.wlo[bi] >> 62);
+  return ev > bv;
+}
+
+// claim_blocks (scheduler.py:313-324) via the MARS reclaimer -- thread 0
+__device__ int walk_claim(const Cfg& c, Tab& t, Bufs& b, WalkShared& S, VEnt* st, u32* fs_row,
+                          u8* fs_pin, i32* fs_blk, long long need, int bi) {
+  if (S.freeb >= need) return CL_TRUE;
+  if (S.fs_ready && S.fs_need == need && S.fs_b == bi) {
+    S.fs_ready = 0;
+    if (S.fs_n == 0) return CL_FALSE;
+    for (int k = 0; k < S.fs_n; ++k) {
+      walk_evict(t, b, S, fs_row[k], fs_pin[k] != 0, fs_blk[k]);
+      for (int q = 0; q < S.stream_len; ++q)
+        if (st[q].row == fs_row[k]) st[q].dead = 1;
+    }
+    return S.freeb >= need ? CL_TRUE : CL_FALSE;
+  }
+  if (!S.stream_ready) return CL_NEED_SORT;
+  // scan the stream prefix for the shortest sufficient eligible prefix
+  long long freed = 0;
+  int nch = 0;
+  bool found = false;
+  for (int q = S.stream_first; q < S.stream_len; ++q) {
+    VEnt& e = st[q];
+    if (e.dead) continue;
+    if (!e.pinned) {
+      if (e.blk <= 0) continue;
+      if (!run_eligible(c, S, e.row, e.whi, e.wlo, e.wi, bi)) continue;
+    }
+    fs_row[nch] = (u32)q;  // temporarily stream indices
+    nch++;
+    freed += e.blk;
+    if (S.freeb + freed >= need) {
+      found = true;
+      break;
+    }
+  }
+  if (found) {
+    for (int k = 0; k < nch; ++k) {
+      VEnt& e = st[fs_row[k]];
+      e.dead = 1;
+      walk_evict(t, b, S, e.row, e.pinned != 0, e.blk);
+    }
+    while (S.stream_first < S.stream_len && st[S.stream_first].dead) S.stream_first++;
+    return CL_TRUE;
+  }
+  if (S.stream_complete) return CL_FALSE;  // reclaim_for returns [] (scheduler.py:267)
+  S.fs_need = need;
+  S.fs_b = bi;
+  return CL_NEED_FULL;
+}
+
+// try_fit (scheduler.py:136-157) -- thread 0; allocates on success
+__device__ long long walk_try_fit(const Cfg& c, Bufs& b, WalkShared& S, int wi, long long desired) {
+  long long kvv = S.wkv[wi];
+  long long held = ceil_div64(kvv, c.bs);
+  long long room = (held + S.freeb) * c.bs - kvv;
+  long long g = desired <= room ? desired : (room / c.bs) * c.bs;
+  if (g < 1) return 0;
+  long long need = ceil_div64(kvv + g, c.bs) - held;
+  if (need > 0) {
+    S.freeb -= need;
+    jpush(b, S, MARS_J_ALLOC, S.wrow[wi], (i32)need);
+  }
+  return g;
+}
+
+// the sequential walk; returns a request code when it needs the whole CTA
+__device__ int walk_run(const Cfg& c, Tab& t, Bufs& b, WalkShared& S, VEnt* st, u32* fs_row,
+                        u8* fs_pin, i32* fs_blk) {
+  const long long budget = c.budget;
+  while (true) {
+    if (S.pass == 0) {
+      if (S.idx >= S.nwin) {
+        S.pass = 1;
+        S.idx = 0;
+        S.sub = 0;
+        continue;
+      }
+      int i = S.idx;
+      if (S.wph[i] != MARS_DECODE || S.wrem[i] < 1) {
+        S.idx++;
+        continue;
+      }
+      if (S.total >= budget || S.ndec >= c.max_dec) {
+        S.idx++;
+        continue;
+      }
+      long long need = (S.wkv[i] % c.bs == 0) ? 1 : 0;
+      if (need > 0) {
+        int r = walk_claim(c, t, b, S, st, fs_row, fs_pin, fs_blk, need, i);
+        if (r == CL_NEED_SORT) return REQ_SORT;
+        if (r == CL_NEED_FULL) return REQ_FULLSCAN;
+        if (r == CL_FALSE) {
+          S.idx++;
+          continue;
+        }
+        S.freeb -= need;
+        jpush(b, S, MARS_J_ALLOC, S.wrow[i], (i32)need);
+      }
+      b.dec_rows[S.ndec] = S.wrow[i];
+      S.ndec++;
+      S.wplanned[i] = 1;
+      S.total += 1;
+      S.idx++;
+    } else {
+      if (S.idx >= S.nwin) return REQ_DONE;
+      int i = S.idx;
+      if (S.wph[i] != MARS_PREFILL) {
+        S.idx++;
+        continue;
+      }
+      long long left = budget - S.total;
+      if (left < 1) return REQ_DONE;
+      long long rp = (long long)S.wctx[i] - S.wkv[i];
+      long long desired = rp < left ? rp : left;
+      if (desired < 1) {
+        S.idx++;
+        continue;
+      }
+      long long g = 0;
+      long long kvv = S.wkv[i];
+      long long incr = ceil_div64(kvv + desired, c.bs) - ceil_div64(kvv, c.bs);
+      if (c.cosched) {
+        if (S.sub == 0) {
+          g = walk_try_fit(c, b, S, i, desired);
+          if (g == 0) S.sub = 1;
+        }
+        if (S.sub == 1) {
+          int r = walk_claim(c, t, b, S, st, fs_row, fs_pin, fs_blk, incr, i);
+          if (r == CL_NEED_SORT) return REQ_SORT;
+          if (r == CL_NEED_FULL) return REQ_FULLSCAN;
+          S.sub = 0;
+          g = (r == CL_TRUE) ? walk_try_fit(c, b, S, i, desired) : 0;
+        }
+      } else {
+        if (incr == 0) {
+          g = desired;
+        } else {
+          int r = walk_claim(c, t, b, S, st, fs_row, fs_pin, fs_blk, incr, i);
+          if (r == CL_NEED_SORT) return REQ_SORT;
+          if (r == CL_NEED_FULL) return REQ_FULLSCAN;
+          if (r == CL_TRUE) {
+            S.freeb -= incr;
+            jpush(b, S, MARS_J_ALLOC, S.wrow[i], (i32)incr);
+            g = desired;
+          }
+        }
+      }
+      if (g > 0) {
+        b.pre_rows[S.npre] = S.wrow[i];
+        b.pre_grant[S.npre] = (i32)g;
+        S.npre++;
+        S.wplanned[i] = 1;
+        S.total += g;
+      }
+      S.idx++;
+    }
+  }
+}
+
+// exact reclaim_for over the whole table (fallback when the stream prefix is
+// not enough) -- all threads
+__device__ void walk_fullscan(const Cfg& c, Tab& t, WalkShared& S, i64 n_rows, double now,
+                              u32* fs_row, u8* fs_pin, i32* fs_blk) {
+  __shared__ long long shl[32];
+  __shared__ unsigned long long shk[32];
+  __shared__ u32 shr[32];
+  const int bi = S.fs_b;
+  const long long need = S.fs_need;
+  // eligibility + total available
+  long long tot = 0;
+  for (i64 r = threadIdx.x; r < n_rows; r += blockDim.x) {
+    u8 f = t.flags[r];
+    if (f & MARS_F_PINNED) {
+      tot += t.pb[r];
+    } else if ((f & MARS_F_ACTIVE) && (t.phase[r] == MARS_PREFILL || t.phase[r] == MARS_DECODE)) {
+      i32 kvv = t.kv[r];
+      if (kvv <= 0) continue;
+      u64 hi, lo;
+      window_key(c.coord ? t.level[r] : 0u, c.coord ? t.rs[r] : t.arr[r], t.rank[r], hi, lo);
+      int wi = t.winpos[r];
+      if (run_eligible(c, S, (u32)r, hi, lo, wi, bi)) tot += ceil_div64(kvv, c.bs);
+    }
+  }
+  tot = block_sum<long long>(tot, shl);
+  __shared__ int s_n;
+  __shared__ long long s_freed;
+  if (threadIdx.x == 0) {
+    s_n = 0;
+    s_freed = 0;
+  }
+  __syncthreads();
+  if (S.freeb + tot < need) {
+    if (threadIdx.x == 0) {
+      S.fs_n = 0;
+      S.fs_ready = 1;
+    }
+    __syncthreads();
+    return;
+  }
+  u64 last = 0;
+  bool first = true;
+  while (true) {
+    u64 best = ~0ull;
+    u32 brow = 0xffffffffu;
+    for (i64 r = threadIdx.x; r < n_rows; r += blockDim.x) {
+      u8 f = t.flags[r];
+      u64 k;
+      if (f & MARS_F_PINNED) {
+        bool nonexp = !(t.dl[r] < now);
+        k = victim_key(false, nonexp, t.plevel[r], t.pb[r], t.rank[r]);
+      } else if ((f & MARS_F_ACTIVE) &&
+                 (t.phase[r] == MARS_PREFILL || t.phase[r] == MARS_DECODE)) {
+        i32 kvv = t.kv[r];
+        if (kvv <= 0) continue;
+        u64 hi, lo;
+        u32 lv = c.coord ? t.level[r] : 0u;
+        window_key(lv, c.coord ? t.rs[r] : t.arr[r], t.rank[r], hi, lo);
+        if (!run_eligible(c, S, (u32)r, hi, lo, t.winpos[r], bi)) continue;
+        k = victim_key(true, false, lv, ceil_div64(kvv, c.bs), t.rank[r]);
+      } else {
+        continue;
+      }
+      if (!first && k <= last) continue;
+      if (k < best) {
+        best = k;
+        brow = (u32)r;
+      }
+    }
+    // block argmin (keys unique through the rank field)
+    int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int o = 16; o > 0; o >>= 1) {
+      u64 ok = __shfl_xor_sync(FULL, best, o);
+      u32 orow = __shfl_xor_sync(FULL, brow, o);
+      if (ok < best) {
+        best = ok;
+        brow = orow;
+      }
+    }
+    if (lane == 0) {
+      shk[wid] = best;
+      shr[wid] = brow;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      u64 bk = ~0ull;
+      u32 br = 0xffffffffu;
+      for (int q = 0; q < (int)(blockDim.x >> 5); ++q)
+        if (shk[q] < bk) {
+          bk = shk[q];
+          br = shr[q];
+        }
+      shk[0] = bk;
+      shr[0] = br;
+      if (br != 0xffffffffu && s_n < FS_CAP) {
+        bool pinned = (bk >> 63) == 0;
+        i32 blk = pinned ? t.pb[br] : (i32)ceil_div64(t.kv[br], c.bs);
+        fs_row[s_n] = br;
+        fs_pin[s_n] = pinned;
+        fs_blk[s_n] = blk;
+        s_n++;
+        s_freed += blk;
+      }
+    }
+    __syncthreads();
+    u64 bk = shk[0];
+    u32 br = shr[0];
+    __syncthreads();
+    if (br == 0xffffffffu || S.freeb + s_freed >= need || s_n >= FS_CAP) break;
+    last = bk;
+    first = false;
+  }
+  if (threadIdx.x == 0) {
+    if (S.freeb + s_freed < need) S.status |= ST_WALK_OVERFLOW;
+    S.fs_n = s_n;
+    S.fs_ready = 1;
+  }
+  __syncthreads();
+}
+
+// select the `k` smallest (hi, lo) keys of a global candidate list into smem,
+// sorted.  Bitonic when n <= SORT_CAP, else MSD radix refinement first.
+__device__ int cta_select_sorted(const u64* ghi, const u64* glo, const u32* gpay, int n, int k,
+                                 u64* kh, u64* kl, u32* pv, u32* hist /*256*/) {
+  if (n <= SORT_CAP) {
+    int n2 = next_pow2(n > 1 ? n : 1);
+    for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+      kh[i] = i < n ? ghi[i] : ~0ull;
+      kl[i] = i < n ? glo[i] : ~0ull;
+      pv[i] = i < n ? gpay[i] : 0xffffffffu;
+    }
+    __syncthreads();
+    bitonic_sort(kh, kl, pv, n2);
+    return n < k ? n : k;
+  }
+  // MSD refinement over the 128-bit key: find the k-th smallest key exactly
+  __shared__ u64 s_ph, s_pl, s_mh, s_ml;
+  __shared__ int s_need;
+  if (threadIdx.x == 0) {
+    s_ph = s_pl = s_mh = s_ml = 0;
+    s_need = k;
+  }
+  __syncthreads();
+  for (int d = 0; d < 16; ++d) {
+    int shift = 56 - 8 * (d & 7);
+    bool hiword = d < 8;
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    u64 ph = s_ph, pl = s_pl, mh = s_mh, ml = s_ml;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      u64 h = ghi[i], l = glo[i];
+      if ((h & mh) == ph && (l & ml) == pl) {
+        u32 dg = (u32)(((hiword ? h : l) >> shift) & 255u);
+        atomicAdd(&hist[dg], 1u);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int need = s_need;
+      u32 cum = 0;
+      int bin = 255;
+      for (int q = 0; q < 256; ++q) {
+        if (cum + hist[q] >= (u32)need) {
+          bin = q;
+          break;
+        }
+        cum += hist[q];
+      }
+      s_need = need - (int)cum;
+      if (hiword) {
+        s_ph |= ((u64)bin) << shift;
+        s_mh |= 255ull << shift;
+      } else {
+        s_pl |= ((u64)bin) << shift;
+        s_ml |= 255ull << shift;
+      }
+    }
+    __syncthreads();
+  }
+  // s_ph/s_pl is now the exact k-th smallest key; gather keys <= it
+  __shared__ int s_cnt;
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
+  u64 th = s_ph, tl = s_pl;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    u64 h = ghi[i], l = glo[i];
+    if (!key_lt(th, tl, h, l)) {
+      int s = atomicAdd(&s_cnt, 1);
+      if (s < SORT_CAP) {
+        kh[s] = h;
+        kl[s] = l;
+        pv[s] = gpay[i];
+      }
+    }
+  }
+  __syncthreads();
+  int m = s_cnt < SORT_CAP ? s_cnt : SORT_CAP;
+  int n2 = next_pow2(m > 1 ? m : 1);
+  for (int i = m + threadIdx.x; i < n2; i += blockDim.x) {
+    kh[i] = ~0ull;
+    kl[i] = ~0ull;
+    pv[i] = 0xffffffffu;
+  }
+  __syncthreads();
+  bitonic_sort(kh, kl, pv, n2);
+  return m < k ? m : k;
+}
+
+__global__ void __launch_bounds__(WALK_TPB) k_walk(Tab t, Cfg c, Work* w, Bufs b,
+                                                   mars_scalars* sc, i64 n_rows) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ WalkShared S;
+  __shared__ u32 hist[256];
+  // dynamic smem: sort area (SORT_CAP x (8+8+4)) reused for the victim stream
+  u64* kh = (u64*)smem;
+  u64* kl = kh + SORT_CAP;
+  u32* pv = (u32*)(kl + SORT_CAP);
+  VEnt* st = (VEnt*)(pv + SORT_CAP);           // VSTREAM_CAP entries
+  u32* fs_row = (u32*)(st + VSTREAM_CAP);       // FS_CAP
+  u8* fs_pin = (u8*)(fs_row + FS_CAP);
+  i32* fs_blk = (i32*)(((uintptr_t)(fs_pin + FS_CAP) + 15) & ~(uintptr_t)15);
+
+  const double now = w->in.now;
+  // 1. window = top-k of the candidates (k_compact + admitted rows)
+  int nwc = w->n_wc;
+  int nwin = cta_select_sorted(b.wc_hi, b.wc_lo, b.wc_row, nwc, c.window, kh, kl, pv, hist);
+  for (int i = threadIdx.x; i < nwin; i += blockDim.x) {
+    u32 r = pv[i];
+    S.whi[i] = kh[i];
+    S.wlo[i] = kl[i];
+    S.wrow[i] = r;
+    S.wkv[i] = t.kv[r];
+    S.wctx[i] = t.ctx[r];
+    S.wrem[i] = t.rem[r];
+    S.wph[i] = t.phase[r];
+    S.wplanned[i] = 0;
+    t.winpos[r] = (int16_t)i;
+    b.win_rows[i] = r;
+  }
+  if (threadIdx.x == 0) {
+    S.nwin = nwin;
+    S.pass = 0;
+    S.idx = 0;
+    S.sub = 0;
+    S.ndec = S.npre = S.nev = S.nj = 0;
+    S.total = 0;
+    S.freeb = sc->free_blocks;
+    S.stream_ready = 0;
+    S.stream_len = 0;
+    S.stream_first = 0;
+    S.stream_complete = 0;
+    S.fs_ready = 0;
+    S.status = 0;
+    S.fast_ok = 0;
+  }
+  __syncthreads();
+
+  // 2. fast path (warp 0): no claim can fail when the free pool covers every
+  //    allocation of the greedy plan -> prefix sums reproduce build_plan.
+  if (threadIdx.x < 32) {
+    int lane = threadIdx.x;
+    const long long bs = c.bs;
+    long long budget = c.budget;
+    long long lim_dec = c.max_dec < budget ? c.max_dec : budget;
+    // decode eligibility counts
+    int base = 0;
+    long long need_dec = 0;
+    int selected_mask[4] = {0, 0, 0, 0};
+    int cnt_before = 0;
+    for (int q = 0; q < 4; ++q) {
+      int i = q * 32 + lane;
+      bool e = i < nwin && S.wph[i] == MARS_DECODE && S.wrem[i] >= 1;
+      u32 m = __ballot_sync(FULL, e);
+      int pos = cnt_before + __popc(m & ((1u << lane) - 1u));
+      bool sel = e && pos < lim_dec;
+      selected_mask[q] = sel;
+      if (sel && (S.wkv[i] % bs == 0)) need_dec += 1;
+      cnt_before += __popc(m);
+    }
+    (void)base;
+    long long ndec = cnt_before < lim_dec ? cnt_before : lim_dec;
+    need_dec = warp_sum<long long>(need_dec);
+    long long left0 = budget - ndec;
+    // prefill grants: S_j = min(P_j, left0), g_j = min(rp_j, left0 - S_j)
+    long long run = 0;  // P_j prefix over earlier PREFILL entries
+    long long need_pre = 0;
+    long long grant[4] = {0, 0, 0, 0};
+    for (int q = 0; q < 4; ++q) {
+      int i = q * 32 + lane;
+      bool p = i < nwin && S.wph[i] == MARS_PREFILL;
+      long long rp = p ? ((long long)S.wctx[i] - S.wkv[i]) : 0;
+      long long rpp = rp > 0 ? rp : 0;
+      // inclusive warp scan of rpp
+      long long incl = rpp;
+      for (int o = 1; o < 32; o <<= 1) {
+        long long x = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += x;
+      }
+      long long P = run + incl - rpp;
+      long long Sj = P < left0 ? P : left0;
+      long long lft = left0 - Sj;
+      long long g = 0;
+      if (p && lft >= 1 && rp >= 1) g = rp < lft ? rp : lft;
+      grant[q] = g;
+      if (g > 0) need_pre += ceil_div64(S.wkv[i] + g, bs) - ceil_div64(S.wkv[i], bs);
+      run += __shfl_sync(FULL, incl, 31);
+    }
+    need_pre = warp_sum<long long>(need_pre);
+    bool ok = S.freeb >= need_dec + need_pre;
+    if (ok) {
+      // emit in window order: decode allocations, then prefill allocations
+      int dcount = 0, pcount = 0, jcount = 0;
+      for (int q = 0; q < 4; ++q) {
+        int i = q * 32 + lane;
+        bool sel = selected_mask[q];
+        u32 m = __ballot_sync(FULL, sel);
+        int pos = dcount + __popc(m & ((1u << lane) - 1u));
+        if (sel) {
+          b.dec_rows[pos] = S.wrow[i];
+          S.wplanned[i] = 1;
+        }
+        dcount += __popc(m);
+        bool need = sel && (S.wkv[i] % bs == 0);
+        u32 mj = __ballot_sync(FULL, need);
+        int jp = jcount + __popc(mj & ((1u << lane) - 1u));
+        if (need) {
+          b.j_op[jp] = MARS_J_ALLOC;
+          b.j_row[jp] = S.wrow[i];
+          b.j_n[jp] = 1;
+        }
+        jcount += __popc(mj);
+      }
+      long long tot = ndec;
+      for (int q = 0; q < 4; ++q) {
+        int i = q * 32 + lane;
+        long long g = grant[q];
+        bool gp = g > 0;
+        u32 m = __ballot_sync(FULL, gp);
+        int pos = pcount + __popc(m & ((1u << lane) - 1u));
+        long long nd = gp ? ceil_div64(S.wkv[i] + g, bs) - ceil_div64(S.wkv[i], bs) : 0;
+        if (gp) {
+          b.pre_rows[pos] = S.wrow[i];
+          b.pre_grant[pos] = (i32)g;
+          S.wplanned[i] = 1;
+        }
+        pcount += __popc(m);
+        bool hn = nd > 0;
+        u32 mj = __ballot_sync(FULL, hn);
+        int jp = jcount + __popc(mj & ((1u << lane) - 1u));
+        if (hn) {
+          b.j_op[jp] = MARS_J_ALLOC;
+          b.j_row[jp] = S.wrow[i];
+          b.j_n[jp] = (i32)nd;
+        }
+        jcount += __popc(mj);
+        tot += warp_sum<long long>(g);
+      }
+      if (lane == 0) {
+        S.fast_ok = 1;
+        S.ndec = dcount;
+        S.npre = pcount;
+        S.nj = jcount;
+        S.total = tot;
+        S.freeb -= need_dec + need_pre;
+        S.request = REQ_DONE;
+      }
+    }
+  }
+  __syncthreads();
+
+  // 3. sequential walk with on-demand help from the whole CTA
+  if (!S.fast_ok) {
+    while (true) {
+      if (threadIdx.x == 0) S.request = walk_run(c, t, b, S, st, fs_row, fs_pin, fs_blk);
+      __syncthreads();
+      int rq = S.request;
+      if (rq == REQ_DONE) break;
+      if (rq == REQ_SORT) {
+        // victim stream: the smallest VSTREAM_CAP reclaim keys among the candidates
+        int nvc = w->n_vc;
+        int len = cta_select_sorted(b.vc_key, b.vc_key /*lo unused*/, b.vc_row, nvc,
+                                    VSTREAM_CAP, kh, kl, pv, hist);
+        // kl holds vc_key again (lo == hi); payload = row; recover per-entry data by
+        // a second lookup: build index map row -> candidate slot
+        __syncthreads();
+        for (int q = threadIdx.x; q < nvc; q += blockDim.x) {
+          u64 key = b.vc_key[q];
+          // position of this key in the sorted prefix (binary search)
+          int lo = 0, hi = len;
+          while (lo < hi) {
+            int mid = (lo + hi) >> 1;
+            if (kh[mid] < key) lo = mid + 1; else hi = mid;
+          }
+          if (lo < len && kh[lo] == key) {
+            VEnt e;
+            e.key = key;
+            e.whi = b.vc_whi[q];
+            e.wlo = b.vc_wlo[q];
+            e.row = b.vc_row[q];
+            e.blk = b.vc_blk[q];
+            e.pinned = (key >> 63) == 0;
+            e.dead = 0;
+            e.wi = t.winpos[e.row];
+            st[lo] = e;
+          }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          S.stream_ready = 1;
+          S.stream_len = len;
+          S.stream_first = 0;
+          S.stream_complete = (len == nvc && nvc == w->n_victims) ? 1 : 0;
+          // entries already evicted this walk (none before the first sort)
+        }
+        __syncthreads();
+      } else if (rq == REQ_FULLSCAN) {
+        walk_fullscan(c, t, S, n_rows, now, fs_row, fs_pin, fs_blk);
+      }
+    }
+  }
+  __syncthreads();
+
+  // 4. outputs, scalars, winpos reset
+  for (int i = threadIdx.x; i < nwin; i += blockDim.x) t.winpos[S.wrow[i]] = -1;
+  if (threadIdx.x == 0) {
+    w->n_window = nwin;
+    w->n_dec = S.ndec;
+    w->n_pre = S.npre;
+    w->n_evict = S.nev;
+    w->n_journal = S.nj;
+    w->total_tokens = S.total;
+    w->walk_slow = S.fast_ok ? 0 : 1;
+    w->status |= S.status;
+    sc->free_blocks = S.freeb;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// standalone retention batch (mars_retention_batch)
+// ---------------------------------------------------------------------------
+
+__global__ void k_retention_batch(Cfg c, i64 n, const i32* ctx, const i32* kv, i64 total,
+                                  double usage, double ema, double now, u8* pin, double* bb,
+                                  double* cc, double* dd) {
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (i64)gridDim.x * blockDim.x) {
+    u8 p;
+    double x, y, z;
+    decide_retention(c, ctx[i], kv[i], total, usage, ema, now, p, x, y, z);
+    pin[i] = p;
+    bb[i] = x;
+    cc[i] = y;
+    dd[i] = z;
+  }
+}
+
+__global__ void k_flush(u8* p, i64 n, u32 salt) {
+  u32* q = (u32*)p;
+  i64 m = n / 4;
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (i64)gridDim.x * blockDim.x)
+    q[i] = (u32)i ^ salt;
+}
+
+__global__ void k_work_init(Work* w) {
+  if (threadIdx.x == 0) {
+    w->tmin_win = 0xffffffffu;
+    w->tmin_vic = 0xffffffffu;
+    w->min_req = 0x7fffffff;
+  }
+}
+
+// row scatter / gather for the session-state store (element size 1, 4 or 8)
+__global__ void k_scatter(u8* dst, const u8* src, const i64* rows, i64 n, int esz) {
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (i64)gridDim.x * blockDim.x) {
+    i64 r = rows[i];
+    if (esz == 1) dst[r] = src[i];
+    else if (esz == 4) ((u32*)dst)[r] = ((const u32*)src)[i];
+    else ((u64*)dst)[r] = ((const u64*)src)[i];
+  }
+}
+
+__global__ void k_gather(u8* dst, const u8* src, const i64* rows, i64 n, int esz) {
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (i64)gridDim.x * blockDim.x) {
+    i64 r = rows[i];
+    if (esz == 1) dst[i] = src[r];
+    else if (esz == 4) ((u32*)dst)[i] = ((const u32*)src)[r];
+    else ((u64*)dst)[i] = ((const u64*)src)[r];
+  }
+}
+
+int mars_enqueue_scatter(cudaStream_t s, void* dst, const void* src, const i64* rows, i64 n,
+                         int esz) {
+  if (n <= 0) return 0;
+  int g = (int)((n + 255) / 256);
+  if (g > 1184) g = 1184;
+  k_scatter<<<g, 256, 0, s>>>((u8*)dst, (const u8*)src, rows, n, esz);
+  return (int)cudaGetLastError();
+}
+
+int mars_enqueue_gather(cudaStream_t s, void* dst, const void* src, const i64* rows, i64 n,
+                        int esz) {
+  if (n <= 0) return 0;
+  int g = (int)((n + 255) / 256);
+  if (g > 1184) g = 1184;
+  k_gather<<<g, 256, 0, s>>>((u8*)dst, (const u8*)src, rows, n, esz);
+  return (int)cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// host-side launch sequence
+// ---------------------------------------------------------------------------
+
+static size_t walk_smem_bytes() {
+  size_t s = (size_t)SORT_CAP * (8 + 8 + 4);
+  s += (size_t)VSTREAM_CAP * sizeof(VEnt);
+  s += (size_t)FS_CAP * (4 + 1) + 16 + (size_t)FS_CAP * 4;
+  return s;
+}
+
+static size_t sort_smem_bytes() { return (size_t)SORT_CAP * (8 + 8 + 4); }
+
+int mars_kernels_init() {
+  cudaError_t e;
+  e = cudaFuncSetAttribute(k_walk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)walk_smem_bytes());
+  if (e != cudaSuccess) return (int)e;
+  e = cudaFuncSetAttribute(k_pack_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sort_smem_bytes());
+  if (e != cudaSuccess) return (int)e;
+  e = cudaFuncSetAttribute(k_exp_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sort_smem_bytes());
+  return (int)e;
+}
+
+int mars_enqueue_step(const LaunchArgs* a) {
+  cudaStream_t s = a->stream, s2 = a->side;
+  int launches = 0;
+  cudaMemsetAsync(a->work, 0, sizeof(Work), s);
+  // tmin = max, min_req = max
+  cudaMemcpyAsync(a->work, a->host_in, sizeof(mars_step_in), cudaMemcpyHostToDevice, s);
+  k_work_init<<<1, 32, 0, s>>>(a->work);
+  launches++;
+  int nsm = a->num_sms;
+  i64 n = a->n_rows;
+  int g_scan = (int)((n + 2047) / 2048);
+  if (g_scan > 2 * nsm) g_scan = 2 * nsm;
+  if (g_scan < 1) g_scan = 1;
+  k_scan<<<g_scan, SCAN_TPB, 0, s>>>(a->tab, a->cfg, a->work, a->bufs, a->sc, n);
+  launches++;
+  cudaEventRecord(a->ev_fork, s);
+  cudaStreamWaitEvent(s2, a->ev_fork, 0);
+  int g_c = (int)((n + SCAN_TPB - 1) / SCAN_TPB);
+  if (g_c > 4 * nsm) g_c = 4 * nsm;
+  if (g_c < 1) g_c = 1;
+  k_compact<<<g_c, SCAN_TPB, 0, s2>>>(a->tab, a->cfg, a->work, a->bufs, a->sc, n);
+  launches++;
+  k_exp_small<<<1, 1024, sort_smem_bytes(), s2>>>(a->work, a->bufs, a->xlsd);
+  launches++;
+  if (a->exp_may_be_big) {
+    for (int p = 0; p < 4; ++p) {
+      k_lsd_hist<<<LSD_G, 256, 0, s2>>>(a->xlsd, a->work, 1, p);
+      k_lsd_scan<<<1, 256, 0, s2>>>(a->xlsd, a->work, 1, p, LSD_G);
+      k_lsd_scatter<<<LSD_G, 256, 0, s2>>>(a->xlsd, a->work, 1, p);
+      launches += 3;
+    }
+    k_exp_gather<<<nsm, 256, 0, s2>>>(a->work, a->bufs, a->xlsd);
+    launches++;
+  }
+  cudaEventRecord(a->ev_join, s2);
+  if (a->control_possible) {
+    k_pack_small<<<1, 1024, sort_smem_bytes(), s>>>(a->work, a->queue, a->qlsd, a->sc, a->qsel);
+    launches++;
+    for (int p = 0; p < a->queue_passes; ++p) {
+      k_lsd_hist<<<LSD_G, 256, 0, s>>>(a->qlsd, a->work, 0, p);
+      k_lsd_scan<<<1, 256, 0, s>>>(a->qlsd, a->work, 0, p, LSD_G);
+      k_lsd_scatter<<<LSD_G, 256, 0, s>>>(a->qlsd, a->work, 0, p);
+      launches += 3;
+    }
+  }
+  cudaStreamWaitEvent(s, a->ev_join, 0);
+  if (a->control_possible) {
+    int g_ap = (int)((a->queue_upper + SCAN_TPB - 1) / SCAN_TPB);
+    if (g_ap > 2 * nsm) g_ap = 2 * nsm;
+    if (g_ap < 1) g_ap = 1;
+    k_admit_apply<<<g_ap, SCAN_TPB, 0, s>>>(a->tab, a->cfg, a->work, a->bufs, a->queue, a->qlsd,
+                                            a->sc, a->qsel);
+    launches++;
+  }
+  k_walk<<<1, WALK_TPB, walk_smem_bytes(), s>>>(a->tab, a->cfg, a->work, a->bufs, a->sc, n);
+  launches++;
+  return launches;
+}
+
+int mars_enqueue_retention(const Cfg& c, cudaStream_t s, i64 n, const i32* ctx, const i32* kv,
+                           i64 total, double usage, double ema, double now, u8* pin, double* bb,
+                           double* cc, double* dd) {
+  int g = (int)((n + 255) / 256);
+  if (g > 1184) g = 1184;
+  if (g < 1) g = 1;
+  k_retention_batch<<<g, 256, 0, s>>>(c, n, ctx, kv, total, usage, ema, now, pin, bb, cc, dd);
+  return (int)cudaGetLastError();
+}
+
+int mars_enqueue_flush(cudaStream_t s, u8* p, i64 n, u32 salt) {
+  k_flush<<<1184, 256, 0, s>>>(p, n, salt);
+  return (int)cudaGetLastError();
+}

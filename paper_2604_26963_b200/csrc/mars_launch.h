@@ -1,0 +1,35 @@
+// Host-side launch interface between the C ABI (mars_abi.cu) and the kernels.
+#pragma once
+
+#include "mars_internal.cuh"
+
+struct LaunchArgs {
+  cudaStream_t stream, side;
+  cudaEvent_t ev_fork, ev_join;
+  Tab tab;
+  Cfg cfg;
+  Work* work;
+  Bufs bufs;
+  mars_scalars* sc;
+  Queue queue;
+  Lsd qlsd, xlsd;
+  i32* qsel;
+  const mars_step_in* host_in;
+  i64 n_rows;
+  int num_sms;
+  int control_possible;  // the step may run the control plane
+  int queue_passes;      // LSD passes needed for the largest queue key (0 = small only)
+  i64 queue_upper;       // upper bound of the queue length at step start
+  int exp_may_be_big;    // more than SORT_CAP pins may expire
+};
+
+int mars_kernels_init();
+int mars_enqueue_step(const LaunchArgs* a);
+int mars_enqueue_retention(const Cfg& c, cudaStream_t s, i64 n, const i32* ctx, const i32* kv,
+                           i64 total, double usage, double ema, double now, u8* pin, double* bb,
+                           double* cc, double* dd);
+int mars_enqueue_flush(cudaStream_t s, u8* p, i64 n, u32 salt);
+int mars_enqueue_scatter(cudaStream_t s, void* dst, const void* src, const i64* rows, i64 n,
+                         int esz);
+int mars_enqueue_gather(cudaStream_t s, void* dst, const void* src, const i64* rows, i64 n,
+                        int esz);

@@ -1,0 +1,322 @@
+"""Host-side handle on one device replica of the MARS session table.
+
+``MarsEngine`` owns a ``mars_ctx`` (include/mars_b200.h): the structure-of-
+arrays session table in HBM, the admission list, the pool/telemetry/controller
+scalars, and the step pipeline.  It is the device-resident engine mode the
+benchmark and the multi-GPU replicas use; the reference-plugin drop-in
+(``policy.GpuMarsPolicy``) drives the same context one tick at a time.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Dict, List, Optional
+
+import numpy as np
+
+from . import _native as N
+from .snapshot import COLUMNS, F_LONG, Snapshot
+
+JOURNAL_NAMES = {1: "alloc", 2: "free", 3: "free", 4: "free"}
+
+
+def _ptr(a: np.ndarray, ct):
+    return a.ctypes.data_as(C.POINTER(ct))
+
+
+_CT = {np.uint8: C.c_uint8, np.uint32: C.c_uint32, np.int32: C.c_int32, np.int64: C.c_int64,
+       np.float64: C.c_double}
+
+
+def make_config(enable_coordinator: bool = True, enable_coscheduler: bool = True,
+                initial_window: Optional[float] = None, **overrides) -> N.MarsConfig:
+    lib = N.load()
+    cfg = N.MarsConfig()
+    lib.mars_config_default(C.byref(cfg))
+    cfg.enable_coordinator = int(bool(enable_coordinator))
+    cfg.enable_coscheduler = int(bool(enable_coscheduler))
+    if initial_window is not None:
+        cfg.initial_window = float(initial_window)
+    for k, v in overrides.items():
+        setattr(cfg, k, v)
+    return cfg
+
+
+@dataclass
+class StepResult:
+    status: int
+    expired_rows: np.ndarray
+    expired_blocks: np.ndarray
+    admitted_rows: np.ndarray
+    window_rows: np.ndarray
+    decode_rows: np.ndarray
+    prefill_rows: np.ndarray
+    prefill_grants: np.ndarray
+    evict_rows: np.ndarray
+    evict_kind: np.ndarray
+    evict_blocks: np.ndarray
+    journal_op: np.ndarray
+    journal_row: np.ndarray
+    journal_n: np.ndarray
+    ret_rows: np.ndarray
+    ret_pin: np.ndarray
+    ret_benefit: np.ndarray
+    ret_cost: np.ndarray
+    ret_deadline: np.ndarray
+    n_ready: int
+    n_promoted: int
+    pack_mode: int
+    total_tokens: int
+    free_after_expiry: int
+    free_blocks: int
+    limit: int
+    slots: int
+
+
+def _arr(p, n, dt):
+    if n <= 0:
+        return np.zeros(0, dtype=dt)
+    return np.ctypeslib.as_array(p, shape=(n,)).astype(dt, copy=True)
+
+
+class MarsEngine:
+    """One device replica (one ``mars_ctx``)."""
+
+    def __init__(self, max_rows: int, max_queue: Optional[int] = None, device: int = 0,
+                 config: Optional[N.MarsConfig] = None) -> None:
+        self.lib = N.load()
+        self.cfg = config if config is not None else make_config()
+        self.max_rows = int(max_rows)
+        self.max_queue = int(max_queue if max_queue is not None else max_rows)
+        ctx = C.c_void_p()
+        N.check(self.lib.mars_create(C.byref(self.cfg), device, self.max_rows, self.max_queue,
+                                     C.byref(ctx)))
+        self.ctx = ctx
+        self.n_rows = 0
+
+    def close(self) -> None:
+        if self.ctx:
+            self.lib.mars_destroy(self.ctx)
+            self.ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc: int) -> None:
+        N.check(rc, self.ctx)
+
+    # -- session-state store -------------------------------------------------
+
+    def upsert(self, cols: Dict[str, np.ndarray], rows: Optional[np.ndarray] = None) -> None:
+        keep = []
+        mc = N.MarsCols()
+        n = None
+        for name, field in N.COL_FIELDS.items():
+            if name not in cols:
+                continue
+            a = np.ascontiguousarray(cols[name], dtype=COLUMNS[name])
+            keep.append(a)
+            setattr(mc, field, _ptr(a, _CT[COLUMNS[name]]))
+            n = len(a) if n is None else n
+            if len(a) != n:
+                raise ValueError("column lengths differ")
+        if n is None:
+            return
+        if rows is None:
+            self._check(self.lib.mars_upsert_rows(self.ctx, n, None, C.byref(mc)))
+            self.n_rows = max(self.n_rows, n)
+        else:
+            r = np.ascontiguousarray(rows, dtype=np.int64)
+            if len(r) != n:
+                raise ValueError("rows / column length mismatch")
+            self._check(self.lib.mars_upsert_rows(self.ctx, n, r.ctypes.data_as(C.c_void_p),
+                                                  C.byref(mc)))
+            if n:
+                self.n_rows = max(self.n_rows, int(r.max()) + 1)
+
+    def read(self, names=None, rows: Optional[np.ndarray] = None) -> Dict[str, np.ndarray]:
+        names = list(names or N.COL_FIELDS)
+        n = self.n_rows if rows is None else len(rows)
+        out = {k: np.zeros(n, dtype=COLUMNS[k]) for k in names}
+        mc = N.MarsCols()
+        for k in names:
+            setattr(mc, N.COL_FIELDS[k], _ptr(out[k], _CT[COLUMNS[k]]))
+        if rows is None:
+            self._check(self.lib.mars_read_rows(self.ctx, n, None, C.byref(mc)))
+        else:
+            r = np.ascontiguousarray(rows, dtype=np.int64)
+            self._check(self.lib.mars_read_rows(self.ctx, n, r.ctypes.data_as(C.c_void_p),
+                                                C.byref(mc)))
+        return out
+
+    def set_queue(self, rows: np.ndarray, req: np.ndarray, is_long: np.ndarray) -> None:
+        r = np.ascontiguousarray(rows, dtype=np.uint32)
+        q = np.ascontiguousarray(req, dtype=np.int32)
+        lg = np.ascontiguousarray(is_long, dtype=np.uint8)
+        self._check(self.lib.mars_set_queue(self.ctx, len(r), r.ctypes.data_as(C.c_void_p),
+                                            q.ctypes.data_as(C.c_void_p),
+                                            lg.ctypes.data_as(C.c_void_p)))
+
+    def get_queue(self) -> np.ndarray:
+        n = C.c_int64()
+        self._check(self.lib.mars_get_queue(self.ctx, 0, None, C.byref(n)))
+        out = np.zeros(n.value, dtype=np.uint32)
+        if n.value:
+            self._check(self.lib.mars_get_queue(self.ctx, n.value, out.ctypes.data_as(C.c_void_p),
+                                                C.byref(n)))
+        return out
+
+    def set_scalars(self, s: N.MarsScalars) -> None:
+        self._check(self.lib.mars_set_scalars(self.ctx, C.byref(s)))
+
+    def get_scalars(self) -> N.MarsScalars:
+        s = N.MarsScalars()
+        self._check(self.lib.mars_get_scalars(self.ctx, C.byref(s)))
+        return s
+
+    def load_snapshot(self, snap: Snapshot) -> None:
+        if snap.n > self.max_rows:
+            raise ValueError("snapshot larger than the engine's row capacity")
+        self._check(self.lib.mars_set_rows(self.ctx, snap.n))
+        self.upsert(snap.cols)
+        self.n_rows = snap.n
+        q = snap.queue
+        self.set_queue(q, snap.cols["req_blocks"][q],
+                       (snap.cols["flags"][q] & F_LONG) != 0)
+        s = N.MarsScalars()
+        s.total_blocks = snap.total_blocks
+        s.free_blocks = snap.free_blocks
+        s.available_kv = snap.free_blocks
+        s.w_adm = float(snap.initial_window)
+        s.last_update = 0.0
+        s.has_ema_tool = int(snap.ema_tool is not None)
+        s.ema_tool = float(snap.ema_tool or 0.0)
+        s.has_ema_blocks = int(snap.ema_blocks is not None)
+        s.ema_blocks = float(snap.ema_blocks or 0.0)
+        s.has_blocks_seed = int(snap.blocks_seed is not None)
+        s.blocks_seed = float(snap.blocks_seed or 0.0)
+        s.queue_len = len(q)
+        for k, v in snap.telemetry.items():
+            setattr(s, k, int(v))
+        self.set_scalars(s)
+
+    # -- the step ----------------------------------------------------------------
+
+    @staticmethod
+    def step_in(now: float, control_due: bool = True, active_tools: int = 0,
+                queued_tools: int = 0, worker_slots: int = 8,
+                skip_expiry: bool = False) -> N.MarsStepIn:
+        si = N.MarsStepIn()
+        si.now = float(now)
+        si.control_due = int(bool(control_due))
+        si.active_tools = int(active_tools)
+        si.queued_tools = int(queued_tools)
+        si.worker_slots = int(worker_slots)
+        si.skip_expiry = int(bool(skip_expiry))
+        return si
+
+    def enqueue(self, si: N.MarsStepIn) -> None:
+        self._check(self.lib.mars_step_enqueue(self.ctx, C.byref(si)))
+
+    def fetch(self) -> StepResult:
+        o = N.MarsStepOut()
+        self._check(self.lib.mars_step_fetch(self.ctx, C.byref(o)))
+        return StepResult(
+            status=o.status,
+            expired_rows=_arr(o.expired_rows, o.n_expired, np.uint32),
+            expired_blocks=_arr(o.expired_blocks, o.n_expired, np.int32),
+            admitted_rows=_arr(o.admitted_rows, o.n_admitted, np.uint32),
+            window_rows=_arr(o.window_rows, o.n_window, np.uint32),
+            decode_rows=_arr(o.decode_rows, o.n_decode, np.uint32),
+            prefill_rows=_arr(o.prefill_rows, o.n_prefill, np.uint32),
+            prefill_grants=_arr(o.prefill_grants, o.n_prefill, np.int32),
+            evict_rows=_arr(o.evict_rows, o.n_evict, np.uint32),
+            evict_kind=_arr(o.evict_kind, o.n_evict, np.uint8),
+            evict_blocks=_arr(o.evict_blocks, o.n_evict, np.int32),
+            journal_op=_arr(o.journal_op, o.n_journal, np.uint8),
+            journal_row=_arr(o.journal_row, o.n_journal, np.uint32),
+            journal_n=_arr(o.journal_n, o.n_journal, np.int32),
+            ret_rows=_arr(o.ret_rows, o.n_retention, np.uint32),
+            ret_pin=_arr(o.ret_pin, o.n_retention, np.uint8),
+            ret_benefit=_arr(o.ret_benefit, o.n_retention, np.float64),
+            ret_cost=_arr(o.ret_cost, o.n_retention, np.float64),
+            ret_deadline=_arr(o.ret_deadline, o.n_retention, np.float64),
+            n_ready=o.n_ready, n_promoted=o.n_promoted, pack_mode=o.pack_mode,
+            total_tokens=o.total_tokens, free_after_expiry=o.free_after_expiry,
+            free_blocks=o.free_blocks, limit=o.limit, slots=o.slots)
+
+    def step(self, si: N.MarsStepIn) -> StepResult:
+        self.enqueue(si)
+        return self.fetch()
+
+    def retention_batch(self, context: np.ndarray, kv: np.ndarray, total_blocks: int,
+                        usage: float, ema: float, now: float):
+        ctx = np.ascontiguousarray(context, dtype=np.int32)
+        kvv = np.ascontiguousarray(kv, dtype=np.int32)
+        n = len(ctx)
+        pin = np.zeros(n, np.uint8)
+        b, c, d = (np.zeros(n, np.float64) for _ in range(3))
+        self._check(self.lib.mars_retention_batch(
+            self.ctx, n, ctx.ctypes.data_as(C.c_void_p), kvv.ctypes.data_as(C.c_void_p),
+            int(total_blocks), float(usage), float(ema), float(now),
+            pin.ctypes.data_as(C.c_void_p), b.ctypes.data_as(C.c_void_p),
+            c.ctypes.data_as(C.c_void_p), d.ctypes.data_as(C.c_void_p)))
+        return pin.astype(bool), b, c, d
+
+    def checkpoint(self) -> None:
+        self._check(self.lib.mars_checkpoint(self.ctx))
+
+    def restore(self) -> None:
+        self._check(self.lib.mars_restore(self.ctx))
+
+    def flush_l2(self, nbytes: int) -> None:
+        self._check(self.lib.mars_flush_l2(self.ctx, int(nbytes)))
+
+    def launches(self) -> int:
+        return int(self.lib.mars_last_launch_count(self.ctx))
+
+
+def canonical(res: StepResult, eng: MarsEngine, snap: Snapshot, control_due: bool = True) -> dict:
+    """Device step result in the oracle's canonical layout (oracle/snapshot_step.py)."""
+    sc = eng.get_scalars()
+    kinds = {0: "running", 1: "pinned"}
+    exp = [(int(r), int(b)) for r, b in zip(res.expired_rows, res.expired_blocks)]
+    out = dict(
+        expired=exp,
+        expiry_journal=[("free", r, b, True) for r, b in exp],
+        probe=dict(available_kv=int(res.free_after_expiry), usage=float(sc.kv_usage_ratio),
+                   active_sessions=int(sc.active_sessions)),
+        control=None,
+        retention=[],
+        window=[int(x) for x in res.window_rows],
+        decodes=[int(x) for x in res.decode_rows],
+        prefills=[(int(r), int(g)) for r, g in zip(res.prefill_rows, res.prefill_grants)],
+        evictions=[(int(r), kinds[int(k)], int(b))
+                   for r, k, b in zip(res.evict_rows, res.evict_kind, res.evict_blocks)],
+        total_tokens=int(res.total_tokens),
+        journal=[(JOURNAL_NAMES[int(o)], int(r), int(n), int(o) == 3)
+                 for o, r, n in zip(res.journal_op, res.journal_row, res.journal_n)],
+        free_blocks=int(res.free_blocks),
+        n_ready=int(res.n_ready) + len(res.admitted_rows),
+    )
+    if control_due:
+        out["control"] = dict(
+            w_adm=float(sc.w_adm), last_update=float(sc.last_update), limit=int(res.limit),
+            slots=int(res.slots), admitted=[int(x) for x in res.admitted_rows],
+            queue=[int(x) for x in eng.get_queue()],
+            cpu_overloaded=bool(sc.cpu_overloaded), kv_overloaded=bool(sc.kv_overloaded),
+            streaks=(int(sc.cpu_high_streak), int(sc.cpu_low_streak), int(sc.kv_high_streak),
+                     int(sc.kv_low_streak)),
+            blocks_seed=(float(sc.blocks_seed) if sc.has_blocks_seed else None),
+            available_kv=int(sc.available_kv))
+    order = np.argsort(res.ret_rows, kind="stable")
+    out["retention"] = [(int(res.ret_rows[i]), bool(res.ret_pin[i]), float(res.ret_benefit[i]),
+                         float(res.ret_cost[i]), float(res.ret_deadline[i])) for i in order]
+    st = eng.read(["phase", "flags", "level", "promos", "wait_since", "ready_since", "context",
+                   "kv", "rem_decode", "preempt", "served"])
+    out["state"] = st
+    return out

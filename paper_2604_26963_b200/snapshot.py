@@ -58,6 +58,10 @@ class Snapshot:
     ema_tool: Optional[float] = 5.0
     ema_blocks: Optional[float] = None
     blocks_seed: Optional[float] = None
+    # initial Telemetry hysteresis state (telemetry.py:80-91): any of
+    # cpu_overloaded, kv_overloaded, cpu_high_streak, cpu_low_streak,
+    # kv_high_streak, kv_low_streak
+    telemetry: dict = field(default_factory=dict)
     meta: dict = field(default_factory=dict)
 
     @property
@@ -72,6 +76,7 @@ class Snapshot:
         s.cols = {k: v.copy() for k, v in self.cols.items()}
         s.queue = self.queue.copy()
         s.meta = dict(self.meta)
+        s.telemetry = dict(self.telemetry)
         return s
 
 

@@ -1,0 +1,113 @@
+"""Parity of the B200 step (through the C ABI) with the reference.
+
+* small snapshots: against outputs frozen from the reference itself
+  (tests/golden/snapshot_steps.json);
+* up to 1M sessions: against the CPU oracle on the same seeded inputs,
+  every decision bit-exact (window, plan, evictions, journal, expiry order,
+  admitted set + residual queue order, retention f64 values) plus the full
+  post-step session table.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle.snapshot_step import run_step
+from paper_2604_26963_b200.engine import MarsEngine, canonical, make_config
+from paper_2604_26963_b200.snapshot import snapshot_v1
+from tests._canon import canon
+from tests._variants import variant
+from tests.conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+SNAP = json.load(open(os.path.join(GOLDEN, "snapshot_steps.json")))
+
+
+def device_step(snap, control_due=True, **flags):
+    eng = MarsEngine(max_rows=snap.n, max_queue=max(len(snap.queue), 1),
+                     config=make_config(**flags, initial_window=snap.initial_window))
+    eng.load_snapshot(snap)
+    si = eng.step_in(snap.now, control_due, snap.active_tools, snap.queued_tools,
+                     snap.worker_slots)
+    res = eng.step(si)
+    out = canonical(res, eng, snap, control_due)
+    eng.close()
+    assert res.status == 0, res.status
+    return out
+
+
+def assert_same(got, want):
+    g, w = canon(got), canon(want)
+    for k in w:
+        if g[k] != w[k]:
+            gs, ws = json.dumps(g[k]), json.dumps(w[k])
+            raise AssertionError(f"{k} differs:\n device {gs[:600]}\n oracle {ws[:600]}")
+
+
+@pytest.mark.parametrize("i", range(len(SNAP)))
+def test_step_matches_reference_golden(i):
+    case = dict(SNAP[i]["case"])
+    kw = {k: case.pop(k) for k in ("enable_coordinator", "enable_coscheduler") if k in case}
+    snap = snapshot_v1(case["n"], seed=case["seed"], pool=case["pool"])
+    got = canon(device_step(snap, **kw))
+    for k, v in SNAP[i]["out"].items():
+        assert got[k] == v, k
+
+
+@pytest.mark.parametrize("n,seed,kind", [
+    (100_000, 21, "headroom"),
+    (100_000, 22, "pressure"),
+    (30_000, 23, "first_fit"),
+    (30_000, 24, "desc"),
+    (150_000, 25, "expired_big"),
+    (20_000, 26, "no_queue_control"),
+])
+def test_step_matches_oracle(n, seed, kind):
+    snap = variant(n, seed, kind)
+    assert_same(device_step(snap.copy()), run_step(snap.copy()))
+
+
+@pytest.mark.parametrize("flags", [dict(enable_coordinator=False), dict(enable_coscheduler=False)])
+def test_ablations_match_oracle(flags):
+    snap = snapshot_v1(40_000, seed=31, pool="pressure")
+    assert_same(device_step(snap.copy(), **flags), run_step(snap.copy(), **flags))
+
+
+def test_step_without_control_matches_oracle():
+    snap = snapshot_v1(50_000, seed=32, pool="pressure")
+    assert_same(device_step(snap.copy(), control_due=False),
+                run_step(snap.copy(), control_due=False))
+
+
+def test_one_million_sessions_match_oracle():
+    snap = snapshot_v1(1_000_000, seed=0, pool="headroom")
+    assert_same(device_step(snap.copy()), run_step(snap.copy()))
+
+
+def test_restore_replays_identically():
+    snap = snapshot_v1(60_000, seed=41, pool="pressure")
+    eng = MarsEngine(max_rows=snap.n, max_queue=len(snap.queue),
+                     config=make_config(initial_window=snap.initial_window))
+    eng.load_snapshot(snap)
+    eng.checkpoint()
+    si = eng.step_in(snap.now, True, snap.active_tools, 0, snap.worker_slots)
+    a = canon(canonical(eng.step(si), eng, snap))
+    eng.restore()
+    b = canon(canonical(eng.step(si), eng, snap))
+    eng.close()
+    assert a == b
+
+
+def test_retention_batch_matches_reference_kat():
+    kat = json.load(open(os.path.join(GOLDEN, "kat.json")))["retention"]
+    eng = MarsEngine(max_rows=16, max_queue=1)
+    for r in kat:
+        ema = r["ema"] if r["ema"] is not None else 5.0
+        pin, b, c, d = eng.retention_batch(np.array([r["ctx"]]), np.array([r["kv"]]), r["total"],
+                                           r["usage"], ema, r["now"])
+        assert (bool(pin[0]), float(b[0]), float(c[0]), float(d[0])) == (
+            r["pin"], r["benefit"], r["cost"], r["deadline"])
+    eng.close()
