@@ -1,0 +1,349 @@
+"""Benchmark: one MARS scheduling step over a 1M-session table per GPU.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--sessions S] [--impl reference]
+
+A *step* is one full pass of the hot path over the device-resident session
+table (snapshot_v1, mix A, headroom pool): pin expiry, telemetry probe,
+control-plane admission (refresh_pressure, pack_queue, AIMD window, admit),
+MLFQ aging, window top-128, the build_plan walk with chunk fitting and
+reclamation, and S2 retention for the boundary rows.  Every timed step starts
+from the same snapshot (device-side restore, untimed) with L2 flushed, so each
+step repeats the identical decisions.
+
+Multi-GPU (torchrun): data-parallel engine replicas, each rank owns its own
+1M-session shard (weak scaling); time = max over ranks.
+
+``--impl reference`` times the reference CPU path (the oracle port of
+agentsched, single-threaded CPython) on the same workload and prints the same
+JSON line with "impl": "reference".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sched steps/s & sessions/s at 1M sessions; KV evict/restore GB/s"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d.get("hbm_gbs", FALLBACK_HBM_GBS)), "measured"
+    return FALLBACK_HBM_GBS, "fallback"
+
+
+def _ncu_traffic():
+    p = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return d.get("k_scan", {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.fh, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self):
+        if self.proc is None or not os.path.exists(self.path):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def scan_bytes(snap) -> int:
+    """Algorithmic bytes of one k_scan launch: phase+flags for
+    every row; level, promos, wait_since, ready_since, kv for ready rows; the
+    promotion write-back; deadline/pinned_blocks/plevel for pinned rows;
+    req_blocks for queued rows; the expiry write-back + expired list."""
+    import numpy as np
+
+    from paper_2604_26963_b200.snapshot import DECODE, F_PINNED, F_QUEUED, PREFILL
+
+    c = snap.cols
+    ready = (c["phase"] == DECODE) | (c["phase"] == PREFILL)
+    pinned = (c["flags"] & F_PINNED) != 0
+    queued = (c["flags"] & F_QUEUED) != 0
+    now = snap.now
+    promo = ready & (c["level"] > 0) & (c["promos"] < 3) & (now - c["wait_since"] >= 10.0)
+    expired = pinned & (c["deadline"] < now)
+    return int(2 * snap.n + 22 * ready.sum() + 10 * promo.sum() + 13 * pinned.sum()
+               + 4 * queued.sum() + 17 * expired.sum())
+
+
+def step_bytes(snap) -> int:
+    """Whole-step algorithmic bytes, SURVEY.md §8(d) accounting."""
+    from paper_2604_26963_b200.snapshot import DECODE, F_BOUNDARY, F_PINNED, F_QUEUED, PREFILL
+
+    c = snap.cols
+    ready = (c["phase"] == DECODE) | (c["phase"] == PREFILL)
+    now = snap.now
+    promo = ready & (c["level"] > 0) & (c["promos"] < 3) & (now - c["wait_since"] >= 10.0)
+    return int(snap.n * 1 + ready.sum() * 18 + promo.sum() * 10
+               + ((c["flags"] & F_PINNED) != 0).sum() * 8
+               + ((c["flags"] & F_BOUNDARY) != 0).sum() * 17
+               + ((c["flags"] & F_QUEUED) != 0).sum() * 13)
+
+
+def cpu_reference(sessions: int, seed: int, reps: int = 1):
+    """Times the oracle port's full step (materialisation excluded)."""
+    from oracle.snapshot_step import World, run_step
+    from paper_2604_26963_b200.snapshot import snapshot_v1
+
+    times = []
+    for r in range(reps):
+        snap = snapshot_v1(sessions, seed=seed + r, pool="headroom")
+        w = World(snap)
+        t0 = time.perf_counter()
+        run_step(snap, world=w)
+        times.append(time.perf_counter() - t0)
+        del w
+    return times
+
+
+def run_reference_arm(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    n = a.ref_sample
+    times = []
+    for i in range(a.warmup + a.steps):
+        t = cpu_reference(n, seed=100 + i)[0]
+        if i >= a.warmup:
+            times.append(t)
+    per = sum(times) / len(times)
+    val = n / per
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "sessions/s",
+        "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": per * 1e3,
+        "steps_per_s": 1.0 / per, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64+i64", "data": "synthetic (snapshot_v1, mix A)",
+        "config": {"workload": "one MARS scheduling step (expiry, probe, admission, aging, "
+                               "window top-128, build_plan walk, S2 retention)",
+                   "sessions": a.sessions, "pool": "headroom", "parallelism": "replicas"},
+        "cpu_baseline": {"value": val, "unit": "sessions/s", "cores": 1, "kind": "port",
+                         "sample": f"one full step over a {n}-session snapshot_v1 (fresh seed per "
+                                   "step), object-level CPython restatement of agentsched "
+                                   "(oracle/), materialisation excluded"},
+        "e2e": {"value": val, "unit": "sessions/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--sessions", type=int, default=1_000_000)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--ref-sample", type=int, default=100_000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--flush-mb", type=int, default=512)
+    a = ap.parse_args()
+    if a.impl == "reference":
+        return run_reference_arm(a)
+
+    import numpy as np
+    import torch
+
+    from paper_2604_26963_b200.engine import MarsEngine, make_config
+    from paper_2604_26963_b200.snapshot import snapshot_v1
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    snap = snapshot_v1(a.sessions, seed=rank, pool="headroom")
+    eng = MarsEngine(max_rows=snap.n, max_queue=max(len(snap.queue), 1), device=local,
+                     config=make_config(initial_window=snap.initial_window))
+    stream = torch.cuda.current_stream()
+    eng.lib.mars_set_stream(eng.ctx, stream.cuda_stream)
+    eng.load_snapshot(snap)
+    eng.checkpoint()
+    si = eng.step_in(snap.now, True, snap.active_tools, snap.queued_tools, snap.worker_slots)
+    flush = a.flush_mb << 20
+
+    # correctness guard: one fetched step must succeed with status 0
+    res = eng.step(si)
+    if res.status != 0:
+        raise SystemExit(f"device step status {res.status}")
+    eng.restore()
+
+    for _ in range(a.warmup):
+        eng.enqueue(si)
+        eng.restore()
+    barrier()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+    launches = 0
+    ktimes = []
+    # per-kernel CUDA events inside the library (same streams as the kernels)
+    eng.set_profiling(True)
+    with Clocks(local) as clk:
+        barrier()
+        for i in range(a.steps):
+            eng.restore()
+            eng.flush_l2(flush)
+            starts[i].record(stream)
+            eng.enqueue(si)
+            ends[i].record(stream)
+            launches += eng.launches()
+            ktimes.append(eng.kernel_times())  # syncs after the step (outside the events)
+        barrier()
+    eng.set_profiling(False)
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    dev_ms = sum(step_ms)
+    t = torch.tensor([dev_ms], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_per_step = float(t.item()) / a.steps
+    kernel_ms = {k: statistics.median([kt[k] for kt in ktimes]) for k in ktimes[0]}
+    scan_avg = sum(kt["k_scan"] for kt in ktimes) / len(ktimes)
+
+    # e2e: through the C ABI with host buffers: upload the table from pinned
+    # host memory, run the step, fetch the plan/journal/decisions to the host
+    pinned = {k: torch.from_numpy(v).pin_memory().numpy() for k, v in snap.cols.items()}
+    h2d = sum(v.nbytes for v in pinned.values())
+    e2e_t = []
+    d2h = 0
+    for i in range(a.e2e_steps + 1):
+        eng.restore()
+        eng.flush_l2(flush)
+        barrier()
+        t0 = time.perf_counter()
+        eng.upsert(pinned)
+        r = eng.step(si)
+        t1 = time.perf_counter()
+        if i > 0:
+            e2e_t.append(t1 - t0)
+        d2h = (r.expired_rows.nbytes * 2 + r.admitted_rows.nbytes + r.window_rows.nbytes
+               + r.decode_rows.nbytes + r.prefill_rows.nbytes * 2 + r.evict_rows.nbytes * 3
+               + r.journal_row.nbytes * 3 + r.ret_rows.nbytes * 7 + 4096)
+    e2e_s = statistics.median(e2e_t)
+    te = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_s = float(te.item())
+
+    peak, peak_kind = _peaks()
+    sb = scan_bytes(snap)
+    achieved = sb / (scan_avg * 1e-3) / 1e9
+    total_sessions = a.sessions * world
+    steps_per_s = 1e3 / ms_per_step
+    value = total_sessions * steps_per_s
+    line = {
+        "metric": METRIC, "value": value, "unit": "sessions/s", "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_per_step,
+        "steps_per_s": steps_per_s, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64+i64", "data": "synthetic (snapshot_v1 mix A, seed=rank)",
+        "config": {"workload": "one MARS scheduling step (expiry, probe, control-plane admission, "
+                               "aging, window top-128, build_plan walk, S2 retention) per replica",
+                   "sessions_per_gpu": a.sessions, "pool": "headroom",
+                   "parallelism": f"replicas x{world}",
+                   "l2": f"flushed before every timed step ({a.flush_mb} MiB scratch write); "
+                         "state restored from a device checkpoint (untimed)"},
+        "roofline": {"bound": "hbm", "kernel": "k_scan", "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": _ncu_traffic(),
+                     "algorithmic_bytes": sb, "kernel_ms": scan_avg, "peak_source": peak_kind,
+                     "step_algorithmic_bytes": step_bytes(snap),
+                     "step_frac": step_bytes(snap) / (ms_per_step * 1e-3) / 1e9 / peak},
+        "e2e": {"value": total_sessions / e2e_s, "unit": "sessions/s",
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "ms_per_step": e2e_s * 1e3},
+        "gpu_launches": launches,
+        "kernel_ms_median": kernel_ms,
+        "clocks": clk.summary(),
+        "step_ms_min": min(step_ms), "step_ms_max": max(step_ms),
+    }
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        t_cpu = cpu_reference(a.sessions, seed=0)[0]
+        line["cpu_baseline"] = {
+            "value": a.sessions / t_cpu, "unit": "sessions/s", "cores": 1, "kind": "port",
+            "sample": f"one full step over snapshot_v1({a.sessions}) on the oracle "
+                      "(object-level CPython restatement of agentsched), materialisation excluded",
+            "seconds": t_cpu}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -201,6 +201,13 @@ int mars_flush_l2(mars_ctx* ctx, int64_t bytes);
 /* number of kernel launches issued by the last step (incl. early-exit ones) */
 int mars_last_launch_count(mars_ctx* ctx);
 
+/* per-kernel device times of the last step, recorded with CUDA events on the
+ * stream each kernel runs on: [scan, compact, expired-sort, pack, admit, walk]
+ * in ms (-1 = not launched).  Profiling must be enabled before the step. */
+#define MARS_NUM_KTIMES 6
+int mars_set_profiling(mars_ctx* ctx, int on);
+int mars_kernel_times(mars_ctx* ctx, float* ms, int n);   /* sync */
+
 #ifdef __cplusplus
 }
 #endif

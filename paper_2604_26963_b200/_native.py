@@ -114,7 +114,11 @@ _SIGS = {
     "mars_restore": (i32, [C.c_void_p]),
     "mars_flush_l2": (i32, [C.c_void_p, i64]),
     "mars_last_launch_count": (i32, [C.c_void_p]),
+    "mars_set_profiling": (i32, [C.c_void_p, C.c_int]),
+    "mars_kernel_times": (i32, [C.c_void_p, P(C.c_float), C.c_int]),
 }
+
+KTIME_NAMES = ("k_scan", "k_compact", "k_expired_sort", "k_pack", "k_admit_apply", "k_walk")
 
 EXPORTS = tuple(_SIGS)
 

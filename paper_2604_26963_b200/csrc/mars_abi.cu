@@ -60,6 +60,9 @@ struct mars_ctx {
   int q_maxreq = 0;
   i64 pinned_upper = 0;
   int last_launches = 0;
+  bool profiling = false;
+  cudaEvent_t prof[2 * MARS_NUM_KTIMES] = {};
+  int prof_used[MARS_NUM_KTIMES] = {};
   unsigned flush_salt = 1;
   std::string err;
 };
@@ -368,6 +371,8 @@ int mars_destroy(mars_ctx* ctx) {
   cudaFreeHost(ctx->h_work);
   cudaFreeHost(ctx->h_sc);
   cudaFreeHost(ctx->h_out);
+  for (auto& e : ctx->prof)
+    if (e) cudaEventDestroy(e);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -541,6 +546,8 @@ static LaunchArgs launch_args(mars_ctx* ctx, const mars_step_in* in) {
   }
   a.queue_passes = passes;
   a.exp_may_be_big = (in->skip_expiry == 0 && ctx->n_rows > SORT_CAP) ? 1 : 0;
+  a.prof = ctx->profiling ? ctx->prof : nullptr;
+  a.prof_used = ctx->prof_used;
   return a;
 }
 
@@ -697,6 +704,29 @@ int mars_restore(mars_ctx* ctx) {
   CK(cudaMemcpyAsync(ctx->qsel, ctx->ck_qsel, sizeof(i32), cudaMemcpyDeviceToDevice, ctx->stream));
   ctx->q_upper = ctx->ck_q_upper;
   ctx->q_maxreq = ctx->ck_q_maxreq;
+  return MARS_OK;
+}
+
+int mars_set_profiling(mars_ctx* ctx, int on) {
+  if (!ctx) return MARS_ERR_ARG;
+  CK(cudaSetDevice(ctx->device));
+  if (on && !ctx->prof[0])
+    for (auto& e : ctx->prof) CK(cudaEventCreate(&e));
+  ctx->profiling = on != 0;
+  return MARS_OK;
+}
+
+int mars_kernel_times(mars_ctx* ctx, float* ms, int n) {
+  if (!ctx || !ms) return MARS_ERR_ARG;
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(ctx->stream));
+  for (int k = 0; k < n && k < MARS_NUM_KTIMES; ++k) {
+    ms[k] = -1.0f;
+    if (ctx->profiling && ctx->prof_used[k]) {
+      float t = 0;
+      if (cudaEventElapsedTime(&t, ctx->prof[2 * k], ctx->prof[2 * k + 1]) == cudaSuccess) ms[k] = t;
+    }
+  }
   return MARS_OK;
 }
 

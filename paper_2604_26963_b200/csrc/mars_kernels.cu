@@ -1740,8 +1740,14 @@ int mars_kernels_init() {
 int mars_enqueue_step(const LaunchArgs* a) {
   cudaStream_t s = a->stream, s2 = a->side;
   int launches = 0;
+  auto mark = [&](int k, int end, cudaStream_t st) {
+    if (!a->prof) return;
+    cudaEventRecord(a->prof[2 * k + end], st);
+    if (end) a->prof_used[k] = 1;
+  };
+  if (a->prof)
+    for (int k = 0; k < MARS_NUM_KTIMES; ++k) a->prof_used[k] = 0;
   cudaMemsetAsync(a->work, 0, sizeof(Work), s);
-  // tmin = max, min_req = max
   cudaMemcpyAsync(a->work, a->host_in, sizeof(mars_step_in), cudaMemcpyHostToDevice, s);
   k_work_init<<<1, 32, 0, s>>>(a->work);
   launches++;
@@ -1750,15 +1756,20 @@ int mars_enqueue_step(const LaunchArgs* a) {
   int g_scan = (int)((n + 2047) / 2048);
   if (g_scan > 2 * nsm) g_scan = 2 * nsm;
   if (g_scan < 1) g_scan = 1;
+  mark(0, 0, s);
   k_scan<<<g_scan, SCAN_TPB, 0, s>>>(a->tab, a->cfg, a->work, a->bufs, a->sc, n);
+  mark(0, 1, s);
   launches++;
   cudaEventRecord(a->ev_fork, s);
   cudaStreamWaitEvent(s2, a->ev_fork, 0);
   int g_c = (int)((n + SCAN_TPB - 1) / SCAN_TPB);
   if (g_c > 4 * nsm) g_c = 4 * nsm;
   if (g_c < 1) g_c = 1;
+  mark(1, 0, s2);
   k_compact<<<g_c, SCAN_TPB, 0, s2>>>(a->tab, a->cfg, a->work, a->bufs, a->sc, n);
+  mark(1, 1, s2);
   launches++;
+  mark(2, 0, s2);
   k_exp_small<<<1, 1024, sort_smem_bytes(), s2>>>(a->work, a->bufs, a->xlsd);
   launches++;
   if (a->exp_may_be_big) {
@@ -1771,8 +1782,10 @@ int mars_enqueue_step(const LaunchArgs* a) {
     k_exp_gather<<<nsm, 256, 0, s2>>>(a->work, a->bufs, a->xlsd);
     launches++;
   }
+  mark(2, 1, s2);
   cudaEventRecord(a->ev_join, s2);
   if (a->control_possible) {
+    mark(3, 0, s);
     k_pack_small<<<1, 1024, sort_smem_bytes(), s>>>(a->work, a->queue, a->qlsd, a->sc, a->qsel);
     launches++;
     for (int p = 0; p < a->queue_passes; ++p) {
@@ -1781,17 +1794,22 @@ int mars_enqueue_step(const LaunchArgs* a) {
       k_lsd_scatter<<<LSD_G, 256, 0, s>>>(a->qlsd, a->work, 0, p);
       launches += 3;
     }
+    mark(3, 1, s);
   }
   cudaStreamWaitEvent(s, a->ev_join, 0);
   if (a->control_possible) {
     int g_ap = (int)((a->queue_upper + SCAN_TPB - 1) / SCAN_TPB);
     if (g_ap > 2 * nsm) g_ap = 2 * nsm;
     if (g_ap < 1) g_ap = 1;
+    mark(4, 0, s);
     k_admit_apply<<<g_ap, SCAN_TPB, 0, s>>>(a->tab, a->cfg, a->work, a->bufs, a->queue, a->qlsd,
                                             a->sc, a->qsel);
+    mark(4, 1, s);
     launches++;
   }
+  mark(5, 0, s);
   k_walk<<<1, WALK_TPB, walk_smem_bytes(), s>>>(a->tab, a->cfg, a->work, a->bufs, a->sc, n);
+  mark(5, 1, s);
   launches++;
   return launches;
 }

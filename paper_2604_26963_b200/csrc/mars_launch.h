@@ -21,6 +21,8 @@ struct LaunchArgs {
   int queue_passes;      // LSD passes needed for the largest queue key (0 = small only)
   i64 queue_upper;       // upper bound of the queue length at step start
   int exp_may_be_big;    // more than SORT_CAP pins may expire
+  cudaEvent_t* prof;     // 2*MARS_NUM_KTIMES events, or null
+  int* prof_used;        // which pairs were recorded
 };
 
 int mars_kernels_init();

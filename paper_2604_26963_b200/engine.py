@@ -276,6 +276,14 @@ class MarsEngine:
     def flush_l2(self, nbytes: int) -> None:
         self._check(self.lib.mars_flush_l2(self.ctx, int(nbytes)))
 
+    def set_profiling(self, on: bool) -> None:
+        self._check(self.lib.mars_set_profiling(self.ctx, int(bool(on))))
+
+    def kernel_times(self) -> Dict[str, float]:
+        ms = (C.c_float * 6)()
+        self._check(self.lib.mars_kernel_times(self.ctx, ms, 6))
+        return {k: float(v) for k, v in zip(N.KTIME_NAMES, ms)}
+
     def launches(self) -> int:
         return int(self.lib.mars_last_launch_count(self.ctx))
 
