@@ -231,8 +231,12 @@ def main():
     snap = snapshot_v1(a.sessions, seed=rank, pool="headroom")
     eng = MarsEngine(max_rows=snap.n, max_queue=max(len(snap.queue), 1), device=local,
                      config=make_config(initial_window=snap.initial_window))
-    stream = torch.cuda.current_stream()
+    # a dedicated (non-default) stream: the step is captured as a CUDA graph and
+    # the timing events are recorded on the stream the kernels run on
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     eng.lib.mars_set_stream(eng.ctx, stream.cuda_stream)
+    eng.set_graph(True)  # the whole step is one CUDA graph launch
     eng.load_snapshot(snap)
     eng.checkpoint()
     si = eng.step_in(snap.now, True, snap.active_tools, snap.queued_tools, snap.worker_slots)

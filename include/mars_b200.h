@@ -127,13 +127,27 @@ typedef struct mars_scalars {
   int64_t queue_len;
 } mars_scalars;
 
+/* mars_step_in.mode bits.  0 = the device-resident engine step.  The
+ * reference-plugin drop-in (policy.py / admission.py) lets the reference's
+ * own tick loop do what it does itself and asks the device only for the rest. */
+#define MARS_MODE_SKIP_EXPIRY 1       /* the caller evicts expired pins (sim.py:324-325) */
+#define MARS_MODE_SKIP_PROBE 2        /* telemetry scalars come from mars_set_scalars */
+#define MARS_MODE_SKIP_REFRESH 4      /* refresh_pressure already ran (sim.py:330) */
+#define MARS_MODE_NO_ROWS 8           /* admission only: queue entries have no table rows */
+#define MARS_MODE_SERVICE 16          /* charge_service at tick end for planned rows
+                                         (baselines.py:362-367, sim.py:364) */
+#define MARS_MODE_FINISH_RETENTION 32 /* decide_retention for decodes finishing their round
+                                         this tick, on post-tick values (sim.py:250) */
+#define MARS_MODE_RANK_ORDERED 64     /* caller asserts rank[row] == row order (row order is
+                                         session-id order): expired pins need no sort */
+
 typedef struct mars_step_in {
   double now;
   int32_t control_due;     /* sim.py:329: run refresh_pressure + balance_and_admit */
   int32_t active_tools;    /* ToolPlane.active_count() at the probe (sim.py:327) */
   int32_t queued_tools;    /* ToolPlane.queued_count() */
   int32_t worker_slots;    /* ToolPlane.worker_slots */
-  int32_t skip_expiry;     /* drop-in mode: the sim evicts expired pins itself */
+  int32_t mode;            /* MARS_MODE_* bits */
 } mars_step_in;
 
 /* Step result.  Pointers refer to pinned host buffers owned by the context,
@@ -154,6 +168,12 @@ typedef struct mars_step_out {
   const uint8_t *journal_op; const uint32_t *journal_row; const int32_t *journal_n;
   const uint32_t *ret_rows; const uint8_t *ret_pin;
   const double *ret_benefit, *ret_cost, *ret_deadline;
+  /* MARS_MODE_SERVICE: MLFQ level of each planned row after its charge */
+  const uint8_t *decode_level, *prefill_level;
+  /* MARS_MODE_FINISH_RETENTION: decode rows with remaining_decode == 1 */
+  int32_t n_finish;
+  const uint32_t *fin_rows; const uint8_t *fin_pin;
+  const double *fin_benefit, *fin_cost, *fin_deadline;
 } mars_step_out;
 
 /* ---- lifecycle ------------------------------------------------------- */
@@ -184,6 +204,9 @@ int mars_get_scalars(mars_ctx* ctx, mars_scalars* s);                           
 int mars_step(mars_ctx* ctx, const mars_step_in* in, mars_step_out* out);          /* sync */
 int mars_step_enqueue(mars_ctx* ctx, const mars_step_in* in);   /* async, device-resident */
 int mars_step_fetch(mars_ctx* ctx, mars_step_out* out);          /* sync, after enqueue */
+/* capture the whole step (both streams) as one CUDA graph; re-captured only
+ * when the launch shape (rows, queue bucket, mode) changes */
+int mars_set_graph(mars_ctx* ctx, int on);
 
 /* decide_retention (scheduler.py:190-213) for explicit inputs; elementwise f64
  * on the device, bit-exact (no FMA contraction). */
@@ -197,6 +220,43 @@ int mars_checkpoint(mars_ctx* ctx);
 int mars_restore(mars_ctx* ctx);
 /* write `bytes` of scratch to evict L2 between timed steps */
 int mars_flush_l2(mars_ctx* ctx, int64_t bytes);
+
+/* ---- S5: paged KV block manager + HBM <-> pinned-host tier ----------------
+ * Block IDs follow the LIFO policy written down in oracle/block_ids.py (the
+ * reference KvPool counts only: engine.py:116-221).  Once enabled, every
+ * mars_step also applies its own journal (expired pins in rank order, then
+ * the plan's alloc/evict ops) to the block tables; mars_kv_apply replays any
+ * other pool op stream (the KvPool.observer callbacks, engine.py:129-143). */
+#define MARS_KV_ALLOC 1     /* pop n IDs onto the row's table */
+#define MARS_KV_FREE 2      /* push the last n IDs back (n = -1: the whole table) */
+#define MARS_KV_PIN 3       /* ownership only (no table change) */
+#define MARS_KV_UNPIN 4
+
+typedef struct mars_kv_config {
+  int64_t total_blocks;        /* KvPool.total_blocks */
+  int32_t max_blocks_per_row;  /* table capacity per session */
+  int64_t block_bytes;         /* KV bytes per block (0 = block IDs only, no data) */
+  int32_t layers;              /* >1: layer-major device layout, `layers` pieces per block */
+  int64_t host_blocks;         /* pinned host-tier capacity in blocks */
+} mars_kv_config;
+
+int mars_kv_init(mars_ctx* ctx, const mars_kv_config* cfg);
+int mars_kv_apply(mars_ctx* ctx, int64_t n_ops, const uint8_t* op, const uint32_t* row,
+                  const int32_t* n);                                              /* sync */
+int mars_kv_table(mars_ctx* ctx, uint32_t row, int64_t cap, uint32_t* ids, int64_t* n); /* sync */
+/* next `k` IDs the stack would pop, plus its depth (explicit, fresh) */
+int mars_kv_state(mars_ctx* ctx, int64_t k, uint32_t* top_ids, int64_t* explicit_depth,
+                  int64_t* fresh, int32_t* status);                               /* sync */
+/* evict (HBM -> host slots [slot0, slot0+n)) / restore (host -> HBM) block data.
+ * method 0: copy engines (one cudaMemcpyAsync per block piece),
+ * method 1: SM-driven zero-copy kernel over mapped pinned memory. */
+int mars_kv_evict(mars_ctx* ctx, int64_t n, const uint32_t* block_ids, int64_t slot0, int method);
+int mars_kv_restore(mars_ctx* ctx, int64_t n, const uint32_t* block_ids, int64_t slot0,
+                    int method);
+int mars_kv_host_ptr(mars_ctx* ctx, void** host, void** device);
+/* pinned cudaMemcpyAsync peak of the host link: best of `reps` per direction */
+int mars_host_link_peak(mars_ctx* ctx, int64_t bytes, int reps, double* d2h_gbs, double* h2d_gbs,
+                        double* bidir_gbs);
 
 /* number of kernel launches issued by the last step (incl. early-exit ones) */
 int mars_last_launch_count(mars_ctx* ctx);

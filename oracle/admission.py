@@ -180,6 +180,11 @@ class Controller:
         self.w_adm = float(initial_window)
         self.last_update = 0.0
 
+    @property
+    def config(self) -> "Controller":
+        """ControllerState.config (control.py:56): the same object here."""
+        return self
+
 
 class Pending:
     """A queue entry (control.py:64-73)."""

@@ -66,9 +66,13 @@ class _Empty:
 def run(traces: Sequence[Trace], eng: Engine, policy, controller: Optional[adm.Controller] = None,
         pressure: Optional[adm.Pressure] = None, enable_control_plane: bool = True,
         max_ticks: int = MAX_TICKS, session_factory=Session, round_factory=Round,
-        on_tick=None) -> RunOut:
+        on_tick=None, balance_and_admit=None) -> RunOut:
     """One deterministic run.  ``policy`` is any object with the PolicyBase
-    hooks (baselines.py:56-101)."""
+    hooks (baselines.py:56-101); ``balance_and_admit`` any function with the
+    reference signature (control.py:166-174), default the oracle's."""
+    if balance_and_admit is None:
+        def balance_and_admit(q, st, tel, slots, p, clk, lg):
+            return adm.admit_step(q, st, tel, slots, p, clk.now, lg)
     ctl = controller or adm.Controller()
     prs = pressure or adm.Pressure()
     gpu = eng.gpu()
@@ -233,7 +237,7 @@ def run(traces: Sequence[Trace], eng: Engine, policy, controller: Optional[adm.C
         if admission and now >= next_control - 1e-9:
             adm.refresh_pressure(tel, prs, tools.worker_slots)
             log.emit(now, "telemetry", None, **tel.snapshot())
-            for e in adm.admit_step(queue, ctl, tel, tools.worker_slots, prs, now, log):
+            for e in balance_and_admit(queue, ctl, tel, tools.worker_slots, prs, clock, log):
                 admit(e.call, now)
             next_control = now + ctl.control_interval_s
         ready = [c for c in active.values() if c.phase in (PREFILL, DECODE)]

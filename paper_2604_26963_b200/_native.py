@@ -70,9 +70,21 @@ class MarsScalars(C.Structure):
     ]
 
 
+class MarsKvConfig(C.Structure):
+    _fields_ = [("total_blocks", i64), ("max_blocks_per_row", i32), ("block_bytes", i64),
+                ("layers", i32), ("host_blocks", i64)]
+
+
+KV_ALLOC, KV_FREE, KV_PIN, KV_UNPIN = 1, 2, 3, 4
+
+
 class MarsStepIn(C.Structure):
     _fields_ = [("now", f64), ("control_due", i32), ("active_tools", i32),
-                ("queued_tools", i32), ("worker_slots", i32), ("skip_expiry", i32)]
+                ("queued_tools", i32), ("worker_slots", i32), ("mode", i32)]
+
+
+MODE_SKIP_EXPIRY, MODE_SKIP_PROBE, MODE_SKIP_REFRESH, MODE_NO_ROWS = 1, 2, 4, 8
+MODE_SERVICE, MODE_FINISH_RETENTION, MODE_RANK_ORDERED = 16, 32, 64
 
 
 class MarsStepOut(C.Structure):
@@ -88,6 +100,9 @@ class MarsStepOut(C.Structure):
         ("evict_blocks", P(i32)), ("journal_op", P(u8)), ("journal_row", P(u32)),
         ("journal_n", P(i32)), ("ret_rows", P(u32)), ("ret_pin", P(u8)),
         ("ret_benefit", P(f64)), ("ret_cost", P(f64)), ("ret_deadline", P(f64)),
+        ("decode_level", P(u8)), ("prefill_level", P(u8)), ("n_finish", i32),
+        ("fin_rows", P(u32)), ("fin_pin", P(u8)), ("fin_benefit", P(f64)),
+        ("fin_cost", P(f64)), ("fin_deadline", P(f64)),
     ]
 
 
@@ -108,6 +123,15 @@ _SIGS = {
     "mars_step": (i32, [C.c_void_p, P(MarsStepIn), P(MarsStepOut)]),
     "mars_step_enqueue": (i32, [C.c_void_p, P(MarsStepIn)]),
     "mars_step_fetch": (i32, [C.c_void_p, P(MarsStepOut)]),
+    "mars_set_graph": (i32, [C.c_void_p, C.c_int]),
+    "mars_kv_init": (i32, [C.c_void_p, C.c_void_p]),
+    "mars_kv_apply": (i32, [C.c_void_p, i64, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "mars_kv_table": (i32, [C.c_void_p, u32, i64, C.c_void_p, P(i64)]),
+    "mars_kv_state": (i32, [C.c_void_p, i64, C.c_void_p, P(i64), P(i64), P(i32)]),
+    "mars_kv_evict": (i32, [C.c_void_p, i64, C.c_void_p, i64, C.c_int]),
+    "mars_kv_restore": (i32, [C.c_void_p, i64, C.c_void_p, i64, C.c_int]),
+    "mars_kv_host_ptr": (i32, [C.c_void_p, P(C.c_void_p), P(C.c_void_p)]),
+    "mars_host_link_peak": (i32, [C.c_void_p, i64, C.c_int, P(f64), P(f64), P(f64)]),
     "mars_retention_batch": (i32, [C.c_void_p, i64, C.c_void_p, C.c_void_p, i64, f64, f64, f64,
                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "mars_checkpoint": (i32, [C.c_void_p]),

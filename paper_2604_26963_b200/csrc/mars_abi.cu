@@ -30,7 +30,7 @@ struct mars_ctx {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   mars_config hcfg;
   Cfg cfg;
-  i64 max_rows = 0, max_queue = 0, n_rows = 0;
+  i64 max_rows = 0, max_queue = 0, n_rows = 0, alloc_rows = 0;
   Tab tab;
   Queue queue;
   Lsd qlsd, xlsd;
@@ -60,11 +60,21 @@ struct mars_ctx {
   int q_maxreq = 0;
   i64 pinned_upper = 0;
   int last_launches = 0;
+  bool use_graph = false;
+  cudaGraphExec_t graph_exec = nullptr;
+  long long graph_key[8] = {};
+  int graph_launches = 0;
   bool profiling = false;
   cudaEvent_t prof[2 * MARS_NUM_KTIMES] = {};
   int prof_used[MARS_NUM_KTIMES] = {};
   unsigned flush_salt = 1;
   std::string err;
+  // S5 block manager + host tier (mars_kv_init)
+  bool kv_on = false;
+  Kv kv = {};
+  void* kv_host = nullptr;          // pinned, mapped
+  unsigned char* kv_stage = nullptr; // device staging for op streams / ids
+  i64 kv_stage_bytes = 0;
 };
 
 static int fail(mars_ctx* c, int code, const char* fmt, ...) {
@@ -89,6 +99,9 @@ static Cfg make_cfg(const mars_config& h) {
   Cfg c;
   memset(&c, 0, sizeof c);
   c.bs = h.block_size;
+  c.bs_shift = -1;
+  for (int k = 0; k < 31; ++k)
+    if (h.block_size == (1 << k)) c.bs_shift = k;
   c.budget = h.token_budget;
   c.window = h.window_size;
   c.max_dec = h.max_decode_slots;
@@ -197,6 +210,7 @@ int mars_create(const mars_config* hcfg, int device, int64_t max_rows, int64_t m
   ctx->hcfg = *hcfg;
   ctx->cfg = make_cfg(*hcfg);
   ctx->max_rows = max_rows;
+  ctx->alloc_rows = (max_rows + ROW_PAD - 1) / ROW_PAD * ROW_PAD;
   ctx->max_queue = max_queue < 1 ? 1 : max_queue;
   CK(cudaSetDevice(device));
   CK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
@@ -208,7 +222,7 @@ int mars_create(const mars_config* hcfg, int device, int64_t max_rows, int64_t m
     int rc = mars_kernels_init();
     if (rc) return fail(ctx, MARS_ERR_CUDA, "kernel init: %s", cudaGetErrorString((cudaError_t)rc));
   }
-  const i64 R = max_rows, Qc = ctx->max_queue;
+  const i64 R = ctx->alloc_rows, Qc = ctx->max_queue;
   Tab& t = ctx->tab;
   memset(&t, 0, sizeof t);
   t.cap = R;
@@ -258,6 +272,9 @@ int mars_create(const mars_config* hcfg, int device, int64_t max_rows, int64_t m
   CK(cudaMemset(ctx->qsel, 0, sizeof(i32)));
   Bufs& b = ctx->bufs;
   memset(&b, 0, sizeof b);
+  ALLOC(b.exp_seg_row, R * 4);
+  ALLOC(b.exp_seg_blk, R * 4);
+  ALLOC(b.exp_seg_rank, R * 4);
   ALLOC(b.exp_row, R * 4);
   ALLOC(b.exp_blk, R * 4);
   ALLOC(b.exp_rank, R * 4);
@@ -281,6 +298,13 @@ int mars_create(const mars_config* hcfg, int device, int64_t max_rows, int64_t m
   ALLOC(b.dec_rows, WIN_MAX * 4);
   ALLOC(b.pre_rows, WIN_MAX * 4);
   ALLOC(b.pre_grant, WIN_MAX * 4);
+  ALLOC(b.dec_level, WIN_MAX);
+  ALLOC(b.pre_level, WIN_MAX);
+  ALLOC(b.fin_row, WIN_MAX * 4);
+  ALLOC(b.fin_pin, WIN_MAX);
+  ALLOC(b.fin_b, WIN_MAX * 8);
+  ALLOC(b.fin_c, WIN_MAX * 8);
+  ALLOC(b.fin_d, WIN_MAX * 8);
   b.ev_cap = R;
   ALLOC(b.ev_row, R * 4);
   ALLOC(b.ev_kind, R);
@@ -295,7 +319,7 @@ int mars_create(const mars_config* hcfg, int device, int64_t max_rows, int64_t m
   CK(cudaMallocHost((void**)&ctx->h_in, sizeof(mars_step_in)));
   CK(cudaMallocHost((void**)&ctx->h_work, sizeof(Work)));
   CK(cudaMallocHost((void**)&ctx->h_sc, sizeof(mars_scalars)));
-  ctx->h_out_bytes = (size_t)R * 48 + (size_t)Qc * 4 + (size_t)b.j_cap * 9 + 4 * WIN_MAX * 4 + 4096;
+  ctx->h_out_bytes = (size_t)R * 48 + (size_t)Qc * 4 + (size_t)b.j_cap * 9 + 4 * WIN_MAX * 4 + WIN_MAX * 40 + 8192;
   CK(cudaMallocHost((void**)&ctx->h_out, ctx->h_out_bytes));
   memset(ctx->h_in, 0, sizeof(mars_step_in));
   // scalars: empty pool of one block until mars_set_scalars
@@ -355,10 +379,11 @@ int mars_destroy(mars_ctx* ctx) {
   cudaFree(ctx->sc);
   cudaFree(ctx->qsel);
   Bufs& b = ctx->bufs;
-  void* bs[] = {b.exp_row, b.exp_blk, b.exp_rank, b.exp_row_sorted, b.exp_blk_sorted, b.wc_hi,
+  void* bs[] = {b.exp_seg_row, b.exp_seg_blk, b.exp_seg_rank, b.exp_row, b.exp_blk, b.exp_rank, b.exp_row_sorted, b.exp_blk_sorted, b.wc_hi,
                 b.wc_lo, b.wc_row, b.vc_key, b.vc_whi, b.vc_wlo, b.vc_row, b.vc_blk, b.ret_row,
                 b.ret_pin, b.ret_b, b.ret_c, b.ret_d, b.admitted, b.win_rows, b.dec_rows,
                 b.pre_rows, b.pre_grant, b.ev_row, b.ev_kind, b.ev_blk, b.j_op, b.j_row, b.j_n,
+                b.dec_level, b.pre_level, b.fin_row, b.fin_pin, b.fin_b, b.fin_c, b.fin_d,
                 b.flush};
   for (void* p : bs) cudaFree(p);
   cudaFree(ctx->d_stage);
@@ -371,8 +396,15 @@ int mars_destroy(mars_ctx* ctx) {
   cudaFreeHost(ctx->h_work);
   cudaFreeHost(ctx->h_sc);
   cudaFreeHost(ctx->h_out);
+  {
+    Kv& k = ctx->kv;
+    void* kp[] = {k.fs, k.chunks, k.cfs, k.dir, k.len, k.s, k.data, ctx->kv_stage};
+    for (void* p : kp) cudaFree(p);
+    if (ctx->kv_host) cudaFreeHost(ctx->kv_host);
+  }
   for (auto& e : ctx->prof)
     if (e) cudaEventDestroy(e);
+  if (ctx->graph_exec) cudaGraphExecDestroy(ctx->graph_exec);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -545,9 +577,11 @@ static LaunchArgs launch_args(mars_ctx* ctx, const mars_step_in* in) {
     while (passes < 4 && (mx >> (8 * passes)) != 0) passes++;
   }
   a.queue_passes = passes;
-  a.exp_may_be_big = (in->skip_expiry == 0 && ctx->n_rows > SORT_CAP) ? 1 : 0;
+  a.exp_sort = (!(in->mode & MARS_MODE_SKIP_EXPIRY) && !(in->mode & MARS_MODE_RANK_ORDERED)) ? 1 : 0;
+  a.exp_may_be_big = (a.exp_sort && ctx->n_rows > SORT_CAP) ? 1 : 0;
   a.prof = ctx->profiling ? ctx->prof : nullptr;
   a.prof_used = ctx->prof_used;
+  a.kv = ctx->kv_on ? &ctx->kv : nullptr;
   return a;
 }
 
@@ -556,8 +590,44 @@ int mars_step_enqueue(mars_ctx* ctx, const mars_step_in* in) {
   CK(cudaSetDevice(ctx->device));
   *ctx->h_in = *in;
   LaunchArgs a = launch_args(ctx, in);
-  ctx->last_launches = mars_enqueue_step(&a);
-  CK(cudaGetLastError());
+  if (!ctx->use_graph) {
+    ctx->last_launches = mars_enqueue_step(&a);
+    CK(cudaGetLastError());
+    return MARS_OK;
+  }
+  // whole-step CUDA graph, re-captured only when the launch shape changes
+  i64 qb = 1;
+  while (qb < a.queue_upper) qb <<= 1;
+  long long key[8] = {a.n_rows, a.control_possible, a.queue_passes, qb, a.exp_sort,
+                      a.exp_may_be_big, a.prof ? 1 : 0, (long long)(uintptr_t)ctx->stream};
+  if (!ctx->graph_exec || memcmp(key, ctx->graph_key, sizeof key) != 0) {
+    if (ctx->graph_exec) {
+      cudaGraphExecDestroy(ctx->graph_exec);
+      ctx->graph_exec = nullptr;
+    }
+    cudaGraph_t g = nullptr;
+    if (ctx->stream == nullptr || ctx->stream == cudaStreamLegacy ||
+        ctx->stream == cudaStreamPerThread)
+      return fail(ctx, MARS_ERR_ARG, "graph mode needs a non-default stream");
+    CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    ctx->graph_launches = mars_enqueue_step(&a);
+    cudaError_t ce = cudaStreamEndCapture(ctx->stream, &g);
+    if (ce != cudaSuccess) {
+      cudaGetLastError();
+      return fail(ctx, MARS_ERR_CUDA, "graph capture failed: %s", cudaGetErrorString(ce));
+    }
+    CK(cudaGraphInstantiate(&ctx->graph_exec, g, 0));
+    cudaGraphDestroy(g);
+    memcpy(ctx->graph_key, key, sizeof key);
+  }
+  CK(cudaGraphLaunch(ctx->graph_exec, ctx->stream));
+  ctx->last_launches = ctx->graph_launches;
+  return MARS_OK;
+}
+
+int mars_set_graph(mars_ctx* ctx, int on) {
+  if (!ctx) return MARS_ERR_ARG;
+  ctx->use_graph = on != 0;
   return MARS_OK;
 }
 
@@ -616,6 +686,14 @@ int mars_step_fetch(mars_ctx* ctx, mars_step_out* o) {
   o->ret_benefit = (const double*)pull(ctx, off, b.ret_b, (size_t)w.n_ret * 8);
   o->ret_cost = (const double*)pull(ctx, off, b.ret_c, (size_t)w.n_ret * 8);
   o->ret_deadline = (const double*)pull(ctx, off, b.ret_d, (size_t)w.n_ret * 8);
+  o->decode_level = (const uint8_t*)pull(ctx, off, b.dec_level, (size_t)w.n_dec);
+  o->prefill_level = (const uint8_t*)pull(ctx, off, b.pre_level, (size_t)w.n_pre);
+  o->n_finish = w.n_finish;
+  o->fin_rows = (const uint32_t*)pull(ctx, off, b.fin_row, (size_t)w.n_finish * 4);
+  o->fin_pin = (const uint8_t*)pull(ctx, off, b.fin_pin, (size_t)w.n_finish);
+  o->fin_benefit = (const double*)pull(ctx, off, b.fin_b, (size_t)w.n_finish * 8);
+  o->fin_cost = (const double*)pull(ctx, off, b.fin_c, (size_t)w.n_finish * 8);
+  o->fin_deadline = (const double*)pull(ctx, off, b.fin_d, (size_t)w.n_finish * 8);
   CK(cudaStreamSynchronize(ctx->stream));
   CK(cudaGetLastError());
   // free_blocks after the plan
@@ -663,7 +741,7 @@ int mars_checkpoint(mars_ctx* ctx) {
   CK(cudaSetDevice(ctx->device));
   const i64 R = ctx->max_rows, Qc = ctx->max_queue;
   for (auto& cs : ctx->cols) {
-    if (!cs.ckpt) CK(cudaMalloc(&cs.ckpt, (size_t)R * cs.esz));
+    if (!cs.ckpt) CK(cudaMalloc(&cs.ckpt, (size_t)ctx->alloc_rows * cs.esz));
     CK(cudaMemcpyAsync(cs.ckpt, *cs.dev, (size_t)ctx->n_rows * cs.esz, cudaMemcpyDeviceToDevice,
                        ctx->stream));
   }
@@ -740,7 +818,237 @@ int mars_flush_l2(mars_ctx* ctx, int64_t bytes) {
     ctx->bufs.flush_bytes = bytes;
   }
   int rc = mars_enqueue_flush(ctx->stream, ctx->bufs.flush, bytes, ctx->flush_salt++);
+  if (rc >= 1000)
+    return fail(ctx, MARS_ERR_CUDA, "flush: pending error from an earlier call: %s",
+                cudaGetErrorString((cudaError_t)(rc - 1000)));
   if (rc) return fail(ctx, MARS_ERR_CUDA, "flush: %s", cudaGetErrorString((cudaError_t)rc));
+  return MARS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// S5: block manager + host tier
+// ---------------------------------------------------------------------------
+
+static int kv_stage(mars_ctx* ctx, i64 bytes) {
+  if (bytes <= ctx->kv_stage_bytes) return MARS_OK;
+  cudaFree(ctx->kv_stage);
+  ctx->kv_stage = nullptr;
+  CK(cudaMalloc((void**)&ctx->kv_stage, (size_t)bytes));
+  ctx->kv_stage_bytes = bytes;
+  return MARS_OK;
+}
+
+int mars_kv_init(mars_ctx* ctx, const mars_kv_config* kc) {
+  if (!ctx || !kc) return MARS_ERR_ARG;
+  if (kc->total_blocks < 1 || kc->total_blocks > 0xffffffffll || kc->max_blocks_per_row < 1)
+    return fail(ctx, MARS_ERR_ARG, "bad kv config");
+  const i32 layers = kc->layers < 1 ? 1 : kc->layers;
+  if (kc->block_bytes % (16ll * layers) != 0)
+    return fail(ctx, MARS_ERR_ARG, "block_bytes must be a multiple of 16 * layers");
+  CK(cudaSetDevice(ctx->device));
+  if (ctx->kv_on) return fail(ctx, MARS_ERR_ARG, "kv manager already initialised");
+  Kv& k = ctx->kv;
+  k.total = kc->total_blocks;
+  k.D = (kc->max_blocks_per_row + KV_CH - 1) / KV_CH;
+  k.rows = ctx->alloc_rows;
+  k.nchunks = (k.total + KV_CH - 1) / KV_CH + k.rows;
+  k.layers = layers;
+  k.block_bytes = kc->block_bytes;
+  k.host_blocks = kc->host_blocks;
+  CK(cudaMalloc((void**)&k.fs, (size_t)k.total * 4));
+  CK(cudaMalloc((void**)&k.chunks, (size_t)k.nchunks * KV_CH * 4));
+  CK(cudaMalloc((void**)&k.cfs, (size_t)k.nchunks * 4));
+  CK(cudaMalloc((void**)&k.dir, (size_t)k.rows * k.D * 4));
+  CK(cudaMalloc((void**)&k.len, (size_t)k.rows * 4));
+  CK(cudaMalloc((void**)&k.s, sizeof(KvScal)));
+  CK(cudaMemset(k.len, 0, (size_t)k.rows * 4));
+  {
+    std::vector<u32> iota((size_t)k.nchunks);
+    for (i64 i = 0; i < k.nchunks; ++i) iota[i] = (u32)(k.nchunks - 1 - i);  // pops 0,1,2,..
+    CK(cudaMemcpy(k.cfs, iota.data(), (size_t)k.nchunks * 4, cudaMemcpyHostToDevice));
+  }
+  KvScal s0 = {0, 0, k.nchunks, 0};
+  CK(cudaMemcpy(k.s, &s0, sizeof s0, cudaMemcpyHostToDevice));
+  if (k.block_bytes > 0) {
+    CK(cudaMalloc((void**)&k.data, (size_t)k.total * k.block_bytes));
+    if (k.host_blocks > 0) {
+      CK(cudaHostAlloc(&ctx->kv_host, (size_t)k.host_blocks * k.block_bytes, cudaHostAllocMapped));
+      void* dp = nullptr;
+      CK(cudaHostGetDevicePointer(&dp, ctx->kv_host, 0));
+      k.host = (u8*)dp;
+    }
+  }
+  ctx->kv_on = true;
+  return MARS_OK;
+}
+
+int mars_kv_apply(mars_ctx* ctx, int64_t n, const uint8_t* op, const uint32_t* row,
+                  const int32_t* cnt) {
+  if (!ctx || n < 0) return MARS_ERR_ARG;
+  if (!ctx->kv_on) return fail(ctx, MARS_ERR_ARG, "kv manager not initialised");
+  if (n == 0) return MARS_OK;
+  for (int64_t i = 0; i < n; ++i)
+    if ((i64)row[i] >= ctx->kv.rows) return fail(ctx, MARS_ERR_CAPACITY, "kv row out of range");
+  CK(cudaSetDevice(ctx->device));
+  int rc = kv_stage(ctx, n * 9 + 64);
+  if (rc) return rc;
+  u32* drow = (u32*)ctx->kv_stage;
+  i32* dn = (i32*)(drow + n);
+  u8* dop = (u8*)(dn + n);
+  CK(cudaMemcpyAsync(drow, row, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(dn, cnt, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(dop, op, n, cudaMemcpyHostToDevice, ctx->stream));
+  rc = mars_kv_enqueue_apply(ctx->kv, ctx->stream, n, dop, drow, dn);
+  if (rc) return fail(ctx, MARS_ERR_CUDA, "kv apply: %s", cudaGetErrorString((cudaError_t)rc));
+  KvScal s;
+  CK(cudaMemcpyAsync(&s, ctx->kv.s, sizeof s, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (s.status) return fail(ctx, MARS_ERR_CONTRACT, "kv op stream broke the pool (status %d)", s.status);
+  return MARS_OK;
+}
+
+int mars_kv_table(mars_ctx* ctx, uint32_t row, int64_t cap, uint32_t* ids, int64_t* n) {
+  if (!ctx || !n) return MARS_ERR_ARG;
+  if (!ctx->kv_on) return fail(ctx, MARS_ERR_ARG, "kv manager not initialised");
+  if ((i64)row >= ctx->kv.rows) return MARS_ERR_CAPACITY;
+  CK(cudaSetDevice(ctx->device));
+  i32 len = 0;
+  CK(cudaMemcpyAsync(&len, ctx->kv.len + row, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  *n = len;
+  i64 m = len < cap ? len : cap;
+  if (ids && m > 0) {
+    int rc = kv_stage(ctx, m * 4);
+    if (rc) return rc;
+    rc = mars_kv_enqueue_table(ctx->kv, ctx->stream, row, m, (u32*)ctx->kv_stage);
+    if (rc) return fail(ctx, MARS_ERR_CUDA, "kv table: %s", cudaGetErrorString((cudaError_t)rc));
+    CK(cudaMemcpyAsync(ids, ctx->kv_stage, m * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  return MARS_OK;
+}
+
+int mars_kv_state(mars_ctx* ctx, int64_t k, uint32_t* top_ids, int64_t* explicit_depth,
+                  int64_t* fresh, int32_t* status) {
+  if (!ctx) return MARS_ERR_ARG;
+  if (!ctx->kv_on) return fail(ctx, MARS_ERR_ARG, "kv manager not initialised");
+  CK(cudaSetDevice(ctx->device));
+  KvScal s;
+  CK(cudaMemcpyAsync(&s, ctx->kv.s, sizeof s, cudaMemcpyDeviceToHost, ctx->stream));
+  if (top_ids && k > 0) {
+    int rc = kv_stage(ctx, k * 4);
+    if (rc) return rc;
+    rc = mars_kv_enqueue_top(ctx->kv, ctx->stream, k, (u32*)ctx->kv_stage);
+    if (rc) return fail(ctx, MARS_ERR_CUDA, "kv top: %s", cudaGetErrorString((cudaError_t)rc));
+    CK(cudaMemcpyAsync(top_ids, ctx->kv_stage, k * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (explicit_depth) *explicit_depth = s.fs_top;
+  if (fresh) *fresh = s.fresh;
+  if (status) *status = s.status;
+  return MARS_OK;
+}
+
+static int kv_move(mars_ctx* ctx, int64_t n, const uint32_t* ids, int64_t slot0, int method,
+                   int dir) {
+  if (!ctx || n < 0 || !ids) return MARS_ERR_ARG;
+  Kv& k = ctx->kv;
+  if (!ctx->kv_on || !k.data || !k.host) return fail(ctx, MARS_ERR_ARG, "no kv data tier");
+  if (slot0 < 0 || slot0 + n > k.host_blocks) return fail(ctx, MARS_ERR_CAPACITY, "host slots");
+  for (int64_t i = 0; i < n; ++i)
+    if ((i64)ids[i] >= k.total) return fail(ctx, MARS_ERR_CONTRACT, "block id out of range");
+  if (n == 0) return MARS_OK;
+  CK(cudaSetDevice(ctx->device));
+  const i64 piece = k.block_bytes / k.layers;
+  if (method == 1) {
+    int rc = kv_stage(ctx, n * 4);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(ctx->kv_stage, ids, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+    int grid = ctx->num_sms * 4;
+    rc = mars_kv_enqueue_copy(k, ctx->stream, (const u32*)ctx->kv_stage, n, slot0, dir, grid);
+    if (rc) return fail(ctx, MARS_ERR_CUDA, "kv copy: %s", cudaGetErrorString((cudaError_t)rc));
+  } else {
+    u8* hbase = (u8*)ctx->kv_host;
+    for (int64_t i = 0; i < n; ++i) {
+      for (int l = 0; l < k.layers; ++l) {
+        u8* dp = k.data + ((i64)l * k.total + ids[i]) * piece;
+        u8* hp = hbase + ((slot0 + i) * k.layers + l) * piece;
+        if (dir == 0)
+          CK(cudaMemcpyAsync(hp, dp, piece, cudaMemcpyDeviceToHost, ctx->stream));
+        else
+          CK(cudaMemcpyAsync(dp, hp, piece, cudaMemcpyHostToDevice, ctx->stream));
+      }
+    }
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  return MARS_OK;
+}
+
+int mars_kv_evict(mars_ctx* ctx, int64_t n, const uint32_t* ids, int64_t slot0, int method) {
+  return kv_move(ctx, n, ids, slot0, method, 0);
+}
+
+int mars_kv_restore(mars_ctx* ctx, int64_t n, const uint32_t* ids, int64_t slot0, int method) {
+  return kv_move(ctx, n, ids, slot0, method, 1);
+}
+
+int mars_kv_host_ptr(mars_ctx* ctx, void** host, void** device) {
+  if (!ctx) return MARS_ERR_ARG;
+  if (host) *host = ctx->kv_host;
+  if (device) *device = ctx->kv.data;
+  return MARS_OK;
+}
+
+int mars_host_link_peak(mars_ctx* ctx, int64_t bytes, int reps, double* d2h, double* h2d,
+                        double* bidir) {
+  if (!ctx || bytes < 1 || reps < 1) return MARS_ERR_ARG;
+  CK(cudaSetDevice(ctx->device));
+  void *h0 = nullptr, *h1 = nullptr, *d0 = nullptr, *d1 = nullptr;
+  cudaStream_t s2 = nullptr;
+  cudaEvent_t e0, e1, e2;
+  CK(cudaHostAlloc(&h0, bytes, cudaHostAllocDefault));
+  CK(cudaHostAlloc(&h1, bytes, cudaHostAllocDefault));
+  CK(cudaMalloc(&d0, bytes));
+  CK(cudaMalloc(&d1, bytes));
+  CK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventCreate(&e2));
+  memset(h0, 1, bytes);
+  memset(h1, 2, bytes);
+  double best[3] = {0, 0, 0};
+  for (int r = 0; r < reps; ++r) {
+    for (int mode = 0; mode < 3; ++mode) {
+      CK(cudaStreamSynchronize(ctx->stream));
+      CK(cudaEventRecord(e0, ctx->stream));
+      if (mode == 0 || mode == 2)
+        CK(cudaMemcpyAsync(h0, d0, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+      if (mode == 1) CK(cudaMemcpyAsync(d1, h1, bytes, cudaMemcpyHostToDevice, ctx->stream));
+      if (mode == 2) {
+        CK(cudaStreamWaitEvent(s2, e0, 0));
+        CK(cudaMemcpyAsync(d1, h1, bytes, cudaMemcpyHostToDevice, s2));
+        CK(cudaEventRecord(e2, s2));
+        CK(cudaStreamWaitEvent(ctx->stream, e2, 0));
+      }
+      CK(cudaEventRecord(e1, ctx->stream));
+      CK(cudaEventSynchronize(e1));
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      double gbs = (mode == 2 ? 2.0 : 1.0) * (double)bytes / (ms * 1e-3) / 1e9;
+      if (gbs > best[mode]) best[mode] = gbs;
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaEventDestroy(e2);
+  cudaStreamDestroy(s2);
+  cudaFree(d0);
+  cudaFree(d1);
+  cudaFreeHost(h0);
+  cudaFreeHost(h1);
+  if (d2h) *d2h = best[0];
+  if (h2d) *h2d = best[1];
+  if (bidir) *bidir = best[2];
   return MARS_OK;
 }
 

@@ -20,6 +20,9 @@ typedef int64_t i64;
 #define VSEL 1024             // victim-stream target length (prefix of reclaim order)
 #define VSTREAM_CAP 2048      // victim stream entries kept in shared memory
 #define LSD_G 148             // CTAs of the multi-CTA LSD radix sort
+#define SCAN_RPT 4            // consecutive rows per thread in the table scans
+#define MAX_SCAN_CTAS 1024    // upper bound of k_scan's grid
+#define ROW_PAD 2048          // row capacity is padded to this multiple
 #define MAXH 0x0FFFFFFFull    // 28-bit complement base for -blocks in victim keys
 
 // pack modes (control.py:101-122)
@@ -35,7 +38,7 @@ typedef int64_t i64;
 
 // device copy of the configuration (mars_config + derived)
 struct Cfg {
-  i32 bs, budget, window, max_dec, num_levels, max_promos, hyst, w_min;
+  i32 bs, bs_shift, budget, window, max_dec, num_levels, max_promos, hyst, w_min;
   i32 coord, cosched;
   i64 bounds[4], quotas[4];
   double tick_s, prefill_rate, promo_wait, slack, horizon, pw_clip;
@@ -78,6 +81,9 @@ struct Work {
   u32 ticket_ap;
   unsigned long long exp_blocks;
   i32 n_exp, n_active, n_queued, n_long_q, n_ready, n_promoted, n_victims, n_boundary;
+  i32 exp_seg_cnt[MAX_SCAN_CTAS], exp_seg_off[MAX_SCAN_CTAS];
+  i32 scan_ctas;
+  i64 scan_chunk;
   i32 max_req, min_req;
   u32 tmin_win, tmin_vic;
   u32 hist_win[HIST_BINS];
@@ -105,11 +111,13 @@ struct Work {
   i64 free_after_expiry;
   i32 status;
   i32 walk_slow;
+  i32 n_finish;
 };
 
 // variable-length step buffers
 struct Bufs {
-  // expired pins (K_A append, K_X sorts by rank)
+  // expired pins: per-CTA row-ordered segments (K_A), contiguous (K_C), rank order
+  u32 *exp_seg_row; i32 *exp_seg_blk; u32 *exp_seg_rank;
   u32 *exp_row; i32 *exp_blk; u32 *exp_rank;
   u32 *exp_row_sorted; i32 *exp_blk_sorted;
   // window candidates
@@ -122,6 +130,8 @@ struct Bufs {
   u32 *admitted;
   // plan outputs
   u32 *win_rows, *dec_rows, *pre_rows; i32 *pre_grant;
+  u8 *dec_level, *pre_level;
+  u32 *fin_row; u8 *fin_pin; double *fin_b, *fin_c, *fin_d;
   u32 *ev_row; u8 *ev_kind; i32 *ev_blk;
   u8 *j_op; u32 *j_row; i32 *j_n;
   i64 ev_cap, j_cap;
@@ -182,6 +192,12 @@ __device__ __forceinline__ u32 victim_digit(bool running, bool nonexp, u32 level
 }
 
 __device__ __forceinline__ i64 ceil_div64(i64 a, i64 b) { return (a + b - 1) / b; }
+
+// held_blocks / blocks_for_tokens (engine.py:112-113, 314-315) for kv >= 0
+__device__ __forceinline__ i64 held_blocks(const Cfg& c, i32 kv) {
+  if (c.bs_shift >= 0) return (i64)(((u32)kv + (u32)c.bs - 1u) >> c.bs_shift);
+  return (i64)(((u32)kv + (u32)c.bs - 1u) / (u32)c.bs);
+}
 
 __device__ __forceinline__ bool key_lt(u64 ah, u64 al, u64 bh, u64 bl) {
   return ah < bh || (ah == bh && al < bl);

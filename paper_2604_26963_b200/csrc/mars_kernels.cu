@@ -188,9 +188,10 @@ __global__ void __launch_bounds__(SCAN_TPB) k_scan(Tab t, Cfg c, Work* w, Bufs b
   __syncthreads();
 
   const double now = w->in.now;
-  const bool do_exp = !w->in.skip_expiry;
+  const bool do_exp = !(w->in.mode & MARS_MODE_SKIP_EXPIRY);
   const double scale = (now > 0.0 && now < 1e300) ? 1024.0 / now : 0.0;
-  const i64 chunk = (n_rows + gridDim.x - 1) / gridDim.x;
+  const i64 tile = (i64)blockDim.x * SCAN_RPT;
+  const i64 chunk = ((n_rows + gridDim.x - 1) / gridDim.x + tile - 1) / tile * tile;
   const i64 start = (i64)blockIdx.x * chunk;
   i64 end = start + chunk;
   if (end > n_rows) end = n_rows;
@@ -198,67 +199,128 @@ __global__ void __launch_bounds__(SCAN_TPB) k_scan(Tab t, Cfg c, Work* w, Bufs b
   long long exp_blocks = 0;
   int n_active = 0, n_queued = 0, n_long = 0, n_ready = 0, n_prom = 0, n_vic = 0, n_bnd = 0;
   int max_req = 0, min_req = 0x7fffffff;
+  int n_exp_local = 0;  // expired rows of this CTA, written in row order at b.exp_seg_*[start..]
+  __shared__ int s_wexp[SCAN_TPB / 32];
+  __shared__ int s_tile_exp;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 
-  for (i64 r0 = start; r0 < end; r0 += blockDim.x) {
-    i64 r = r0 + threadIdx.x;
-    bool valid = r < end;
-    u8 f = valid ? t.flags[r] : 0;
-    u8 ph = valid ? t.phase[r] : MARS_EMPTY;
-    bool expire = false;
-    i32 pbk = 0;
-    if (f & MARS_F_ACTIVE) n_active++;
-    if (f & MARS_F_QUEUED) {
-      n_queued++;
-      if (f & MARS_F_LONG) n_long++;
-      i32 q = t.req[r];
-      max_req = q > max_req ? q : max_req;
-      min_req = q < min_req ? q : min_req;
+  // Each thread owns SCAN_RPT consecutive rows per tile: the byte columns
+  // arrive as one 32-bit load, kv as one 128-bit load and the two f64
+  // columns as two 128-bit loads each, all issued before any use, so the
+  // whole tile's DRAM traffic is in flight at once.
+  for (i64 base = start + (i64)threadIdx.x * SCAN_RPT; base - (i64)threadIdx.x * SCAN_RPT < end;
+       base += (i64)blockDim.x * SCAN_RPT) {
+    const bool any = base < end;
+    u32 f4 = 0, ph4 = 0x07070707u, lv4 = 0, pr4 = 0;
+    int4 kv4 = make_int4(0, 0, 0, 0);
+    double2 rsa = make_double2(0, 0), rsb = rsa, wsa = rsa, wsb = rsa;
+    if (any) {
+      f4 = *(const u32*)(t.flags + base);
+      ph4 = *(const u32*)(t.phase + base);
+      lv4 = *(const u32*)(t.level + base);
+      pr4 = *(const u32*)(t.promos + base);
+      kv4 = *(const int4*)(t.kv + base);
+      const double* tcol = c.coord ? t.rs : t.arr;
+      rsa = *(const double2*)(tcol + base);
+      rsb = *(const double2*)(tcol + base + 2);
+      wsa = *(const double2*)(t.ws + base);
+      wsb = *(const double2*)(t.ws + base + 2);
     }
-    if (f & MARS_F_BOUNDARY) n_bnd++;
-    if (f & MARS_F_PINNED) {
-      double d = t.dl[r];
-      bool exp_ = d < now;
-      pbk = t.pb[r];
-      if (do_exp && exp_) {
-        expire = true;
-        t.flags[r] = f & ~MARS_F_PINNED;
-        t.kv[r] = 0;
-        exp_blocks += pbk;
-      } else {
-        u32 plv = t.plevel[r];
-        atomicAdd(&hv[victim_digit(false, !exp_, plv, pbk)], 1u);
-        n_vic++;
+    const i32 kva[4] = {kv4.x, kv4.y, kv4.z, kv4.w};
+    const double tt[4] = {rsa.x, rsa.y, rsb.x, rsb.y};
+    const double wsv[4] = {wsa.x, wsa.y, wsb.x, wsb.y};
+    int ne = 0;
+    u32 exp_mask = 0;
+    i32 exp_pb[SCAN_RPT];
+#pragma unroll
+    for (int j = 0; j < SCAN_RPT; ++j) {
+      const i64 r = base + j;
+      exp_pb[j] = 0;
+      if (r >= end) continue;
+      u8 f = (u8)(f4 >> (8 * j));
+      u8 ph = (u8)(ph4 >> (8 * j));
+      if (f & MARS_F_ACTIVE) n_active++;
+      if (f & MARS_F_QUEUED) {
+        n_queued++;
+        if (f & MARS_F_LONG) n_long++;
+        i32 q = t.req[r];
+        max_req = q > max_req ? q : max_req;
+        min_req = q < min_req ? q : min_req;
       }
-    }
-    int slot = warp_append(&w->n_exp, expire);
-    if (slot >= 0) {
-      b.exp_row[slot] = (u32)r;
-      b.exp_blk[slot] = pbk;
-      b.exp_rank[slot] = t.rank[r];
-    }
-    if ((f & MARS_F_ACTIVE) && (ph == MARS_PREFILL || ph == MARS_DECODE)) {
-      n_ready++;
-      u32 lv = t.level[r];
-      if (c.coord) {
-        if (lv != 0 && t.promos[r] < (u32)c.max_promos) {
-          double ws = t.ws[r];
-          if (now - ws >= c.promo_wait) {  // scheduler.py:123
+      if (f & MARS_F_BOUNDARY) n_bnd++;
+      if (f & MARS_F_PINNED) {
+        double d = t.dl[r];
+        bool exp_ = d < now;
+        i32 pbk = t.pb[r];
+        if (do_exp && exp_) {
+          t.flags[r] = f & ~MARS_F_PINNED;
+          t.kv[r] = 0;
+          exp_blocks += pbk;
+          exp_mask |= 1u << j;
+          exp_pb[j] = pbk;
+          ne++;
+        } else {
+          atomicAdd(&hv[victim_digit(false, !exp_, t.plevel[r], pbk)], 1u);
+          n_vic++;
+        }
+      }
+      if ((f & MARS_F_ACTIVE) && (ph == MARS_PREFILL || ph == MARS_DECODE)) {
+        n_ready++;
+        u32 lv = (lv4 >> (8 * j)) & 255u;
+        if (c.coord) {
+          u32 pr = (pr4 >> (8 * j)) & 255u;
+          if (lv != 0 && pr < (u32)c.max_promos && now - wsv[j] >= c.promo_wait) {
+            // promote_waiting (scheduler.py:120-127)
             lv -= 1;
             t.level[r] = (u8)lv;
-            t.promos[r] = t.promos[r] + 1;
+            t.promos[r] = (u8)(pr + 1);
             t.ws[r] = now;
             n_prom++;
           }
+        } else {
+          lv = 0;
         }
-        atomicAdd(&hw[window_digit(lv, t.rs[r], scale)], 1u);
-      } else {
-        atomicAdd(&hw[window_digit(0, t.arr[r], scale)], 1u);
+        atomicAdd(&hw[window_digit(lv, tt[j], scale)], 1u);
+        i32 kvv = kva[j];
+        if (kvv > 0) {
+          atomicAdd(&hv[victim_digit(true, false, lv, held_blocks(c, kvv))], 1u);
+          n_vic++;
+        }
       }
-      i32 kvv = t.kv[r];
-      if (kvv > 0) {
-        atomicAdd(&hv[victim_digit(true, false, c.coord ? lv : 0u, ceil_div64(kvv, c.bs))], 1u);
-        n_vic++;
+    }
+    // expired rows, compacted in row order into this CTA's segment
+    if (__syncthreads_or(ne)) {
+      int incl = ne;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int x = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += x;
       }
+      if (lane == 31) s_wexp[wid] = incl;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int q = 0; q < (int)(blockDim.x >> 5); ++q) {
+          int x = s_wexp[q];
+          s_wexp[q] = acc;
+          acc += x;
+        }
+        s_tile_exp = acc;
+      }
+      __syncthreads();
+      int pos = n_exp_local + s_wexp[wid] + incl - ne;
+#pragma unroll
+      for (int j = 0; j < SCAN_RPT; ++j) {
+        if (exp_mask & (1u << j)) {
+          const i64 r = base + j;
+          b.exp_seg_row[start + pos] = (u32)r;
+          b.exp_seg_blk[start + pos] = exp_pb[j];
+          b.exp_seg_rank[start + pos] = t.rank[r];
+          pos++;
+        }
+      }
+      n_exp_local += s_tile_exp;
+      __syncthreads();
     }
   }
   __syncthreads();
@@ -277,27 +339,41 @@ __global__ void __launch_bounds__(SCAN_TPB) k_scan(Tab t, Cfg c, Work* w, Bufs b
     atomicMin(&w->tmin_vic, (u32)tv);
   }
 
-  long long eb = block_sum<long long>(exp_blocks, shl);
-  int a0 = block_sum<int>(n_active, shi);
-  int a1 = block_sum<int>(n_queued, shi);
-  int a2 = block_sum<int>(n_long, shi);
-  int a3 = block_sum<int>(n_ready, shi);
-  int a4 = block_sum<int>(n_prom, shi);
-  int a5 = block_sum<int>(n_vic, shi);
-  int a6 = block_sum<int>(n_bnd, shi);
-  int mx = block_max<int>(max_req, shi, 0);
-  int mn = block_min<int>(min_req, shi, 0x7fffffff);
+  // counters: warp shuffles, then one shared and one global atomic per warp/CTA
+  __shared__ int s_cnt[9];
+  __shared__ unsigned long long s_eb;
+  if (threadIdx.x < 9) s_cnt[threadIdx.x] = (threadIdx.x == 8) ? 0x7fffffff : 0;
+  if (threadIdx.x == 0) s_eb = 0;
+  __syncthreads();
+  {
+    unsigned long long eb = warp_sum<unsigned long long>((unsigned long long)exp_blocks);
+    int v[7] = {n_active, n_queued, n_long, n_ready, n_prom, n_vic, n_bnd};
+#pragma unroll
+    for (int q = 0; q < 7; ++q) v[q] = warp_sum<int>(v[q]);
+    int mx = warp_max<int>(max_req), mn = warp_min<int>(min_req);
+    if (lane == 0) {
+      if (eb) atomicAdd(&s_eb, eb);
+#pragma unroll
+      for (int q = 0; q < 7; ++q)
+        if (v[q]) atomicAdd(&s_cnt[q], v[q]);
+      atomicMax(&s_cnt[7], mx);
+      atomicMin(&s_cnt[8], mn);
+    }
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
-    atomicAdd(&w->exp_blocks, (unsigned long long)eb);
-    atomicAdd(&w->n_active, a0);
-    atomicAdd(&w->n_queued, a1);
-    atomicAdd(&w->n_long_q, a2);
-    atomicAdd(&w->n_ready, a3);
-    atomicAdd(&w->n_promoted, a4);
-    atomicAdd(&w->n_victims, a5);
-    atomicAdd(&w->n_boundary, a6);
-    atomicMax(&w->max_req, mx);
-    atomicMin(&w->min_req, mn);
+    atomicAdd(&w->exp_blocks, s_eb);
+    atomicAdd(&w->n_active, s_cnt[0]);
+    atomicAdd(&w->n_queued, s_cnt[1]);
+    atomicAdd(&w->n_long_q, s_cnt[2]);
+    atomicAdd(&w->n_ready, s_cnt[3]);
+    atomicAdd(&w->n_promoted, s_cnt[4]);
+    atomicAdd(&w->n_victims, s_cnt[5]);
+    atomicAdd(&w->n_boundary, s_cnt[6]);
+    atomicMax(&w->max_req, s_cnt[7]);
+    atomicMin(&w->min_req, s_cnt[8]);
+    w->exp_seg_cnt[blockIdx.x] = n_exp_local;
+    atomicAdd(&w->n_exp, n_exp_local);
     __threadfence();
     u32 tk = atomicAdd(&w->ticket, 1u);
     s_last = (tk == gridDim.x - 1);
@@ -305,6 +381,18 @@ __global__ void __launch_bounds__(SCAN_TPB) k_scan(Tab t, Cfg c, Work* w, Bufs b
   __syncthreads();
   if (!s_last) return;
   __threadfence();
+  if (threadIdx.x == 0) {
+    // exclusive prefix of the per-CTA expired segments (row order == CTA order)
+    volatile Work* vw0 = w;
+    int acc = 0;
+    for (int q = 0; q < (int)gridDim.x; ++q) {
+      int x = vw0->exp_seg_cnt[q];
+      w->exp_seg_off[q] = acc;
+      acc += x;
+    }
+    w->scan_ctas = gridDim.x;
+    w->scan_chunk = chunk;
+  }
 
   // ---- last CTA: finalise ------------------------------------------------
   volatile Work* vw = w;
@@ -325,20 +413,23 @@ __global__ void __launch_bounds__(SCAN_TPB) k_scan(Tab t, Cfg c, Work* w, Bufs b
     w->t_vic = gv;
     w->n_win_cand_expected = (i32)wu;
     w->n_vic_cand_expected = (i32)vu;
-    // Telemetry.probe (telemetry.py:152-158) after the expiry evictions
+    const int mode = w->in.mode;
     i64 total = sc->total_blocks;
     i64 freeb = sc->free_blocks + (i64)vw->exp_blocks;
     sc->free_blocks = freeb;
     w->free_after_expiry = freeb;
-    sc->available_kv = freeb;
-    sc->kv_usage_ratio = (double)(total - freeb) / (double)total;
-    sc->active_sessions = vw->n_active;
-    sc->active_tools = w->in.active_tools;
-    sc->queued_tools = w->in.queued_tools;
+    if (!(mode & MARS_MODE_SKIP_PROBE)) {
+      // Telemetry.probe (telemetry.py:152-158) after the expiry evictions
+      sc->available_kv = freeb;
+      sc->kv_usage_ratio = (double)(total - freeb) / (double)total;
+      sc->active_sessions = vw->n_active;
+      sc->active_tools = w->in.active_tools;
+      sc->queued_tools = w->in.queued_tools;
+    }
     i64 qlen = sc->queue_len;
     w->qlen = qlen;
-    if ((i64)vw->n_queued != qlen) w->status |= ST_QUEUE_MISMATCH;
-    if (w->in.control_due) {
+    if (!(mode & MARS_MODE_NO_ROWS) && (i64)vw->n_queued != qlen) w->status |= ST_QUEUE_MISMATCH;
+    if (w->in.control_due && !(mode & MARS_MODE_SKIP_REFRESH)) {
       // refresh_pressure (telemetry.py:174-208)
       double slots = (double)w->in.worker_slots;
       int at = sc->active_tools, qt = sc->queued_tools;
@@ -373,16 +464,6 @@ __global__ void __launch_bounds__(SCAN_TPB) k_scan(Tab t, Cfg c, Work* w, Bufs b
       sc->kv_overloaded = on;
       sc->kv_high_streak = hs;
       sc->kv_low_streak = ls;
-      // pack_queue mode (control.py:109-122)
-      int mode = sc->cpu_overloaded ? PACK_DESC
-                                    : ((qlen > 0 && (i64)vw->n_long_q == qlen) ? PACK_FF : PACK_ASC);
-      w->pack_mode = mode;
-      w->need_seed = (!sc->has_ema_blocks && !sc->has_blocks_seed && qlen > 0) ? 1 : 0;
-      int big = (qlen > SORT_CAP && mode != PACK_FF) ? 1 : 0;
-      w->big_queue = big;
-      w->lsd_big = big;
-      w->lsd_n = (i32)qlen;
-      w->lsd_maxkey = (mode == PACK_ASC) ? (u64)vw->max_req : (u64)(vw->max_req - vw->min_req);
     }
     int ne = vw->n_exp;
     w->xlsd_big = ne > SORT_CAP ? 1 : 0;
@@ -405,6 +486,30 @@ __global__ void __launch_bounds__(SCAN_TPB) k_compact(Tab t, Cfg c, Work* w, Buf
   const double ema = sc->has_ema_tool ? sc->ema_tool : c.tool_prior;
   const i64 stride = (i64)gridDim.x * blockDim.x;
   const i64 lim = ((n_rows + 31) / 32) * 32;
+  // expired pins: k_scan's per-CTA segments are in row order and CTA order is
+  // row order, so their concatenation is row order -- already the rank order
+  // expired_pins() sorts by when the table is rank-ordered (baselines.py:396-399)
+  {
+    const int nseg = w->scan_ctas;
+    const i64 chunk = w->scan_chunk;
+    const bool ro = (w->in.mode & MARS_MODE_RANK_ORDERED) != 0;
+    for (int sg = blockIdx.x; sg < nseg; sg += gridDim.x) {
+      const int cnt = w->exp_seg_cnt[sg], off = w->exp_seg_off[sg];
+      const i64 src = (i64)sg * chunk;
+      for (int k = threadIdx.x; k < cnt; k += blockDim.x) {
+        u32 r = b.exp_seg_row[src + k];
+        i32 bk = b.exp_seg_blk[src + k];
+        if (ro) {
+          b.exp_row_sorted[off + k] = r;
+          b.exp_blk_sorted[off + k] = bk;
+        } else {
+          b.exp_row[off + k] = r;
+          b.exp_blk[off + k] = bk;
+          b.exp_rank[off + k] = b.exp_seg_rank[src + k];
+        }
+      }
+    }
+  }
   for (i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x; r < lim + 0; r += stride) {
     bool valid = r < n_rows;
     u8 f = valid ? t.flags[r] : 0;
@@ -715,9 +820,34 @@ __global__ void __launch_bounds__(1024) k_pack_small(Work* w, Queue Q, Lsd L,
   if (qlen <= 0) return;
   int sel = *qsel_p;
   const i32* req = Q.req[sel];
-  int mode = w->pack_mode;
+  const u8* lng = Q.lng[sel];
   __shared__ u32 shu[1024 + 32];
   __shared__ u32 hist[256];
+  __shared__ int shr[32];
+  // pack_queue mode (control.py:109-122) from the queue itself
+  int all_long = 1, mx = 0, mn = 0x7fffffff;
+  for (int i = threadIdx.x; i < qlen; i += blockDim.x) {
+    all_long &= lng[i] ? 1 : 0;
+    i32 rq = req[i];
+    mx = rq > mx ? rq : mx;
+    mn = rq < mn ? rq : mn;
+  }
+  all_long = block_min<int>(all_long, shr, 1);
+  mx = block_max<int>(mx, shr, 0);
+  mn = block_min<int>(mn, shr, 0x7fffffff);
+  const int mode = sc->cpu_overloaded ? PACK_DESC : (all_long ? PACK_FF : PACK_ASC);
+  if (threadIdx.x == 0) {
+    w->pack_mode = mode;
+    w->need_seed = (!sc->has_ema_blocks && !sc->has_blocks_seed) ? 1 : 0;
+    int big = (qlen > SORT_CAP && mode != PACK_FF) ? 1 : 0;
+    w->big_queue = big;
+    w->lsd_big = big;
+    w->lsd_n = qlen;
+    w->max_req = mx;
+    w->min_req = mn;
+    w->lsd_maxkey = (mode == PACK_ASC) ? (u64)mx : (u64)(mx - mn);
+  }
+  __syncthreads();
   if (mode == PACK_FF) {
     // first fit against available_kv, in current list order; fits, then deferred
     __shared__ long long s_cap;
@@ -795,7 +925,7 @@ __global__ void __launch_bounds__(1024) k_pack_small(Work* w, Queue Q, Lsd L,
     if (threadIdx.x == 0) w->lsd_cur = 0;
     return;
   }
-  i32 mr = w->max_req;
+  i32 mr = mx;
   if (qlen > SORT_CAP) {
     // big queue: seed LSD keys (stable sort by req asc, or by -req via max-req)
     for (int i = threadIdx.x; i < qlen; i += blockDim.x) {
@@ -892,7 +1022,9 @@ __global__ void __launch_bounds__(SCAN_TPB) k_admit_apply(Tab t, Cfg c, Work* w,
     bool wc = false;
     u64 whi = 0, wlo = 0;
     u32 row = 0;
-    if (valid) {
+    if (valid && (w->in.mode & MARS_MODE_NO_ROWS)) {
+      b.admitted[i] = Q.row[sel][perm[i]];
+    } else if (valid) {
       u32 pos = perm[i];
       row = Q.row[sel][pos];
       i32 r0p = t.r0p[row];
@@ -1622,7 +1754,61 @@ __global__ void __launch_bounds__(WALK_TPB) k_walk(Tab t, Cfg c, Work* w, Bufs b
   }
   __syncthreads();
 
-  // 4. outputs, scalars, winpos reset
+  // 4. drop-in epilogues on the planned rows: charge_service at tick end
+  //    (baselines.py:362-367 via sim.py:364) and decide_retention for decodes
+  //    that finish their round this tick, on post-tick values (sim.py:233-250,
+  //    engine.py:503-512: kv+1, context+1, now + tick).
+  const int mode = w->in.mode;
+  if (mode & (MARS_MODE_SERVICE | MARS_MODE_FINISH_RETENTION)) {
+    const double tick_end = now + c.tick_s;
+    const int nd = S.ndec, np_ = S.npre;
+    const i64 total = sc->total_blocks;
+    const double usage = sc->kv_usage_ratio;
+    const double ema = sc->has_ema_tool ? sc->ema_tool : c.tool_prior;
+    for (int i = threadIdx.x; i < nd + np_; i += blockDim.x) {
+      bool dec = i < nd;
+      u32 r = dec ? b.dec_rows[i] : b.pre_rows[i - nd];
+      i64 tokens = dec ? 1 : b.pre_grant[i - nd];
+      u32 lv = t.level[r];
+      if ((mode & MARS_MODE_SERVICE) && c.coord) {
+        i64 served = t.served[r] + tokens;
+        if (served > c.quotas[lv] && (int)lv < c.num_levels - 1) {
+          lv += 1;
+          served = 0;
+        }
+        t.served[r] = served;
+        t.level[r] = (u8)lv;
+        t.ws[r] = tick_end;
+      }
+      if (dec) b.dec_level[i] = (u8)lv;
+      else b.pre_level[i - nd] = (u8)lv;
+    }
+    if (mode & MARS_MODE_FINISH_RETENTION) {
+      int lim = ((nd + 31) / 32) * 32;
+      for (int i = threadIdx.x; i < lim; i += blockDim.x) {
+        bool fin = false;
+        u32 r = 0;
+        if (i < nd) {
+          r = b.dec_rows[i];
+          fin = t.rem[r] == 1;
+        }
+        int sl = warp_append(&w->n_finish, fin);
+        if (sl >= 0) {
+          u8 pin;
+          double bb, cc, dd;
+          decide_retention(c, (i64)t.ctx[r] + 1, (i64)t.kv[r] + 1, total, usage, ema, tick_end,
+                           pin, bb, cc, dd);
+          b.fin_row[sl] = r;
+          b.fin_pin[sl] = pin;
+          b.fin_b[sl] = bb;
+          b.fin_c[sl] = cc;
+          b.fin_d[sl] = dd;
+        }
+      }
+    }
+  }
+
+  // 5. outputs, scalars, winpos reset
   for (int i = threadIdx.x; i < nwin; i += blockDim.x) t.winpos[S.wrow[i]] = -1;
   if (threadIdx.x == 0) {
     w->n_window = nwin;
@@ -1753,8 +1939,9 @@ int mars_enqueue_step(const LaunchArgs* a) {
   launches++;
   int nsm = a->num_sms;
   i64 n = a->n_rows;
-  int g_scan = (int)((n + 2047) / 2048);
-  if (g_scan > 2 * nsm) g_scan = 2 * nsm;
+  int g_scan = (int)((n + SCAN_TPB * SCAN_RPT - 1) / (SCAN_TPB * SCAN_RPT));
+  if (g_scan > 4 * nsm) g_scan = 4 * nsm;
+  if (g_scan > MAX_SCAN_CTAS) g_scan = MAX_SCAN_CTAS;
   if (g_scan < 1) g_scan = 1;
   mark(0, 0, s);
   k_scan<<<g_scan, SCAN_TPB, 0, s>>>(a->tab, a->cfg, a->work, a->bufs, a->sc, n);
@@ -1770,8 +1957,10 @@ int mars_enqueue_step(const LaunchArgs* a) {
   mark(1, 1, s2);
   launches++;
   mark(2, 0, s2);
-  k_exp_small<<<1, 1024, sort_smem_bytes(), s2>>>(a->work, a->bufs, a->xlsd);
-  launches++;
+  if (a->exp_sort) {
+    k_exp_small<<<1, 1024, sort_smem_bytes(), s2>>>(a->work, a->bufs, a->xlsd);
+    launches++;
+  }
   if (a->exp_may_be_big) {
     for (int p = 0; p < 4; ++p) {
       k_lsd_hist<<<LSD_G, 256, 0, s2>>>(a->xlsd, a->work, 1, p);
@@ -1798,7 +1987,9 @@ int mars_enqueue_step(const LaunchArgs* a) {
   }
   cudaStreamWaitEvent(s, a->ev_join, 0);
   if (a->control_possible) {
-    int g_ap = (int)((a->queue_upper + SCAN_TPB - 1) / SCAN_TPB);
+    i64 qb = 1;
+    while (qb < a->queue_upper) qb <<= 1;  // pow2 bucket: stable launch shape for graphs
+    int g_ap = (int)((qb + SCAN_TPB - 1) / SCAN_TPB);
     if (g_ap > 2 * nsm) g_ap = 2 * nsm;
     if (g_ap < 1) g_ap = 1;
     mark(4, 0, s);
@@ -1809,6 +2000,10 @@ int mars_enqueue_step(const LaunchArgs* a) {
   }
   mark(5, 0, s);
   k_walk<<<1, WALK_TPB, walk_smem_bytes(), s>>>(a->tab, a->cfg, a->work, a->bufs, a->sc, n);
+  if (a->kv) {
+    mars_kv_enqueue_apply_step(*a->kv, s, a->work, a->bufs);
+    launches++;
+  }
   mark(5, 1, s);
   launches++;
   return launches;
@@ -1825,6 +2020,8 @@ int mars_enqueue_retention(const Cfg& c, cudaStream_t s, i64 n, const i32* ctx, 
 }
 
 int mars_enqueue_flush(cudaStream_t s, u8* p, i64 n, u32 salt) {
+  cudaError_t prior = cudaGetLastError();
+  if (prior != cudaSuccess) return 1000 + (int)prior;  // an earlier call left an error
   k_flush<<<1184, 256, 0, s>>>(p, n, salt);
   return (int)cudaGetLastError();
 }

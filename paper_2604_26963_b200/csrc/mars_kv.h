@@ -1,0 +1,40 @@
+// Device layout of the paged KV block manager (mars_kv.cu).
+#pragma once
+
+#include "mars_internal.cuh"
+
+#define KV_CH 64  // block IDs per table chunk
+
+struct KvScal {
+  i64 fs_top;   // explicit stack entries
+  i64 fresh;    // next never-used block ID (implicit stack bottom)
+  i64 cfs_top;  // free table chunks
+  i32 status;   // contract-break bits
+};
+
+struct Kv {
+  i64 total;      // KvPool.total_blocks
+  i32 D;          // chunk-directory entries per row
+  i64 rows;
+  i64 nchunks;
+  u32* fs;        // explicit free stack (top = fs[fs_top-1])
+  u32* chunks;    // [nchunks][KV_CH] block IDs
+  u32* cfs;       // free chunk stack
+  u32* dir;       // [rows][D] chunk indices
+  i32* len;       // [rows] table length
+  KvScal* s;
+  // data plane
+  u8* data;       // HBM pool: layer-major [layers][total][block_bytes/layers]
+  u8* host;       // pinned host tier: [host_blocks][layers][piece]
+  i64 block_bytes;
+  i32 layers;
+  i64 host_blocks;
+};
+
+int mars_kv_enqueue_apply(const Kv& k, cudaStream_t s, i64 n_ops, const u8* op, const u32* row,
+                          const i32* n);
+int mars_kv_enqueue_apply_step(const Kv& k, cudaStream_t s, Work* w, const Bufs& b);
+int mars_kv_enqueue_table(const Kv& k, cudaStream_t s, u32 row, i64 cap, u32* out);
+int mars_kv_enqueue_top(const Kv& k, cudaStream_t s, i64 cnt, u32* out);
+int mars_kv_enqueue_copy(const Kv& k, cudaStream_t s, const u32* ids, i64 n, i64 slot0, int dir,
+                         int grid);

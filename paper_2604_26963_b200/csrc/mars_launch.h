@@ -2,6 +2,7 @@
 #pragma once
 
 #include "mars_internal.cuh"
+#include "mars_kv.h"
 
 struct LaunchArgs {
   cudaStream_t stream, side;
@@ -20,9 +21,11 @@ struct LaunchArgs {
   int control_possible;  // the step may run the control plane
   int queue_passes;      // LSD passes needed for the largest queue key (0 = small only)
   i64 queue_upper;       // upper bound of the queue length at step start
+  int exp_sort;          // expired pins need a rank sort (table not rank-ordered)
   int exp_may_be_big;    // more than SORT_CAP pins may expire
   cudaEvent_t* prof;     // 2*MARS_NUM_KTIMES events, or null
   int* prof_used;        // which pairs were recorded
+  const Kv* kv;          // block manager to update with the step's journal, or null
 };
 
 int mars_kernels_init();

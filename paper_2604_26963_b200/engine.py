@@ -64,6 +64,13 @@ class StepResult:
     ret_benefit: np.ndarray
     ret_cost: np.ndarray
     ret_deadline: np.ndarray
+    decode_level: np.ndarray
+    prefill_level: np.ndarray
+    fin_rows: np.ndarray
+    fin_pin: np.ndarray
+    fin_benefit: np.ndarray
+    fin_cost: np.ndarray
+    fin_deadline: np.ndarray
     n_ready: int
     n_promoted: int
     pack_mode: int
@@ -203,21 +210,28 @@ class MarsEngine:
         for k, v in snap.telemetry.items():
             setattr(s, k, int(v))
         self.set_scalars(s)
+        # rows laid out in session-id order: expired pins come out of the scan
+        # already in expired_pins() order (no sort pass)
+        self.rank_ordered = bool(np.array_equal(snap.cols["rank"],
+                                                np.arange(snap.n, dtype=np.uint32)))
 
     # -- the step ----------------------------------------------------------------
 
-    @staticmethod
-    def step_in(now: float, control_due: bool = True, active_tools: int = 0,
-                queued_tools: int = 0, worker_slots: int = 8,
-                skip_expiry: bool = False) -> N.MarsStepIn:
+    rank_ordered = False
+
+    def step_in(self, now: float, control_due: bool = True, active_tools: int = 0,
+                queued_tools: int = 0, worker_slots: int = 8, mode: int = 0) -> N.MarsStepIn:
         si = N.MarsStepIn()
         si.now = float(now)
         si.control_due = int(bool(control_due))
         si.active_tools = int(active_tools)
         si.queued_tools = int(queued_tools)
         si.worker_slots = int(worker_slots)
-        si.skip_expiry = int(bool(skip_expiry))
+        si.mode = int(mode) | (N.MODE_RANK_ORDERED if self.rank_ordered else 0)
         return si
+
+    def set_graph(self, on: bool) -> None:
+        self._check(self.lib.mars_set_graph(self.ctx, int(bool(on))))
 
     def enqueue(self, si: N.MarsStepIn) -> None:
         self._check(self.lib.mars_step_enqueue(self.ctx, C.byref(si)))
@@ -245,6 +259,13 @@ class MarsEngine:
             ret_benefit=_arr(o.ret_benefit, o.n_retention, np.float64),
             ret_cost=_arr(o.ret_cost, o.n_retention, np.float64),
             ret_deadline=_arr(o.ret_deadline, o.n_retention, np.float64),
+            decode_level=_arr(o.decode_level, o.n_decode, np.uint8),
+            prefill_level=_arr(o.prefill_level, o.n_prefill, np.uint8),
+            fin_rows=_arr(o.fin_rows, o.n_finish, np.uint32),
+            fin_pin=_arr(o.fin_pin, o.n_finish, np.uint8),
+            fin_benefit=_arr(o.fin_benefit, o.n_finish, np.float64),
+            fin_cost=_arr(o.fin_cost, o.n_finish, np.float64),
+            fin_deadline=_arr(o.fin_deadline, o.n_finish, np.float64),
             n_ready=o.n_ready, n_promoted=o.n_promoted, pack_mode=o.pack_mode,
             total_tokens=o.total_tokens, free_after_expiry=o.free_after_expiry,
             free_blocks=o.free_blocks, limit=o.limit, slots=o.slots)

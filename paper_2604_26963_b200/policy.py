@@ -1,0 +1,406 @@
+"""``GpuMarsPolicy``: drop-in for ``agentsched.baselines.MarsPolicy``.
+
+Same hook surface as the reference plugin API (``PolicyBase``,
+baselines.py:56-101) and the same ablation switches (baselines.py:334-349);
+register it under a new ``POLICY_KINDS`` entry or pass it to
+``run_simulation`` directly.  Each ``plan_tick`` runs ONE device step on the
+B200 (promote_waiting + window top-k + build_plan with chunk fitting and
+reclamation, scheduler.py:111-128/283-371, baselines.py:406-455) and replays
+the step's ordered journal through the caller's own ``KvPool`` and evictor, so
+the reference's event log comes out byte-identical.
+
+State ownership mirrors the reference: the sim owns ``Call`` objects and the
+pool; the policy's MLFQ states and pin registry live in the device session
+table.  ``charge_service`` (on_service) and ``decide_retention`` for rounds
+that finish this tick are evaluated by the same device step, on post-tick
+values (engine.py:503-512), and handed back when the sim asks for them.
+"""
+
+from __future__ import annotations
+
+import math
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _native as N
+from .engine import MarsEngine, make_config
+from .snapshot import DECODE, F_ACTIVE, F_PINNED, PHASE_NAMES, PREFILL
+
+ContractViolation = N.ContractViolation
+_PHASE_CODE = {p: i for i, p in enumerate(PHASE_NAMES)}
+_DROPIN_MODE = (N.MODE_SKIP_EXPIRY | N.MODE_SKIP_PROBE | N.MODE_SKIP_REFRESH | N.MODE_SERVICE
+                | N.MODE_FINISH_RETENTION)
+
+
+def _phase_code(phase) -> int:
+    return _PHASE_CODE[getattr(phase, "value", phase)]
+
+
+def _i64(x) -> int:
+    return 2**63 - 1 if x == math.inf else int(x)
+
+
+class Victim:
+    """scheduler.py:221-225 (fields read by the sim's evictor, sim.py:186-188)."""
+
+    __slots__ = ("session_id", "kind", "blocks")
+
+    def __init__(self, session_id: str, kind: str, blocks: int) -> None:
+        self.session_id, self.kind, self.blocks = session_id, kind, blocks
+
+    def __repr__(self) -> str:
+        return f"Victim({self.session_id!r}, {self.kind!r}, {self.blocks})"
+
+
+class TickPlan:
+    """scheduler.py:275-280."""
+
+    def __init__(self) -> None:
+        self.decode_ids: List[str] = []
+        self.prefill_grants: List[Tuple[str, int]] = []
+        self.evictions: List[Victim] = []
+        self.total_tokens = 0
+
+
+class RetentionDecision:
+    """scheduler.py:175-180."""
+
+    __slots__ = ("pin", "benefit_s", "cost_s", "retention_deadline")
+
+    def __init__(self, pin: bool, benefit_s: float, cost_s: float, retention_deadline: float):
+        self.pin, self.benefit_s, self.cost_s = pin, benefit_s, cost_s
+        self.retention_deadline = retention_deadline
+
+
+def config_from(mlfq=None, retention=None, pressure=None, controller=None,
+                enable_coordinator=True, enable_coscheduler=True, gpu=None) -> N.MarsConfig:
+    """mars_config from reference-style config objects (duck-typed)."""
+    cfg = make_config(enable_coordinator, enable_coscheduler)
+    if mlfq is not None:
+        cfg.num_levels = mlfq.num_levels
+        cfg.max_promotions = mlfq.max_promotions
+        cfg.max_decode_slots = mlfq.max_decode_slots
+        cfg.window_size = mlfq.window_size
+        cfg.promotion_wait_s = float(mlfq.promotion_wait_s)
+        for i in range(4):
+            bs = list(mlfq.level_boundaries_tokens) + [math.inf] * 4
+            qs = list(mlfq.level_quotas_tokens) + [math.inf] * 4
+            cfg.level_bounds[i] = _i64(bs[i])
+            cfg.level_quotas[i] = _i64(qs[i])
+    if retention is not None:
+        cfg.deadline_slack = float(retention.deadline_slack)
+        cfg.max_pin_horizon_s = float(retention.max_pin_horizon_s)
+        cfg.pressure_weight_clip = float(retention.pressure_weight_clip)
+    if pressure is not None:
+        for f in ("cpu_high_fraction", "cpu_low_fraction", "kv_high_watermark",
+                  "kv_low_watermark", "ema_smoothing", "initial_tool_estimate_s"):
+            setattr(cfg, f, float(getattr(pressure, f)))
+        cfg.hysteresis_window = int(pressure.hysteresis_window)
+    if controller is not None:
+        cfg.w_min = int(controller.w_min)
+        for f in ("aimd_increase", "aimd_decrease", "control_interval_s", "initial_window",
+                  "cpu_oversubscription", "reserve_fraction", "long_session_fraction"):
+            setattr(cfg, f, float(getattr(controller, f)))
+    if gpu is not None:
+        cfg.token_budget = int(gpu.token_budget_per_tick)
+        cfg.tick_duration_s = float(gpu.tick_duration_s)
+    return cfg
+
+
+class GpuMarsPolicy:
+    """B200 drop-in for MarsPolicy (baselines.py:318-455)."""
+
+    name = "mars"
+    uses_admission_control = True
+
+    def __init__(self, mlfq=None, retention=None, pressure=None, enable_coordinator: bool = True,
+                 enable_coscheduler: bool = True, max_sessions: int = 1 << 16,
+                 device: int = 0, kv_blocks: bool = False) -> None:
+        self._kv_enabled = kv_blocks
+        self.kv = None                 # KvBlockManager once the pool is known
+        self._kv_pending: List[tuple] = []
+        self.mlfq, self.retention, self.pressure = mlfq, retention, pressure
+        self.enable_coordinator = enable_coordinator
+        self.enable_coscheduler = enable_coscheduler
+        self._cfg_args = dict(mlfq=mlfq, retention=retention, pressure=pressure,
+                              enable_coordinator=enable_coordinator,
+                              enable_coscheduler=enable_coscheduler)
+        self._max = int(max_sessions)
+        self._device = device
+        self.eng: Optional[MarsEngine] = None
+        self._gpu_key = None
+        self.calls: Dict[str, object] = {}
+        self._row: Dict[str, int] = {}
+        self._sid: List[str] = []
+        self._max_sid: Optional[str] = None
+        self._ranks_dirty = False
+        self._dev_ready: set = set()
+        self._pins: Dict[str, float] = {}       # sid -> retention deadline (registry view)
+        self._levels: Dict[str, int] = {}       # sid -> MLFQ level (device value)
+        self._admitted: set = set()
+        self._fin: Dict[str, tuple] = {}        # sid -> (ctx, kv, now, usage, ema, decision)
+        self._service: Dict[str, tuple] = {}    # sid -> (tokens, tick_end) charged on device
+        self._replaying = False
+        self.last_window: List[str] = []
+        b = getattr(mlfq, "level_boundaries_tokens", (4_000, 32_000, 128_000, math.inf))
+        self._bounds = tuple(b)
+        self._levels_n = getattr(mlfq, "num_levels", 4)
+        self._tool_prior = getattr(pressure, "initial_tool_estimate_s", 5.0)
+
+    # -- device context ---------------------------------------------------------
+
+    def _engine(self, gpu=None) -> MarsEngine:
+        if self.eng is not None:
+            if gpu is not None and (gpu.token_budget_per_tick, gpu.tick_duration_s) != (
+                    self.eng.cfg.token_budget, self.eng.cfg.tick_duration_s):
+                if self._sid:
+                    raise ContractViolation("GpuModel changed after sessions were registered")
+                self.eng.close()
+                self.eng = None
+        if self.eng is None:
+            cfg = config_from(gpu=gpu, **self._cfg_args)
+            self.eng = MarsEngine(max_rows=self._max, max_queue=1, device=self._device,
+                                  config=cfg)
+        return self.eng
+
+    def close(self) -> None:
+        if self.eng is not None:
+            self.eng.close()
+            self.eng = None
+
+    # -- PolicyBase hooks -----------------------------------------------------------
+
+    def register_call(self, call) -> None:
+        sid = call.session_id
+        self.calls[sid] = call
+        if sid in self._row:
+            return
+        if len(self._sid) >= self._max:
+            raise RuntimeError(f"GpuMarsPolicy: more than max_sessions={self._max} sessions")
+        r = len(self._sid)
+        self._row[sid] = r
+        # rank = position in lexicographic session-id order; a new id that is
+        # not the largest so far shifts the ranks of every larger id
+        if self._max_sid is not None and sid < self._max_sid:
+            self._ranks_dirty = True
+        else:
+            self._max_sid = sid
+        self._sid.append(sid)
+        eng = self._engine()
+        eng.upsert({"phase": np.array([_phase_code(call.phase)], np.uint8),
+                    "flags": np.zeros(1, np.uint8), "rank": np.array([r], np.uint32),
+                    "arrival": np.array([call.arrival_time], np.float64)},
+                   rows=np.array([r]))
+        if self._ranks_dirty:
+            self._sync_ranks()
+
+    def _sync_ranks(self) -> None:
+        order = sorted(range(len(self._sid)), key=self._sid.__getitem__)
+        rank = np.empty(len(order), np.uint32)
+        rank[np.array(order, dtype=np.int64)] = np.arange(len(order), dtype=np.uint32)
+        self._engine().upsert({"rank": rank}, rows=np.arange(len(order)))
+        self._ranks_dirty = False
+
+    def _initial_level(self, tokens: int) -> int:  # scheduler.py:87-97
+        if tokens < 1:
+            raise ContractViolation("context_tokens must be >= 1")
+        for i, b in enumerate(self._bounds):
+            if tokens <= b:
+                return i
+        return self._levels_n - 1
+
+    def on_admit(self, call, now: float) -> None:
+        sid = call.session_id
+        lv = self._initial_level(call.rounds[0].new_prefill_tokens)
+        r = self._row[sid]
+        self._engine().upsert({"level": np.array([lv], np.uint8), "promos": np.zeros(1, np.uint8),
+                               "served": np.zeros(1, np.int64),
+                               "wait_since": np.array([now], np.float64),
+                               "flags": np.array([F_ACTIVE], np.uint8)}, rows=np.array([r]))
+        self._levels[sid] = lv
+        self._admitted.add(sid)
+
+    def on_resume(self, call, now: float) -> None:
+        sid = call.session_id
+        if sid in self._admitted:
+            self._engine().upsert({"wait_since": np.array([now], np.float64)},
+                                  rows=np.array([self._row[sid]]))
+
+    def on_service(self, session_id: str, tokens: int, now: float) -> None:
+        if session_id not in self._admitted or not self.enable_coordinator:
+            return
+        exp = self._service.pop(session_id, None)
+        if exp is not None and exp == (tokens, now):
+            return  # already charged by the device step at tick end
+        # a charge the plan did not predict: apply it to the device row
+        r = self._row[session_id]
+        st = self._engine().read(["level", "served"], rows=np.array([r]))
+        lv, served = int(st["level"][0]), int(st["served"][0]) + int(tokens)
+        if tokens < 0:
+            raise ContractViolation("cannot charge negative service")
+        q = list(getattr(self.mlfq, "level_quotas_tokens", (2_000, 8_000, 32_000, math.inf)))
+        if served > q[lv] and lv < self._levels_n - 1:
+            lv, served = lv + 1, 0
+        self._engine().upsert({"level": np.array([lv], np.uint8),
+                               "served": np.array([served], np.int64),
+                               "wait_since": np.array([now], np.float64)}, rows=np.array([r]))
+        self._levels[session_id] = lv
+
+    def level_of(self, call) -> int:
+        if not self.enable_coordinator:
+            return 0
+        return self._levels[call.session_id]
+
+    def retention_decision(self, call, pool, telemetry, gpu, now):
+        if not self.enable_coscheduler:
+            return None
+        sid = call.session_id
+        ema = telemetry.ema_tool_duration
+        ema = self._tool_prior if ema is None else ema
+        usage = telemetry.kv_usage_ratio
+        pre = self._fin.pop(sid, None)
+        if pre is not None and pre[:5] == (call.context_tokens, call.kv_tokens, now, usage, ema) \
+                and pre[6] == pool.total_blocks:
+            return pre[5]
+        pin, b, c, d = self._engine().retention_batch(
+            np.array([call.context_tokens]), np.array([call.kv_tokens]), pool.total_blocks,
+            usage, ema, now)
+        return RetentionDecision(bool(pin[0]), float(b[0]), float(c[0]), float(d[0]))
+
+    def note_pin(self, call, decision, blocks: int, now: float) -> None:
+        sid = call.session_id
+        r = self._row[sid]
+        lv = self.level_of(call)
+        self._engine().upsert({"flags": np.array([F_ACTIVE | F_PINNED], np.uint8),
+                               "deadline": np.array([decision.retention_deadline], np.float64),
+                               "pinned_blocks": np.array([blocks], np.int32),
+                               "plevel": np.array([lv], np.uint8)},
+                              rows=np.array([r]))
+        self._pins[sid] = decision.retention_deadline
+
+    def expired_pins(self, now: float) -> List[str]:
+        return sorted(sid for sid, dl in self._pins.items() if dl < now)
+
+    def on_evicted(self, session_id: str) -> None:
+        if self._pins.pop(session_id, None) is None:
+            return
+        if self._replaying:
+            return  # the device step already released this pin
+        r = self._row[session_id]
+        call = self.calls[session_id]
+        flags = F_ACTIVE if session_id in self._admitted else 0
+        self._engine().upsert({"flags": np.array([flags], np.uint8),
+                               "kv": np.array([call.kv_tokens], np.int32)}, rows=np.array([r]))
+
+    # -- the tick ---------------------------------------------------------------------
+
+    # -- S5 block IDs: tee of the caller's pool op stream -------------------------
+
+    def _kv_attach(self, pool, gpu) -> None:
+        from .kvstore import OBSERVER_OPS, KvBlockManager
+
+        per_row = -(-gpu.context_limit_tokens // pool.block_size) + 1
+        self.kv = KvBlockManager(self._engine(gpu), pool.total_blocks,
+                                 max_blocks_per_row=min(per_row, pool.total_blocks))
+        inner = pool.observer
+
+        def tee(op, sid, blocks, from_pinned=False):
+            # ops the device step produced itself are already applied on the device
+            if not self._replaying:
+                self._kv_pending.append((OBSERVER_OPS[op], self._row[sid], int(blocks)))
+            if inner is not None:
+                inner(op, sid, blocks, from_pinned)
+
+        pool.observer = tee
+
+    def kv_flush(self) -> None:
+        """Applies pool ops observed since the last step to the device tables."""
+        if self.kv is not None and self._kv_pending:
+            self.kv.apply(self._kv_pending)
+            self._kv_pending = []
+
+    def plan_tick(self, ready: Sequence, pool, gpu, telemetry, now: float, evictor) -> TickPlan:
+        eng = self._engine(gpu)
+        if self._kv_enabled and self.kv is None:
+            self._kv_attach(pool, gpu)
+        self.kv_flush()
+        if self._ranks_dirty:
+            self._sync_ranks()
+        rows = np.fromiter((self._row[c.session_id] for c in ready), dtype=np.int64,
+                           count=len(ready))
+        ready_set = set(rows.tolist())
+        gone = sorted(self._dev_ready - ready_set)
+        n = len(ready)
+        cols = {
+            "phase": np.fromiter((_phase_code(c.phase) for c in ready), np.uint8, n),
+            "flags": np.full(n, F_ACTIVE, np.uint8),
+            "kv": np.fromiter((c.kv_tokens for c in ready), np.int32, n),
+            "context": np.fromiter((c.context_tokens for c in ready), np.int32, n),
+            "rem_decode": np.fromiter((c.remaining_decode for c in ready), np.int32, n),
+            "ready_since": np.fromiter((c.ready_since for c in ready), np.float64, n),
+            "arrival": np.fromiter((c.arrival_time for c in ready), np.float64, n),
+        }
+        if n:
+            eng.upsert(cols, rows=rows)
+        if gone:
+            eng.upsert({"phase": np.array([_phase_code(self.calls[self._sid[r]].phase)
+                                           for r in gone], np.uint8)},
+                       rows=np.array(gone, np.int64))
+        s = N.MarsScalars()
+        s.total_blocks = pool.total_blocks
+        s.free_blocks = pool.free_blocks
+        s.available_kv = pool.free_blocks
+        s.kv_usage_ratio = float(telemetry.kv_usage_ratio)
+        ema = telemetry.ema_tool_duration
+        s.has_ema_tool = int(ema is not None)
+        s.ema_tool = float(ema) if ema is not None else 0.0
+        s.w_adm = 1.0
+        eng.set_scalars(s)
+        eng._check(eng.lib.mars_set_rows(eng.ctx, len(self._sid)))
+        si = eng.step_in(now, False, 0, 0, 1, _DROPIN_MODE)
+        res = eng.step(si)
+        if res.status:
+            raise RuntimeError(f"device step status {res.status}")
+        self._dev_ready = ready_set
+        sid = self._sid
+        plan = TickPlan()
+        self.last_window = [sid[r] for r in res.window_rows]
+        # replay the ordered journal through the caller's pool and evictor so the
+        # observer sees alloc / free / evict in build_plan's order
+        self._replaying = True
+        try:
+            for op, r, k in zip(res.journal_op.tolist(), res.journal_row.tolist(),
+                                res.journal_n.tolist()):
+                if op == 1:
+                    if not pool.allocate(sid[r], k):
+                        raise ContractViolation(f"device plan allocation refused for {sid[r]}")
+                else:
+                    v = Victim(sid[r], "pinned" if op == 3 else "running", k)
+                    evictor(v)
+                    plan.evictions.append(v)
+        finally:
+            self._replaying = False
+        plan.decode_ids = [sid[r] for r in res.decode_rows.tolist()]
+        plan.prefill_grants = [(sid[r], int(g)) for r, g in zip(res.prefill_rows.tolist(),
+                                                                 res.prefill_grants.tolist())]
+        plan.total_tokens = int(res.total_tokens)
+        tick_end = now + gpu.tick_duration_s
+        self._service.clear()
+        for r, lv in zip(res.decode_rows.tolist(), res.decode_level.tolist()):
+            self._levels[sid[r]] = lv
+            self._service[sid[r]] = (1, tick_end)
+        for (r, g), lv in zip(zip(res.prefill_rows.tolist(), res.prefill_grants.tolist()),
+                              res.prefill_level.tolist()):
+            self._levels[sid[r]] = lv
+            self._service[sid[r]] = (g, tick_end)
+        self._fin.clear()
+        ema_v = self._tool_prior if ema is None else ema
+        for r, p, b, c, d in zip(res.fin_rows.tolist(), res.fin_pin.tolist(),
+                                 res.fin_benefit.tolist(), res.fin_cost.tolist(),
+                                 res.fin_deadline.tolist()):
+            call = self.calls[sid[r]]
+            self._fin[sid[r]] = (call.context_tokens + 1, call.kv_tokens + 1, tick_end,
+                                 telemetry.kv_usage_ratio, ema_v,
+                                 RetentionDecision(bool(p), b, c, d), pool.total_blocks)
+        return plan

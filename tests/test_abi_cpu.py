@@ -69,6 +69,7 @@ def test_create_without_gpu_fails_loudly(lib):
 STRUCTS = {
     "mars_config": N.MarsConfig, "mars_cols": N.MarsCols, "mars_scalars": N.MarsScalars,
     "mars_step_in": N.MarsStepIn, "mars_step_out": N.MarsStepOut,
+    "mars_kv_config": N.MarsKvConfig,
 }
 
 

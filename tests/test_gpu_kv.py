@@ -1,0 +1,164 @@
+"""S5 on the B200: block-ID manager parity with the CPU restatement
+(oracle/block_ids.py) and exact KV byte round trips through the host tier."""
+
+import random
+
+import numpy as np
+import pytest
+
+from oracle.block_ids import BlockIdPool
+from oracle.snapshot_step import run_step
+from paper_2604_26963_b200 import _native as N
+from paper_2604_26963_b200.engine import MarsEngine, make_config
+from paper_2604_26963_b200.kvstore import KvBlockManager, host_link_peak
+from paper_2604_26963_b200.policy import GpuMarsPolicy
+from paper_2604_26963_b200.snapshot import F_PINNED, snapshot_v1
+from paper_2604_26963_b200.admission import balance_and_admit
+from tests._sim import run_sim
+
+pytestmark = pytest.mark.gpu
+
+
+def _same_state(kv, pool: BlockIdPool, rows):
+    for sid, r in rows.items():
+        assert kv.table(r).tolist() == pool.table(sid), sid
+    top, depth, fresh, status = kv.state(64)
+    assert status == 0
+    assert top.tolist() == pool.top(64)
+    assert depth + (pool.total - fresh) == len(pool.stack)
+
+
+def test_fuzzed_op_stream_matches_the_restatement():
+    # acceptance criterion 3's op mix (test_acceptance.py:334-366) on block IDs
+    rng = random.Random(303)
+    total = 512
+    eng = MarsEngine(max_rows=4096, max_queue=1)
+    kv = KvBlockManager(eng, total, max_blocks_per_row=total)
+    ref = BlockIdPool(total)
+    alloc, pinned, rows = {}, {}, {}
+    ops = []
+    for step in range(20_000):
+        choices = ["alloc_new"]
+        if alloc:
+            choices += ["alloc_more", "free_some", "free_all", "pin"]
+        if pinned:
+            choices += ["unpin", "release_pinned"]
+        op = rng.choice(choices)
+        free_now = total - sum(alloc.values()) - sum(pinned.values())
+        if op in ("alloc_new", "alloc_more"):
+            n = rng.randrange(1, 48)
+            if n > free_now:
+                continue
+            sid = f"f{len(rows)}" if op == "alloc_new" else rng.choice(sorted(alloc))
+            rows.setdefault(sid, len(rows))
+            alloc[sid] = alloc.get(sid, 0) + n
+            ref.apply("alloc", sid, n)
+            ops.append((N.KV_ALLOC, rows[sid], n))
+        elif op in ("free_some", "free_all"):
+            sid = rng.choice(sorted(alloc))
+            n = rng.randrange(1, alloc[sid] + 1) if op == "free_some" else alloc[sid]
+            alloc[sid] -= n
+            if not alloc[sid]:
+                del alloc[sid]
+            ref.apply("free", sid, n)
+            ops.append((N.KV_FREE, rows[sid], n))
+        elif op == "pin":
+            sid = rng.choice(sorted(alloc))
+            pinned[sid] = alloc.pop(sid)
+            ops.append((N.KV_PIN, rows[sid], pinned[sid]))
+        elif op == "unpin":
+            sid = rng.choice(sorted(pinned))
+            alloc[sid] = pinned.pop(sid)
+            ops.append((N.KV_UNPIN, rows[sid], alloc[sid]))
+        else:
+            sid = rng.choice(sorted(pinned))
+            n = pinned.pop(sid)
+            ref.apply("free", sid, n)
+            ops.append((N.KV_FREE, rows[sid], n))
+        if len(ops) >= 2_000:
+            kv.apply(ops)
+            ops = []
+            _same_state(kv, ref, {s: r for s, r in rows.items() if s in ref.tables})
+    kv.apply(ops)
+    _same_state(kv, ref, rows)
+    eng.close()
+
+
+def test_step_journal_updates_block_tables_like_the_restatement():
+    snap = snapshot_v1(20_000, seed=51, pool="pressure")
+    c = snap.cols
+    eng = MarsEngine(max_rows=snap.n, max_queue=len(snap.queue),
+                     config=make_config(initial_window=snap.initial_window))
+    eng.load_snapshot(snap)
+    kv = KvBlockManager(eng, snap.total_blocks, max_blocks_per_row=1 << 14)
+    ref = BlockIdPool(snap.total_blocks)
+    held = -(-c["kv"].astype(np.int64) // 16)
+    init = []
+    for r in range(snap.n):
+        h = int(c["pinned_blocks"][r]) if c["flags"][r] & F_PINNED else int(held[r])
+        if h:
+            init.append((N.KV_ALLOC, r, h))
+            ref.apply("alloc", snap.sid(r), h)
+    kv.apply(init)
+    res = eng.step(eng.step_in(snap.now, True, snap.active_tools, 0, snap.worker_slots))
+    assert res.status == 0
+    out = run_step(snap.copy())
+    assert len(out["evictions"]) > 0
+    for op, r, n, from_pinned in out["expiry_journal"] + out["journal"]:
+        ref.apply(op, snap.sid(r), n)
+    touched = {snap.sid(r) for _, r, _, _ in out["expiry_journal"] + out["journal"]}
+    _same_state(kv, ref, {s: int(s[1:]) for s in touched})
+    eng.close()
+
+
+@pytest.mark.parametrize("method", [0, 1])
+def test_kv_bytes_round_trip_through_the_host_tier(method):
+    bb, layers = 2 << 20, 32
+    eng = MarsEngine(max_rows=64, max_queue=1)
+    kv = KvBlockManager(eng, 256, max_blocks_per_row=256, block_bytes=bb, layers=layers,
+                        host_blocks=64)
+    host = kv.host_view()
+    rng = np.random.default_rng(7)
+    host[:16] = rng.integers(0, 256, size=(16, bb), dtype=np.uint8)
+    src = host[:16].copy()
+    ids = rng.choice(256, size=16, replace=False).astype(np.uint32)
+    kv.restore(ids, slot0=0, method=method)        # host slots 0..15 -> scattered blocks
+    host[:16] = 0
+    kv.evict(ids, slot0=32, method=method)         # blocks -> host slots 32..47
+    assert np.array_equal(host[32:48], src)
+    # per-block checksums survive a second scattered hop
+    ids2 = rng.choice(256, size=16, replace=False).astype(np.uint32)
+    kv.restore(ids2, slot0=32, method=1 - method)
+    kv.evict(ids2, slot0=0, method=method)
+    assert [int(x) for x in host[:16].sum(axis=1, dtype=np.uint64)] == \
+        [int(x) for x in src.sum(axis=1, dtype=np.uint64)]
+    eng.close()
+
+
+def test_host_link_peak_is_measurable():
+    eng = MarsEngine(max_rows=16, max_queue=1)
+    d2h, h2d, bi = host_link_peak(eng, 1 << 28, 3)
+    eng.close()
+    assert d2h > 1.0 and h2d > 1.0 and bi > 1.0
+
+
+@pytest.mark.parametrize("key", ["demo64/mars", "faceoff200/mars"])
+def test_dropin_block_ids_follow_the_reference_op_stream(key):
+    """Drop-in run with the device block manager teed onto the pool: the log
+    stays byte-identical and the final tables equal the restatement replaying
+    the reference's own pool op stream."""
+    import hashlib
+
+    from tests._sim import SIM
+
+    pol = GpuMarsPolicy(kv_blocks=True)
+    out = run_sim(key, policy=pol, balance_and_admit=balance_and_admit)
+    pol.kv_flush()
+    assert hashlib.sha256(out.log.jsonl_bytes()).hexdigest() == SIM[key]["sha256"]
+    ref = BlockIdPool(out.pool.total_blocks)
+    for rec in out.events:
+        if rec["kind"] in ("alloc", "free", "pin", "unpin"):
+            ref.apply(rec["kind"], rec["session_id"], rec["blocks"])
+    rows = {sid: pol._row[sid] for sid in pol._row}
+    _same_state(pol.kv, ref, rows)
+    pol.close()

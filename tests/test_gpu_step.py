@@ -97,6 +97,11 @@ def test_restore_replays_identically():
     a = canon(canonical(eng.step(si), eng, snap))
     eng.restore()
     b = canon(canonical(eng.step(si), eng, snap))
+    eng.set_graph(True)  # whole-step CUDA graph replays the same decisions
+    for _ in range(2):
+        eng.restore()
+        c = canon(canonical(eng.step(si), eng, snap))
+        assert c == a
     eng.close()
     assert a == b
 

@@ -31,20 +31,7 @@ SIM = _load("sim_logs.json")
 SNAP = _load("snapshot_steps.json")
 KAT = _load("kat.json")
 
-VARIANT_KW = {"mars": {}, "mars-no-coordinator": {"enable_coordinator": False},
-              "mars-no-coscheduler": {"enable_coscheduler": False}, "mars-no-control": {}}
-
-
-def run_oracle_sim(key, policy=None):
-    spec = SIM[key]
-    traces = tracefile.load(os.path.join(GOLDEN, spec["trace"]))
-    eng = loop.Engine(**spec["engine"])
-    variant = key.split("/")[1]
-    pol = policy if policy is not None else op.MarsOracle(**VARIANT_KW[variant])
-    run = dict(spec["run"])
-    if "controller" in run:
-        run["controller"] = oa.Controller(**run["controller"])
-    return loop.run(traces, eng, pol, **run)
+from tests._sim import run_sim as run_oracle_sim
 
 
 @pytest.mark.parametrize("key", sorted(SIM))
