@@ -256,27 +256,36 @@ def main():
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
     launches = 0
-    ktimes = []
-    # per-kernel CUDA events inside the library (same streams as the kernels)
-    eng.set_profiling(True)
     with Clocks(local) as clk:
         barrier()
         for i in range(a.steps):
             eng.restore()
             eng.flush_l2(flush)
             starts[i].record(stream)
-            eng.enqueue(si)
+            eng.enqueue(si)          # one CUDA-graph launch per step
             ends[i].record(stream)
             launches += eng.launches()
-            ktimes.append(eng.kernel_times())  # syncs after the step (outside the events)
         barrier()
-    eng.set_profiling(False)
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     dev_ms = sum(step_ms)
     t = torch.tensor([dev_ms], dtype=torch.float64, device="cuda")
     if dist is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_per_step = float(t.item()) / a.steps
+
+    # per-kernel device times: CUDA events recorded by the library on the
+    # stream each kernel runs on (stream launches: event timing is not
+    # available inside graphs), same restore + L2 flush before every step
+    eng.set_graph(False)
+    eng.set_profiling(True)
+    ktimes = []
+    for i in range(a.steps):
+        eng.restore()
+        eng.flush_l2(flush)
+        eng.enqueue(si)
+        ktimes.append(eng.kernel_times())
+    eng.set_profiling(False)
+    eng.set_graph(True)
     kernel_ms = {k: statistics.median([kt[k] for kt in ktimes]) for k in ktimes[0]}
     scan_avg = sum(kt["k_scan"] for kt in ktimes) / len(ktimes)
 

@@ -258,6 +258,9 @@ int mars_kv_host_ptr(mars_ctx* ctx, void** host, void** device);
 int mars_host_link_peak(mars_ctx* ctx, int64_t bytes, int reps, double* d2h_gbs, double* h2d_gbs,
                         double* bidir_gbs);
 
+/* drain the context's stream and report any pending CUDA error */
+int mars_sync(mars_ctx* ctx);
+
 /* number of kernel launches issued by the last step (incl. early-exit ones) */
 int mars_last_launch_count(mars_ctx* ctx);
 

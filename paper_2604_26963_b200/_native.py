@@ -124,6 +124,7 @@ _SIGS = {
     "mars_step_enqueue": (i32, [C.c_void_p, P(MarsStepIn)]),
     "mars_step_fetch": (i32, [C.c_void_p, P(MarsStepOut)]),
     "mars_set_graph": (i32, [C.c_void_p, C.c_int]),
+    "mars_sync": (i32, [C.c_void_p]),
     "mars_kv_init": (i32, [C.c_void_p, C.c_void_p]),
     "mars_kv_apply": (i32, [C.c_void_p, i64, C.c_void_p, C.c_void_p, C.c_void_p]),
     "mars_kv_table": (i32, [C.c_void_p, u32, i64, C.c_void_p, P(i64)]),

@@ -590,7 +590,7 @@ int mars_step_enqueue(mars_ctx* ctx, const mars_step_in* in) {
   CK(cudaSetDevice(ctx->device));
   *ctx->h_in = *in;
   LaunchArgs a = launch_args(ctx, in);
-  if (!ctx->use_graph) {
+  if (!ctx->use_graph || ctx->profiling) {  // event timing does not work inside graphs
     ctx->last_launches = mars_enqueue_step(&a);
     CK(cudaGetLastError());
     return MARS_OK;
@@ -622,6 +622,15 @@ int mars_step_enqueue(mars_ctx* ctx, const mars_step_in* in) {
   }
   CK(cudaGraphLaunch(ctx->graph_exec, ctx->stream));
   ctx->last_launches = ctx->graph_launches;
+  return MARS_OK;
+}
+
+int mars_sync(mars_ctx* ctx) {
+  if (!ctx) return MARS_ERR_ARG;
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaStreamSynchronize(ctx->side));
+  CK(cudaGetLastError());
   return MARS_OK;
 }
 
@@ -802,7 +811,10 @@ int mars_kernel_times(mars_ctx* ctx, float* ms, int n) {
     ms[k] = -1.0f;
     if (ctx->profiling && ctx->prof_used[k]) {
       float t = 0;
-      if (cudaEventElapsedTime(&t, ctx->prof[2 * k], ctx->prof[2 * k + 1]) == cudaSuccess) ms[k] = t;
+      if (cudaEventElapsedTime(&t, ctx->prof[2 * k], ctx->prof[2 * k + 1]) == cudaSuccess)
+        ms[k] = t;
+      else
+        cudaGetLastError();  // do not leave the failure pending for the next call
     }
   }
   return MARS_OK;

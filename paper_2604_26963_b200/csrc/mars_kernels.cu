@@ -381,17 +381,30 @@ __global__ void __launch_bounds__(SCAN_TPB) k_scan(Tab t, Cfg c, Work* w, Bufs b
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  if (threadIdx.x == 0) {
-    // exclusive prefix of the per-CTA expired segments (row order == CTA order)
+  {
+    // exclusive prefix of the per-CTA expired segments (row order == CTA order),
+    // two counts per thread + one block scan (gridDim <= MAX_SCAN_CTAS = 2 * 512)
     volatile Work* vw0 = w;
-    int acc = 0;
-    for (int q = 0; q < (int)gridDim.x; ++q) {
-      int x = vw0->exp_seg_cnt[q];
-      w->exp_seg_off[q] = acc;
-      acc += x;
+    const int G = gridDim.x;
+    int i0 = 2 * threadIdx.x, i1 = i0 + 1;
+    int c0 = i0 < G ? vw0->exp_seg_cnt[i0] : 0;
+    int c1 = i1 < G ? vw0->exp_seg_cnt[i1] : 0;
+    shu[threadIdx.x] = (u32)(c0 + c1);
+    __syncthreads();
+    for (int off = 1; off < (int)blockDim.x; off <<= 1) {
+      u32 x = threadIdx.x >= (unsigned)off ? shu[threadIdx.x - off] : 0u;
+      __syncthreads();
+      shu[threadIdx.x] += x;
+      __syncthreads();
     }
-    w->scan_ctas = gridDim.x;
-    w->scan_chunk = chunk;
+    int excl = (int)shu[threadIdx.x] - (c0 + c1);
+    if (i0 < G) w->exp_seg_off[i0] = excl;
+    if (i1 < G) w->exp_seg_off[i1] = excl + c0;
+    if (threadIdx.x == 0) {
+      w->scan_ctas = G;
+      w->scan_chunk = chunk;
+    }
+    __syncthreads();
   }
 
   // ---- last CTA: finalise ------------------------------------------------

@@ -32,7 +32,7 @@ def test_fuzzed_op_stream_matches_the_restatement():
     # acceptance criterion 3's op mix (test_acceptance.py:334-366) on block IDs
     rng = random.Random(303)
     total = 512
-    eng = MarsEngine(max_rows=4096, max_queue=1)
+    eng = MarsEngine(max_rows=32768, max_queue=1)
     kv = KvBlockManager(eng, total, max_blocks_per_row=total)
     ref = BlockIdPool(total)
     alloc, pinned, rows = {}, {}, {}
