@@ -140,6 +140,9 @@ typedef struct mars_scalars {
                                          this tick, on post-tick values (sim.py:250) */
 #define MARS_MODE_RANK_ORDERED 64     /* caller asserts rank[row] == row order (row order is
                                          session-id order): expired pins need no sort */
+#define MARS_MODE_SHARDED 128         /* this context is one replica of a sharded engine:
+                                         the control plane runs on all-reduced counters and
+                                         the all-gathered admission list (mars_step_phase) */
 
 typedef struct mars_step_in {
   double now;
@@ -257,6 +260,19 @@ int mars_kv_host_ptr(mars_ctx* ctx, void** host, void** device);
 /* pinned cudaMemcpyAsync peak of the host link: best of `reps` per direction */
 int mars_host_link_peak(mars_ctx* ctx, int64_t bytes, int reps, double* d2h_gbs, double* h2d_gbs,
                         double* bidir_gbs);
+
+/* ---- sharded engine: one context per GPU, sessions partitioned across
+ * replicas; S1/S2/S4/S5 replica-local, the control plane global.
+ * A step is mars_step_phase(1) -> all-reduce(sum) of the XC_N int64 counters
+ * at `xc` -> all-gather of `send_words` uint64 from `xsend` into `xrecv`
+ * (rank-major) -> mars_step_phase(2) -> mars_step_fetch.  The collectives
+ * are the caller's (NCCL through torch.distributed), on the same stream. */
+int mars_shard_init(mars_ctx* ctx, int world, int rank);
+int mars_shard_buffers(mars_ctx* ctx, void** xc, void** xsend, void** xrecv, int64_t* send_words);
+/* global list positions of the local admission entries (dense over the union) */
+int mars_set_queue_gpos(mars_ctx* ctx, int64_t n, const uint32_t* gpos);
+int mars_get_queue_gpos(mars_ctx* ctx, int64_t cap, uint32_t* gpos, int64_t* n);  /* sync */
+int mars_step_phase(mars_ctx* ctx, const mars_step_in* in, int phase);
 
 /* drain the context's stream and report any pending CUDA error */
 int mars_sync(mars_ctx* ctx);

@@ -84,7 +84,8 @@ class MarsStepIn(C.Structure):
 
 
 MODE_SKIP_EXPIRY, MODE_SKIP_PROBE, MODE_SKIP_REFRESH, MODE_NO_ROWS = 1, 2, 4, 8
-MODE_SERVICE, MODE_FINISH_RETENTION, MODE_RANK_ORDERED = 16, 32, 64
+MODE_SERVICE, MODE_FINISH_RETENTION, MODE_RANK_ORDERED, MODE_SHARDED = 16, 32, 64, 128
+XC_N = 8
 
 
 class MarsStepOut(C.Structure):
@@ -125,6 +126,12 @@ _SIGS = {
     "mars_step_fetch": (i32, [C.c_void_p, P(MarsStepOut)]),
     "mars_set_graph": (i32, [C.c_void_p, C.c_int]),
     "mars_sync": (i32, [C.c_void_p]),
+    "mars_shard_init": (i32, [C.c_void_p, C.c_int, C.c_int]),
+    "mars_shard_buffers": (i32, [C.c_void_p, P(C.c_void_p), P(C.c_void_p), P(C.c_void_p),
+                                 P(i64)]),
+    "mars_set_queue_gpos": (i32, [C.c_void_p, i64, C.c_void_p]),
+    "mars_get_queue_gpos": (i32, [C.c_void_p, i64, C.c_void_p, P(i64)]),
+    "mars_step_phase": (i32, [C.c_void_p, P(MarsStepIn), C.c_int]),
     "mars_kv_init": (i32, [C.c_void_p, C.c_void_p]),
     "mars_kv_apply": (i32, [C.c_void_p, i64, C.c_void_p, C.c_void_p, C.c_void_p]),
     "mars_kv_table": (i32, [C.c_void_p, u32, i64, C.c_void_p, P(i64)]),

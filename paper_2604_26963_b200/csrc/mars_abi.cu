@@ -5,7 +5,9 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <algorithm>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "mars_internal.cuh"
@@ -75,6 +77,8 @@ struct mars_ctx {
   void* kv_host = nullptr;          // pinned, mapped
   unsigned char* kv_stage = nullptr; // device staging for op streams / ids
   i64 kv_stage_bytes = 0;
+  // sharded replica (mars_shard_init)
+  Xchg x = {};
 };
 
 static int fail(mars_ctx* c, int code, const char* fmt, ...) {
@@ -255,6 +259,7 @@ int mars_create(const mars_config* hcfg, int device, int64_t max_rows, int64_t m
     ALLOC(q.row[i], Qc * 4);
     ALLOC(q.req[i], Qc * 4);
     ALLOC(q.lng[i], Qc);
+    ALLOC(q.gpos[i], Qc * 4);
   }
   i64 Lc = Qc > R ? Qc : R;
   Lsd* ls[2] = {&ctx->qlsd, &ctx->xlsd};
@@ -275,6 +280,8 @@ int mars_create(const mars_config* hcfg, int device, int64_t max_rows, int64_t m
   ALLOC(b.exp_seg_row, R * 4);
   ALLOC(b.exp_seg_blk, R * 4);
   ALLOC(b.exp_seg_rank, R * 4);
+  ALLOC(b.tile_cnt, (R / 4096 + 2) * 4);
+  ALLOC(b.tile_off, (R / 4096 + 2) * 4);
   ALLOC(b.exp_row, R * 4);
   ALLOC(b.exp_blk, R * 4);
   ALLOC(b.exp_rank, R * 4);
@@ -368,6 +375,7 @@ int mars_destroy(mars_ctx* ctx) {
     cudaFree(ctx->queue.row[i]);
     cudaFree(ctx->queue.req[i]);
     cudaFree(ctx->queue.lng[i]);
+    cudaFree(ctx->queue.gpos[i]);
     cudaFree(ctx->qlsd.k[i]);
     cudaFree(ctx->qlsd.v[i]);
     cudaFree(ctx->xlsd.k[i]);
@@ -379,7 +387,7 @@ int mars_destroy(mars_ctx* ctx) {
   cudaFree(ctx->sc);
   cudaFree(ctx->qsel);
   Bufs& b = ctx->bufs;
-  void* bs[] = {b.exp_seg_row, b.exp_seg_blk, b.exp_seg_rank, b.exp_row, b.exp_blk, b.exp_rank, b.exp_row_sorted, b.exp_blk_sorted, b.wc_hi,
+  void* bs[] = {b.exp_seg_row, b.exp_seg_blk, b.exp_seg_rank, b.tile_cnt, b.tile_off, b.exp_row, b.exp_blk, b.exp_rank, b.exp_row_sorted, b.exp_blk_sorted, b.wc_hi,
                 b.wc_lo, b.wc_row, b.vc_key, b.vc_whi, b.vc_wlo, b.vc_row, b.vc_blk, b.ret_row,
                 b.ret_pin, b.ret_b, b.ret_c, b.ret_d, b.admitted, b.win_rows, b.dec_rows,
                 b.pre_rows, b.pre_grant, b.ev_row, b.ev_kind, b.ev_blk, b.j_op, b.j_row, b.j_n,
@@ -401,6 +409,11 @@ int mars_destroy(mars_ctx* ctx) {
     void* kp[] = {k.fs, k.chunks, k.cfs, k.dir, k.len, k.s, k.data, ctx->kv_stage};
     for (void* p : kp) cudaFree(p);
     if (ctx->kv_host) cudaFreeHost(ctx->kv_host);
+  }
+  {
+    Xchg& x = ctx->x;
+    void* xp[] = {x.xc, x.xsend, x.xrecv, x.gq_row, x.gq_req, x.gq_lng, x.adm_idx};
+    for (void* p : xp) cudaFree(p);
   }
   for (auto& e : ctx->prof)
     if (e) cudaEventDestroy(e);
@@ -582,6 +595,18 @@ static LaunchArgs launch_args(mars_ctx* ctx, const mars_step_in* in) {
   a.prof = ctx->profiling ? ctx->prof : nullptr;
   a.prof_used = ctx->prof_used;
   a.kv = ctx->kv_on ? &ctx->kv : nullptr;
+  a.phase = 0;
+  a.sharded = (in->mode & MARS_MODE_SHARDED) ? 1 : 0;
+  a.x = ctx->x;
+  a.gq.row[0] = a.gq.row[1] = ctx->x.gq_row;
+  a.gq.req[0] = a.gq.req[1] = ctx->x.gq_req;
+  a.gq.lng[0] = a.gq.lng[1] = ctx->x.gq_lng;
+  a.gq.gpos[0] = a.gq.gpos[1] = nullptr;
+  a.gq.cap = ctx->x.cap * ctx->x.world;
+  if (a.sharded) {
+    a.queue_upper = ctx->x.cap * ctx->x.world;
+    a.queue_passes = a.queue_upper > SORT_CAP ? 4 : 0;
+  }
   return a;
 }
 
@@ -659,7 +684,9 @@ int mars_step_fetch(mars_ctx* ctx, mars_step_out* o) {
   memset(o, 0, sizeof *o);
   o->status = w.status;
   o->n_expired = w.n_exp;
-  o->n_admitted = (int32_t)w.take;
+  const bool sharded = (ctx->h_in->mode & MARS_MODE_SHARDED) != 0;
+  const i64 n_adm = sharded ? (i64)w.n_adm_own : w.take;
+  o->n_admitted = (int32_t)n_adm;
   o->n_window = w.n_window;
   o->n_decode = w.n_dec;
   o->n_prefill = w.n_pre;
@@ -677,7 +704,9 @@ int mars_step_fetch(mars_ctx* ctx, mars_step_out* o) {
   size_t off = 0;
   o->expired_rows = (const uint32_t*)pull(ctx, off, b.exp_row_sorted, (size_t)w.n_exp * 4);
   o->expired_blocks = (const int32_t*)pull(ctx, off, b.exp_blk_sorted, (size_t)w.n_exp * 4);
-  o->admitted_rows = (const uint32_t*)pull(ctx, off, b.admitted, (size_t)w.take * 4);
+  o->admitted_rows = (const uint32_t*)pull(ctx, off, b.admitted, (size_t)n_adm * 4);
+  const uint32_t* adm_idx = nullptr;
+  if (sharded) adm_idx = (const uint32_t*)pull(ctx, off, ctx->x.adm_idx, (size_t)n_adm * 4);
   o->window_rows = (const uint32_t*)pull(ctx, off, b.win_rows, (size_t)w.n_window * 4);
   o->decode_rows = (const uint32_t*)pull(ctx, off, b.dec_rows, (size_t)w.n_dec * 4);
   o->prefill_rows = (const uint32_t*)pull(ctx, off, b.pre_rows, (size_t)w.n_pre * 4);
@@ -705,11 +734,25 @@ int mars_step_fetch(mars_ctx* ctx, mars_step_out* o) {
   o->fin_deadline = (const double*)pull(ctx, off, b.fin_d, (size_t)w.n_finish * 8);
   CK(cudaStreamSynchronize(ctx->stream));
   CK(cudaGetLastError());
+  if (sharded && n_adm > 1) {
+    // this replica's admitted rows in global packed order
+    std::vector<std::pair<uint32_t, uint32_t>> pr((size_t)n_adm);
+    for (i64 i = 0; i < n_adm; ++i) pr[i] = {adm_idx[i], o->admitted_rows[i]};
+    std::sort(pr.begin(), pr.end());
+    uint32_t* dst = const_cast<uint32_t*>(o->admitted_rows);
+    for (i64 i = 0; i < n_adm; ++i) dst[i] = pr[i].second;
+  }
   // free_blocks after the plan
   int64_t fb = 0;
   CK(cudaMemcpy(&fb, &ctx->sc->free_blocks, 8, cudaMemcpyDeviceToHost));
   o->free_blocks = fb;
-  ctx->q_upper -= w.take;
+  if (sharded) {
+    int64_t ql = 0;
+    CK(cudaMemcpy(&ql, &ctx->sc->queue_len, 8, cudaMemcpyDeviceToHost));
+    ctx->q_upper = ql;
+  } else {
+    ctx->q_upper -= w.take;
+  }
   if (ctx->q_upper < 0) ctx->q_upper = 0;
   return MARS_OK;
 }
@@ -718,6 +761,89 @@ int mars_step(mars_ctx* ctx, const mars_step_in* in, mars_step_out* out) {
   int rc = mars_step_enqueue(ctx, in);
   if (rc) return rc;
   return mars_step_fetch(ctx, out);
+}
+
+// ---------------------------------------------------------------------------
+// sharded replicas
+// ---------------------------------------------------------------------------
+
+int mars_shard_init(mars_ctx* ctx, int world, int rank) {
+  if (!ctx || world < 1 || rank < 0 || rank >= world) return MARS_ERR_ARG;
+  CK(cudaSetDevice(ctx->device));
+  Xchg& x = ctx->x;
+  if (x.xc) return fail(ctx, MARS_ERR_ARG, "already sharded");
+  x.world = world;
+  x.rank = rank;
+  x.cap = ctx->max_queue;
+  const i64 words = 1 + 2 * x.cap;
+  CK(cudaMalloc((void**)&x.xc, XC_N * 8));
+  CK(cudaMemset(x.xc, 0, XC_N * 8));
+  CK(cudaMalloc((void**)&x.xsend, words * 8));
+  CK(cudaMalloc((void**)&x.xrecv, words * 8 * world));
+  CK(cudaMalloc((void**)&x.gq_row, x.cap * world * 4));
+  CK(cudaMalloc((void**)&x.gq_req, x.cap * world * 4));
+  CK(cudaMalloc((void**)&x.gq_lng, x.cap * world));
+  CK(cudaMalloc((void**)&x.adm_idx, x.cap * 4));
+  // the all-gathered list can be world x longer than the local one
+  for (Lsd* l : {&ctx->qlsd}) {
+    if (l->cap < x.cap * world) {
+      for (int i = 0; i < 2; ++i) {
+        cudaFree(l->k[i]);
+        cudaFree(l->v[i]);
+        CK(cudaMalloc((void**)&l->k[i], x.cap * world * 8));
+        CK(cudaMalloc((void**)&l->v[i], x.cap * world * 4));
+      }
+      l->cap = x.cap * world;
+    }
+  }
+  return MARS_OK;
+}
+
+int mars_shard_buffers(mars_ctx* ctx, void** xc, void** xsend, void** xrecv, int64_t* send_words) {
+  if (!ctx || !ctx->x.xc) return MARS_ERR_ARG;
+  if (xc) *xc = ctx->x.xc;
+  if (xsend) *xsend = ctx->x.xsend;
+  if (xrecv) *xrecv = ctx->x.xrecv;
+  if (send_words) *send_words = 1 + 2 * ctx->x.cap;
+  return MARS_OK;
+}
+
+int mars_set_queue_gpos(mars_ctx* ctx, int64_t n, const uint32_t* gpos) {
+  if (!ctx || n < 0) return MARS_ERR_ARG;
+  if (n > ctx->max_queue) return MARS_ERR_CAPACITY;
+  CK(cudaSetDevice(ctx->device));
+  i32 sel = 0;
+  CK(cudaMemcpyAsync(&sel, ctx->qsel, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (n) CK(cudaMemcpy(ctx->queue.gpos[sel], gpos, n * 4, cudaMemcpyHostToDevice));
+  return MARS_OK;
+}
+
+int mars_get_queue_gpos(mars_ctx* ctx, int64_t cap, uint32_t* gpos, int64_t* n) {
+  if (!ctx || !n) return MARS_ERR_ARG;
+  CK(cudaSetDevice(ctx->device));
+  int64_t len = 0;
+  i32 sel = 0;
+  CK(cudaMemcpyAsync(&len, &ctx->sc->queue_len, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(&sel, ctx->qsel, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  *n = len;
+  if (gpos && len) CK(cudaMemcpy(gpos, ctx->queue.gpos[sel], (len < cap ? len : cap) * 4,
+                                 cudaMemcpyDeviceToHost));
+  return MARS_OK;
+}
+
+int mars_step_phase(mars_ctx* ctx, const mars_step_in* in, int phase) {
+  if (!ctx || !in || phase < 1 || phase > 2) return MARS_ERR_ARG;
+  if (!ctx->x.xc || !(in->mode & MARS_MODE_SHARDED))
+    return fail(ctx, MARS_ERR_ARG, "mars_step_phase needs mars_shard_init + MARS_MODE_SHARDED");
+  CK(cudaSetDevice(ctx->device));
+  if (phase == 1) *ctx->h_in = *in;
+  LaunchArgs a = launch_args(ctx, ctx->h_in);
+  a.phase = phase;
+  ctx->last_launches = mars_enqueue_step(&a) + (phase == 2 ? ctx->last_launches : 0);
+  CK(cudaGetLastError());
+  return MARS_OK;
 }
 
 int mars_retention_batch(mars_ctx* ctx, int64_t n, const int32_t* context, const int32_t* kv,

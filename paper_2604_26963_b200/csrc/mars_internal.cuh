@@ -17,7 +17,7 @@ typedef int64_t i64;
 #define HIST_BINS 4096
 #define WIN_MAX 128
 #define SORT_CAP 4096         // bitonic sort capacity of the single-CTA selector
-#define VSEL 1024             // victim-stream target length (prefix of reclaim order)
+#define VSEL 256              // victim-stream target length (prefix of reclaim order)
 #define VSTREAM_CAP 2048      // victim stream entries kept in shared memory
 #define LSD_G 148             // CTAs of the multi-CTA LSD radix sort
 #define SCAN_RPT 4            // consecutive rows per thread in the table scans
@@ -62,7 +62,23 @@ struct Queue {
   u32 *row[2];
   i32 *req[2];
   u8 *lng[2];
+  u32 *gpos[2];  // sharded mode: global list position of each local entry
   i64 cap;
+};
+
+// sharded (multi-GPU) exchange: counters all-reduced, queue entries all-gathered
+#define XC_N 8          // i64 counters: free, total, active, qlen
+#define XQ_NONE 0xffffffffu
+struct Xchg {
+  i64* xc;            // [XC_N] local, then (after the all-reduce) global sums
+  u64* xsend;         // [1 + cap] : header count, then (gpos<<32 | req<<1 | long, row) pairs
+  u64* xrecv;         // [world][1 + cap] pairs
+  u32* gq_row;        // global queue by gpos: own local row or XQ_NONE
+  i32* gq_req;
+  u8* gq_lng;
+  u32* adm_idx;       // packed index of each own admitted entry
+  i32 world, rank;
+  i64 cap;            // per-rank queue capacity
 };
 
 // generic multi-CTA LSD radix sort scratch (u64 keys, u32 vals)
@@ -81,7 +97,7 @@ struct Work {
   u32 ticket_ap;
   unsigned long long exp_blocks;
   i32 n_exp, n_active, n_queued, n_long_q, n_ready, n_promoted, n_victims, n_boundary;
-  i32 exp_seg_cnt[MAX_SCAN_CTAS], exp_seg_off[MAX_SCAN_CTAS];
+  i32 tab_long_q, tab_max_req, tab_min_req;  // queue stats from the table scan
   i32 scan_ctas;
   i64 scan_chunk;
   i32 max_req, min_req;
@@ -99,12 +115,19 @@ struct Work {
   double ff_median;
   i32 lsd_cur, lsd_skip[8], lsd_in[8];
   u64 lsd_maxkey;
+  u64 lsd_raw_ptr;  // queue pass 0 reads req[] straight from the admission list
   i32 lsd_big, lsd_n;
   i32 xlsd_cur, xlsd_skip[8], xlsd_in[8];
   u64 xlsd_maxkey;
   i32 xlsd_big, xlsd_n;
   i64 limit, slots, take;
   long long projected;
+  // the telemetry the control plane sees: the replica's probe, or the pooled
+  // (all-reduced) view in sharded mode
+  i64 adm_avail, adm_total, adm_active;
+  double adm_usage;
+  i32 n_adm_own, n_res_own;
+  i64 global_residual;
   // plan
   i32 n_window, n_dec, n_pre, n_evict, n_journal;
   i64 total_tokens;
@@ -118,6 +141,7 @@ struct Work {
 struct Bufs {
   // expired pins: per-CTA row-ordered segments (K_A), contiguous (K_C), rank order
   u32 *exp_seg_row; i32 *exp_seg_blk; u32 *exp_seg_rank;
+  i32 *tile_cnt, *tile_off;  // per-4096-row-tile expired counts / offsets
   u32 *exp_row; i32 *exp_blk; u32 *exp_rank;
   u32 *exp_row_sorted; i32 *exp_blk_sorted;
   // window candidates

@@ -169,19 +169,114 @@ __device__ __forceinline__ int warp_append(int* counter, bool pred) {
   return base + __popc(m & ((1u << lane) - 1u));
 }
 
+// refresh_pressure (telemetry.py:174-208): two-threshold hysteresis on both flags
+__device__ void refresh_pressure(const Cfg& c, mars_scalars* sc, int worker_slots, double u) {
+  double slots = (double)worker_slots;
+  int at = sc->active_tools, qt = sc->queued_tools;
+  bool hi = ((double)at >= c.cpu_hi * slots) || qt > 0;
+  bool lo = ((double)at < c.cpu_lo * slots) && qt == 0;
+  int hs = hi ? sc->cpu_high_streak + 1 : 0;
+  int ls = lo ? sc->cpu_low_streak + 1 : 0;
+  int on = sc->cpu_overloaded;
+  if (!on && hs >= c.hyst) {
+    on = 1;
+    ls = 0;
+  } else if (on && ls >= c.hyst) {
+    on = 0;
+    hs = 0;
+  }
+  sc->cpu_overloaded = on;
+  sc->cpu_high_streak = hs;
+  sc->cpu_low_streak = ls;
+  hi = u >= c.kv_hi;
+  lo = u < c.kv_lo;
+  hs = hi ? sc->kv_high_streak + 1 : 0;
+  ls = lo ? sc->kv_low_streak + 1 : 0;
+  on = sc->kv_overloaded;
+  if (!on && hs >= c.hyst) {
+    on = 1;
+    ls = 0;
+  } else if (on && ls >= c.hyst) {
+    on = 0;
+    hs = 0;
+  }
+  sc->kv_overloaded = on;
+  sc->kv_high_streak = hs;
+  sc->kv_low_streak = ls;
+}
+
 // ---------------------------------------------------------------------------
 // K_A: scan (expiry, aging, counters, histograms); last CTA finalises
 // ---------------------------------------------------------------------------
 
-#define SCAN_TPB 512
+#define SCAN_TPB 1024
+#define SCAN_TILE (SCAN_TPB * SCAN_RPT)  // rows per tile (4096)
 
-__global__ void __launch_bounds__(SCAN_TPB) k_scan(Tab t, Cfg c, Work* w, Bufs b,
-                                                   mars_scalars* sc, i64 n_rows) {
+// Smallest bin d with cumsum(h[0..d]) >= k over HIST_BINS shared bins (nb-1
+// if the total is below k); *upto = cumsum(h[0..d]).  Warp-shuffle scans:
+// two barriers.  blockDim.x == SCAN_TPB, HIST_BINS / SCAN_TPB bins per thread.
+__device__ void block_threshold_fast(const u32* h, u32 k, u32* wsum, int* out_d, u32* upto) {
+  constexpr int PER = HIST_BINS / SCAN_TPB;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int base = threadIdx.x * PER;
+  u32 v[PER];
+  u32 s = 0;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    v[i] = h[base + i];
+    s += v[i];
+  }
+  u32 incl = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    u32 x = __shfl_up_sync(FULL, incl, o);
+    if (lane >= o) incl += x;
+  }
+  __shared__ int s_d;
+  __shared__ u32 s_up;
+  if (lane == 31) wsum[wid] = incl;
+  if (threadIdx.x == 0) {
+    s_d = HIST_BINS - 1;
+    s_up = 0xffffffffu;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    u32 t = wsum[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      u32 x = __shfl_up_sync(FULL, t, o);
+      if (lane >= o) t += x;
+    }
+    wsum[lane] = t;
+  }
+  __syncthreads();
+  const u32 total = wsum[31];
+  incl += wid ? wsum[wid - 1] : 0u;
+  const u32 excl = incl - s;
+  if (total >= k && excl < k && incl >= k) {
+    u32 cum = excl;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      u32 nc = cum + v[i];
+      if (cum < k && nc >= k) {
+        s_d = base + i;
+        s_up = nc;
+      }
+      cum = nc;
+    }
+  }
+  __syncthreads();
+  *out_d = s_d;
+  *upto = (s_up == 0xffffffffu) ? total : s_up;
+  __syncthreads();
+}
+
+// Persistent: one CTA per SM walks tiles t = blockIdx.x, blockIdx.x + gridDim.x, ...
+__global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Bufs b,
+                                                      mars_scalars* sc, i64 n_rows, i64* xc) {
   __shared__ u32 hw[HIST_BINS];
   __shared__ u32 hv[HIST_BINS];
-  __shared__ u32 shu[SCAN_TPB + 32];
-  __shared__ long long shl[32];
-  __shared__ int shi[32];
+  __shared__ u32 wsum[32];
   __shared__ bool s_last;
 
   for (int i = threadIdx.x; i < HIST_BINS; i += blockDim.x) hw[i] = hv[i] = 0;
@@ -190,27 +285,22 @@ __global__ void __launch_bounds__(SCAN_TPB) k_scan(Tab t, Cfg c, Work* w, Bufs b
   const double now = w->in.now;
   const bool do_exp = !(w->in.mode & MARS_MODE_SKIP_EXPIRY);
   const double scale = (now > 0.0 && now < 1e300) ? 1024.0 / now : 0.0;
-  const i64 tile = (i64)blockDim.x * SCAN_RPT;
-  const i64 chunk = ((n_rows + gridDim.x - 1) / gridDim.x + tile - 1) / tile * tile;
-  const i64 start = (i64)blockIdx.x * chunk;
-  i64 end = start + chunk;
-  if (end > n_rows) end = n_rows;
+  const i64 ntiles = (n_rows + SCAN_TILE - 1) / SCAN_TILE;
 
   long long exp_blocks = 0;
   int n_active = 0, n_queued = 0, n_long = 0, n_ready = 0, n_prom = 0, n_vic = 0, n_bnd = 0;
   int max_req = 0, min_req = 0x7fffffff;
-  int n_exp_local = 0;  // expired rows of this CTA, written in row order at b.exp_seg_*[start..]
   __shared__ int s_wexp[SCAN_TPB / 32];
-  __shared__ int s_tile_exp;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 
   // Each thread owns SCAN_RPT consecutive rows per tile: the byte columns
   // arrive as one 32-bit load, kv as one 128-bit load and the two f64
-  // columns as two 128-bit loads each, all issued before any use, so the
-  // whole tile's DRAM traffic is in flight at once.
-  for (i64 base = start + (i64)threadIdx.x * SCAN_RPT; base - (i64)threadIdx.x * SCAN_RPT < end;
-       base += (i64)blockDim.x * SCAN_RPT) {
-    const bool any = base < end;
+  // columns as two 128-bit loads each, all issued before any use.
+  for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const i64 tstart = tile * SCAN_TILE;
+    const i64 tend = (tstart + SCAN_TILE < n_rows) ? tstart + SCAN_TILE : n_rows;
+    const i64 base = tstart + (i64)threadIdx.x * SCAN_RPT;
+    const bool any = base < tend;
     u32 f4 = 0, ph4 = 0x07070707u, lv4 = 0, pr4 = 0;
     int4 kv4 = make_int4(0, 0, 0, 0);
     double2 rsa = make_double2(0, 0), rsb = rsa, wsa = rsa, wsb = rsa;
@@ -236,7 +326,7 @@ __global__ void __launch_bounds__(SCAN_TPB) k_scan(Tab t, Cfg c, Work* w, Bufs b
     for (int j = 0; j < SCAN_RPT; ++j) {
       const i64 r = base + j;
       exp_pb[j] = 0;
-      if (r >= end) continue;
+      if (r >= tend) continue;
       u8 f = (u8)(f4 >> (8 * j));
       u8 ph = (u8)(ph4 >> (8 * j));
       if (f & MARS_F_ACTIVE) n_active++;
@@ -288,7 +378,8 @@ __global__ void __launch_bounds__(SCAN_TPB) k_scan(Tab t, Cfg c, Work* w, Bufs b
         }
       }
     }
-    // expired rows, compacted in row order into this CTA's segment
+    // expired rows of this tile, compacted in row order into the tile's segment
+    int tile_exp = 0;
     if (__syncthreads_or(ne)) {
       int incl = ne;
 #pragma unroll
@@ -298,38 +389,41 @@ __global__ void __launch_bounds__(SCAN_TPB) k_scan(Tab t, Cfg c, Work* w, Bufs b
       }
       if (lane == 31) s_wexp[wid] = incl;
       __syncthreads();
-      if (threadIdx.x == 0) {
-        int acc = 0;
-        for (int q = 0; q < (int)(blockDim.x >> 5); ++q) {
-          int x = s_wexp[q];
-          s_wexp[q] = acc;
-          acc += x;
+      if (wid == 0) {
+        int v = s_wexp[lane];
+        int inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          int x = __shfl_up_sync(FULL, inc, o);
+          if (lane >= o) inc += x;
         }
-        s_tile_exp = acc;
+        s_wexp[lane] = inc - v;  // exclusive
+        if (lane == 31) wsum[0] = (u32)inc;
       }
       __syncthreads();
-      int pos = n_exp_local + s_wexp[wid] + incl - ne;
+      int pos = s_wexp[wid] + incl - ne;
 #pragma unroll
       for (int j = 0; j < SCAN_RPT; ++j) {
         if (exp_mask & (1u << j)) {
           const i64 r = base + j;
-          b.exp_seg_row[start + pos] = (u32)r;
-          b.exp_seg_blk[start + pos] = exp_pb[j];
-          b.exp_seg_rank[start + pos] = t.rank[r];
+          b.exp_seg_row[tstart + pos] = (u32)r;
+          b.exp_seg_blk[tstart + pos] = exp_pb[j];
+          b.exp_seg_rank[tstart + pos] = t.rank[r];
           pos++;
         }
       }
-      n_exp_local += s_tile_exp;
+      tile_exp = (int)wsum[0];
       __syncthreads();
     }
+    if (threadIdx.x == 0) b.tile_cnt[tile] = tile_exp;
   }
   __syncthreads();
 
   // local thresholds: only bins at or below them can hold a global top-k key
   int tw, tv;
-  u32 bl, up;
-  block_threshold(hw, HIST_BINS, (u32)c.window, shu, &tw, &bl, &up);
-  block_threshold(hv, HIST_BINS, (u32)VSEL, shu, &tv, &bl, &up);
+  u32 up;
+  block_threshold_fast(hw, (u32)c.window, wsum, &tw, &up);
+  block_threshold_fast(hv, (u32)VSEL, wsum, &tv, &up);
   for (int i = threadIdx.x; i <= tw; i += blockDim.x)
     if (hw[i]) atomicAdd(&w->hist_win[i], hw[i]);
   for (int i = threadIdx.x; i <= tv; i += blockDim.x)
@@ -372,8 +466,6 @@ __global__ void __launch_bounds__(SCAN_TPB) k_scan(Tab t, Cfg c, Work* w, Bufs b
     atomicAdd(&w->n_boundary, s_cnt[6]);
     atomicMax(&w->max_req, s_cnt[7]);
     atomicMin(&w->min_req, s_cnt[8]);
-    w->exp_seg_cnt[blockIdx.x] = n_exp_local;
-    atomicAdd(&w->n_exp, n_exp_local);
     __threadfence();
     u32 tk = atomicAdd(&w->ticket, 1u);
     s_last = (tk == gridDim.x - 1);
@@ -381,34 +473,46 @@ __global__ void __launch_bounds__(SCAN_TPB) k_scan(Tab t, Cfg c, Work* w, Bufs b
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  {
-    // exclusive prefix of the per-CTA expired segments (row order == CTA order),
-    // two counts per thread + one block scan (gridDim <= MAX_SCAN_CTAS = 2 * 512)
-    volatile Work* vw0 = w;
-    const int G = gridDim.x;
-    int i0 = 2 * threadIdx.x, i1 = i0 + 1;
-    int c0 = i0 < G ? vw0->exp_seg_cnt[i0] : 0;
-    int c1 = i1 < G ? vw0->exp_seg_cnt[i1] : 0;
-    shu[threadIdx.x] = (u32)(c0 + c1);
-    __syncthreads();
-    for (int off = 1; off < (int)blockDim.x; off <<= 1) {
-      u32 x = threadIdx.x >= (unsigned)off ? shu[threadIdx.x - off] : 0u;
-      __syncthreads();
-      shu[threadIdx.x] += x;
-      __syncthreads();
-    }
-    int excl = (int)shu[threadIdx.x] - (c0 + c1);
-    if (i0 < G) w->exp_seg_off[i0] = excl;
-    if (i1 < G) w->exp_seg_off[i1] = excl + c0;
-    if (threadIdx.x == 0) {
-      w->scan_ctas = G;
-      w->scan_chunk = chunk;
-    }
-    __syncthreads();
-  }
 
   // ---- last CTA: finalise ------------------------------------------------
   volatile Work* vw = w;
+  {
+    // exclusive prefix of the per-tile expired segments (tile order == row order)
+    volatile i32* tc = b.tile_cnt;
+    int run = 0;
+    for (i64 t0 = 0; t0 < ntiles; t0 += SCAN_TPB) {
+      i64 q = t0 + threadIdx.x;
+      int cnt = q < ntiles ? tc[q] : 0;
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int x = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += x;
+      }
+      if (lane == 31) wsum[wid] = (u32)incl;
+      __syncthreads();
+      if (wid == 0) {
+        int v = (int)wsum[lane];
+        int inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          int x = __shfl_up_sync(FULL, inc, o);
+          if (lane >= o) inc += x;
+        }
+        wsum[lane] = (u32)inc;
+      }
+      __syncthreads();
+      int excl = run + (wid ? (int)wsum[wid - 1] : 0) + incl - cnt;
+      if (q < ntiles) b.tile_off[q] = excl;
+      run += (int)wsum[31];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      w->n_exp = run;
+      w->scan_ctas = (i32)ntiles;
+      w->scan_chunk = SCAN_TILE;
+    }
+  }
   // global thresholds over the exact prefix of the merged histograms
   for (int i = threadIdx.x; i < HIST_BINS; i += blockDim.x) {
     hw[i] = (i <= (int)vw->tmin_win) ? vw->hist_win[i] : 0u;
@@ -416,9 +520,9 @@ __global__ void __launch_bounds__(SCAN_TPB) k_scan(Tab t, Cfg c, Work* w, Bufs b
   }
   __syncthreads();
   int gw, gv;
-  u32 wb, wu, vb, vu;
-  block_threshold(hw, HIST_BINS, (u32)c.window, shu, &gw, &wb, &wu);
-  block_threshold(hv, HIST_BINS, (u32)VSEL, shu, &gv, &vb, &vu);
+  u32 wu, vu;
+  block_threshold_fast(hw, (u32)c.window, wsum, &gw, &wu);
+  block_threshold_fast(hv, (u32)VSEL, wsum, &gv, &vu);
   if (threadIdx.x == 0) {
     if (gw > (int)vw->tmin_win) gw = (int)vw->tmin_win;
     if (gv > (int)vw->tmin_vic) gv = (int)vw->tmin_vic;
@@ -442,46 +546,28 @@ __global__ void __launch_bounds__(SCAN_TPB) k_scan(Tab t, Cfg c, Work* w, Bufs b
     i64 qlen = sc->queue_len;
     w->qlen = qlen;
     if (!(mode & MARS_MODE_NO_ROWS) && (i64)vw->n_queued != qlen) w->status |= ST_QUEUE_MISMATCH;
-    if (w->in.control_due && !(mode & MARS_MODE_SKIP_REFRESH)) {
-      // refresh_pressure (telemetry.py:174-208)
-      double slots = (double)w->in.worker_slots;
-      int at = sc->active_tools, qt = sc->queued_tools;
-      bool hi = ((double)at >= c.cpu_hi * slots) || qt > 0;
-      bool lo = ((double)at < c.cpu_lo * slots) && qt == 0;
-      int hs = hi ? sc->cpu_high_streak + 1 : 0;
-      int ls = lo ? sc->cpu_low_streak + 1 : 0;
-      int on = sc->cpu_overloaded;
-      if (!on && hs >= c.hyst) {
-        on = 1;
-        ls = 0;
-      } else if (on && ls >= c.hyst) {
-        on = 0;
-        hs = 0;
-      }
-      sc->cpu_overloaded = on;
-      sc->cpu_high_streak = hs;
-      sc->cpu_low_streak = ls;
-      double u = sc->kv_usage_ratio;
-      hi = u >= c.kv_hi;
-      lo = u < c.kv_lo;
-      hs = hi ? sc->kv_high_streak + 1 : 0;
-      ls = lo ? sc->kv_low_streak + 1 : 0;
-      on = sc->kv_overloaded;
-      if (!on && hs >= c.hyst) {
-        on = 1;
-        ls = 0;
-      } else if (on && ls >= c.hyst) {
-        on = 0;
-        hs = 0;
-      }
-      sc->kv_overloaded = on;
-      sc->kv_high_streak = hs;
-      sc->kv_low_streak = ls;
+    // what the control plane sees: this replica's probe (pooled in sharded mode,
+    // see k_global_control)
+    w->adm_avail = sc->available_kv;
+    w->adm_total = total;
+    w->adm_usage = sc->kv_usage_ratio;
+    w->adm_active = sc->active_sessions;
+    if (mode & MARS_MODE_SHARDED) {
+      xc[0] = sc->available_kv;
+      xc[1] = total;
+      xc[2] = sc->active_sessions;
+      xc[3] = sc->queue_len;
+    } else if (w->in.control_due && !(mode & MARS_MODE_SKIP_REFRESH)) {
+      refresh_pressure(c, sc, w->in.worker_slots, sc->kv_usage_ratio);
     }
     int ne = vw->n_exp;
     w->xlsd_big = ne > SORT_CAP ? 1 : 0;
     w->xlsd_n = ne;
     w->xlsd_maxkey = 0xffffffffull;
+    // table-backed queue statistics for pack_queue (control.py:109-122)
+    w->tab_long_q = vw->n_long_q;
+    w->tab_max_req = vw->max_req;
+    w->tab_min_req = vw->min_req;
   }
 }
 
@@ -507,7 +593,7 @@ __global__ void __launch_bounds__(SCAN_TPB) k_compact(Tab t, Cfg c, Work* w, Buf
     const i64 chunk = w->scan_chunk;
     const bool ro = (w->in.mode & MARS_MODE_RANK_ORDERED) != 0;
     for (int sg = blockIdx.x; sg < nseg; sg += gridDim.x) {
-      const int cnt = w->exp_seg_cnt[sg], off = w->exp_seg_off[sg];
+      const int cnt = b.tile_cnt[sg], off = b.tile_off[sg];
       const i64 src = (i64)sg * chunk;
       for (int k = threadIdx.x; k < cnt; k += blockDim.x) {
         u32 r = b.exp_seg_row[src + k];
@@ -523,25 +609,48 @@ __global__ void __launch_bounds__(SCAN_TPB) k_compact(Tab t, Cfg c, Work* w, Buf
       }
     }
   }
-  for (i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x; r < lim + 0; r += stride) {
-    bool valid = r < n_rows;
-    u8 f = valid ? t.flags[r] : 0;
-    u8 ph = valid ? t.phase[r] : MARS_EMPTY;
+  (void)lim;
+  // groups of SCAN_RPT consecutive rows per thread, vector loads as in k_scan;
+  // ranks are read only for the (few) candidates
+  const i64 ngroups = (n_rows + SCAN_RPT - 1) / SCAN_RPT;
+  const i64 glim = ((ngroups + 31) / 32) * 32;
+  for (i64 gi = (i64)blockIdx.x * blockDim.x + threadIdx.x; gi < glim; gi += stride) {
+  const i64 base = gi * SCAN_RPT;
+  u32 f4 = 0, ph4 = 0x07070707u, lv4 = 0;
+  int4 kv4 = make_int4(0, 0, 0, 0);
+  double2 ta = make_double2(0, 0), tb = ta;
+  if (base < n_rows) {
+    f4 = *(const u32*)(t.flags + base);
+    ph4 = *(const u32*)(t.phase + base);
+    lv4 = *(const u32*)(t.level + base);
+    kv4 = *(const int4*)(t.kv + base);
+    const double* tcol = c.coord ? t.rs : t.arr;
+    ta = *(const double2*)(tcol + base);
+    tb = *(const double2*)(tcol + base + 2);
+  }
+  const i32 kva[4] = {kv4.x, kv4.y, kv4.z, kv4.w};
+  const double tv4[4] = {ta.x, ta.y, tb.x, tb.y};
+#pragma unroll
+  for (int j = 0; j < SCAN_RPT; ++j) {
+    const i64 r = base + j;
+    const bool valid = r < n_rows;
+    u8 f = valid ? (u8)(f4 >> (8 * j)) : 0;
+    u8 ph = valid ? (u8)(ph4 >> (8 * j)) : MARS_EMPTY;
     bool ready = (f & MARS_F_ACTIVE) && (ph == MARS_PREFILL || ph == MARS_DECODE);
     bool wcand = false, vcand = false, bnd = (f & MARS_F_BOUNDARY) != 0;
     u64 whi = 0, wlo = 0, vk = 0;
     i32 blk = 0;
     if (ready) {
-      u32 lv = c.coord ? (u32)t.level[r] : 0u;
-      double tt = c.coord ? t.rs[r] : t.arr[r];
-      u32 rk = t.rank[r];
-      window_key(lv, tt, rk, whi, wlo);
+      u32 lv = c.coord ? ((lv4 >> (8 * j)) & 255u) : 0u;
+      double tt = tv4[j];
       wcand = window_digit(lv, tt, scale) <= tw;
-      i32 kvv = t.kv[r];
-      if (kvv > 0) {
-        i64 h = ceil_div64(kvv, c.bs);
-        if (victim_digit(true, false, lv, h) <= tv) {
-          vcand = true;
+      i32 kvv = kva[j];
+      i64 h = kvv > 0 ? held_blocks(c, kvv) : 0;
+      vcand = kvv > 0 && victim_digit(true, false, lv, h) <= tv;
+      if (wcand || vcand) {
+        u32 rk = t.rank[r];
+        window_key(lv, tt, rk, whi, wlo);
+        if (vcand) {
           vk = victim_key(true, false, lv, h, rk);
           blk = (i32)h;
         }
@@ -581,6 +690,7 @@ __global__ void __launch_bounds__(SCAN_TPB) k_compact(Tab t, Cfg c, Work* w, Buf
       b.ret_c[s] = cc;
       b.ret_d[s] = dd;
     }
+  }
   }
 }
 
@@ -645,6 +755,17 @@ __device__ __forceinline__ LsdView lsd_view(Work* w, int which) {
   return v;
 }
 
+// key of element i: the queue's first pass reads req[] from the admission list
+// (pack_queue key: req ascending, or max_req - req for the descending pack)
+__device__ __forceinline__ u64 lsd_key(const Lsd& L, const Work* w, int which, int pass, int buf,
+                                       int i) {
+  if (which == 0 && pass == 0) {
+    i32 rq = ((const i32*)(uintptr_t)w->lsd_raw_ptr)[i];
+    return (u64)(w->pack_mode == PACK_ASC ? rq : (w->max_req - rq));
+  }
+  return L.k[buf][i];
+}
+
 __global__ void __launch_bounds__(256) k_lsd_hist(Lsd L, Work* w, int which, int pass) {
   LsdView v = lsd_view(w, which);
   if (!*v.big) return;
@@ -658,7 +779,7 @@ __global__ void __launch_bounds__(256) k_lsd_hist(Lsd L, Work* w, int which, int
   int chunk = (n + gridDim.x - 1) / gridDim.x;
   int s = blockIdx.x * chunk, e = min(n, s + chunk);
   for (int i = s + threadIdx.x; i < e; i += blockDim.x)
-    atomicAdd(&h[(L.k[cur][i] >> shift) & 255u], 1u);
+    atomicAdd(&h[(lsd_key(L, w, which, pass, cur, i) >> shift) & 255u], 1u);
   __syncthreads();
   L.cnt[blockIdx.x * 256 + threadIdx.x] = h[threadIdx.x];
 }
@@ -674,6 +795,7 @@ __global__ void __launch_bounds__(256) k_lsd_scan(Lsd L, Work* w, int which, int
   __shared__ u32 sh[256];
   int d = threadIdx.x;
   u32 tot = 0;
+#pragma unroll 8
   for (int cta = 0; cta < G; ++cta) tot += L.cnt[cta * 256 + d];
   sh[d] = tot;
   __syncthreads();
@@ -715,8 +837,8 @@ __global__ void __launch_bounds__(256) k_lsd_scatter(Lsd L, Work* w, int which, 
   for (int base = s; base < e; base += 256) {
     int i = base + threadIdx.x;
     bool valid = i < e;
-    u64 key = valid ? L.k[in][i] : 0;
-    u32 val = valid ? L.v[in][i] : 0;
+    u64 key = valid ? lsd_key(L, w, which, pass, in, i) : 0;
+    u32 val = valid ? ((which == 0 && pass == 0) ? (u32)i : L.v[in][i]) : 0;
     u32 dig = valid ? (u32)((key >> shift) & 255u) : (256u + (u32)lane);
     u32 peers = __match_any_sync(FULL, dig);
     u32 rk = __popc(peers & ((1u << lane) - 1u));
@@ -826,28 +948,39 @@ __device__ i32 cta_kth_i32(const i32* a, int n, int k, u32* hist /*256*/, u32* s
 }
 
 __global__ void __launch_bounds__(1024) k_pack_small(Work* w, Queue Q, Lsd L,
-                                                     mars_scalars* sc, i32* qsel_p) {
+                                                     mars_scalars* sc, i32* qsel_p, Queue G) {
   extern __shared__ __align__(16) unsigned char smem[];
   if (!w->in.control_due) return;
   int qlen = (int)w->qlen;
   if (qlen <= 0) return;
+  const bool sharded = (w->in.mode & MARS_MODE_SHARDED) != 0;
   int sel = *qsel_p;
-  const i32* req = Q.req[sel];
-  const u8* lng = Q.lng[sel];
+  const i32* req = sharded ? G.req[0] : Q.req[sel];
+  const u8* lng = sharded ? G.lng[0] : Q.lng[sel];
   __shared__ u32 shu[1024 + 32];
   __shared__ u32 hist[256];
   __shared__ int shr[32];
-  // pack_queue mode (control.py:109-122) from the queue itself
-  int all_long = 1, mx = 0, mn = 0x7fffffff;
-  for (int i = threadIdx.x; i < qlen; i += blockDim.x) {
-    all_long &= lng[i] ? 1 : 0;
-    i32 rq = req[i];
-    mx = rq > mx ? rq : mx;
-    mn = rq < mn ? rq : mn;
+  // pack_queue mode (control.py:109-122): the table scan (or the global-list
+  // build) already reduced the queue; only a row-less queue is reduced here
+  int all_long, mx, mn;
+  if (!(w->in.mode & MARS_MODE_NO_ROWS)) {
+    all_long = w->tab_long_q == qlen ? 1 : 0;
+    mx = w->tab_max_req;
+    mn = w->tab_min_req;
+  } else {
+    all_long = 1;
+    mx = 0;
+    mn = 0x7fffffff;
+    for (int i = threadIdx.x; i < qlen; i += blockDim.x) {
+      all_long &= lng[i] ? 1 : 0;
+      i32 rq = req[i];
+      mx = rq > mx ? rq : mx;
+      mn = rq < mn ? rq : mn;
+    }
+    all_long = block_min<int>(all_long, shr, 1);
+    mx = block_max<int>(mx, shr, 0);
+    mn = block_min<int>(mn, shr, 0x7fffffff);
   }
-  all_long = block_min<int>(all_long, shr, 1);
-  mx = block_max<int>(mx, shr, 0);
-  mn = block_min<int>(mn, shr, 0x7fffffff);
   const int mode = sc->cpu_overloaded ? PACK_DESC : (all_long ? PACK_FF : PACK_ASC);
   if (threadIdx.x == 0) {
     w->pack_mode = mode;
@@ -866,7 +999,7 @@ __global__ void __launch_bounds__(1024) k_pack_small(Work* w, Queue Q, Lsd L,
     __shared__ long long s_cap;
     __shared__ int s_cursor, s_found, s_nfit;
     if (threadIdx.x == 0) {
-      s_cap = sc->available_kv;
+      s_cap = w->adm_avail;
       s_nfit = 0;
     }
     u32* fit = L.v[1];  // scratch flags (reuse LSD buffer)
@@ -940,13 +1073,13 @@ __global__ void __launch_bounds__(1024) k_pack_small(Work* w, Queue Q, Lsd L,
   }
   i32 mr = mx;
   if (qlen > SORT_CAP) {
-    // big queue: seed LSD keys (stable sort by req asc, or by -req via max-req)
-    for (int i = threadIdx.x; i < qlen; i += blockDim.x) {
-      i32 rq = req[i];
-      L.k[0][i] = (u64)(mode == PACK_ASC ? rq : (mr - rq));
-      L.v[0][i] = (u32)i;
+    // big queue: the multi-CTA LSD sort's first pass reads the list itself
+    // (key = req, or max_req - req for the descending pack; value = position)
+    (void)mr;
+    if (threadIdx.x == 0) {
+      w->lsd_raw_ptr = (u64)(uintptr_t)req;
+      w->lsd_cur = 0;
     }
-    if (threadIdx.x == 0) w->lsd_cur = 0;
     return;
   }
   int n2 = next_pow2(qlen);
@@ -974,13 +1107,19 @@ __global__ void __launch_bounds__(1024) k_pack_small(Work* w, Queue Q, Lsd L,
 // ---------------------------------------------------------------------------
 
 __global__ void __launch_bounds__(SCAN_TPB) k_admit_apply(Tab t, Cfg c, Work* w, Bufs b, Queue Q,
-                                                          Lsd L, mars_scalars* sc, i32* qsel_p) {
+                                                          Lsd L, mars_scalars* sc, i32* qsel_p,
+                                                          Queue G, Xchg x) {
   if (!w->in.control_due) return;
   __shared__ long long shl[32];
   __shared__ bool s_last;
   const double now = w->in.now;
   const i64 qlen = w->qlen;
+  const bool sharded = (w->in.mode & MARS_MODE_SHARDED) != 0;
   const int sel = *qsel_p;
+  // packed source: the local list, or (sharded) the all-gathered global list
+  const u32* src_row = sharded ? G.row[0] : Q.row[sel];
+  const i32* src_req = sharded ? G.req[0] : Q.req[sel];
+  const u8* src_lng = sharded ? G.lng[0] : Q.lng[sel];
   const u32* perm = L.v[w->lsd_cur];
   const int mode = w->pack_mode;
   // balance_and_admit scalars (control.py:181-190), computed redundantly per CTA
@@ -991,17 +1130,17 @@ __global__ void __launch_bounds__(SCAN_TPB) k_admit_apply(Tab t, Cfg c, Work* w,
     if (mode == PACK_FF) {
       seed = w->ff_median;
     } else {
-      i32 r1 = Q.req[sel][perm[(qlen - 1) / 2]];
-      i32 r2 = Q.req[sel][perm[qlen / 2]];
+      i32 r1 = src_req[perm[(qlen - 1) / 2]];
+      i32 r2 = src_req[perm[qlen / 2]];
       seed = (qlen & 1) ? (double)r1 : (double)((i64)r1 + (i64)r2) / 2.0;
     }
   }
   double wadm = sc->w_adm, last = sc->last_update;
   if (now - last >= c.ctl_interval) {  // update_window (control.py:154-160)
     if (sc->cpu_overloaded || sc->kv_overloaded) {
-      double x = wadm * c.md;
-      wadm = (x > (double)c.w_min) ? x : (double)c.w_min;
-    } else if (sc->kv_usage_ratio < c.kv_lo) {
+      double xm = wadm * c.md;
+      wadm = (xm > (double)c.w_min) ? xm : (double)c.w_min;
+    } else if (w->adm_usage < c.kv_lo) {
       wadm = wadm + c.ai;
     }
     last = now;
@@ -1010,8 +1149,8 @@ __global__ void __launch_bounds__(SCAN_TPB) k_admit_apply(Tab t, Cfg c, Work* w,
   double cpu = (raw > (double)c.w_min) ? raw : (double)c.w_min;
   double eff = sc->has_ema_blocks ? sc->ema_blocks : (has_seed ? seed : 1.0);
   double per = (1.0 > eff) ? 1.0 : eff;
-  i64 cap = (i64)floor((double)sc->available_kv * (1.0 - c.reserve) / per);
-  i64 act = sc->active_sessions;
+  i64 cap = (i64)floor((double)w->adm_avail * (1.0 - c.reserve) / per);
+  i64 act = w->adm_active;
   double kvl = ((double)(cap + act) > (double)c.w_min) ? (double)(cap + act) : (double)c.w_min;
   double m = wadm;
   if (cpu < m) m = cpu;
@@ -1032,33 +1171,40 @@ __global__ void __launch_bounds__(SCAN_TPB) k_admit_apply(Tab t, Cfg c, Work* w,
   const i64 lim = ((take + 31) / 32) * 32;
   for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < lim; i += stride) {
     bool valid = i < take;
-    bool wc = false;
+    bool wc = false, own = false;
     u64 whi = 0, wlo = 0;
     u32 row = 0;
     if (valid && (w->in.mode & MARS_MODE_NO_ROWS)) {
-      b.admitted[i] = Q.row[sel][perm[i]];
+      b.admitted[i] = src_row[perm[i]];
     } else if (valid) {
       u32 pos = perm[i];
-      row = Q.row[sel][pos];
-      i32 r0p = t.r0p[row];
-      i32 kvv = t.kv[row];
-      i64 cn = (i64)t.ctx[row] + r0p;
-      t.ctx[row] = (i32)cn;
-      t.rem[row] = t.r0d[row];
-      t.rs[row] = now;
-      t.ws[row] = now;
-      t.phase[row] = MARS_PREFILL;
-      t.flags[row] = (t.flags[row] | MARS_F_ACTIVE) & ~MARS_F_QUEUED;
-      u32 lv = initial_level(c, r0p);
-      t.level[row] = (u8)lv;
-      t.promos[row] = 0;
-      t.served[row] = 0;
-      proj += ceil_div64(cn, c.bs) - ceil_div64(kvv, c.bs);
-      b.admitted[i] = row;
-      u32 kl = c.coord ? lv : 0u;
-      double tt = c.coord ? now : t.arr[row];
-      window_key(kl, tt, t.rank[row], whi, wlo);
-      wc = window_digit(kl, tt, scale) <= tw;
+      row = src_row[pos];
+      if (sharded && row == XQ_NONE) {
+        // another replica's session: a fresh queued session projects exactly
+        // req_blocks (context 0, kv 0: control.py:86-87 vs sim.py:162)
+        proj += src_req[pos];
+      } else {
+        own = sharded;
+        i32 r0p = t.r0p[row];
+        i32 kvv = t.kv[row];
+        i64 cn = (i64)t.ctx[row] + r0p;
+        t.ctx[row] = (i32)cn;
+        t.rem[row] = t.r0d[row];
+        t.rs[row] = now;
+        t.ws[row] = now;
+        t.phase[row] = MARS_PREFILL;
+        t.flags[row] = (t.flags[row] | MARS_F_ACTIVE) & ~MARS_F_QUEUED;
+        u32 lv = initial_level(c, r0p);
+        t.level[row] = (u8)lv;
+        t.promos[row] = 0;
+        t.served[row] = 0;
+        proj += ceil_div64(cn, c.bs) - ceil_div64(kvv, c.bs);
+        if (!sharded) b.admitted[i] = row;
+        u32 kl = c.coord ? lv : 0u;
+        double tt = c.coord ? now : t.arr[row];
+        window_key(kl, tt, t.rank[row], whi, wlo);
+        wc = window_digit(kl, tt, scale) <= tw;
+      }
     }
     int s = warp_append(&w->n_wc, wc);
     if (s >= 0) {
@@ -1066,13 +1212,40 @@ __global__ void __launch_bounds__(SCAN_TPB) k_admit_apply(Tab t, Cfg c, Work* w,
       b.wc_lo[s] = wlo;
       b.wc_row[s] = row;
     }
+    // sharded: this replica's admitted rows, tagged with their packed index
+    s = warp_append(&w->n_adm_own, own);
+    if (s >= 0) {
+      b.admitted[s] = row;
+      x.adm_idx[s] = (u32)i;
+    }
   }
-  // residual queue, in packed order (control.py:190)
-  for (i64 j = (i64)blockIdx.x * blockDim.x + threadIdx.x; j < qlen - take; j += stride) {
-    u32 pos = perm[take + j];
-    Q.row[1 - sel][j] = Q.row[sel][pos];
-    Q.req[1 - sel][j] = Q.req[sel][pos];
-    Q.lng[1 - sel][j] = Q.lng[sel][pos];
+  // residual queue in packed order (control.py:190); sharded: this replica's
+  // entries only, each with its new dense global position
+  const i64 nres = qlen - take;
+  const i64 rlim = ((nres + 31) / 32) * 32;
+  for (i64 j = (i64)blockIdx.x * blockDim.x + threadIdx.x; j < rlim; j += stride) {
+    if (!sharded) {
+      if (j < nres) {
+        u32 pos = perm[take + j];
+        Q.row[1 - sel][j] = Q.row[sel][pos];
+        Q.req[1 - sel][j] = Q.req[sel][pos];
+        Q.lng[1 - sel][j] = Q.lng[sel][pos];
+      }
+      continue;
+    }
+    bool mine = false;
+    u32 pos = 0;
+    if (j < nres) {
+      pos = perm[take + j];
+      mine = src_row[pos] != XQ_NONE;
+    }
+    int s = warp_append(&w->n_res_own, mine);
+    if (s >= 0) {
+      Q.row[1 - sel][s] = src_row[pos];
+      Q.req[1 - sel][s] = src_req[pos];
+      Q.lng[1 - sel][s] = src_lng[pos];
+      Q.gpos[1 - sel][s] = (u32)j;
+    }
   }
   long long ps = block_sum<long long>(proj, shl);
   if (threadIdx.x == 0) {
@@ -1094,9 +1267,74 @@ __global__ void __launch_bounds__(SCAN_TPB) k_admit_apply(Tab t, Cfg c, Work* w,
     sc->last_w_adm = wadm;  // telemetry.record("window_update") (telemetry.py:326-327)
     sc->has_last_w_adm = 1;
     sc->last_window_update = now;
-    sc->available_kv -= (i64)vw->projected;  // gpu_submit debits (telemetry.py:324-325)
-    sc->queue_len = qlen - take;
+    // gpu_submit debits (telemetry.py:324-325) on the admission-view counter
+    sc->available_kv = w->adm_avail - (i64)vw->projected;
+    sc->queue_len = sharded ? (i64)vw->n_res_own : qlen - take;
+    w->global_residual = nres;
     *qsel_p = 1 - sel;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// sharded control plane: export / all-gather / pooled telemetry / global list
+// ---------------------------------------------------------------------------
+
+// this replica's admission list -> the all-gather send buffer
+__global__ void k_export_queue(Queue Q, const i32* qsel_p, mars_scalars* sc, Xchg x, Work* w) {
+  const int sel = *qsel_p;
+  i64 n = sc->queue_len;
+  if (n > x.cap) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) w->status |= ST_BAD_INPUT;
+    n = x.cap;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) x.xsend[0] = (u64)n;
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    u64 key = ((u64)Q.gpos[sel][i] << 32) | ((u64)(u32)Q.req[sel][i] << 1) | (u64)(Q.lng[sel][i] & 1);
+    x.xsend[1 + 2 * i] = key;
+    x.xsend[2 + 2 * i] = (u64)Q.row[sel][i];
+  }
+}
+
+// all-reduced counters -> pooled telemetry; refresh_pressure on the pooled view
+__global__ void k_global_control(Cfg c, Work* w, mars_scalars* sc, Xchg x) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const i64 avail = x.xc[0], total = x.xc[1], active = x.xc[2], qlen = x.xc[3];
+  w->adm_avail = avail;
+  w->adm_total = total;
+  w->adm_usage = (double)(total - avail) / (double)total;
+  w->adm_active = active;
+  w->qlen = qlen;
+  w->tab_long_q = 0;  // recomputed over the union list by k_build_global_queue
+  w->tab_max_req = 0;
+  w->tab_min_req = 0x7fffffff;
+  if (w->in.control_due && !(w->in.mode & MARS_MODE_SKIP_REFRESH))
+    refresh_pressure(c, sc, w->in.worker_slots, w->adm_usage);
+}
+
+// all-gathered entries -> the global list indexed by global position
+__global__ void k_build_global_queue(Work* w, Xchg x) {
+  const i64 stride1 = 1 + 2 * x.cap;
+  const i64 total = (i64)x.world * x.cap;
+  const i64 qlen = w->qlen;
+  for (i64 f = (i64)blockIdx.x * blockDim.x + threadIdx.x; f < total;
+       f += (i64)gridDim.x * blockDim.x) {
+    i64 g = f / x.cap, k = f % x.cap;
+    i64 cnt = (i64)x.xrecv[g * stride1];
+    if (k >= cnt) continue;
+    u64 key = x.xrecv[g * stride1 + 1 + 2 * k];
+    u32 gp = (u32)(key >> 32);
+    if ((i64)gp >= qlen) {
+      w->status |= ST_BAD_INPUT;
+      continue;
+    }
+    i32 rq = (i32)((key >> 1) & 0x7fffffffu);
+    x.gq_req[gp] = rq;
+    x.gq_lng[gp] = (u8)(key & 1);
+    x.gq_row[gp] = (g == x.rank) ? (u32)x.xrecv[g * stride1 + 2 + 2 * k] : XQ_NONE;
+    // statistics of the union list for pack_queue's mode (k_pack_small)
+    if (key & 1) atomicAdd(&w->tab_long_q, 1);
+    atomicMax(&w->tab_max_req, rq);
+    atomicMin(&w->tab_min_req, rq);
   }
 }
 
@@ -1469,6 +1707,36 @@ __device__ void walk_fullscan(const Cfg& c, Tab& t, WalkShared& S, i64 n_rows, d
 // sorted.  Bitonic when n <= SORT_CAP, else MSD radix refinement first.
 __device__ int cta_select_sorted(const u64* ghi, const u64* glo, const u32* gpay, int n, int k,
                                  u64* kh, u64* kl, u32* pv, u32* hist /*256*/) {
+  if (n <= (int)blockDim.x && n <= SORT_CAP / 4) {
+    // small candidate sets: rank by counting (keys are unique through the
+    // session rank), two barriers instead of a log^2 sorting network
+    u64* th = kh + SORT_CAP / 2;
+    u64* tl = kl + SORT_CAP / 2;
+    u32* tp = pv + SORT_CAP / 2;
+    const int i = threadIdx.x;
+    u64 h = 0, l = 0;
+    u32 p = 0;
+    if (i < n) {
+      h = ghi[i];
+      l = glo[i];
+      p = gpay[i];
+      th[i] = h;
+      tl[i] = l;
+      tp[i] = p;
+    }
+    __syncthreads();
+    if (i < n) {
+      int rnk = 0;
+      for (int j = 0; j < n; ++j) rnk += key_lt(th[j], tl[j], h, l) ? 1 : 0;
+      if (rnk < k) {
+        kh[rnk] = h;
+        kl[rnk] = l;
+        pv[rnk] = p;
+      }
+    }
+    __syncthreads();
+    return n < k ? n : k;
+  }
   if (n <= SORT_CAP) {
     int n2 = next_pow2(n > 1 ? n : 1);
     for (int i = threadIdx.x; i < n2; i += blockDim.x) {
@@ -1944,26 +2212,40 @@ int mars_enqueue_step(const LaunchArgs* a) {
     cudaEventRecord(a->prof[2 * k + end], st);
     if (end) a->prof_used[k] = 1;
   };
-  if (a->prof)
-    for (int k = 0; k < MARS_NUM_KTIMES; ++k) a->prof_used[k] = 0;
-  cudaMemsetAsync(a->work, 0, sizeof(Work), s);
-  cudaMemcpyAsync(a->work, a->host_in, sizeof(mars_step_in), cudaMemcpyHostToDevice, s);
-  k_work_init<<<1, 32, 0, s>>>(a->work);
-  launches++;
-  int nsm = a->num_sms;
-  i64 n = a->n_rows;
-  int g_scan = (int)((n + SCAN_TPB * SCAN_RPT - 1) / (SCAN_TPB * SCAN_RPT));
-  if (g_scan > 4 * nsm) g_scan = 4 * nsm;
-  if (g_scan > MAX_SCAN_CTAS) g_scan = MAX_SCAN_CTAS;
-  if (g_scan < 1) g_scan = 1;
-  mark(0, 0, s);
-  k_scan<<<g_scan, SCAN_TPB, 0, s>>>(a->tab, a->cfg, a->work, a->bufs, a->sc, n);
-  mark(0, 1, s);
-  launches++;
+  const int nsm = a->num_sms;
+  const i64 n = a->n_rows;
+  const bool sharded = a->sharded != 0;
+  if (a->phase != 2) {
+    // ---- head: reset, k_scan (+ sharded: export the local admission list)
+    if (a->prof)
+      for (int k = 0; k < MARS_NUM_KTIMES; ++k) a->prof_used[k] = 0;
+    cudaMemsetAsync(a->work, 0, sizeof(Work), s);
+    cudaMemcpyAsync(a->work, a->host_in, sizeof(mars_step_in), cudaMemcpyHostToDevice, s);
+    k_work_init<<<1, 32, 0, s>>>(a->work);
+    launches++;
+    int g_scan = (int)((n + SCAN_TILE - 1) / SCAN_TILE);  // persistent: <= 1 CTA per SM
+    if (g_scan > nsm) g_scan = nsm;
+    if (g_scan < 1) g_scan = 1;
+    mark(0, 0, s);
+    k_scan<<<g_scan, SCAN_TPB, 0, s>>>(a->tab, a->cfg, a->work, a->bufs, a->sc, n, a->x.xc);
+    mark(0, 1, s);
+    launches++;
+    if (sharded) {
+      k_export_queue<<<nsm, 256, 0, s>>>(a->queue, a->qsel, a->sc, a->x, a->work);
+      launches++;
+    }
+    if (a->phase == 1) return launches;
+  }
+  // ---- tail (sharded: after the counter all-reduce and the list all-gather)
+  if (sharded) {
+    k_global_control<<<1, 32, 0, s>>>(a->cfg, a->work, a->sc, a->x);
+    k_build_global_queue<<<nsm, 256, 0, s>>>(a->work, a->x);
+    launches += 2;
+  }
   cudaEventRecord(a->ev_fork, s);
   cudaStreamWaitEvent(s2, a->ev_fork, 0);
-  int g_c = (int)((n + SCAN_TPB - 1) / SCAN_TPB);
-  if (g_c > 4 * nsm) g_c = 4 * nsm;
+  int g_c = (int)((n + SCAN_TPB * SCAN_RPT - 1) / (SCAN_TPB * SCAN_RPT));
+  if (g_c > 2 * nsm) g_c = 2 * nsm;
   if (g_c < 1) g_c = 1;
   mark(1, 0, s2);
   k_compact<<<g_c, SCAN_TPB, 0, s2>>>(a->tab, a->cfg, a->work, a->bufs, a->sc, n);
@@ -1988,12 +2270,16 @@ int mars_enqueue_step(const LaunchArgs* a) {
   cudaEventRecord(a->ev_join, s2);
   if (a->control_possible) {
     mark(3, 0, s);
-    k_pack_small<<<1, 1024, sort_smem_bytes(), s>>>(a->work, a->queue, a->qlsd, a->sc, a->qsel);
+    k_pack_small<<<1, 1024, sort_smem_bytes(), s>>>(a->work, a->queue, a->qlsd, a->sc, a->qsel,
+                                                    a->gq);
     launches++;
+    // ~4K list entries per CTA: the single-CTA offset scan walks G columns
+    i64 lgq = (a->queue_upper + 4095) / 4096;
+    int lg = (int)(lgq < 1 ? 1 : (lgq > LSD_G ? LSD_G : lgq));
     for (int p = 0; p < a->queue_passes; ++p) {
-      k_lsd_hist<<<LSD_G, 256, 0, s>>>(a->qlsd, a->work, 0, p);
-      k_lsd_scan<<<1, 256, 0, s>>>(a->qlsd, a->work, 0, p, LSD_G);
-      k_lsd_scatter<<<LSD_G, 256, 0, s>>>(a->qlsd, a->work, 0, p);
+      k_lsd_hist<<<lg, 256, 0, s>>>(a->qlsd, a->work, 0, p);
+      k_lsd_scan<<<1, 256, 0, s>>>(a->qlsd, a->work, 0, p, lg);
+      k_lsd_scatter<<<lg, 256, 0, s>>>(a->qlsd, a->work, 0, p);
       launches += 3;
     }
     mark(3, 1, s);
@@ -2007,7 +2293,7 @@ int mars_enqueue_step(const LaunchArgs* a) {
     if (g_ap < 1) g_ap = 1;
     mark(4, 0, s);
     k_admit_apply<<<g_ap, SCAN_TPB, 0, s>>>(a->tab, a->cfg, a->work, a->bufs, a->queue, a->qlsd,
-                                            a->sc, a->qsel);
+                                            a->sc, a->qsel, a->gq, a->x);
     mark(4, 1, s);
     launches++;
   }

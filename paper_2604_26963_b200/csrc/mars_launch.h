@@ -26,6 +26,10 @@ struct LaunchArgs {
   cudaEvent_t* prof;     // 2*MARS_NUM_KTIMES events, or null
   int* prof_used;        // which pairs were recorded
   const Kv* kv;          // block manager to update with the step's journal, or null
+  int phase;             // 0 whole step; sharded: 1 head (before the exchange), 2 tail
+  int sharded;
+  Xchg x;                // sharded exchange buffers
+  Queue gq;              // view of the all-gathered global admission list
 };
 
 int mars_kernels_init();
