@@ -231,25 +231,49 @@ def main():
     snap = snapshot_v1(a.sessions, seed=rank, pool="headroom")
     eng = MarsEngine(max_rows=snap.n, max_queue=max(len(snap.queue), 1), device=local,
                      config=make_config(initial_window=snap.initial_window))
-    # a dedicated (non-default) stream: the step is captured as a CUDA graph and
-    # the timing events are recorded on the stream the kernels run on
-    stream = torch.cuda.Stream()
-    torch.cuda.set_stream(stream)
-    eng.lib.mars_set_stream(eng.ctx, stream.cuda_stream)
-    eng.set_graph(True)  # the whole step is one CUDA graph launch
     eng.load_snapshot(snap)
-    eng.checkpoint()
     si = eng.step_in(snap.now, True, snap.active_tools, snap.queued_tools, snap.worker_slots)
     flush = a.flush_mb << 20
+    if world == 1:
+        # a dedicated (non-default) stream: the step is captured as one CUDA
+        # graph and the timing events are recorded on the stream it runs on
+        stream = torch.cuda.Stream()
+        torch.cuda.set_stream(stream)
+        eng.lib.mars_set_stream(eng.ctx, stream.cuda_stream)
+        eng.set_graph(True)
+
+        def enqueue_step():
+            eng.enqueue(si)
+    else:
+        # sharded replicas: every rank owns a 1M-session shard, the control
+        # plane runs on NCCL-reduced counters and the all-gathered union list
+        from paper_2604_26963_b200.dist import COUNTERS, ShardedEngine, exchange, interleaved_gpos
+
+        ql = torch.tensor([len(snap.queue)], dtype=torch.int64, device="cuda")
+        allq = [torch.zeros_like(ql) for _ in range(world)]
+        dist.all_gather(allq, ql)
+        gpos = interleaved_gpos([int(x.item()) for x in allq])[rank]
+        sh = ShardedEngine(eng, world=world, rank=rank)
+        stream = sh.stream
+        torch.cuda.set_stream(stream)
+        q = snap.queue
+        sh.set_queue(q, snap.cols["req_blocks"][q], (snap.cols["flags"][q] & 16) != 0, gpos)
+
+        def enqueue_step():
+            sh.phase(si, 1)
+            exchange(sh.xc[:len(COUNTERS)], sh.xsend, sh.xrecv)
+            sh.phase(si, 2)
+    eng.checkpoint()
 
     # correctness guard: one fetched step must succeed with status 0
-    res = eng.step(si)
+    enqueue_step()
+    res = eng.fetch()
     if res.status != 0:
         raise SystemExit(f"device step status {res.status}")
     eng.restore()
 
     for _ in range(a.warmup):
-        eng.enqueue(si)
+        enqueue_step()
         eng.restore()
     barrier()
 
@@ -262,7 +286,7 @@ def main():
             eng.restore()
             eng.flush_l2(flush)
             starts[i].record(stream)
-            eng.enqueue(si)          # one CUDA-graph launch per step
+            enqueue_step()           # N=1: one CUDA-graph launch per step
             ends[i].record(stream)
             launches += eng.launches()
         barrier()
@@ -282,10 +306,10 @@ def main():
     for i in range(a.steps):
         eng.restore()
         eng.flush_l2(flush)
-        eng.enqueue(si)
+        enqueue_step()
         ktimes.append(eng.kernel_times())
     eng.set_profiling(False)
-    eng.set_graph(True)
+    eng.set_graph(world == 1)
     kernel_ms = {k: statistics.median([kt[k] for kt in ktimes]) for k in ktimes[0]}
     scan_avg = sum(kt["k_scan"] for kt in ktimes) / len(ktimes)
 
@@ -301,7 +325,8 @@ def main():
         barrier()
         t0 = time.perf_counter()
         eng.upsert(pinned)
-        r = eng.step(si)
+        enqueue_step()
+        r = eng.fetch()
         t1 = time.perf_counter()
         if i > 0:
             e2e_t.append(t1 - t0)
@@ -328,7 +353,9 @@ def main():
         "config": {"workload": "one MARS scheduling step (expiry, probe, control-plane admission, "
                                "aging, window top-128, build_plan walk, S2 retention) per replica",
                    "sessions_per_gpu": a.sessions, "pool": "headroom",
-                   "parallelism": f"replicas x{world}",
+                   "parallelism": (f"replicas x{world}" if world == 1 else
+                                   f"sharded replicas x{world}: NCCL all-reduce of probe "
+                                   "counters + all-gather of the admission list"),
                    "l2": f"flushed before every timed step ({a.flush_mb} MiB scratch write); "
                          "state restored from a device checkpoint (untimed)"},
         "roofline": {"bound": "hbm", "kernel": "k_scan", "achieved": achieved, "peak": peak,

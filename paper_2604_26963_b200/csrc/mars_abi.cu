@@ -52,7 +52,7 @@ struct mars_ctx {
   i64* d_rows = nullptr;
   // checkpoint
   bool have_ckpt = false;
-  void* ck_q[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  void* ck_q[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   mars_scalars* ck_sc = nullptr;
   i32* ck_qsel = nullptr;
   i64 ck_q_upper = 0;
@@ -871,6 +871,21 @@ int mars_retention_batch(mars_ctx* ctx, int64_t n, const int32_t* context, const
   return MARS_OK;
 }
 
+// every admission-list array (both buffers) and its size
+static void queue_arrays(mars_ctx* ctx, void** qp, size_t* qs) {
+  const size_t Qc = (size_t)ctx->max_queue;
+  for (int b = 0; b < 2; ++b) {
+    qp[4 * b + 0] = ctx->queue.row[b];
+    qs[4 * b + 0] = Qc * 4;
+    qp[4 * b + 1] = ctx->queue.req[b];
+    qs[4 * b + 1] = Qc * 4;
+    qp[4 * b + 2] = ctx->queue.lng[b];
+    qs[4 * b + 2] = Qc;
+    qp[4 * b + 3] = ctx->queue.gpos[b];
+    qs[4 * b + 3] = Qc * 4;
+  }
+}
+
 int mars_checkpoint(mars_ctx* ctx) {
   if (!ctx) return MARS_ERR_ARG;
   CK(cudaSetDevice(ctx->device));
@@ -880,11 +895,10 @@ int mars_checkpoint(mars_ctx* ctx) {
     CK(cudaMemcpyAsync(cs.ckpt, *cs.dev, (size_t)ctx->n_rows * cs.esz, cudaMemcpyDeviceToDevice,
                        ctx->stream));
   }
-  size_t qs[6] = {(size_t)Qc * 4, (size_t)Qc * 4, (size_t)Qc, (size_t)Qc * 4, (size_t)Qc * 4,
-                  (size_t)Qc};
-  void* qp[6] = {ctx->queue.row[0], ctx->queue.req[0], ctx->queue.lng[0], ctx->queue.row[1],
-                 ctx->queue.req[1], ctx->queue.lng[1]};
-  for (int i = 0; i < 6; ++i) {
+  size_t qs[8];
+  void* qp[8];
+  queue_arrays(ctx, qp, qs);
+  for (int i = 0; i < 8; ++i) {
     if (!ctx->ck_q[i]) CK(cudaMalloc(&ctx->ck_q[i], qs[i]));
     CK(cudaMemcpyAsync(ctx->ck_q[i], qp[i], qs[i], cudaMemcpyDeviceToDevice, ctx->stream));
   }
@@ -907,11 +921,11 @@ int mars_restore(mars_ctx* ctx) {
   for (auto& cs : ctx->cols)
     CK(cudaMemcpyAsync(*cs.dev, cs.ckpt, (size_t)ctx->n_rows * cs.esz, cudaMemcpyDeviceToDevice,
                        ctx->stream));
-  size_t qs[6] = {(size_t)Qc * 4, (size_t)Qc * 4, (size_t)Qc, (size_t)Qc * 4, (size_t)Qc * 4,
-                  (size_t)Qc};
-  void* qp[6] = {ctx->queue.row[0], ctx->queue.req[0], ctx->queue.lng[0], ctx->queue.row[1],
-                 ctx->queue.req[1], ctx->queue.lng[1]};
-  for (int i = 0; i < 6; ++i)
+  (void)Qc;
+  size_t qs[8];
+  void* qp[8];
+  queue_arrays(ctx, qp, qs);
+  for (int i = 0; i < 8; ++i)
     CK(cudaMemcpyAsync(qp[i], ctx->ck_q[i], qs[i], cudaMemcpyDeviceToDevice, ctx->stream));
   CK(cudaMemcpyAsync(ctx->sc, ctx->ck_sc, sizeof(mars_scalars), cudaMemcpyDeviceToDevice, ctx->stream));
   CK(cudaMemcpyAsync(ctx->qsel, ctx->ck_qsel, sizeof(i32), cudaMemcpyDeviceToDevice, ctx->stream));
