@@ -146,6 +146,50 @@ def step_bytes(snap) -> int:
                + ((c["flags"] & F_QUEUED) != 0).sum() * 13)
 
 
+def kv_sweep(device: int, batches=(1, 16, 256, 2048), reps: int = 3) -> dict:
+    """BASELINE configs[3]: paged KV evict (HBM -> pinned host) / restore sweep,
+    Llama-3-8B geometry (2 MiB per 16-token block, 32 layer-major pieces),
+    scattered random block IDs, each call timed end to end through the ABI,
+    against the measured pinned-copy peak of the host link."""
+    import numpy as np
+
+    from paper_2604_26963_b200.engine import MarsEngine
+    from paper_2604_26963_b200.kvstore import (LLAMA3_8B_BLOCK_BYTES, LLAMA3_8B_LAYERS,
+                                               KvBlockManager, host_link_peak)
+
+    eng = MarsEngine(max_rows=64, max_queue=1, device=device)
+    d2h, h2d, bidir = host_link_peak(eng, 1 << 30, 5)
+    total, host_blocks = 8192, max(batches)
+    kv = KvBlockManager(eng, total, max_blocks_per_row=16, block_bytes=LLAMA3_8B_BLOCK_BYTES,
+                        layers=LLAMA3_8B_LAYERS, host_blocks=host_blocks)
+    rng = np.random.default_rng(3)
+    names = {0: "copy_engine_per_piece", 1: "sm_zero_copy", 2: "staged_dma"}
+    sweep = []
+    for n in batches:
+        ids = rng.choice(total, size=n, replace=False).astype(np.uint32)
+        for m in (0, 1, 2):
+            for direction in ("evict", "restore"):
+                fn = kv.evict if direction == "evict" else kv.restore
+                fn(ids, 0, m)  # warm
+                ts = []
+                for _ in range(reps):
+                    t0 = time.perf_counter()
+                    fn(ids, 0, m)
+                    ts.append(time.perf_counter() - t0)
+                gbs = n * LLAMA3_8B_BLOCK_BYTES / min(ts) / 1e9
+                sweep.append({"blocks": n, "method": names[m], "op": direction, "gbs": gbs})
+    eng.close()
+    big = [s for s in sweep if s["blocks"] == max(batches)]
+    ev = max((s for s in big if s["op"] == "evict"), key=lambda s: s["gbs"])
+    rs = max((s for s in big if s["op"] == "restore"), key=lambda s: s["gbs"])
+    return {"evict_gbs": ev["gbs"], "evict_method": ev["method"], "restore_gbs": rs["gbs"],
+            "restore_method": rs["method"], "peak_d2h_gbs": d2h, "peak_h2d_gbs": h2d,
+            "peak_bidir_gbs": bidir, "evict_frac": ev["gbs"] / d2h, "restore_frac": rs["gbs"] / h2d,
+            "block_bytes": LLAMA3_8B_BLOCK_BYTES, "batch_blocks": max(batches),
+            "peak_source": "pinned cudaMemcpyAsync 1 GiB, best of 5, measured in this run",
+            "sweep": sweep}
+
+
 def cpu_reference(sessions: int, seed: int, reps: int = 1):
     """Times the oracle port's full step (materialisation excluded)."""
     from oracle.snapshot_step import World, run_step
@@ -203,6 +247,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--flush-mb", type=int, default=512)
+    ap.add_argument("--no-kv", action="store_true", help="skip the KV evict/restore sweep")
     a = ap.parse_args()
     if a.impl == "reference":
         return run_reference_arm(a)
@@ -371,6 +416,11 @@ def main():
         "clocks": clk.summary(),
         "step_ms_min": min(step_ms), "step_ms_max": max(step_ms),
     }
+    if not a.no_kv:
+        try:
+            line["kv"] = kv_sweep(local)
+        except Exception as exc:  # the scheduler number stands on its own
+            line["kv"] = {"error": repr(exc)[:300]}
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         t_cpu = cpu_reference(a.sessions, seed=0)[0]
         line["cpu_baseline"] = {

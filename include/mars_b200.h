@@ -252,7 +252,8 @@ int mars_kv_state(mars_ctx* ctx, int64_t k, uint32_t* top_ids, int64_t* explicit
                   int64_t* fresh, int32_t* status);                               /* sync */
 /* evict (HBM -> host slots [slot0, slot0+n)) / restore (host -> HBM) block data.
  * method 0: copy engines (one cudaMemcpyAsync per block piece),
- * method 1: SM-driven zero-copy kernel over mapped pinned memory. */
+ * method 1: SM-driven zero-copy kernel over mapped pinned memory,
+ * method 2: staged -- HBM gather/scatter kernel + one large DMA per 64 blocks. */
 int mars_kv_evict(mars_ctx* ctx, int64_t n, const uint32_t* block_ids, int64_t slot0, int method);
 int mars_kv_restore(mars_ctx* ctx, int64_t n, const uint32_t* block_ids, int64_t slot0,
                     int method);

@@ -77,6 +77,7 @@ struct mars_ctx {
   void* kv_host = nullptr;          // pinned, mapped
   unsigned char* kv_stage = nullptr; // device staging for op streams / ids
   i64 kv_stage_bytes = 0;
+  u8* kv_dstage = nullptr;           // HBM staging for the staged host-tier path
   // sharded replica (mars_shard_init)
   Xchg x = {};
 };
@@ -406,7 +407,7 @@ int mars_destroy(mars_ctx* ctx) {
   cudaFreeHost(ctx->h_out);
   {
     Kv& k = ctx->kv;
-    void* kp[] = {k.fs, k.chunks, k.cfs, k.dir, k.len, k.s, k.data, ctx->kv_stage};
+    void* kp[] = {k.fs, k.chunks, k.cfs, k.dir, k.len, k.s, k.data, ctx->kv_stage, ctx->kv_dstage};
     for (void* p : kp) cudaFree(p);
     if (ctx->kv_host) cudaFreeHost(ctx->kv_host);
   }
@@ -1119,6 +1120,29 @@ static int kv_move(mars_ctx* ctx, int64_t n, const uint32_t* ids, int64_t slot0,
     int grid = ctx->num_sms * 4;
     rc = mars_kv_enqueue_copy(k, ctx->stream, (const u32*)ctx->kv_stage, n, slot0, dir, grid);
     if (rc) return fail(ctx, MARS_ERR_CUDA, "kv copy: %s", cudaGetErrorString((cudaError_t)rc));
+  } else if (method == 2) {
+    // staged: HBM gather/scatter kernel + one large copy-engine DMA per chunk
+    int rc = kv_stage(ctx, n * 4);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(ctx->kv_stage, ids, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+    const i64 chunk = KV_STAGE_BLOCKS;
+    if (!ctx->kv_dstage) CK(cudaMalloc((void**)&ctx->kv_dstage, (size_t)chunk * k.block_bytes));
+    u8* hbase = (u8*)ctx->kv_host;
+    for (i64 c0 = 0; c0 < n; c0 += chunk) {
+      const i64 m = (n - c0) < chunk ? (n - c0) : chunk;
+      const u32* cid = (const u32*)ctx->kv_stage + c0;
+      const size_t bytes = (size_t)m * k.block_bytes;
+      u8* hp = hbase + (size_t)(slot0 + c0) * k.block_bytes;
+      if (dir == 0) {
+        rc = mars_kv_enqueue_stage(k, ctx->stream, cid, m, ctx->kv_dstage, 0, ctx->num_sms * 2);
+        if (rc) return fail(ctx, MARS_ERR_CUDA, "kv stage: %s", cudaGetErrorString((cudaError_t)rc));
+        CK(cudaMemcpyAsync(hp, ctx->kv_dstage, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+      } else {
+        CK(cudaMemcpyAsync(ctx->kv_dstage, hp, bytes, cudaMemcpyHostToDevice, ctx->stream));
+        rc = mars_kv_enqueue_stage(k, ctx->stream, cid, m, ctx->kv_dstage, 1, ctx->num_sms * 2);
+        if (rc) return fail(ctx, MARS_ERR_CUDA, "kv stage: %s", cudaGetErrorString((cudaError_t)rc));
+      }
+    }
   } else {
     u8* hbase = (u8*)ctx->kv_host;
     for (int64_t i = 0; i < n; ++i) {

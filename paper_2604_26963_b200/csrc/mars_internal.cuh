@@ -19,7 +19,7 @@ typedef int64_t i64;
 #define SORT_CAP 4096         // bitonic sort capacity of the single-CTA selector
 #define VSEL 256              // victim-stream target length (prefix of reclaim order)
 #define VSTREAM_CAP 2048      // victim stream entries kept in shared memory
-#define LSD_G 148             // CTAs of the multi-CTA LSD radix sort
+#define LSD_G 592             // max CTAs of the multi-CTA LSD radix sort (4 x 148 SMs)
 #define SCAN_RPT 4            // consecutive rows per thread in the table scans
 #define MAX_SCAN_CTAS 1024    // upper bound of k_scan's grid
 #define ROW_PAD 2048          // row capacity is padded to this multiple

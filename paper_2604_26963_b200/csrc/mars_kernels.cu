@@ -514,9 +514,13 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
     }
   }
   // global thresholds over the exact prefix of the merged histograms
-  for (int i = threadIdx.x; i < HIST_BINS; i += blockDim.x) {
-    hw[i] = (i <= (int)vw->tmin_win) ? vw->hist_win[i] : 0u;
-    hv[i] = (i <= (int)vw->tmin_vic) ? vw->hist_vic[i] : 0u;
+  // (L2 loads, all in flight at once: other CTAs' atomics are complete)
+  const u32 tmw = __ldcg(&w->tmin_win), tmv = __ldcg(&w->tmin_vic);
+#pragma unroll
+  for (int q = 0; q < HIST_BINS / SCAN_TPB; ++q) {
+    const int i = q * SCAN_TPB + threadIdx.x;
+    hw[i] = (i <= (int)tmw) ? __ldcg(&w->hist_win[i]) : 0u;
+    hv[i] = (i <= (int)tmv) ? __ldcg(&w->hist_vic[i]) : 0u;
   }
   __syncthreads();
   int gw, gv;
@@ -524,50 +528,70 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
   block_threshold_fast(hw, (u32)c.window, wsum, &gw, &wu);
   block_threshold_fast(hv, (u32)VSEL, wsum, &gv, &vu);
   if (threadIdx.x == 0) {
-    if (gw > (int)vw->tmin_win) gw = (int)vw->tmin_win;
-    if (gv > (int)vw->tmin_vic) gv = (int)vw->tmin_vic;
+    // scalar epilogue on register copies: one burst of independent loads in,
+    // plain stores out (no dependent global round trips)
+    mars_scalars s;
+    {
+      const unsigned long long* src = (const unsigned long long*)sc;
+      unsigned long long* dst = (unsigned long long*)&s;
+#pragma unroll
+      for (int q = 0; q < (int)(sizeof(mars_scalars) / 8); ++q) dst[q] = __ldcg(src + q);
+    }
+    const unsigned long long exp_blocks = __ldcg(&w->exp_blocks);
+    const int n_active_all = __ldcg(&w->n_active), n_queued_all = __ldcg(&w->n_queued);
+    const int n_long_all = __ldcg(&w->n_long_q), mx_all = __ldcg(&w->max_req);
+    const int mn_all = __ldcg(&w->min_req);
+    const mars_step_in in = w->in;
+    if (gw > (int)tmw) gw = (int)tmw;
+    if (gv > (int)tmv) gv = (int)tmv;
     w->t_win = gw;
     w->t_vic = gv;
     w->n_win_cand_expected = (i32)wu;
     w->n_vic_cand_expected = (i32)vu;
-    const int mode = w->in.mode;
-    i64 total = sc->total_blocks;
-    i64 freeb = sc->free_blocks + (i64)vw->exp_blocks;
-    sc->free_blocks = freeb;
+    const int mode = in.mode;
+    const i64 total = s.total_blocks;
+    const i64 freeb = s.free_blocks + (i64)exp_blocks;
+    s.free_blocks = freeb;
     w->free_after_expiry = freeb;
     if (!(mode & MARS_MODE_SKIP_PROBE)) {
       // Telemetry.probe (telemetry.py:152-158) after the expiry evictions
-      sc->available_kv = freeb;
-      sc->kv_usage_ratio = (double)(total - freeb) / (double)total;
-      sc->active_sessions = vw->n_active;
-      sc->active_tools = w->in.active_tools;
-      sc->queued_tools = w->in.queued_tools;
+      s.available_kv = freeb;
+      s.kv_usage_ratio = (double)(total - freeb) / (double)total;
+      s.active_sessions = n_active_all;
+      s.active_tools = in.active_tools;
+      s.queued_tools = in.queued_tools;
     }
-    i64 qlen = sc->queue_len;
+    const i64 qlen = s.queue_len;
     w->qlen = qlen;
-    if (!(mode & MARS_MODE_NO_ROWS) && (i64)vw->n_queued != qlen) w->status |= ST_QUEUE_MISMATCH;
+    if (!(mode & MARS_MODE_NO_ROWS) && (i64)n_queued_all != qlen) w->status |= ST_QUEUE_MISMATCH;
     // what the control plane sees: this replica's probe (pooled in sharded mode,
     // see k_global_control)
-    w->adm_avail = sc->available_kv;
+    w->adm_avail = s.available_kv;
     w->adm_total = total;
-    w->adm_usage = sc->kv_usage_ratio;
-    w->adm_active = sc->active_sessions;
+    w->adm_usage = s.kv_usage_ratio;
+    w->adm_active = s.active_sessions;
     if (mode & MARS_MODE_SHARDED) {
-      xc[0] = sc->available_kv;
+      xc[0] = s.available_kv;
       xc[1] = total;
-      xc[2] = sc->active_sessions;
-      xc[3] = sc->queue_len;
-    } else if (w->in.control_due && !(mode & MARS_MODE_SKIP_REFRESH)) {
-      refresh_pressure(c, sc, w->in.worker_slots, sc->kv_usage_ratio);
+      xc[2] = s.active_sessions;
+      xc[3] = s.queue_len;
+    } else if (in.control_due && !(mode & MARS_MODE_SKIP_REFRESH)) {
+      refresh_pressure(c, &s, in.worker_slots, s.kv_usage_ratio);
+    }
+    {
+      const unsigned long long* src = (const unsigned long long*)&s;
+      unsigned long long* dst = (unsigned long long*)sc;
+#pragma unroll
+      for (int q = 0; q < (int)(sizeof(mars_scalars) / 8); ++q) dst[q] = src[q];
     }
     int ne = vw->n_exp;
     w->xlsd_big = ne > SORT_CAP ? 1 : 0;
     w->xlsd_n = ne;
     w->xlsd_maxkey = 0xffffffffull;
     // table-backed queue statistics for pack_queue (control.py:109-122)
-    w->tab_long_q = vw->n_long_q;
-    w->tab_max_req = vw->max_req;
-    w->tab_min_req = vw->min_req;
+    w->tab_long_q = n_long_all;
+    w->tab_max_req = mx_all;
+    w->tab_min_req = mn_all;
   }
 }
 
@@ -575,7 +599,7 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
 // K_C: candidates at the exact thresholds + S2 retention (boundary rows)
 // ---------------------------------------------------------------------------
 
-__global__ void __launch_bounds__(SCAN_TPB) k_compact(Tab t, Cfg c, Work* w, Bufs b,
+__global__ void __launch_bounds__(SCAN_TPB, 2) k_compact(Tab t, Cfg c, Work* w, Bufs b,
                                                       mars_scalars* sc, i64 n_rows) {
   const double now = w->in.now;
   const double scale = (now > 0.0 && now < 1e300) ? 1024.0 / now : 0.0;
@@ -784,7 +808,7 @@ __global__ void __launch_bounds__(256) k_lsd_hist(Lsd L, Work* w, int which, int
   L.cnt[blockIdx.x * 256 + threadIdx.x] = h[threadIdx.x];
 }
 
-__global__ void __launch_bounds__(256) k_lsd_scan(Lsd L, Work* w, int which, int pass, int G) {
+__global__ void __launch_bounds__(1024) k_lsd_scan(Lsd L, Work* w, int which, int pass, int G) {
   LsdView v = lsd_view(w, which);
   if (!*v.big) return;
   int shift = 8 * pass;
@@ -792,26 +816,50 @@ __global__ void __launch_bounds__(256) k_lsd_scan(Lsd L, Work* w, int which, int
     if (threadIdx.x == 0) v.skip[pass] = 1;
     return;
   }
-  __shared__ u32 sh[256];
-  int d = threadIdx.x;
+  // 1024 threads: digit d = tid % 256 over CTA quarter p = tid / 256
+  __shared__ u32 part[4][256];
+  __shared__ u32 base[256];
+  const int d = threadIdx.x & 255, p = threadIdx.x >> 8;
+  const int c0 = (G * p) / 4, c1 = (G * (p + 1)) / 4;
   u32 tot = 0;
 #pragma unroll 8
-  for (int cta = 0; cta < G; ++cta) tot += L.cnt[cta * 256 + d];
-  sh[d] = tot;
+  for (int cta = c0; cta < c1; ++cta) tot += L.cnt[cta * 256 + d];
+  part[p][d] = tot;
   __syncthreads();
-  for (int off = 1; off < 256; off <<= 1) {
-    u32 x = d >= off ? sh[d - off] : 0;
-    __syncthreads();
-    sh[d] += x;
-    __syncthreads();
+  if (threadIdx.x < 256) {
+    u32 all = part[0][d] + part[1][d] + part[2][d] + part[3][d];
+    base[d] = all;
   }
-  u32 run = sh[d] - tot;
-  for (int cta = 0; cta < G; ++cta) {
+  __syncthreads();
+  if (threadIdx.x < 32) {  // exclusive scan of the 256 digit totals, 8 per lane
+    u32 v[8], s = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      v[q] = base[threadIdx.x * 8 + q];
+      s += v[q];
+    }
+    u32 incl = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      u32 x = __shfl_up_sync(FULL, incl, o);
+      if ((int)threadIdx.x >= o) incl += x;
+    }
+    u32 run = incl - s;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      base[threadIdx.x * 8 + q] = run;
+      run += v[q];
+    }
+  }
+  __syncthreads();
+  u32 run = base[d];
+  for (int q = 0; q < p; ++q) run += part[q][d];
+  for (int cta = c0; cta < c1; ++cta) {
     u32 x = L.cnt[cta * 256 + d];
     L.cnt[cta * 256 + d] = run;
     run += x;
   }
-  if (d == 0) {
+  if (threadIdx.x == 0) {
     v.skip[pass] = 0;
     v.in[pass] = *v.cur;
     *v.cur = 1 - *v.cur;
@@ -1169,6 +1217,9 @@ __global__ void __launch_bounds__(SCAN_TPB) k_admit_apply(Tab t, Cfg c, Work* w,
   long long proj = 0;
   const i64 stride = (i64)gridDim.x * blockDim.x;
   const i64 lim = ((take + 31) / 32) * 32;
+  // the whole list is admitted: apply admit() in list order (row writes stay
+  // sequential for a row-ordered list) -- the admitted set is the same
+  const bool in_order = !sharded && !(w->in.mode & MARS_MODE_NO_ROWS) && take == qlen;
   for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < lim; i += stride) {
     bool valid = i < take;
     bool wc = false, own = false;
@@ -1177,7 +1228,7 @@ __global__ void __launch_bounds__(SCAN_TPB) k_admit_apply(Tab t, Cfg c, Work* w,
     if (valid && (w->in.mode & MARS_MODE_NO_ROWS)) {
       b.admitted[i] = src_row[perm[i]];
     } else if (valid) {
-      u32 pos = perm[i];
+      u32 pos = in_order ? (u32)i : perm[i];
       row = src_row[pos];
       if (sharded && row == XQ_NONE) {
         // another replica's session: a fresh queued session projects exactly
@@ -1199,7 +1250,7 @@ __global__ void __launch_bounds__(SCAN_TPB) k_admit_apply(Tab t, Cfg c, Work* w,
         t.promos[row] = 0;
         t.served[row] = 0;
         proj += ceil_div64(cn, c.bs) - ceil_div64(kvv, c.bs);
-        if (!sharded) b.admitted[i] = row;
+        if (!sharded) b.admitted[i] = in_order ? src_row[perm[i]] : row;
         u32 kl = c.coord ? lv : 0u;
         double tt = c.coord ? now : t.arr[row];
         window_key(kl, tt, t.rank[row], whi, wlo);
@@ -2259,7 +2310,7 @@ int mars_enqueue_step(const LaunchArgs* a) {
   if (a->exp_may_be_big) {
     for (int p = 0; p < 4; ++p) {
       k_lsd_hist<<<LSD_G, 256, 0, s2>>>(a->xlsd, a->work, 1, p);
-      k_lsd_scan<<<1, 256, 0, s2>>>(a->xlsd, a->work, 1, p, LSD_G);
+      k_lsd_scan<<<1, 1024, 0, s2>>>(a->xlsd, a->work, 1, p, LSD_G);
       k_lsd_scatter<<<LSD_G, 256, 0, s2>>>(a->xlsd, a->work, 1, p);
       launches += 3;
     }
@@ -2274,11 +2325,11 @@ int mars_enqueue_step(const LaunchArgs* a) {
                                                     a->gq);
     launches++;
     // ~4K list entries per CTA: the single-CTA offset scan walks G columns
-    i64 lgq = (a->queue_upper + 4095) / 4096;
+    i64 lgq = (a->queue_upper + 1023) / 1024;  // ~1K list entries per CTA
     int lg = (int)(lgq < 1 ? 1 : (lgq > LSD_G ? LSD_G : lgq));
     for (int p = 0; p < a->queue_passes; ++p) {
       k_lsd_hist<<<lg, 256, 0, s>>>(a->qlsd, a->work, 0, p);
-      k_lsd_scan<<<1, 256, 0, s>>>(a->qlsd, a->work, 0, p, lg);
+      k_lsd_scan<<<1, 1024, 0, s>>>(a->qlsd, a->work, 0, p, lg);
       k_lsd_scatter<<<lg, 256, 0, s>>>(a->qlsd, a->work, 0, p);
       launches += 3;
     }

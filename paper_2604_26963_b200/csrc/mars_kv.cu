@@ -178,3 +178,27 @@ int mars_kv_enqueue_copy(const Kv& k, cudaStream_t s, const u32* ids, i64 n, i64
   k_kv_copy<<<grid, 512, 0, s>>>(k, ids, n, slot0, dir);
   return (int)cudaGetLastError();
 }
+
+// staged path: gather scattered blocks (layer-major pool) into a contiguous
+// HBM staging buffer [n][layers][piece] -- or scatter back -- so the PCIe
+// transfer is one large copy-engine DMA.  dir 0: pool -> staging, 1: back.
+__global__ void __launch_bounds__(512) k_kv_stage(const Kv k, const u32* ids, i64 n, u8* stage,
+                                                  int dir) {
+  const i64 piece = k.block_bytes / k.layers;
+  const i64 pieces = n * k.layers;
+  for (i64 pc = blockIdx.x; pc < pieces; pc += gridDim.x) {
+    i64 bi = pc / k.layers, layer = pc % k.layers;
+    u8* pool = k.data + (layer * k.total + (i64)ids[bi]) * piece;
+    u8* st = stage + (bi * k.layers + layer) * piece;
+    const int4* s4 = (const int4*)(dir == 0 ? pool : st);
+    int4* d4 = (int4*)(dir == 0 ? st : pool);
+    const i64 m = piece / 16;
+    for (i64 j = threadIdx.x; j < m; j += blockDim.x) d4[j] = s4[j];
+  }
+}
+
+int mars_kv_enqueue_stage(const Kv& k, cudaStream_t s, const u32* ids, i64 n, u8* stage, int dir,
+                          int grid) {
+  k_kv_stage<<<grid, 512, 0, s>>>(k, ids, n, stage, dir);
+  return (int)cudaGetLastError();
+}

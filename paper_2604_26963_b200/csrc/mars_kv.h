@@ -4,6 +4,7 @@
 #include "mars_internal.cuh"
 
 #define KV_CH 64  // block IDs per table chunk
+#define KV_STAGE_BLOCKS 64  // blocks per staged host-tier DMA (128 MiB at 2 MiB/block)
 
 struct KvScal {
   i64 fs_top;   // explicit stack entries
@@ -38,3 +39,5 @@ int mars_kv_enqueue_table(const Kv& k, cudaStream_t s, u32 row, i64 cap, u32* ou
 int mars_kv_enqueue_top(const Kv& k, cudaStream_t s, i64 cnt, u32* out);
 int mars_kv_enqueue_copy(const Kv& k, cudaStream_t s, const u32* ids, i64 n, i64 slot0, int dir,
                          int grid);
+int mars_kv_enqueue_stage(const Kv& k, cudaStream_t s, const u32* ids, i64 n, u8* stage, int dir,
+                          int grid);

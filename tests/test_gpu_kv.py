@@ -111,7 +111,7 @@ def test_step_journal_updates_block_tables_like_the_restatement():
     eng.close()
 
 
-@pytest.mark.parametrize("method", [0, 1])
+@pytest.mark.parametrize("method", [0, 1, 2])
 def test_kv_bytes_round_trip_through_the_host_tier(method):
     bb, layers = 2 << 20, 32
     eng = MarsEngine(max_rows=64, max_queue=1)
@@ -128,7 +128,7 @@ def test_kv_bytes_round_trip_through_the_host_tier(method):
     assert np.array_equal(host[32:48], src)
     # per-block checksums survive a second scattered hop
     ids2 = rng.choice(256, size=16, replace=False).astype(np.uint32)
-    kv.restore(ids2, slot0=32, method=1 - method)
+    kv.restore(ids2, slot0=32, method=(method + 1) % 3)
     kv.evict(ids2, slot0=0, method=method)
     assert [int(x) for x in host[:16].sum(axis=1, dtype=np.uint64)] == \
         [int(x) for x in src.sum(axis=1, dtype=np.uint64)]

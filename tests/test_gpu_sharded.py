@@ -20,8 +20,10 @@ from tests._canon import canon
 pytestmark = pytest.mark.gpu
 
 
-def _replica(snap, world, rank, gpos):
-    eng = MarsEngine(max_rows=snap.n, max_queue=max(len(snap.queue), 1) * 2,
+def _replica(snap, world, rank, gpos, cap=None):
+    # every replica exchanges the same fixed-size buffers: one capacity for all
+    cap = cap or max(len(snap.queue), 1) * 2
+    eng = MarsEngine(max_rows=snap.n, max_queue=cap,
                      config=make_config(initial_window=snap.initial_window))
     eng.load_snapshot(snap)
     sh = ShardedEngine(eng, world=world, rank=rank)
@@ -55,7 +57,8 @@ def test_two_replicas_on_one_gpu_match_the_sharded_oracle():
     snaps = [snapshot_v1(30_000, seed=70 + g, pool="headroom") for g in range(2)]
     gpos = interleaved_gpos([len(s.queue) for s in snaps])
     want = run_multi_step([s.copy() for s in snaps], gpos)
-    reps = [_replica(s, 2, g, gpos[g]) for g, s in enumerate(snaps)]
+    cap = 2 * max(len(s.queue) for s in snaps)
+    reps = [_replica(s, 2, g, gpos[g], cap) for g, s in enumerate(snaps)]
     sis = [e.step_in(s.now, True, s.active_tools, 0, s.worker_slots) for (e, _), s in
            zip(reps, snaps)]
     for (e, sh), si in zip(reps, sis):
