@@ -177,6 +177,9 @@ typedef struct mars_step_out {
   int32_t n_finish;
   const uint32_t *fin_rows; const uint8_t *fin_pin;
   const double *fin_benefit, *fin_cost, *fin_deadline;
+  /* diagnostics: candidate counts at the exact thresholds, 1 if the walk
+   * left the prefix-sum fast path */
+  int32_t n_window_cand, n_victim_cand, walk_slow;
 } mars_step_out;
 
 /* ---- lifecycle ------------------------------------------------------- */
@@ -282,9 +285,9 @@ int mars_sync(mars_ctx* ctx);
 int mars_last_launch_count(mars_ctx* ctx);
 
 /* per-kernel device times of the last step, recorded with CUDA events on the
- * stream each kernel runs on: [scan, compact, expired-sort, pack, admit, walk]
- * in ms (-1 = not launched).  Profiling must be enabled before the step. */
-#define MARS_NUM_KTIMES 6
+ * stream each kernel runs on: [scan, compact, expired-sort, pack, admit, walk,
+ * pack-sort] in ms (-1 = not launched).  Profiling must be enabled before the step. */
+#define MARS_NUM_KTIMES 7
 int mars_set_profiling(mars_ctx* ctx, int on);
 int mars_kernel_times(mars_ctx* ctx, float* ms, int n);   /* sync */
 

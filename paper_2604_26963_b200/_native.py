@@ -104,6 +104,7 @@ class MarsStepOut(C.Structure):
         ("decode_level", P(u8)), ("prefill_level", P(u8)), ("n_finish", i32),
         ("fin_rows", P(u32)), ("fin_pin", P(u8)), ("fin_benefit", P(f64)),
         ("fin_cost", P(f64)), ("fin_deadline", P(f64)),
+        ("n_window_cand", i32), ("n_victim_cand", i32), ("walk_slow", i32),
     ]
 
 
@@ -150,7 +151,8 @@ _SIGS = {
     "mars_kernel_times": (i32, [C.c_void_p, P(C.c_float), C.c_int]),
 }
 
-KTIME_NAMES = ("k_scan", "k_compact", "k_expired_sort", "k_pack", "k_admit_apply", "k_walk")
+KTIME_NAMES = ("k_scan", "k_compact", "k_expired_sort", "k_pack", "k_admit_apply", "k_walk",
+               "k_pack_sort")
 
 EXPORTS = tuple(_SIGS)
 

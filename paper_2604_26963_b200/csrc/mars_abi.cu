@@ -278,11 +278,8 @@ int mars_create(const mars_config* hcfg, int device, int64_t max_rows, int64_t m
   CK(cudaMemset(ctx->qsel, 0, sizeof(i32)));
   Bufs& b = ctx->bufs;
   memset(&b, 0, sizeof b);
-  ALLOC(b.exp_seg_row, R * 4);
-  ALLOC(b.exp_seg_blk, R * 4);
-  ALLOC(b.exp_seg_rank, R * 4);
   ALLOC(b.tile_cnt, (R / 4096 + 2) * 4);
-  ALLOC(b.tile_off, (R / 4096 + 2) * 4);
+  ALLOC(b.row_dig, R * 4);
   ALLOC(b.exp_row, R * 4);
   ALLOC(b.exp_blk, R * 4);
   ALLOC(b.exp_rank, R * 4);
@@ -388,7 +385,7 @@ int mars_destroy(mars_ctx* ctx) {
   cudaFree(ctx->sc);
   cudaFree(ctx->qsel);
   Bufs& b = ctx->bufs;
-  void* bs[] = {b.exp_seg_row, b.exp_seg_blk, b.exp_seg_rank, b.tile_cnt, b.tile_off, b.exp_row, b.exp_blk, b.exp_rank, b.exp_row_sorted, b.exp_blk_sorted, b.wc_hi,
+  void* bs[] = {b.tile_cnt, b.row_dig, b.exp_row, b.exp_blk, b.exp_rank, b.exp_row_sorted, b.exp_blk_sorted, b.wc_hi,
                 b.wc_lo, b.wc_row, b.vc_key, b.vc_whi, b.vc_wlo, b.vc_row, b.vc_blk, b.ret_row,
                 b.ret_pin, b.ret_b, b.ret_c, b.ret_d, b.admitted, b.win_rows, b.dec_rows,
                 b.pre_rows, b.pre_grant, b.ev_row, b.ev_kind, b.ev_blk, b.j_op, b.j_row, b.j_n,
@@ -728,6 +725,9 @@ int mars_step_fetch(mars_ctx* ctx, mars_step_out* o) {
   o->decode_level = (const uint8_t*)pull(ctx, off, b.dec_level, (size_t)w.n_dec);
   o->prefill_level = (const uint8_t*)pull(ctx, off, b.pre_level, (size_t)w.n_pre);
   o->n_finish = w.n_finish;
+  o->n_window_cand = w.n_wc;
+  o->n_victim_cand = w.n_vc;
+  o->walk_slow = w.walk_slow;
   o->fin_rows = (const uint32_t*)pull(ctx, off, b.fin_row, (size_t)w.n_finish * 4);
   o->fin_pin = (const uint8_t*)pull(ctx, off, b.fin_pin, (size_t)w.n_finish);
   o->fin_benefit = (const double*)pull(ctx, off, b.fin_b, (size_t)w.n_finish * 8);

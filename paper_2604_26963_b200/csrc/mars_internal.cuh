@@ -19,7 +19,7 @@ typedef int64_t i64;
 #define SORT_CAP 4096         // bitonic sort capacity of the single-CTA selector
 #define VSEL 256              // victim-stream target length (prefix of reclaim order)
 #define VSTREAM_CAP 2048      // victim stream entries kept in shared memory
-#define LSD_G 592             // max CTAs of the multi-CTA LSD radix sort (4 x 148 SMs)
+#define LSD_G 592             // max CTAs of the cooperative LSD radix sort (>= #SMs)
 #define SCAN_RPT 4            // consecutive rows per thread in the table scans
 #define MAX_SCAN_CTAS 1024    // upper bound of k_scan's grid
 #define ROW_PAD 2048          // row capacity is padded to this multiple
@@ -93,13 +93,10 @@ struct Lsd {
 struct Work {
   mars_step_in in;
   // K_A accumulators
-  u32 ticket;
   u32 ticket_ap;
   unsigned long long exp_blocks;
   i32 n_exp, n_active, n_queued, n_long_q, n_ready, n_promoted, n_victims, n_boundary;
   i32 tab_long_q, tab_max_req, tab_min_req;  // queue stats from the table scan
-  i32 scan_ctas;
-  i64 scan_chunk;
   i32 max_req, min_req;
   u32 tmin_win, tmin_vic;
   u32 hist_win[HIST_BINS];
@@ -139,9 +136,9 @@ struct Work {
 
 // variable-length step buffers
 struct Bufs {
-  // expired pins: per-CTA row-ordered segments (K_A), contiguous (K_C), rank order
-  u32 *exp_seg_row; i32 *exp_seg_blk; u32 *exp_seg_rank;
-  i32 *tile_cnt, *tile_off;  // per-4096-row-tile expired counts / offsets
+  // expired pins: row order (k_scan), rank order (k_exp_*)
+  i32 *tile_cnt;             // per-k_scan-CTA expired counts
+  u32 *row_dig;              // k_scan digit record when it exceeds shared memory
   u32 *exp_row; i32 *exp_blk; u32 *exp_rank;
   u32 *exp_row_sorted; i32 *exp_blk_sorted;
   // window candidates
@@ -215,7 +212,26 @@ __device__ __forceinline__ u32 victim_digit(bool running, bool nonexp, u32 level
          (255u - blocks_bucket(blocks));
 }
 
-__device__ __forceinline__ i64 ceil_div64(i64 a, i64 b) { return (a + b - 1) / b; }
+// 64-bit division kept out of line: the single-CTA kernels pay for every
+// instruction-cache line they touch, so rarely taken slow paths stay compact
+static __device__ __noinline__ i64 div64_slow(i64 a, i64 b) { return a / b; }
+static __device__ __noinline__ i64 mod64_slow(i64 a, i64 b) { return a % b; }
+__device__ __forceinline__ i64 ceil_div64(i64 a, i64 b) { return div64_slow(a + b - 1, b); }
+
+// blocks_for_tokens (engine.py:112-113) for x >= 0: a shift when the block
+// size is a power of two (no 64-bit division on the hot paths)
+__device__ __forceinline__ i64 blocks_ceil(const Cfg& c, i64 x) {
+  if (c.bs_shift >= 0) return (x + (i64)c.bs - 1) >> c.bs_shift;
+  return ceil_div64(x, c.bs);
+}
+// (x // bs) * bs for x >= 0
+__device__ __forceinline__ i64 blocks_floor_tokens(const Cfg& c, i64 x) {
+  if (c.bs_shift >= 0) return x & ~((i64)c.bs - 1);
+  return div64_slow(x, c.bs) * c.bs;
+}
+__device__ __forceinline__ bool block_aligned(const Cfg& c, i64 x) {
+  return c.bs_shift >= 0 ? (x & ((i64)c.bs - 1)) == 0 : mod64_slow(x, c.bs) == 0;
+}
 
 // held_blocks / blocks_for_tokens (engine.py:112-113, 314-315) for kv >= 0
 __device__ __forceinline__ i64 held_blocks(const Cfg& c, i32 kv) {
@@ -242,7 +258,7 @@ __device__ __forceinline__ void decide_retention(const Cfg& c, i64 context, i64 
                                                  double now, u8& pin, double& benefit,
                                                  double& cost, double& deadline) {
   benefit = (double)context / c.prefill_rate;
-  i64 foot = ceil_div64(kv, c.bs);
+  i64 foot = blocks_ceil(c, kv);
   double pw;
   if (usage >= 1.0) {
     pw = c.pw_clip;

@@ -1,15 +1,19 @@
 // B200 (sm_100a) kernels of the MARS scheduling step.
 //
-// Pipeline, one CUDA stream + one side stream:
-//   k_scan        multi-CTA pass over the session table: pin expiry, MLFQ aging
-//                 (promote_waiting), counters, per-CTA key histograms; the
-//                 last CTA finalises pool/telemetry scalars, refresh_pressure,
-//                 and the exact global top-k thresholds.
-//   k_compact     [side] second pass: window / victim candidates at the exact
-//                 thresholds, S2 retention for BOUNDARY rows.
-//   k_exp_*       [side] expired pins in session-id (rank) order.
+// Pipeline, one CUDA stream (+ a side stream for the rare
+// expired-pin sort):
+//   k_scan        persistent cooperative pass over the session table, one CTA
+//                 per SM: pin expiry, MLFQ aging (promote_waiting), counters,
+//                 per-CTA key histograms and a per-row digit record; grid
+//                 barrier; exact global top-k thresholds, window / victim
+//                 candidates, S2 retention for BOUNDARY rows, expired pins in
+//                 row order; CTA 0 finalises pool/telemetry scalars and
+//                 refresh_pressure.
+//   k_exp_*       [side] expired pins in session-id (rank) order when the
+//                 table is not rank-ordered.
 //   k_pack_small  control plane: pack_queue for small queues (bitonic) and the
-//                 first-fit mode; k_lsd_* multi-CTA stable LSD sort for big ones.
+//                 first-fit mode; k_lsd_coop cooperative stable LSD sort for
+//                 big ones.
 //   k_admit_apply update_window + triple clamp, admit() of the packed prefix,
 //                 residual queue, admitted rows join the window candidates.
 //   k_walk        single CTA: window top-k, build_plan decode/prefill passes
@@ -19,13 +23,51 @@
 // Compiled with --fmad=false: every f64 expression keeps CPython's IEEE
 // rounding so retention / admission scalars are bit-identical.
 
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdio.h>
+
+namespace cg = cooperative_groups;
 
 #include "mars_internal.cuh"
 #include "mars_launch.h"
 
 #define FULL 0xffffffffu
+
+#ifdef MARS_PHASE_TIMING
+// Debug builds only (-DMARS_PHASE_TIMING): per-CTA %globaltimer stamps at
+// named points of the step, dumped as a timeline after each step.
+#define PT_SLOTS 24
+__device__ unsigned long long g_ptime[1024][PT_SLOTS];
+__device__ __forceinline__ void ptime(int k) {
+  if (threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_ptime[blockIdx.x][k] = t;
+  }
+}
+__global__ void k_ptime_dump() {
+  unsigned long long t0 = ~0ull;
+  for (int i = 0; i < 1024; ++i)
+    if (g_ptime[i][0]) t0 = min(t0, g_ptime[i][0]);
+  for (int k = 0; k < PT_SLOTS; ++k) {
+    unsigned long long mn = ~0ull, mx = 0;
+    int cnt = 0;
+    for (int i = 0; i < 1024; ++i) {
+      unsigned long long v = g_ptime[i][k];
+      if (!v) continue;
+      cnt++;
+      mn = min(mn, v - t0);
+      mx = max(mx, v - t0);
+      g_ptime[i][k] = 0;
+    }
+    if (cnt) printf("stamp %2d: ctas %4d  min %7.2f us  max %7.2f us\n", k, cnt, mn / 1e3, mx / 1e3);
+  }
+}
+#define PTIME(k) ptime(k)
+#else
+#define PTIME(k)
+#endif
 
 // ---------------------------------------------------------------------------
 // block utilities
@@ -212,154 +254,272 @@ __device__ void refresh_pressure(const Cfg& c, mars_scalars* sc, int worker_slot
 #define SCAN_TPB 1024
 #define SCAN_TILE (SCAN_TPB * SCAN_RPT)  // rows per tile (4096)
 
-// Smallest bin d with cumsum(h[0..d]) >= k over HIST_BINS shared bins (nb-1
-// if the total is below k); *upto = cumsum(h[0..d]).  Warp-shuffle scans:
-// two barriers.  blockDim.x == SCAN_TPB, HIST_BINS / SCAN_TPB bins per thread.
-__device__ void block_threshold_fast(const u32* h, u32 k, u32* wsum, int* out_d, u32* upto) {
+// Per-row digit record written by phase 1 and read by phase 2 of k_scan:
+// low half = window digit (DIG_NONE if the row is not ready, DIG_BND set for
+// a boundary row), high half = victim digit (DIG_NONE if not a victim,
+// DIG_EXP for a pin that expired this step).
+#define DIG_NONE 0x8000u
+#define DIG_BND 0x4000u
+#define DIG_EXP 0x4000u
+#define DIG_SMEM_MAX (64 * 1024)  // record kept in shared memory up to this size
+
+// For two HIST_BINS shared histograms at once: the smallest bin d with
+// cumsum(h[0..d]) >= k (HIST_BINS-1 if the total is below k), and
+// *upto = cumsum(h[0..d]).  Warp-shuffle scans, three barriers for both.
+// blockDim.x == SCAN_TPB, HIST_BINS / SCAN_TPB bins per thread.
+__device__ void block_threshold_pair(const u32* ha, u32 ka, const u32* hb, u32 kb, u32* wsum2,
+                                     int* da, u32* ua, int* db, u32* ub) {
   constexpr int PER = HIST_BINS / SCAN_TPB;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int base = threadIdx.x * PER;
-  u32 v[PER];
-  u32 s = 0;
+  u32 va[PER], vb[PER];
+  u32 sa = 0, sb = 0;
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
-    v[i] = h[base + i];
-    s += v[i];
+    va[i] = ha[base + i];
+    vb[i] = hb[base + i];
+    sa += va[i];
+    sb += vb[i];
   }
-  u32 incl = s;
+  u32 ia = sa, ib = sb;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    u32 x = __shfl_up_sync(FULL, incl, o);
-    if (lane >= o) incl += x;
+    u32 xa = __shfl_up_sync(FULL, ia, o), xb = __shfl_up_sync(FULL, ib, o);
+    if (lane >= o) {
+      ia += xa;
+      ib += xb;
+    }
   }
-  __shared__ int s_d;
-  __shared__ u32 s_up;
-  if (lane == 31) wsum[wid] = incl;
+  __shared__ int s_d[2];
+  __shared__ u32 s_up[2];
+  if (lane == 31) {
+    wsum2[wid] = ia;
+    wsum2[32 + wid] = ib;
+  }
   if (threadIdx.x == 0) {
-    s_d = HIST_BINS - 1;
-    s_up = 0xffffffffu;
+    s_d[0] = s_d[1] = HIST_BINS - 1;
+    s_up[0] = s_up[1] = 0xffffffffu;
   }
   __syncthreads();
-  if (wid == 0) {
-    u32 t = wsum[lane];
+  if (wid < 2) {
+    u32 t = wsum2[wid * 32 + lane];
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       u32 x = __shfl_up_sync(FULL, t, o);
       if (lane >= o) t += x;
     }
-    wsum[lane] = t;
+    wsum2[wid * 32 + lane] = t;
   }
   __syncthreads();
-  const u32 total = wsum[31];
-  incl += wid ? wsum[wid - 1] : 0u;
-  const u32 excl = incl - s;
-  if (total >= k && excl < k && incl >= k) {
-    u32 cum = excl;
+  const u32 ta = wsum2[31], tb = wsum2[63];
+  ia += wid ? wsum2[wid - 1] : 0u;
+  ib += wid ? wsum2[32 + wid - 1] : 0u;
+  const u32 ea = ia - sa, eb = ib - sb;
+  if (ta >= ka && ea < ka && ia >= ka) {
+    u32 cum = ea;
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
-      u32 nc = cum + v[i];
-      if (cum < k && nc >= k) {
-        s_d = base + i;
-        s_up = nc;
+      u32 nc = cum + va[i];
+      if (cum < ka && nc >= ka) {
+        s_d[0] = base + i;
+        s_up[0] = nc;
+      }
+      cum = nc;
+    }
+  }
+  if (tb >= kb && eb < kb && ib >= kb) {
+    u32 cum = eb;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      u32 nc = cum + vb[i];
+      if (cum < kb && nc >= kb) {
+        s_d[1] = base + i;
+        s_up[1] = nc;
       }
       cum = nc;
     }
   }
   __syncthreads();
-  *out_d = s_d;
-  *upto = (s_up == 0xffffffffu) ? total : s_up;
+  *da = s_d[0];
+  *ua = (s_up[0] == 0xffffffffu) ? ta : s_up[0];
+  *db = s_d[1];
+  *ub = (s_up[1] == 0xffffffffu) ? tb : s_up[1];
   __syncthreads();
 }
 
-// Persistent: one CTA per SM walks tiles t = blockIdx.x, blockIdx.x + gridDim.x, ...
+// ---- 1D TMA (cp.async.bulk) + mbarrier helpers -----------------------------
+__device__ __forceinline__ u32 smem_u32(const void* p) {
+  return (u32)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(u64* bar, u32 count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(u64* bar, u32 bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64* bar, u32 parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// bulk copy global -> shared (16-byte aligned, size a multiple of 16)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, u32 bytes, u64* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// k_scan staging: one round = SCAN_TPB consecutive rows (one per thread),
+// every column k_scan reads arrives by TMA into one of SCAN_NBUF ring buffers.
+#define SCAN_R SCAN_TPB
+#define SCAN_NBUF 3
+#define SB_RS 0                       // f64 ready_since (or arrival when coordinator off)
+#define SB_WS (SB_RS + 8 * SCAN_R)    // f64 wait_since
+#define SB_DL (SB_WS + 8 * SCAN_R)    // f64 pin deadline
+#define SB_KV (SB_DL + 8 * SCAN_R)    // i32 kv tokens
+#define SB_PB (SB_KV + 4 * SCAN_R)    // i32 pinned blocks
+#define SB_REQ (SB_PB + 4 * SCAN_R)   // i32 queued req blocks
+#define SB_FL (SB_REQ + 4 * SCAN_R)   // u8 flags
+#define SB_PH (SB_FL + SCAN_R)        // u8 phase
+#define SB_LV (SB_PH + SCAN_R)        // u8 level
+#define SB_PR (SB_LV + SCAN_R)        // u8 promotions
+#define SB_PL (SB_PR + SCAN_R)        // u8 pinned level
+#define SB_BYTES (SB_PL + SCAN_R)     // 41 bytes per row
+#define SCAN_ROW_BYTES 41
+
+static size_t scan_stage_bytes() { return (size_t)SCAN_NBUF * SB_BYTES; }
+
+// Persistent cooperative scan, one CTA per SM; CTA g owns the contiguous rows
+// [g * chunk, (g + 1) * chunk), chunk a multiple of 16.
+//  phase 1: stream the rows once through a 3-deep TMA ring (bulk copies of
+//           every column the scan reads, completion on mbarriers) -- expiry,
+//           aging (promote_waiting), counters, local histograms, the per-row
+//           digit record, expired pins compacted in row order into the CTA's
+//           segment.  After rounds 0 and 2 the CTA's running top-k bins bound
+//           the histogram: rows above them cannot be in the CTA's (so not in
+//           the global) top-k and skip their shared-memory atomics;
+//  grid barrier;
+//  phase 2: every CTA derives the global thresholds from the merged histogram
+//           prefix and emits its own window / victim candidates from the digit
+//           record, the S2 retention of its boundary rows and its expired
+//           pins at their place in the row-ordered list; CTA 0 finalises the
+//           probe / refresh scalars.
 __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Bufs b,
-                                                      mars_scalars* sc, i64 n_rows, i64* xc) {
+                                                      mars_scalars* sc, i64 n_rows, i64* xc,
+                                                      i64 chunk, int dig_in_smem) {
+  extern __shared__ __align__(128) unsigned char sdyn[];
   __shared__ u32 hw[HIST_BINS];
   __shared__ u32 hv[HIST_BINS];
-  __shared__ u32 wsum[32];
-  __shared__ bool s_last;
+  __shared__ u32 wsum[64];
+  __shared__ u32 s_bw, s_bv;  // running histogram bounds (digits above are not counted)
+  __shared__ __align__(8) u64 bars[SCAN_NBUF];
+  cg::grid_group grid = cg::this_grid();
 
+  PTIME(0);
   for (int i = threadIdx.x; i < HIST_BINS; i += blockDim.x) hw[i] = hv[i] = 0;
-  __syncthreads();
+  const int me = blockIdx.x;
+  const i64 cs = (i64)me * chunk;
+  const i64 ce = (cs + chunk < n_rows) ? cs + chunk : n_rows;
+  const int nrounds = ce > cs ? (int)((ce - cs + SCAN_R - 1) / SCAN_R) : 0;
+  const double* tcol = c.coord ? t.rs : t.arr;
+  // one thread issues a round's bulk copies (rows rounded up to 16: the
+  // columns are padded, the extra rows are never used)
+  auto issue = [&](int rd) {
+    const i64 rb = cs + (i64)rd * SCAN_R;
+    const int nr = (int)((ce - rb) < SCAN_R ? (ce - rb) : SCAN_R);
+    const u32 n16 = (u32)((nr + 15) & ~15);
+    unsigned char* B = sdyn + (size_t)(rd % SCAN_NBUF) * SB_BYTES;
+    u64* bar = &bars[rd % SCAN_NBUF];
+    mbar_expect_tx(bar, n16 * SCAN_ROW_BYTES);
+    bulk_g2s(B + SB_RS, tcol + rb, n16 * 8, bar);
+    bulk_g2s(B + SB_WS, t.ws + rb, n16 * 8, bar);
+    bulk_g2s(B + SB_DL, t.dl + rb, n16 * 8, bar);
+    bulk_g2s(B + SB_KV, t.kv + rb, n16 * 4, bar);
+    bulk_g2s(B + SB_PB, t.pb + rb, n16 * 4, bar);
+    bulk_g2s(B + SB_REQ, t.req + rb, n16 * 4, bar);
+    bulk_g2s(B + SB_FL, t.flags + rb, n16, bar);
+    bulk_g2s(B + SB_PH, t.phase + rb, n16, bar);
+    bulk_g2s(B + SB_LV, t.level + rb, n16, bar);
+    bulk_g2s(B + SB_PR, t.promos + rb, n16, bar);
+    bulk_g2s(B + SB_PL, t.plevel + rb, n16, bar);
+  };
+  if (threadIdx.x == 0) {
+    s_bw = s_bv = HIST_BINS - 1;
+    for (int q = 0; q < SCAN_NBUF; ++q) mbar_init(&bars[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int rd = 0; rd < nrounds && rd < SCAN_NBUF; ++rd) issue(rd);
+  }
 
   const double now = w->in.now;
-  const bool do_exp = !(w->in.mode & MARS_MODE_SKIP_EXPIRY);
+  const int mode = w->in.mode;
+  const bool do_exp = !(mode & MARS_MODE_SKIP_EXPIRY);
   const double scale = (now > 0.0 && now < 1e300) ? 1024.0 / now : 0.0;
-  const i64 ntiles = (n_rows + SCAN_TILE - 1) / SCAN_TILE;
+  u32* dig = dig_in_smem ? (u32*)(sdyn + (size_t)SCAN_NBUF * SB_BYTES) : b.row_dig + cs;
+  // pre-step scalars: CTA 0 rewrites *sc after the grid barrier
+  const i64 sc_total = sc->total_blocks, sc_free = sc->free_blocks;
+  const double sc_usage = sc->kv_usage_ratio;
+  const double ema = sc->has_ema_tool ? sc->ema_tool : c.tool_prior;
 
   long long exp_blocks = 0;
   int n_active = 0, n_queued = 0, n_long = 0, n_ready = 0, n_prom = 0, n_vic = 0, n_bnd = 0;
+  int n_exp = 0;
   int max_req = 0, min_req = 0x7fffffff;
-  __shared__ int s_wexp[SCAN_TPB / 32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
 
-  // Each thread owns SCAN_RPT consecutive rows per tile: the byte columns
-  // arrive as one 32-bit load, kv as one 128-bit load and the two f64
-  // columns as two 128-bit loads each, all issued before any use.
-  for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const i64 tstart = tile * SCAN_TILE;
-    const i64 tend = (tstart + SCAN_TILE < n_rows) ? tstart + SCAN_TILE : n_rows;
-    const i64 base = tstart + (i64)threadIdx.x * SCAN_RPT;
-    const bool any = base < tend;
-    u32 f4 = 0, ph4 = 0x07070707u, lv4 = 0, pr4 = 0;
-    int4 kv4 = make_int4(0, 0, 0, 0);
-    double2 rsa = make_double2(0, 0), rsb = rsa, wsa = rsa, wsb = rsa;
-    if (any) {
-      f4 = *(const u32*)(t.flags + base);
-      ph4 = *(const u32*)(t.phase + base);
-      lv4 = *(const u32*)(t.level + base);
-      pr4 = *(const u32*)(t.promos + base);
-      kv4 = *(const int4*)(t.kv + base);
-      const double* tcol = c.coord ? t.rs : t.arr;
-      rsa = *(const double2*)(tcol + base);
-      rsb = *(const double2*)(tcol + base + 2);
-      wsa = *(const double2*)(t.ws + base);
-      wsb = *(const double2*)(t.ws + base + 2);
-    }
-    const i32 kva[4] = {kv4.x, kv4.y, kv4.z, kv4.w};
-    const double tt[4] = {rsa.x, rsa.y, rsb.x, rsb.y};
-    const double wsv[4] = {wsa.x, wsa.y, wsb.x, wsb.y};
-    int ne = 0;
-    u32 exp_mask = 0;
-    i32 exp_pb[SCAN_RPT];
-#pragma unroll
-    for (int j = 0; j < SCAN_RPT; ++j) {
-      const i64 r = base + j;
-      exp_pb[j] = 0;
-      if (r >= tend) continue;
-      u8 f = (u8)(f4 >> (8 * j));
-      u8 ph = (u8)(ph4 >> (8 * j));
+  // ---- phase 1 ---------------------------------------------------------------
+  for (int rd = 0; rd < nrounds; ++rd) {
+    const unsigned char* B = sdyn + (size_t)(rd % SCAN_NBUF) * SB_BYTES;
+    mbar_wait(&bars[rd % SCAN_NBUF], (u32)((rd / SCAN_NBUF) & 1));
+    const int lr = threadIdx.x;
+    const i64 r = cs + (i64)rd * SCAN_R + lr;
+    const bool valid = r < ce;
+    const u32 bw = s_bw, bv = s_bv;
+    u32 rw = DIG_NONE, rv = DIG_NONE;
+    if (valid) {
+      const u8 f = B[SB_FL + lr];
+      const u8 ph = B[SB_PH + lr];
       if (f & MARS_F_ACTIVE) n_active++;
       if (f & MARS_F_QUEUED) {
         n_queued++;
         if (f & MARS_F_LONG) n_long++;
-        i32 q = t.req[r];
+        const i32 q = ((const i32*)(B + SB_REQ))[lr];
         max_req = q > max_req ? q : max_req;
         min_req = q < min_req ? q : min_req;
       }
-      if (f & MARS_F_BOUNDARY) n_bnd++;
       if (f & MARS_F_PINNED) {
-        double d = t.dl[r];
-        bool exp_ = d < now;
-        i32 pbk = t.pb[r];
+        const double d = ((const double*)(B + SB_DL))[lr];
+        const bool exp_ = d < now;
+        const i32 pbk = ((const i32*)(B + SB_PB))[lr];
         if (do_exp && exp_) {
           t.flags[r] = f & ~MARS_F_PINNED;
           t.kv[r] = 0;
           exp_blocks += pbk;
-          exp_mask |= 1u << j;
-          exp_pb[j] = pbk;
-          ne++;
+          n_exp++;
+          rv = DIG_EXP;
         } else {
-          atomicAdd(&hv[victim_digit(false, !exp_, t.plevel[r], pbk)], 1u);
+          rv = victim_digit(false, !exp_, B[SB_PL + lr], pbk);
+          if (rv <= bv) atomicAdd(&hv[rv], 1u);
           n_vic++;
         }
       }
       if ((f & MARS_F_ACTIVE) && (ph == MARS_PREFILL || ph == MARS_DECODE)) {
         n_ready++;
-        u32 lv = (lv4 >> (8 * j)) & 255u;
+        u32 lv = B[SB_LV + lr];
         if (c.coord) {
-          u32 pr = (pr4 >> (8 * j)) & 255u;
-          if (lv != 0 && pr < (u32)c.max_promos && now - wsv[j] >= c.promo_wait) {
+          const u32 pr = B[SB_PR + lr];
+          if (lv != 0 && pr < (u32)c.max_promos &&
+              now - ((const double*)(B + SB_WS))[lr] >= c.promo_wait) {
             // promote_waiting (scheduler.py:120-127)
             lv -= 1;
             t.level[r] = (u8)lv;
@@ -370,151 +530,100 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
         } else {
           lv = 0;
         }
-        atomicAdd(&hw[window_digit(lv, tt[j], scale)], 1u);
-        i32 kvv = kva[j];
+        rw = window_digit(lv, ((const double*)(B + SB_RS))[lr], scale);
+        if (rw <= bw) atomicAdd(&hw[rw], 1u);
+        const i32 kvv = ((const i32*)(B + SB_KV))[lr];
         if (kvv > 0) {
-          atomicAdd(&hv[victim_digit(true, false, lv, held_blocks(c, kvv))], 1u);
+          rv = victim_digit(true, false, lv, held_blocks(c, kvv));
+          if (rv <= bv) atomicAdd(&hv[rv], 1u);
           n_vic++;
         }
       }
+      if (f & MARS_F_BOUNDARY) {
+        n_bnd++;
+        rw |= DIG_BND;
+      }
+      dig[r - cs] = rw | (rv << 16);
     }
-    // expired rows of this tile, compacted in row order into the tile's segment
-    int tile_exp = 0;
-    if (__syncthreads_or(ne)) {
-      int incl = ne;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        int x = __shfl_up_sync(FULL, incl, o);
-        if (lane >= o) incl += x;
-      }
-      if (lane == 31) s_wexp[wid] = incl;
-      __syncthreads();
-      if (wid == 0) {
-        int v = s_wexp[lane];
-        int inc = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          int x = __shfl_up_sync(FULL, inc, o);
-          if (lane >= o) inc += x;
-        }
-        s_wexp[lane] = inc - v;  // exclusive
-        if (lane == 31) wsum[0] = (u32)inc;
-      }
-      __syncthreads();
-      int pos = s_wexp[wid] + incl - ne;
-#pragma unroll
-      for (int j = 0; j < SCAN_RPT; ++j) {
-        if (exp_mask & (1u << j)) {
-          const i64 r = base + j;
-          b.exp_seg_row[tstart + pos] = (u32)r;
-          b.exp_seg_blk[tstart + pos] = exp_pb[j];
-          b.exp_seg_rank[tstart + pos] = t.rank[r];
-          pos++;
-        }
-      }
-      tile_exp = (int)wsum[0];
-      __syncthreads();
+    // every thread is done with this round's buffer: refill it
+    __syncthreads();
+    if (threadIdx.x == 0 && rd + SCAN_NBUF < nrounds) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(rd + SCAN_NBUF);
     }
-    if (threadIdx.x == 0) b.tile_cnt[tile] = tile_exp;
+    // tighten the histogram bounds to the CTA's running top-k bins
+    if ((rd == 0 || rd == 2) && rd + 1 < nrounds) {
+      int tw, tv;
+      u32 up, upv;
+      block_threshold_pair(hw, (u32)c.window, hv, (u32)VSEL, wsum, &tw, &up, &tv, &upv);
+      if (threadIdx.x == 0) {
+        s_bw = (u32)tw;
+        s_bv = (u32)tv;
+      }
+    }
+    __syncthreads();
   }
-  __syncthreads();
 
   // local thresholds: only bins at or below them can hold a global top-k key
-  int tw, tv;
-  u32 up;
-  block_threshold_fast(hw, (u32)c.window, wsum, &tw, &up);
-  block_threshold_fast(hv, (u32)VSEL, wsum, &tv, &up);
-  for (int i = threadIdx.x; i <= tw; i += blockDim.x)
-    if (hw[i]) atomicAdd(&w->hist_win[i], hw[i]);
-  for (int i = threadIdx.x; i <= tv; i += blockDim.x)
-    if (hv[i]) atomicAdd(&w->hist_vic[i], hv[i]);
-  if (threadIdx.x == 0) {
-    atomicMin(&w->tmin_win, (u32)tw);
-    atomicMin(&w->tmin_vic, (u32)tv);
+  {
+    int tw, tv;
+    u32 up;
+    u32 upv;
+    block_threshold_pair(hw, (u32)c.window, hv, (u32)VSEL, wsum, &tw, &up, &tv, &upv);
+    for (int i = threadIdx.x; i <= tw; i += blockDim.x)
+      if (hw[i]) atomicAdd(&w->hist_win[i], hw[i]);
+    for (int i = threadIdx.x; i <= tv; i += blockDim.x)
+      if (hv[i]) atomicAdd(&w->hist_vic[i], hv[i]);
+    if (threadIdx.x == 0) {
+      atomicMin(&w->tmin_win, (u32)tw);
+      atomicMin(&w->tmin_vic, (u32)tv);
+    }
   }
 
   // counters: warp shuffles, then one shared and one global atomic per warp/CTA
-  __shared__ int s_cnt[9];
-  __shared__ unsigned long long s_eb;
-  if (threadIdx.x < 9) s_cnt[threadIdx.x] = (threadIdx.x == 8) ? 0x7fffffff : 0;
-  if (threadIdx.x == 0) s_eb = 0;
-  __syncthreads();
   {
+    __shared__ int s_cnt[10];
+    __shared__ unsigned long long s_eb;
+    if (threadIdx.x < 10) s_cnt[threadIdx.x] = (threadIdx.x == 8) ? 0x7fffffff : 0;
+    if (threadIdx.x == 0) s_eb = 0;
+    __syncthreads();
     unsigned long long eb = warp_sum<unsigned long long>((unsigned long long)exp_blocks);
-    int v[7] = {n_active, n_queued, n_long, n_ready, n_prom, n_vic, n_bnd};
+    u32 v[8] = {(u32)n_active, (u32)n_queued, (u32)n_long, (u32)n_ready,
+                (u32)n_prom,   (u32)n_vic,    (u32)n_bnd,  (u32)n_exp};
 #pragma unroll
-    for (int q = 0; q < 7; ++q) v[q] = warp_sum<int>(v[q]);
-    int mx = warp_max<int>(max_req), mn = warp_min<int>(min_req);
+    for (int q = 0; q < 8; ++q) v[q] = __reduce_add_sync(FULL, v[q]);
+    int mx = __reduce_max_sync(FULL, max_req), mn = __reduce_min_sync(FULL, min_req);
     if (lane == 0) {
       if (eb) atomicAdd(&s_eb, eb);
 #pragma unroll
       for (int q = 0; q < 7; ++q)
-        if (v[q]) atomicAdd(&s_cnt[q], v[q]);
+        if (v[q]) atomicAdd(&s_cnt[q], (int)v[q]);
+      if (v[7]) atomicAdd(&s_cnt[9], (int)v[7]);
       atomicMax(&s_cnt[7], mx);
       atomicMin(&s_cnt[8], mn);
     }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    atomicAdd(&w->exp_blocks, s_eb);
-    atomicAdd(&w->n_active, s_cnt[0]);
-    atomicAdd(&w->n_queued, s_cnt[1]);
-    atomicAdd(&w->n_long_q, s_cnt[2]);
-    atomicAdd(&w->n_ready, s_cnt[3]);
-    atomicAdd(&w->n_promoted, s_cnt[4]);
-    atomicAdd(&w->n_victims, s_cnt[5]);
-    atomicAdd(&w->n_boundary, s_cnt[6]);
-    atomicMax(&w->max_req, s_cnt[7]);
-    atomicMin(&w->min_req, s_cnt[8]);
-    __threadfence();
-    u32 tk = atomicAdd(&w->ticket, 1u);
-    s_last = (tk == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-
-  // ---- last CTA: finalise ------------------------------------------------
-  volatile Work* vw = w;
-  {
-    // exclusive prefix of the per-tile expired segments (tile order == row order)
-    volatile i32* tc = b.tile_cnt;
-    int run = 0;
-    for (i64 t0 = 0; t0 < ntiles; t0 += SCAN_TPB) {
-      i64 q = t0 + threadIdx.x;
-      int cnt = q < ntiles ? tc[q] : 0;
-      int incl = cnt;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        int x = __shfl_up_sync(FULL, incl, o);
-        if (lane >= o) incl += x;
-      }
-      if (lane == 31) wsum[wid] = (u32)incl;
-      __syncthreads();
-      if (wid == 0) {
-        int v = (int)wsum[lane];
-        int inc = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          int x = __shfl_up_sync(FULL, inc, o);
-          if (lane >= o) inc += x;
-        }
-        wsum[lane] = (u32)inc;
-      }
-      __syncthreads();
-      int excl = run + (wid ? (int)wsum[wid - 1] : 0) + incl - cnt;
-      if (q < ntiles) b.tile_off[q] = excl;
-      run += (int)wsum[31];
-      __syncthreads();
-    }
+    __syncthreads();
     if (threadIdx.x == 0) {
-      w->n_exp = run;
-      w->scan_ctas = (i32)ntiles;
-      w->scan_chunk = SCAN_TILE;
+      b.tile_cnt[me] = s_cnt[9];
+      atomicAdd(&w->exp_blocks, s_eb);
+      atomicAdd(&w->n_active, s_cnt[0]);
+      atomicAdd(&w->n_queued, s_cnt[1]);
+      atomicAdd(&w->n_long_q, s_cnt[2]);
+      atomicAdd(&w->n_ready, s_cnt[3]);
+      atomicAdd(&w->n_promoted, s_cnt[4]);
+      atomicAdd(&w->n_victims, s_cnt[5]);
+      atomicAdd(&w->n_boundary, s_cnt[6]);
+      atomicMax(&w->max_req, s_cnt[7]);
+      atomicMin(&w->min_req, s_cnt[8]);
     }
   }
+
+  PTIME(1);
+  grid.sync();
+  PTIME(2);
+
+  // ---- phase 2 ---------------------------------------------------------------
   // global thresholds over the exact prefix of the merged histograms
-  // (L2 loads, all in flight at once: other CTAs' atomics are complete)
   const u32 tmw = __ldcg(&w->tmin_win), tmv = __ldcg(&w->tmin_vic);
 #pragma unroll
   for (int q = 0; q < HIST_BINS / SCAN_TPB; ++q) {
@@ -525,197 +634,247 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
   __syncthreads();
   int gw, gv;
   u32 wu, vu;
-  block_threshold_fast(hw, (u32)c.window, wsum, &gw, &wu);
-  block_threshold_fast(hv, (u32)VSEL, wsum, &gv, &vu);
-  if (threadIdx.x == 0) {
-    // scalar epilogue on register copies: one burst of independent loads in,
-    // plain stores out (no dependent global round trips)
-    mars_scalars s;
-    {
-      const unsigned long long* src = (const unsigned long long*)sc;
-      unsigned long long* dst = (unsigned long long*)&s;
-#pragma unroll
-      for (int q = 0; q < (int)(sizeof(mars_scalars) / 8); ++q) dst[q] = __ldcg(src + q);
-    }
-    const unsigned long long exp_blocks = __ldcg(&w->exp_blocks);
-    const int n_active_all = __ldcg(&w->n_active), n_queued_all = __ldcg(&w->n_queued);
-    const int n_long_all = __ldcg(&w->n_long_q), mx_all = __ldcg(&w->max_req);
-    const int mn_all = __ldcg(&w->min_req);
-    const mars_step_in in = w->in;
-    if (gw > (int)tmw) gw = (int)tmw;
-    if (gv > (int)tmv) gv = (int)tmv;
-    w->t_win = gw;
-    w->t_vic = gv;
-    w->n_win_cand_expected = (i32)wu;
-    w->n_vic_cand_expected = (i32)vu;
-    const int mode = in.mode;
-    const i64 total = s.total_blocks;
-    const i64 freeb = s.free_blocks + (i64)exp_blocks;
-    s.free_blocks = freeb;
-    w->free_after_expiry = freeb;
-    if (!(mode & MARS_MODE_SKIP_PROBE)) {
-      // Telemetry.probe (telemetry.py:152-158) after the expiry evictions
-      s.available_kv = freeb;
-      s.kv_usage_ratio = (double)(total - freeb) / (double)total;
-      s.active_sessions = n_active_all;
-      s.active_tools = in.active_tools;
-      s.queued_tools = in.queued_tools;
-    }
-    const i64 qlen = s.queue_len;
-    w->qlen = qlen;
-    if (!(mode & MARS_MODE_NO_ROWS) && (i64)n_queued_all != qlen) w->status |= ST_QUEUE_MISMATCH;
-    // what the control plane sees: this replica's probe (pooled in sharded mode,
-    // see k_global_control)
-    w->adm_avail = s.available_kv;
-    w->adm_total = total;
-    w->adm_usage = s.kv_usage_ratio;
-    w->adm_active = s.active_sessions;
-    if (mode & MARS_MODE_SHARDED) {
-      xc[0] = s.available_kv;
-      xc[1] = total;
-      xc[2] = s.active_sessions;
-      xc[3] = s.queue_len;
-    } else if (in.control_due && !(mode & MARS_MODE_SKIP_REFRESH)) {
-      refresh_pressure(c, &s, in.worker_slots, s.kv_usage_ratio);
-    }
-    {
-      const unsigned long long* src = (const unsigned long long*)&s;
-      unsigned long long* dst = (unsigned long long*)sc;
-#pragma unroll
-      for (int q = 0; q < (int)(sizeof(mars_scalars) / 8); ++q) dst[q] = src[q];
-    }
-    int ne = vw->n_exp;
-    w->xlsd_big = ne > SORT_CAP ? 1 : 0;
-    w->xlsd_n = ne;
-    w->xlsd_maxkey = 0xffffffffull;
-    // table-backed queue statistics for pack_queue (control.py:109-122)
-    w->tab_long_q = n_long_all;
-    w->tab_max_req = mx_all;
-    w->tab_min_req = mn_all;
-  }
-}
+  block_threshold_pair(hw, (u32)c.window, hv, (u32)VSEL, wsum, &gw, &wu, &gv, &vu);
+  if (gw > (int)tmw) gw = (int)tmw;
+  if (gv > (int)tmv) gv = (int)tmv;
 
-// ---------------------------------------------------------------------------
-// K_C: candidates at the exact thresholds + S2 retention (boundary rows)
-// ---------------------------------------------------------------------------
+  // the probe's view after the expiry evictions (telemetry.py:152-158): the
+  // usage S2 prices retention with
+  const unsigned long long exp_total = __ldcg(&w->exp_blocks);
+  const i64 freeb = sc_free + (i64)exp_total;
+  const double usage =
+      (mode & MARS_MODE_SKIP_PROBE) ? sc_usage : (double)(sc_total - freeb) / (double)sc_total;
 
-__global__ void __launch_bounds__(SCAN_TPB, 2) k_compact(Tab t, Cfg c, Work* w, Bufs b,
-                                                      mars_scalars* sc, i64 n_rows) {
-  const double now = w->in.now;
-  const double scale = (now > 0.0 && now < 1e300) ? 1024.0 / now : 0.0;
-  const u32 tw = (u32)w->t_win, tv = (u32)w->t_vic;
-  const i64 total = sc->total_blocks;
-  const double usage = sc->kv_usage_ratio;
-  const double ema = sc->has_ema_tool ? sc->ema_tool : c.tool_prior;
-  const i64 stride = (i64)gridDim.x * blockDim.x;
-  const i64 lim = ((n_rows + 31) / 32) * 32;
-  // expired pins: k_scan's per-CTA segments are in row order and CTA order is
-  // row order, so their concatenation is row order -- already the rank order
-  // expired_pins() sorts by when the table is rank-ordered (baselines.py:396-399)
+  // this CTA's expired pins go after those of the CTAs before it: CTA order
+  // is row order, so the list is row-ordered -- already the rank order
+  // expired_pins() sorts by when the table is rank-ordered
+  // (baselines.py:396-399)
+  int n_exp_all, exp_off;
   {
-    const int nseg = w->scan_ctas;
-    const i64 chunk = w->scan_chunk;
-    const bool ro = (w->in.mode & MARS_MODE_RANK_ORDERED) != 0;
-    for (int sg = blockIdx.x; sg < nseg; sg += gridDim.x) {
-      const int cnt = b.tile_cnt[sg], off = b.tile_off[sg];
-      const i64 src = (i64)sg * chunk;
-      for (int k = threadIdx.x; k < cnt; k += blockDim.x) {
-        u32 r = b.exp_seg_row[src + k];
-        i32 bk = b.exp_seg_blk[src + k];
-        if (ro) {
-          b.exp_row_sorted[off + k] = r;
-          b.exp_blk_sorted[off + k] = bk;
-        } else {
-          b.exp_row[off + k] = r;
-          b.exp_blk[off + k] = bk;
-          b.exp_rank[off + k] = b.exp_seg_rank[src + k];
-        }
-      }
+    __shared__ int s_b[32], s_a[32];
+    const int G = gridDim.x;  // <= SCAN_TPB (host-checked)
+    const int cg_ = (int)threadIdx.x < G ? __ldcg(&b.tile_cnt[threadIdx.x]) : 0;
+    const int bs = __reduce_add_sync(FULL, (int)threadIdx.x < me ? cg_ : 0);
+    const int as = __reduce_add_sync(FULL, cg_);
+    if (lane == 0) {
+      s_b[wid] = bs;
+      s_a[wid] = as;
     }
-  }
-  (void)lim;
-  // groups of SCAN_RPT consecutive rows per thread, vector loads as in k_scan;
-  // ranks are read only for the (few) candidates
-  const i64 ngroups = (n_rows + SCAN_RPT - 1) / SCAN_RPT;
-  const i64 glim = ((ngroups + 31) / 32) * 32;
-  for (i64 gi = (i64)blockIdx.x * blockDim.x + threadIdx.x; gi < glim; gi += stride) {
-  const i64 base = gi * SCAN_RPT;
-  u32 f4 = 0, ph4 = 0x07070707u, lv4 = 0;
-  int4 kv4 = make_int4(0, 0, 0, 0);
-  double2 ta = make_double2(0, 0), tb = ta;
-  if (base < n_rows) {
-    f4 = *(const u32*)(t.flags + base);
-    ph4 = *(const u32*)(t.phase + base);
-    lv4 = *(const u32*)(t.level + base);
-    kv4 = *(const int4*)(t.kv + base);
-    const double* tcol = c.coord ? t.rs : t.arr;
-    ta = *(const double2*)(tcol + base);
-    tb = *(const double2*)(tcol + base + 2);
-  }
-  const i32 kva[4] = {kv4.x, kv4.y, kv4.z, kv4.w};
-  const double tv4[4] = {ta.x, ta.y, tb.x, tb.y};
+    __syncthreads();
+    exp_off = 0;
+    n_exp_all = 0;
 #pragma unroll
-  for (int j = 0; j < SCAN_RPT; ++j) {
-    const i64 r = base + j;
-    const bool valid = r < n_rows;
-    u8 f = valid ? (u8)(f4 >> (8 * j)) : 0;
-    u8 ph = valid ? (u8)(ph4 >> (8 * j)) : MARS_EMPTY;
-    bool ready = (f & MARS_F_ACTIVE) && (ph == MARS_PREFILL || ph == MARS_DECODE);
-    bool wcand = false, vcand = false, bnd = (f & MARS_F_BOUNDARY) != 0;
-    u64 whi = 0, wlo = 0, vk = 0;
-    i32 blk = 0;
-    if (ready) {
-      u32 lv = c.coord ? ((lv4 >> (8 * j)) & 255u) : 0u;
-      double tt = tv4[j];
-      wcand = window_digit(lv, tt, scale) <= tw;
-      i32 kvv = kva[j];
-      i64 h = kvv > 0 ? held_blocks(c, kvv) : 0;
-      vcand = kvv > 0 && victim_digit(true, false, lv, h) <= tv;
-      if (wcand || vcand) {
-        u32 rk = t.rank[r];
-        window_key(lv, tt, rk, whi, wlo);
-        if (vcand) {
-          vk = victim_key(true, false, lv, h, rk);
-          blk = (i32)h;
+    for (int q = 0; q < SCAN_TPB / 32; ++q) {
+      exp_off += s_b[q];
+      n_exp_all += s_a[q];
+    }
+  }
+  PTIME(3);
+
+  // candidates at the exact thresholds, S2 retention of boundary rows and the
+  // expired pins, from the digit record.  Each thread owns a contiguous run of
+  // rows (thread order == row order, as the expired list needs):
+  // (A) per-thread counts, one block scan, one global atomic per unordered
+  // list; (B) row ids straight into the output lists; (C) one thread per
+  // emitted entry reads its row's columns -- all the entries' loads in flight.
+  {
+    __shared__ unsigned long long s_scan[32];
+    __shared__ u32 s_escan[32];
+    __shared__ int s_base[3], s_tot[4];
+    const i64 len = ce - cs;
+    const i64 per = (len + SCAN_TPB - 1) / SCAN_TPB;
+    const i64 r0 = (i64)threadIdx.x * per;
+    const i64 r1 = (r0 + per < len) ? r0 + per : len;
+    constexpr int FB = 21;  // count field width (chunk < 2^21 rows)
+    constexpr unsigned long long FM = (1ull << FB) - 1;
+    unsigned long long cnt = 0;
+    u32 ecnt = 0;
+    for (i64 i = r0; i < r1; ++i) {
+      const u32 rc = dig[i];
+      const u32 rw = rc & 0xffffu, rv = rc >> 16;
+      cnt += ((rw & ~DIG_BND) <= (u32)gw ? 1ull : 0ull) + ((rv <= (u32)gv ? 1ull : 0ull) << FB) +
+             ((rw & DIG_BND) ? (1ull << (2 * FB)) : 0ull);
+      ecnt += rv == DIG_EXP ? 1u : 0u;
+    }
+    unsigned long long incl = cnt;
+    u32 eincl = ecnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long x = __shfl_up_sync(FULL, incl, o);
+      const u32 y = __shfl_up_sync(FULL, eincl, o);
+      if (lane >= o) {
+        incl += x;
+        eincl += y;
+      }
+    }
+    if (lane == 31) {
+      s_scan[wid] = incl;
+      s_escan[wid] = eincl;
+    }
+    __syncthreads();
+    if (wid == 0) {
+      unsigned long long v = s_scan[lane];
+      u32 e = s_escan[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long x = __shfl_up_sync(FULL, v, o);
+        const u32 y = __shfl_up_sync(FULL, e, o);
+        if (lane >= o) {
+          v += x;
+          e += y;
         }
       }
-    } else if (f & MARS_F_PINNED) {
-      bool nonexp = !(t.dl[r] < now);
-      u32 plv = (u32)t.plevel[r];
-      i32 pbk = t.pb[r];
-      if (victim_digit(false, nonexp, plv, pbk) <= tv) {
-        vcand = true;
-        vk = victim_key(false, nonexp, plv, pbk, t.rank[r]);
-        blk = pbk;
+      s_scan[lane] = v;
+      s_escan[lane] = e;
+      if (lane == 31) {
+        const int nw = (int)(v & FM), nv = (int)((v >> FB) & FM), nb = (int)(v >> (2 * FB));
+        s_tot[0] = nw;
+        s_tot[1] = nv;
+        s_tot[2] = nb;
+        s_tot[3] = (int)e;
+        s_base[0] = nw ? atomicAdd(&w->n_wc, nw) : 0;
+        s_base[1] = nv ? atomicAdd(&w->n_vc, nv) : 0;
+        s_base[2] = nb ? atomicAdd(&w->n_ret, nb) : 0;
       }
     }
-    int s = warp_append(&w->n_wc, wcand);
-    if (s >= 0) {
-      b.wc_hi[s] = whi;
-      b.wc_lo[s] = wlo;
-      b.wc_row[s] = (u32)r;
+    __syncthreads();
+    const int nw = s_tot[0], nv = s_tot[1], nb = s_tot[2], ne = s_tot[3];
+    const int bw = s_base[0], bv = s_base[1], bb = s_base[2];
+    const bool ro = (mode & MARS_MODE_RANK_ORDERED) != 0;
+    u32* exp_rows = ro ? b.exp_row_sorted : b.exp_row;
+    if (cnt | ecnt) {
+      const unsigned long long ex = incl - cnt + (wid ? s_scan[wid - 1] : 0ull);
+      int pw = bw + (int)(ex & FM), pv = bv + (int)((ex >> FB) & FM), pr = bb + (int)(ex >> (2 * FB));
+      int pe = exp_off + (int)(eincl - ecnt + (wid ? s_escan[wid - 1] : 0u));
+      for (i64 i = r0; i < r1; ++i) {
+        const u32 rc = dig[i];
+        const u32 rw = rc & 0xffffu, rv = rc >> 16;
+        const u32 r = (u32)(cs + i);
+        if ((rw & ~DIG_BND) <= (u32)gw) b.wc_row[pw++] = r;
+        if (rv <= (u32)gv) b.vc_row[pv++] = r;
+        if (rw & DIG_BND) b.ret_row[pr++] = r;
+        if (rv == DIG_EXP) exp_rows[pe++] = r;
+      }
     }
-    s = warp_append(&w->n_vc, vcand);
-    if (s >= 0) {
-      b.vc_key[s] = vk;
-      b.vc_whi[s] = whi;
-      b.vc_wlo[s] = wlo;
-      b.vc_row[s] = (u32)r;
-      b.vc_blk[s] = blk;
-    }
-    s = warp_append(&w->n_ret, bnd);
-    if (s >= 0) {
-      u8 pin;
-      double bb, cc, dd;
-      decide_retention(c, t.ctx[r], t.kv[r], total, usage, ema, now, pin, bb, cc, dd);
-      b.ret_row[s] = (u32)r;
-      b.ret_pin[s] = pin;
-      b.ret_b[s] = bb;
-      b.ret_c[s] = cc;
-      b.ret_d[s] = dd;
+    __syncthreads();
+    for (int k = threadIdx.x; k < nw + nv + nb + ne; k += blockDim.x) {
+      if (k < nw + nv) {
+        const bool is_w = k < nw;
+        const int slot = is_w ? bw + k : bv + (k - nw);
+        const u32 r = is_w ? __ldcg(&b.wc_row[slot]) : __ldcg(&b.vc_row[slot]);
+        const bool ready = (dig[(i64)r - cs] & DIG_NONE) == 0;
+        const u32 rk = t.rank[r];
+        u64 whi = 0, wlo = 0;
+        if (ready) {  // post-aging level
+          const u32 lv = c.coord ? (u32)t.level[r] : 0u;
+          const double tt = c.coord ? t.rs[r] : t.arr[r];
+          window_key(lv, tt, rk, whi, wlo);
+        }
+        if (is_w) {
+          b.wc_hi[slot] = whi;
+          b.wc_lo[slot] = wlo;
+        } else {
+          u64 vk;
+          i32 blk;
+          if (ready) {
+            const i64 h = held_blocks(c, t.kv[r]);
+            vk = victim_key(true, false, c.coord ? (u32)t.level[r] : 0u, h, rk);
+            blk = (i32)h;
+          } else {  // pinned row
+            const bool nonexp = !(t.dl[r] < now);
+            const i32 pbk = t.pb[r];
+            vk = victim_key(false, nonexp, (u32)t.plevel[r], pbk, rk);
+            blk = pbk;
+          }
+          b.vc_key[slot] = vk;
+          b.vc_whi[slot] = whi;
+          b.vc_wlo[slot] = wlo;
+          b.vc_blk[slot] = blk;
+        }
+      } else if (k < nw + nv + nb) {
+        const int slot = bb + (k - nw - nv);
+        const u32 r = __ldcg(&b.ret_row[slot]);
+        u8 pin;
+        double rb_, rc_, rd_;
+        decide_retention(c, t.ctx[r], t.kv[r], sc_total, usage, ema, now, pin, rb_, rc_, rd_);
+        b.ret_pin[slot] = pin;
+        b.ret_b[slot] = rb_;
+        b.ret_c[slot] = rc_;
+        b.ret_d[slot] = rd_;
+      } else {  // expired pin: its blocks (and rank, for the rank sort)
+        const int slot = exp_off + (k - nw - nv - nb);
+        const u32 r = __ldcg(&exp_rows[slot]);
+        if (ro) {
+          b.exp_blk_sorted[slot] = t.pb[r];
+        } else {
+          b.exp_blk[slot] = t.pb[r];
+          b.exp_rank[slot] = t.rank[r];
+        }
+      }
     }
   }
+
+  PTIME(4);
+  if (me != 0 || threadIdx.x != 0) return;
+  // ---- CTA 0: scalar epilogue on register copies: one burst of independent
+  // loads in, plain stores out (no dependent global round trips)
+  mars_scalars s;
+  {
+    const unsigned long long* src = (const unsigned long long*)sc;
+    unsigned long long* dst = (unsigned long long*)&s;
+#pragma unroll
+    for (int q = 0; q < (int)(sizeof(mars_scalars) / 8); ++q) dst[q] = __ldcg(src + q);
   }
+  const int n_active_all = __ldcg(&w->n_active), n_queued_all = __ldcg(&w->n_queued);
+  const int n_long_all = __ldcg(&w->n_long_q), mx_all = __ldcg(&w->max_req);
+  const int mn_all = __ldcg(&w->min_req);
+  const mars_step_in in = w->in;
+  w->t_win = gw;
+  w->t_vic = gv;
+  w->n_win_cand_expected = (i32)wu;
+  w->n_vic_cand_expected = (i32)vu;
+  w->n_exp = n_exp_all;
+  const i64 total = s.total_blocks;
+  s.free_blocks = freeb;
+  w->free_after_expiry = freeb;
+  if (!(mode & MARS_MODE_SKIP_PROBE)) {
+    // Telemetry.probe (telemetry.py:152-158) after the expiry evictions
+    s.available_kv = freeb;
+    s.kv_usage_ratio = usage;
+    s.active_sessions = n_active_all;
+    s.active_tools = in.active_tools;
+    s.queued_tools = in.queued_tools;
+  }
+  const i64 qlen = s.queue_len;
+  w->qlen = qlen;
+  if (!(mode & MARS_MODE_NO_ROWS) && (i64)n_queued_all != qlen) w->status |= ST_QUEUE_MISMATCH;
+  // what the control plane sees: this replica's probe (pooled in sharded mode,
+  // see k_global_control)
+  w->adm_avail = s.available_kv;
+  w->adm_total = total;
+  w->adm_usage = s.kv_usage_ratio;
+  w->adm_active = s.active_sessions;
+  if (mode & MARS_MODE_SHARDED) {
+    xc[0] = s.available_kv;
+    xc[1] = total;
+    xc[2] = s.active_sessions;
+    xc[3] = s.queue_len;
+  } else if (in.control_due && !(mode & MARS_MODE_SKIP_REFRESH)) {
+    refresh_pressure(c, &s, in.worker_slots, s.kv_usage_ratio);
+  }
+  {
+    const unsigned long long* src = (const unsigned long long*)&s;
+    unsigned long long* dst = (unsigned long long*)sc;
+#pragma unroll
+    for (int q = 0; q < (int)(sizeof(mars_scalars) / 8); ++q) dst[q] = src[q];
+  }
+  w->xlsd_big = n_exp_all > SORT_CAP ? 1 : 0;
+  w->xlsd_n = n_exp_all;
+  w->xlsd_maxkey = 0xffffffffull;
+  // table-backed queue statistics for pack_queue (control.py:109-122)
+  w->tab_long_q = n_long_all;
+  w->tab_max_req = mx_all;
+  w->tab_min_req = mn_all;
 }
 
 // ---------------------------------------------------------------------------
@@ -779,137 +938,142 @@ __device__ __forceinline__ LsdView lsd_view(Work* w, int which) {
   return v;
 }
 
-// key of element i: the queue's first pass reads req[] from the admission list
-// (pack_queue key: req ascending, or max_req - req for the descending pack)
-__device__ __forceinline__ u64 lsd_key(const Lsd& L, const Work* w, int which, int pass, int buf,
-                                       int i) {
-  if (which == 0 && pass == 0) {
-    i32 rq = ((const i32*)(uintptr_t)w->lsd_raw_ptr)[i];
-    return (u64)(w->pack_mode == PACK_ASC ? rq : (w->max_req - rq));
-  }
-  return L.k[buf][i];
-}
-
-__global__ void __launch_bounds__(256) k_lsd_hist(Lsd L, Work* w, int which, int pass) {
+// One cooperative launch sorts the whole list: per 8-bit pass, chunk
+// histograms -> grid barrier -> every CTA derives its own digit offsets from
+// all chunk counts (no separate scan launch) -> stable in-order scatter ->
+// grid barrier.  Grid <= #SMs, one 1024-thread CTA per SM (co-resident).
+__global__ void __launch_bounds__(1024, 1) k_lsd_coop(Lsd L, Work* w, int which, int npass) {
   LsdView v = lsd_view(w, which);
-  if (!*v.big) return;
-  int shift = 8 * pass;
-  if (pass > 0 && ((*v.maxkey) >> shift) == 0) return;
-  int n = *v.n;
+  if (!*v.big) return;  // grid-uniform
+  PTIME(5);
+  cg::grid_group grid = cg::this_grid();
+  const int n = *v.n;
+  const u64 maxkey = *v.maxkey;
+  const int G = gridDim.x, me = blockIdx.x;
+  const int chunk = (n + G - 1) / G;
+  const int s = me * chunk, e = min(n, s + chunk);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int d = tid & 255, p = tid >> 8;
+  __shared__ u32 h[256], off[256], tt[256];
+  __shared__ u32 part[4][256], below[4][256];
+  __shared__ u32 wc[32][256];
+  const i32* raw = (which == 0) ? (const i32*)(uintptr_t)w->lsd_raw_ptr : nullptr;
+  const bool asc = w->pack_mode == PACK_ASC;
+  const i32 mr = w->max_req;
   int cur = *v.cur;
-  __shared__ u32 h[256];
-  h[threadIdx.x] = 0;
-  __syncthreads();
-  int chunk = (n + gridDim.x - 1) / gridDim.x;
-  int s = blockIdx.x * chunk, e = min(n, s + chunk);
-  for (int i = s + threadIdx.x; i < e; i += blockDim.x)
-    atomicAdd(&h[(lsd_key(L, w, which, pass, cur, i) >> shift) & 255u], 1u);
-  __syncthreads();
-  L.cnt[blockIdx.x * 256 + threadIdx.x] = h[threadIdx.x];
+  for (int pass = 0; pass < npass; ++pass) {
+    const int shift = 8 * pass;
+    if (pass > 0 && (maxkey >> shift) == 0) {
+      if (me == 0 && tid == 0) v.skip[pass] = 1;
+      continue;
+    }
+    // the queue's first pass reads req[] straight from the admission list
+    const bool rawp = raw != nullptr && pass == 0;
+    const u64* kin = L.k[cur];
+    const u32* vin = L.v[cur];
+    u64* kout = L.k[1 - cur];
+    u32* vout = L.v[1 - cur];
+    if (tid < 256) h[tid] = 0;
+    __syncthreads();
+    for (int i = s + tid; i < e; i += 1024) {
+      u64 k = rawp ? (u64)(asc ? raw[i] : mr - raw[i]) : kin[i];
+      atomicAdd(&h[(k >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    if (tid < 256) L.cnt[me * 256 + tid] = h[tid];
+    if (pass == 0) PTIME(6);
+    grid.sync();
+    if (pass == 0) PTIME(7);
+    // digit d's total over all chunks and over the chunks before mine
+    const int c0 = (G * p) / 4, c1 = (G * (p + 1)) / 4;
+    u32 tot = 0, bel = 0;
+    for (int c = c0; c < c1; c += 16) {  // 16 independent L2 loads in flight
+      u32 x[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) x[q] = c + q < c1 ? __ldcg(&L.cnt[(c + q) * 256 + d]) : 0u;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        tot += x[q];
+        bel += c + q < me ? x[q] : 0u;
+      }
+    }
+    part[p][d] = tot;
+    below[p][d] = bel;
+    __syncthreads();
+    if (tid < 32) {  // exclusive scan of the 256 digit totals, 8 per lane
+      u32 x[8], sum = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        int dd = tid * 8 + q;
+        x[q] = part[0][dd] + part[1][dd] + part[2][dd] + part[3][dd];
+        sum += x[q];
+      }
+      u32 incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        u32 y = __shfl_up_sync(FULL, incl, o);
+        if (tid >= o) incl += y;
+      }
+      u32 run = incl - sum;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        int dd = tid * 8 + q;
+        off[dd] = run + below[0][dd] + below[1][dd] + below[2][dd] + below[3][dd];
+        run += x[q];
+      }
+    }
+    for (int q = p; q < 32; q += 4) wc[q][d] = 0;
+    __syncthreads();
+    if (pass == 0) PTIME(8);
+    for (int base = s; base < e; base += 1024) {
+      int i = base + tid;
+      bool valid = i < e;
+      u64 k = 0;
+      u32 val = 0;
+      if (valid) {
+        k = rawp ? (u64)(asc ? raw[i] : mr - raw[i]) : kin[i];
+        val = rawp ? (u32)i : vin[i];
+      }
+      u32 dig = valid ? (u32)((k >> shift) & 255u) : (256u + (u32)lane);
+      u32 peers = __match_any_sync(FULL, dig);
+      u32 rk = __popc(peers & ((1u << lane) - 1u));
+      if (valid && rk == 0) wc[wid][dig] = __popc(peers);
+      __syncthreads();
+      if (tid < 256) {
+        u32 acc = 0;
+        for (int q = 0; q < 32; ++q) {
+          u32 x = wc[q][tid];
+          wc[q][tid] = acc;
+          acc += x;
+        }
+        tt[tid] = acc;
+      }
+      __syncthreads();
+      if (valid) {
+        u32 pos = off[dig] + wc[wid][dig] + rk;
+        kout[pos] = k;
+        vout[pos] = val;
+      }
+      __syncthreads();
+      if (tid < 256) off[tid] += tt[tid];
+      for (int q = p; q < 32; q += 4) wc[q][d] = 0;
+      __syncthreads();
+    }
+    if (me == 0 && tid == 0) {
+      v.skip[pass] = 0;
+      v.in[pass] = cur;
+    }
+    cur = 1 - cur;
+    if (pass == 0) PTIME(9);
+    grid.sync();  // the next pass reads this pass' output and rewrites L.cnt
+  }
+  PTIME(10);
+  if (me == 0 && tid == 0) *v.cur = cur;
 }
 
-__global__ void __launch_bounds__(1024) k_lsd_scan(Lsd L, Work* w, int which, int pass, int G) {
-  LsdView v = lsd_view(w, which);
-  if (!*v.big) return;
-  int shift = 8 * pass;
-  if (pass > 0 && ((*v.maxkey) >> shift) == 0) {
-    if (threadIdx.x == 0) v.skip[pass] = 1;
-    return;
-  }
-  // 1024 threads: digit d = tid % 256 over CTA quarter p = tid / 256
-  __shared__ u32 part[4][256];
-  __shared__ u32 base[256];
-  const int d = threadIdx.x & 255, p = threadIdx.x >> 8;
-  const int c0 = (G * p) / 4, c1 = (G * (p + 1)) / 4;
-  u32 tot = 0;
-#pragma unroll 8
-  for (int cta = c0; cta < c1; ++cta) tot += L.cnt[cta * 256 + d];
-  part[p][d] = tot;
-  __syncthreads();
-  if (threadIdx.x < 256) {
-    u32 all = part[0][d] + part[1][d] + part[2][d] + part[3][d];
-    base[d] = all;
-  }
-  __syncthreads();
-  if (threadIdx.x < 32) {  // exclusive scan of the 256 digit totals, 8 per lane
-    u32 v[8], s = 0;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      v[q] = base[threadIdx.x * 8 + q];
-      s += v[q];
-    }
-    u32 incl = s;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      u32 x = __shfl_up_sync(FULL, incl, o);
-      if ((int)threadIdx.x >= o) incl += x;
-    }
-    u32 run = incl - s;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      base[threadIdx.x * 8 + q] = run;
-      run += v[q];
-    }
-  }
-  __syncthreads();
-  u32 run = base[d];
-  for (int q = 0; q < p; ++q) run += part[q][d];
-  for (int cta = c0; cta < c1; ++cta) {
-    u32 x = L.cnt[cta * 256 + d];
-    L.cnt[cta * 256 + d] = run;
-    run += x;
-  }
-  if (threadIdx.x == 0) {
-    v.skip[pass] = 0;
-    v.in[pass] = *v.cur;
-    *v.cur = 1 - *v.cur;
-  }
-}
-
-__global__ void __launch_bounds__(256) k_lsd_scatter(Lsd L, Work* w, int which, int pass) {
-  LsdView v = lsd_view(w, which);
-  if (!*v.big || v.skip[pass]) return;
-  int shift = 8 * pass;
-  int n = *v.n;
-  int in = v.in[pass], out = 1 - in;
-  __shared__ u32 off[256];
-  __shared__ u32 wc[8][256];
-  __shared__ u32 tt[256];
-  int d = threadIdx.x;
-  off[d] = L.cnt[blockIdx.x * 256 + d];
-  for (int q = 0; q < 8; ++q) wc[q][d] = 0;
-  __syncthreads();
-  int chunk = (n + gridDim.x - 1) / gridDim.x;
-  int s = blockIdx.x * chunk, e = min(n, s + chunk);
-  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int base = s; base < e; base += 256) {
-    int i = base + threadIdx.x;
-    bool valid = i < e;
-    u64 key = valid ? lsd_key(L, w, which, pass, in, i) : 0;
-    u32 val = valid ? ((which == 0 && pass == 0) ? (u32)i : L.v[in][i]) : 0;
-    u32 dig = valid ? (u32)((key >> shift) & 255u) : (256u + (u32)lane);
-    u32 peers = __match_any_sync(FULL, dig);
-    u32 rk = __popc(peers & ((1u << lane) - 1u));
-    if (valid && rk == 0) wc[wid][dig] = __popc(peers);
-    __syncthreads();
-    u32 acc = 0;
-    for (int q = 0; q < 8; ++q) {
-      u32 x = wc[q][d];
-      wc[q][d] = acc;
-      acc += x;
-    }
-    tt[d] = acc;
-    __syncthreads();
-    if (valid) {
-      u32 pos = off[dig] + wc[wid][dig] + rk;
-      L.k[out][pos] = key;
-      L.v[out][pos] = val;
-    }
-    __syncthreads();
-    off[d] += tt[d];
-    for (int q = 0; q < 8; ++q) wc[q][d] = 0;
-    __syncthreads();
-  }
+static void launch_lsd(Lsd L, Work* w, int which, int npass, int grid, cudaStream_t s) {
+  void* args[] = {&L, &w, &which, &npass};
+  cudaLaunchCooperativeKernel((const void*)k_lsd_coop, dim3(grid), dim3(1024), args, 0, s);
 }
 
 // ---------------------------------------------------------------------------
@@ -999,6 +1163,7 @@ __global__ void __launch_bounds__(1024) k_pack_small(Work* w, Queue Q, Lsd L,
                                                      mars_scalars* sc, i32* qsel_p, Queue G) {
   extern __shared__ __align__(16) unsigned char smem[];
   if (!w->in.control_due) return;
+  PTIME(18);
   int qlen = (int)w->qlen;
   if (qlen <= 0) return;
   const bool sharded = (w->in.mode & MARS_MODE_SHARDED) != 0;
@@ -1128,6 +1293,7 @@ __global__ void __launch_bounds__(1024) k_pack_small(Work* w, Queue Q, Lsd L,
       w->lsd_raw_ptr = (u64)(uintptr_t)req;
       w->lsd_cur = 0;
     }
+    PTIME(19);
     return;
   }
   int n2 = next_pow2(qlen);
@@ -1158,6 +1324,7 @@ __global__ void __launch_bounds__(SCAN_TPB) k_admit_apply(Tab t, Cfg c, Work* w,
                                                           Lsd L, mars_scalars* sc, i32* qsel_p,
                                                           Queue G, Xchg x) {
   if (!w->in.control_due) return;
+  PTIME(12);
   __shared__ long long shl[32];
   __shared__ bool s_last;
   const double now = w->in.now;
@@ -1249,7 +1416,7 @@ __global__ void __launch_bounds__(SCAN_TPB) k_admit_apply(Tab t, Cfg c, Work* w,
         t.level[row] = (u8)lv;
         t.promos[row] = 0;
         t.served[row] = 0;
-        proj += ceil_div64(cn, c.bs) - ceil_div64(kvv, c.bs);
+        proj += blocks_ceil(c, cn) - blocks_ceil(c, kvv);
         if (!sharded) b.admitted[i] = in_order ? src_row[perm[i]] : row;
         u32 kl = c.coord ? lv : 0u;
         double tt = c.coord ? now : t.arr[row];
@@ -1270,6 +1437,7 @@ __global__ void __launch_bounds__(SCAN_TPB) k_admit_apply(Tab t, Cfg c, Work* w,
       x.adm_idx[s] = (u32)i;
     }
   }
+  PTIME(13);
   // residual queue in packed order (control.py:190); sharded: this replica's
   // entries only, each with its new dense global position
   const i64 nres = qlen - take;
@@ -1298,6 +1466,7 @@ __global__ void __launch_bounds__(SCAN_TPB) k_admit_apply(Tab t, Cfg c, Work* w,
       Q.gpos[1 - sel][s] = (u32)j;
     }
   }
+  PTIME(14);
   long long ps = block_sum<long long>(proj, shl);
   if (threadIdx.x == 0) {
     atomicAdd((unsigned long long*)&w->projected, (unsigned long long)ps);
@@ -1323,6 +1492,7 @@ __global__ void __launch_bounds__(SCAN_TPB) k_admit_apply(Tab t, Cfg c, Work* w,
     sc->queue_len = sharded ? (i64)vw->n_res_own : qlen - take;
     w->global_residual = nres;
     *qsel_p = 1 - sel;
+    PTIME(15);
   }
 }
 
@@ -1528,11 +1698,11 @@ __device__ int walk_claim(const Cfg& c, Tab& t, Bufs& b, WalkShared& S, VEnt* st
 // try_fit (scheduler.py:136-157) -- thread 0; allocates on success
 __device__ long long walk_try_fit(const Cfg& c, Bufs& b, WalkShared& S, int wi, long long desired) {
   long long kvv = S.wkv[wi];
-  long long held = ceil_div64(kvv, c.bs);
+  long long held = blocks_ceil(c, kvv);
   long long room = (held + S.freeb) * c.bs - kvv;
-  long long g = desired <= room ? desired : (room / c.bs) * c.bs;
+  long long g = desired <= room ? desired : blocks_floor_tokens(c, room);
   if (g < 1) return 0;
-  long long need = ceil_div64(kvv + g, c.bs) - held;
+  long long need = blocks_ceil(c, kvv + g) - held;
   if (need > 0) {
     S.freeb -= need;
     jpush(b, S, MARS_J_ALLOC, S.wrow[wi], (i32)need);
@@ -1561,7 +1731,7 @@ __device__ int walk_run(const Cfg& c, Tab& t, Bufs& b, WalkShared& S, VEnt* st, 
         S.idx++;
         continue;
       }
-      long long need = (S.wkv[i] % c.bs == 0) ? 1 : 0;
+      long long need = block_aligned(c, S.wkv[i]) ? 1 : 0;
       if (need > 0) {
         int r = walk_claim(c, t, b, S, st, fs_row, fs_pin, fs_blk, need, i);
         if (r == CL_NEED_SORT) return REQ_SORT;
@@ -1595,7 +1765,7 @@ __device__ int walk_run(const Cfg& c, Tab& t, Bufs& b, WalkShared& S, VEnt* st, 
       }
       long long g = 0;
       long long kvv = S.wkv[i];
-      long long incr = ceil_div64(kvv + desired, c.bs) - ceil_div64(kvv, c.bs);
+      long long incr = blocks_ceil(c, kvv + desired) - blocks_ceil(c, kvv);
       if (c.cosched) {
         if (S.sub == 0) {
           g = walk_try_fit(c, b, S, i, desired);
@@ -1655,7 +1825,7 @@ __device__ void walk_fullscan(const Cfg& c, Tab& t, WalkShared& S, i64 n_rows, d
       u64 hi, lo;
       window_key(c.coord ? t.level[r] : 0u, c.coord ? t.rs[r] : t.arr[r], t.rank[r], hi, lo);
       int wi = t.winpos[r];
-      if (run_eligible(c, S, (u32)r, hi, lo, wi, bi)) tot += ceil_div64(kvv, c.bs);
+      if (run_eligible(c, S, (u32)r, hi, lo, wi, bi)) tot += blocks_ceil(c, kvv);
     }
   }
   tot = block_sum<long long>(tot, shl);
@@ -1693,7 +1863,7 @@ __device__ void walk_fullscan(const Cfg& c, Tab& t, WalkShared& S, i64 n_rows, d
         u32 lv = c.coord ? t.level[r] : 0u;
         window_key(lv, c.coord ? t.rs[r] : t.arr[r], t.rank[r], hi, lo);
         if (!run_eligible(c, S, (u32)r, hi, lo, t.winpos[r], bi)) continue;
-        k = victim_key(true, false, lv, ceil_div64(kvv, c.bs), t.rank[r]);
+        k = victim_key(true, false, lv, blocks_ceil(c, kvv), t.rank[r]);
       } else {
         continue;
       }
@@ -1730,7 +1900,7 @@ __device__ void walk_fullscan(const Cfg& c, Tab& t, WalkShared& S, i64 n_rows, d
       shr[0] = br;
       if (br != 0xffffffffu && s_n < FS_CAP) {
         bool pinned = (bk >> 63) == 0;
-        i32 blk = pinned ? t.pb[br] : (i32)ceil_div64(t.kv[br], c.bs);
+        i32 blk = pinned ? t.pb[br] : (i32)blocks_ceil(c, t.kv[br]);
         fs_row[s_n] = br;
         fs_pin[s_n] = pinned;
         fs_blk[s_n] = blk;
@@ -1758,32 +1928,60 @@ __device__ void walk_fullscan(const Cfg& c, Tab& t, WalkShared& S, i64 n_rows, d
 // sorted.  Bitonic when n <= SORT_CAP, else MSD radix refinement first.
 __device__ int cta_select_sorted(const u64* ghi, const u64* glo, const u32* gpay, int n, int k,
                                  u64* kh, u64* kl, u32* pv, u32* hist /*256*/) {
-  if (n <= (int)blockDim.x && n <= SORT_CAP / 4) {
-    // small candidate sets: rank by counting (keys are unique through the
-    // session rank), two barriers instead of a log^2 sorting network
-    u64* th = kh + SORT_CAP / 2;
-    u64* tl = kl + SORT_CAP / 2;
-    u32* tp = pv + SORT_CAP / 2;
+  if (n <= (int)blockDim.x && n <= SORT_CAP / 2) {
+    // small candidate sets: bitonic network with one key per thread held in
+    // registers -- partners exchange by warp shuffle for strides < 32 and
+    // through shared memory (two barriers) only for the wider strides
+    u64* xh = kh + SORT_CAP / 2;
+    u64* xl = kl + SORT_CAP / 2;
+    u32* xp = pv + SORT_CAP / 2;
     const int i = threadIdx.x;
-    u64 h = 0, l = 0;
-    u32 p = 0;
+    const int n2 = next_pow2(n > 1 ? n : 1);
+    u64 h = ~0ull, l = ~0ull;
+    u32 p = 0xffffffffu;
     if (i < n) {
       h = ghi[i];
       l = glo[i];
       p = gpay[i];
-      th[i] = h;
-      tl[i] = l;
-      tp[i] = p;
+    }
+    for (int kk = 2; kk <= n2; kk <<= 1) {
+      for (int j = kk >> 1; j > 0; j >>= 1) {
+        u64 oh, ol;
+        u32 op;
+        if (j >= 32) {
+          __syncthreads();
+          if (i < n2) {
+            xh[i] = h;
+            xl[i] = l;
+            xp[i] = p;
+          }
+          __syncthreads();
+          const int q = (i ^ j) < n2 ? (i ^ j) : i;
+          oh = xh[q];
+          ol = xl[q];
+          op = xp[q];
+        } else if ((i & ~31) < n2) {  // warps without elements skip the shuffles
+          oh = __shfl_xor_sync(FULL, h, j);
+          ol = __shfl_xor_sync(FULL, l, j);
+          op = __shfl_xor_sync(FULL, p, j);
+        } else {
+          continue;
+        }
+        // the lower position of an ascending pair keeps the minimum
+        const bool want_min = ((i & j) == 0) == ((i & kk) == 0);
+        const bool other_less = key_lt(oh, ol, h, l);
+        if (i < n2 && (want_min ? other_less : key_lt(h, l, oh, ol))) {
+          h = oh;
+          l = ol;
+          p = op;
+        }
+      }
     }
     __syncthreads();
-    if (i < n) {
-      int rnk = 0;
-      for (int j = 0; j < n; ++j) rnk += key_lt(th[j], tl[j], h, l) ? 1 : 0;
-      if (rnk < k) {
-        kh[rnk] = h;
-        kl[rnk] = l;
-        pv[rnk] = p;
-      }
+    if (i < n && i < k) {
+      kh[i] = h;
+      kl[i] = l;
+      pv[i] = p;
     }
     __syncthreads();
     return n < k ? n : k;
@@ -1887,7 +2085,8 @@ __global__ void __launch_bounds__(WALK_TPB) k_walk(Tab t, Cfg c, Work* w, Bufs b
   i32* fs_blk = (i32*)(((uintptr_t)(fs_pin + FS_CAP) + 15) & ~(uintptr_t)15);
 
   const double now = w->in.now;
-  // 1. window = top-k of the candidates (k_compact + admitted rows)
+  PTIME(16);
+  // 1. window = top-k of the candidates (k_scan + admitted rows)
   int nwc = w->n_wc;
   int nwin = cta_select_sorted(b.wc_hi, b.wc_lo, b.wc_row, nwc, c.window, kh, kl, pv, hist);
   for (int i = threadIdx.x; i < nwin; i += blockDim.x) {
@@ -1920,12 +2119,12 @@ __global__ void __launch_bounds__(WALK_TPB) k_walk(Tab t, Cfg c, Work* w, Bufs b
     S.fast_ok = 0;
   }
   __syncthreads();
+  PTIME(17);
 
   // 2. fast path (warp 0): no claim can fail when the free pool covers every
   //    allocation of the greedy plan -> prefix sums reproduce build_plan.
   if (threadIdx.x < 32) {
     int lane = threadIdx.x;
-    const long long bs = c.bs;
     long long budget = c.budget;
     long long lim_dec = c.max_dec < budget ? c.max_dec : budget;
     // decode eligibility counts
@@ -1933,6 +2132,7 @@ __global__ void __launch_bounds__(WALK_TPB) k_walk(Tab t, Cfg c, Work* w, Bufs b
     long long need_dec = 0;
     int selected_mask[4] = {0, 0, 0, 0};
     int cnt_before = 0;
+    #pragma unroll 1
     for (int q = 0; q < 4; ++q) {
       int i = q * 32 + lane;
       bool e = i < nwin && S.wph[i] == MARS_DECODE && S.wrem[i] >= 1;
@@ -1940,17 +2140,19 @@ __global__ void __launch_bounds__(WALK_TPB) k_walk(Tab t, Cfg c, Work* w, Bufs b
       int pos = cnt_before + __popc(m & ((1u << lane) - 1u));
       bool sel = e && pos < lim_dec;
       selected_mask[q] = sel;
-      if (sel && (S.wkv[i] % bs == 0)) need_dec += 1;
+      if (sel && block_aligned(c, S.wkv[i])) need_dec += 1;
       cnt_before += __popc(m);
     }
     (void)base;
     long long ndec = cnt_before < lim_dec ? cnt_before : lim_dec;
     need_dec = warp_sum<long long>(need_dec);
+    PTIME(22);
     long long left0 = budget - ndec;
     // prefill grants: S_j = min(P_j, left0), g_j = min(rp_j, left0 - S_j)
     long long run = 0;  // P_j prefix over earlier PREFILL entries
     long long need_pre = 0;
     long long grant[4] = {0, 0, 0, 0};
+    #pragma unroll 1
     for (int q = 0; q < 4; ++q) {
       int i = q * 32 + lane;
       bool p = i < nwin && S.wph[i] == MARS_PREFILL;
@@ -1968,14 +2170,16 @@ __global__ void __launch_bounds__(WALK_TPB) k_walk(Tab t, Cfg c, Work* w, Bufs b
       long long g = 0;
       if (p && lft >= 1 && rp >= 1) g = rp < lft ? rp : lft;
       grant[q] = g;
-      if (g > 0) need_pre += ceil_div64(S.wkv[i] + g, bs) - ceil_div64(S.wkv[i], bs);
+      if (g > 0) need_pre += blocks_ceil(c, S.wkv[i] + g) - blocks_ceil(c, S.wkv[i]);
       run += __shfl_sync(FULL, incl, 31);
     }
     need_pre = warp_sum<long long>(need_pre);
+    PTIME(23);
     bool ok = S.freeb >= need_dec + need_pre;
     if (ok) {
       // emit in window order: decode allocations, then prefill allocations
       int dcount = 0, pcount = 0, jcount = 0;
+      #pragma unroll 1
       for (int q = 0; q < 4; ++q) {
         int i = q * 32 + lane;
         bool sel = selected_mask[q];
@@ -1986,7 +2190,7 @@ __global__ void __launch_bounds__(WALK_TPB) k_walk(Tab t, Cfg c, Work* w, Bufs b
           S.wplanned[i] = 1;
         }
         dcount += __popc(m);
-        bool need = sel && (S.wkv[i] % bs == 0);
+        bool need = sel && block_aligned(c, S.wkv[i]);
         u32 mj = __ballot_sync(FULL, need);
         int jp = jcount + __popc(mj & ((1u << lane) - 1u));
         if (need) {
@@ -1997,13 +2201,14 @@ __global__ void __launch_bounds__(WALK_TPB) k_walk(Tab t, Cfg c, Work* w, Bufs b
         jcount += __popc(mj);
       }
       long long tot = ndec;
+      #pragma unroll 1
       for (int q = 0; q < 4; ++q) {
         int i = q * 32 + lane;
         long long g = grant[q];
         bool gp = g > 0;
         u32 m = __ballot_sync(FULL, gp);
         int pos = pcount + __popc(m & ((1u << lane) - 1u));
-        long long nd = gp ? ceil_div64(S.wkv[i] + g, bs) - ceil_div64(S.wkv[i], bs) : 0;
+        long long nd = gp ? blocks_ceil(c, S.wkv[i] + g) - blocks_ceil(c, S.wkv[i]) : 0;
         if (gp) {
           b.pre_rows[pos] = S.wrow[i];
           b.pre_grant[pos] = (i32)g;
@@ -2033,6 +2238,7 @@ __global__ void __launch_bounds__(WALK_TPB) k_walk(Tab t, Cfg c, Work* w, Bufs b
     }
   }
   __syncthreads();
+  PTIME(20);
 
   // 3. sequential walk with on-demand help from the whole CTA
   if (!S.fast_ok) {
@@ -2152,6 +2358,7 @@ __global__ void __launch_bounds__(WALK_TPB) k_walk(Tab t, Cfg c, Work* w, Bufs b
     w->walk_slow = S.fast_ok ? 0 : 1;
     w->status |= S.status;
     sc->free_blocks = S.freeb;
+    PTIME(21);
   }
 }
 
@@ -2242,8 +2449,40 @@ static size_t walk_smem_bytes() {
 
 static size_t sort_smem_bytes() { return (size_t)SORT_CAP * (8 + 8 + 4); }
 
+// k_scan geometry: <= 1 CTA per SM, contiguous row ranges of `chunk` rows
+// (a multiple of SCAN_RPT), the digit record in shared memory when it fits
+static void scan_geometry(i64 n, int nsm, int* grid, i64* chunk, int* in_smem) {
+  i64 g = (n + SCAN_TILE - 1) / SCAN_TILE;
+  if (g > nsm) g = nsm;
+  if (g > SCAN_TPB) g = SCAN_TPB;
+  if (g < 1) g = 1;
+  i64 units = (n + 15) / 16;  // TMA rounds start 16-row (16-byte) aligned
+  *grid = (int)g;
+  *chunk = ((units + g - 1) / g) * 16;
+  *in_smem = (*chunk * 4 <= DIG_SMEM_MAX) ? 1 : 0;
+}
+
+static void launch_scan(const LaunchArgs* a, int nsm, cudaStream_t s) {
+  int grid, in_smem;
+  i64 chunk;
+  scan_geometry(a->n_rows, nsm, &grid, &chunk, &in_smem);
+  Tab t = a->tab;
+  Cfg c = a->cfg;
+  Work* w = a->work;
+  Bufs b = a->bufs;
+  mars_scalars* sc = a->sc;
+  i64 n = a->n_rows;
+  i64* xc = a->x.xc;
+  void* args[] = {&t, &c, &w, &b, &sc, &n, &xc, &chunk, &in_smem};
+  cudaLaunchCooperativeKernel((const void*)k_scan, dim3(grid), dim3(SCAN_TPB), args,
+                              scan_stage_bytes() + (in_smem ? (size_t)chunk * 4 : 0), s);
+}
+
 int mars_kernels_init() {
   cudaError_t e;
+  e = cudaFuncSetAttribute(k_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(scan_stage_bytes() + DIG_SMEM_MAX));
+  if (e != cudaSuccess) return (int)e;
   e = cudaFuncSetAttribute(k_walk, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)walk_smem_bytes());
   if (e != cudaSuccess) return (int)e;
@@ -2274,11 +2513,8 @@ int mars_enqueue_step(const LaunchArgs* a) {
     cudaMemcpyAsync(a->work, a->host_in, sizeof(mars_step_in), cudaMemcpyHostToDevice, s);
     k_work_init<<<1, 32, 0, s>>>(a->work);
     launches++;
-    int g_scan = (int)((n + SCAN_TILE - 1) / SCAN_TILE);  // persistent: <= 1 CTA per SM
-    if (g_scan > nsm) g_scan = nsm;
-    if (g_scan < 1) g_scan = 1;
     mark(0, 0, s);
-    k_scan<<<g_scan, SCAN_TPB, 0, s>>>(a->tab, a->cfg, a->work, a->bufs, a->sc, n, a->x.xc);
+    launch_scan(a, nsm, s);
     mark(0, 1, s);
     launches++;
     if (sharded) {
@@ -2293,49 +2529,41 @@ int mars_enqueue_step(const LaunchArgs* a) {
     k_build_global_queue<<<nsm, 256, 0, s>>>(a->work, a->x);
     launches += 2;
   }
-  cudaEventRecord(a->ev_fork, s);
-  cudaStreamWaitEvent(s2, a->ev_fork, 0);
-  int g_c = (int)((n + SCAN_TPB * SCAN_RPT - 1) / (SCAN_TPB * SCAN_RPT));
-  if (g_c > 2 * nsm) g_c = 2 * nsm;
-  if (g_c < 1) g_c = 1;
-  mark(1, 0, s2);
-  k_compact<<<g_c, SCAN_TPB, 0, s2>>>(a->tab, a->cfg, a->work, a->bufs, a->sc, n);
-  mark(1, 1, s2);
-  launches++;
-  mark(2, 0, s2);
-  if (a->exp_sort) {
-    k_exp_small<<<1, 1024, sort_smem_bytes(), s2>>>(a->work, a->bufs, a->xlsd);
-    launches++;
-  }
-  if (a->exp_may_be_big) {
-    for (int p = 0; p < 4; ++p) {
-      k_lsd_hist<<<LSD_G, 256, 0, s2>>>(a->xlsd, a->work, 1, p);
-      k_lsd_scan<<<1, 1024, 0, s2>>>(a->xlsd, a->work, 1, p, LSD_G);
-      k_lsd_scatter<<<LSD_G, 256, 0, s2>>>(a->xlsd, a->work, 1, p);
-      launches += 3;
+  // expired pins in rank order (tables that are not rank-ordered only)
+  const bool side = a->exp_sort || a->exp_may_be_big;
+  if (side) {
+    cudaEventRecord(a->ev_fork, s);
+    cudaStreamWaitEvent(s2, a->ev_fork, 0);
+    mark(2, 0, s2);
+    if (a->exp_sort) {
+      k_exp_small<<<1, 1024, sort_smem_bytes(), s2>>>(a->work, a->bufs, a->xlsd);
+      launches++;
     }
-    k_exp_gather<<<nsm, 256, 0, s2>>>(a->work, a->bufs, a->xlsd);
-    launches++;
+    if (a->exp_may_be_big) {
+      launch_lsd(a->xlsd, a->work, 1, 4, nsm, s2);
+      launches++;
+      k_exp_gather<<<nsm, 256, 0, s2>>>(a->work, a->bufs, a->xlsd);
+      launches++;
+    }
+    mark(2, 1, s2);
+    cudaEventRecord(a->ev_join, s2);
   }
-  mark(2, 1, s2);
-  cudaEventRecord(a->ev_join, s2);
   if (a->control_possible) {
     mark(3, 0, s);
     k_pack_small<<<1, 1024, sort_smem_bytes(), s>>>(a->work, a->queue, a->qlsd, a->sc, a->qsel,
                                                     a->gq);
     launches++;
-    // ~4K list entries per CTA: the single-CTA offset scan walks G columns
-    i64 lgq = (a->queue_upper + 1023) / 1024;  // ~1K list entries per CTA
-    int lg = (int)(lgq < 1 ? 1 : (lgq > LSD_G ? LSD_G : lgq));
-    for (int p = 0; p < a->queue_passes; ++p) {
-      k_lsd_hist<<<lg, 256, 0, s>>>(a->qlsd, a->work, 0, p);
-      k_lsd_scan<<<1, 1024, 0, s>>>(a->qlsd, a->work, 0, p, lg);
-      k_lsd_scatter<<<lg, 256, 0, s>>>(a->qlsd, a->work, 0, p);
-      launches += 3;
-    }
     mark(3, 1, s);
+    if (a->queue_passes > 0) {
+      mark(6, 0, s);
+      i64 lgq = (a->queue_upper + 1023) / 1024;  // ~1K list entries per CTA
+      int lg = (int)(lgq < 1 ? 1 : (lgq > nsm ? nsm : lgq));
+      launch_lsd(a->qlsd, a->work, 0, a->queue_passes, lg, s);
+      launches++;
+      mark(6, 1, s);
+    }
   }
-  cudaStreamWaitEvent(s, a->ev_join, 0);
+  if (side) cudaStreamWaitEvent(s, a->ev_join, 0);
   if (a->control_possible) {
     i64 qb = 1;
     while (qb < a->queue_upper) qb <<= 1;  // pow2 bucket: stable launch shape for graphs
@@ -2356,6 +2584,9 @@ int mars_enqueue_step(const LaunchArgs* a) {
   }
   mark(5, 1, s);
   launches++;
+#ifdef MARS_PHASE_TIMING
+  k_ptime_dump<<<1, 1, 0, s>>>();
+#endif
   return launches;
 }
 

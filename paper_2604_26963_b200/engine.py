@@ -10,7 +10,7 @@ benchmark and the multi-GPU replicas use; the reference-plugin drop-in
 from __future__ import annotations
 
 import ctypes as C
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 from typing import Dict, List, Optional
 
 import numpy as np
@@ -79,6 +79,7 @@ class StepResult:
     free_blocks: int
     limit: int
     slots: int
+    diag: Dict[str, int] = field(default_factory=dict)
 
 
 def _arr(p, n, dt):
@@ -268,7 +269,9 @@ class MarsEngine:
             fin_deadline=_arr(o.fin_deadline, o.n_finish, np.float64),
             n_ready=o.n_ready, n_promoted=o.n_promoted, pack_mode=o.pack_mode,
             total_tokens=o.total_tokens, free_after_expiry=o.free_after_expiry,
-            free_blocks=o.free_blocks, limit=o.limit, slots=o.slots)
+            free_blocks=o.free_blocks, limit=o.limit, slots=o.slots,
+            diag={"n_window_cand": o.n_window_cand, "n_victim_cand": o.n_victim_cand,
+                  "walk_slow": o.walk_slow})
 
     def step(self, si: N.MarsStepIn) -> StepResult:
         self.enqueue(si)
@@ -301,8 +304,8 @@ class MarsEngine:
         self._check(self.lib.mars_set_profiling(self.ctx, int(bool(on))))
 
     def kernel_times(self) -> Dict[str, float]:
-        ms = (C.c_float * 6)()
-        self._check(self.lib.mars_kernel_times(self.ctx, ms, 6))
+        ms = (C.c_float * len(N.KTIME_NAMES))()
+        self._check(self.lib.mars_kernel_times(self.ctx, ms, len(N.KTIME_NAMES)))
         return {k: float(v) for k, v in zip(N.KTIME_NAMES, ms)}
 
     def launches(self) -> int:
