@@ -37,7 +37,7 @@ namespace cg = cooperative_groups;
 #ifdef MARS_PHASE_TIMING
 // Debug builds only (-DMARS_PHASE_TIMING): per-CTA %globaltimer stamps at
 // named points of the step, dumped as a timeline after each step.
-#define PT_SLOTS 24
+#define PT_SLOTS 32
 __device__ unsigned long long g_ptime[1024][PT_SLOTS];
 __device__ __forceinline__ void ptime(int k) {
   if (threadIdx.x == 0) {
@@ -348,6 +348,9 @@ __device__ void block_threshold_pair(const u32* ha, u32 ka, const u32* hb, u32 k
 }
 
 // ---- 1D TMA (cp.async.bulk) + mbarrier helpers -----------------------------
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 __device__ __forceinline__ u32 smem_u32(const void* p) {
   return (u32)__cvta_generic_to_shared(p);
 }
@@ -625,6 +628,7 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
   // ---- phase 2 ---------------------------------------------------------------
   // global thresholds over the exact prefix of the merged histograms
   const u32 tmw = __ldcg(&w->tmin_win), tmv = __ldcg(&w->tmin_vic);
+  const int tile_cnt_g = (int)threadIdx.x < (int)gridDim.x ? __ldcg(&b.tile_cnt[threadIdx.x]) : 0;
 #pragma unroll
   for (int q = 0; q < HIST_BINS / SCAN_TPB; ++q) {
     const int i = q * SCAN_TPB + threadIdx.x;
@@ -652,8 +656,7 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
   int n_exp_all, exp_off;
   {
     __shared__ int s_b[32], s_a[32];
-    const int G = gridDim.x;  // <= SCAN_TPB (host-checked)
-    const int cg_ = (int)threadIdx.x < G ? __ldcg(&b.tile_cnt[threadIdx.x]) : 0;
+    const int cg_ = tile_cnt_g;  // gridDim.x <= SCAN_TPB (host-checked)
     const int bs = __reduce_add_sync(FULL, (int)threadIdx.x < me ? cg_ : 0);
     const int as = __reduce_add_sync(FULL, cg_);
     if (lane == 0) {
@@ -1928,6 +1931,97 @@ __device__ void walk_fullscan(const Cfg& c, Tab& t, WalkShared& S, i64 n_rows, d
 // sorted.  Bitonic when n <= SORT_CAP, else MSD radix refinement first.
 __device__ int cta_select_sorted(const u64* ghi, const u64* glo, const u32* gpay, int n, int k,
                                  u64* kh, u64* kl, u32* pv, u32* hist /*256*/) {
+  if (n > k && n <= (int)blockDim.x && n <= SORT_CAP / 2) {
+    // more candidates than wanted: a 256-bucket linear histogram over the
+    // candidates' hi range (monotone in the key) keeps the buckets up to the
+    // k-th key's; the survivors are ranked by counting, 1024 threads sharing
+    // the comparisons (keys are unique through the session rank)
+    __shared__ u64 s_mm[32];
+    __shared__ int s_B, s_ns;
+    __shared__ u32 s_rank[512];
+    u64* th = kh + SORT_CAP / 2;
+    u64* tl = kl + SORT_CAP / 2;
+    u32* tp = pv + SORT_CAP / 2;
+    const int i = threadIdx.x;
+    u64 h = ~0ull, l = ~0ull;
+    u32 p = 0;
+    if (i < n) {
+      h = ghi[i];
+      l = glo[i];
+      p = gpay[i];
+    }
+    const u64 mn = block_min<u64>(h, s_mm, ~0ull);
+    const u64 mx = block_max<u64>(i < n ? h : 0ull, s_mm, 0ull);
+    const double span = (double)(mx - mn);
+    const double inv = span > 0.0 ? 255.0 / span : 0.0;
+    u32 bk = 0;
+    if (i < n) {
+      const double f = (double)(h - mn) * inv;
+      bk = f >= 255.0 ? 255u : (u32)f;
+    }
+    for (int q = i; q < 256; q += blockDim.x) hist[q] = 0;
+    if (i == 0) s_ns = 0;
+    __syncthreads();
+    if (i < n) atomicAdd(&hist[bk], 1u);
+    __syncthreads();
+    if (i < 32) {  // first bucket whose cumulative count reaches k
+      u32 v[8], sum = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        v[q] = hist[i * 8 + q];
+        sum += v[q];
+      }
+      u32 incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const u32 x = __shfl_up_sync(FULL, incl, o);
+        if (i >= o) incl += x;
+      }
+      u32 cum = incl - sum;
+      int B = 0x7fffffff;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (cum < (u32)k && cum + v[q] >= (u32)k) B = i * 8 + q;
+        cum += v[q];
+      }
+      B = __reduce_min_sync(FULL, B);
+      if (i == 0) s_B = B;
+    }
+    __syncthreads();
+    if (i < n && (int)bk <= s_B) {
+      const int sl = atomicAdd(&s_ns, 1);
+      th[sl] = h;
+      tl[sl] = l;
+      tp[sl] = p;
+    }
+    __syncthreads();
+    const int ns = s_ns;
+    if (ns <= 512) {
+      // parts threads per survivor, each counting a slice of the others
+      const int parts = ns <= 256 ? 4 : 2;
+      const int q = i / parts, part = i % parts;
+      if (i < 512) s_rank[i] = 0;
+      __syncthreads();
+      if (q < ns) {
+        const u64 qh = th[q], ql = tl[q];
+        int cnt = 0;
+        for (int j = part; j < ns; j += parts) cnt += key_lt(th[j], tl[j], qh, ql) ? 1 : 0;
+        if (cnt) atomicAdd(&s_rank[q], (u32)cnt);
+      }
+      __syncthreads();
+      if (i < ns) {
+        const int rnk = (int)s_rank[i];
+        if (rnk < k) {
+          kh[rnk] = th[i];
+          kl[rnk] = tl[i];
+          pv[rnk] = tp[i];
+        }
+      }
+      __syncthreads();
+      return k;
+    }
+    // clustered keys: fall through to the full sort
+  }
   if (n <= (int)blockDim.x && n <= SORT_CAP / 2) {
     // small candidate sets: bitonic network with one key per thread held in
     // registers -- partners exchange by warp shuffle for strides < 32 and
@@ -2089,6 +2183,7 @@ __global__ void __launch_bounds__(WALK_TPB) k_walk(Tab t, Cfg c, Work* w, Bufs b
   // 1. window = top-k of the candidates (k_scan + admitted rows)
   int nwc = w->n_wc;
   int nwin = cta_select_sorted(b.wc_hi, b.wc_lo, b.wc_row, nwc, c.window, kh, kl, pv, hist);
+  PTIME(24);
   for (int i = threadIdx.x; i < nwin; i += blockDim.x) {
     u32 r = pv[i];
     S.whi[i] = kh[i];
