@@ -990,12 +990,12 @@ __global__ void __launch_bounds__(1024, 1) k_lsd_coop(Lsd L, Work* w, int which,
     // digit d's total over all chunks and over the chunks before mine
     const int c0 = (G * p) / 4, c1 = (G * (p + 1)) / 4;
     u32 tot = 0, bel = 0;
-    for (int c = c0; c < c1; c += 16) {  // 16 independent L2 loads in flight
-      u32 x[16];
+    for (int c = c0; c < c1; c += 32) {  // up to 32 independent L2 loads in flight
+      u32 x[32];
 #pragma unroll
-      for (int q = 0; q < 16; ++q) x[q] = c + q < c1 ? __ldcg(&L.cnt[(c + q) * 256 + d]) : 0u;
+      for (int q = 0; q < 32; ++q) x[q] = c + q < c1 ? __ldcg(&L.cnt[(c + q) * 256 + d]) : 0u;
 #pragma unroll
-      for (int q = 0; q < 16; ++q) {
+      for (int q = 0; q < 32; ++q) {
         tot += x[q];
         bel += c + q < me ? x[q] : 0u;
       }
@@ -1296,6 +1296,8 @@ __global__ void __launch_bounds__(1024) k_pack_small(Work* w, Queue Q, Lsd L,
       w->lsd_raw_ptr = (u64)(uintptr_t)req;
       w->lsd_cur = 0;
     }
+    // the sort's first pass reads the list straight away: pull it into L2 now
+    for (int i = threadIdx.x * 32; i < qlen; i += blockDim.x * 32) prefetch_l2(req + i);
     PTIME(19);
     return;
   }
@@ -1398,33 +1400,41 @@ __global__ void __launch_bounds__(SCAN_TPB) k_admit_apply(Tab t, Cfg c, Work* w,
     if (valid && (w->in.mode & MARS_MODE_NO_ROWS)) {
       b.admitted[i] = src_row[perm[i]];
     } else if (valid) {
-      u32 pos = in_order ? (u32)i : perm[i];
+      // every load is issued before the first table store (the stores may
+      // alias them as far as the compiler knows): two dependent round trips
+      const u32 pi = perm[i];
+      const u32 pos = in_order ? (u32)i : pi;
       row = src_row[pos];
+      const u32 adm = in_order ? src_row[pi] : row;
       if (sharded && row == XQ_NONE) {
         // another replica's session: a fresh queued session projects exactly
         // req_blocks (context 0, kv 0: control.py:86-87 vs sim.py:162)
         proj += src_req[pos];
       } else {
         own = sharded;
-        i32 r0p = t.r0p[row];
-        i32 kvv = t.kv[row];
-        i64 cn = (i64)t.ctx[row] + r0p;
+        const i32 r0p = t.r0p[row];
+        const i32 kvv = t.kv[row];
+        const i32 ctx0 = t.ctx[row];
+        const i32 r0d = t.r0d[row];
+        const u8 fl = t.flags[row];
+        const double arr = c.coord ? now : t.arr[row];
+        const i64 cn = (i64)ctx0 + r0p;
+        const u32 lv = initial_level(c, r0p);
+        const u32 kl = c.coord ? lv : 0u;
+        wc = window_digit(kl, arr, scale) <= tw;
+        const u32 rk = wc ? t.rank[row] : 0u;
         t.ctx[row] = (i32)cn;
-        t.rem[row] = t.r0d[row];
+        t.rem[row] = r0d;
         t.rs[row] = now;
         t.ws[row] = now;
         t.phase[row] = MARS_PREFILL;
-        t.flags[row] = (t.flags[row] | MARS_F_ACTIVE) & ~MARS_F_QUEUED;
-        u32 lv = initial_level(c, r0p);
+        t.flags[row] = (fl | MARS_F_ACTIVE) & ~MARS_F_QUEUED;
         t.level[row] = (u8)lv;
         t.promos[row] = 0;
         t.served[row] = 0;
         proj += blocks_ceil(c, cn) - blocks_ceil(c, kvv);
-        if (!sharded) b.admitted[i] = in_order ? src_row[perm[i]] : row;
-        u32 kl = c.coord ? lv : 0u;
-        double tt = c.coord ? now : t.arr[row];
-        window_key(kl, tt, t.rank[row], whi, wlo);
-        wc = window_digit(kl, tt, scale) <= tw;
+        if (!sharded) b.admitted[i] = adm;
+        if (wc) window_key(kl, arr, rk, whi, wlo);
       }
     }
     int s = warp_append(&w->n_wc, wc);
