@@ -131,6 +131,8 @@ struct Work {
   i64 free_after_expiry;
   i32 status;
   i32 walk_slow;
+  i32 n_queued_kv;  // queued rows holding KV (admission then touches reclaim state)
+  u32 admit_done;   // set by k_admit_apply; k_walk may wait on it
   i32 n_finish;
 };
 

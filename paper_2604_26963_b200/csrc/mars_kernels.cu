@@ -475,7 +475,7 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
 
   long long exp_blocks = 0;
   int n_active = 0, n_queued = 0, n_long = 0, n_ready = 0, n_prom = 0, n_vic = 0, n_bnd = 0;
-  int n_exp = 0;
+  int n_exp = 0, n_qkv = 0;
   int max_req = 0, min_req = 0x7fffffff;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   __syncthreads();
@@ -496,6 +496,7 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
       if (f & MARS_F_QUEUED) {
         n_queued++;
         if (f & MARS_F_LONG) n_long++;
+        if (((const i32*)(B + SB_KV))[lr] > 0) n_qkv++;
         const i32 q = ((const i32*)(B + SB_REQ))[lr];
         max_req = q > max_req ? q : max_req;
         min_req = q < min_req ? q : min_req;
@@ -585,16 +586,16 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
 
   // counters: warp shuffles, then one shared and one global atomic per warp/CTA
   {
-    __shared__ int s_cnt[10];
+    __shared__ int s_cnt[11];
     __shared__ unsigned long long s_eb;
-    if (threadIdx.x < 10) s_cnt[threadIdx.x] = (threadIdx.x == 8) ? 0x7fffffff : 0;
+    if (threadIdx.x < 11) s_cnt[threadIdx.x] = (threadIdx.x == 8) ? 0x7fffffff : 0;
     if (threadIdx.x == 0) s_eb = 0;
     __syncthreads();
     unsigned long long eb = warp_sum<unsigned long long>((unsigned long long)exp_blocks);
-    u32 v[8] = {(u32)n_active, (u32)n_queued, (u32)n_long, (u32)n_ready,
-                (u32)n_prom,   (u32)n_vic,    (u32)n_bnd,  (u32)n_exp};
+    u32 v[9] = {(u32)n_active, (u32)n_queued, (u32)n_long, (u32)n_ready, (u32)n_prom,
+                (u32)n_vic,    (u32)n_bnd,    (u32)n_exp,  (u32)n_qkv};
 #pragma unroll
-    for (int q = 0; q < 8; ++q) v[q] = __reduce_add_sync(FULL, v[q]);
+    for (int q = 0; q < 9; ++q) v[q] = __reduce_add_sync(FULL, v[q]);
     int mx = __reduce_max_sync(FULL, max_req), mn = __reduce_min_sync(FULL, min_req);
     if (lane == 0) {
       if (eb) atomicAdd(&s_eb, eb);
@@ -602,6 +603,7 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
       for (int q = 0; q < 7; ++q)
         if (v[q]) atomicAdd(&s_cnt[q], (int)v[q]);
       if (v[7]) atomicAdd(&s_cnt[9], (int)v[7]);
+      if (v[8]) atomicAdd(&s_cnt[10], (int)v[8]);
       atomicMax(&s_cnt[7], mx);
       atomicMin(&s_cnt[8], mn);
     }
@@ -618,6 +620,7 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
       atomicAdd(&w->n_boundary, s_cnt[6]);
       atomicMax(&w->max_req, s_cnt[7]);
       atomicMin(&w->min_req, s_cnt[8]);
+      if (s_cnt[10]) atomicAdd(&w->n_queued_kv, s_cnt[10]);
     }
   }
 
@@ -1328,7 +1331,10 @@ __global__ void __launch_bounds__(1024) k_pack_small(Work* w, Queue Q, Lsd L,
 __global__ void __launch_bounds__(SCAN_TPB) k_admit_apply(Tab t, Cfg c, Work* w, Bufs b, Queue Q,
                                                           Lsd L, mars_scalars* sc, i32* qsel_p,
                                                           Queue G, Xchg x) {
-  if (!w->in.control_due) return;
+  if (!w->in.control_due) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicExch(&w->admit_done, 1u);
+    return;
+  }
   PTIME(12);
   __shared__ long long shl[32];
   __shared__ bool s_last;
@@ -1505,6 +1511,8 @@ __global__ void __launch_bounds__(SCAN_TPB) k_admit_apply(Tab t, Cfg c, Work* w,
     sc->queue_len = sharded ? (i64)vw->n_res_own : qlen - take;
     w->global_residual = nres;
     *qsel_p = 1 - sel;
+    __threadfence();
+    atomicExch(&w->admit_done, 1u);  // k_walk may be waiting (admit_async)
     PTIME(15);
   }
 }
@@ -2175,7 +2183,8 @@ __device__ int cta_select_sorted(const u64* ghi, const u64* glo, const u32* gpay
 }
 
 __global__ void __launch_bounds__(WALK_TPB) k_walk(Tab t, Cfg c, Work* w, Bufs b,
-                                                   mars_scalars* sc, i64 n_rows) {
+                                                   mars_scalars* sc, i64 n_rows,
+                                                   int admit_async) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ WalkShared S;
   __shared__ u32 hist[256];
@@ -2190,6 +2199,30 @@ __global__ void __launch_bounds__(WALK_TPB) k_walk(Tab t, Cfg c, Work* w, Bufs b
 
   const double now = w->in.now;
   PTIME(16);
+  // Admission runs concurrently on the side stream.  Admitted sessions hold no
+  // KV (fresh arrivals), so they are never reclaim victims; they can only join
+  // the window when their window digit (level << 10 | bucket(now) = 1023, or
+  // the arrival bucket with the coordinator off) reaches the threshold -- then
+  // wait for the admission to finish (its candidates and row state).
+  if (admit_async) {
+    if (threadIdx.x == 0) {
+      const bool independent = c.coord && now > 0.0 && now < 1e300 && (u32)w->t_win < 1023u &&
+                               w->n_queued_kv == 0;
+      if (!independent) {
+        // bounded: a missing completion flag is reported, never a hang
+        long long spins = 0;
+        while (atomicAdd(&w->admit_done, 0u) == 0u) {
+          __nanosleep(128);
+          if (++spins > (1ll << 24)) {
+            w->status |= ST_BAD_INPUT;
+            break;
+          }
+        }
+        __threadfence();
+      }
+    }
+    __syncthreads();
+  }
   // 1. window = top-k of the candidates (k_scan + admitted rows)
   int nwc = w->n_wc;
   int nwin = cta_select_sorted(b.wc_hi, b.wc_lo, b.wc_row, nwc, c.window, kh, kl, pv, hist);
@@ -2634,61 +2667,66 @@ int mars_enqueue_step(const LaunchArgs* a) {
     k_build_global_queue<<<nsm, 256, 0, s>>>(a->work, a->x);
     launches += 2;
   }
-  // expired pins in rank order (tables that are not rank-ordered only)
-  const bool side = a->exp_sort || a->exp_may_be_big;
+  // Side stream: the expired-pin rank sort (tables that are not rank-ordered)
+  // and the control plane (pack_queue sort, admission).  The walk runs
+  // concurrently on the main stream: it reads no state admission writes
+  // unless an admitted session can enter the window, and then waits for the
+  // admission's completion flag (k_walk, admit_async).
+  const bool side = a->exp_sort || a->exp_may_be_big || a->control_possible;
   if (side) {
     cudaEventRecord(a->ev_fork, s);
     cudaStreamWaitEvent(s2, a->ev_fork, 0);
+  }
+  if (a->exp_sort || a->exp_may_be_big) {
     mark(2, 0, s2);
     if (a->exp_sort) {
       k_exp_small<<<1, 1024, sort_smem_bytes(), s2>>>(a->work, a->bufs, a->xlsd);
       launches++;
     }
     if (a->exp_may_be_big) {
-      launch_lsd(a->xlsd, a->work, 1, 4, nsm, s2);
+      launch_lsd(a->xlsd, a->work, 1, 4, nsm - 1, s2);  // the walk keeps one SM
       launches++;
       k_exp_gather<<<nsm, 256, 0, s2>>>(a->work, a->bufs, a->xlsd);
       launches++;
     }
     mark(2, 1, s2);
-    cudaEventRecord(a->ev_join, s2);
   }
   if (a->control_possible) {
-    mark(3, 0, s);
-    k_pack_small<<<1, 1024, sort_smem_bytes(), s>>>(a->work, a->queue, a->qlsd, a->sc, a->qsel,
-                                                    a->gq);
+    mark(3, 0, s2);
+    k_pack_small<<<1, 1024, sort_smem_bytes(), s2>>>(a->work, a->queue, a->qlsd, a->sc, a->qsel,
+                                                     a->gq);
     launches++;
-    mark(3, 1, s);
+    mark(3, 1, s2);
     if (a->queue_passes > 0) {
-      mark(6, 0, s);
+      mark(6, 0, s2);
       i64 lgq = (a->queue_upper + 1023) / 1024;  // ~1K list entries per CTA
-      int lg = (int)(lgq < 1 ? 1 : (lgq > nsm ? nsm : lgq));
-      launch_lsd(a->qlsd, a->work, 0, a->queue_passes, lg, s);
+      int lg = (int)(lgq < 1 ? 1 : (lgq > nsm - 1 ? nsm - 1 : lgq));  // the walk keeps one SM
+      launch_lsd(a->qlsd, a->work, 0, a->queue_passes, lg, s2);
       launches++;
-      mark(6, 1, s);
+      mark(6, 1, s2);
     }
-  }
-  if (side) cudaStreamWaitEvent(s, a->ev_join, 0);
-  if (a->control_possible) {
     i64 qb = 1;
     while (qb < a->queue_upper) qb <<= 1;  // pow2 bucket: stable launch shape for graphs
     int g_ap = (int)((qb + SCAN_TPB - 1) / SCAN_TPB);
-    if (g_ap > 2 * nsm) g_ap = 2 * nsm;
+    if (g_ap > nsm - 1) g_ap = nsm - 1;  // leaves the walk's SM free
     if (g_ap < 1) g_ap = 1;
-    mark(4, 0, s);
-    k_admit_apply<<<g_ap, SCAN_TPB, 0, s>>>(a->tab, a->cfg, a->work, a->bufs, a->queue, a->qlsd,
-                                            a->sc, a->qsel, a->gq, a->x);
-    mark(4, 1, s);
+    mark(4, 0, s2);
+    k_admit_apply<<<g_ap, SCAN_TPB, 0, s2>>>(a->tab, a->cfg, a->work, a->bufs, a->queue, a->qlsd,
+                                             a->sc, a->qsel, a->gq, a->x);
+    mark(4, 1, s2);
     launches++;
   }
+  if (side) cudaEventRecord(a->ev_join, s2);
   mark(5, 0, s);
-  k_walk<<<1, WALK_TPB, walk_smem_bytes(), s>>>(a->tab, a->cfg, a->work, a->bufs, a->sc, n);
+  k_walk<<<1, WALK_TPB, walk_smem_bytes(), s>>>(a->tab, a->cfg, a->work, a->bufs, a->sc, n,
+                                                a->control_possible);
   if (a->kv) {
     mars_kv_enqueue_apply_step(*a->kv, s, a->work, a->bufs);
     launches++;
   }
   mark(5, 1, s);
   launches++;
+  if (side) cudaStreamWaitEvent(s, a->ev_join, 0);
 #ifdef MARS_PHASE_TIMING
   k_ptime_dump<<<1, 1, 0, s>>>();
 #endif
