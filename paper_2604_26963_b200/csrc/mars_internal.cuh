@@ -93,7 +93,6 @@ struct Lsd {
 struct Work {
   mars_step_in in;
   // K_A accumulators
-  u32 ticket_ap;
   unsigned long long exp_blocks;
   i32 n_exp, n_active, n_queued, n_long_q, n_ready, n_promoted, n_victims, n_boundary;
   i32 tab_long_q, tab_max_req, tab_min_req;  // queue stats from the table scan
@@ -132,7 +131,7 @@ struct Work {
   i32 status;
   i32 walk_slow;
   i32 n_queued_kv;  // queued rows holding KV (admission then touches reclaim state)
-  u32 admit_done;   // set by k_admit_apply; k_walk may wait on it
+  u32 admit_done;   // set by k_control after admission; k_walk may wait on it
   i32 n_finish;
 };
 

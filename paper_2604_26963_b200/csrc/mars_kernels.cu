@@ -1,7 +1,7 @@
 // B200 (sm_100a) kernels of the MARS scheduling step.
 //
-// Pipeline, one CUDA stream (+ a side stream for the rare
-// expired-pin sort):
+// Pipeline: k_scan on the main stream, then the control plane
+// on a side stream concurrently with the walk on the main stream:
 //   k_scan        persistent cooperative pass over the session table, one CTA
 //                 per SM: pin expiry, MLFQ aging (promote_waiting), counters,
 //                 per-CTA key histograms and a per-row digit record; grid
@@ -11,14 +11,15 @@
 //                 refresh_pressure.
 //   k_exp_*       [side] expired pins in session-id (rank) order when the
 //                 table is not rank-ordered.
-//   k_pack_small  control plane: pack_queue for small queues (bitonic) and the
-//                 first-fit mode; k_lsd_coop cooperative stable LSD sort for
-//                 big ones.
-//   k_admit_apply update_window + triple clamp, admit() of the packed prefix,
-//                 residual queue, admitted rows join the window candidates.
+//   k_control     [side] the control plane in one cooperative launch: pack_queue
+//                 (one CTA for small queues / first fit, grid-wide stable LSD
+//                 sort for big ones), update_window + triple clamp, admit() of
+//                 the packed prefix, residual queue; admitted rows that can
+//                 join the window become candidates.
 //   k_walk        single CTA: window top-k, build_plan decode/prefill passes
 //                 with try_fit and reclamation (victim stream or exact
-//                 full-table fallback), plan + ordered journal.
+//                 full-table fallback), plan + ordered journal.  Waits for the
+//                 admission only when an admitted session can join the window.
 //
 // Compiled with --fmad=false: every f64 expression keeps CPython's IEEE
 // rounding so retention / admission scalars are bit-identical.
@@ -948,13 +949,36 @@ __device__ __forceinline__ LsdView lsd_view(Work* w, int which) {
 // histograms -> grid barrier -> every CTA derives its own digit offsets from
 // all chunk counts (no separate scan launch) -> stable in-order scatter ->
 // grid barrier.  Grid <= #SMs, one 1024-thread CTA per SM (co-resident).
-__global__ void __launch_bounds__(1024, 1) k_lsd_coop(Lsd L, Work* w, int which, int npass) {
+// what one grid-wide sort works on (read by every CTA, never from memory
+// another CTA may still be writing)
+struct LsdArgs {
+  int n;
+  u64 maxkey;
+  const i32* raw;  // the queue's first pass reads req[] straight from the list
+  bool asc;        // key = req (ascending pack) or max_req - req (descending)
+  i32 mr;
+  int cur;
+};
+
+__device__ LsdArgs lsd_args_from(Work* w, int which) {
   LsdView v = lsd_view(w, which);
-  if (!*v.big) return;  // grid-uniform
+  LsdArgs a;
+  a.n = *v.n;
+  a.maxkey = *v.maxkey;
+  a.raw = (which == 0) ? (const i32*)(uintptr_t)w->lsd_raw_ptr : nullptr;
+  a.asc = w->pack_mode == PACK_ASC;
+  a.mr = w->max_req;
+  a.cur = *v.cur;
+  return a;
+}
+
+// Returns the buffer holding the sorted values (every CTA; CTA 0 also
+// publishes it).  wc: 32 x 256 u32 of (dynamic) shared memory.
+__device__ int lsd_grid_sort(Lsd L, LsdView v, LsdArgs a, int npass, u32 (*wc)[256]) {
   PTIME(5);
   cg::grid_group grid = cg::this_grid();
-  const int n = *v.n;
-  const u64 maxkey = *v.maxkey;
+  const int n = a.n;
+  const u64 maxkey = a.maxkey;
   const int G = gridDim.x, me = blockIdx.x;
   const int chunk = (n + G - 1) / G;
   const int s = me * chunk, e = min(n, s + chunk);
@@ -962,11 +986,10 @@ __global__ void __launch_bounds__(1024, 1) k_lsd_coop(Lsd L, Work* w, int which,
   const int d = tid & 255, p = tid >> 8;
   __shared__ u32 h[256], off[256], tt[256];
   __shared__ u32 part[4][256], below[4][256];
-  __shared__ u32 wc[32][256];
-  const i32* raw = (which == 0) ? (const i32*)(uintptr_t)w->lsd_raw_ptr : nullptr;
-  const bool asc = w->pack_mode == PACK_ASC;
-  const i32 mr = w->max_req;
-  int cur = *v.cur;
+  const i32* raw = a.raw;
+  const bool asc = a.asc;
+  const i32 mr = a.mr;
+  int cur = a.cur;
   for (int pass = 0; pass < npass; ++pass) {
     const int shift = 8 * pass;
     if (pass > 0 && (maxkey >> shift) == 0) {
@@ -1075,11 +1098,22 @@ __global__ void __launch_bounds__(1024, 1) k_lsd_coop(Lsd L, Work* w, int which,
   }
   PTIME(10);
   if (me == 0 && tid == 0) *v.cur = cur;
+  return cur;
+}
+
+#define LSD_WC_BYTES (32 * 256 * 4)
+
+__global__ void __launch_bounds__(1024, 1) k_lsd_coop(Lsd L, Work* w, int which, int npass) {
+  extern __shared__ __align__(16) u32 lsd_wc[];
+  LsdView v = lsd_view(w, which);
+  if (!*v.big) return;  // grid-uniform
+  lsd_grid_sort(L, v, lsd_args_from(w, which), npass, (u32(*)[256])lsd_wc);
 }
 
 static void launch_lsd(Lsd L, Work* w, int which, int npass, int grid, cudaStream_t s) {
   void* args[] = {&L, &w, &which, &npass};
-  cudaLaunchCooperativeKernel((const void*)k_lsd_coop, dim3(grid), dim3(1024), args, 0, s);
+  cudaLaunchCooperativeKernel((const void*)k_lsd_coop, dim3(grid), dim3(1024), args,
+                              LSD_WC_BYTES, s);
 }
 
 // ---------------------------------------------------------------------------
@@ -1165,10 +1199,11 @@ __device__ i32 cta_kth_i32(const i32* a, int n, int k, u32* hist /*256*/, u32* s
   return (i32)(prefix ^ 0x80000000u);
 }
 
-__global__ void __launch_bounds__(1024) k_pack_small(Work* w, Queue Q, Lsd L,
-                                                     mars_scalars* sc, i32* qsel_p, Queue G) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  if (!w->in.control_due) return;
+// pack_queue (control.py:101-122) on one CTA: the mode, and the whole pack for
+// small queues (bitonic) and the first-fit mode; big queues only set up the
+// grid-wide LSD sort
+__device__ void pack_small_cta(Work* w, Queue Q, Lsd L, mars_scalars* sc, i32* qsel_p, Queue G,
+                               unsigned char* smem) {
   PTIME(18);
   int qlen = (int)w->qlen;
   if (qlen <= 0) return;
@@ -1299,8 +1334,6 @@ __global__ void __launch_bounds__(1024) k_pack_small(Work* w, Queue Q, Lsd L,
       w->lsd_raw_ptr = (u64)(uintptr_t)req;
       w->lsd_cur = 0;
     }
-    // the sort's first pass reads the list straight away: pull it into L2 now
-    for (int i = threadIdx.x * 32; i < qlen; i += blockDim.x * 32) prefetch_l2(req + i);
     PTIME(19);
     return;
   }
@@ -1328,16 +1361,11 @@ __global__ void __launch_bounds__(1024) k_pack_small(Work* w, Queue Q, Lsd L,
 // K_AP: update_window + clamp + admit prefix + residual queue
 // ---------------------------------------------------------------------------
 
-__global__ void __launch_bounds__(SCAN_TPB) k_admit_apply(Tab t, Cfg c, Work* w, Bufs b, Queue Q,
-                                                          Lsd L, mars_scalars* sc, i32* qsel_p,
-                                                          Queue G, Xchg x) {
-  if (!w->in.control_due) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) atomicExch(&w->admit_done, 1u);
-    return;
-  }
+__device__ void admit_grid(Tab t, Cfg c, Work* w, Bufs b, Queue Q, const u32* perm, int mode,
+                           bool need_seed, mars_scalars* sc, i32* qsel_p, Queue G, Xchg x) {
   PTIME(12);
   __shared__ long long shl[32];
-  __shared__ bool s_last;
+  cg::grid_group grid = cg::this_grid();
   const double now = w->in.now;
   const i64 qlen = w->qlen;
   const bool sharded = (w->in.mode & MARS_MODE_SHARDED) != 0;
@@ -1346,12 +1374,10 @@ __global__ void __launch_bounds__(SCAN_TPB) k_admit_apply(Tab t, Cfg c, Work* w,
   const u32* src_row = sharded ? G.row[0] : Q.row[sel];
   const i32* src_req = sharded ? G.req[0] : Q.req[sel];
   const u8* src_lng = sharded ? G.lng[0] : Q.lng[sel];
-  const u32* perm = L.v[w->lsd_cur];
-  const int mode = w->pack_mode;
   // balance_and_admit scalars (control.py:181-190), computed redundantly per CTA
   bool has_seed = sc->has_blocks_seed;
   double seed = sc->blocks_seed;
-  if (w->need_seed) {
+  if (need_seed) {
     has_seed = true;
     if (mode == PACK_FF) {
       seed = w->ff_median;
@@ -1487,19 +1513,13 @@ __global__ void __launch_bounds__(SCAN_TPB) k_admit_apply(Tab t, Cfg c, Work* w,
   }
   PTIME(14);
   long long ps = block_sum<long long>(proj, shl);
-  if (threadIdx.x == 0) {
-    atomicAdd((unsigned long long*)&w->projected, (unsigned long long)ps);
-    __threadfence();
-    u32 tk = atomicAdd(&w->ticket_ap, 1u);
-    s_last = tk == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (s_last && threadIdx.x == 0) {
-    __threadfence();
+  if (threadIdx.x == 0 && ps) atomicAdd((unsigned long long*)&w->projected, (unsigned long long)ps);
+  grid.sync();
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
     volatile Work* vw = w;
     sc->w_adm = wadm;
     sc->last_update = last;
-    if (w->need_seed) {
+    if (need_seed) {
       sc->has_blocks_seed = 1;
       sc->blocks_seed = seed;
     }
@@ -1515,6 +1535,67 @@ __global__ void __launch_bounds__(SCAN_TPB) k_admit_apply(Tab t, Cfg c, Work* w,
     atomicExch(&w->admit_done, 1u);  // k_walk may be waiting (admit_async)
     PTIME(15);
   }
+}
+
+// The control plane in one cooperative launch (grid <= #SMs - 1, the walk
+// keeps an SM): CTA 0 packs small queues / first-fit; big queues are sorted by
+// the whole grid (LSD); then update_window + clamp + admit() over the grid.
+__global__ void __launch_bounds__(1024, 1) k_control(Tab t, Cfg c, Work* w, Bufs b, Queue Q,
+                                                     Lsd L, mars_scalars* sc, i32* qsel_p,
+                                                     Queue G, Xchg x, int npass) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  if (!w->in.control_due) {  // grid-uniform
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicExch(&w->admit_done, 1u);
+    return;
+  }
+  cg::grid_group grid = cg::this_grid();
+  const int qlen = (int)w->qlen;
+  const bool sharded = (w->in.mode & MARS_MODE_SHARDED) != 0;
+  const i32* req = sharded ? G.req[0] : Q.req[*qsel_p];
+  // pack_queue's mode (control.py:109-122) from the queue statistics the table
+  // scan (or the global-list build) reduced: computed by every CTA, so a big
+  // queue goes straight into the grid-wide sort without a barrier
+  int mode = PACK_ASC;
+  bool big = false;
+  if (!(w->in.mode & MARS_MODE_NO_ROWS) && qlen > 0) {
+    const int all_long = w->tab_long_q == qlen ? 1 : 0;
+    mode = sc->cpu_overloaded ? PACK_DESC : (all_long ? PACK_FF : PACK_ASC);
+    big = qlen > SORT_CAP && mode != PACK_FF;
+  }
+  int cur;
+  if (big) {
+    const int mx = w->tab_max_req, mn = w->tab_min_req;
+    LsdArgs a;
+    a.n = qlen;
+    a.maxkey = (mode == PACK_ASC) ? (u64)mx : (u64)(mx - mn);
+    a.raw = req;
+    a.asc = mode == PACK_ASC;
+    a.mr = mx;
+    a.cur = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      w->pack_mode = mode;
+      w->need_seed = (!sc->has_ema_blocks && !sc->has_blocks_seed) ? 1 : 0;
+      w->big_queue = 1;
+      w->lsd_big = 1;
+      w->lsd_n = qlen;
+      w->max_req = mx;
+      w->min_req = mn;
+      w->lsd_maxkey = a.maxkey;
+    }
+    cur = lsd_grid_sort(L, lsd_view(w, 0), a, npass, (u32(*)[256])smem);
+    if (npass == 0) grid.sync();  // (no sort barrier to order the published mode)
+  } else {
+    // small queue, first fit, or a row-less queue: one CTA packs
+    if (blockIdx.x == 0 && qlen > 0) pack_small_cta(w, Q, L, sc, qsel_p, G, smem);
+    grid.sync();
+    cur = 0;
+    if (npass > 0 && w->lsd_big)  // row-less big queue (reduced by pack_small_cta)
+      cur = lsd_grid_sort(L, lsd_view(w, 0), lsd_args_from(w, 0), npass, (u32(*)[256])smem);
+    mode = w->pack_mode;
+  }
+  // the median seed is taken only from a non-empty queue (pack_small_cta)
+  const bool need_seed = qlen > 0 && !sc->has_ema_blocks && !sc->has_blocks_seed;
+  admit_grid(t, c, w, b, Q, L.v[cur], mode, need_seed, sc, qsel_p, G, x);
 }
 
 // ---------------------------------------------------------------------------
@@ -1573,7 +1654,7 @@ __global__ void k_build_global_queue(Work* w, Xchg x) {
     x.gq_req[gp] = rq;
     x.gq_lng[gp] = (u8)(key & 1);
     x.gq_row[gp] = (g == x.rank) ? (u32)x.xrecv[g * stride1 + 2 + 2 * k] : XQ_NONE;
-    // statistics of the union list for pack_queue's mode (k_pack_small)
+    // statistics of the union list for pack_queue's mode (pack_small_cta)
     if (key & 1) atomicAdd(&w->tab_long_q, 1);
     atomicMax(&w->tab_max_req, rq);
     atomicMin(&w->tab_min_req, rq);
@@ -2624,7 +2705,7 @@ int mars_kernels_init() {
   e = cudaFuncSetAttribute(k_walk, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)walk_smem_bytes());
   if (e != cudaSuccess) return (int)e;
-  e = cudaFuncSetAttribute(k_pack_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  e = cudaFuncSetAttribute(k_control, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)sort_smem_bytes());
   if (e != cudaSuccess) return (int)e;
   e = cudaFuncSetAttribute(k_exp_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2692,28 +2773,24 @@ int mars_enqueue_step(const LaunchArgs* a) {
     mark(2, 1, s2);
   }
   if (a->control_possible) {
+    i64 lgq = (a->queue_upper + 1023) / 1024;  // ~1K list entries per CTA
+    int lg = (int)(lgq < 1 ? 1 : (lgq > nsm - 1 ? nsm - 1 : lgq));  // the walk keeps one SM
+    Tab t = a->tab;
+    Cfg c = a->cfg;
+    Work* w = a->work;
+    Bufs b = a->bufs;
+    Queue Q = a->queue;
+    Lsd L = a->qlsd;
+    mars_scalars* sc = a->sc;
+    i32* qsel = a->qsel;
+    Queue G = a->gq;
+    Xchg x = a->x;
+    int npass = a->queue_passes;
+    void* args[] = {&t, &c, &w, &b, &Q, &L, &sc, &qsel, &G, &x, &npass};
     mark(3, 0, s2);
-    k_pack_small<<<1, 1024, sort_smem_bytes(), s2>>>(a->work, a->queue, a->qlsd, a->sc, a->qsel,
-                                                     a->gq);
-    launches++;
+    cudaLaunchCooperativeKernel((const void*)k_control, dim3(lg), dim3(1024), args,
+                                sort_smem_bytes(), s2);
     mark(3, 1, s2);
-    if (a->queue_passes > 0) {
-      mark(6, 0, s2);
-      i64 lgq = (a->queue_upper + 1023) / 1024;  // ~1K list entries per CTA
-      int lg = (int)(lgq < 1 ? 1 : (lgq > nsm - 1 ? nsm - 1 : lgq));  // the walk keeps one SM
-      launch_lsd(a->qlsd, a->work, 0, a->queue_passes, lg, s2);
-      launches++;
-      mark(6, 1, s2);
-    }
-    i64 qb = 1;
-    while (qb < a->queue_upper) qb <<= 1;  // pow2 bucket: stable launch shape for graphs
-    int g_ap = (int)((qb + SCAN_TPB - 1) / SCAN_TPB);
-    if (g_ap > nsm - 1) g_ap = nsm - 1;  // leaves the walk's SM free
-    if (g_ap < 1) g_ap = 1;
-    mark(4, 0, s2);
-    k_admit_apply<<<g_ap, SCAN_TPB, 0, s2>>>(a->tab, a->cfg, a->work, a->bufs, a->queue, a->qlsd,
-                                             a->sc, a->qsel, a->gq, a->x);
-    mark(4, 1, s2);
     launches++;
   }
   if (side) cudaEventRecord(a->ev_join, s2);
