@@ -355,7 +355,8 @@ def main():
         ktimes.append(eng.kernel_times())
     eng.set_profiling(False)
     eng.set_graph(world == 1)
-    kernel_ms = {k: statistics.median([kt[k] for kt in ktimes]) for k in ktimes[0]}
+    kernel_ms = {k: statistics.median([kt[k] for kt in ktimes]) for k in ktimes[0]
+                 if all(kt[k] >= 0 for kt in ktimes)}  # launched kernels only
     scan_avg = sum(kt["k_scan"] for kt in ktimes) / len(ktimes)
 
     # e2e: through the C ABI with host buffers: upload the table from pinned

@@ -285,9 +285,9 @@ int mars_sync(mars_ctx* ctx);
 int mars_last_launch_count(mars_ctx* ctx);
 
 /* per-kernel device times of the last step, recorded with CUDA events on the
- * stream each kernel runs on: [scan, compact, expired-sort, pack, admit, walk,
- * pack-sort] in ms (-1 = not launched).  Profiling must be enabled before the step. */
-#define MARS_NUM_KTIMES 7
+ * stream each kernel runs on: [scan, expired-sort, control, walk] in ms
+ * (-1 = not launched).  Profiling must be enabled before the step. */
+#define MARS_NUM_KTIMES 4
 int mars_set_profiling(mars_ctx* ctx, int on);
 int mars_kernel_times(mars_ctx* ctx, float* ms, int n);   /* sync */
 

@@ -151,8 +151,7 @@ _SIGS = {
     "mars_kernel_times": (i32, [C.c_void_p, P(C.c_float), C.c_int]),
 }
 
-KTIME_NAMES = ("k_scan", "k_compact", "k_expired_sort", "k_pack", "k_admit_apply", "k_walk",
-               "k_pack_sort")
+KTIME_NAMES = ("k_scan", "k_expired_sort", "k_control", "k_walk")
 
 EXPORTS = tuple(_SIGS)
 

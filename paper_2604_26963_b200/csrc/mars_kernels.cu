@@ -2759,7 +2759,7 @@ int mars_enqueue_step(const LaunchArgs* a) {
     cudaStreamWaitEvent(s2, a->ev_fork, 0);
   }
   if (a->exp_sort || a->exp_may_be_big) {
-    mark(2, 0, s2);
+    mark(1, 0, s2);
     if (a->exp_sort) {
       k_exp_small<<<1, 1024, sort_smem_bytes(), s2>>>(a->work, a->bufs, a->xlsd);
       launches++;
@@ -2770,7 +2770,7 @@ int mars_enqueue_step(const LaunchArgs* a) {
       k_exp_gather<<<nsm, 256, 0, s2>>>(a->work, a->bufs, a->xlsd);
       launches++;
     }
-    mark(2, 1, s2);
+    mark(1, 1, s2);
   }
   if (a->control_possible) {
     i64 lgq = (a->queue_upper + 1023) / 1024;  // ~1K list entries per CTA
@@ -2787,21 +2787,21 @@ int mars_enqueue_step(const LaunchArgs* a) {
     Xchg x = a->x;
     int npass = a->queue_passes;
     void* args[] = {&t, &c, &w, &b, &Q, &L, &sc, &qsel, &G, &x, &npass};
-    mark(3, 0, s2);
+    mark(2, 0, s2);
     cudaLaunchCooperativeKernel((const void*)k_control, dim3(lg), dim3(1024), args,
                                 sort_smem_bytes(), s2);
-    mark(3, 1, s2);
+    mark(2, 1, s2);
     launches++;
   }
   if (side) cudaEventRecord(a->ev_join, s2);
-  mark(5, 0, s);
+  mark(3, 0, s);
   k_walk<<<1, WALK_TPB, walk_smem_bytes(), s>>>(a->tab, a->cfg, a->work, a->bufs, a->sc, n,
                                                 a->control_possible);
   if (a->kv) {
     mars_kv_enqueue_apply_step(*a->kv, s, a->work, a->bufs);
     launches++;
   }
-  mark(5, 1, s);
+  mark(3, 1, s);
   launches++;
   if (side) cudaStreamWaitEvent(s, a->ev_join, 0);
 #ifdef MARS_PHASE_TIMING
