@@ -31,6 +31,12 @@ def variant(n, seed, kind):
         pinned = (s.cols["flags"] & F_PINNED) != 0
         s.cols["deadline"][pinned] = s.now - 1.0
         return s
+    if kind == "expired_shuffled":
+        # session ids not in row order: the expired pins need the rank sort
+        # (> 4096 of them: the grid-wide LSD path)
+        s = variant(n, seed, "expired_big")
+        s.cols["rank"][:] = np.random.default_rng(seed).permutation(n).astype(np.uint32)
+        return s
     if kind == "no_queue_control":
         s = snapshot_v1(n, seed=seed, pool="headroom")
         q = s.queue

@@ -63,6 +63,7 @@ def test_step_matches_reference_golden(i):
     (30_000, 23, "first_fit"),
     (30_000, 24, "desc"),
     (150_000, 25, "expired_big"),
+    (150_000, 27, "expired_shuffled"),
     (20_000, 26, "no_queue_control"),
 ])
 def test_step_matches_oracle(n, seed, kind):
