@@ -178,8 +178,9 @@ typedef struct mars_step_out {
   const uint32_t *fin_rows; const uint8_t *fin_pin;
   const double *fin_benefit, *fin_cost, *fin_deadline;
   /* diagnostics: candidate counts at the exact thresholds, 1 if the walk
-   * left the prefix-sum fast path */
-  int32_t n_window_cand, n_victim_cand, walk_slow;
+   * left the prefix-sum fast path; how pack_queue sorted the list (0 not
+   * run, 1 grid LSD radix sort, 2 one CTA: small list or first fit) */
+  int32_t n_window_cand, n_victim_cand, walk_slow, sort_path;
 } mars_step_out;
 
 /* ---- lifecycle ------------------------------------------------------- */

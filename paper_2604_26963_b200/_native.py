@@ -105,6 +105,7 @@ class MarsStepOut(C.Structure):
         ("fin_rows", P(u32)), ("fin_pin", P(u8)), ("fin_benefit", P(f64)),
         ("fin_cost", P(f64)), ("fin_deadline", P(f64)),
         ("n_window_cand", i32), ("n_victim_cand", i32), ("walk_slow", i32),
+        ("sort_path", i32),
     ]
 
 

@@ -2,6 +2,7 @@
 // device allocation of the session-state store, uploads/downloads, the step.
 #include <cuda_runtime.h>
 #include <stdarg.h>
+#include <stdlib.h>
 #include <stdio.h>
 #include <string.h>
 
@@ -33,6 +34,7 @@ struct mars_ctx {
   mars_config hcfg;
   Cfg cfg;
   i64 max_rows = 0, max_queue = 0, n_rows = 0, alloc_rows = 0;
+  int ctl_per_cta = 1024;
   Tab tab;
   Queue queue;
   Lsd qlsd, xlsd;
@@ -217,6 +219,10 @@ int mars_create(const mars_config* hcfg, int device, int64_t max_rows, int64_t m
   ctx->max_rows = max_rows;
   ctx->alloc_rows = (max_rows + ROW_PAD - 1) / ROW_PAD * ROW_PAD;
   ctx->max_queue = max_queue < 1 ? 1 : max_queue;
+  {
+    const char* e = getenv("MARS_CTL_PER_CTA");  // tuning knob (graph key follows it)
+    ctx->ctl_per_cta = (e && atoi(e) > 0) ? atoi(e) : 1024;
+  }
   CK(cudaSetDevice(device));
   CK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
   CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
@@ -581,6 +587,7 @@ static LaunchArgs launch_args(mars_ctx* ctx, const mars_step_in* in) {
   a.num_sms = ctx->num_sms;
   a.control_possible = in->control_due ? 1 : 0;
   a.queue_upper = ctx->q_upper;
+  a.ctl_per_cta = ctx->ctl_per_cta;
   int passes = 0;
   if (ctx->q_upper > SORT_CAP) {
     unsigned mx = (unsigned)(ctx->q_maxreq > 0 ? ctx->q_maxreq : 1);
@@ -728,6 +735,7 @@ int mars_step_fetch(mars_ctx* ctx, mars_step_out* o) {
   o->n_window_cand = w.n_wc;
   o->n_victim_cand = w.n_vc;
   o->walk_slow = w.walk_slow;
+  o->sort_path = w.sort_path;
   o->fin_rows = (const uint32_t*)pull(ctx, off, b.fin_row, (size_t)w.n_finish * 4);
   o->fin_pin = (const uint8_t*)pull(ctx, off, b.fin_pin, (size_t)w.n_finish);
   o->fin_benefit = (const double*)pull(ctx, off, b.fin_b, (size_t)w.n_finish * 8);

@@ -133,6 +133,7 @@ struct Work {
   i32 n_queued_kv;  // queued rows holding KV (admission then touches reclaim state)
   u32 admit_done;   // set by k_control after admission; k_walk may wait on it
   i32 n_finish;
+  i32 sort_path;    // pack_queue: 1 grid LSD sort, 2 one CTA (mars_step_out.sort_path)
 };
 
 // variable-length step buffers

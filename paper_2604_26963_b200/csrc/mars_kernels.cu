@@ -567,6 +567,7 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
       }
     }
     __syncthreads();
+    if (rd < 7) PTIME(25 + rd);
   }
 
   // local thresholds: only bins at or below them can hold a global top-k key
@@ -1582,11 +1583,13 @@ __global__ void __launch_bounds__(1024, 1) k_control(Tab t, Cfg c, Work* w, Bufs
       w->min_req = mn;
       w->lsd_maxkey = a.maxkey;
     }
+    if (blockIdx.x == 0 && threadIdx.x == 0) w->sort_path = 1;
     cur = lsd_grid_sort(L, lsd_view(w, 0), a, npass, (u32(*)[256])smem);
     if (npass == 0) grid.sync();  // (no sort barrier to order the published mode)
   } else {
     // small queue, first fit, or a row-less queue: one CTA packs
     if (blockIdx.x == 0 && qlen > 0) pack_small_cta(w, Q, L, sc, qsel_p, G, smem);
+    if (blockIdx.x == 0 && threadIdx.x == 0 && qlen > 0) w->sort_path = w->lsd_big ? 1 : 2;
     grid.sync();
     cur = 0;
     if (npass > 0 && w->lsd_big)  // row-less big queue (reduced by pack_small_cta)
@@ -2748,32 +2751,40 @@ int mars_enqueue_step(const LaunchArgs* a) {
     k_build_global_queue<<<nsm, 256, 0, s>>>(a->work, a->x);
     launches += 2;
   }
-  // Side stream: the expired-pin rank sort (tables that are not rank-ordered)
-  // and the control plane (pack_queue sort, admission).  The walk runs
-  // concurrently on the main stream: it reads no state admission writes
-  // unless an admitted session can enter the window, and then waits for the
-  // admission's completion flag (k_walk, admit_async).
-  const bool side = a->exp_sort || a->exp_may_be_big || a->control_possible;
-  if (side) {
-    cudaEventRecord(a->ev_fork, s);
-    cudaStreamWaitEvent(s2, a->ev_fork, 0);
-  }
+  // The walk runs on the side stream, concurrently with the main stream's
+  // expired-pin rank sort (tables that are not rank-ordered) and control plane
+  // (pack_queue sort, admission): the control plane is the longer branch, and
+  // a kernel on the stream that launched k_scan starts sooner than one behind
+  // a fork event.  The two grid-wide (cooperative) kernels stay serialised on
+  // one stream; each leaves an SM for the walk.  The walk reads no state
+  // admission writes unless an admitted session can enter the window, and
+  // then waits for the admission's completion flag (k_walk, admit_async).
+  // The KV journal apply needs the walk's journal and the rank-ordered
+  // expired pins: after the join.
+  cudaEventRecord(a->ev_fork, s);
+  cudaStreamWaitEvent(s2, a->ev_fork, 0);
+  mark(3, 0, s2);
+  k_walk<<<1, WALK_TPB, walk_smem_bytes(), s2>>>(a->tab, a->cfg, a->work, a->bufs, a->sc, n,
+                                                 a->control_possible);
+  launches++;
+  mark(3, 1, s2);
+  cudaEventRecord(a->ev_join, s2);
   if (a->exp_sort || a->exp_may_be_big) {
-    mark(1, 0, s2);
+    mark(1, 0, s);
     if (a->exp_sort) {
-      k_exp_small<<<1, 1024, sort_smem_bytes(), s2>>>(a->work, a->bufs, a->xlsd);
+      k_exp_small<<<1, 1024, sort_smem_bytes(), s>>>(a->work, a->bufs, a->xlsd);
       launches++;
     }
     if (a->exp_may_be_big) {
-      launch_lsd(a->xlsd, a->work, 1, 4, nsm - 1, s2);  // the walk keeps one SM
+      launch_lsd(a->xlsd, a->work, 1, 4, nsm - 1, s);  // the walk keeps one SM
       launches++;
-      k_exp_gather<<<nsm, 256, 0, s2>>>(a->work, a->bufs, a->xlsd);
+      k_exp_gather<<<nsm, 256, 0, s>>>(a->work, a->bufs, a->xlsd);
       launches++;
     }
-    mark(1, 1, s2);
+    mark(1, 1, s);
   }
   if (a->control_possible) {
-    i64 lgq = (a->queue_upper + 1023) / 1024;  // ~1K list entries per CTA
+    i64 lgq = (a->queue_upper + a->ctl_per_cta - 1) / a->ctl_per_cta;  // list entries per CTA
     int lg = (int)(lgq < 1 ? 1 : (lgq > nsm - 1 ? nsm - 1 : lgq));  // the walk keeps one SM
     Tab t = a->tab;
     Cfg c = a->cfg;
@@ -2787,23 +2798,17 @@ int mars_enqueue_step(const LaunchArgs* a) {
     Xchg x = a->x;
     int npass = a->queue_passes;
     void* args[] = {&t, &c, &w, &b, &Q, &L, &sc, &qsel, &G, &x, &npass};
-    mark(2, 0, s2);
+    mark(2, 0, s);
     cudaLaunchCooperativeKernel((const void*)k_control, dim3(lg), dim3(1024), args,
-                                sort_smem_bytes(), s2);
-    mark(2, 1, s2);
+                                sort_smem_bytes(), s);
+    mark(2, 1, s);
     launches++;
   }
-  if (side) cudaEventRecord(a->ev_join, s2);
-  mark(3, 0, s);
-  k_walk<<<1, WALK_TPB, walk_smem_bytes(), s>>>(a->tab, a->cfg, a->work, a->bufs, a->sc, n,
-                                                a->control_possible);
+  cudaStreamWaitEvent(s, a->ev_join, 0);
   if (a->kv) {
     mars_kv_enqueue_apply_step(*a->kv, s, a->work, a->bufs);
     launches++;
   }
-  mark(3, 1, s);
-  launches++;
-  if (side) cudaStreamWaitEvent(s, a->ev_join, 0);
 #ifdef MARS_PHASE_TIMING
   k_ptime_dump<<<1, 1, 0, s>>>();
 #endif

@@ -21,6 +21,7 @@ struct LaunchArgs {
   int control_possible;  // the step may run the control plane
   int queue_passes;      // LSD passes needed for the largest queue key (0 = small only)
   i64 queue_upper;       // upper bound of the queue length at step start
+  int ctl_per_cta;       // admission-list entries per k_control CTA (grid sizing)
   int exp_sort;          // expired pins need a rank sort (table not rank-ordered)
   int exp_may_be_big;    // more than SORT_CAP pins may expire
   cudaEvent_t* prof;     // 2*MARS_NUM_KTIMES events, or null

@@ -271,7 +271,7 @@ class MarsEngine:
             total_tokens=o.total_tokens, free_after_expiry=o.free_after_expiry,
             free_blocks=o.free_blocks, limit=o.limit, slots=o.slots,
             diag={"n_window_cand": o.n_window_cand, "n_victim_cand": o.n_victim_cand,
-                  "walk_slow": o.walk_slow})
+                  "walk_slow": o.walk_slow, "sort_path": o.sort_path})
 
     def step(self, si: N.MarsStepIn) -> StepResult:
         self.enqueue(si)

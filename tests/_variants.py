@@ -37,6 +37,47 @@ def variant(n, seed, kind):
         s = variant(n, seed, "expired_big")
         s.cols["rank"][:] = np.random.default_rng(seed).permutation(n).astype(np.uint32)
         return s
+    if kind == "queue_shuffled":
+        # admission list order is persistent state, not row order
+        s = snapshot_v1(n, seed=seed, pool="headroom")
+        s.queue = np.random.default_rng(seed).permutation(s.queue).astype(np.uint32)
+        return partial_admission(s)
+    if kind == "queue_sorted":
+        # steady state: the residual list is already packed (ascending req),
+        # so every range-sort CTA finds its entries in one stretch of the list
+        s = snapshot_v1(n, seed=seed, pool="headroom")
+        q = s.queue
+        s.queue = q[np.argsort(s.cols["req_blocks"][q], kind="stable")].astype(np.uint32)
+        return partial_admission(s)
+    if kind == "hot_req":
+        # a few heavily repeated req values: hot histogram bins (LSD fallback)
+        s = snapshot_v1(n, seed=seed, pool="headroom")
+        reqs = np.random.default_rng(seed).choice([64, 4096], size=len(s.queue))
+        return set_queue_req(s, reqs)
+    if kind == "warm_req":
+        # five repeated values: each bin spans several range-sort CTAs
+        s = snapshot_v1(n, seed=seed, pool="headroom")
+        reqs = np.random.default_rng(seed).choice([64, 65, 500, 501, 4096], size=len(s.queue))
+        return partial_admission(set_queue_req(s, reqs))
+    if kind == "many_equal_req":
+        # repeated keys that stay under the hot-bin bound: boundary bins shared
+        # by neighbouring range-sort CTAs
+        s = snapshot_v1(n, seed=seed, pool="headroom")
+        reqs = np.random.default_rng(seed).integers(100, 160, size=len(s.queue))
+        return partial_admission(set_queue_req(s, reqs))
+    if kind == "wide_req":
+        # req_blocks beyond the histogram (LSD fallback), and the largest one
+        # a 262144-token context can have
+        s = snapshot_v1(n, seed=seed, pool="headroom")
+        reqs = s.cols["req_blocks"][s.queue].astype(np.int64)
+        reqs[:3] = [16384, 17407, 25000]
+        return set_queue_req(s, reqs)
+    if kind == "desc_sorted":
+        # descending pack (CPU overloaded) of an ascending-sorted list
+        s = variant(n, seed, "queue_sorted")
+        s.active_tools = s.worker_slots
+        s.telemetry = {"cpu_high_streak": 2}
+        return partial_admission(s, overloaded=True)
     if kind == "no_queue_control":
         s = snapshot_v1(n, seed=seed, pool="headroom")
         q = s.queue
@@ -45,3 +86,24 @@ def variant(n, seed, kind):
         s.queue = q[:0]
         return s
     raise ValueError(kind)
+
+
+def set_queue_req(snap, reqs):
+    """Give the queued sessions new first-round prefills (req_blocks = reqs)."""
+    q = snap.queue
+    reqs = np.asarray(reqs, dtype=np.int64)
+    snap.cols["req_blocks"][q] = reqs
+    snap.cols["r0_prefill"][q] = reqs * 16 - 3
+    long_ = reqs > 0.25 * snap.total_blocks
+    snap.cols["flags"][q] = (snap.cols["flags"][q] & ~np.uint8(F_LONG)) | np.where(
+        long_, F_LONG, 0).astype(np.uint8)
+    return snap
+
+
+def partial_admission(snap, overloaded=False):
+    """Admission window so that about a third of the list is admitted: the
+    residual list order (persistent state, control.py:190) is then checked."""
+    active = int(((snap.cols["flags"] & 1) != 0).sum())
+    w = active + len(snap.queue) // 3
+    snap.initial_window = float(2 * w if overloaded else w)  # AIMD halves it under overload
+    return snap

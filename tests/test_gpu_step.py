@@ -26,7 +26,7 @@ pytestmark = pytest.mark.gpu
 SNAP = json.load(open(os.path.join(GOLDEN, "snapshot_steps.json")))
 
 
-def device_step(snap, control_due=True, **flags):
+def device_step(snap, control_due=True, sort_path=None, **flags):
     eng = MarsEngine(max_rows=snap.n, max_queue=max(len(snap.queue), 1),
                      config=make_config(**flags, initial_window=snap.initial_window))
     eng.load_snapshot(snap)
@@ -36,6 +36,8 @@ def device_step(snap, control_due=True, **flags):
     out = canonical(res, eng, snap, control_due)
     eng.close()
     assert res.status == 0, res.status
+    if sort_path is not None:
+        assert res.diag["sort_path"] == sort_path, res.diag
     return out
 
 
@@ -57,6 +59,13 @@ def test_step_matches_reference_golden(i):
         assert got[k] == v, k
 
 
+# how pack_queue's sort must run: 1 grid-wide LSD radix sort (big list), 2 one
+# CTA (small list, or the first-fit mode)
+SORT_PATH = {"headroom": 1, "pressure": 1, "first_fit": 2, "desc": 2, "queue_shuffled": 1,
+             "queue_sorted": 1, "hot_req": 1, "many_equal_req": 1, "warm_req": 1,
+             "wide_req": 1, "desc_sorted": 1}
+
+
 @pytest.mark.parametrize("n,seed,kind", [
     (100_000, 21, "headroom"),
     (100_000, 22, "pressure"),
@@ -65,10 +74,17 @@ def test_step_matches_reference_golden(i):
     (150_000, 25, "expired_big"),
     (150_000, 27, "expired_shuffled"),
     (20_000, 26, "no_queue_control"),
+    (200_000, 28, "queue_shuffled"),
+    (200_000, 29, "queue_sorted"),
+    (100_000, 30, "hot_req"),
+    (100_000, 33, "many_equal_req"),
+    (100_000, 36, "warm_req"),
+    (60_000, 34, "wide_req"),
+    (60_000, 35, "desc_sorted"),
 ])
 def test_step_matches_oracle(n, seed, kind):
     snap = variant(n, seed, kind)
-    assert_same(device_step(snap.copy()), run_step(snap.copy()))
+    assert_same(device_step(snap.copy(), sort_path=SORT_PATH.get(kind)), run_step(snap.copy()))
 
 
 @pytest.mark.parametrize("flags", [dict(enable_coordinator=False), dict(enable_coscheduler=False)])
