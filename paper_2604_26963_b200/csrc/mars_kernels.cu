@@ -631,14 +631,32 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
   PTIME(2);
 
   // ---- phase 2 ---------------------------------------------------------------
-  // global thresholds over the exact prefix of the merged histograms
+  // Every load that does not depend on another is issued at once: the CTA
+  // thresholds' minimum, the expiry totals and, speculatively, the low half of
+  // both merged histograms (the thresholds almost always fall there: the
+  // window top-k sits at level 0, the victim top-k among the pinned rows).
   const u32 tmw = __ldcg(&w->tmin_win), tmv = __ldcg(&w->tmin_vic);
   const int tile_cnt_g = (int)threadIdx.x < (int)gridDim.x ? __ldcg(&b.tile_cnt[threadIdx.x]) : 0;
+  const unsigned long long exp_total = __ldcg(&w->exp_blocks);
+  {
+    constexpr int HALF = HIST_BINS / 2 / SCAN_TPB;
+    u32 xw[HALF], xv[HALF];
 #pragma unroll
-  for (int q = 0; q < HIST_BINS / SCAN_TPB; ++q) {
-    const int i = q * SCAN_TPB + threadIdx.x;
-    hw[i] = (i <= (int)tmw) ? __ldcg(&w->hist_win[i]) : 0u;
-    hv[i] = (i <= (int)tmv) ? __ldcg(&w->hist_vic[i]) : 0u;
+    for (int q = 0; q < HALF; ++q) {
+      xw[q] = __ldcg(&w->hist_win[q * SCAN_TPB + threadIdx.x]);
+      xv[q] = __ldcg(&w->hist_vic[q * SCAN_TPB + threadIdx.x]);
+    }
+#pragma unroll
+    for (int q = 0; q < HIST_BINS / SCAN_TPB; ++q) {
+      const int i = q * SCAN_TPB + threadIdx.x;
+      if (q < HALF) {
+        hw[i] = (i <= (int)tmw) ? xw[q] : 0u;
+        hv[i] = (i <= (int)tmv) ? xv[q] : 0u;
+      } else {
+        hw[i] = (i <= (int)tmw) ? __ldcg(&w->hist_win[i]) : 0u;
+        hv[i] = (i <= (int)tmv) ? __ldcg(&w->hist_vic[i]) : 0u;
+      }
+    }
   }
   __syncthreads();
   int gw, gv;
@@ -649,7 +667,6 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
 
   // the probe's view after the expiry evictions (telemetry.py:152-158): the
   // usage S2 prices retention with
-  const unsigned long long exp_total = __ldcg(&w->exp_blocks);
   const i64 freeb = sc_free + (i64)exp_total;
   const double usage =
       (mode & MARS_MODE_SKIP_PROBE) ? sc_usage : (double)(sc_total - freeb) / (double)sc_total;
@@ -669,22 +686,22 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
       s_a[wid] = as;
     }
     __syncthreads();
-    exp_off = 0;
-    n_exp_all = 0;
-#pragma unroll
-    for (int q = 0; q < SCAN_TPB / 32; ++q) {
-      exp_off += s_b[q];
-      n_exp_all += s_a[q];
-    }
+    exp_off = __reduce_add_sync(FULL, s_b[lane]);
+    n_exp_all = __reduce_add_sync(FULL, s_a[lane]);
   }
   PTIME(3);
 
   // candidates at the exact thresholds, S2 retention of boundary rows and the
   // expired pins, from the digit record.  Each thread owns a contiguous run of
   // rows (thread order == row order, as the expired list needs):
-  // (A) per-thread counts, one block scan, one global atomic per unordered
-  // list; (B) row ids straight into the output lists; (C) one thread per
-  // emitted entry reads its row's columns -- all the entries' loads in flight.
+  // (A) per-thread counts, one block scan -> CTA-local list offsets; thread 0
+  //     issues the global list reservations (their results are first needed
+  //     in (D), so the atomics' round trip overlaps (C));
+  // (B) the row ids into CTA-local lists (shared memory, the free TMA ring);
+  // (C) one thread per entry gathers its row's columns and stages the record;
+  // (D) the records and row ids go to the global lists.
+  // A CTA with more entries than the staging area holds takes the unstaged
+  // path (row ids straight to the global lists, re-read for the gathers).
   {
     __shared__ unsigned long long s_scan[32];
     __shared__ u32 s_escan[32];
@@ -735,41 +752,83 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
       s_scan[lane] = v;
       s_escan[lane] = e;
       if (lane == 31) {
-        const int nw = (int)(v & FM), nv = (int)((v >> FB) & FM), nb = (int)(v >> (2 * FB));
-        s_tot[0] = nw;
-        s_tot[1] = nv;
-        s_tot[2] = nb;
+        s_tot[0] = (int)(v & FM);
+        s_tot[1] = (int)((v >> FB) & FM);
+        s_tot[2] = (int)(v >> (2 * FB));
         s_tot[3] = (int)e;
-        s_base[0] = nw ? atomicAdd(&w->n_wc, nw) : 0;
-        s_base[1] = nv ? atomicAdd(&w->n_vc, nv) : 0;
-        s_base[2] = nb ? atomicAdd(&w->n_ret, nb) : 0;
       }
     }
     __syncthreads();
     const int nw = s_tot[0], nv = s_tot[1], nb = s_tot[2], ne = s_tot[3];
-    const int bw = s_base[0], bv = s_base[1], bb = s_base[2];
+    const int ntot = nw + nv + nb + ne;
     const bool ro = (mode & MARS_MODE_RANK_ORDERED) != 0;
     u32* exp_rows = ro ? b.exp_row_sorted : b.exp_row;
+    // staging: CTA-local row lists (4 B) + one 32-byte record per entry
+    constexpr int STAGE_REC = 32;
+    const bool staged = ((((size_t)ntot * 4 + 15) & ~(size_t)15) + (size_t)ntot * STAGE_REC) <=
+                        (size_t)SCAN_NBUF * SB_BYTES;
+    u32* lrow = (u32*)sdyn;                                       // [ntot]
+    unsigned char* rec = sdyn + (((size_t)ntot * 4 + 15) & ~(size_t)15);  // [ntot][32]
+    // (A') global list reservations, issued now, consumed in (D)
+    int gb0 = 0, gb1 = 0, gb2 = 0;
+    if (threadIdx.x == 0) {
+      gb0 = nw ? atomicAdd(&w->n_wc, nw) : 0;
+      gb1 = nv ? atomicAdd(&w->n_vc, nv) : 0;
+      gb2 = nb ? atomicAdd(&w->n_ret, nb) : 0;
+      if (!staged) {
+        s_base[0] = gb0;
+        s_base[1] = gb1;
+        s_base[2] = gb2;
+      }
+    }
+    if (!staged) __syncthreads();
+    // (B) row ids: local lists (staged) or the global lists
     if (cnt | ecnt) {
       const unsigned long long ex = incl - cnt + (wid ? s_scan[wid - 1] : 0ull);
-      int pw = bw + (int)(ex & FM), pv = bv + (int)((ex >> FB) & FM), pr = bb + (int)(ex >> (2 * FB));
-      int pe = exp_off + (int)(eincl - ecnt + (wid ? s_escan[wid - 1] : 0u));
+      int pw = (int)(ex & FM), pv = nw + (int)((ex >> FB) & FM);
+      int pr = nw + nv + (int)(ex >> (2 * FB));
+      int pe = nw + nv + nb + (int)(eincl - ecnt + (wid ? s_escan[wid - 1] : 0u));
+      if (!staged) {
+        pw += s_base[0];
+        pv += s_base[1] - nw;
+        pr += s_base[2] - nw - nv;
+        pe += exp_off - nw - nv - nb;
+      }
       for (i64 i = r0; i < r1; ++i) {
         const u32 rc = dig[i];
         const u32 rw = rc & 0xffffu, rv = rc >> 16;
         const u32 r = (u32)(cs + i);
-        if ((rw & ~DIG_BND) <= (u32)gw) b.wc_row[pw++] = r;
-        if (rv <= (u32)gv) b.vc_row[pv++] = r;
-        if (rw & DIG_BND) b.ret_row[pr++] = r;
-        if (rv == DIG_EXP) exp_rows[pe++] = r;
+        if (staged) {
+          if ((rw & ~DIG_BND) <= (u32)gw) lrow[pw++] = r;
+          if (rv <= (u32)gv) lrow[pv++] = r;
+          if (rw & DIG_BND) lrow[pr++] = r;
+          if (rv == DIG_EXP) lrow[pe++] = r;
+        } else {
+          if ((rw & ~DIG_BND) <= (u32)gw) b.wc_row[pw++] = r;
+          if (rv <= (u32)gv) b.vc_row[pv++] = r;
+          if (rw & DIG_BND) b.ret_row[pr++] = r;
+          if (rv == DIG_EXP) exp_rows[pe++] = r;
+        }
       }
     }
     __syncthreads();
-    for (int k = threadIdx.x; k < nw + nv + nb + ne; k += blockDim.x) {
+    // (C) gathers; staged: records in shared memory, else straight to global
+    for (int k = threadIdx.x; k < ntot; k += blockDim.x) {
+      u32 r;
+      if (staged) {
+        r = lrow[k];
+      } else if (k < nw) {
+        r = __ldcg(&b.wc_row[s_base[0] + k]);
+      } else if (k < nw + nv) {
+        r = __ldcg(&b.vc_row[s_base[1] + k - nw]);
+      } else if (k < nw + nv + nb) {
+        r = __ldcg(&b.ret_row[s_base[2] + k - nw - nv]);
+      } else {
+        r = __ldcg(&exp_rows[exp_off + k - nw - nv - nb]);
+      }
+      unsigned char* R = rec + (size_t)k * STAGE_REC;
       if (k < nw + nv) {
         const bool is_w = k < nw;
-        const int slot = is_w ? bw + k : bv + (k - nw);
-        const u32 r = is_w ? __ldcg(&b.wc_row[slot]) : __ldcg(&b.vc_row[slot]);
         const bool ready = (dig[(i64)r - cs] & DIG_NONE) == 0;
         const u32 rk = t.rank[r];
         u64 whi = 0, wlo = 0;
@@ -779,8 +838,13 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
           window_key(lv, tt, rk, whi, wlo);
         }
         if (is_w) {
-          b.wc_hi[slot] = whi;
-          b.wc_lo[slot] = wlo;
+          if (staged) {
+            ((u64*)R)[0] = whi;
+            ((u64*)R)[1] = wlo;
+          } else {
+            b.wc_hi[s_base[0] + k] = whi;
+            b.wc_lo[s_base[0] + k] = wlo;
+          }
         } else {
           u64 vk;
           i32 blk;
@@ -794,29 +858,76 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
             vk = victim_key(false, nonexp, (u32)t.plevel[r], pbk, rk);
             blk = pbk;
           }
-          b.vc_key[slot] = vk;
-          b.vc_whi[slot] = whi;
-          b.vc_wlo[slot] = wlo;
-          b.vc_blk[slot] = blk;
+          if (staged) {
+            ((u64*)R)[0] = vk;
+            ((u64*)R)[1] = whi;
+            ((u64*)R)[2] = wlo;
+            ((i32*)R)[6] = blk;
+          } else {
+            const int slot = s_base[1] + k - nw;
+            b.vc_key[slot] = vk;
+            b.vc_whi[slot] = whi;
+            b.vc_wlo[slot] = wlo;
+            b.vc_blk[slot] = blk;
+          }
         }
       } else if (k < nw + nv + nb) {
-        const int slot = bb + (k - nw - nv);
-        const u32 r = __ldcg(&b.ret_row[slot]);
         u8 pin;
         double rb_, rc_, rd_;
         decide_retention(c, t.ctx[r], t.kv[r], sc_total, usage, ema, now, pin, rb_, rc_, rd_);
-        b.ret_pin[slot] = pin;
-        b.ret_b[slot] = rb_;
-        b.ret_c[slot] = rc_;
-        b.ret_d[slot] = rd_;
+        if (staged) {
+          ((double*)R)[0] = rb_;
+          ((double*)R)[1] = rc_;
+          ((double*)R)[2] = rd_;
+          R[24] = pin;
+        } else {
+          const int slot = s_base[2] + k - nw - nv;
+          b.ret_pin[slot] = pin;
+          b.ret_b[slot] = rb_;
+          b.ret_c[slot] = rc_;
+          b.ret_d[slot] = rd_;
+        }
       } else {  // expired pin: its blocks (and rank, for the rank sort)
-        const int slot = exp_off + (k - nw - nv - nb);
-        const u32 r = __ldcg(&exp_rows[slot]);
+        const int slot = exp_off + k - nw - nv - nb;
         if (ro) {
           b.exp_blk_sorted[slot] = t.pb[r];
         } else {
           b.exp_blk[slot] = t.pb[r];
           b.exp_rank[slot] = t.rank[r];
+        }
+        if (staged) exp_rows[slot] = r;
+      }
+    }
+    if (staged) {
+      if (threadIdx.x == 0) {  // the reservations' results, first use
+        s_base[0] = gb0;
+        s_base[1] = gb1;
+        s_base[2] = gb2;
+      }
+      __syncthreads();
+      // (D) staged records and row ids -> the global lists
+      const int bw = s_base[0], bv = s_base[1], bb = s_base[2];
+      for (int k = threadIdx.x; k < nw + nv + nb; k += blockDim.x) {
+        const u32 r = lrow[k];
+        const unsigned char* R = rec + (size_t)k * STAGE_REC;
+        if (k < nw) {
+          b.wc_row[bw + k] = r;
+          b.wc_hi[bw + k] = ((const u64*)R)[0];
+          b.wc_lo[bw + k] = ((const u64*)R)[1];
+        } else if (k < nw + nv) {
+          const int slot = bv + k - nw;
+          b.vc_row[slot] = r;
+          b.vc_key[slot] = ((const u64*)R)[0];
+          b.vc_whi[slot] = ((const u64*)R)[1];
+          b.vc_wlo[slot] = ((const u64*)R)[2];
+          b.vc_blk[slot] = ((const i32*)R)[6];
+        } else {
+          const int slot = bb + k - nw - nv;
+          b.ret_row[slot] = r;
+          b.ret_b[slot] = ((const double*)R)[0];
+          b.ret_c[slot] = ((const double*)R)[1];
+          b.ret_d[slot] = ((const double*)R)[2];
+          b.ret_pin[slot] = R[24];
         }
       }
     }
