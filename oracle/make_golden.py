@@ -11,6 +11,8 @@ run time) and writes under ``tests/golden/``:
 * ``sim_logs.json``            -- for every (trace, policy variant): record
   count + SHA-256 of the reference ``run_simulation`` event log serialised the
   way ``EventLog.dump_jsonl`` does (engine.py:95-98), plus the counters.
+* ``sim_logs_baselines.json``  -- the same for the reference's comparison
+  policies (fcfs, program_priority, static_ttl, dynamic_ttl) on four traces.
 * ``snapshot_steps.json``      -- canonical outputs of one scheduling step
   computed with the reference's own objects/functions on small
   ``snapshot_v1`` instances (headroom, pressure, coordinator-off,
@@ -135,6 +137,34 @@ def freeze_sims(A, out):
                              horizon_s=res.horizon_s)
             print(f"  {key}: {len(res.events)} records")
     out["sim_logs.json"] = logs
+
+
+BASELINE_KINDS = ("fcfs", "program_priority", "static_ttl", "dynamic_ttl")
+BASELINE_TRACES = ("small12", "demo64", "crit7_80", "faceoff200")
+
+
+def freeze_baseline_sims(A, out):
+    """The reference's four comparison policies (baselines.py:108-315) on the
+    frozen traces: record count, SHA-256 and counters of each event log."""
+    logs = {}
+    for name, traces, pkw, rkw in sim_cases(A):
+        if name not in BASELINE_TRACES:
+            continue
+        path = os.path.join(GOLDEN, "traces", f"{name}.jsonl")
+        for kind in BASELINE_KINDS:
+            kw = dict(rkw)
+            if "controller" in kw:
+                kw["controller"] = A.ControllerConfig(**kw["controller"])
+            res = A.run_simulation(A.load_trace(path), A.EngineParams(**pkw),
+                                   A.make_policy(kind), **kw)
+            key = f"{name}/{kind}"
+            logs[key] = dict(trace=f"traces/{name}.jsonl", engine=pkw,
+                             run={k: (v2 if k != "controller" else rkw["controller"])
+                                  for k, v2 in kw.items()},
+                             policy=kind, records=len(res.events), sha256=_sha(res.events),
+                             counters=res.counters, horizon_s=res.horizon_s)
+            print(f"  {key}: {len(res.events)} records")
+    out["sim_logs_baselines.json"] = logs
 
 
 # ---------------------------------------------------------------------------
@@ -530,6 +560,8 @@ def main(argv=None):
     only = set(filter(None, a.only.split(",")))
     if not only or "sims" in only:
         freeze_sims(A, out)
+    if not only or "baselines" in only:
+        freeze_baseline_sims(A, out)
     if not only or "snapshots" in only:
         freeze_snapshots(A, out)
     if not only or "kat" in only:

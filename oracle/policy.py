@@ -371,3 +371,184 @@ class MarsOracle:
                          self.mlfq.max_decode_slots, self.enable_coscheduler,
                          self._reclaimer(ready, now, pool), evictor,
                          window_out=self.last_window)
+
+
+# ---------------------------------------------------------------------------
+# Comparison policies (baselines.py:104-315) sharing the same plan builder
+# ---------------------------------------------------------------------------
+
+K_STATIC_TTL_S = 30.0          # baselines.py:50
+K_DYNAMIC_TTL_MULTIPLIER = 1.5  # baselines.py:51
+
+
+def arrival_key(s) -> tuple:  # baselines.py:104-105
+    return (s.arrival_time, s.session_id)
+
+
+def _prefix_victims(cands: Sequence[Session], need: int, pool: BlockCounter,
+                    chosen: Optional[List[Victim]] = None, freed: int = 0) -> List[Victim]:
+    """Shortest prefix of running candidates whose blocks cover the shortfall,
+    else [] (baselines.py:129-138)."""
+    chosen = list(chosen or [])
+    for c in cands:
+        b = c.held_blocks(pool.block_size)
+        chosen.append(Victim(c.session_id, "running", b))
+        freed += b
+        if pool.free_blocks + freed >= need:
+            return chosen
+    return []
+
+
+class _BaselineOracle:
+    """PolicyBase defaults (baselines.py:56-101): no admission control, no pins."""
+
+    name = "base"
+    uses_admission_control = False
+    strict_order = False
+
+    def __init__(self, window_size: int = 128, max_decode_slots: int = DECODE_SLOTS) -> None:
+        self.window_size = window_size
+        self.max_decode_slots = max_decode_slots
+        self.calls: Dict[str, Session] = {}
+        self.last_window: List[Session] = []
+
+    def register_call(self, call) -> None:
+        self.calls[call.session_id] = call
+
+    def on_admit(self, call, now: float) -> None:
+        pass
+
+    def on_resume(self, call, now: float) -> None:
+        pass
+
+    def on_service(self, sid: str, tokens: int, now: float) -> None:
+        pass
+
+    def retention_decision(self, call, pool, telemetry, gpu, now):
+        return None
+
+    def note_pin(self, call, decision, blocks: int, now: float) -> None:
+        pass
+
+    def expired_pins(self, now: float) -> List[str]:
+        return []
+
+    def on_evicted(self, sid: str) -> None:
+        pass
+
+    def order_key(self, call) -> tuple:
+        return arrival_key(call)
+
+    def _running(self, ready, who, planned, bs):
+        raise NotImplementedError
+
+    def _reclaimer(self, ready: Sequence[Session], now: float, pool: BlockCounter):
+        def pick(need: int, who, planned: Sequence[str]) -> List[Victim]:
+            return _prefix_victims(self._running(ready, who, planned, pool.block_size), need, pool)
+        return pick
+
+    def plan_tick(self, ready, pool, gpu, telemetry, now, evictor) -> Plan:
+        self.last_window = []
+        return make_plan(ready, pool, gpu, self.order_key, self.window_size,
+                         self.max_decode_slots, False, self._reclaimer(ready, now, pool), evictor,
+                         strict_order=self.strict_order, window_out=self.last_window)
+
+
+class FcfsOracle(_BaselineOracle):
+    """FcfsPolicy (baselines.py:108-155): arrival order, head-of-line blocking,
+    victims are later arrivals, latest first."""
+
+    name = "fcfs"
+    strict_order = True
+
+    def _running(self, ready, who, planned, bs):
+        c = [s for s in ready if s.session_id != who.session_id and s.session_id not in planned
+             and s.arrival_time > who.arrival_time and s.held_blocks(bs) > 0]
+        c.sort(key=lambda s: (-s.arrival_time, s.session_id))
+        return c
+
+
+class ProgramPriorityOracle(_BaselineOracle):
+    """ProgramPriorityPolicy (baselines.py:158-208): least cumulative service
+    first; victims have more service, most first."""
+
+    name = "program_priority"
+
+    def order_key(self, call) -> tuple:
+        return (call.served_tokens, call.arrival_time, call.session_id)
+
+    def _running(self, ready, who, planned, bs):
+        c = [s for s in ready if s.session_id != who.session_id and s.session_id not in planned
+             and s.served_tokens > who.served_tokens and s.held_blocks(bs) > 0]
+        c.sort(key=lambda s: (-s.served_tokens, s.session_id))
+        return c
+
+
+class TtlOracle(_BaselineOracle):
+    """TtlPolicy (baselines.py:211-315): fcfs order plus unconditional pins
+    with a static or EMA-scaled deadline; pins are reclaimed first (expired,
+    then earliest deadline, then largest), then later arrivals."""
+
+    strict_order = True
+
+    def __init__(self, kind: str, pressure: Optional[Pressure] = None,
+                 ttl_seconds: float = K_STATIC_TTL_S, multiplier: float = K_DYNAMIC_TTL_MULTIPLIER,
+                 window_size: int = 128, max_decode_slots: int = DECODE_SLOTS) -> None:
+        super().__init__(window_size, max_decode_slots)
+        if kind not in ("static_ttl", "dynamic_ttl"):
+            raise ValueError(kind)
+        self.name = kind
+        self.pressure = pressure or Pressure()
+        self.ttl_seconds = ttl_seconds
+        self.multiplier = multiplier
+        self.pinned: Dict[str, Pin] = {}
+
+    def retention_decision(self, call, pool, telemetry, gpu, now):
+        if self.name == "static_ttl":
+            deadline = now + self.ttl_seconds
+        else:
+            deadline = now + self.multiplier * telemetry.effective_tool_estimate(self.pressure)
+        return Decision(True, 0.0, 0.0, deadline)
+
+    def note_pin(self, call, decision, blocks: int, now: float) -> None:
+        self.pinned[call.session_id] = Pin(call.session_id, blocks, now,
+                                           decision.retention_deadline,
+                                           decision.retention_deadline, 0)
+
+    def expired_pins(self, now: float) -> List[str]:
+        return sorted(sid for sid, ps in self.pinned.items() if ps.retention_deadline < now)
+
+    def on_evicted(self, sid: str) -> None:
+        self.pinned.pop(sid, None)
+
+    def _reclaimer(self, ready: Sequence[Session], now: float, pool: BlockCounter):
+        def pick(need: int, who, planned: Sequence[str]) -> List[Victim]:
+            chosen: List[Victim] = []
+            freed = 0
+            pins = sorted(self.pinned.values(),
+                          key=lambda ps: (0 if ps.retention_deadline < now else 1,
+                                          ps.retention_deadline, -ps.pinned_blocks, ps.session_id))
+            for ps in pins:
+                chosen.append(Victim(ps.session_id, "pinned", ps.pinned_blocks))
+                freed += ps.pinned_blocks
+                if pool.free_blocks + freed >= need:
+                    return chosen
+            run = [s for s in ready if s.session_id != who.session_id
+                   and s.session_id not in planned and s.arrival_time > who.arrival_time
+                   and s.held_blocks(pool.block_size) > 0]
+            run.sort(key=lambda s: (-s.arrival_time, s.session_id))
+            return _prefix_victims(run, need, pool, chosen, freed)
+        return pick
+
+
+def make_oracle_policy(kind: str, **kw):
+    """make_policy (baselines.py:458-495) over the oracle policies."""
+    if kind == "mars":
+        return MarsOracle(**kw)
+    if kind == "fcfs":
+        return FcfsOracle(**kw)
+    if kind == "program_priority":
+        return ProgramPriorityOracle(**kw)
+    if kind in ("static_ttl", "dynamic_ttl"):
+        return TtlOracle(kind, **kw)
+    raise ValueError(kind)

@@ -31,6 +31,7 @@ SIM = _load("sim_logs.json")
 SNAP = _load("snapshot_steps.json")
 KAT = _load("kat.json")
 
+from tests._sim import SIM_BASE
 from tests._sim import run_sim as run_oracle_sim
 
 
@@ -41,6 +42,14 @@ def test_oracle_sim_log_is_byte_identical_to_reference(key):
     assert len(out.events) == SIM[key]["records"]
     assert got == SIM[key]["sha256"]
     assert out.counters == SIM[key]["counters"]
+
+
+@pytest.mark.parametrize("key", sorted(SIM_BASE))
+def test_oracle_baseline_policy_log_is_byte_identical_to_reference(key):
+    out = run_oracle_sim(key)
+    assert len(out.events) == SIM_BASE[key]["records"]
+    assert hashlib.sha256(out.log.jsonl_bytes()).hexdigest() == SIM_BASE[key]["sha256"]
+    assert out.counters == SIM_BASE[key]["counters"]
 
 
 @pytest.mark.parametrize("i", range(len(SNAP)))
