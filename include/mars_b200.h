@@ -36,7 +36,7 @@ extern "C" {
 #define MARS_ERR_CAPACITY 3
 #define MARS_ERR_ARG 4
 
-#define MARS_ABI_VERSION 1
+#define MARS_ABI_VERSION 2
 
 /* phase codes: agentsched/engine.py:250-256 */
 #define MARS_WAITING_ADMISSION 0
@@ -95,7 +95,22 @@ typedef struct mars_config {
   double long_session_fraction;                 /* control.py:27 */
   int32_t enable_coordinator;                   /* baselines.py:339 */
   int32_t enable_coscheduler;                   /* baselines.py:340 */
+  /* which policy the step runs (POLICY_KINDS, baselines.py:48): MARS, or one
+   * of the comparison policies on the same build_plan walk
+   * (baselines.py:108-315).  The comparison policies order the window by
+   * arrival (fcfs, ttl) or by (served_tokens, arrival) (program_priority,
+   * the `served` column then holding Call.served_tokens), never age, fit
+   * whole chunks, and fcfs/ttl block at the head of line. */
+  int32_t policy;                               /* MARS_POLICY_* */
+  double ttl_seconds;                           /* static_ttl deadline, baselines.py:50 */
+  double ttl_multiplier;                        /* dynamic_ttl x EMA tool time, :51 */
 } mars_config;
+
+#define MARS_POLICY_MARS 0
+#define MARS_POLICY_FCFS 1
+#define MARS_POLICY_PROGRAM_PRIORITY 2
+#define MARS_POLICY_STATIC_TTL 3
+#define MARS_POLICY_DYNAMIC_TTL 4
 
 /* Structure-of-arrays column pointers (host side).  NULL = column not
  * transferred.  Widths are the minimal exact widths of the reference values

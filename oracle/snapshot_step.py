@@ -28,7 +28,7 @@ import numpy as np
 from . import admission as adm
 from .core import (DECODE, PREFILL, BlockCounter, Journal, Round, Session, TickModel,
                    ceil_div, submit_round)
-from .policy import MarsOracle, Mlfq, Pin, Prio, Retention, retention
+from .policy import MarsOracle, Mlfq, Pin, Prio, Retention, make_oracle_policy, retention
 
 PHASES = ("waiting_admission", "prefill", "decode", "tool", "waiting_resume", "done")
 PHASE_CODE = {p: i for i, p in enumerate(PHASES)}
@@ -45,14 +45,21 @@ class World:
     def __init__(self, snap, enable_coordinator=True, enable_coscheduler=True,
                  mlfq: Optional[Mlfq] = None, controller: Optional[adm.Controller] = None,
                  pressure: Optional[adm.Pressure] = None,
-                 ret: Optional[Retention] = None) -> None:
+                 ret: Optional[Retention] = None, policy: str = "mars") -> None:
         c = snap.cols
         n = snap.n
         self.snap = snap
-        self.policy = MarsOracle(mlfq=mlfq, ret=ret, pressure=pressure,
-                                 enable_coordinator=enable_coordinator,
-                                 enable_coscheduler=enable_coscheduler)
-        self.pressure = self.policy.pressure
+        self.kind = policy
+        if policy == "mars":
+            self.policy = MarsOracle(mlfq=mlfq, ret=ret, pressure=pressure,
+                                     enable_coordinator=enable_coordinator,
+                                     enable_coscheduler=enable_coscheduler)
+        elif policy in ("static_ttl", "dynamic_ttl"):
+            self.policy = make_oracle_policy(policy, pressure=pressure)
+        else:  # fcfs / program_priority: no pins, no MLFQ state; `served` is
+            # Call.served_tokens (baselines.py:170-171)
+            self.policy = make_oracle_policy(policy)
+        self.pressure = getattr(self.policy, "pressure", None) or pressure or adm.Pressure()
         self.pool = BlockCounter(snap.total_blocks)
         self.gpu = TickModel()
         self.tel = adm.Counters(snap.total_blocks)
@@ -103,13 +110,17 @@ class World:
             f = fl[i]
             if f & F_ACTIVE:
                 self.active[sid] = s
-                self.policy.states[sid] = Prio(lv[i], lv[i], sv[i], ws[i], pr[i])
+                if policy == "mars":
+                    self.policy.states[sid] = Prio(lv[i], lv[i], sv[i], ws[i], pr[i])
+                else:
+                    s.served_tokens = sv[i]
             if f & F_PINNED:
                 s.pinned = True
                 s.retention_deadline = dl[i]
                 pinned[sid] = pb[i]
                 used += pb[i]
-                self.policy.pinned[sid] = Pin(sid, pb[i], 0.0, 0.0, dl[i], plv[i])
+                if hasattr(self.policy, "pinned"):
+                    self.policy.pinned[sid] = Pin(sid, pb[i], 0.0, 0.0, dl[i], plv[i])
             elif kv[i] > 0:
                 h = ceil_div(kv[i], 16)
                 alloc[sid] = h
@@ -200,7 +211,12 @@ def run_step(snap, control_due: bool = True, world: Optional[World] = None, **kw
     # 4. S2 retention on boundary rows
     ret = []
     for r in w.boundary:
-        d = retention(w.sessions[r], tel, pool, w.gpu, pol.retention, w.pressure, now)
+        if w.kind == "mars":
+            d = retention(w.sessions[r], tel, pool, w.gpu, pol.retention, w.pressure, now)
+        else:  # the policy's own rule; None = never pin (baselines.py:82-86)
+            d = pol.retention_decision(w.sessions[r], pool, tel, w.gpu, now)
+            if d is None:
+                continue
         ret.append((r, d.pin, d.benefit_s, d.cost_s, d.retention_deadline))
     # 5. plan
     ready = [s for s in w.active.values() if s.phase in (PREFILL, DECODE)]
@@ -254,7 +270,7 @@ def extract_state(w: World) -> Dict[str, np.ndarray]:
         if s.session_id in w.pool.pinned:
             f |= F_PINNED
         st["flags"][i] = f
-        p = w.policy.states.get(s.session_id)
+        p = getattr(w.policy, "states", {}).get(s.session_id)
         if p is not None:
             st["level"][i], st["promos"][i] = p.level, p.promotions
             st["wait_since"][i], st["served"][i] = p.wait_since, p.served_tokens_at_level

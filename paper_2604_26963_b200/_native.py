@@ -32,7 +32,12 @@ class MarsConfig(C.Structure):
         ("aimd_increase", f64), ("aimd_decrease", f64), ("control_interval_s", f64),
         ("initial_window", f64), ("cpu_oversubscription", f64), ("reserve_fraction", f64),
         ("long_session_fraction", f64), ("enable_coordinator", i32), ("enable_coscheduler", i32),
+        ("policy", i32), ("ttl_seconds", f64), ("ttl_multiplier", f64),
     ]
+
+
+# mars_config.policy (POLICY_KINDS, baselines.py:48)
+POLICY_CODES = {"mars": 0, "fcfs": 1, "program_priority": 2, "static_ttl": 3, "dynamic_ttl": 4}
 
 
 class MarsCols(C.Structure):

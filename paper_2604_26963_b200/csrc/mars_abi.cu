@@ -141,6 +141,17 @@ static Cfg make_cfg(const mars_config& h) {
   c.oversub = h.cpu_oversubscription;
   c.reserve = h.reserve_fraction;
   c.long_frac = h.long_session_fraction;
+  c.policy = h.policy;
+  c.ttl_s = h.ttl_seconds;
+  c.ttl_mult = h.ttl_multiplier;
+  if (c.policy != POL_MARS) {
+    // comparison policies: arrival (or served, arrival) order with no aging
+    // and the coordinator-off victim eligibility; whole-chunk fitting
+    // (shrink_chunks=False, baselines.py:149/201/309)
+    c.coord = 0;
+    c.cosched = 0;
+  }
+  c.strict = (c.policy == POL_FCFS || c.policy == POL_STATIC_TTL || c.policy == POL_DYNAMIC_TTL);
   return c;
 }
 
@@ -184,6 +195,9 @@ void mars_config_default(mars_config* h) {
   h->long_session_fraction = 0.25;
   h->enable_coordinator = 1;
   h->enable_coscheduler = 1;
+  h->policy = MARS_POLICY_MARS;
+  h->ttl_seconds = 30.0;     // K_STATIC_TTL_S (baselines.py:50)
+  h->ttl_multiplier = 1.5;   // K_DYNAMIC_TTL_MULTIPLIER (baselines.py:51)
 }
 
 const char* mars_last_error(mars_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
@@ -207,6 +221,8 @@ static int alloc(mars_ctx* ctx, void** p, size_t bytes) {
 int mars_create(const mars_config* hcfg, int device, int64_t max_rows, int64_t max_queue,
                 mars_ctx** out) {
   if (!hcfg || !out || max_rows < 1 || max_queue < 0) return MARS_ERR_ARG;
+  if (hcfg->policy < MARS_POLICY_MARS || hcfg->policy > MARS_POLICY_DYNAMIC_TTL)
+    return MARS_ERR_ARG;
   if (hcfg->window_size < 1 || hcfg->window_size > WIN_MAX || hcfg->num_levels < 1 ||
       hcfg->num_levels > 4 || hcfg->block_size < 1 || hcfg->token_budget < 1 ||
       hcfg->max_decode_slots < 0)
@@ -617,6 +633,8 @@ static LaunchArgs launch_args(mars_ctx* ctx, const mars_step_in* in) {
 
 int mars_step_enqueue(mars_ctx* ctx, const mars_step_in* in) {
   if (!ctx || !in) return MARS_ERR_ARG;
+  if (in->control_due && ctx->cfg.policy != POL_MARS)  // PolicyBase.uses_admission_control
+    return fail(ctx, MARS_ERR_ARG, "the comparison policies have no admission control");
   CK(cudaSetDevice(ctx->device));
   *ctx->h_in = *in;
   LaunchArgs a = launch_args(ctx, in);

@@ -36,10 +36,19 @@ typedef int64_t i64;
 #define ST_WALK_OVERFLOW 2
 #define ST_BAD_INPUT 4
 
+// policies (mars_config.policy)
+#define POL_MARS MARS_POLICY_MARS
+#define POL_FCFS MARS_POLICY_FCFS
+#define POL_PP MARS_POLICY_PROGRAM_PRIORITY
+#define POL_STATIC_TTL MARS_POLICY_STATIC_TTL
+#define POL_DYNAMIC_TTL MARS_POLICY_DYNAMIC_TTL
+
 // device copy of the configuration (mars_config + derived)
 struct Cfg {
   i32 bs, bs_shift, budget, window, max_dec, num_levels, max_promos, hyst, w_min;
   i32 coord, cosched;
+  i32 policy, strict;  // strict: head-of-line blocking in the prefill pass
+  double ttl_s, ttl_mult;
   i64 bounds[4], quotas[4];
   double tick_s, prefill_rate, promo_wait, slack, horizon, pw_clip;
   double cpu_hi, cpu_lo, kv_hi, kv_lo, ema_alpha, tool_prior;
@@ -189,6 +198,47 @@ __device__ __forceinline__ u32 window_digit(u32 level, double t, double scale) {
   return (level << 10) | b;
 }
 
+// program_priority order key (baselines.py:170-171): (Call.served_tokens,
+// arrival_time, session_id); served_tokens < 2^32 (k_scan flags larger ones)
+__device__ __forceinline__ void pp_window_key(i64 served, double arr, u32 rank, u64& hi, u64& lo) {
+  const u64 o = ord_f64(arr);
+  const u64 s = served <= 0 ? 0ull : (served >= 0xffffffffll ? 0xffffffffull : (u64)served);
+  hi = (s << 32) | (o >> 32);
+  lo = (o << 32) | (u64)rank;
+}
+
+__device__ __forceinline__ u32 blocks_bucket(i64 h);
+
+// monotone 12-bit digit of the program_priority key: a log-scale bucket of
+// served_tokens (exact below 8), refined by arrival only where the bucket is
+// a single served value
+__device__ __forceinline__ u32 pp_window_digit(i64 served, double arr, double scale) {
+  const u32 b = blocks_bucket(served);
+  u32 sub = 0;
+  if (served < 8) {
+    const double y = arr * scale;
+    sub = ((y >= 1023.0) ? 1023u : (y > 0.0 ? (u32)y : 0u)) >> 6;
+  }
+  return (b << 4) | sub;
+}
+
+// the policy's window order key for one row (baselines.py:104-105, 170-171,
+// 374-377)
+__device__ __forceinline__ void row_window_key(const Cfg& c, u32 level, double rs, double arr,
+                                               i64 served, u32 rank, u64& hi, u64& lo) {
+  if (c.policy == POL_PP)
+    pp_window_key(served, arr, rank, hi, lo);
+  else if (c.coord)
+    window_key(level, rs, rank, hi, lo);
+  else
+    window_key(0u, arr, rank, hi, lo);
+}
+
+// policies that pin KV at tool boundaries (and so expire and reclaim pins)
+__device__ __forceinline__ bool policy_pins(const Cfg& c) {
+  return c.policy == POL_MARS || c.policy == POL_STATIC_TTL || c.policy == POL_DYNAMIC_TTL;
+}
+
 // monotone non-decreasing 8-bit bucket of a block count
 __device__ __forceinline__ u32 blocks_bucket(i64 h) {
   if (h <= 0) return 0;
@@ -259,6 +309,14 @@ __device__ __forceinline__ void decide_retention(const Cfg& c, i64 context, i64 
                                                  i64 total_blocks, double usage, double ema,
                                                  double now, u8& pin, double& benefit,
                                                  double& cost, double& deadline) {
+  if (c.policy == POL_STATIC_TTL || c.policy == POL_DYNAMIC_TTL) {
+    // TtlPolicy.retention_decision (baselines.py:238-243): always pin
+    pin = 1;
+    benefit = 0.0;
+    cost = 0.0;
+    deadline = (c.policy == POL_STATIC_TTL) ? now + c.ttl_s : now + c.ttl_mult * ema;
+    return;
+  }
   benefit = (double)context / c.prefill_rate;
   i64 foot = blocks_ceil(c, kv);
   double pw;

@@ -466,7 +466,13 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
 
   const double now = w->in.now;
   const int mode = w->in.mode;
-  const bool do_exp = !(mode & MARS_MODE_SKIP_EXPIRY);
+  const bool do_exp = !(mode & MARS_MODE_SKIP_EXPIRY) && policy_pins(c);
+  // the k_scan victim stream is MARS's reclaim order; the comparison policies
+  // reclaim through the walk's exact full-table search
+  const bool vic = c.policy == POL_MARS;
+  // S2 at tool boundaries: MARS's economics or the TTL rule; fcfs and
+  // program_priority never pin (retention_decision None, baselines.py:82-86)
+  const bool ret_on = c.policy != POL_FCFS && c.policy != POL_PP;
   const double scale = (now > 0.0 && now < 1e300) ? 1024.0 / now : 0.0;
   u32* dig = dig_in_smem ? (u32*)(sdyn + (size_t)SCAN_NBUF * SB_BYTES) : b.row_dig + cs;
   // pre-step scalars: CTA 0 rewrites *sc after the grid barrier
@@ -512,7 +518,7 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
           exp_blocks += pbk;
           n_exp++;
           rv = DIG_EXP;
-        } else {
+        } else if (vic) {
           rv = victim_digit(false, !exp_, B[SB_PL + lr], pbk);
           if (rv <= bv) atomicAdd(&hv[rv], 1u);
           n_vic++;
@@ -535,16 +541,22 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
         } else {
           lv = 0;
         }
-        rw = window_digit(lv, ((const double*)(B + SB_RS))[lr], scale);
+        if (c.policy == POL_PP) {
+          const i64 sv = t.served[r];
+          if (sv > 0xffffffffll) w->status |= ST_BAD_INPUT;  // outside the packed key
+          rw = pp_window_digit(sv, ((const double*)(B + SB_RS))[lr], scale);
+        } else {
+          rw = window_digit(lv, ((const double*)(B + SB_RS))[lr], scale);
+        }
         if (rw <= bw) atomicAdd(&hw[rw], 1u);
         const i32 kvv = ((const i32*)(B + SB_KV))[lr];
-        if (kvv > 0) {
+        if (kvv > 0 && vic) {
           rv = victim_digit(true, false, lv, held_blocks(c, kvv));
           if (rv <= bv) atomicAdd(&hv[rv], 1u);
           n_vic++;
         }
       }
-      if (f & MARS_F_BOUNDARY) {
+      if ((f & MARS_F_BOUNDARY) && ret_on) {
         n_bnd++;
         rw |= DIG_BND;
       }
@@ -833,9 +845,13 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
         const u32 rk = t.rank[r];
         u64 whi = 0, wlo = 0;
         if (ready) {  // post-aging level
-          const u32 lv = c.coord ? (u32)t.level[r] : 0u;
-          const double tt = c.coord ? t.rs[r] : t.arr[r];
-          window_key(lv, tt, rk, whi, wlo);
+          if (c.policy == POL_PP) {
+            pp_window_key(t.served[r], t.arr[r], rk, whi, wlo);
+          } else {
+            const u32 lv = c.coord ? (u32)t.level[r] : 0u;
+            const double tt = c.coord ? t.rs[r] : t.arr[r];
+            window_key(lv, tt, rk, whi, wlo);
+          }
         }
         if (is_w) {
           if (staged) {
@@ -1855,6 +1871,9 @@ __device__ __forceinline__ bool run_eligible(const Cfg& c, const WalkShared& S, 
                                              u64 elo, int ewi, int bi) {
   if (row == S.wrow[bi]) return false;
   if (ewi >= 0 && S.wplanned[ewi]) return false;
+  // program_priority: strictly more service (baselines.py:180-186); the
+  // key's top 32 bits are served_tokens
+  if (c.policy == POL_PP) return (ehi >> 32) > (S.whi[bi] >> 32);
   if (c.coord) return key_lt(S.whi[bi], S.wlo[bi], ehi, elo);
   // coordinator off: arrival_time strictly greater (baselines.py:431); the
   // key's time part is ord(arrival)
@@ -2014,35 +2033,83 @@ __device__ int walk_run(const Cfg& c, Tab& t, Bufs& b, WalkShared& S, VEnt* st, 
         S.npre++;
         S.wplanned[i] = 1;
         S.total += g;
+      } else if (c.strict) {
+        return REQ_DONE;  // head-of-line blocking (scheduler.py:369-370)
       }
       S.idx++;
     }
   }
 }
 
-// exact reclaim_for over the whole table (fallback when the stream prefix is
-// not enough) -- all threads
+// Row r's place in the policy's reclaim order, if it is an eligible victim
+// for beneficiary bi: a unique 128-bit key (kh, kl), pinned rows first.
+//  mars     pinned (expired first, -level, -blocks, sid), then running
+//           (-level, -blocks, sid) ranked after the beneficiary
+//           (scheduler.py:249-259, baselines.py:406-438);
+//  fcfs     running later arrivals, latest first (baselines.py:120-130);
+//  program_priority  running with more service, most first (:176-186);
+//  ttl      pinned (expired first, deadline, -blocks, sid), then running like
+//           fcfs (:268-298).
+__device__ __forceinline__ bool fs_key(const Cfg& c, Tab& t, const WalkShared& S, i64 r,
+                                       double now, int bi, u64& kh, u64& kl) {
+  const u8 f = t.flags[r];
+  if (f & MARS_F_PINNED) {
+    if (!policy_pins(c)) return false;
+    const bool nonexp = !(t.dl[r] < now);
+    if (c.policy == POL_MARS) {
+      kh = victim_key(false, nonexp, t.plevel[r], t.pb[r], t.rank[r]);
+      kl = 0;
+    } else {
+      const u64 o = ord_f64(t.dl[r]);
+      const i64 pb = t.pb[r];
+      const u64 bb = pb > (i64)MAXH ? MAXH : (u64)(pb < 0 ? 0 : pb);
+      kh = ((u64)(nonexp ? 1 : 0) << 62) | (o >> 2);
+      kl = ((o & 3ull) << 62) | ((MAXH - bb) << 32) | (u64)t.rank[r];
+    }
+    return true;
+  }
+  if (!((f & MARS_F_ACTIVE) && (t.phase[r] == MARS_PREFILL || t.phase[r] == MARS_DECODE)))
+    return false;
+  const i32 kvv = t.kv[r];
+  if (kvv <= 0) return false;
+  const u32 rk = t.rank[r];
+  const u32 lv = c.coord ? t.level[r] : 0u;
+  u64 hi, lo;
+  row_window_key(c, lv, t.rs[r], t.arr[r], t.served[r], rk, hi, lo);
+  if (!run_eligible(c, S, (u32)r, hi, lo, t.winpos[r], bi)) return false;
+  if (c.policy == POL_MARS) {
+    kh = victim_key(true, false, lv, blocks_ceil(c, kvv), rk);
+    kl = 0;
+  } else if (c.policy == POL_PP) {
+    const i64 sv = t.served[r];
+    const u64 su = sv <= 0 ? 0ull : (u64)sv;
+    kh = (1ull << 63) | (0x3fffffffffffffffull - (su & 0x3fffffffffffffffull));
+    kl = rk;
+  } else {
+    const u64 o = ~ord_f64(t.arr[r]);  // latest arrival first
+    kh = (1ull << 63) | (o >> 1);
+    kl = ((o & 1ull) << 63) | (u64)rk;
+  }
+  return true;
+}
+
+// exact reclaimer over the whole table (the comparison policies, and MARS
+// when the stream prefix is not enough) -- all threads: the shortest prefix
+// of the policy's reclaim order that covers the shortfall, by repeated block
+// argmin, or nothing when even every eligible victim would not cover it
 __device__ void walk_fullscan(const Cfg& c, Tab& t, WalkShared& S, i64 n_rows, double now,
                               u32* fs_row, u8* fs_pin, i32* fs_blk) {
   __shared__ long long shl[32];
-  __shared__ unsigned long long shk[32];
+  __shared__ unsigned long long shk[32], shk2[32];
   __shared__ u32 shr[32];
   const int bi = S.fs_b;
   const long long need = S.fs_need;
   // eligibility + total available
   long long tot = 0;
   for (i64 r = threadIdx.x; r < n_rows; r += blockDim.x) {
-    u8 f = t.flags[r];
-    if (f & MARS_F_PINNED) {
-      tot += t.pb[r];
-    } else if ((f & MARS_F_ACTIVE) && (t.phase[r] == MARS_PREFILL || t.phase[r] == MARS_DECODE)) {
-      i32 kvv = t.kv[r];
-      if (kvv <= 0) continue;
-      u64 hi, lo;
-      window_key(c.coord ? t.level[r] : 0u, c.coord ? t.rs[r] : t.arr[r], t.rank[r], hi, lo);
-      int wi = t.winpos[r];
-      if (run_eligible(c, S, (u32)r, hi, lo, wi, bi)) tot += blocks_ceil(c, kvv);
-    }
+    u64 kh, kl;
+    if (!fs_key(c, t, S, r, now, bi, kh, kl)) continue;
+    tot += (kh >> 63) == 0 ? (long long)t.pb[r] : blocks_ceil(c, t.kv[r]);
   }
   tot = block_sum<long long>(tot, shl);
   __shared__ int s_n;
@@ -2060,63 +2127,54 @@ __device__ void walk_fullscan(const Cfg& c, Tab& t, WalkShared& S, i64 n_rows, d
     __syncthreads();
     return;
   }
-  u64 last = 0;
+  u64 lasth = 0, lastl = 0;
   bool first = true;
   while (true) {
-    u64 best = ~0ull;
+    u64 bh = ~0ull, bl = ~0ull;
     u32 brow = 0xffffffffu;
     for (i64 r = threadIdx.x; r < n_rows; r += blockDim.x) {
-      u8 f = t.flags[r];
-      u64 k;
-      if (f & MARS_F_PINNED) {
-        bool nonexp = !(t.dl[r] < now);
-        k = victim_key(false, nonexp, t.plevel[r], t.pb[r], t.rank[r]);
-      } else if ((f & MARS_F_ACTIVE) &&
-                 (t.phase[r] == MARS_PREFILL || t.phase[r] == MARS_DECODE)) {
-        i32 kvv = t.kv[r];
-        if (kvv <= 0) continue;
-        u64 hi, lo;
-        u32 lv = c.coord ? t.level[r] : 0u;
-        window_key(lv, c.coord ? t.rs[r] : t.arr[r], t.rank[r], hi, lo);
-        if (!run_eligible(c, S, (u32)r, hi, lo, t.winpos[r], bi)) continue;
-        k = victim_key(true, false, lv, blocks_ceil(c, kvv), t.rank[r]);
-      } else {
-        continue;
-      }
-      if (!first && k <= last) continue;
-      if (k < best) {
-        best = k;
+      u64 kh, kl;
+      if (!fs_key(c, t, S, r, now, bi, kh, kl)) continue;
+      if (!first && !key_lt(lasth, lastl, kh, kl)) continue;
+      if (key_lt(kh, kl, bh, bl)) {
+        bh = kh;
+        bl = kl;
         brow = (u32)r;
       }
     }
     // block argmin (keys unique through the rank field)
     int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (int o = 16; o > 0; o >>= 1) {
-      u64 ok = __shfl_xor_sync(FULL, best, o);
-      u32 orow = __shfl_xor_sync(FULL, brow, o);
-      if (ok < best) {
-        best = ok;
+      const u64 oh = __shfl_xor_sync(FULL, bh, o);
+      const u64 ol = __shfl_xor_sync(FULL, bl, o);
+      const u32 orow = __shfl_xor_sync(FULL, brow, o);
+      if (key_lt(oh, ol, bh, bl)) {
+        bh = oh;
+        bl = ol;
         brow = orow;
       }
     }
     if (lane == 0) {
-      shk[wid] = best;
+      shk[wid] = bh;
+      shk2[wid] = bl;
       shr[wid] = brow;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      u64 bk = ~0ull;
+      u64 kh = ~0ull, kl = ~0ull;
       u32 br = 0xffffffffu;
       for (int q = 0; q < (int)(blockDim.x >> 5); ++q)
-        if (shk[q] < bk) {
-          bk = shk[q];
+        if (key_lt(shk[q], shk2[q], kh, kl)) {
+          kh = shk[q];
+          kl = shk2[q];
           br = shr[q];
         }
-      shk[0] = bk;
+      shk[0] = kh;
+      shk2[0] = kl;
       shr[0] = br;
       if (br != 0xffffffffu && s_n < FS_CAP) {
-        bool pinned = (bk >> 63) == 0;
-        i32 blk = pinned ? t.pb[br] : (i32)blocks_ceil(c, t.kv[br]);
+        const bool pinned = (kh >> 63) == 0;
+        const i32 blk = pinned ? t.pb[br] : (i32)blocks_ceil(c, t.kv[br]);
         fs_row[s_n] = br;
         fs_pin[s_n] = pinned;
         fs_blk[s_n] = blk;
@@ -2125,11 +2183,12 @@ __device__ void walk_fullscan(const Cfg& c, Tab& t, WalkShared& S, i64 n_rows, d
       }
     }
     __syncthreads();
-    u64 bk = shk[0];
-    u32 br = shr[0];
+    const u64 kh = shk[0], kl = shk2[0];
+    const u32 br = shr[0];
     __syncthreads();
     if (br == 0xffffffffu || S.freeb + s_freed >= need || s_n >= FS_CAP) break;
-    last = bk;
+    lasth = kh;
+    lastl = kl;
     first = false;
   }
   if (threadIdx.x == 0) {
@@ -2450,6 +2509,12 @@ __global__ void __launch_bounds__(WALK_TPB) k_walk(Tab t, Cfg c, Work* w, Bufs b
     S.fs_ready = 0;
     S.status = 0;
     S.fast_ok = 0;
+    if (c.policy != POL_MARS) {
+      // no k_scan victim stream (it is MARS's reclaim order): every claim
+      // that the free pool cannot cover goes to the exact full-table search
+      S.stream_ready = 1;
+      S.stream_complete = 0;
+    }
   }
   __syncthreads();
   PTIME(17);

@@ -30,10 +30,12 @@ _CT = {np.uint8: C.c_uint8, np.uint32: C.c_uint32, np.int32: C.c_int32, np.int64
 
 
 def make_config(enable_coordinator: bool = True, enable_coscheduler: bool = True,
-                initial_window: Optional[float] = None, **overrides) -> N.MarsConfig:
+                initial_window: Optional[float] = None, policy: str = "mars",
+                **overrides) -> N.MarsConfig:
     lib = N.load()
     cfg = N.MarsConfig()
     lib.mars_config_default(C.byref(cfg))
+    cfg.policy = N.POLICY_CODES[policy]
     cfg.enable_coordinator = int(bool(enable_coordinator))
     cfg.enable_coscheduler = int(bool(enable_coscheduler))
     if initial_window is not None:

@@ -74,9 +74,12 @@ class RetentionDecision:
 
 
 def config_from(mlfq=None, retention=None, pressure=None, controller=None,
-                enable_coordinator=True, enable_coscheduler=True, gpu=None) -> N.MarsConfig:
+                enable_coordinator=True, enable_coscheduler=True, gpu=None,
+                policy: str = "mars", **extra) -> N.MarsConfig:
     """mars_config from reference-style config objects (duck-typed)."""
-    cfg = make_config(enable_coordinator, enable_coscheduler)
+    cfg = make_config(enable_coordinator, enable_coscheduler, policy=policy)
+    for k, v in extra.items():
+        setattr(cfg, k, v)
     if mlfq is not None:
         cfg.num_levels = mlfq.num_levels
         cfg.max_promotions = mlfq.max_promotions
@@ -113,6 +116,9 @@ class GpuMarsPolicy:
 
     name = "mars"
     uses_admission_control = True
+    # the drop-in step: no expiry / probe / refresh (the sim does those), MLFQ
+    # charges at tick end and S2 for the rounds that finish this tick
+    _mode = _DROPIN_MODE
 
     def __init__(self, mlfq=None, retention=None, pressure=None, enable_coordinator: bool = True,
                  enable_coscheduler: bool = True, max_sessions: int = 1 << 16,
@@ -295,6 +301,9 @@ class GpuMarsPolicy:
 
     # -- the tick ---------------------------------------------------------------------
 
+    def _extra_cols(self, ready: Sequence, n: int) -> dict:
+        return {}
+
     # -- S5 block IDs: tee of the caller's pool op stream -------------------------
 
     def _kv_attach(self, pool, gpu) -> None:
@@ -341,6 +350,7 @@ class GpuMarsPolicy:
             "ready_since": np.fromiter((c.ready_since for c in ready), np.float64, n),
             "arrival": np.fromiter((c.arrival_time for c in ready), np.float64, n),
         }
+        cols.update(self._extra_cols(ready, n))
         if n:
             eng.upsert(cols, rows=rows)
         if gone:
@@ -358,7 +368,7 @@ class GpuMarsPolicy:
         s.w_adm = 1.0
         eng.set_scalars(s)
         eng._check(eng.lib.mars_set_rows(eng.ctx, len(self._sid)))
-        si = eng.step_in(now, False, 0, 0, 1, _DROPIN_MODE)
+        si = eng.step_in(now, False, 0, 0, 1, self._mode)
         res = eng.step(si)
         if res.status:
             raise RuntimeError(f"device step status {res.status}")
@@ -404,3 +414,121 @@ class GpuMarsPolicy:
                                  telemetry.kv_usage_ratio, ema_v,
                                  RetentionDecision(bool(p), b, c, d), pool.total_blocks)
         return plan
+
+
+# ---------------------------------------------------------------------------
+# The reference's comparison policies on the same device step
+# ---------------------------------------------------------------------------
+
+
+class _Slots:
+    """The two MlfqConfig fields the comparison policies take (baselines.py:113-116)."""
+
+    def __init__(self, window_size: int, max_decode_slots: int) -> None:
+        self.window_size, self.max_decode_slots = window_size, max_decode_slots
+        self.num_levels, self.max_promotions, self.promotion_wait_s = 4, 3, 10.0
+        self.level_boundaries_tokens = (4_000, 32_000, 128_000, math.inf)
+        self.level_quotas_tokens = (2_000, 8_000, 32_000, math.inf)
+
+
+class _GpuComparisonPolicy(GpuMarsPolicy):
+    """PolicyBase defaults (baselines.py:56-101) over the B200 step: no
+    admission control, no MLFQ state, the window ordered by the policy's key
+    and build_plan run with whole-chunk fitting (the device walk with
+    mars_config.policy set).  The sim's pool and evictor see the same ordered
+    journal replay as GpuMarsPolicy."""
+
+    uses_admission_control = False
+    _mode = N.MODE_SKIP_EXPIRY | N.MODE_SKIP_PROBE | N.MODE_SKIP_REFRESH
+
+    def __init__(self, window_size: int = 128, max_decode_slots: int = 64,
+                 max_sessions: int = 1 << 16, device: int = 0, kv_blocks: bool = False,
+                 pressure=None, **cfg_extra) -> None:
+        super().__init__(mlfq=_Slots(window_size, max_decode_slots), pressure=pressure,
+                         enable_coordinator=False, enable_coscheduler=False,
+                         max_sessions=max_sessions, device=device, kv_blocks=kv_blocks)
+        self.window_size, self.max_decode_slots = window_size, max_decode_slots
+        self._cfg_args.update(policy=self.name, **cfg_extra)
+
+    def on_admit(self, call, now: float) -> None:
+        r = self._row[call.session_id]
+        self._engine().upsert({"level": np.zeros(1, np.uint8), "promos": np.zeros(1, np.uint8),
+                               "served": np.array([call.served_tokens], np.int64),
+                               "flags": np.array([F_ACTIVE], np.uint8)}, rows=np.array([r]))
+        self._levels[call.session_id] = 0
+        self._admitted.add(call.session_id)
+
+    def on_resume(self, call, now: float) -> None:
+        pass
+
+    def on_service(self, session_id: str, tokens: int, now: float) -> None:
+        pass
+
+    def level_of(self, call) -> int:
+        return 0
+
+    def retention_decision(self, call, pool, telemetry, gpu, now):
+        return None
+
+
+class GpuFcfsPolicy(_GpuComparisonPolicy):
+    """Drop-in for FcfsPolicy (baselines.py:108-155)."""
+
+    name = "fcfs"
+
+
+class GpuProgramPriorityPolicy(_GpuComparisonPolicy):
+    """Drop-in for ProgramPriorityPolicy (baselines.py:158-208): the window
+    key reads Call.served_tokens from the `served` column, refreshed for the
+    ready rows every tick."""
+
+    name = "program_priority"
+
+    def _extra_cols(self, ready: Sequence, n: int) -> dict:
+        return {"served": np.fromiter((c.served_tokens for c in ready), np.int64, n)}
+
+
+class GpuTtlPolicy(_GpuComparisonPolicy):
+    """Drop-in for TtlPolicy (baselines.py:211-315): unconditional pins with
+    a static or EMA-scaled deadline; expired pins and the pin-first reclaim
+    order run through the same device tables as MARS's."""
+
+    def __init__(self, kind: str, pressure=None, ttl_seconds: float = 30.0,
+                 multiplier: float = 1.5, window_size: int = 128, max_decode_slots: int = 64,
+                 **kw) -> None:
+        if kind not in ("static_ttl", "dynamic_ttl"):
+            raise ValueError(f"not a ttl policy kind: {kind}")
+        self.name = kind
+        super().__init__(window_size, max_decode_slots, pressure=pressure,
+                         ttl_seconds=float(ttl_seconds), ttl_multiplier=float(multiplier), **kw)
+        self.ttl_seconds, self.multiplier = ttl_seconds, multiplier
+
+    def retention_decision(self, call, pool, telemetry, gpu, now):
+        # TtlPolicy.retention_decision (baselines.py:238-243): always pin
+        if self.name == "static_ttl":
+            deadline = now + self.ttl_seconds
+        else:
+            ema = telemetry.ema_tool_duration
+            deadline = now + self.multiplier * (self._tool_prior if ema is None else ema)
+        return RetentionDecision(True, 0.0, 0.0, deadline)
+
+
+def make_gpu_policy(kind: str, mlfq=None, retention=None, pressure=None, params=None,
+                    enable_coordinator: bool = True, enable_coscheduler: bool = True,
+                    **kw):
+    """make_policy (baselines.py:458-495) over the B200 drop-ins."""
+    params = dict(params or {})
+    window = params.pop("window_size", getattr(mlfq, "window_size", 128))
+    slots = params.pop("max_decode_slots", getattr(mlfq, "max_decode_slots", 64))
+    if kind == "fcfs":
+        return GpuFcfsPolicy(window_size=window, max_decode_slots=slots, **kw)
+    if kind == "program_priority":
+        return GpuProgramPriorityPolicy(window_size=window, max_decode_slots=slots, **kw)
+    if kind in ("static_ttl", "dynamic_ttl"):
+        return GpuTtlPolicy(kind, pressure, ttl_seconds=params.pop("ttl_seconds", 30.0),
+                            multiplier=params.pop("multiplier", 1.5), window_size=window,
+                            max_decode_slots=slots, **kw)
+    if kind == "mars":
+        return GpuMarsPolicy(mlfq, retention, pressure, enable_coordinator=enable_coordinator,
+                             enable_coscheduler=enable_coscheduler, **kw)
+    raise ValueError(f"unknown policy kind {kind!r}")

@@ -107,3 +107,31 @@ def partial_admission(snap, overloaded=False):
     w = active + len(snap.queue) // 3
     snap.initial_window = float(2 * w if overloaded else w)  # AIMD halves it under overload
     return snap
+
+
+def comparison_variant(n, seed, policy, pool):
+    """A snapshot the reference's comparison policies can hold: fcfs and
+    program_priority never pin (their pinned rows become unpinned tool rows
+    and the pool shrinks by those blocks, so the pressure is unchanged);
+    program_priority's `served` column is Call.served_tokens, with ties and
+    small values so every branch of its key and digit runs."""
+    s = snapshot_v1(n, seed=seed, pool=pool)
+    c = s.cols
+    rng = np.random.default_rng(seed + 1000)
+    if policy in ("fcfs", "program_priority"):
+        pinned = (c["flags"] & F_PINNED) != 0
+        blocks = int(c["pinned_blocks"][pinned].astype(np.int64).sum())
+        c["flags"][pinned] &= ~np.uint8(F_PINNED)
+        c["kv"][pinned] = 0
+        c["pinned_blocks"][pinned] = 0
+        c["deadline"][pinned] = 0.0
+        c["plevel"][pinned] = 0
+        s.total_blocks -= blocks
+    if policy == "program_priority":
+        served = rng.integers(0, 60_000, size=n)
+        u = rng.random(n)
+        served[u < 0.05] = 0
+        served[(u >= 0.05) & (u < 0.08)] = rng.integers(1, 8, size=int(((u >= 0.05) & (u < 0.08)).sum()))
+        served[(u >= 0.08) & (u < 0.10)] = 4096
+        c["served"][:] = served
+    return s

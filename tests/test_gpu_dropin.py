@@ -13,8 +13,8 @@ import hashlib
 import pytest
 
 from paper_2604_26963_b200.admission import balance_and_admit
-from paper_2604_26963_b200.policy import GpuMarsPolicy
-from tests._sim import SIM, VARIANT_KW, run_sim
+from paper_2604_26963_b200.policy import GpuMarsPolicy, make_gpu_policy
+from tests._sim import SIM, SIM_BASE, VARIANT_KW, run_sim
 
 pytestmark = pytest.mark.gpu
 
@@ -36,3 +36,20 @@ def test_dropin_event_log_is_byte_identical(key):
     assert len(out.events) == SIM[key]["records"]
     assert got == SIM[key]["sha256"]
     assert out.counters == SIM[key]["counters"]
+
+
+# demo64/program_priority (173K records) replays ~10x longer than the rest;
+# its CPU oracle replay is pinned in tests/test_oracle_golden.py
+BASE_KEYS = sorted(k for k in SIM_BASE if k != "demo64/program_priority")
+
+
+@pytest.mark.parametrize("key", BASE_KEYS)
+def test_comparison_policy_event_log_is_byte_identical(key):
+    """fcfs / program_priority / static_ttl / dynamic_ttl through the B200
+    drop-ins reproduce the reference's own event logs byte for byte."""
+    pol = make_gpu_policy(key.split("/")[1])
+    out = run_sim(key, policy=pol)
+    pol.close()
+    assert len(out.events) == SIM_BASE[key]["records"]
+    assert hashlib.sha256(out.log.jsonl_bytes()).hexdigest() == SIM_BASE[key]["sha256"]
+    assert out.counters == SIM_BASE[key]["counters"]

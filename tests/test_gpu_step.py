@@ -18,7 +18,7 @@ from oracle.snapshot_step import run_step
 from paper_2604_26963_b200.engine import MarsEngine, canonical, make_config
 from paper_2604_26963_b200.snapshot import snapshot_v1
 from tests._canon import canon
-from tests._variants import variant
+from tests._variants import comparison_variant, variant
 from tests.conftest import GOLDEN
 
 pytestmark = pytest.mark.gpu
@@ -133,3 +133,17 @@ def test_retention_batch_matches_reference_kat():
         assert (bool(pin[0]), float(b[0]), float(c[0]), float(d[0])) == (
             r["pin"], r["benefit"], r["cost"], r["deadline"])
     eng.close()
+
+
+@pytest.mark.parametrize("policy", ["fcfs", "program_priority", "static_ttl", "dynamic_ttl"])
+@pytest.mark.parametrize("pool,n,seed", [("headroom", 100_000, 51), ("pressure", 20_000, 52)])
+def test_comparison_policy_step_matches_oracle(policy, pool, n, seed):
+    """The reference's comparison policies (baselines.py:108-315) on the same
+    device step: window order, whole-chunk fitting, head-of-line blocking,
+    their reclaim orders (exact full-table search) and the TTL pin rule."""
+    snap = comparison_variant(n, seed, policy, pool)
+    got = device_step(snap.copy(), control_due=False, policy=policy)
+    want = run_step(snap.copy(), control_due=False, policy=policy)
+    assert_same(got, want)
+    if pool == "pressure":
+        assert want["evictions"], "the pressure case must exercise the reclaimer"
