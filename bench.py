@@ -190,6 +190,73 @@ def kv_sweep(device: int, batches=(1, 16, 256, 2048), reps: int = 3) -> dict:
             "sweep": sweep}
 
 
+def hbm_sweep(device: int, sizes, steps: int = 5, warmup: int = 3, flush_mb: int = 512) -> list:
+    """the step and its scan kernel on tables far beyond the
+    126 MB L2 (L2 flushed before every step), where the 1M-session step's
+    latency floor no longer hides the bandwidth the kernels reach."""
+    import statistics as st
+
+    import torch
+
+    from paper_2604_26963_b200.engine import MarsEngine, make_config
+    from paper_2604_26963_b200.snapshot import snapshot_v1
+
+    peak, _ = _peaks()
+    out = []
+    for n in sizes:
+        snap = snapshot_v1(n, seed=7, pool="headroom")
+        eng = MarsEngine(max_rows=snap.n, max_queue=max(len(snap.queue), 1), device=device,
+                         config=make_config(initial_window=snap.initial_window))
+        eng.load_snapshot(snap)
+        si = eng.step_in(snap.now, True, snap.active_tools, snap.queued_tools, snap.worker_slots)
+        stream = torch.cuda.Stream()
+        torch.cuda.set_stream(stream)
+        eng.lib.mars_set_stream(eng.ctx, stream.cuda_stream)
+        eng.checkpoint()
+        eng.set_graph(True)
+        for _ in range(warmup):
+            eng.restore()
+            eng.enqueue(si)
+        torch.cuda.synchronize()
+        ms = []
+        for _ in range(steps):
+            eng.restore()
+            eng.flush_l2(flush_mb << 20)
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            eng.enqueue(si)
+            b.record(stream)
+            torch.cuda.synchronize()
+            ms.append(a.elapsed_time(b))
+        eng.set_graph(False)
+        eng.set_profiling(True)
+        kt = []
+        for _ in range(steps):
+            eng.restore()
+            eng.flush_l2(flush_mb << 20)
+            eng.enqueue(si)
+            kt.append(eng.kernel_times())
+        eng.set_profiling(False)
+        res = eng.fetch()
+        scan_ms = st.median(k["k_scan"] for k in kt)
+        sb = scan_bytes(snap)
+        sbs = step_bytes(snap)
+        step_ms = st.median(ms)
+        out.append({"sessions": n, "status": int(res.status), "ms_per_step": step_ms,
+                    "sessions_per_s": n / (step_ms * 1e-3),
+                    "k_scan_ms": scan_ms, "k_scan_gbs": sb / (scan_ms * 1e-3) / 1e9,
+                    "k_scan_frac": sb / (scan_ms * 1e-3) / 1e9 / peak,
+                    "k_control_ms": st.median(k["k_control"] for k in kt),
+                    "k_walk_ms": st.median(k["k_walk"] for k in kt),
+                    "step_frac": sbs / (step_ms * 1e-3) / 1e9 / peak,
+                    "table_mb": sum(v.nbytes for v in snap.cols.values()) / 1e6})
+        eng.close()
+        del snap
+        torch.cuda.synchronize()
+    return out
+
+
 def cpu_reference(sessions: int, seed: int, reps: int = 1):
     """Times the oracle port's full step (materialisation excluded)."""
     from oracle.snapshot_step import World, run_step
@@ -248,6 +315,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--flush-mb", type=int, default=512)
     ap.add_argument("--no-kv", action="store_true", help="skip the KV evict/restore sweep")
+    ap.add_argument("--hbm-sweep", default="4000000,16000000,64000000",
+                    help="table sizes for the beyond-L2 sweep (comma list, '' to skip)")
     a = ap.parse_args()
     if a.impl == "reference":
         return run_reference_arm(a)
@@ -422,6 +491,11 @@ def main():
             line["kv"] = kv_sweep(local)
         except Exception as exc:  # the scheduler number stands on its own
             line["kv"] = {"error": repr(exc)[:300]}
+    if rank == 0 and world == 1 and a.hbm_sweep:
+        try:
+            line["hbm_sweep"] = hbm_sweep(local, [int(x) for x in a.hbm_sweep.split(",") if x])
+        except Exception as exc:  # the headline line stands on its own
+            line["hbm_sweep"] = {"error": repr(exc)[:300]}
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         t_cpu = cpu_reference(a.sessions, seed=0)[0]
         line["cpu_baseline"] = {

@@ -25,6 +25,7 @@
 // rounding so retention / admission scalars are bit-identical.
 
 #include <cooperative_groups.h>
+#include <stdlib.h>
 #include <cuda_runtime.h>
 #include <stdio.h>
 
@@ -262,6 +263,7 @@ __device__ void refresh_pressure(const Cfg& c, mars_scalars* sc, int worker_slot
 #define DIG_NONE 0x8000u
 #define DIG_BND 0x4000u
 #define DIG_EXP 0x4000u
+#define DIG_ABOVE 0x7fffu  // victim digit above every threshold (not computed)
 #define DIG_SMEM_MAX (64 * 1024)  // record kept in shared memory up to this size
 
 // For two HIST_BINS shared histograms at once: the smallest bin d with
@@ -488,12 +490,19 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
   __syncthreads();
 
   // ---- phase 1 ---------------------------------------------------------------
-  for (int rd = 0; rd < nrounds; ++rd) {
-    const unsigned char* B = sdyn + (size_t)(rd % SCAN_NBUF) * SB_BYTES;
-    mbar_wait(&bars[rd % SCAN_NBUF], (u32)((rd / SCAN_NBUF) & 1));
+  // Running-victim digits and the window digit's f64 part are skipped once the
+  // CTA's running bound already rules the row out: such a row can be neither
+  // in the CTA's top-k nor in the global one, and its digit record only has to
+  // stay above every threshold (DIG_ABOVE, or the level's largest digit).
+  int buf = 0;
+  u32 par = 0;
+  u32* dig_rd = dig;
+  for (int rd = 0; rd < nrounds; ++rd, dig_rd += SCAN_R) {
+    const unsigned char* B = sdyn + (size_t)buf * SB_BYTES;
+    mbar_wait(&bars[buf], par);
     const int lr = threadIdx.x;
     const i64 r = cs + (i64)rd * SCAN_R + lr;
-    const bool valid = r < ce;
+    const bool valid = lr < (int)(ce - (cs + (i64)rd * SCAN_R));
     const u32 bw = s_bw, bv = s_bv;
     u32 rw = DIG_NONE, rv = DIG_NONE;
     if (valid) {
@@ -545,22 +554,33 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
           const i64 sv = t.served[r];
           if (sv > 0xffffffffll) w->status |= ST_BAD_INPUT;  // outside the packed key
           rw = pp_window_digit(sv, ((const double*)(B + SB_RS))[lr], scale);
+          if (rw <= bw) atomicAdd(&hw[rw], 1u);
+        } else if ((lv << 10) > bw) {
+          rw = (lv << 10) | 1023u;  // the level alone is above the bound
         } else {
           rw = window_digit(lv, ((const double*)(B + SB_RS))[lr], scale);
+          if (rw <= bw) atomicAdd(&hw[rw], 1u);
         }
-        if (rw <= bw) atomicAdd(&hw[rw], 1u);
         const i32 kvv = ((const i32*)(B + SB_KV))[lr];
         if (kvv > 0 && vic) {
-          rv = victim_digit(true, false, lv, held_blocks(c, kvv));
-          if (rv <= bv) atomicAdd(&hv[rv], 1u);
           n_vic++;
+          if (bv >= (1u << 11)) {  // running digits start at 1 << 11
+            rv = victim_digit(true, false, lv, held_blocks(c, kvv));
+            if (rv <= bv) atomicAdd(&hv[rv], 1u);
+          } else {
+            rv = DIG_ABOVE;
+          }
         }
       }
       if ((f & MARS_F_BOUNDARY) && ret_on) {
         n_bnd++;
         rw |= DIG_BND;
       }
-      dig[r - cs] = rw | (rv << 16);
+      dig_rd[lr] = rw | (rv << 16);
+    }
+    if (++buf == SCAN_NBUF) {
+      buf = 0;
+      par ^= 1u;
     }
     // every thread is done with this round's buffer: refill it
     __syncthreads();
@@ -718,21 +738,31 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
     __shared__ unsigned long long s_scan[32];
     __shared__ u32 s_escan[32];
     __shared__ int s_base[3], s_tot[4];
+    // Two layouts of the CTA's rows over its threads.  Digit record in
+    // shared memory: thread t owns a contiguous run (sequential, conflict-free
+    // reads).  Record in global memory (large tables): warp w owns the rows
+    // [w*S, (w+1)*S), read 32 consecutive rows at a time (coalesced).  Either
+    // way thread / warp order is row order.
+    const bool tr = dig_in_smem != 0;
     const i64 len = ce - cs;
     const i64 per = (len + SCAN_TPB - 1) / SCAN_TPB;
-    const i64 r0 = (i64)threadIdx.x * per;
-    const i64 r1 = (r0 + per < len) ? r0 + per : len;
+    const i64 r0 = tr ? (i64)threadIdx.x * per : (i64)wid * per * 32 + lane;
+    const i64 rlim = tr ? r0 + per : (i64)(wid + 1) * per * 32;
+    const i64 r1 = rlim < len ? rlim : len;
+    const i64 step = tr ? 1 : 32;
     constexpr int FB = 21;  // count field width (chunk < 2^21 rows)
     constexpr unsigned long long FM = (1ull << FB) - 1;
     unsigned long long cnt = 0;
     u32 ecnt = 0;
-    for (i64 i = r0; i < r1; ++i) {
+    for (i64 i = r0; i < r1; i += step) {
       const u32 rc = dig[i];
       const u32 rw = rc & 0xffffu, rv = rc >> 16;
       cnt += ((rw & ~DIG_BND) <= (u32)gw ? 1ull : 0ull) + ((rv <= (u32)gv ? 1ull : 0ull) << FB) +
              ((rw & DIG_BND) ? (1ull << (2 * FB)) : 0ull);
       ecnt += rv == DIG_EXP ? 1u : 0u;
     }
+    // thread-level inclusive scan (fields never carry: each < 2^21); the
+    // warp layout needs only the warp totals (lane 31's inclusive value)
     unsigned long long incl = cnt;
     u32 eincl = ecnt;
 #pragma unroll
@@ -761,7 +791,7 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
           e += y;
         }
       }
-      s_scan[lane] = v;
+      s_scan[lane] = v;  // inclusive over warps
       s_escan[lane] = e;
       if (lane == 31) {
         s_tot[0] = (int)(v & FM);
@@ -795,31 +825,56 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
     }
     if (!staged) __syncthreads();
     // (B) row ids: local lists (staged) or the global lists
-    if (cnt | ecnt) {
-      const unsigned long long ex = incl - cnt + (wid ? s_scan[wid - 1] : 0ull);
+    const unsigned long long wtot = __shfl_sync(FULL, incl, 31);
+    const u32 wetot = __shfl_sync(FULL, eincl, 31);
+    if (tr ? (cnt | ecnt) != 0 : (wtot | wetot) != 0) {
+      const unsigned long long ex = (tr ? incl - cnt : 0ull) + (wid ? s_scan[wid - 1] : 0ull);
       int pw = (int)(ex & FM), pv = nw + (int)((ex >> FB) & FM);
       int pr = nw + nv + (int)(ex >> (2 * FB));
-      int pe = nw + nv + nb + (int)(eincl - ecnt + (wid ? s_escan[wid - 1] : 0u));
+      int pe = nw + nv + nb + (int)((tr ? eincl - ecnt : 0u) + (wid ? s_escan[wid - 1] : 0u));
+      u32* ow = lrow;
+      u32* ov = lrow;
+      u32* orr = lrow;
+      u32* oe = lrow;
       if (!staged) {
         pw += s_base[0];
         pv += s_base[1] - nw;
         pr += s_base[2] - nw - nv;
         pe += exp_off - nw - nv - nb;
+        ow = b.wc_row;
+        ov = b.vc_row;
+        orr = b.ret_row;
+        oe = exp_rows;
       }
-      for (i64 i = r0; i < r1; ++i) {
-        const u32 rc = dig[i];
-        const u32 rw = rc & 0xffffu, rv = rc >> 16;
-        const u32 r = (u32)(cs + i);
-        if (staged) {
-          if ((rw & ~DIG_BND) <= (u32)gw) lrow[pw++] = r;
-          if (rv <= (u32)gv) lrow[pv++] = r;
-          if (rw & DIG_BND) lrow[pr++] = r;
-          if (rv == DIG_EXP) lrow[pe++] = r;
-        } else {
-          if ((rw & ~DIG_BND) <= (u32)gw) b.wc_row[pw++] = r;
-          if (rv <= (u32)gv) b.vc_row[pv++] = r;
-          if (rw & DIG_BND) b.ret_row[pr++] = r;
-          if (rv == DIG_EXP) exp_rows[pe++] = r;
+      if (tr) {
+        for (i64 i = r0; i < r1; ++i) {
+          const u32 rc = dig[i];
+          const u32 rw = rc & 0xffffu, rv = rc >> 16;
+          const u32 r = (u32)(cs + i);
+          if ((rw & ~DIG_BND) <= (u32)gw) ow[pw++] = r;
+          if (rv <= (u32)gv) ov[pv++] = r;
+          if (rw & DIG_BND) orr[pr++] = r;
+          if (rv == DIG_EXP) oe[pe++] = r;
+        }
+      } else {  // 32 consecutive rows per ballot, lane order = row order
+        const u32 lt = (1u << lane) - 1u;
+        for (i64 c0 = r0 - lane; c0 < r1; c0 += 32) {
+          const i64 i = c0 + lane;
+          const u32 rc = i < r1 ? dig[i] : (DIG_NONE | (DIG_NONE << 16));
+          const u32 rw = rc & 0xffffu, rv = rc >> 16;
+          const u32 r = (u32)(cs + i);
+          const bool qw = (rw & ~DIG_BND) <= (u32)gw, qv = rv <= (u32)gv;
+          const bool qb = (rw & DIG_BND) != 0, qe = rv == DIG_EXP;
+          const u32 mw = __ballot_sync(FULL, qw), mv = __ballot_sync(FULL, qv);
+          const u32 mb = __ballot_sync(FULL, qb), me_ = __ballot_sync(FULL, qe);
+          if (qw) ow[pw + __popc(mw & lt)] = r;
+          if (qv) ov[pv + __popc(mv & lt)] = r;
+          if (qb) orr[pr + __popc(mb & lt)] = r;
+          if (qe) oe[pe + __popc(me_ & lt)] = r;
+          pw += __popc(mw);
+          pv += __popc(mv);
+          pr += __popc(mb);
+          pe += __popc(me_);
         }
       }
     }
@@ -2849,6 +2904,8 @@ static size_t sort_smem_bytes() { return (size_t)SORT_CAP * (8 + 8 + 4); }
 
 // k_scan geometry: <= 1 CTA per SM, contiguous row ranges of `chunk` rows
 // (a multiple of SCAN_RPT), the digit record in shared memory when it fits
+static int g_dig_global = 0;  // MARS_DIG_GLOBAL=1: digit record in global memory (tests)
+
 static void scan_geometry(i64 n, int nsm, int* grid, i64* chunk, int* in_smem) {
   i64 g = (n + SCAN_TILE - 1) / SCAN_TILE;
   if (g > nsm) g = nsm;
@@ -2857,7 +2914,7 @@ static void scan_geometry(i64 n, int nsm, int* grid, i64* chunk, int* in_smem) {
   i64 units = (n + 15) / 16;  // TMA rounds start 16-row (16-byte) aligned
   *grid = (int)g;
   *chunk = ((units + g - 1) / g) * 16;
-  *in_smem = (*chunk * 4 <= DIG_SMEM_MAX) ? 1 : 0;
+  *in_smem = (*chunk * 4 <= DIG_SMEM_MAX && !g_dig_global) ? 1 : 0;
 }
 
 static void launch_scan(const LaunchArgs* a, int nsm, cudaStream_t s) {
@@ -2877,6 +2934,10 @@ static void launch_scan(const LaunchArgs* a, int nsm, cudaStream_t s) {
 }
 
 int mars_kernels_init() {
+  {
+    const char* v = getenv("MARS_DIG_GLOBAL");
+    g_dig_global = (v && v[0] == '1') ? 1 : 0;
+  }
   cudaError_t e;
   e = cudaFuncSetAttribute(k_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)(scan_stage_bytes() + DIG_SMEM_MAX));

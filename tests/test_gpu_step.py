@@ -147,3 +147,13 @@ def test_comparison_policy_step_matches_oracle(policy, pool, n, seed):
     assert_same(got, want)
     if pool == "pressure":
         assert want["evictions"], "the pressure case must exercise the reclaimer"
+
+
+def test_digit_record_in_global_memory_matches_oracle(monkeypatch):
+    """Tables whose per-CTA digit record exceeds shared memory (> 2.4M rows)
+    keep it in HBM and emit with the coalesced warp layout; forced here on a
+    smaller table."""
+    monkeypatch.setenv("MARS_DIG_GLOBAL", "1")
+    for kind, n, seed in (("headroom", 200_000, 61), ("expired_big", 150_000, 62)):
+        snap = variant(n, seed, kind)
+        assert_same(device_step(snap.copy()), run_step(snap.copy()))
