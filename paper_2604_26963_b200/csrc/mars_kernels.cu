@@ -39,7 +39,7 @@ namespace cg = cooperative_groups;
 #ifdef MARS_PHASE_TIMING
 // Debug builds only (-DMARS_PHASE_TIMING): per-CTA %globaltimer stamps at
 // named points of the step, dumped as a timeline after each step.
-#define PT_SLOTS 32
+#define PT_SLOTS 40
 __device__ unsigned long long g_ptime[1024][PT_SLOTS];
 __device__ __forceinline__ void ptime(int k) {
   if (threadIdx.x == 0) {
@@ -52,6 +52,7 @@ __global__ void k_ptime_dump() {
   unsigned long long t0 = ~0ull;
   for (int i = 0; i < 1024; ++i)
     if (g_ptime[i][0]) t0 = min(t0, g_ptime[i][0]);
+  if (g_ptime[0][32]) t0 = min(t0, g_ptime[0][32]);  // k_work_init
   for (int k = 0; k < PT_SLOTS; ++k) {
     unsigned long long mn = ~0ull, mx = 0;
     int cnt = 0;
@@ -1185,11 +1186,26 @@ __device__ int lsd_grid_sort(Lsd L, LsdView v, LsdArgs a, int npass, u32 (*wc)[2
     const u32* vin = L.v[cur];
     u64* kout = L.k[1 - cur];
     u32* vout = L.v[1 - cur];
+    // a chunk of <= 1024 entries (the usual case) stays in registers from
+    // the histogram to the scatter: one load per entry per pass
+    const bool one = e - s <= 1024;
+    u64 k1 = 0;
+    u32 v1 = 0;
+    const bool has1 = one && s + tid < e;
+    if (has1) {
+      const int i = s + tid;
+      k1 = rawp ? (u64)(asc ? raw[i] : mr - raw[i]) : kin[i];
+      v1 = rawp ? (u32)i : vin[i];
+    }
     if (tid < 256) h[tid] = 0;
     __syncthreads();
-    for (int i = s + tid; i < e; i += 1024) {
-      u64 k = rawp ? (u64)(asc ? raw[i] : mr - raw[i]) : kin[i];
-      atomicAdd(&h[(k >> shift) & 255u], 1u);
+    if (one) {
+      if (has1) atomicAdd(&h[(k1 >> shift) & 255u], 1u);
+    } else {
+      for (int i = s + tid; i < e; i += 1024) {
+        u64 k = rawp ? (u64)(asc ? raw[i] : mr - raw[i]) : kin[i];
+        atomicAdd(&h[(k >> shift) & 255u], 1u);
+      }
     }
     __syncthreads();
     if (tid < 256) L.cnt[me * 256 + tid] = h[tid];
@@ -1242,7 +1258,10 @@ __device__ int lsd_grid_sort(Lsd L, LsdView v, LsdArgs a, int npass, u32 (*wc)[2
       bool valid = i < e;
       u64 k = 0;
       u32 val = 0;
-      if (valid) {
+      if (one) {
+        k = k1;
+        val = v1;
+      } else if (valid) {
         k = rawp ? (u64)(asc ? raw[i] : mr - raw[i]) : kin[i];
         val = rawp ? (u32)i : vin[i];
       }
@@ -1544,8 +1563,9 @@ __device__ void pack_small_cta(Work* w, Queue Q, Lsd L, mars_scalars* sc, i32* q
 // K_AP: update_window + clamp + admit prefix + residual queue
 // ---------------------------------------------------------------------------
 
-__device__ void admit_grid(Tab t, Cfg c, Work* w, Bufs b, Queue Q, const u32* perm, int mode,
-                           bool need_seed, mars_scalars* sc, i32* qsel_p, Queue G, Xchg x) {
+__device__ void admit_grid(Tab t, Cfg c, Work* w, Bufs b, Queue Q, const u32* perm,
+                           const u64* sorted_keys, int mode, bool need_seed, mars_scalars* sc,
+                           i32* qsel_p, Queue G, Xchg x) {
   PTIME(12);
   __shared__ long long shl[32];
   cg::grid_group grid = cg::this_grid();
@@ -1564,6 +1584,14 @@ __device__ void admit_grid(Tab t, Cfg c, Work* w, Bufs b, Queue Q, const u32* pe
     has_seed = true;
     if (mode == PACK_FF) {
       seed = w->ff_median;
+    } else if (sorted_keys != nullptr) {
+      // statistics.median of req (control.py:183-186) straight from the
+      // sorted keys (req, or max_req - req descending): one load, no gather
+      const u64 ka = sorted_keys[(qlen - 1) / 2], kb = sorted_keys[qlen / 2];
+      const i64 mr = w->max_req;
+      const i64 r1 = mode == PACK_ASC ? (i64)ka : mr - (i64)ka;
+      const i64 r2 = mode == PACK_ASC ? (i64)kb : mr - (i64)kb;
+      seed = (qlen & 1) ? (double)r1 : (double)(r1 + r2) / 2.0;
     } else {
       i32 r1 = src_req[perm[(qlen - 1) / 2]];
       i32 r2 = src_req[perm[qlen / 2]];
@@ -1746,6 +1774,7 @@ __global__ void __launch_bounds__(1024, 1) k_control(Tab t, Cfg c, Work* w, Bufs
     big = qlen > SORT_CAP && mode != PACK_FF;
   }
   int cur;
+  const u64* lsd_keys = nullptr;
   if (big) {
     const int mx = w->tab_max_req, mn = w->tab_min_req;
     LsdArgs a;
@@ -1768,6 +1797,8 @@ __global__ void __launch_bounds__(1024, 1) k_control(Tab t, Cfg c, Work* w, Bufs
     if (blockIdx.x == 0 && threadIdx.x == 0) w->sort_path = 1;
     cur = lsd_grid_sort(L, lsd_view(w, 0), a, npass, (u32(*)[256])smem);
     if (npass == 0) grid.sync();  // (no sort barrier to order the published mode)
+    // sorted keys exist when at least one pass ran (pass 0 always does)
+    if (npass > 0) lsd_keys = L.k[cur];
   } else {
     // small queue, first fit, or a row-less queue: one CTA packs
     if (blockIdx.x == 0 && qlen > 0) pack_small_cta(w, Q, L, sc, qsel_p, G, smem);
@@ -1780,7 +1811,8 @@ __global__ void __launch_bounds__(1024, 1) k_control(Tab t, Cfg c, Work* w, Bufs
   }
   // the median seed is taken only from a non-empty queue (pack_small_cta)
   const bool need_seed = qlen > 0 && !sc->has_ema_blocks && !sc->has_blocks_seed;
-  admit_grid(t, c, w, b, Q, L.v[cur], mode, need_seed, sc, qsel_p, G, x);
+  // the grid LSD sort leaves the sorted keys next to the permutation
+  admit_grid(t, c, w, b, Q, L.v[cur], lsd_keys, mode, need_seed, sc, qsel_p, G, x);
 }
 
 // ---------------------------------------------------------------------------
@@ -2842,7 +2874,25 @@ __global__ void k_flush(u8* p, i64 n, u32 salt) {
     q[i] = (u32)i ^ salt;
 }
 
-__global__ void k_work_init(Work* w) {
+// Step head in one node: zero the work area, take this step's inputs
+// straight from the pinned host copy (mapped, UVA: a ~100-byte PCIe read, no
+// separate memset / memcpy graph nodes) and seed the min/max accumulators.
+__global__ void __launch_bounds__(1024) k_work_init(Work* w, const mars_step_in* h_in) {
+  PTIME(32);
+  static_assert(sizeof(Work) % 16 == 0 || true, "");
+  const size_t n16 = sizeof(Work) / 16;
+  uint4* p = (uint4*)w;
+  const uint4 z = make_uint4(0, 0, 0, 0);
+  for (size_t i = threadIdx.x; i < n16; i += blockDim.x) p[i] = z;
+  unsigned char* tail = (unsigned char*)w + n16 * 16;
+  for (size_t i = threadIdx.x; i < sizeof(Work) - n16 * 16; i += blockDim.x) tail[i] = 0;
+  __syncthreads();
+  {
+    const unsigned int* src = (const unsigned int*)h_in;
+    unsigned int* dst = (unsigned int*)&w->in;
+    static_assert(sizeof(mars_step_in) % 4 == 0, "step_in is word-sized");
+    for (size_t i = threadIdx.x; i < sizeof(mars_step_in) / 4; i += blockDim.x) dst[i] = src[i];
+  }
   if (threadIdx.x == 0) {
     w->tmin_win = 0xffffffffu;
     w->tmin_vic = 0xffffffffu;
@@ -2968,9 +3018,7 @@ int mars_enqueue_step(const LaunchArgs* a) {
     // ---- head: reset, k_scan (+ sharded: export the local admission list)
     if (a->prof)
       for (int k = 0; k < MARS_NUM_KTIMES; ++k) a->prof_used[k] = 0;
-    cudaMemsetAsync(a->work, 0, sizeof(Work), s);
-    cudaMemcpyAsync(a->work, a->host_in, sizeof(mars_step_in), cudaMemcpyHostToDevice, s);
-    k_work_init<<<1, 32, 0, s>>>(a->work);
+    k_work_init<<<1, 1024, 0, s>>>(a->work, a->host_in);
     launches++;
     mark(0, 0, s);
     launch_scan(a, nsm, s);
