@@ -303,7 +303,7 @@ int mars_last_launch_count(mars_ctx* ctx);
 /* per-kernel device times of the last step, recorded with CUDA events on the
  * stream each kernel runs on: [scan, expired-sort, control, walk] in ms
  * (-1 = not launched).  Profiling must be enabled before the step. */
-#define MARS_NUM_KTIMES 4
+#define MARS_NUM_KTIMES 5  /* k_scan, expired sort, k_control, k_walk, k_pack */
 int mars_set_profiling(mars_ctx* ctx, int on);
 int mars_kernel_times(mars_ctx* ctx, float* ms, int n);   /* sync */
 

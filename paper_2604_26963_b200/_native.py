@@ -157,7 +157,7 @@ _SIGS = {
     "mars_kernel_times": (i32, [C.c_void_p, P(C.c_float), C.c_int]),
 }
 
-KTIME_NAMES = ("k_scan", "k_expired_sort", "k_control", "k_walk")
+KTIME_NAMES = ("k_scan", "k_expired_sort", "k_control", "k_walk", "k_pack")
 
 EXPORTS = tuple(_SIGS)
 

@@ -28,9 +28,10 @@ struct ColSpec {
 struct mars_ctx {
   int device = 0;
   int num_sms = 148;
-  cudaStream_t stream = nullptr, side = nullptr;
+  cudaStream_t stream = nullptr, side = nullptr, side2 = nullptr;
   bool own_stream = true;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_head = nullptr, ev_pack = nullptr;
+  int pack_ctas = 20;
   mars_config hcfg;
   Cfg cfg;
   i64 max_rows = 0, max_queue = 0, n_rows = 0, alloc_rows = 0;
@@ -66,7 +67,7 @@ struct mars_ctx {
   int last_launches = 0;
   bool use_graph = false;
   cudaGraphExec_t graph_exec = nullptr;
-  long long graph_key[8] = {};
+  long long graph_key[9] = {};
   int graph_launches = 0;
   bool profiling = false;
   cudaEvent_t prof[2 * MARS_NUM_KTIMES] = {};
@@ -245,6 +246,13 @@ int mars_create(const mars_config* hcfg, int device, int64_t max_rows, int64_t m
   CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+  CK(cudaStreamCreateWithFlags(&ctx->side2, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&ctx->ev_head, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ctx->ev_pack, cudaEventDisableTiming));
+  {
+    const char* e = getenv("MARS_PACK_CTAS");  // tuning knob: 0 disables the early pack
+    if (e) ctx->pack_ctas = atoi(e);
+  }
   {
     int rc = mars_kernels_init();
     if (rc) return fail(ctx, MARS_ERR_CUDA, "kernel init: %s", cudaGetErrorString((cudaError_t)rc));
@@ -440,6 +448,9 @@ int mars_destroy(mars_ctx* ctx) {
   if (ctx->graph_exec) cudaGraphExecDestroy(ctx->graph_exec);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+  if (ctx->ev_head) cudaEventDestroy(ctx->ev_head);
+  if (ctx->ev_pack) cudaEventDestroy(ctx->ev_pack);
+  if (ctx->side2) cudaStreamDestroy(ctx->side2);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->side) cudaStreamDestroy(ctx->side);
   delete ctx;
@@ -589,6 +600,9 @@ static LaunchArgs launch_args(mars_ctx* ctx, const mars_step_in* in) {
   a.side = ctx->side;
   a.ev_fork = ctx->ev_fork;
   a.ev_join = ctx->ev_join;
+  a.side2 = ctx->side2;
+  a.ev_head = ctx->ev_head;
+  a.ev_pack = ctx->ev_pack;
   a.tab = ctx->tab;
   a.cfg = ctx->cfg;
   a.work = ctx->work;
@@ -619,6 +633,12 @@ static LaunchArgs launch_args(mars_ctx* ctx, const mars_step_in* in) {
   a.phase = 0;
   a.sharded = (in->mode & MARS_MODE_SHARDED) ? 1 : 0;
   a.x = ctx->x;
+  // pack_queue's big-list sort concurrently with k_scan: table-backed local
+  // queues only (the sharded list exists only after the exchange)
+  a.pack_ctas = ctx->pack_ctas;
+  a.pack_early = (a.control_possible && !(in->mode & (MARS_MODE_SHARDED | MARS_MODE_NO_ROWS)) &&
+                  a.queue_passes > 0 && ctx->pack_ctas > 0 && ctx->pack_ctas < ctx->num_sms / 2)
+                     ? 1 : 0;
   a.gq.row[0] = a.gq.row[1] = ctx->x.gq_row;
   a.gq.req[0] = a.gq.req[1] = ctx->x.gq_req;
   a.gq.lng[0] = a.gq.lng[1] = ctx->x.gq_lng;
@@ -646,8 +666,9 @@ int mars_step_enqueue(mars_ctx* ctx, const mars_step_in* in) {
   // whole-step CUDA graph, re-captured only when the launch shape changes
   i64 qb = 1;
   while (qb < a.queue_upper) qb <<= 1;
-  long long key[8] = {a.n_rows, a.control_possible, a.queue_passes, qb, a.exp_sort,
-                      a.exp_may_be_big, a.prof ? 1 : 0, (long long)(uintptr_t)ctx->stream};
+  long long key[9] = {a.n_rows, a.control_possible, a.queue_passes, qb, a.exp_sort,
+                      a.exp_may_be_big, a.prof ? 1 : 0, (long long)(uintptr_t)ctx->stream,
+                      a.pack_early};
   if (!ctx->graph_exec || memcmp(key, ctx->graph_key, sizeof key) != 0) {
     if (ctx->graph_exec) {
       cudaGraphExecDestroy(ctx->graph_exec);
@@ -678,6 +699,7 @@ int mars_sync(mars_ctx* ctx) {
   CK(cudaSetDevice(ctx->device));
   CK(cudaStreamSynchronize(ctx->stream));
   CK(cudaStreamSynchronize(ctx->side));
+  CK(cudaStreamSynchronize(ctx->side2));
   CK(cudaGetLastError());
   return MARS_OK;
 }

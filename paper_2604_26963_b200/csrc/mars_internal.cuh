@@ -142,7 +142,14 @@ struct Work {
   i32 n_queued_kv;  // queued rows holding KV (admission then touches reclaim state)
   u32 admit_done;   // set by k_control after admission; k_walk may wait on it
   i32 n_finish;
-  i32 sort_path;    // pack_queue: 1 grid LSD sort, 2 one CTA (mars_step_out.sort_path)
+  i32 sort_path;    // pack_queue: 1 grid LSD sort, 2 one CTA, 3 early grid LSD (k_pack)
+  // pre-step copies (k_work_init) for k_pack, which runs concurrently with
+  // k_scan (whose CTA 0 rewrites the scalars)
+  i32 pre_cpu_overloaded, pre_cpu_high_streak, pre_cpu_low_streak;
+  i32 pre_active_tools, pre_queued_tools;
+  i64 pre_queue_len;
+  // k_pack results: the packed permutation is L.v[pk_cur], keys L.k[pk_cur]
+  i32 pk_done, pk_mode, pk_cur, pk_n_long, pk_max_req, pk_min_req;
 };
 
 // variable-length step buffers

@@ -1105,6 +1105,7 @@ __device__ __forceinline__ int next_pow2(int n) {
 
 // ---------------------------------------------------------------------------
 // generic multi-CTA stable LSD radix sort (u64 keys, u32 values, 8-bit digits)
+#define LSD_SEG_J 6  // entries per lane of the warp-segment ranking (chunks <= 6144)
 // control words live in Work (queue: lsd_*, expired: xlsd_*)
 // ---------------------------------------------------------------------------
 
@@ -1158,6 +1159,10 @@ __device__ LsdArgs lsd_args_from(Work* w, int which) {
 
 // Returns the buffer holding the sorted values (every CTA; CTA 0 also
 // publishes it).  wc: 32 x 256 u32 of (dynamic) shared memory.
+// SEG: compile the warp-segment ranking for mid-size chunks (the grids with
+// few CTAs: k_pack, the expired-pin sort); k_control's wide grid keeps <= 1K
+// entries per CTA and stays lean on registers without it.
+template <bool SEG>
 __device__ int lsd_grid_sort(Lsd L, LsdView v, LsdArgs a, int npass, u32 (*wc)[256]) {
   PTIME(5);
   cg::grid_group grid = cg::this_grid();
@@ -1189,6 +1194,12 @@ __device__ int lsd_grid_sort(Lsd L, LsdView v, LsdArgs a, int npass, u32 (*wc)[2
     // a chunk of <= 1024 entries (the usual case) stays in registers from
     // the histogram to the scatter: one load per entry per pass
     const bool one = e - s <= 1024;
+    // chunks up to LSD_SEG_J x 1024 entries: warp w ranks the contiguous
+    // segment [s + w*S, s + (w+1)*S) 32 entries at a time with match_any and
+    // running per-warp digit counts, all in registers -- one column scan over
+    // the warps per pass instead of one per 1024-entry batch, and the CTA
+    // histogram falls out of the warp counts
+    const bool seg = SEG && !one && e - s <= LSD_SEG_J * 1024;
     u64 k1 = 0;
     u32 v1 = 0;
     const bool has1 = one && s + tid < e;
@@ -1197,17 +1208,66 @@ __device__ int lsd_grid_sort(Lsd L, LsdView v, LsdArgs a, int npass, u32 (*wc)[2
       k1 = rawp ? (u64)(asc ? raw[i] : mr - raw[i]) : kin[i];
       v1 = rawp ? (u32)i : vin[i];
     }
-    if (tid < 256) h[tid] = 0;
-    __syncthreads();
-    if (one) {
-      if (has1) atomicAdd(&h[(k1 >> shift) & 255u], 1u);
-    } else {
-      for (int i = s + tid; i < e; i += 1024) {
-        u64 k = rawp ? (u64)(asc ? raw[i] : mr - raw[i]) : kin[i];
-        atomicAdd(&h[(k >> shift) & 255u], 1u);
+    u64 sk[LSD_SEG_J];
+    u32 sv[LSD_SEG_J], sr[LSD_SEG_J];  // sr: digit << 16 | rank in the warp (0xffffffff: none)
+    if (seg) {
+      for (int q = p; q < 32; q += 4) wc[q][d] = 0;
+      __syncthreads();
+      const int S = (((e - s) + 31) / 32 + 31) & ~31;
+      const int ws = s + wid * S, we = min(e, ws + S);
+      // every load in flight before the first rank (the ranking's warp
+      // syncs would otherwise serialise one memory round trip per batch)
+#pragma unroll
+      for (int j = 0; j < LSD_SEG_J; ++j) {
+        const int i = ws + j * 32 + lane;
+        sk[j] = 0;
+        sv[j] = 0;
+        if (i < we) {
+          sk[j] = rawp ? (u64)(asc ? raw[i] : mr - raw[i]) : kin[i];
+          sv[j] = rawp ? (u32)i : vin[i];
+        }
       }
+#pragma unroll
+      for (int j = 0; j < LSD_SEG_J; ++j) {
+        const int i = ws + j * 32 + lane;
+        const bool valid = i < we;
+        const u64 k = sk[j];
+        const u32 dig = valid ? (u32)((k >> shift) & 255u) : (256u + (u32)lane);
+        const u32 peers = __match_any_sync(FULL, dig);
+        const int leader = __ffs(peers) - 1;
+        u32 base = 0;
+        if (valid && lane == leader) {
+          base = wc[wid][dig];
+          wc[wid][dig] = base + __popc(peers);
+        }
+        base = __shfl_sync(FULL, base, leader);
+        __syncwarp();
+        sr[j] = valid ? ((dig << 16) | (base + __popc(peers & ((1u << lane) - 1u)))) : 0xffffffffu;
+      }
+      __syncthreads();
+      if (tid < 256) {  // exclusive scan over the warps; the total is the CTA histogram
+        u32 acc = 0;
+        for (int q = 0; q < 32; ++q) {
+          const u32 x = wc[q][tid];
+          wc[q][tid] = acc;
+          acc += x;
+        }
+        h[tid] = acc;
+      }
+      __syncthreads();
+    } else {
+      if (tid < 256) h[tid] = 0;
+      __syncthreads();
+      if (one) {
+        if (has1) atomicAdd(&h[(k1 >> shift) & 255u], 1u);
+      } else {
+        for (int i = s + tid; i < e; i += 1024) {
+          u64 k = rawp ? (u64)(asc ? raw[i] : mr - raw[i]) : kin[i];
+          atomicAdd(&h[(k >> shift) & 255u], 1u);
+        }
+      }
+      __syncthreads();
     }
-    __syncthreads();
     if (tid < 256) L.cnt[me * 256 + tid] = h[tid];
     if (pass == 0) PTIME(6);
     grid.sync();
@@ -1250,10 +1310,21 @@ __device__ int lsd_grid_sort(Lsd L, LsdView v, LsdArgs a, int npass, u32 (*wc)[2
         run += x[q];
       }
     }
-    for (int q = p; q < 32; q += 4) wc[q][d] = 0;
+    if (!seg)
+      for (int q = p; q < 32; q += 4) wc[q][d] = 0;
     __syncthreads();
     if (pass == 0) PTIME(8);
-    for (int base = s; base < e; base += 1024) {
+    if (seg) {
+#pragma unroll
+      for (int j = 0; j < LSD_SEG_J; ++j) {
+        if (sr[j] == 0xffffffffu) continue;
+        const u32 dg = sr[j] >> 16;
+        const u32 pos = off[dg] + wc[wid][dg] + (sr[j] & 0xffffu);
+        kout[pos] = sk[j];
+        vout[pos] = sv[j];
+      }
+    }
+    for (int base = s; base < e && !seg; base += 1024) {
       int i = base + tid;
       bool valid = i < e;
       u64 k = 0;
@@ -1309,7 +1380,7 @@ __global__ void __launch_bounds__(1024, 1) k_lsd_coop(Lsd L, Work* w, int which,
   extern __shared__ __align__(16) u32 lsd_wc[];
   LsdView v = lsd_view(w, which);
   if (!*v.big) return;  // grid-uniform
-  lsd_grid_sort(L, v, lsd_args_from(w, which), npass, (u32(*)[256])lsd_wc);
+  lsd_grid_sort<true>(L, v, lsd_args_from(w, which), npass, (u32(*)[256])lsd_wc);
 }
 
 static void launch_lsd(Lsd L, Work* w, int which, int npass, int grid, cudaStream_t s) {
@@ -1564,8 +1635,8 @@ __device__ void pack_small_cta(Work* w, Queue Q, Lsd L, mars_scalars* sc, i32* q
 // ---------------------------------------------------------------------------
 
 __device__ void admit_grid(Tab t, Cfg c, Work* w, Bufs b, Queue Q, const u32* perm,
-                           const u64* sorted_keys, int mode, bool need_seed, mars_scalars* sc,
-                           i32* qsel_p, Queue G, Xchg x) {
+                           const u64* sorted_keys, u64 keyc, int mode, bool need_seed,
+                           mars_scalars* sc, i32* qsel_p, Queue G, Xchg x) {
   PTIME(12);
   __shared__ long long shl[32];
   cg::grid_group grid = cg::this_grid();
@@ -1588,7 +1659,7 @@ __device__ void admit_grid(Tab t, Cfg c, Work* w, Bufs b, Queue Q, const u32* pe
       // statistics.median of req (control.py:183-186) straight from the
       // sorted keys (req, or max_req - req descending): one load, no gather
       const u64 ka = sorted_keys[(qlen - 1) / 2], kb = sorted_keys[qlen / 2];
-      const i64 mr = w->max_req;
+      const i64 mr = keyc ? (i64)keyc : (i64)w->max_req;
       const i64 r1 = mode == PACK_ASC ? (i64)ka : mr - (i64)ka;
       const i64 r2 = mode == PACK_ASC ? (i64)kb : mr - (i64)kb;
       seed = (qlen & 1) ? (double)r1 : (double)(r1 + r2) / 2.0;
@@ -1748,6 +1819,64 @@ __device__ void admit_grid(Tab t, Cfg c, Work* w, Bufs b, Queue Q, const u32* pe
   }
 }
 
+// refresh_pressure's CPU flag (telemetry.py:174-196) as k_scan's CTA 0 will
+// leave it this step, from the pre-step copies: pack_queue's mode
+// (control.py:109-110) is known before the table scan ends
+__device__ int cpu_overloaded_after_refresh(const Cfg& c, const Work* w) {
+  const mars_step_in in = w->in;
+  const bool probe = !(in.mode & MARS_MODE_SKIP_PROBE);
+  const int at = probe ? in.active_tools : w->pre_active_tools;
+  const int qt = probe ? in.queued_tools : w->pre_queued_tools;
+  int on = w->pre_cpu_overloaded;
+  if (in.control_due && !(in.mode & MARS_MODE_SKIP_REFRESH)) {
+    const double slots = (double)in.worker_slots;
+    const bool hi = ((double)at >= c.cpu_hi * slots) || qt > 0;
+    const bool lo = ((double)at < c.cpu_lo * slots) && qt == 0;
+    const int hs = hi ? w->pre_cpu_high_streak + 1 : 0;
+    const int ls = lo ? w->pre_cpu_low_streak + 1 : 0;
+    if (!on && hs >= c.hyst)
+      on = 1;
+    else if (on && ls >= c.hyst)
+      on = 0;
+  }
+  return on;
+}
+
+// pack_queue's stable sort of a big table-backed admission list
+// (control.py:101-122), run on a few SMs concurrently with k_scan on the
+// others: it depends only on the list (the previous step's residual plus the
+// arrivals) and on the CPU flag, not on the scan.  The descending key is
+// C - req with C = 2^(8 npass) - 1 (the same order as max_req - req, with no
+// reduction over the list first).  k_control takes the packed permutation
+// (and the sorted keys) when the mode it derives from the scan agrees; the
+// first-fit mode (every entry long) stays with k_control's CTA 0.
+__global__ void __launch_bounds__(1024, 1) k_pack(Cfg c, Work* w, Queue Q, Lsd L,
+                                                  const i32* qsel_p, int npass) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  PTIME(33);
+  const int qlen = (int)w->pre_queue_len;
+  if (!w->in.control_due || qlen <= SORT_CAP || npass < 1 || npass > 3) return;  // grid-uniform
+  const int sel = *qsel_p;
+  const i32* req = Q.req[sel];
+  const int mode = cpu_overloaded_after_refresh(c, w) ? PACK_DESC : PACK_ASC;
+  const u64 keyc = (1ull << (8 * npass)) - 1ull;  // > every req (host bound q_maxreq)
+  LsdArgs a;
+  a.n = qlen;
+  a.maxkey = keyc;
+  a.raw = req;
+  a.asc = mode == PACK_ASC;
+  a.mr = (i32)keyc;
+  a.cur = 0;
+  const int cur = lsd_grid_sort<true>(L, lsd_view(w, 0), a, npass, (u32(*)[256])smem);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    w->pk_mode = mode;
+    w->pk_cur = cur;
+    w->pk_max_req = (i32)keyc;  // the descending keys' constant
+    w->pk_done = 1;
+  }
+  PTIME(34);
+}
+
 // The control plane in one cooperative launch (grid <= #SMs - 1, the walk
 // keeps an SM): CTA 0 packs small queues / first-fit; big queues are sorted by
 // the whole grid (LSD); then update_window + clamp + admit() over the grid.
@@ -1775,6 +1904,7 @@ __global__ void __launch_bounds__(1024, 1) k_control(Tab t, Cfg c, Work* w, Bufs
   }
   int cur;
   const u64* lsd_keys = nullptr;
+  u64 lsd_keyc = 0;  // descending keys are lsd_keyc - req (0: max_req)
   if (big) {
     const int mx = w->tab_max_req, mn = w->tab_min_req;
     LsdArgs a;
@@ -1784,6 +1914,9 @@ __global__ void __launch_bounds__(1024, 1) k_control(Tab t, Cfg c, Work* w, Bufs
     a.asc = mode == PACK_ASC;
     a.mr = mx;
     a.cur = 0;
+    // k_pack sorted the list during k_scan (ascending or descending by the
+    // CPU flag; a first-fit step never reaches this branch)
+    const bool early = w->pk_done != 0 && w->pk_mode == mode;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       w->pack_mode = mode;
       w->need_seed = (!sc->has_ema_blocks && !sc->has_blocks_seed) ? 1 : 0;
@@ -1793,12 +1926,20 @@ __global__ void __launch_bounds__(1024, 1) k_control(Tab t, Cfg c, Work* w, Bufs
       w->max_req = mx;
       w->min_req = mn;
       w->lsd_maxkey = a.maxkey;
+      w->sort_path = early ? 3 : 1;
+      // the early pack derives the CPU flag from the same pre-step state
+      if (w->pk_done && w->pk_mode != mode) atomicOr(&w->status, ST_QUEUE_MISMATCH);
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) w->sort_path = 1;
-    cur = lsd_grid_sort(L, lsd_view(w, 0), a, npass, (u32(*)[256])smem);
-    if (npass == 0) grid.sync();  // (no sort barrier to order the published mode)
+    if (early) {
+      cur = w->pk_cur;
+      grid.sync();  // (orders the published mode for admission, as the sort's barriers do)
+    } else {
+      cur = lsd_grid_sort<false>(L, lsd_view(w, 0), a, npass, (u32(*)[256])smem);
+      if (npass == 0) grid.sync();  // (no sort barrier to order the published mode)
+    }
     // sorted keys exist when at least one pass ran (pass 0 always does)
     if (npass > 0) lsd_keys = L.k[cur];
+    if (early) lsd_keyc = (u64)w->pk_max_req;
   } else {
     // small queue, first fit, or a row-less queue: one CTA packs
     if (blockIdx.x == 0 && qlen > 0) pack_small_cta(w, Q, L, sc, qsel_p, G, smem);
@@ -1806,13 +1947,13 @@ __global__ void __launch_bounds__(1024, 1) k_control(Tab t, Cfg c, Work* w, Bufs
     grid.sync();
     cur = 0;
     if (npass > 0 && w->lsd_big)  // row-less big queue (reduced by pack_small_cta)
-      cur = lsd_grid_sort(L, lsd_view(w, 0), lsd_args_from(w, 0), npass, (u32(*)[256])smem);
+      cur = lsd_grid_sort<false>(L, lsd_view(w, 0), lsd_args_from(w, 0), npass, (u32(*)[256])smem);
     mode = w->pack_mode;
   }
   // the median seed is taken only from a non-empty queue (pack_small_cta)
   const bool need_seed = qlen > 0 && !sc->has_ema_blocks && !sc->has_blocks_seed;
   // the grid LSD sort leaves the sorted keys next to the permutation
-  admit_grid(t, c, w, b, Q, L.v[cur], lsd_keys, mode, need_seed, sc, qsel_p, G, x);
+  admit_grid(t, c, w, b, Q, L.v[cur], lsd_keys, lsd_keyc, mode, need_seed, sc, qsel_p, G, x);
 }
 
 // ---------------------------------------------------------------------------
@@ -2877,7 +3018,8 @@ __global__ void k_flush(u8* p, i64 n, u32 salt) {
 // Step head in one node: zero the work area, take this step's inputs
 // straight from the pinned host copy (mapped, UVA: a ~100-byte PCIe read, no
 // separate memset / memcpy graph nodes) and seed the min/max accumulators.
-__global__ void __launch_bounds__(1024) k_work_init(Work* w, const mars_step_in* h_in) {
+__global__ void __launch_bounds__(1024) k_work_init(Work* w, const mars_step_in* h_in,
+                                                   const mars_scalars* sc) {
   PTIME(32);
   static_assert(sizeof(Work) % 16 == 0 || true, "");
   const size_t n16 = sizeof(Work) / 16;
@@ -2897,6 +3039,13 @@ __global__ void __launch_bounds__(1024) k_work_init(Work* w, const mars_step_in*
     w->tmin_win = 0xffffffffu;
     w->tmin_vic = 0xffffffffu;
     w->min_req = 0x7fffffff;
+    w->pk_min_req = 0x7fffffff;
+    w->pre_cpu_overloaded = sc->cpu_overloaded;
+    w->pre_cpu_high_streak = sc->cpu_high_streak;
+    w->pre_cpu_low_streak = sc->cpu_low_streak;
+    w->pre_active_tools = sc->active_tools;
+    w->pre_queued_tools = sc->queued_tools;
+    w->pre_queue_len = sc->queue_len;
   }
 }
 
@@ -3000,6 +3149,9 @@ int mars_kernels_init() {
   if (e != cudaSuccess) return (int)e;
   e = cudaFuncSetAttribute(k_exp_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)sort_smem_bytes());
+  if (e != cudaSuccess) return (int)e;
+  e = cudaFuncSetAttribute(k_pack, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sort_smem_bytes());
   return (int)e;
 }
 
@@ -3018,10 +3170,31 @@ int mars_enqueue_step(const LaunchArgs* a) {
     // ---- head: reset, k_scan (+ sharded: export the local admission list)
     if (a->prof)
       for (int k = 0; k < MARS_NUM_KTIMES; ++k) a->prof_used[k] = 0;
-    k_work_init<<<1, 1024, 0, s>>>(a->work, a->host_in);
+    k_work_init<<<1, 1024, 0, s>>>(a->work, a->host_in, a->sc);
     launches++;
+    int scan_sms = nsm;
+    if (a->pack_early) {
+      // pack_queue's sort on `pack_ctas` SMs (second side stream), k_scan on
+      // the rest: both cooperative, together exactly one CTA per SM
+      cudaEventRecord(a->ev_head, s);
+      cudaStreamWaitEvent(a->side2, a->ev_head, 0);
+      Cfg c = a->cfg;
+      Work* w = a->work;
+      Queue Q = a->queue;
+      Lsd L = a->qlsd;
+      const i32* qsel = a->qsel;
+      int npass = a->queue_passes;
+      void* args[] = {&c, &w, &Q, &L, &qsel, &npass};
+      mark(4, 0, a->side2);
+      cudaLaunchCooperativeKernel((const void*)k_pack, dim3(a->pack_ctas), dim3(1024), args,
+                                  sort_smem_bytes(), a->side2);
+      mark(4, 1, a->side2);
+      cudaEventRecord(a->ev_pack, a->side2);
+      launches++;
+      scan_sms = nsm - a->pack_ctas;
+    }
     mark(0, 0, s);
-    launch_scan(a, nsm, s);
+    launch_scan(a, scan_sms, s);
     mark(0, 1, s);
     launches++;
     if (sharded) {
@@ -3054,6 +3227,8 @@ int mars_enqueue_step(const LaunchArgs* a) {
   launches++;
   mark(3, 1, s2);
   cudaEventRecord(a->ev_join, s2);
+  // the early pack's SMs return before any other grid-wide kernel starts
+  if (a->pack_early) cudaStreamWaitEvent(s, a->ev_pack, 0);
   if (a->exp_sort || a->exp_may_be_big) {
     mark(1, 0, s);
     if (a->exp_sort) {

@@ -5,8 +5,8 @@
 #include "mars_kv.h"
 
 struct LaunchArgs {
-  cudaStream_t stream, side;
-  cudaEvent_t ev_fork, ev_join;
+  cudaStream_t stream, side, side2;
+  cudaEvent_t ev_fork, ev_join, ev_head, ev_pack;
   Tab tab;
   Cfg cfg;
   Work* work;
@@ -22,6 +22,8 @@ struct LaunchArgs {
   int queue_passes;      // LSD passes needed for the largest queue key (0 = small only)
   i64 queue_upper;       // upper bound of the queue length at step start
   int ctl_per_cta;       // admission-list entries per k_control CTA (grid sizing)
+  int pack_early;        // pack_queue's sort runs concurrently with k_scan (k_pack)
+  int pack_ctas;         // its grid; k_scan then takes the other SMs
   int exp_sort;          // expired pins need a rank sort (table not rank-ordered)
   int exp_may_be_big;    // more than SORT_CAP pins may expire
   cudaEvent_t* prof;     // 2*MARS_NUM_KTIMES events, or null

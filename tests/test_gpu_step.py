@@ -59,11 +59,12 @@ def test_step_matches_reference_golden(i):
         assert got[k] == v, k
 
 
-# how pack_queue's sort must run: 1 grid-wide LSD radix sort (big list), 2 one
-# CTA (small list, or the first-fit mode)
-SORT_PATH = {"headroom": 1, "pressure": 1, "first_fit": 2, "desc": 2, "queue_shuffled": 1,
-             "queue_sorted": 1, "hot_req": 1, "many_equal_req": 1, "warm_req": 1,
-             "wide_req": 1, "desc_sorted": 1}
+# how pack_queue's sort must run: 3 grid-wide LSD radix sort concurrently with
+# the table scan (k_pack, big list), 1 the same inside the control plane, 2
+# one CTA (small list, or the first-fit mode)
+SORT_PATH = {"headroom": 3, "pressure": 3, "first_fit": 2, "desc": 2, "queue_shuffled": 3,
+             "queue_sorted": 3, "hot_req": 3, "many_equal_req": 3, "warm_req": 3,
+             "wide_req": 3, "desc_sorted": 3}
 
 
 @pytest.mark.parametrize("n,seed,kind", [
@@ -157,3 +158,11 @@ def test_digit_record_in_global_memory_matches_oracle(monkeypatch):
     for kind, n, seed in (("headroom", 200_000, 61), ("expired_big", 150_000, 62)):
         snap = variant(n, seed, kind)
         assert_same(device_step(snap.copy()), run_step(snap.copy()))
+
+
+@pytest.mark.parametrize("kind", ["queue_shuffled", "desc_sorted"])
+def test_pack_sort_inside_control_plane_matches_oracle(kind, monkeypatch):
+    """The big-list sort inside k_control (MARS_PACK_CTAS=0: no early k_pack)."""
+    monkeypatch.setenv("MARS_PACK_CTAS", "0")
+    snap = variant(60_000, 71, kind)
+    assert_same(device_step(snap.copy(), sort_path=1), run_step(snap.copy()))
