@@ -2427,10 +2427,21 @@ __device__ void walk_fullscan(const Cfg& c, Tab& t, WalkShared& S, i64 n_rows, d
   __syncthreads();
 }
 
+// optional: the walk's window columns, gathered for the survivors while the
+// ranking runs (the payload is a table row)
+struct WinGather {
+  const i32 *kv, *ctx, *rem;
+  const u8* phase;
+  i32 *okv, *octx, *orem;
+  u8* oph;
+  int done;  // set when the selection filled the outputs
+};
+
 // select the `k` smallest (hi, lo) keys of a global candidate list into smem,
 // sorted.  Bitonic when n <= SORT_CAP, else MSD radix refinement first.
 __device__ int cta_select_sorted(const u64* ghi, const u64* glo, const u32* gpay, int n, int k,
-                                 u64* kh, u64* kl, u32* pv, u32* hist /*256*/) {
+                                 u64* kh, u64* kl, u32* pv, u32* hist /*256*/,
+                                 WinGather* wg = nullptr) {
   if (n > k && n <= (int)blockDim.x && n <= SORT_CAP / 2) {
     // more candidates than wanted: a 256-bucket linear histogram over the
     // candidates' hi range (monotone in the key) keeps the buckets up to the
@@ -2452,6 +2463,7 @@ __device__ int cta_select_sorted(const u64* ghi, const u64* glo, const u32* gpay
     }
     const u64 mn = block_min<u64>(h, s_mm, ~0ull);
     const u64 mx = block_max<u64>(i < n ? h : 0ull, s_mm, 0ull);
+    PTIME(36);
     const double span = (double)(mx - mn);
     const double inv = span > 0.0 ? 255.0 / span : 0.0;
     u32 bk = 0;
@@ -2495,8 +2507,19 @@ __device__ int cta_select_sorted(const u64* ghi, const u64* glo, const u32* gpay
       tp[sl] = p;
     }
     __syncthreads();
+    PTIME(37);
     const int ns = s_ns;
     if (ns <= 512) {
+      // the survivors' window columns: loads in flight during the ranking
+      i32 gkv = 0, gctx = 0, grem = 0;
+      u8 gph = 0;
+      if (wg != nullptr && i < ns) {
+        const u32 r = tp[i];
+        gkv = wg->kv[r];
+        gctx = wg->ctx[r];
+        grem = wg->rem[r];
+        gph = wg->phase[r];
+      }
       // parts threads per survivor, each counting a slice of the others
       const int parts = ns <= 256 ? 4 : 2;
       const int q = i / parts, part = i % parts;
@@ -2515,8 +2538,15 @@ __device__ int cta_select_sorted(const u64* ghi, const u64* glo, const u32* gpay
           kh[rnk] = th[i];
           kl[rnk] = tl[i];
           pv[rnk] = tp[i];
+          if (wg != nullptr) {
+            wg->okv[rnk] = gkv;
+            wg->octx[rnk] = gctx;
+            wg->orem[rnk] = grem;
+            wg->oph[rnk] = gph;
+          }
         }
       }
+      if (wg != nullptr && i == 0) wg->done = 1;
       __syncthreads();
       return k;
     }
@@ -2680,6 +2710,7 @@ __global__ void __launch_bounds__(WALK_TPB) k_walk(Tab t, Cfg c, Work* w, Bufs b
   i32* fs_blk = (i32*)(((uintptr_t)(fs_pin + FS_CAP) + 15) & ~(uintptr_t)15);
 
   const double now = w->in.now;
+  const long long freeb0 = threadIdx.x == 0 ? sc->free_blocks : 0;  // in flight early
   PTIME(16);
   // Admission runs concurrently on the side stream.  Admitted sessions hold no
   // KV (fresh arrivals), so they are never reclaim victims; they can only join
@@ -2706,18 +2737,35 @@ __global__ void __launch_bounds__(WALK_TPB) k_walk(Tab t, Cfg c, Work* w, Bufs b
     __syncthreads();
   }
   // 1. window = top-k of the candidates (k_scan + admitted rows)
+  PTIME(35);
   int nwc = w->n_wc;
-  int nwin = cta_select_sorted(b.wc_hi, b.wc_lo, b.wc_row, nwc, c.window, kh, kl, pv, hist);
+  __shared__ WinGather wg;
+  if (threadIdx.x == 0) {
+    wg.kv = t.kv;
+    wg.ctx = t.ctx;
+    wg.rem = t.rem;
+    wg.phase = t.phase;
+    wg.okv = S.wkv;
+    wg.octx = S.wctx;
+    wg.orem = S.wrem;
+    wg.oph = S.wph;
+    wg.done = 0;
+  }
+  __syncthreads();
+  int nwin = cta_select_sorted(b.wc_hi, b.wc_lo, b.wc_row, nwc, c.window, kh, kl, pv, hist, &wg);
   PTIME(24);
+  const bool gathered = wg.done != 0;
   for (int i = threadIdx.x; i < nwin; i += blockDim.x) {
     u32 r = pv[i];
     S.whi[i] = kh[i];
     S.wlo[i] = kl[i];
     S.wrow[i] = r;
-    S.wkv[i] = t.kv[r];
-    S.wctx[i] = t.ctx[r];
-    S.wrem[i] = t.rem[r];
-    S.wph[i] = t.phase[r];
+    if (!gathered) {
+      S.wkv[i] = t.kv[r];
+      S.wctx[i] = t.ctx[r];
+      S.wrem[i] = t.rem[r];
+      S.wph[i] = t.phase[r];
+    }
     S.wplanned[i] = 0;
     t.winpos[r] = (int16_t)i;
     b.win_rows[i] = r;
@@ -2729,7 +2777,7 @@ __global__ void __launch_bounds__(WALK_TPB) k_walk(Tab t, Cfg c, Work* w, Bufs b
     S.sub = 0;
     S.ndec = S.npre = S.nev = S.nj = 0;
     S.total = 0;
-    S.freeb = sc->free_blocks;
+    S.freeb = freeb0;
     S.stream_ready = 0;
     S.stream_len = 0;
     S.stream_first = 0;
