@@ -636,8 +636,13 @@ static LaunchArgs launch_args(mars_ctx* ctx, const mars_step_in* in) {
   // pack_queue's big-list sort concurrently with k_scan: table-backed local
   // queues only (the sharded list exists only after the exchange)
   a.pack_ctas = ctx->pack_ctas;
+  // only lists the few pack CTAs rank in one warp-segment batch per pass
+  // (<= LSD_SEG_J x 1024 entries each); longer lists sort on the whole grid
+  // inside k_control, after the scan
   a.pack_early = (a.control_possible && !(in->mode & (MARS_MODE_SHARDED | MARS_MODE_NO_ROWS)) &&
-                  a.queue_passes > 0 && ctx->pack_ctas > 0 && ctx->pack_ctas < ctx->num_sms / 2)
+                  a.queue_passes > 0 && a.queue_passes <= 3 && ctx->pack_ctas > 0 &&
+                  ctx->pack_ctas < ctx->num_sms / 2 &&
+                  ctx->q_upper <= (i64)ctx->pack_ctas * PACK_SEG_ENTRIES)
                      ? 1 : 0;
   a.gq.row[0] = a.gq.row[1] = ctx->x.gq_row;
   a.gq.req[0] = a.gq.req[1] = ctx->x.gq_req;

@@ -24,6 +24,7 @@ typedef int64_t i64;
 #define MAX_SCAN_CTAS 1024    // upper bound of k_scan's grid
 #define ROW_PAD 2048          // row capacity is padded to this multiple
 #define MAXH 0x0FFFFFFFull    // 28-bit complement base for -blocks in victim keys
+#define PACK_SEG_ENTRIES 6144 // list entries one k_pack CTA ranks per pass (LSD_SEG_J x 1024)
 
 // pack modes (control.py:101-122)
 #define PACK_ASC 0

@@ -1105,7 +1105,7 @@ __device__ __forceinline__ int next_pow2(int n) {
 
 // ---------------------------------------------------------------------------
 // generic multi-CTA stable LSD radix sort (u64 keys, u32 values, 8-bit digits)
-#define LSD_SEG_J 6  // entries per lane of the warp-segment ranking (chunks <= 6144)
+#define LSD_SEG_J (PACK_SEG_ENTRIES / 1024)  // entries per lane of the warp-segment ranking
 // control words live in Work (queue: lsd_*, expired: xlsd_*)
 // ---------------------------------------------------------------------------
 
