@@ -273,18 +273,36 @@ def cpu_reference(sessions: int, seed: int, reps: int = 1):
     return times
 
 
+def _ref_worker(job):
+    n, seed = job
+    return cpu_reference(n, seed=seed)[0]
+
+
 def run_reference_arm(a):
+    """The reference's CPU path on every host core it can use: the port is
+    single-threaded CPython, so P processes each run one full step over their
+    own n-session sample concurrently (data-parallel replicas, as the GPU
+    replicas are); a step's time is the slowest process's (materialisation
+    excluded), throughput = P x n / that time."""
+    import multiprocessing as mp
+
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     n = a.ref_sample
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except AttributeError:
+        cores = os.cpu_count() or 1
+    procs = max(1, min(a.ref_procs, cores)) if a.ref_procs > 0 else max(1, min(16, cores))
     times = []
-    for i in range(a.warmup + a.steps):
-        t = cpu_reference(n, seed=100 + i)[0]
-        if i >= a.warmup:
-            times.append(t)
+    with mp.get_context("fork").Pool(procs) as pool:
+        for i in range(a.warmup + a.steps):
+            ts = pool.map(_ref_worker, [(n, 100 + i * procs + j) for j in range(procs)])
+            if i >= a.warmup:
+                times.append(max(ts))
     per = sum(times) / len(times)
-    val = n / per
+    val = procs * n / per
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "sessions/s",
         "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": per * 1e3,
@@ -293,10 +311,12 @@ def run_reference_arm(a):
         "config": {"workload": "one MARS scheduling step (expiry, probe, admission, aging, "
                                "window top-128, build_plan walk, S2 retention)",
                    "sessions": a.sessions, "pool": "headroom", "parallelism": "replicas"},
-        "cpu_baseline": {"value": val, "unit": "sessions/s", "cores": 1, "kind": "port",
-                         "sample": f"one full step over a {n}-session snapshot_v1 (fresh seed per "
-                                   "step), object-level CPython restatement of agentsched "
-                                   "(oracle/), materialisation excluded"},
+        "cpu_baseline": {"value": val, "unit": "sessions/s", "cores": procs, "kind": "port",
+                         "sample": f"{procs} processes, each one full step over its own "
+                                   f"{n}-session snapshot_v1 (fresh seed per step) with the "
+                                   "object-level CPython restatement of agentsched (oracle/), "
+                                   "materialisation excluded; step time = slowest process",
+                         "host_cores": cores},
         "e2e": {"value": val, "unit": "sessions/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -311,6 +331,8 @@ def main():
     ap.add_argument("--sessions", type=int, default=1_000_000)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--ref-sample", type=int, default=100_000)
+    ap.add_argument("--ref-procs", type=int, default=0,
+                    help="reference-arm processes (0: every host core, at most 16)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--flush-mb", type=int, default=512)
