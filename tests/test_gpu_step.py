@@ -166,3 +166,35 @@ def test_pack_sort_inside_control_plane_matches_oracle(kind, monkeypatch):
     monkeypatch.setenv("MARS_PACK_CTAS", "0")
     snap = variant(60_000, 71, kind)
     assert_same(device_step(snap.copy(), sort_path=1), run_step(snap.copy()))
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 17, 129, 2049, 4097])
+@pytest.mark.parametrize("pool", ["headroom", "pressure"])
+def test_tiny_tables_match_oracle(n, pool):
+    """Edge sizes: fewer rows than the window, one TMA round, a partial last
+    round, the small-queue pack, one row per CTA."""
+    snap = snapshot_v1(n, seed=1000 + n, pool=pool)
+    assert_same(device_step(snap.copy()), run_step(snap.copy()))
+
+
+@pytest.mark.parametrize("policy", ["fcfs", "program_priority", "static_ttl"])
+@pytest.mark.parametrize("n", [3, 129, 4097])
+def test_tiny_tables_comparison_policies_match_oracle(policy, n):
+    snap = comparison_variant(n, 2000 + n, policy, "pressure")
+    assert_same(device_step(snap.copy(), control_due=False, policy=policy),
+                run_step(snap.copy(), control_due=False, policy=policy))
+
+
+def test_no_ready_rows_matches_oracle():
+    """Every session waits for admission or sits in a tool call: no window."""
+    from paper_2604_26963_b200.snapshot import DECODE, PREFILL, TOOL
+
+    snap = snapshot_v1(5000, seed=77, pool="headroom")
+    c = snap.cols
+    ready = (c["phase"] == DECODE) | (c["phase"] == PREFILL)
+    held = (-(-c["kv"][ready].astype(np.int64) // 16)).sum()
+    c["phase"][ready] = TOOL
+    c["kv"][ready] = 0
+    c["flags"][ready] &= ~np.uint8(8)  # no boundary rows left
+    snap.free_blocks += int(held)
+    assert_same(device_step(snap.copy()), run_step(snap.copy()))
