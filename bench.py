@@ -352,12 +352,21 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # (validation only: MARS_BENCH_DEVICE pins every rank to one GPU and
+    # MARS_BENCH_BACKEND=gloo replaces NCCL, so the sharded path can be
+    # exercised end to end on a one-GPU box; never used for a bench number)
+    if os.environ.get("MARS_BENCH_DEVICE") is not None:
+        local = int(os.environ["MARS_BENCH_DEVICE"])
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("MARS_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     def barrier():
         if dist is not None:
@@ -365,7 +374,17 @@ def main():
         torch.cuda.synchronize()
 
     snap = snapshot_v1(a.sessions, seed=rank, pool="headroom")
-    eng = MarsEngine(max_rows=snap.n, max_queue=max(len(snap.queue), 1), device=local,
+    qcap = max(len(snap.queue), 1)
+    qlens = [len(snap.queue)]
+    if dist is not None:
+        # the exchange buffers (1 + 2 x queue capacity words) must have the
+        # same size on every rank: size them by the longest shard list
+        ql = torch.tensor([len(snap.queue)], dtype=torch.int64, device="cuda")
+        allq = [torch.zeros_like(ql) for _ in range(world)]
+        dist.all_gather(allq, ql)
+        qlens = [int(x.item()) for x in allq]
+        qcap = max(max(qlens), 1)
+    eng = MarsEngine(max_rows=snap.n, max_queue=qcap, device=local,
                      config=make_config(initial_window=snap.initial_window))
     eng.load_snapshot(snap)
     si = eng.step_in(snap.now, True, snap.active_tools, snap.queued_tools, snap.worker_slots)
@@ -385,10 +404,7 @@ def main():
         # plane runs on NCCL-reduced counters and the all-gathered union list
         from paper_2604_26963_b200.dist import COUNTERS, ShardedEngine, exchange, interleaved_gpos
 
-        ql = torch.tensor([len(snap.queue)], dtype=torch.int64, device="cuda")
-        allq = [torch.zeros_like(ql) for _ in range(world)]
-        dist.all_gather(allq, ql)
-        gpos = interleaved_gpos([int(x.item()) for x in allq])[rank]
+        gpos = interleaved_gpos(qlens)[rank]
         sh = ShardedEngine(eng, world=world, rank=rank)
         stream = sh.stream
         torch.cuda.set_stream(stream)

@@ -3151,6 +3151,14 @@ static size_t sort_smem_bytes() { return (size_t)SORT_CAP * (8 + 8 + 4); }
 
 // k_scan geometry: <= 1 CTA per SM, contiguous row ranges of `chunk` rows
 // (a multiple of SCAN_RPT), the digit record in shared memory when it fits
+static int g_debug_launch = 0;  // MARS_DEBUG_LAUNCH=1: report each failing launch by name
+
+static void lchk(const char* name) {
+  if (!g_debug_launch) return;
+  const cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) fprintf(stderr, "mars: launch of %s failed: %s\n", name, cudaGetErrorString(e));
+}
+
 static int g_dig_global = 0;  // MARS_DIG_GLOBAL=1: digit record in global memory (tests)
 
 static void scan_geometry(i64 n, int nsm, int* grid, i64* chunk, int* in_smem) {
@@ -3184,6 +3192,8 @@ int mars_kernels_init() {
   {
     const char* v = getenv("MARS_DIG_GLOBAL");
     g_dig_global = (v && v[0] == '1') ? 1 : 0;
+    const char* d = getenv("MARS_DEBUG_LAUNCH");
+    g_debug_launch = (d && d[0] == '1') ? 1 : 0;
   }
   cudaError_t e;
   e = cudaFuncSetAttribute(k_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -3219,6 +3229,7 @@ int mars_enqueue_step(const LaunchArgs* a) {
     if (a->prof)
       for (int k = 0; k < MARS_NUM_KTIMES; ++k) a->prof_used[k] = 0;
     k_work_init<<<1, 1024, 0, s>>>(a->work, a->host_in, a->sc);
+    lchk("k_work_init");
     launches++;
     int scan_sms = nsm;
     if (a->pack_early) {
@@ -3236,6 +3247,7 @@ int mars_enqueue_step(const LaunchArgs* a) {
       mark(4, 0, a->side2);
       cudaLaunchCooperativeKernel((const void*)k_pack, dim3(a->pack_ctas), dim3(1024), args,
                                   sort_smem_bytes(), a->side2);
+      lchk("k_pack");
       mark(4, 1, a->side2);
       cudaEventRecord(a->ev_pack, a->side2);
       launches++;
@@ -3243,10 +3255,12 @@ int mars_enqueue_step(const LaunchArgs* a) {
     }
     mark(0, 0, s);
     launch_scan(a, scan_sms, s);
+    lchk("k_scan");
     mark(0, 1, s);
     launches++;
     if (sharded) {
       k_export_queue<<<nsm, 256, 0, s>>>(a->queue, a->qsel, a->sc, a->x, a->work);
+      lchk("k_export_queue");
       launches++;
     }
     if (a->phase == 1) return launches;
@@ -3255,6 +3269,7 @@ int mars_enqueue_step(const LaunchArgs* a) {
   if (sharded) {
     k_global_control<<<1, 32, 0, s>>>(a->cfg, a->work, a->sc, a->x);
     k_build_global_queue<<<nsm, 256, 0, s>>>(a->work, a->x);
+    lchk("k_global_control / k_build_global_queue");
     launches += 2;
   }
   // The walk runs on the side stream, concurrently with the main stream's
@@ -3272,6 +3287,7 @@ int mars_enqueue_step(const LaunchArgs* a) {
   mark(3, 0, s2);
   k_walk<<<1, WALK_TPB, walk_smem_bytes(), s2>>>(a->tab, a->cfg, a->work, a->bufs, a->sc, n,
                                                  a->control_possible);
+  lchk("k_walk");
   launches++;
   mark(3, 1, s2);
   cudaEventRecord(a->ev_join, s2);
@@ -3281,12 +3297,14 @@ int mars_enqueue_step(const LaunchArgs* a) {
     mark(1, 0, s);
     if (a->exp_sort) {
       k_exp_small<<<1, 1024, sort_smem_bytes(), s>>>(a->work, a->bufs, a->xlsd);
+      lchk("k_exp_small");
       launches++;
     }
     if (a->exp_may_be_big) {
       launch_lsd(a->xlsd, a->work, 1, 4, nsm - 1, s);  // the walk keeps one SM
       launches++;
       k_exp_gather<<<nsm, 256, 0, s>>>(a->work, a->bufs, a->xlsd);
+      lchk("k_lsd_coop / k_exp_gather");
       launches++;
     }
     mark(1, 1, s);
@@ -3309,6 +3327,7 @@ int mars_enqueue_step(const LaunchArgs* a) {
     mark(2, 0, s);
     cudaLaunchCooperativeKernel((const void*)k_control, dim3(lg), dim3(1024), args,
                                 sort_smem_bytes(), s);
+    lchk("k_control");
     mark(2, 1, s);
     launches++;
   }
