@@ -198,3 +198,13 @@ def test_no_ready_rows_matches_oracle():
     c["flags"][ready] &= ~np.uint8(8)  # no boundary rows left
     snap.free_blocks += int(held)
     assert_same(device_step(snap.copy()), run_step(snap.copy()))
+
+
+def test_pack_sort_inside_control_plane_multi_batch(monkeypatch):
+    """The in-control LSD with ~4K list entries per CTA (the sharded union
+    list's regime): several 1024-entry scatter batches per CTA and pass."""
+    monkeypatch.setenv("MARS_PACK_CTAS", "0")
+    monkeypatch.setenv("MARS_CTL_PER_CTA", "4096")
+    for kind in ("queue_shuffled", "desc_sorted", "hot_req"):
+        snap = variant(200_000, 72, kind)
+        assert_same(device_step(snap.copy(), sort_path=1), run_step(snap.copy()))
