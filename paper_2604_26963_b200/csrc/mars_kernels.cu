@@ -39,7 +39,7 @@ namespace cg = cooperative_groups;
 #ifdef MARS_PHASE_TIMING
 // Debug builds only (-DMARS_PHASE_TIMING): per-CTA %globaltimer stamps at
 // named points of the step, dumped as a timeline after each step.
-#define PT_SLOTS 40
+#define PT_SLOTS 48
 __device__ unsigned long long g_ptime[1024][PT_SLOTS];
 __device__ __forceinline__ void ptime(int k) {
   if (threadIdx.x == 0) {
@@ -825,6 +825,7 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
       }
     }
     if (!staged) __syncthreads();
+    PTIME(40);
     // (B) row ids: local lists (staged) or the global lists
     const unsigned long long wtot = __shfl_sync(FULL, incl, 31);
     const u32 wetot = __shfl_sync(FULL, eincl, 31);
@@ -880,6 +881,7 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
       }
     }
     __syncthreads();
+    PTIME(41);
     // (C) gathers; staged: records in shared memory, else straight to global
     for (int k = threadIdx.x; k < ntot; k += blockDim.x) {
       u32 r;
@@ -977,6 +979,7 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
         s_base[2] = gb2;
       }
       __syncthreads();
+      PTIME(42);
       // (D) staged records and row ids -> the global lists
       const int bw = s_base[0], bv = s_base[1], bb = s_base[2];
       for (int k = threadIdx.x; k < nw + nv + nb; k += blockDim.x) {
