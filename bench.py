@@ -337,8 +337,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--flush-mb", type=int, default=512)
     ap.add_argument("--no-kv", action="store_true", help="skip the KV evict/restore sweep")
-    ap.add_argument("--hbm-sweep", default="4000000,16000000,64000000",
-                    help="table sizes for the beyond-L2 sweep (comma list, '' to skip)")
+    ap.add_argument("--hbm-sweep", default="100000,4000000,16000000,64000000",
+                    help="table sizes for the size sweep: SURVEY config (2) at 100K, then beyond L2 (comma list, '' to skip)")
     a = ap.parse_args()
     if a.impl == "reference":
         return run_reference_arm(a)
