@@ -36,7 +36,7 @@ extern "C" {
 #define MARS_ERR_CAPACITY 3
 #define MARS_ERR_ARG 4
 
-#define MARS_ABI_VERSION 2
+#define MARS_ABI_VERSION 3
 
 /* phase codes: agentsched/engine.py:250-256 */
 #define MARS_WAITING_ADMISSION 0
@@ -122,6 +122,7 @@ typedef struct mars_cols {
       *preempt;
   int64_t *served;
   uint32_t *rank;
+  int32_t *rounds_left;  /* rounds after the current one (Call.is_last_round, engine.py:302-304) */
 } mars_cols;
 
 /* Device-resident scalar state: KvPool counters, the Telemetry value
@@ -158,6 +159,12 @@ typedef struct mars_scalars {
 #define MARS_MODE_SHARDED 128         /* this context is one replica of a sharded engine:
                                          the control plane runs on all-reduced counters and
                                          the all-gathered admission list (mars_step_phase) */
+#define MARS_MODE_ADVANCE 256         /* the tick's tail on the device after the plan:
+                                         step_gpu (engine.py:459-514) on the planned rows,
+                                         then each ending round in decode order
+                                         (sim.py:233-279: note_round_blocks, DONE + free on
+                                         the last round, else the retention decision's pin
+                                         or free, phase TOOL).  Implies SERVICE. */
 
 typedef struct mars_step_in {
   double now;
@@ -196,6 +203,8 @@ typedef struct mars_step_out {
    * left the prefix-sum fast path; how pack_queue sorted the list (0 not
    * run, 1 grid LSD radix sort, 2 one CTA: small list or first fit) */
   int32_t n_window_cand, n_victim_cand, walk_slow, sort_path;
+  /* MARS_MODE_ADVANCE: rounds that ended this tick, sessions that finished */
+  int32_t n_round_end, n_done;
 } mars_step_out;
 
 /* ---- lifecycle ------------------------------------------------------- */

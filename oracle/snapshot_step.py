@@ -26,8 +26,8 @@ from typing import Dict, List, Optional
 import numpy as np
 
 from . import admission as adm
-from .core import (DECODE, PREFILL, BlockCounter, Journal, Round, Session, TickModel,
-                   ceil_div, submit_round)
+from .core import (DECODE, DONE, PREFILL, TOOL, BlockCounter, Clock, Journal, Round, Session,
+                   TickModel, ceil_div, execute_tick, submit_round)
 from .policy import MarsOracle, Mlfq, Pin, Prio, Retention, make_oracle_policy, retention
 
 PHASES = ("waiting_admission", "prefill", "decode", "tool", "waiting_resume", "done")
@@ -91,13 +91,15 @@ class World:
         pb = c["pinned_blocks"].tolist()
         plv = c["plevel"].tolist()
         pre = c["preempt"].tolist()
+        rl = c["rounds_left"].tolist() if "rounds_left" in c else [0] * n
         alloc = self.pool.allocated
         pinned = self.pool.pinned
         used = 0
         for i in range(n):
             sid = sid_of(rank[i])
-            s = Session(sid, [Round(r0p[i] if r0p[i] > 0 else 1, r0d[i] if r0d[i] > 0 else 1)],
-                        arr[i])
+            rounds = [Round(r0p[i] if r0p[i] > 0 else 1, r0d[i] if r0d[i] > 0 else 1)]
+            rounds += [Round(1, 1)] * int(rl[i])  # rounds after the current one
+            s = Session(sid, rounds, arr[i])
             s.phase = PHASES[ph[i]] if ph[i] < 6 else "done"
             s.context_tokens = ctx[i]
             s.kv_tokens = kv[i]
@@ -283,3 +285,58 @@ def extract_state(w: World) -> Dict[str, np.ndarray]:
         st["rem_decode"][i] = s.remaining_decode
         st["preempt"][i] = s.preemptions
     return st
+
+
+def finish_round(w: World, s: Session, now: float) -> None:
+    """sim.py:233-279 without the event log and the tool plane (tools are the
+    host's): note_round_blocks, DONE + free on the last round, else the
+    policy's retention decision -- pin or free -- and phase TOOL."""
+    sid = s.session_id
+    pool, tel, pol = w.pool, w.tel, w.policy
+    held = s.held_blocks(pool.block_size)
+    tel.note_round_blocks(ceil_div(s.context_tokens, pool.block_size),
+                          smoothing=w.pressure.ema_smoothing)
+    if s.is_last_round:
+        s.set_phase(DONE)
+        pool.free(sid)
+        s.kv_tokens = 0
+        del w.active[sid]
+        return
+    d = pol.retention_decision(s, pool, tel, w.gpu, now)
+    if d is not None and d.pin and held > 0:
+        pool.pin(sid)
+        s.pinned = True
+        s.retention_deadline = d.retention_deadline
+        pol.note_pin(s, d, held, now)
+    else:
+        pool.free(sid)
+        s.kv_tokens = 0
+    s.set_phase(TOOL)
+
+
+def run_ticks(snap, ticks: int, control_ticks=(0,), **kw):
+    """Consecutive ticks over one snapshot: each tick's scheduling half
+    (run_step), then step_gpu on the plan (engine.py:459-514) and the tick's
+    tail in progress order (sim.py:355-375: on_service, finish_round).  The
+    clock advances by one tick per tick.  Returns each tick's canonical output
+    (the last one carries the end-of-run table state) and the World."""
+    w = World(snap, **kw)
+    clock = Clock()
+    clock.now = snap.now
+    outs = []
+    for k in range(ticks):
+        snap.now = clock.now
+        out = run_step(snap, control_due=k in control_ticks, world=w)
+        out.pop("state")
+        sess = w.sessions
+        batch = [(sess[r], 0, True) for r in out["decodes"]]
+        batch += [(sess[r], g, False) for r, g in out["prefills"]]
+        prog = execute_tick(clock, w.gpu, batch)
+        end = clock.now
+        for (sid, pf, dd, _pdone, rdone) in prog:
+            w.policy.on_service(sid, pf + dd, end)
+            if rdone:
+                finish_round(w, w.policy.calls[sid], end)
+        outs.append(out)
+    outs[-1]["state"] = extract_state(w)
+    return outs, w

@@ -47,7 +47,7 @@ class MarsCols(C.Structure):
         ("deadline", P(f64)), ("arrival", P(f64)), ("context", P(i32)), ("kv", P(i32)),
         ("rem_decode", P(i32)), ("pinned_blocks", P(i32)), ("req_blocks", P(i32)),
         ("r0_prefill", P(i32)), ("r0_decode", P(i32)), ("preempt", P(i32)),
-        ("served", P(i64)), ("rank", P(u32)),
+        ("served", P(i64)), ("rank", P(u32)), ("rounds_left", P(i32)),
     ]
 
 
@@ -58,7 +58,7 @@ COL_FIELDS = {
     "deadline": "deadline", "arrival": "arrival", "context": "context", "kv": "kv",
     "rem_decode": "rem_decode", "pinned_blocks": "pinned_blocks", "req_blocks": "req_blocks",
     "r0_prefill": "r0_prefill", "r0_decode": "r0_decode", "preempt": "preempt",
-    "served": "served", "rank": "rank",
+    "served": "served", "rank": "rank", "rounds_left": "rounds_left",
 }
 
 
@@ -90,6 +90,7 @@ class MarsStepIn(C.Structure):
 
 MODE_SKIP_EXPIRY, MODE_SKIP_PROBE, MODE_SKIP_REFRESH, MODE_NO_ROWS = 1, 2, 4, 8
 MODE_SERVICE, MODE_FINISH_RETENTION, MODE_RANK_ORDERED, MODE_SHARDED = 16, 32, 64, 128
+MODE_ADVANCE = 256
 XC_N = 8
 
 
@@ -110,7 +111,7 @@ class MarsStepOut(C.Structure):
         ("fin_rows", P(u32)), ("fin_pin", P(u8)), ("fin_benefit", P(f64)),
         ("fin_cost", P(f64)), ("fin_deadline", P(f64)),
         ("n_window_cand", i32), ("n_victim_cand", i32), ("walk_slow", i32),
-        ("sort_path", i32),
+        ("sort_path", i32), ("n_round_end", i32), ("n_done", i32),
     ]
 
 

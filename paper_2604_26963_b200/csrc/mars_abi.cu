@@ -67,7 +67,7 @@ struct mars_ctx {
   int last_launches = 0;
   bool use_graph = false;
   cudaGraphExec_t graph_exec = nullptr;
-  long long graph_key[9] = {};
+  long long graph_key[10] = {};
   int graph_launches = 0;
   bool profiling = false;
   cudaEvent_t prof[2 * MARS_NUM_KTIMES] = {};
@@ -280,6 +280,8 @@ int mars_create(const mars_config* hcfg, int device, int64_t max_rows, int64_t m
   ALLOC(t.pre, R * 4);
   ALLOC(t.served, R * 8);
   ALLOC(t.rank, R * 4);
+  ALLOC(t.rleft, R * 4);
+  CK(cudaMemset(t.rleft, 0, R * 4));
   ALLOC(t.winpos, R * 2);
   CK(cudaMemset(t.winpos, 0xff, R * 2));
   CK(cudaMemset(t.phase, MARS_EMPTY, R));
@@ -386,6 +388,7 @@ int mars_create(const mars_config* hcfg, int device, int64_t max_rows, int64_t m
   add(offsetof(mars_cols, preempt), (void**)&t.pre, 4);
   add(offsetof(mars_cols, served), (void**)&t.served, 8);
   add(offsetof(mars_cols, rank), (void**)&t.rank, 4);
+  add(offsetof(mars_cols, rounds_left), (void**)&t.rleft, 4);
   CK(cudaDeviceSynchronize());
   *out = ctx;
   return MARS_OK;
@@ -636,6 +639,7 @@ static LaunchArgs launch_args(mars_ctx* ctx, const mars_step_in* in) {
   // pack_queue's big-list sort concurrently with k_scan: table-backed local
   // queues only (the sharded list exists only after the exchange)
   a.pack_ctas = ctx->pack_ctas;
+  a.advance = (in->mode & MARS_MODE_ADVANCE) ? 1 : 0;
   // only lists the few pack CTAs rank in one warp-segment batch per pass
   // (<= LSD_SEG_J x 1024 entries each); longer lists sort on the whole grid
   // inside k_control, after the scan
@@ -662,6 +666,8 @@ int mars_step_enqueue(mars_ctx* ctx, const mars_step_in* in) {
     return fail(ctx, MARS_ERR_ARG, "the comparison policies have no admission control");
   CK(cudaSetDevice(ctx->device));
   *ctx->h_in = *in;
+  // the device tick tail includes the tick-end MLFQ charges (sim.py:364)
+  if (in->mode & MARS_MODE_ADVANCE) ctx->h_in->mode |= MARS_MODE_SERVICE;
   LaunchArgs a = launch_args(ctx, in);
   if (!ctx->use_graph || ctx->profiling) {  // event timing does not work inside graphs
     ctx->last_launches = mars_enqueue_step(&a);
@@ -671,9 +677,9 @@ int mars_step_enqueue(mars_ctx* ctx, const mars_step_in* in) {
   // whole-step CUDA graph, re-captured only when the launch shape changes
   i64 qb = 1;
   while (qb < a.queue_upper) qb <<= 1;
-  long long key[9] = {a.n_rows, a.control_possible, a.queue_passes, qb, a.exp_sort,
-                      a.exp_may_be_big, a.prof ? 1 : 0, (long long)(uintptr_t)ctx->stream,
-                      a.pack_early};
+  long long key[10] = {a.n_rows, a.control_possible, a.queue_passes, qb, a.exp_sort,
+                       a.exp_may_be_big, a.prof ? 1 : 0, (long long)(uintptr_t)ctx->stream,
+                       a.pack_early, a.advance};
   if (!ctx->graph_exec || memcmp(key, ctx->graph_key, sizeof key) != 0) {
     if (ctx->graph_exec) {
       cudaGraphExecDestroy(ctx->graph_exec);
@@ -781,6 +787,8 @@ int mars_step_fetch(mars_ctx* ctx, mars_step_out* o) {
   o->n_victim_cand = w.n_vc;
   o->walk_slow = w.walk_slow;
   o->sort_path = w.sort_path;
+  o->n_round_end = w.n_round_end;
+  o->n_done = w.n_done;
   o->fin_rows = (const uint32_t*)pull(ctx, off, b.fin_row, (size_t)w.n_finish * 4);
   o->fin_pin = (const uint8_t*)pull(ctx, off, b.fin_pin, (size_t)w.n_finish);
   o->fin_benefit = (const double*)pull(ctx, off, b.fin_b, (size_t)w.n_finish * 8);
@@ -796,10 +804,8 @@ int mars_step_fetch(mars_ctx* ctx, mars_step_out* o) {
     uint32_t* dst = const_cast<uint32_t*>(o->admitted_rows);
     for (i64 i = 0; i < n_adm; ++i) dst[i] = pr[i].second;
   }
-  // free_blocks after the plan
-  int64_t fb = 0;
-  CK(cudaMemcpy(&fb, &ctx->sc->free_blocks, 8, cudaMemcpyDeviceToHost));
-  o->free_blocks = fb;
+  // free_blocks after the plan (MARS_MODE_ADVANCE's tail frees come after)
+  o->free_blocks = w.free_after_plan;
   if (sharded) {
     int64_t ql = 0;
     CK(cudaMemcpy(&ql, &ctx->sc->queue_len, 8, cudaMemcpyDeviceToHost));
@@ -892,7 +898,10 @@ int mars_step_phase(mars_ctx* ctx, const mars_step_in* in, int phase) {
   if (!ctx->x.xc || !(in->mode & MARS_MODE_SHARDED))
     return fail(ctx, MARS_ERR_ARG, "mars_step_phase needs mars_shard_init + MARS_MODE_SHARDED");
   CK(cudaSetDevice(ctx->device));
-  if (phase == 1) *ctx->h_in = *in;
+  if (phase == 1) {
+    *ctx->h_in = *in;
+    if (in->mode & MARS_MODE_ADVANCE) ctx->h_in->mode |= MARS_MODE_SERVICE;
+  }
   LaunchArgs a = launch_args(ctx, ctx->h_in);
   a.phase = phase;
   ctx->last_launches = mars_enqueue_step(&a) + (phase == 2 ? ctx->last_launches : 0);

@@ -63,6 +63,7 @@ struct Tab {
   i32 *ctx, *kv, *rem, *pb, *req, *r0p, *r0d, *pre;
   i64 *served;
   u32 *rank;
+  i32 *rleft;  // rounds after the current one
   int16_t *winpos;  // row -> window index during the walk, -1 otherwise
   i64 cap;
 };
@@ -144,6 +145,8 @@ struct Work {
   u32 admit_done;   // set by k_control after admission; k_walk may wait on it
   i32 n_finish;
   i32 sort_path;    // pack_queue: 1 grid LSD sort, 2 one CTA, 3 early grid LSD (k_pack)
+  i32 n_round_end, n_done;  // MARS_MODE_ADVANCE: rounds that ended, sessions that finished
+  i64 free_after_plan;      // the pool's free blocks after the plan (before the tick's tail)
   // pre-step copies (k_work_init) for k_pack, which runs concurrently with
   // k_scan (whose CTA 0 rewrites the scalars)
   i32 pre_cpu_overloaded, pre_cpu_high_streak, pre_cpu_low_streak;

@@ -3035,8 +3035,93 @@ __global__ void __launch_bounds__(WALK_TPB) k_walk(Tab t, Cfg c, Work* w, Bufs b
     w->walk_slow = S.fast_ok ? 0 : 1;
     w->status |= S.status;
     sc->free_blocks = S.freeb;
+    w->free_after_plan = S.freeb;
     PTIME(21);
   }
+}
+
+// ---------------------------------------------------------------------------
+// MARS_MODE_ADVANCE: the tick's tail on the device
+// ---------------------------------------------------------------------------
+
+// After the plan, the admission and the walk's tick-end charges (SERVICE):
+// step_gpu on the planned rows (engine.py:459-514: a grant extends the KV and
+// ends the prefill when it reaches the context; a decode slot emits one token
+// into context and KV), then every round that ended this tick, in decode order
+// as the sim walks the progress list (sim.py:355-375 -> finish_round,
+// sim.py:233-279): Telemetry.note_round_blocks (a sequential EMA fold,
+// telemetry.py:130-138), DONE and a full free on the last round, otherwise the
+// policy's retention decision on post-tick values -- pin the held blocks
+// (PinnedSession level = the post-charge level, baselines.py:386-394) or free
+// them -- and phase TOOL.  The tool plane and resume_from_tool stay with the
+// host (tool durations are trace data).  One CTA; the sequential part is at
+// most max_decode_slots rows.
+__global__ void __launch_bounds__(1024) k_advance(Tab t, Cfg c, Work* w, Bufs b,
+                                                  mars_scalars* sc) {
+  const int nd = w->n_dec, np = w->n_pre;
+  const double tick_end = w->in.now + c.tick_s;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) {
+    const u32 r = b.pre_rows[i];
+    const i32 kv = t.kv[r] + b.pre_grant[i];
+    t.kv[r] = kv;
+    if (kv == t.ctx[r]) t.phase[r] = MARS_DECODE;  // remaining_prefill == 0
+    if (c.policy == POL_PP) t.served[r] += b.pre_grant[i];  // Call.served_tokens
+  }
+  for (int i = threadIdx.x; i < nd; i += blockDim.x) {
+    const u32 r = b.dec_rows[i];
+    t.kv[r] += 1;
+    t.ctx[r] += 1;
+    t.rem[r] -= 1;
+    if (c.policy == POL_PP) t.served[r] += 1;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  i64 freeb = sc->free_blocks;
+  bool has_ema = sc->has_ema_blocks != 0;
+  double ema_b = sc->ema_blocks;
+  const i64 total = sc->total_blocks;
+  const double usage = sc->kv_usage_ratio;
+  const double ema_t = sc->has_ema_tool ? sc->ema_tool : c.tool_prior;
+  const bool decides = (c.policy == POL_MARS && c.cosched) || c.policy == POL_STATIC_TTL ||
+                       c.policy == POL_DYNAMIC_TTL;
+  int n_end = 0, n_done = 0;
+  for (int i = 0; i < nd; ++i) {
+    const u32 r = b.dec_rows[i];
+    if (t.rem[r] != 0) continue;
+    n_end++;
+    const i32 kv = t.kv[r], ctx = t.ctx[r];
+    const i64 held = held_blocks(c, kv);
+    const double x = (double)blocks_ceil(c, ctx);
+    ema_b = has_ema ? c.ema_alpha * x + (1.0 - c.ema_alpha) * ema_b : x;  // telemetry.py:59-63
+    has_ema = true;
+    const u8 f = t.flags[r];
+    if (t.rleft[r] == 0) {  // last round: DONE, every block freed
+      t.phase[r] = MARS_DONE;
+      t.flags[r] = f & ~MARS_F_ACTIVE;
+      freeb += held;
+      t.kv[r] = 0;
+      n_done++;
+      continue;
+    }
+    u8 pin = 0;
+    double bb, cc, dd = 0.0;
+    if (decides) decide_retention(c, ctx, kv, total, usage, ema_t, tick_end, pin, bb, cc, dd);
+    if (pin && held > 0) {
+      t.flags[r] = f | MARS_F_PINNED;
+      t.dl[r] = dd;
+      t.pb[r] = (i32)held;
+      t.plevel[r] = c.policy == POL_MARS && c.coord ? t.level[r] : 0;
+    } else {
+      freeb += held;
+      t.kv[r] = 0;
+    }
+    t.phase[r] = MARS_TOOL;
+  }
+  sc->free_blocks = freeb;
+  sc->has_ema_blocks = has_ema ? 1 : 0;
+  sc->ema_blocks = ema_b;
+  w->n_round_end = n_end;
+  w->n_done = n_done;
 }
 
 // ---------------------------------------------------------------------------
@@ -3335,6 +3420,10 @@ int mars_enqueue_step(const LaunchArgs* a) {
     launches++;
   }
   cudaStreamWaitEvent(s, a->ev_join, 0);
+  if (a->advance) {
+    k_advance<<<1, 1024, 0, s>>>(a->tab, a->cfg, a->work, a->bufs, a->sc);
+    launches++;
+  }
   if (a->kv) {
     mars_kv_enqueue_apply_step(*a->kv, s, a->work, a->bufs);
     launches++;

@@ -24,6 +24,7 @@ struct LaunchArgs {
   int ctl_per_cta;       // admission-list entries per k_control CTA (grid sizing)
   int pack_early;        // pack_queue's sort runs concurrently with k_scan (k_pack)
   int pack_ctas;         // its grid; k_scan then takes the other SMs
+  int advance;           // MARS_MODE_ADVANCE: k_advance after the join
   int exp_sort;          // expired pins need a rank sort (table not rank-ordered)
   int exp_may_be_big;    // more than SORT_CAP pins may expire
   cudaEvent_t* prof;     // 2*MARS_NUM_KTIMES events, or null

@@ -273,7 +273,8 @@ class MarsEngine:
             total_tokens=o.total_tokens, free_after_expiry=o.free_after_expiry,
             free_blocks=o.free_blocks, limit=o.limit, slots=o.slots,
             diag={"n_window_cand": o.n_window_cand, "n_victim_cand": o.n_victim_cand,
-                  "walk_slow": o.walk_slow, "sort_path": o.sort_path})
+                  "walk_slow": o.walk_slow, "sort_path": o.sort_path,
+                  "n_round_end": o.n_round_end, "n_done": o.n_done})
 
     def step(self, si: N.MarsStepIn) -> StepResult:
         self.enqueue(si)

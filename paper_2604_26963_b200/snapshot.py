@@ -40,7 +40,7 @@ COLUMNS = {
     "arrival": np.float64,
     "context": np.int32, "kv": np.int32, "rem_decode": np.int32, "pinned_blocks": np.int32,
     "req_blocks": np.int32, "r0_prefill": np.int32, "r0_decode": np.int32,
-    "preempt": np.int32, "served": np.int64, "rank": np.uint32,
+    "preempt": np.int32, "served": np.int64, "rank": np.uint32, "rounds_left": np.int32,
 }
 
 
@@ -159,6 +159,8 @@ def snapshot_v1(n: int, seed: int = 0, pool: str = "headroom", now: float = 1000
     flags |= np.where(waiting & long_, F_LONG, 0).astype(np.uint8)
     c["flags"][:] = flags
     queue = np.nonzero(waiting)[0].astype(np.uint32)
+    # rounds after the current one (drawn last: the other columns keep their values)
+    c["rounds_left"][:] = rng.integers(0, 4, size=n)
     return Snapshot(cols=c, queue=queue, now=float(now), total_blocks=int(total),
                     free_blocks=int(total - total_held), worker_slots=max(2 * n, 1),
                     active_tools=int(tool.sum()), queued_tools=0,
