@@ -241,6 +241,15 @@ int mars_set_graph(mars_ctx* ctx, int on);
 
 /* decide_retention (scheduler.py:190-213) for explicit inputs; elementwise f64
  * on the device, bit-exact (no FMA contraction). */
+/* resume_from_tool (sim.py:190-231) for sessions whose tools finished, in
+ * the tool plane's finish order: the tool-duration EMA fold (tool_end,
+ * telemetry.py:96-120), round_index + 1, warm resume (the pin still covers
+ * the finish time: unpin, KV kept) or cold (an expired pin is evicted),
+ * submit_round with the next round's new prefill / decode lengths, and
+ * on_resume.  Synchronous; counts out (warm, cold, pins evicted). */
+int mars_resume(mars_ctx* ctx, int64_t n, const int64_t* rows, const double* finish_time,
+                const double* duration, const int32_t* new_prefill, const int32_t* decode_tokens,
+                double now, int32_t* counts /* [3] */);
 int mars_retention_batch(mars_ctx* ctx, int64_t n, const int32_t* context, const int32_t* kv,
                          int64_t total_blocks, double kv_usage_ratio, double ema_tool,
                          double now, uint8_t* pin, double* benefit, double* cost,

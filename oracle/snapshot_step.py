@@ -26,8 +26,8 @@ from typing import Dict, List, Optional
 import numpy as np
 
 from . import admission as adm
-from .core import (DECODE, DONE, PREFILL, TOOL, BlockCounter, Clock, Journal, Round, Session,
-                   TickModel, ceil_div, execute_tick, submit_round)
+from .core import (DECODE, DONE, PREFILL, TOOL, WAITING_RESUME, BlockCounter, Clock, Journal,
+                   Round, Session, TickModel, ceil_div, execute_tick, resume_cost, submit_round)
 from .policy import MarsOracle, Mlfq, Pin, Prio, Retention, make_oracle_policy, retention
 
 PHASES = ("waiting_admission", "prefill", "decode", "tool", "waiting_resume", "done")
@@ -314,7 +314,33 @@ def finish_round(w: World, s: Session, now: float) -> None:
     s.set_phase(TOOL)
 
 
-def run_ticks(snap, ticks: int, control_ticks=(0,), **kw):
+def tool_return(w: World, s: Session, finish: float, duration: float, now: float) -> str:
+    """The tool_end record's EMA fold (telemetry.py:96-120) and
+    resume_from_tool (sim.py:190-231) on the World; returns warm / cold."""
+    w.tel.record("tool_end", {"duration_s": duration}, smoothing=w.pressure.ema_smoothing)
+    s.round_index += 1
+    s.set_phase(WAITING_RESUME)
+    warm = s.pinned and s.retention_deadline is not None and s.retention_deadline >= finish
+    need = resume_cost(s, warm)
+    if warm:
+        w.pool.unpin(s.session_id)
+        s.pinned = False
+        s.retention_deadline = None
+        w.policy.on_evicted(s.session_id)
+    elif s.pinned:  # the pin expired between grid points: evicted at return
+        w.pool.release_pinned(s.session_id)
+        s.pinned = False
+        s.retention_deadline = None
+        s.kv_tokens = 0
+        w.policy.on_evicted(s.session_id)
+    submit_round(s, now)
+    if s.remaining_prefill != need:
+        raise ValueError("resume cost mismatch")
+    w.policy.on_resume(s, now)
+    return "warm" if warm else "cold"
+
+
+def run_ticks(snap, ticks: int, control_ticks=(0,), resumes=None, **kw):
     """Consecutive ticks over one snapshot: each tick's scheduling half
     (run_step), then step_gpu on the plan (engine.py:459-514) and the tick's
     tail in progress order (sim.py:355-375: on_service, finish_round).  The
@@ -326,6 +352,12 @@ def run_ticks(snap, ticks: int, control_ticks=(0,), **kw):
     outs = []
     for k in range(ticks):
         snap.now = clock.now
+        # tools that finished before this tick: (row, finish, duration,
+        # next round's new prefill, its decode tokens), in finish order
+        for (r, fin, dur, newp, dec) in (resumes or {}).get(k, []):
+            s = w.sessions[r]
+            s.rounds[s.round_index + 1] = Round(newp, dec)
+            tool_return(w, s, fin, dur, clock.now)
         out = run_step(snap, control_due=k in control_ticks, world=w)
         out.pop("state")
         sess = w.sessions

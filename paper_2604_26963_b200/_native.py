@@ -148,6 +148,8 @@ _SIGS = {
     "mars_kv_restore": (i32, [C.c_void_p, i64, C.c_void_p, i64, C.c_int]),
     "mars_kv_host_ptr": (i32, [C.c_void_p, P(C.c_void_p), P(C.c_void_p)]),
     "mars_host_link_peak": (i32, [C.c_void_p, i64, C.c_int, P(f64), P(f64), P(f64)]),
+    "mars_resume": (i32, [C.c_void_p, i64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                          C.c_void_p, f64, C.c_void_p]),
     "mars_retention_batch": (i32, [C.c_void_p, i64, C.c_void_p, C.c_void_p, i64, f64, f64, f64,
                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "mars_checkpoint": (i32, [C.c_void_p]),

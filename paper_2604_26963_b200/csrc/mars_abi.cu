@@ -29,6 +29,7 @@ struct mars_ctx {
   int device = 0;
   int num_sms = 148;
   cudaStream_t stream = nullptr, side = nullptr, side2 = nullptr;
+  void* d_resume = nullptr;  // mars_resume staging (lazily allocated)
   bool own_stream = true;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_head = nullptr, ev_pack = nullptr;
   int pack_ctas = 20;
@@ -426,6 +427,7 @@ int mars_destroy(mars_ctx* ctx) {
                 b.flush};
   for (void* p : bs) cudaFree(p);
   cudaFree(ctx->d_stage);
+  cudaFree(ctx->d_resume);
   cudaFree(ctx->d_rows);
   for (auto& cs : ctx->cols) cudaFree(cs.ckpt);
   for (void* p : ctx->ck_q) cudaFree(p);
@@ -906,6 +908,44 @@ int mars_step_phase(mars_ctx* ctx, const mars_step_in* in, int phase) {
   a.phase = phase;
   ctx->last_launches = mars_enqueue_step(&a) + (phase == 2 ? ctx->last_launches : 0);
   CK(cudaGetLastError());
+  return MARS_OK;
+}
+
+int mars_resume(mars_ctx* ctx, int64_t n, const int64_t* rows, const double* finish_time,
+                const double* duration, const int32_t* new_prefill, const int32_t* decode_tokens,
+                double now, int32_t* counts) {
+  if (!ctx || n < 0 || !counts) return MARS_ERR_ARG;
+  counts[0] = counts[1] = counts[2] = 0;
+  if (n == 0) return MARS_OK;
+  if (n > ctx->max_rows) return MARS_ERR_CAPACITY;
+  for (i64 i = 0; i < n; ++i)
+    if (rows[i] < 0 || rows[i] >= ctx->n_rows) return fail(ctx, MARS_ERR_ARG, "resume row out of range");
+  CK(cudaSetDevice(ctx->device));
+  if (!ctx->d_resume) {
+    CK(cudaMalloc(&ctx->d_resume, (size_t)ctx->max_rows * 32 + 64));
+  }
+  unsigned char* p = (unsigned char*)ctx->d_resume;
+  i64* drows = (i64*)p;
+  double* dfin = (double*)(drows + n);
+  double* ddur = dfin + n;
+  i32* dnew = (i32*)(ddur + n);
+  i32* ddec = dnew + n;
+  int* dcnt = (int*)(ddec + ((n + 1) & ~1ll));
+  CK(cudaMemcpyAsync(drows, rows, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(dfin, finish_time, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ddur, duration, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(dnew, new_prefill, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ddec, decode_tokens, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+  int rc = mars_enqueue_resume(ctx->tab, ctx->cfg, ctx->sc, ctx->stream, n, drows, dfin, ddur,
+                               dnew, ddec, now, dcnt);
+  if (rc) return fail(ctx, MARS_ERR_CUDA, "resume: %s", cudaGetErrorString((cudaError_t)rc));
+  int hc[4] = {0, 0, 0, 0};
+  CK(cudaMemcpyAsync(hc, dcnt, sizeof hc, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  counts[0] = hc[0];
+  counts[1] = hc[1];
+  counts[2] = hc[2];
+  if (hc[3]) return fail(ctx, MARS_ERR_CONTRACT, "resume owes a prefill other than its cost");
   return MARS_OK;
 }
 

@@ -3124,6 +3124,78 @@ __global__ void __launch_bounds__(1024) k_advance(Tab t, Cfg c, Work* w, Bufs b,
   w->n_done = n_done;
 }
 
+// resume_from_tool (sim.py:190-231) for a batch of finished tools (rows are
+// distinct): per row in parallel -- round_index + 1, warm iff pinned with a
+// deadline >= the finish time (unpin, KV kept), else an expired pin is
+// evicted (release_pinned), then submit_round (context += the next round's
+// new prefill, remaining_decode, ready_since = now, PREFILL) and on_resume
+// (MARS: wait_since = now); the tool-duration EMA is folded in finish order
+// on one thread (telemetry.py:96-120).
+__global__ void __launch_bounds__(1024) k_resume(Tab t, Cfg c, mars_scalars* sc, i64 n,
+                                                 const i64* rows, const double* fin,
+                                                 const double* dur, const i32* newp,
+                                                 const i32* dec, double now, int* counts) {
+  __shared__ unsigned long long s_freed;
+  __shared__ int s_warm, s_cold, s_ev, s_bad;
+  if (threadIdx.x == 0) {
+    s_freed = 0;
+    s_warm = s_cold = s_ev = s_bad = 0;
+  }
+  __syncthreads();
+  for (i64 i = threadIdx.x; i < n; i += blockDim.x) {
+    const i64 r = rows[i];
+    const u8 f = t.flags[r];
+    const bool pinned = (f & MARS_F_PINNED) != 0;
+    const bool warm = pinned && t.dl[r] >= fin[i];
+    t.rleft[r] -= 1;
+    i32 kv = t.kv[r];
+    if (pinned) t.flags[r] = f & ~MARS_F_PINNED;  // unpin, or the return-time eviction
+    if (warm) {
+      atomicAdd(&s_warm, 1);
+    } else {
+      if (pinned) {
+        atomicAdd(&s_freed, (unsigned long long)t.pb[r]);
+        atomicAdd(&s_ev, 1);
+        kv = 0;
+        t.kv[r] = 0;
+      }
+      atomicAdd(&s_cold, 1);
+    }
+    const i64 ctx = (i64)t.ctx[r];
+    const i64 need = warm ? (i64)newp[i] : ctx + newp[i];  // resume_cost (engine.py:333-342)
+    t.ctx[r] = (i32)(ctx + newp[i]);
+    t.rem[r] = dec[i];
+    t.rs[r] = now;
+    t.phase[r] = MARS_PREFILL;
+    if (c.policy == POL_MARS) t.ws[r] = now;  // on_resume (baselines.py:357-360)
+    if (ctx + newp[i] - kv != need) atomicAdd(&s_bad, 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double ema = sc->ema_tool;
+    bool has = sc->has_ema_tool != 0;
+    for (i64 i = 0; i < n; ++i) {
+      const double x = dur[i];
+      ema = has ? c.ema_alpha * x + (1.0 - c.ema_alpha) * ema : x;
+      has = true;
+    }
+    sc->ema_tool = ema;
+    sc->has_ema_tool = has ? 1 : 0;
+    sc->free_blocks += (i64)s_freed;
+    counts[0] = s_warm;
+    counts[1] = s_cold;
+    counts[2] = s_ev;
+    counts[3] = s_bad;
+  }
+}
+
+int mars_enqueue_resume(const Tab& t, const Cfg& c, mars_scalars* sc, cudaStream_t s, i64 n,
+                        const i64* rows, const double* fin, const double* dur, const i32* newp,
+                        const i32* dec, double now, int* counts) {
+  k_resume<<<1, 1024, 0, s>>>(t, c, sc, n, rows, fin, dur, newp, dec, now, counts);
+  return (int)cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------------
 // standalone retention batch (mars_retention_batch)
 // ---------------------------------------------------------------------------

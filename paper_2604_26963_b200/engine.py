@@ -306,6 +306,21 @@ class MarsEngine:
     def set_profiling(self, on: bool) -> None:
         self._check(self.lib.mars_set_profiling(self.ctx, int(bool(on))))
 
+    def resume(self, rows, finish_time, duration, new_prefill, decode_tokens,
+               now: float) -> Dict[str, int]:
+        """resume_from_tool (sim.py:190-231) for tools that finished, in the tool
+        plane's finish order (mars_resume)."""
+        rows = np.ascontiguousarray(rows, np.int64)
+        fin = np.ascontiguousarray(finish_time, np.float64)
+        dur = np.ascontiguousarray(duration, np.float64)
+        newp = np.ascontiguousarray(new_prefill, np.int32)
+        dec = np.ascontiguousarray(decode_tokens, np.int32)
+        cnt = np.zeros(3, np.int32)
+        self._check(self.lib.mars_resume(self.ctx, len(rows), rows.ctypes.data, fin.ctypes.data,
+                                         dur.ctypes.data, newp.ctypes.data, dec.ctypes.data,
+                                         float(now), cnt.ctypes.data))
+        return {"warm": int(cnt[0]), "cold": int(cnt[1]), "evicted": int(cnt[2])}
+
     def kernel_times(self) -> Dict[str, float]:
         ms = (C.c_float * len(N.KTIME_NAMES))()
         self._check(self.lib.mars_kernel_times(self.ctx, ms, len(N.KTIME_NAMES)))
