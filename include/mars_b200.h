@@ -203,8 +203,12 @@ typedef struct mars_step_out {
    * left the prefix-sum fast path; how pack_queue sorted the list (0 not
    * run, 1 grid LSD radix sort, 2 one CTA: small list or first fit) */
   int32_t n_window_cand, n_victim_cand, walk_slow, sort_path;
-  /* MARS_MODE_ADVANCE: rounds that ended this tick, sessions that finished */
+  /* MARS_MODE_ADVANCE: rounds that ended this tick, sessions that finished;
+   * per ended round in decode order: its row and what the boundary did
+   * (0 session done, 1 KV pinned -> tool, 2 KV freed -> tool) */
   int32_t n_round_end, n_done;
+  const uint32_t* end_rows;
+  const uint8_t* end_kind;
 } mars_step_out;
 
 /* ---- lifecycle ------------------------------------------------------- */

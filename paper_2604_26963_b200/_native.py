@@ -112,6 +112,7 @@ class MarsStepOut(C.Structure):
         ("fin_cost", P(f64)), ("fin_deadline", P(f64)),
         ("n_window_cand", i32), ("n_victim_cand", i32), ("walk_slow", i32),
         ("sort_path", i32), ("n_round_end", i32), ("n_done", i32),
+        ("end_rows", P(u32)), ("end_kind", P(u8)),
     ]
 
 

@@ -343,6 +343,8 @@ int mars_create(const mars_config* hcfg, int device, int64_t max_rows, int64_t m
   ALLOC(b.fin_b, WIN_MAX * 8);
   ALLOC(b.fin_c, WIN_MAX * 8);
   ALLOC(b.fin_d, WIN_MAX * 8);
+  ALLOC(b.end_row, WIN_MAX * 4);
+  ALLOC(b.end_kind, WIN_MAX);
   b.ev_cap = R;
   ALLOC(b.ev_row, R * 4);
   ALLOC(b.ev_kind, R);
@@ -424,7 +426,7 @@ int mars_destroy(mars_ctx* ctx) {
                 b.ret_pin, b.ret_b, b.ret_c, b.ret_d, b.admitted, b.win_rows, b.dec_rows,
                 b.pre_rows, b.pre_grant, b.ev_row, b.ev_kind, b.ev_blk, b.j_op, b.j_row, b.j_n,
                 b.dec_level, b.pre_level, b.fin_row, b.fin_pin, b.fin_b, b.fin_c, b.fin_d,
-                b.flush};
+                b.flush, b.end_row, b.end_kind};
   for (void* p : bs) cudaFree(p);
   cudaFree(ctx->d_stage);
   cudaFree(ctx->d_resume);
@@ -791,6 +793,8 @@ int mars_step_fetch(mars_ctx* ctx, mars_step_out* o) {
   o->sort_path = w.sort_path;
   o->n_round_end = w.n_round_end;
   o->n_done = w.n_done;
+  o->end_rows = (const uint32_t*)pull(ctx, off, b.end_row, (size_t)w.n_round_end * 4);
+  o->end_kind = (const uint8_t*)pull(ctx, off, b.end_kind, (size_t)w.n_round_end);
   o->fin_rows = (const uint32_t*)pull(ctx, off, b.fin_row, (size_t)w.n_finish * 4);
   o->fin_pin = (const uint8_t*)pull(ctx, off, b.fin_pin, (size_t)w.n_finish);
   o->fin_benefit = (const double*)pull(ctx, off, b.fin_b, (size_t)w.n_finish * 8);

@@ -3095,12 +3095,14 @@ __global__ void __launch_bounds__(1024) k_advance(Tab t, Cfg c, Work* w, Bufs b,
     ema_b = has_ema ? c.ema_alpha * x + (1.0 - c.ema_alpha) * ema_b : x;  // telemetry.py:59-63
     has_ema = true;
     const u8 f = t.flags[r];
+    b.end_row[n_end - 1] = r;
     if (t.rleft[r] == 0) {  // last round: DONE, every block freed
       t.phase[r] = MARS_DONE;
       t.flags[r] = f & ~MARS_F_ACTIVE;
       freeb += held;
       t.kv[r] = 0;
       n_done++;
+      b.end_kind[n_end - 1] = 0;
       continue;
     }
     u8 pin = 0;
@@ -3111,9 +3113,11 @@ __global__ void __launch_bounds__(1024) k_advance(Tab t, Cfg c, Work* w, Bufs b,
       t.dl[r] = dd;
       t.pb[r] = (i32)held;
       t.plevel[r] = c.policy == POL_MARS && c.coord ? t.level[r] : 0;
+      b.end_kind[n_end - 1] = 1;
     } else {
       freeb += held;
       t.kv[r] = 0;
+      b.end_kind[n_end - 1] = 2;
     }
     t.phase[r] = MARS_TOOL;
   }

@@ -1,0 +1,237 @@
+"""A whole trace with the tick on the B200.
+
+``run_device_simulation`` replays the reference tick loop
+(agentsched/sim.py:90-431, ``run_simulation``) with every per-session
+transition on the device: the scheduling half (``mars_step``: pin expiry,
+probe, refresh_pressure + balance_and_admit + admit, MLFQ aging, window,
+build_plan with reclamation), the tick's tail (``MARS_MODE_ADVANCE``:
+step_gpu, charge_service, each ending round's retention / pin / free / DONE)
+and resume_from_tool (``mars_resume``).  The host keeps what is trace data or
+a scalar: arrivals (row upserts + the admission-list append), the tool plane
+(``ToolPlane``, engine.py:366-442: worker slots and the FIFO overflow, whose
+counts feed the probe), the control cadence, and the idle-tick jump.
+
+It returns the reference's run counters (sim.py:137-146) and the final clock,
+which the tests compare with the frozen reference runs.  No event log is
+produced.
+"""
+
+from __future__ import annotations
+
+import heapq
+import math
+from dataclasses import dataclass
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _native as N
+from .engine import MarsEngine, make_config
+from .snapshot import COLUMNS, F_LONG, F_QUEUED
+
+WAITING_ADMISSION, EMPTY = 0, 7
+
+
+@dataclass
+class FinishedTool:
+    row: int
+    start_time: float
+    finish_time: float
+    duration_s: float
+
+
+class ToolPlane:
+    """engine.py:366-442: fixed worker slots plus a FIFO overflow queue; a
+    freed slot goes to the oldest queued tool, started at the instant the
+    slot freed (or its enqueue instant, if later)."""
+
+    def __init__(self, worker_slots: int) -> None:
+        if worker_slots < 1:
+            raise ValueError("tool plane needs at least one worker slot")
+        self.worker_slots = worker_slots
+        self._running: List[Tuple[float, int, int, float, float, float]] = []
+        self._queued: List[Tuple[int, float, float]] = []
+        self._seq = 0
+
+    def active_count(self) -> int:
+        return len(self._running)
+
+    def queued_count(self) -> int:
+        return len(self._queued)
+
+    def next_finish_time(self) -> Optional[float]:
+        return self._running[0][0] if self._running else None
+
+    def start_tool(self, row: int, duration_s: float, now: float) -> bool:
+        if duration_s < 0:
+            raise N.ContractViolation("tool duration must be >= 0")
+        if len(self._running) < self.worker_slots:
+            self._seq += 1
+            heapq.heappush(self._running, (now + duration_s, self._seq, row, now, duration_s, now))
+            return True
+        self._queued.append((row, duration_s, now))
+        return False
+
+    def complete_tools(self, now: float) -> List[FinishedTool]:
+        done: List[FinishedTool] = []
+        while self._running and self._running[0][0] <= now:
+            finish, _, row, start, dur, _enq = heapq.heappop(self._running)
+            done.append(FinishedTool(row, start, finish, dur))
+            if self._queued:
+                qrow, qdur, qenq = self._queued.pop(0)
+                qstart = max(finish, qenq)
+                self._seq += 1
+                heapq.heappush(self._running, (qstart + qdur, self._seq, qrow, qstart, qdur, qenq))
+        return done
+
+
+def run_device_simulation(traces: Sequence, total_blocks: int, tool_worker_slots: int,
+                          enable_coordinator: bool = True, enable_coscheduler: bool = True,
+                          initial_window: Optional[float] = None, device: int = 0,
+                          max_ticks: int = 5_000_000) -> Tuple[Dict[str, int], float]:
+    """MARS with its control plane over ``traces`` (objects with session_id,
+    arrival_time_s and rounds of new_prefill_tokens / decode_tokens /
+    tool_duration_s, as agentsched.workload.Trace).  Returns (counters,
+    final clock)."""
+    order = sorted(traces, key=lambda t: (t.arrival_time_s, t.session_id))
+    n = len(order)
+    cfg = make_config(enable_coordinator, enable_coscheduler, initial_window=initial_window)
+    bs = int(cfg.block_size)
+    for tr in order:  # sim.py:103-109
+        ctx = sum(r.new_prefill_tokens + r.decode_tokens for r in tr.rounds)
+        if -(-ctx // bs) > total_blocks:
+            raise N.ContractViolation(f"session {tr.session_id} cannot fit the pool")
+    eng = MarsEngine(max_rows=max(n, 1), max_queue=max(n, 1), device=device, config=cfg)
+    try:
+        return _run(eng, cfg, order, total_blocks, tool_worker_slots, max_ticks)
+    finally:
+        eng.close()
+
+
+def _run(eng: MarsEngine, cfg, order, total_blocks: int, slots: int, max_ticks: int):
+    n = len(order)
+    bs = int(cfg.block_size)
+    sid_rank = {sid: i for i, sid in enumerate(sorted(t.session_id for t in order))}
+    r0p = np.array([t.rounds[0].new_prefill_tokens for t in order], np.int32)
+    req = -(-r0p.astype(np.int64) // bs)
+    long_ = req > cfg.long_session_fraction * total_blocks   # control.py:91 (strict)
+    eng._check(eng.lib.mars_set_rows(eng.ctx, n))
+    eng.n_rows = n
+    cols = {k: np.zeros(n, t) for k, t in COLUMNS.items()}
+    cols.update({
+        "phase": np.full(n, EMPTY, np.uint8),
+        "rank": np.array([sid_rank[t.session_id] for t in order], np.uint32),
+        "arrival": np.array([t.arrival_time_s for t in order], np.float64),
+        "r0_prefill": r0p,
+        "r0_decode": np.array([t.rounds[0].decode_tokens for t in order], np.int32),
+        "req_blocks": req.astype(np.int32),
+        "rounds_left": np.array([len(t.rounds) - 1 for t in order], np.int32),
+    })
+    eng.upsert(cols)
+    eng.rank_ordered = all(sid_rank[t.session_id] == i for i, t in enumerate(order))
+    s = N.MarsScalars()
+    s.total_blocks = s.free_blocks = s.available_kv = total_blocks
+    s.w_adm = float(cfg.initial_window)
+    eng.set_scalars(s)
+
+    tools = ToolPlane(slots)
+    tick = float(cfg.tick_duration_s)
+    clock = 0.0
+    next_control = 0.0
+    nxt = 0
+    queue: List[int] = []
+    rnd = [0] * n
+    active = pinned = 0
+    cnt = dict(admitted=0, completed=0, evictions=0, preemptions=0, warm_resumes=0,
+               cold_resumes=0, pins=0, gpu_tokens=0)
+    ticks = 0
+    while nxt < n or queue or active:
+        ticks += 1
+        if ticks > max_ticks:
+            raise RuntimeError(f"exceeded max_ticks={max_ticks} with work outstanding")
+        now = clock
+        # arrivals (sim.py:289-301): queued for admission, list order = arrival order
+        new = []
+        while nxt < n and order[nxt].arrival_time_s <= now + 1e-9:
+            new.append(nxt)
+            nxt += 1
+        if new:
+            rows = np.array(new, np.int64)
+            eng.upsert({"phase": np.full(len(new), WAITING_ADMISSION, np.uint8),
+                        "flags": (F_QUEUED | np.where(long_[rows], F_LONG, 0)).astype(np.uint8)},
+                       rows=rows)
+            queue += new
+            # appended to the device list, whose residual keeps the packed order
+            q = np.concatenate([np.asarray(eng.get_queue(), np.int64), rows])
+            eng.set_queue(q.astype(np.uint32), req[q].astype(np.int32), long_[q])
+        # tools that finished (sim.py:303-322): resume_from_tool on the device
+        done = tools.complete_tools(now)
+        if done:
+            rows = [d.row for d in done]
+            nr = [order[r].rounds[rnd[r] + 1] for r in rows]
+            c = eng.resume(rows, [d.finish_time for d in done], [d.duration_s for d in done],
+                           [x.new_prefill_tokens for x in nr], [x.decode_tokens for x in nr], now)
+            for r in rows:
+                rnd[r] += 1
+            cnt["warm_resumes"] += c["warm"]
+            cnt["cold_resumes"] += c["cold"]
+            cnt["evictions"] += c["evicted"]
+            pinned -= c["warm"] + c["evicted"]
+        # the tick: expiry, probe, control plane, plan, step_gpu, round ends
+        due = now >= next_control - 1e-9
+        si = eng.step_in(now, due, tools.active_count(), tools.queued_count(), slots,
+                         N.MODE_ADVANCE)
+        res = eng.step(si)
+        if res.status:
+            raise RuntimeError(f"device step status {res.status}")
+        if due:
+            next_control = now + cfg.control_interval_s
+            admitted = set(int(x) for x in res.admitted_rows)
+            queue = [r for r in queue if r not in admitted]
+            cnt["admitted"] += len(admitted)
+            active += len(admitted)
+        cnt["evictions"] += len(res.expired_rows)
+        pinned -= len(res.expired_rows)
+        for k in res.evict_kind.tolist():
+            cnt["evictions"] += 1
+            if k == 0:
+                cnt["preemptions"] += 1
+            else:
+                pinned -= 1
+        if res.total_tokens > 0:
+            cnt["gpu_tokens"] += int(res.total_tokens)
+            end = now + tick
+            for r, kind in zip(res.end_rows.tolist(), res.end_kind.tolist()):
+                if kind == 0:
+                    cnt["completed"] += 1
+                    active -= 1
+                    continue
+                if kind == 1:
+                    cnt["pins"] += 1
+                    pinned += 1
+                else:
+                    cnt["evictions"] += 1
+                dur = order[r].rounds[rnd[r]].tool_duration_s
+                tools.start_tool(r, dur if dur is not None else 0.0, end)
+            clock = end
+            continue
+        # idle tick: jump to the next instant anything can change (sim.py:377-418)
+        cand = []
+        if nxt < n:
+            cand.append(order[nxt].arrival_time_s)
+        nf = tools.next_finish_time()
+        if nf is not None:
+            cand.append(nf)
+        if queue or active:
+            cand.append(next_control)
+        ready = int(res.n_ready) + len(res.admitted_rows) > 0
+        if ready or pinned > 0:
+            cand.append(now + tick)
+        if not cand:
+            if active or queue:
+                raise RuntimeError("no future event but sessions remain")
+            break
+        target = min(cand)
+        steps = max(1, math.ceil((target - now) / tick - 1e-9))
+        clock = now + steps * tick
+    return cnt, clock

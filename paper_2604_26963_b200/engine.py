@@ -73,6 +73,8 @@ class StepResult:
     fin_benefit: np.ndarray
     fin_cost: np.ndarray
     fin_deadline: np.ndarray
+    end_rows: np.ndarray   # MARS_MODE_ADVANCE: rounds that ended (decode order)
+    end_kind: np.ndarray   # 0 done, 1 pinned -> tool, 2 freed -> tool
     n_ready: int
     n_promoted: int
     pack_mode: int
@@ -269,6 +271,8 @@ class MarsEngine:
             fin_benefit=_arr(o.fin_benefit, o.n_finish, np.float64),
             fin_cost=_arr(o.fin_cost, o.n_finish, np.float64),
             fin_deadline=_arr(o.fin_deadline, o.n_finish, np.float64),
+            end_rows=_arr(o.end_rows, o.n_round_end, np.uint32),
+            end_kind=_arr(o.end_kind, o.n_round_end, np.uint8),
             n_ready=o.n_ready, n_promoted=o.n_promoted, pack_mode=o.pack_mode,
             total_tokens=o.total_tokens, free_after_expiry=o.free_after_expiry,
             free_blocks=o.free_blocks, limit=o.limit, slots=o.slots,
