@@ -86,16 +86,21 @@ class ToolPlane:
 
 
 def run_device_simulation(traces: Sequence, total_blocks: int, tool_worker_slots: int,
-                          enable_coordinator: bool = True, enable_coscheduler: bool = True,
+                          policy: str = "mars", enable_coordinator: bool = True,
+                          enable_coscheduler: bool = True, enable_control_plane: bool = True,
                           initial_window: Optional[float] = None, device: int = 0,
                           max_ticks: int = 5_000_000) -> Tuple[Dict[str, int], float]:
-    """MARS with its control plane over ``traces`` (objects with session_id,
-    arrival_time_s and rounds of new_prefill_tokens / decode_tokens /
-    tool_duration_s, as agentsched.workload.Trace).  Returns (counters,
-    final clock)."""
+    """``policy`` (a POLICY_KINDS name) over ``traces`` (objects with
+    session_id, arrival_time_s and rounds of new_prefill_tokens /
+    decode_tokens / tool_duration_s, as agentsched.workload.Trace).  MARS
+    admits through its control plane unless ``enable_control_plane`` is off;
+    the comparison policies admit at arrival (sim.py:116).  Returns
+    (counters, final clock)."""
     order = sorted(traces, key=lambda t: (t.arrival_time_s, t.session_id))
     n = len(order)
-    cfg = make_config(enable_coordinator, enable_coscheduler, initial_window=initial_window)
+    cfg = make_config(enable_coordinator, enable_coscheduler, initial_window=initial_window,
+                      policy=policy)
+    cfg_admission = enable_control_plane and policy == "mars"
     bs = int(cfg.block_size)
     for tr in order:  # sim.py:103-109
         ctx = sum(r.new_prefill_tokens + r.decode_tokens for r in tr.rounds)
@@ -103,16 +108,26 @@ def run_device_simulation(traces: Sequence, total_blocks: int, tool_worker_slots
             raise N.ContractViolation(f"session {tr.session_id} cannot fit the pool")
     eng = MarsEngine(max_rows=max(n, 1), max_queue=max(n, 1), device=device, config=cfg)
     try:
-        return _run(eng, cfg, order, total_blocks, tool_worker_slots, max_ticks)
+        return _run(eng, cfg, order, total_blocks, tool_worker_slots, max_ticks, cfg_admission,
+                    policy)
     finally:
         eng.close()
 
 
-def _run(eng: MarsEngine, cfg, order, total_blocks: int, slots: int, max_ticks: int):
+def _initial_level(tokens: int, cfg) -> int:  # scheduler.py:87-97
+    for i in range(cfg.num_levels):
+        if tokens <= cfg.level_bounds[i]:
+            return i
+    return cfg.num_levels - 1
+
+
+def _run(eng: MarsEngine, cfg, order, total_blocks: int, slots: int, max_ticks: int,
+         admission: bool, policy: str):
     n = len(order)
     bs = int(cfg.block_size)
     sid_rank = {sid: i for i, sid in enumerate(sorted(t.session_id for t in order))}
     r0p = np.array([t.rounds[0].new_prefill_tokens for t in order], np.int32)
+    dec0 = np.array([t.rounds[0].decode_tokens for t in order], np.int32)
     req = -(-r0p.astype(np.int64) // bs)
     long_ = req > cfg.long_session_fraction * total_blocks   # control.py:91 (strict)
     eng._check(eng.lib.mars_set_rows(eng.ctx, n))
@@ -123,7 +138,7 @@ def _run(eng: MarsEngine, cfg, order, total_blocks: int, slots: int, max_ticks: 
         "rank": np.array([sid_rank[t.session_id] for t in order], np.uint32),
         "arrival": np.array([t.arrival_time_s for t in order], np.float64),
         "r0_prefill": r0p,
-        "r0_decode": np.array([t.rounds[0].decode_tokens for t in order], np.int32),
+        "r0_decode": dec0,
         "req_blocks": req.astype(np.int32),
         "rounds_left": np.array([len(t.rounds) - 1 for t in order], np.int32),
     })
@@ -155,7 +170,7 @@ def _run(eng: MarsEngine, cfg, order, total_blocks: int, slots: int, max_ticks: 
         while nxt < n and order[nxt].arrival_time_s <= now + 1e-9:
             new.append(nxt)
             nxt += 1
-        if new:
+        if new and admission:
             rows = np.array(new, np.int64)
             eng.upsert({"phase": np.full(len(new), WAITING_ADMISSION, np.uint8),
                         "flags": (F_QUEUED | np.where(long_[rows], F_LONG, 0)).astype(np.uint8)},
@@ -164,6 +179,17 @@ def _run(eng: MarsEngine, cfg, order, total_blocks: int, slots: int, max_ticks: 
             # appended to the device list, whose residual keeps the packed order
             q = np.concatenate([np.asarray(eng.get_queue(), np.int64), rows])
             eng.set_queue(q.astype(np.uint32), req[q].astype(np.int32), long_[q])
+        elif new:
+            # admit() at arrival (sim.py:148-166): submit_round + on_admit
+            rows = np.array(new, np.int64)
+            k = len(new)
+            lv = [_initial_level(int(r0p[r]), cfg) if policy == "mars" else 0 for r in new]
+            eng.upsert({"phase": np.full(k, 1, np.uint8), "flags": np.ones(k, np.uint8),
+                        "context": r0p[rows], "rem_decode": dec0[rows],
+                        "ready_since": np.full(k, now), "wait_since": np.full(k, now),
+                        "level": np.array(lv, np.uint8)}, rows=rows)
+            cnt["admitted"] += k
+            active += k
         # tools that finished (sim.py:303-322): resume_from_tool on the device
         done = tools.complete_tools(now)
         if done:
@@ -178,7 +204,7 @@ def _run(eng: MarsEngine, cfg, order, total_blocks: int, slots: int, max_ticks: 
             cnt["evictions"] += c["evicted"]
             pinned -= c["warm"] + c["evicted"]
         # the tick: expiry, probe, control plane, plan, step_gpu, round ends
-        due = now >= next_control - 1e-9
+        due = admission and now >= next_control - 1e-9
         si = eng.step_in(now, due, tools.active_count(), tools.queued_count(), slots,
                          N.MODE_ADVANCE)
         res = eng.step(si)
@@ -222,7 +248,7 @@ def _run(eng: MarsEngine, cfg, order, total_blocks: int, slots: int, max_ticks: 
         nf = tools.next_finish_time()
         if nf is not None:
             cand.append(nf)
-        if queue or active:
+        if admission and (queue or active):
             cand.append(next_control)
         ready = int(res.n_ready) + len(res.admitted_rows) > 0
         if ready or pinned > 0:

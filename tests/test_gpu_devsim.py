@@ -12,24 +12,38 @@ import pytest
 
 from oracle import tracefile
 from paper_2604_26963_b200.devsim import run_device_simulation
-from tests._sim import SIM, VARIANT_KW
+from tests._sim import SIM, SIM_BASE, VARIANT_KW
 from tests.conftest import GOLDEN
 
 pytestmark = pytest.mark.gpu
 
-# the device loop runs MARS with its control plane (mars-no-control admits at
-# arrival, outside the device control plane; starvation runs without it)
-KEYS = sorted(k for k in SIM if not k.endswith("no-control") and not k.startswith("starvation"))
-
-
-@pytest.mark.parametrize("key", KEYS)
+@pytest.mark.parametrize("key", sorted(SIM))
 def test_device_simulation_reproduces_reference_counters(key):
+    """MARS, its ablations and the control-plane-off runs (admission at arrival)."""
     spec = SIM[key]
     traces = tracefile.load(os.path.join(GOLDEN, spec["trace"]))
     kw = dict(VARIANT_KW[key.split("/")[1]])
     ctl = spec["run"].get("controller") or {}
+    cnt, horizon = run_device_simulation(
+        traces, spec["engine"]["total_blocks"], spec["engine"]["tool_worker_slots"],
+        enable_control_plane=spec["run"].get("enable_control_plane", True),
+        initial_window=ctl.get("initial_window"), **kw)
+    assert cnt == spec["counters"]
+    assert horizon == spec["horizon_s"]
+
+
+# demo64/program_priority's run is ~10x longer than the others (see test_gpu_dropin)
+BASE_KEYS = sorted(k for k in SIM_BASE if k != "demo64/program_priority")
+
+
+@pytest.mark.parametrize("key", BASE_KEYS)
+def test_device_simulation_comparison_policies(key):
+    """fcfs / program_priority / static_ttl / dynamic_ttl: admission at
+    arrival, their plans, boundaries and pins all on the device."""
+    spec = SIM_BASE[key]
+    traces = tracefile.load(os.path.join(GOLDEN, spec["trace"]))
     cnt, horizon = run_device_simulation(traces, spec["engine"]["total_blocks"],
                                          spec["engine"]["tool_worker_slots"],
-                                         initial_window=ctl.get("initial_window"), **kw)
+                                         policy=spec["policy"])
     assert cnt == spec["counters"]
     assert horizon == spec["horizon_s"]
