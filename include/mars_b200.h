@@ -36,7 +36,7 @@ extern "C" {
 #define MARS_ERR_CAPACITY 3
 #define MARS_ERR_ARG 4
 
-#define MARS_ABI_VERSION 3
+#define MARS_ABI_VERSION 4
 
 /* phase codes: agentsched/engine.py:250-256 */
 #define MARS_WAITING_ADMISSION 0
@@ -209,6 +209,14 @@ typedef struct mars_step_out {
   int32_t n_round_end, n_done;
   const uint32_t* end_rows;
   const uint8_t* end_kind;
+  /* ... and the payloads the reference logs for it (sim.py:233-279): the
+   * blocks pinned or freed, the retention decision (when the policy makes
+   * one: pin, benefit_s, cost_s, deadline); per planned prefill, 1 if its
+   * grant finished the prefill (engine.py:489-497, gpu_1st_token) (ABI v4) */
+  const int32_t* end_blocks;
+  const uint8_t* end_pin;
+  const double *end_benefit, *end_cost, *end_deadline;
+  const uint8_t* prefill_done;
 } mars_step_out;
 
 /* ---- lifecycle ------------------------------------------------------- */
@@ -254,6 +262,12 @@ int mars_set_graph(mars_ctx* ctx, int on);
 int mars_resume(mars_ctx* ctx, int64_t n, const int64_t* rows, const double* finish_time,
                 const double* duration, const int32_t* new_prefill, const int32_t* decode_tokens,
                 double now, int32_t* counts /* [3] */);
+/* per row of the last mars_resume, in its order (sync; ABI v4): kind 0 warm
+ * (unpinned), 1 cold, 2 cold after the return-time release of an expired pin
+ * (sim.py:193-205); blocks unpinned or released; and gpu_submit's payload
+ * (sim.py:224-230): context_tokens, required_prefill, projected_blocks */
+int mars_resume_rows(mars_ctx* ctx, int64_t n, uint8_t* kind, int32_t* blocks, int32_t* context,
+                     int32_t* need, int32_t* projected);
 int mars_retention_batch(mars_ctx* ctx, int64_t n, const int32_t* context, const int32_t* kv,
                          int64_t total_blocks, double kv_usage_ratio, double ema_tool,
                          double now, uint8_t* pin, double* benefit, double* cost,

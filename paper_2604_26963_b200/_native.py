@@ -113,6 +113,8 @@ class MarsStepOut(C.Structure):
         ("n_window_cand", i32), ("n_victim_cand", i32), ("walk_slow", i32),
         ("sort_path", i32), ("n_round_end", i32), ("n_done", i32),
         ("end_rows", P(u32)), ("end_kind", P(u8)),
+        ("end_blocks", P(i32)), ("end_pin", P(u8)), ("end_benefit", P(f64)),
+        ("end_cost", P(f64)), ("end_deadline", P(f64)), ("prefill_done", P(u8)),
     ]
 
 
@@ -151,6 +153,8 @@ _SIGS = {
     "mars_host_link_peak": (i32, [C.c_void_p, i64, C.c_int, P(f64), P(f64), P(f64)]),
     "mars_resume": (i32, [C.c_void_p, i64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                           C.c_void_p, f64, C.c_void_p]),
+    "mars_resume_rows": (i32, [C.c_void_p, i64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                               C.c_void_p]),
     "mars_retention_batch": (i32, [C.c_void_p, i64, C.c_void_p, C.c_void_p, i64, f64, f64, f64,
                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "mars_checkpoint": (i32, [C.c_void_p]),

@@ -29,7 +29,8 @@ struct mars_ctx {
   int device = 0;
   int num_sms = 148;
   cudaStream_t stream = nullptr, side = nullptr, side2 = nullptr;
-  void* d_resume = nullptr;  // mars_resume staging (lazily allocated)
+  void* d_resume = nullptr;  // mars_resume staging + per-row outcome (lazily allocated)
+  i64 last_resume_n = 0;
   bool own_stream = true;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_head = nullptr, ev_pack = nullptr;
   int pack_ctas = 20;
@@ -345,6 +346,12 @@ int mars_create(const mars_config* hcfg, int device, int64_t max_rows, int64_t m
   ALLOC(b.fin_d, WIN_MAX * 8);
   ALLOC(b.end_row, WIN_MAX * 4);
   ALLOC(b.end_kind, WIN_MAX);
+  ALLOC(b.end_blk, WIN_MAX * 4);
+  ALLOC(b.end_pin, WIN_MAX);
+  ALLOC(b.end_b, WIN_MAX * 8);
+  ALLOC(b.end_c, WIN_MAX * 8);
+  ALLOC(b.end_d, WIN_MAX * 8);
+  ALLOC(b.pre_done, WIN_MAX);
   b.ev_cap = R;
   ALLOC(b.ev_row, R * 4);
   ALLOC(b.ev_kind, R);
@@ -426,7 +433,8 @@ int mars_destroy(mars_ctx* ctx) {
                 b.ret_pin, b.ret_b, b.ret_c, b.ret_d, b.admitted, b.win_rows, b.dec_rows,
                 b.pre_rows, b.pre_grant, b.ev_row, b.ev_kind, b.ev_blk, b.j_op, b.j_row, b.j_n,
                 b.dec_level, b.pre_level, b.fin_row, b.fin_pin, b.fin_b, b.fin_c, b.fin_d,
-                b.flush, b.end_row, b.end_kind};
+                b.flush, b.end_row, b.end_kind, b.end_blk, b.end_pin, b.end_b, b.end_c,
+                b.end_d, b.pre_done};
   for (void* p : bs) cudaFree(p);
   cudaFree(ctx->d_stage);
   cudaFree(ctx->d_resume);
@@ -795,6 +803,14 @@ int mars_step_fetch(mars_ctx* ctx, mars_step_out* o) {
   o->n_done = w.n_done;
   o->end_rows = (const uint32_t*)pull(ctx, off, b.end_row, (size_t)w.n_round_end * 4);
   o->end_kind = (const uint8_t*)pull(ctx, off, b.end_kind, (size_t)w.n_round_end);
+  o->end_blocks = (const int32_t*)pull(ctx, off, b.end_blk, (size_t)w.n_round_end * 4);
+  o->end_pin = (const uint8_t*)pull(ctx, off, b.end_pin, (size_t)w.n_round_end);
+  o->end_benefit = (const double*)pull(ctx, off, b.end_b, (size_t)w.n_round_end * 8);
+  o->end_cost = (const double*)pull(ctx, off, b.end_c, (size_t)w.n_round_end * 8);
+  o->end_deadline = (const double*)pull(ctx, off, b.end_d, (size_t)w.n_round_end * 8);
+  o->prefill_done = (w.in.mode & MARS_MODE_ADVANCE)
+                        ? (const uint8_t*)pull(ctx, off, b.pre_done, (size_t)w.n_pre)
+                        : nullptr;
   o->fin_rows = (const uint32_t*)pull(ctx, off, b.fin_row, (size_t)w.n_finish * 4);
   o->fin_pin = (const uint8_t*)pull(ctx, off, b.fin_pin, (size_t)w.n_finish);
   o->fin_benefit = (const double*)pull(ctx, off, b.fin_b, (size_t)w.n_finish * 8);
@@ -926,7 +942,7 @@ int mars_resume(mars_ctx* ctx, int64_t n, const int64_t* rows, const double* fin
     if (rows[i] < 0 || rows[i] >= ctx->n_rows) return fail(ctx, MARS_ERR_ARG, "resume row out of range");
   CK(cudaSetDevice(ctx->device));
   if (!ctx->d_resume) {
-    CK(cudaMalloc(&ctx->d_resume, (size_t)ctx->max_rows * 32 + 64));
+    CK(cudaMalloc(&ctx->d_resume, (size_t)ctx->max_rows * 52 + 256));
   }
   unsigned char* p = (unsigned char*)ctx->d_resume;
   i64* drows = (i64*)p;
@@ -935,13 +951,21 @@ int mars_resume(mars_ctx* ctx, int64_t n, const int64_t* rows, const double* fin
   i32* dnew = (i32*)(ddur + n);
   i32* ddec = dnew + n;
   int* dcnt = (int*)(ddec + ((n + 1) & ~1ll));
+  // per-row outcome (mars_resume_rows): after the counts, 16-byte aligned
+  const i64 mr = ctx->max_rows;
+  i32* o_blk = (i32*)((unsigned char*)ctx->d_resume + mr * 32 + 64);
+  i32* o_ctx = o_blk + mr;
+  i32* o_need = o_ctx + mr;
+  i32* o_proj = o_need + mr;
+  u8* o_kind = (u8*)(o_proj + mr);
+  ctx->last_resume_n = n;
   CK(cudaMemcpyAsync(drows, rows, n * 8, cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(dfin, finish_time, n * 8, cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(ddur, duration, n * 8, cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(dnew, new_prefill, n * 4, cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(ddec, decode_tokens, n * 4, cudaMemcpyHostToDevice, ctx->stream));
   int rc = mars_enqueue_resume(ctx->tab, ctx->cfg, ctx->sc, ctx->stream, n, drows, dfin, ddur,
-                               dnew, ddec, now, dcnt);
+                               dnew, ddec, now, dcnt, o_kind, o_blk, o_ctx, o_need, o_proj);
   if (rc) return fail(ctx, MARS_ERR_CUDA, "resume: %s", cudaGetErrorString((cudaError_t)rc));
   int hc[4] = {0, 0, 0, 0};
   CK(cudaMemcpyAsync(hc, dcnt, sizeof hc, cudaMemcpyDeviceToHost, ctx->stream));
@@ -950,6 +974,24 @@ int mars_resume(mars_ctx* ctx, int64_t n, const int64_t* rows, const double* fin
   counts[1] = hc[1];
   counts[2] = hc[2];
   if (hc[3]) return fail(ctx, MARS_ERR_CONTRACT, "resume owes a prefill other than its cost");
+  return MARS_OK;
+}
+
+int mars_resume_rows(mars_ctx* ctx, int64_t n, uint8_t* kind, int32_t* blocks, int32_t* context,
+                     int32_t* need, int32_t* projected) {
+  if (!ctx || n < 0) return MARS_ERR_ARG;
+  if (n != ctx->last_resume_n) return fail(ctx, MARS_ERR_ARG, "resume_rows: %lld rows, the last resume had %lld",
+                                           (long long)n, (long long)ctx->last_resume_n);
+  if (n == 0) return MARS_OK;
+  CK(cudaSetDevice(ctx->device));
+  const i64 mr = ctx->max_rows;
+  i32* o_blk = (i32*)((unsigned char*)ctx->d_resume + mr * 32 + 64);
+  CK(cudaMemcpyAsync(blocks, o_blk, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(context, o_blk + mr, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(need, o_blk + 2 * mr, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(projected, o_blk + 3 * mr, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(kind, (u8*)(o_blk + 4 * mr), n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
   return MARS_OK;
 }
 

@@ -176,6 +176,8 @@ struct Bufs {
   u8 *dec_level, *pre_level;
   u32 *fin_row; u8 *fin_pin; double *fin_b, *fin_c, *fin_d;
   u32 *end_row; u8 *end_kind;  // MARS_MODE_ADVANCE: rounds that ended, decode order
+  i32 *end_blk; u8 *end_pin; double *end_b, *end_c, *end_d;  // blocks pinned/freed, decision
+  u8 *pre_done;                // MARS_MODE_ADVANCE: the grant finished the prefill
   u32 *ev_row; u8 *ev_kind; i32 *ev_blk;
   u8 *j_op; u32 *j_row; i32 *j_n;
   i64 ev_cap, j_cap;

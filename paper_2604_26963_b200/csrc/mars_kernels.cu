@@ -3064,7 +3064,9 @@ __global__ void __launch_bounds__(1024) k_advance(Tab t, Cfg c, Work* w, Bufs b,
     const u32 r = b.pre_rows[i];
     const i32 kv = t.kv[r] + b.pre_grant[i];
     t.kv[r] = kv;
-    if (kv == t.ctx[r]) t.phase[r] = MARS_DECODE;  // remaining_prefill == 0
+    const bool done = kv == t.ctx[r];  // remaining_prefill == 0
+    if (done) t.phase[r] = MARS_DECODE;
+    b.pre_done[i] = done ? 1 : 0;
     if (c.policy == POL_PP) t.served[r] += b.pre_grant[i];  // Call.served_tokens
   }
   for (int i = threadIdx.x; i < nd; i += blockDim.x) {
@@ -3095,29 +3097,36 @@ __global__ void __launch_bounds__(1024) k_advance(Tab t, Cfg c, Work* w, Bufs b,
     ema_b = has_ema ? c.ema_alpha * x + (1.0 - c.ema_alpha) * ema_b : x;  // telemetry.py:59-63
     has_ema = true;
     const u8 f = t.flags[r];
-    b.end_row[n_end - 1] = r;
+    const int e = n_end - 1;
+    b.end_row[e] = r;
+    b.end_blk[e] = (i32)held;
     if (t.rleft[r] == 0) {  // last round: DONE, every block freed
       t.phase[r] = MARS_DONE;
       t.flags[r] = f & ~MARS_F_ACTIVE;
       freeb += held;
       t.kv[r] = 0;
       n_done++;
-      b.end_kind[n_end - 1] = 0;
+      b.end_kind[e] = 0;
+      b.end_pin[e] = 0;
       continue;
     }
     u8 pin = 0;
-    double bb, cc, dd = 0.0;
+    double bb = 0.0, cc = 0.0, dd = 0.0;
     if (decides) decide_retention(c, ctx, kv, total, usage, ema_t, tick_end, pin, bb, cc, dd);
+    b.end_pin[e] = pin;  // the `retention` event's payload (sim.py:251-260)
+    b.end_b[e] = bb;
+    b.end_c[e] = cc;
+    b.end_d[e] = dd;
     if (pin && held > 0) {
       t.flags[r] = f | MARS_F_PINNED;
       t.dl[r] = dd;
       t.pb[r] = (i32)held;
       t.plevel[r] = c.policy == POL_MARS && c.coord ? t.level[r] : 0;
-      b.end_kind[n_end - 1] = 1;
+      b.end_kind[e] = 1;
     } else {
       freeb += held;
       t.kv[r] = 0;
-      b.end_kind[n_end - 1] = 2;
+      b.end_kind[e] = 2;
     }
     t.phase[r] = MARS_TOOL;
   }
@@ -3138,7 +3147,9 @@ __global__ void __launch_bounds__(1024) k_advance(Tab t, Cfg c, Work* w, Bufs b,
 __global__ void __launch_bounds__(1024) k_resume(Tab t, Cfg c, mars_scalars* sc, i64 n,
                                                  const i64* rows, const double* fin,
                                                  const double* dur, const i32* newp,
-                                                 const i32* dec, double now, int* counts) {
+                                                 const i32* dec, double now, int* counts,
+                                                 u8* o_kind, i32* o_blk, i32* o_ctx, i32* o_need,
+                                                 i32* o_proj) {
   __shared__ unsigned long long s_freed;
   __shared__ int s_warm, s_cold, s_ev, s_bad;
   if (threadIdx.x == 0) {
@@ -3173,6 +3184,13 @@ __global__ void __launch_bounds__(1024) k_resume(Tab t, Cfg c, mars_scalars* sc,
     t.phase[r] = MARS_PREFILL;
     if (c.policy == POL_MARS) t.ws[r] = now;  // on_resume (baselines.py:357-360)
     if (ctx + newp[i] - kv != need) atomicAdd(&s_bad, 1);
+    // per row, what the reference's log shows for it (sim.py:190-231): the
+    // unpin or return-time release, then gpu_submit's payload
+    o_kind[i] = warm ? 0 : (pinned ? 2 : 1);
+    o_blk[i] = pinned ? t.pb[r] : 0;
+    o_ctx[i] = (i32)(ctx + newp[i]);
+    o_need[i] = (i32)need;
+    o_proj[i] = (i32)(blocks_ceil(c, kv + need) - blocks_ceil(c, kv));
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -3195,8 +3213,10 @@ __global__ void __launch_bounds__(1024) k_resume(Tab t, Cfg c, mars_scalars* sc,
 
 int mars_enqueue_resume(const Tab& t, const Cfg& c, mars_scalars* sc, cudaStream_t s, i64 n,
                         const i64* rows, const double* fin, const double* dur, const i32* newp,
-                        const i32* dec, double now, int* counts) {
-  k_resume<<<1, 1024, 0, s>>>(t, c, sc, n, rows, fin, dur, newp, dec, now, counts);
+                        const i32* dec, double now, int* counts, u8* o_kind, i32* o_blk,
+                        i32* o_ctx, i32* o_need, i32* o_proj) {
+  k_resume<<<1, 1024, 0, s>>>(t, c, sc, n, rows, fin, dur, newp, dec, now, counts, o_kind, o_blk,
+                              o_ctx, o_need, o_proj);
   return (int)cudaGetLastError();
 }
 

@@ -44,7 +44,8 @@ int mars_enqueue_retention(const Cfg& c, cudaStream_t s, i64 n, const i32* ctx, 
 int mars_enqueue_flush(cudaStream_t s, u8* p, i64 n, u32 salt);
 int mars_enqueue_resume(const Tab& t, const Cfg& c, mars_scalars* sc, cudaStream_t s, i64 n,
                         const i64* rows, const double* fin, const double* dur, const i32* newp,
-                        const i32* dec, double now, int* counts);
+                        const i32* dec, double now, int* counts, u8* o_kind, i32* o_blk,
+                        i32* o_ctx, i32* o_need, i32* o_proj);
 int mars_enqueue_scatter(cudaStream_t s, void* dst, const void* src, const i64* rows, i64 n,
                          int esz);
 int mars_enqueue_gather(cudaStream_t s, void* dst, const void* src, const i64* rows, i64 n,

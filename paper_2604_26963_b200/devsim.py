@@ -12,13 +12,20 @@ a scalar: arrivals (row upserts + the admission-list append), the tool plane
 counts feed the probe), the control cadence, and the idle-tick jump.
 
 It returns the reference's run counters (sim.py:137-146) and the final clock,
-which the tests compare with the frozen reference runs.  No event log is
-produced.
+which the tests compare with the frozen reference runs.  Given an
+``EventLog`` it also writes the reference's JSONL event log (engine.py:77-104,
+SURVEY §8(f) row 2): every record the reference's tick loop emits, in its
+order, serialised on the host from the device's per-step outputs -- the
+expiry list, the admission prefix, the plan's ordered alloc / evict journal,
+the plan, prefill completions, each ended round's blocks and retention
+decision, and each resume's warm / cold outcome -- so the log of a device
+run is byte-identical to the reference's.
 """
 
 from __future__ import annotations
 
 import heapq
+import json
 import math
 from dataclasses import dataclass
 from typing import Dict, List, Optional, Sequence, Tuple
@@ -38,6 +45,56 @@ class FinishedTool:
     start_time: float
     finish_time: float
     duration_s: float
+    enqueue_time: float
+
+
+class EventLog:
+    """The reference's append-only event log (engine.py:77-104): records
+    ``{"t", "seq", "kind", "session_id", **payload}`` with ``seq`` from 1,
+    serialised as compact JSON lines in insertion order."""
+
+    def __init__(self) -> None:
+        self.records: List[dict] = []
+
+    def emit(self, t: float, kind: str, sid: Optional[str] = None, **payload) -> None:
+        rec = {"t": t, "seq": len(self.records) + 1, "kind": kind, "session_id": sid}
+        rec.update(payload)
+        self.records.append(rec)
+
+    def jsonl_bytes(self) -> bytes:
+        return b"".join((json.dumps(r, separators=(",", ":")) + "\n").encode()
+                        for r in self.records)
+
+
+class _Telemetry:
+    """The host's view of the reference Telemetry fields that the log shows
+    (telemetry.py:96-120 record, :152-158 probe): what the tick's probe set,
+    plus the drift of the events recorded after it."""
+
+    def __init__(self, total: int) -> None:
+        self.available_kv = total
+        self.kv_usage_ratio = 0.0
+        self.active_tools = self.queued_tools = self.active_sessions = 0
+
+    def probe(self, free: int, total: int, tools: "ToolPlane", active: int) -> None:
+        self.available_kv = free
+        self.kv_usage_ratio = (total - free) / total
+        self.active_tools = tools.active_count()
+        self.queued_tools = tools.queued_count()
+        self.active_sessions = active
+
+    def snapshot(self, sc) -> dict:
+        return {
+            "available_kv": self.available_kv,
+            "kv_usage_ratio": self.kv_usage_ratio,
+            "active_tools": self.active_tools,
+            "queued_tools": self.queued_tools,
+            "ema_tool_duration_s": float(sc.ema_tool) if sc.has_ema_tool else None,
+            "ema_blocks_per_session": float(sc.ema_blocks) if sc.has_ema_blocks else None,
+            "active_sessions": self.active_sessions,
+            "cpu_overloaded": bool(sc.cpu_overloaded),
+            "kv_overloaded": bool(sc.kv_overloaded),
+        }
 
 
 class ToolPlane:
@@ -52,6 +109,7 @@ class ToolPlane:
         self._running: List[Tuple[float, int, int, float, float, float]] = []
         self._queued: List[Tuple[int, float, float]] = []
         self._seq = 0
+        self.promoted: List[Tuple[int, float, float]] = []   # (row, start, duration)
 
     def active_count(self) -> int:
         return len(self._running)
@@ -75,27 +133,34 @@ class ToolPlane:
     def complete_tools(self, now: float) -> List[FinishedTool]:
         done: List[FinishedTool] = []
         while self._running and self._running[0][0] <= now:
-            finish, _, row, start, dur, _enq = heapq.heappop(self._running)
-            done.append(FinishedTool(row, start, finish, dur))
+            finish, _, row, start, dur, enq = heapq.heappop(self._running)
+            done.append(FinishedTool(row, start, finish, dur, enq))
             if self._queued:
                 qrow, qdur, qenq = self._queued.pop(0)
                 qstart = max(finish, qenq)
                 self._seq += 1
                 heapq.heappush(self._running, (qstart + qdur, self._seq, qrow, qstart, qdur, qenq))
+                self.promoted.append((qrow, qstart, qdur))
         return done
+
+    def take_promotions(self) -> List[Tuple[int, float, float]]:
+        out, self.promoted = self.promoted, []
+        return out
 
 
 def run_device_simulation(traces: Sequence, total_blocks: int, tool_worker_slots: int,
                           policy: str = "mars", enable_coordinator: bool = True,
                           enable_coscheduler: bool = True, enable_control_plane: bool = True,
                           initial_window: Optional[float] = None, device: int = 0,
-                          max_ticks: int = 5_000_000) -> Tuple[Dict[str, int], float]:
+                          max_ticks: int = 5_000_000,
+                          log: Optional[EventLog] = None) -> Tuple[Dict[str, int], float]:
     """``policy`` (a POLICY_KINDS name) over ``traces`` (objects with
     session_id, arrival_time_s and rounds of new_prefill_tokens /
     decode_tokens / tool_duration_s, as agentsched.workload.Trace).  MARS
     admits through its control plane unless ``enable_control_plane`` is off;
     the comparison policies admit at arrival (sim.py:116).  Returns
-    (counters, final clock)."""
+    (counters, final clock); fills ``log`` with the run's event log when
+    one is given."""
     order = sorted(traces, key=lambda t: (t.arrival_time_s, t.session_id))
     n = len(order)
     cfg = make_config(enable_coordinator, enable_coscheduler, initial_window=initial_window,
@@ -107,9 +172,10 @@ def run_device_simulation(traces: Sequence, total_blocks: int, tool_worker_slots
         if -(-ctx // bs) > total_blocks:
             raise N.ContractViolation(f"session {tr.session_id} cannot fit the pool")
     eng = MarsEngine(max_rows=max(n, 1), max_queue=max(n, 1), device=device, config=cfg)
+    decides = (policy == "mars" and enable_coscheduler) or policy in ("static_ttl", "dynamic_ttl")
     try:
         return _run(eng, cfg, order, total_blocks, tool_worker_slots, max_ticks, cfg_admission,
-                    policy)
+                    policy, log, decides)
     finally:
         eng.close()
 
@@ -122,7 +188,7 @@ def _initial_level(tokens: int, cfg) -> int:  # scheduler.py:87-97
 
 
 def _run(eng: MarsEngine, cfg, order, total_blocks: int, slots: int, max_ticks: int,
-         admission: bool, policy: str):
+         admission: bool, policy: str, log: Optional[EventLog], decides: bool):
     n = len(order)
     bs = int(cfg.block_size)
     sid_rank = {sid: i for i, sid in enumerate(sorted(t.session_id for t in order))}
@@ -149,7 +215,11 @@ def _run(eng: MarsEngine, cfg, order, total_blocks: int, slots: int, max_ticks: 
     s.w_adm = float(cfg.initial_window)
     eng.set_scalars(s)
 
+    sid = [t.session_id for t in order]
     tools = ToolPlane(slots)
+    tel = _Telemetry(total_blocks)
+    submit_t = [0.0] * n          # Call.round_submit_time (engine.py:322-330)
+    first_seen = set()            # (row, round) with a first token logged (sim.py:365-371)
     tick = float(cfg.tick_duration_s)
     clock = 0.0
     next_control = 0.0
@@ -159,6 +229,24 @@ def _run(eng: MarsEngine, cfg, order, total_blocks: int, slots: int, max_ticks: 
     active = pinned = 0
     cnt = dict(admitted=0, completed=0, evictions=0, preemptions=0, warm_resumes=0,
                cold_resumes=0, pins=0, gpu_tokens=0)
+
+    def admit_log(r: int, now: float) -> None:  # sim.py:148-166 gpu_submit
+        p = int(r0p[r])
+        proj = -(-p // bs)
+        log.emit(now, "gpu_submit", sid[r], round=0, arrival_time=order[r].arrival_time_s,
+                 required_prefill=p, new_tokens=p, context_tokens=p, warm=None,
+                 projected_blocks=proj)
+        tel.available_kv -= proj
+        submit_t[r] = now
+
+    def evict_log(r: int, blocks: int, victim: str, reason: str, t: float) -> None:
+        # sim.py:168-184: the pool op's observer record, then the evict record
+        if victim == "pinned":
+            log.emit(t, "free", sid[r], blocks=blocks, from_pinned=True)
+        elif blocks > 0:
+            log.emit(t, "free", sid[r], blocks=blocks)
+        log.emit(t, "evict", sid[r], blocks=blocks, victim=victim, reason=reason)
+
     ticks = 0
     while nxt < n or queue or active:
         ticks += 1
@@ -190,8 +278,15 @@ def _run(eng: MarsEngine, cfg, order, total_blocks: int, slots: int, max_ticks: 
                         "level": np.array(lv, np.uint8)}, rows=rows)
             cnt["admitted"] += k
             active += k
+            if log is not None:
+                for r in new:
+                    admit_log(r, now)
         # tools that finished (sim.py:303-322): resume_from_tool on the device
         done = tools.complete_tools(now)
+        if log is not None:
+            for r, start, dur in tools.take_promotions():
+                log.emit(start, "tool_start", sid[r], duration_s=dur, active=tools.active_count())
+                tel.active_tools += 1
         if done:
             rows = [d.row for d in done]
             nr = [order[r].rounds[rnd[r] + 1] for r in rows]
@@ -203,13 +298,58 @@ def _run(eng: MarsEngine, cfg, order, total_blocks: int, slots: int, max_ticks: 
             cnt["cold_resumes"] += c["cold"]
             cnt["evictions"] += c["evicted"]
             pinned -= c["warm"] + c["evicted"]
+            if log is not None:
+                rr = eng.resume_rows(len(rows))
+                for i, d in enumerate(done):
+                    r = d.row
+                    log.emit(d.finish_time, "tool_end", sid[r], duration_s=d.duration_s,
+                             queued_delay_s=d.start_time - d.enqueue_time)
+                    tel.active_tools -= 1
+                    kind, blk = int(rr["kind"][i]), int(rr["blocks"][i])
+                    if kind == 0:
+                        log.emit(now, "unpin", sid[r], blocks=blk)
+                    elif kind == 2:
+                        evict_log(r, blk, "pinned", "pin_expired_at_return", now)
+                    proj = int(rr["projected"][i])
+                    log.emit(now, "gpu_submit", sid[r], round=rnd[r],
+                             required_prefill=int(rr["need"][i]),
+                             new_tokens=nr[i].new_prefill_tokens,
+                             context_tokens=int(rr["context"][i]), warm=kind == 0,
+                             projected_blocks=proj)
+                    tel.available_kv -= proj
+                    submit_t[r] = now
         # the tick: expiry, probe, control plane, plan, step_gpu, round ends
         due = admission and now >= next_control - 1e-9
+        pre = eng.get_scalars() if (log is not None and due) else None
         si = eng.step_in(now, due, tools.active_count(), tools.queued_count(), slots,
                          N.MODE_ADVANCE)
         res = eng.step(si)
         if res.status:
             raise RuntimeError(f"device step status {res.status}")
+        if log is not None:
+            for r, b in zip(res.expired_rows.tolist(), res.expired_blocks.tolist()):
+                evict_log(r, b, "pinned", "pin_expired", now)   # sim.py:324-325
+            tel.probe(int(res.free_after_expiry), total_blocks, tools, active)   # sim.py:327
+            if due:  # sim.py:328-335: refresh_pressure, telemetry, balance_and_admit
+                post = eng.get_scalars()
+                post.ema_blocks, post.has_ema_blocks = pre.ema_blocks, pre.has_ema_blocks
+                log.emit(now, "telemetry", None, **tel.snapshot(post))
+                log.emit(now, "window_update", None, w_adm=float(post.w_adm),
+                         limit=int(res.limit), slots=int(res.slots),
+                         admitted=[sid[r] for r in res.admitted_rows.tolist()],
+                         cpu_overloaded=bool(post.cpu_overloaded),
+                         kv_overloaded=bool(post.kv_overloaded))
+                for r in res.admitted_rows.tolist():
+                    admit_log(r, now)
+            # build_plan's ordered pool journal (scheduler.py:300-370 via sim.py:186-188)
+            for op, r, k in zip(res.journal_op.tolist(), res.journal_row.tolist(),
+                                res.journal_n.tolist()):
+                if op == 1:
+                    log.emit(now, "alloc", sid[r], blocks=k)
+                elif op == 3:
+                    evict_log(r, k, "pinned", "reclaim", now)
+                else:
+                    evict_log(r, k, "running", "preempt", now)
         if due:
             next_control = now + cfg.control_interval_s
             admitted = set(int(x) for x in res.admitted_rows)
@@ -227,18 +367,61 @@ def _run(eng: MarsEngine, cfg, order, total_blocks: int, slots: int, max_ticks: 
         if res.total_tokens > 0:
             cnt["gpu_tokens"] += int(res.total_tokens)
             end = now + tick
-            for r, kind in zip(res.end_rows.tolist(), res.end_kind.tolist()):
+            dec_rows = res.decode_rows.tolist()
+            if log is not None:
+                log.emit(now, "tick", None, tokens=int(res.total_tokens),
+                         decodes=[sid[r] for r in dec_rows],
+                         prefills=[[sid[r], g] for r, g in zip(res.prefill_rows.tolist(),
+                                                               res.prefill_grants.tolist())],
+                         evictions=len(res.evict_rows))
+            for e, (r, kind) in enumerate(zip(res.end_rows.tolist(), res.end_kind.tolist())):
+                blk = int(res.end_blocks[e])
                 if kind == 0:
                     cnt["completed"] += 1
                     active -= 1
+                    if log is not None:   # sim.py:240-248
+                        if blk > 0:
+                            log.emit(end, "free", sid[r], blocks=blk)
+                        log.emit(end, "gpu_end", sid[r], round=rnd[r], done=True,
+                                 freed_blocks=blk)
+                        tel.available_kv += blk
                     continue
+                if log is not None and decides:   # sim.py:250-260
+                    log.emit(end, "retention", sid[r], pin=bool(res.end_pin[e]),
+                             benefit_s=float(res.end_benefit[e]), cost_s=float(res.end_cost[e]),
+                             deadline=float(res.end_deadline[e]))
                 if kind == 1:
                     cnt["pins"] += 1
                     pinned += 1
+                    freed = 0
+                    if log is not None:
+                        log.emit(end, "pin", sid[r], blocks=blk)
                 else:
                     cnt["evictions"] += 1
+                    freed = blk
+                    if log is not None:
+                        if blk > 0:
+                            log.emit(end, "free", sid[r], blocks=blk)
+                        log.emit(end, "evict", sid[r], blocks=blk, victim="boundary",
+                                 reason="tool_boundary")
                 dur = order[r].rounds[rnd[r]].tool_duration_s
-                tools.start_tool(r, dur if dur is not None else 0.0, end)
+                dur = dur if dur is not None else 0.0
+                if log is not None:
+                    log.emit(end, "gpu_end", sid[r], round=rnd[r], done=False, freed_blocks=freed)
+                    tel.available_kv += freed
+                started = tools.start_tool(r, dur, end)
+                if log is not None:   # sim.py:273-279
+                    log.emit(end, "tool_num", sid[r], queued=tools.queued_count(), duration_s=dur)
+                    if started:
+                        log.emit(end, "tool_start", sid[r], duration_s=dur,
+                                 active=tools.active_count())
+                        tel.active_tools += 1
+            if log is not None:   # first tokens (sim.py:365-371), prefills after decodes
+                for r, pd in zip(res.prefill_rows.tolist(), res.prefill_done.tolist()):
+                    if pd and (r, rnd[r]) not in first_seen:
+                        first_seen.add((r, rnd[r]))
+                        log.emit(end, "gpu_1st_token", sid[r], round=rnd[r],
+                                 launch_delay_s=end - submit_t[r])
             clock = end
             continue
         # idle tick: jump to the next instant anything can change (sim.py:377-418)
@@ -260,4 +443,6 @@ def _run(eng: MarsEngine, cfg, order, total_blocks: int, slots: int, max_ticks: 
         target = min(cand)
         steps = max(1, math.ceil((target - now) / tick - 1e-9))
         clock = now + steps * tick
+    if log is not None:   # sim.py:421
+        log.emit(clock, "telemetry", None, **tel.snapshot(eng.get_scalars()))
     return cnt, clock

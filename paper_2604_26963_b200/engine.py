@@ -75,6 +75,12 @@ class StepResult:
     fin_deadline: np.ndarray
     end_rows: np.ndarray   # MARS_MODE_ADVANCE: rounds that ended (decode order)
     end_kind: np.ndarray   # 0 done, 1 pinned -> tool, 2 freed -> tool
+    end_blocks: np.ndarray     # blocks pinned or freed at the round's end
+    end_pin: np.ndarray        # the retention decision (when the policy makes one)
+    end_benefit: np.ndarray
+    end_cost: np.ndarray
+    end_deadline: np.ndarray
+    prefill_done: np.ndarray   # MARS_MODE_ADVANCE: the grant finished the prefill
     n_ready: int
     n_promoted: int
     pack_mode: int
@@ -273,6 +279,12 @@ class MarsEngine:
             fin_deadline=_arr(o.fin_deadline, o.n_finish, np.float64),
             end_rows=_arr(o.end_rows, o.n_round_end, np.uint32),
             end_kind=_arr(o.end_kind, o.n_round_end, np.uint8),
+            end_blocks=_arr(o.end_blocks, o.n_round_end, np.int32),
+            end_pin=_arr(o.end_pin, o.n_round_end, np.uint8),
+            end_benefit=_arr(o.end_benefit, o.n_round_end, np.float64),
+            end_cost=_arr(o.end_cost, o.n_round_end, np.float64),
+            end_deadline=_arr(o.end_deadline, o.n_round_end, np.float64),
+            prefill_done=_arr(o.prefill_done, o.n_prefill if o.prefill_done else 0, np.uint8),
             n_ready=o.n_ready, n_promoted=o.n_promoted, pack_mode=o.pack_mode,
             total_tokens=o.total_tokens, free_after_expiry=o.free_after_expiry,
             free_blocks=o.free_blocks, limit=o.limit, slots=o.slots,
@@ -324,6 +336,18 @@ class MarsEngine:
                                          dur.ctypes.data, newp.ctypes.data, dec.ctypes.data,
                                          float(now), cnt.ctypes.data))
         return {"warm": int(cnt[0]), "cold": int(cnt[1]), "evicted": int(cnt[2])}
+
+    def resume_rows(self, n: int) -> Dict[str, np.ndarray]:
+        """Per row of the last ``resume`` (mars_resume_rows): ``kind`` 0 warm,
+        1 cold, 2 cold after the return-time release of an expired pin;
+        ``blocks`` unpinned or released; the gpu_submit payload's ``context``,
+        ``need`` (required_prefill) and ``projected`` blocks (sim.py:190-231)."""
+        out = {k: np.zeros(n, np.int32) for k in ("blocks", "context", "need", "projected")}
+        out["kind"] = np.zeros(n, np.uint8)
+        self._check(self.lib.mars_resume_rows(
+            self.ctx, n, out["kind"].ctypes.data, out["blocks"].ctypes.data,
+            out["context"].ctypes.data, out["need"].ctypes.data, out["projected"].ctypes.data))
+        return out
 
     def kernel_times(self) -> Dict[str, float]:
         ms = (C.c_float * len(N.KTIME_NAMES))()
