@@ -323,6 +323,59 @@ def run_reference_arm(a):
     print(json.dumps(line), flush=True)
 
 
+def advance_run(eng, snap, stream, flush, ticks):
+    """SURVEY §8(f) row 1 measured: ``ticks`` consecutive whole ticks on the
+    device from the 1M snapshot (MARS_MODE_ADVANCE: the scheduling step plus
+    step_gpu / charge_service / every ending round's retention, pin or free),
+    the control plane due every control_interval_s as in the reference loop.
+    The state stays in HBM from tick to tick (no restore); each tick is timed
+    with CUDA events around its graph launch, L2 flushed before it, and its
+    outputs fetched after it (untimed).  The sequence is run once untimed
+    first so every launch shape's graph is captured."""
+    import torch
+
+    from paper_2604_26963_b200 import _native as N
+    cfg = eng.cfg
+    tick = float(cfg.tick_duration_s)
+
+    def run(timed):
+        eng.restore()
+        now, next_ctl = snap.now, snap.now
+        out, evs = [], []
+        for _ in range(ticks):
+            due = now >= next_ctl - 1e-9
+            if due:
+                next_ctl = now + float(cfg.control_interval_s)
+            si = eng.step_in(now, due, snap.active_tools, snap.queued_tools, snap.worker_slots,
+                             N.MODE_ADVANCE)
+            eng.flush_l2(flush)
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            eng.enqueue(si)
+            s1.record(stream)
+            r = eng.fetch()
+            if r.status:
+                raise SystemExit(f"advance tick status {r.status}")
+            evs.append((s0, s1))
+            out.append((due, int(r.total_tokens), len(r.end_rows), len(r.admitted_rows)))
+            now = now + tick
+        return [a.elapsed_time(b) for a, b in evs], out
+
+    run(False)
+    ms, out = run(True)
+    eng.restore()
+    ctl = [m for m, o in zip(ms, out) if o[0]]
+    plain = [m for m, o in zip(ms, out) if not o[0]]
+    return {"ticks": ticks, "sessions": snap.n, "ms_per_tick": sum(ms) / len(ms),
+            "ms_per_tick_control": (sum(ctl) / len(ctl)) if ctl else None,
+            "ms_per_tick_no_control": (sum(plain) / len(plain)) if plain else None,
+            "ticks_per_s": 1e3 * len(ms) / sum(ms),
+            "tokens": sum(o[1] for o in out), "rounds_ended": sum(o[2] for o in out),
+            "admitted": sum(o[3] for o in out),
+            "timing": "CUDA events around each tick's graph launch, L2 flushed before each "
+                      "tick, state resident in HBM across ticks"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -337,6 +390,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--flush-mb", type=int, default=512)
     ap.add_argument("--no-kv", action="store_true", help="skip the KV evict/restore sweep")
+    ap.add_argument("--advance-ticks", type=int, default=40,
+                    help="consecutive device-resident ticks (MARS_MODE_ADVANCE) to time; 0 = off")
     ap.add_argument("--hbm-sweep", default="100000,4000000,16000000,64000000",
                     help="table sizes for the size sweep: SURVEY config (2) at 100K, then beyond L2 (comma list, '' to skip)")
     a = ap.parse_args()
@@ -346,7 +401,7 @@ def main():
     import numpy as np
     import torch
 
-    from paper_2604_26963_b200.engine import MarsEngine, make_config
+    from paper_2604_26963_b200.engine import MarsEngine, make_config, step_columns
     from paper_2604_26963_b200.snapshot import snapshot_v1
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -477,8 +532,10 @@ def main():
     scan_avg = sum(kt["k_scan"] for kt in ktimes) / len(ktimes)
 
     # e2e: through the C ABI with host buffers: upload the table from pinned
-    # host memory, run the step, fetch the plan/journal/decisions to the host
-    pinned = {k: torch.from_numpy(v).pin_memory().numpy() for k, v in snap.cols.items()}
+    # host memory (every column this configuration's step reads,
+    # engine.step_columns), run the step, fetch the plan/journal/decisions
+    pinned = {k: torch.from_numpy(snap.cols[k]).pin_memory().numpy()
+              for k in step_columns(mode=si.mode)}
     h2d = sum(v.nbytes for v in pinned.values())
     e2e_t = []
     d2h = 0
@@ -501,6 +558,9 @@ def main():
     if dist is not None:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_s = float(te.item())
+
+    adv = advance_run(eng, snap, stream, flush, a.advance_ticks) if (
+        world == 1 and a.advance_ticks > 0) else None
 
     peak, peak_kind = _peaks()
     sb = scan_bytes(snap)
@@ -530,6 +590,7 @@ def main():
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "ms_per_step": e2e_s * 1e3},
         "gpu_launches": launches,
+        "advance": adv,
         "kernel_ms_median": kernel_ms,
         "clocks": clk.summary(),
         "step_ms_min": min(step_ms), "step_ms_max": max(step_ms),

@@ -68,9 +68,15 @@ struct mars_ctx {
   i64 pinned_upper = 0;
   int last_launches = 0;
   bool use_graph = false;
-  cudaGraphExec_t graph_exec = nullptr;
-  long long graph_key[10] = {};
-  int graph_launches = 0;
+  // whole-step CUDA graphs by launch shape: a small cache, so a device-resident
+  // run alternating control / non-control ticks replays instead of recapturing
+  static constexpr int NGRAPH = 4;
+  static constexpr int NKEY = 11;
+  cudaGraphExec_t graph_exec[NGRAPH] = {};
+  long long graph_key[NGRAPH][NKEY] = {};
+  int graph_launches[NGRAPH] = {};
+  unsigned long long graph_used[NGRAPH] = {};
+  unsigned long long graph_clock = 0;
   bool profiling = false;
   cudaEvent_t prof[2 * MARS_NUM_KTIMES] = {};
   int prof_used[MARS_NUM_KTIMES] = {};
@@ -460,7 +466,8 @@ int mars_destroy(mars_ctx* ctx) {
   }
   for (auto& e : ctx->prof)
     if (e) cudaEventDestroy(e);
-  if (ctx->graph_exec) cudaGraphExecDestroy(ctx->graph_exec);
+  for (auto& g : ctx->graph_exec)
+    if (g) cudaGraphExecDestroy(g);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->ev_head) cudaEventDestroy(ctx->ev_head);
@@ -689,31 +696,45 @@ int mars_step_enqueue(mars_ctx* ctx, const mars_step_in* in) {
   // whole-step CUDA graph, re-captured only when the launch shape changes
   i64 qb = 1;
   while (qb < a.queue_upper) qb <<= 1;
-  long long key[10] = {a.n_rows, a.control_possible, a.queue_passes, qb, a.exp_sort,
-                       a.exp_may_be_big, a.prof ? 1 : 0, (long long)(uintptr_t)ctx->stream,
-                       a.pack_early, a.advance};
-  if (!ctx->graph_exec || memcmp(key, ctx->graph_key, sizeof key) != 0) {
-    if (ctx->graph_exec) {
-      cudaGraphExecDestroy(ctx->graph_exec);
-      ctx->graph_exec = nullptr;
+  long long key[mars_ctx::NKEY] = {a.n_rows, a.control_possible, a.queue_passes, qb, a.exp_sort,
+                                   a.exp_may_be_big, a.prof ? 1 : 0,
+                                   (long long)(uintptr_t)ctx->stream, a.pack_early, a.advance,
+                                   a.kv ? 1 : 0};
+  int gi = -1;
+  for (int i = 0; i < mars_ctx::NGRAPH; ++i)
+    if (ctx->graph_exec[i] && memcmp(key, ctx->graph_key[i], sizeof key) == 0) gi = i;
+  if (gi < 0) {
+    // evict the least recently used entry (or take an empty one)
+    gi = 0;
+    for (int i = 0; i < mars_ctx::NGRAPH; ++i) {
+      if (!ctx->graph_exec[i]) {
+        gi = i;
+        break;
+      }
+      if (ctx->graph_used[i] < ctx->graph_used[gi]) gi = i;
+    }
+    if (ctx->graph_exec[gi]) {
+      cudaGraphExecDestroy(ctx->graph_exec[gi]);
+      ctx->graph_exec[gi] = nullptr;
     }
     cudaGraph_t g = nullptr;
     if (ctx->stream == nullptr || ctx->stream == cudaStreamLegacy ||
         ctx->stream == cudaStreamPerThread)
       return fail(ctx, MARS_ERR_ARG, "graph mode needs a non-default stream");
     CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-    ctx->graph_launches = mars_enqueue_step(&a);
+    ctx->graph_launches[gi] = mars_enqueue_step(&a);
     cudaError_t ce = cudaStreamEndCapture(ctx->stream, &g);
     if (ce != cudaSuccess) {
       cudaGetLastError();
       return fail(ctx, MARS_ERR_CUDA, "graph capture failed: %s", cudaGetErrorString(ce));
     }
-    CK(cudaGraphInstantiate(&ctx->graph_exec, g, 0));
+    CK(cudaGraphInstantiate(&ctx->graph_exec[gi], g, 0));
     cudaGraphDestroy(g);
-    memcpy(ctx->graph_key, key, sizeof key);
+    memcpy(ctx->graph_key[gi], key, sizeof key);
   }
-  CK(cudaGraphLaunch(ctx->graph_exec, ctx->stream));
-  ctx->last_launches = ctx->graph_launches;
+  ctx->graph_used[gi] = ++ctx->graph_clock;
+  CK(cudaGraphLaunch(ctx->graph_exec[gi], ctx->stream));
+  ctx->last_launches = ctx->graph_launches[gi];
   return MARS_OK;
 }
 

@@ -29,6 +29,24 @@ _CT = {np.uint8: C.c_uint8, np.uint32: C.c_uint32, np.int32: C.c_int32, np.int64
        np.float64: C.c_double}
 
 
+def step_columns(policy: str = "mars", enable_coordinator: bool = True, mode: int = 0):
+    """The session-table columns a step reads in this configuration -- what a
+    caller holding the state on the host must upload before each step
+    (mars_upsert_rows).  ``arrival`` is the order key only with the coordinator
+    off (scheduler.py:391-392 ablation) or for the comparison policies, and
+    admission stamps ``now`` instead (baselines.py:351-356); ``served`` is read
+    by charge_service (SERVICE / ADVANCE) and program_priority's key;
+    ``rounds_left`` only by the tick's tail (ADVANCE)."""
+    skip = set()
+    if policy == "mars" and enable_coordinator:
+        skip.add("arrival")
+    if policy != "program_priority" and not (mode & (N.MODE_SERVICE | N.MODE_ADVANCE)):
+        skip.add("served")
+    if not (mode & N.MODE_ADVANCE):
+        skip.add("rounds_left")
+    return [k for k in COLUMNS if k not in skip]
+
+
 def make_config(enable_coordinator: bool = True, enable_coscheduler: bool = True,
                 initial_window: Optional[float] = None, policy: str = "mars",
                 **overrides) -> N.MarsConfig:

@@ -208,3 +208,28 @@ def test_pack_sort_inside_control_plane_multi_batch(monkeypatch):
     for kind in ("queue_shuffled", "desc_sorted", "hot_req"):
         snap = variant(200_000, 72, kind)
         assert_same(device_step(snap.copy(), sort_path=1), run_step(snap.copy()))
+
+
+@pytest.mark.parametrize("pool", ["headroom", "pressure"])
+def test_step_reads_only_its_columns(pool):
+    """engine.step_columns (the e2e upload set): the columns it leaves out
+    cannot change the step's decisions in that configuration."""
+    from paper_2604_26963_b200.engine import step_columns
+    snap = snapshot_v1(60_000, seed=7, pool=pool)
+    want = device_step(snap.copy())
+    junk = snap.copy()
+    rng = np.random.default_rng(3)
+    keep = set(step_columns())
+    for k, a in junk.cols.items():
+        if k in keep:
+            continue
+        if a.dtype.kind == "f":
+            junk.cols[k] = rng.uniform(-1e6, 1e6, a.shape).astype(a.dtype)
+        else:
+            junk.cols[k] = rng.integers(0, 1000, a.shape).astype(a.dtype)
+    assert keep != set(snap.cols)
+    got = device_step(junk)
+    for k in got["state"]:   # the end-state dump shows the junk itself
+        if k not in keep:
+            got["state"][k] = want["state"][k]
+    assert canon(got) == canon(want)
