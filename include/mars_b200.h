@@ -247,6 +247,9 @@ int mars_get_scalars(mars_ctx* ctx, mars_scalars* s);                           
 int mars_step(mars_ctx* ctx, const mars_step_in* in, mars_step_out* out);          /* sync */
 int mars_step_enqueue(mars_ctx* ctx, const mars_step_in* in);   /* async, device-resident */
 int mars_step_fetch(mars_ctx* ctx, mars_step_out* out);          /* sync, after enqueue */
+/* the pinned host arena every mars_step_out array points into (valid for the
+ * context's lifetime; contents valid until the next fetch) */
+int mars_output_arena(mars_ctx* ctx, void** base, int64_t* bytes);
 /* capture the whole step (both streams) as one CUDA graph; re-captured only
  * when the launch shape (rows, queue bucket, mode) changes */
 int mars_set_graph(mars_ctx* ctx, int on);

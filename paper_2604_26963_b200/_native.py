@@ -153,6 +153,7 @@ _SIGS = {
     "mars_host_link_peak": (i32, [C.c_void_p, i64, C.c_int, P(f64), P(f64), P(f64)]),
     "mars_resume": (i32, [C.c_void_p, i64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                           C.c_void_p, f64, C.c_void_p]),
+    "mars_output_arena": (i32, [C.c_void_p, P(C.c_void_p), P(i64)]),
     "mars_resume_rows": (i32, [C.c_void_p, i64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                C.c_void_p]),
     "mars_retention_batch": (i32, [C.c_void_p, i64, C.c_void_p, C.c_void_p, i64, f64, f64, f64,

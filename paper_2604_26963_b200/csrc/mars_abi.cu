@@ -51,6 +51,7 @@ struct mars_ctx {
   Work* h_work = nullptr;
   mars_scalars* h_sc = nullptr;
   unsigned char* h_out = nullptr;  // pinned output arena
+  OutList out_list{};              // the fetch's pending array copies
   size_t h_out_bytes = 0;
   // device staging for row scatter/gather
   unsigned char* d_stage = nullptr;
@@ -372,7 +373,7 @@ int mars_create(const mars_config* hcfg, int device, int64_t max_rows, int64_t m
   CK(cudaMallocHost((void**)&ctx->h_in, sizeof(mars_step_in)));
   CK(cudaMallocHost((void**)&ctx->h_work, sizeof(Work)));
   CK(cudaMallocHost((void**)&ctx->h_sc, sizeof(mars_scalars)));
-  ctx->h_out_bytes = (size_t)R * 48 + (size_t)Qc * 4 + (size_t)b.j_cap * 9 + 4 * WIN_MAX * 4 + WIN_MAX * 40 + 8192;
+  ctx->h_out_bytes = (size_t)R * 48 + (size_t)Qc * 4 + (size_t)b.j_cap * 9 + 4 * WIN_MAX * 4 + WIN_MAX * 80 + 8192;
   CK(cudaMallocHost((void**)&ctx->h_out, ctx->h_out_bytes));
   memset(ctx->h_in, 0, sizeof(mars_step_in));
   // scalars: empty pool of one block until mars_set_scalars
@@ -754,18 +755,27 @@ int mars_set_graph(mars_ctx* ctx, int on) {
   return MARS_OK;
 }
 
-// copy a device array into the pinned arena and return its host address
+// place a device array in the pinned arena (copied by the one k_gather_out
+// launch of the fetch) and return its host address
 static const void* pull(mars_ctx* ctx, size_t& off, const void* dev, size_t bytes) {
   off = (off + 15) & ~(size_t)15;
   if (off + bytes > ctx->h_out_bytes) return nullptr;
   void* h = ctx->h_out + off;
-  if (bytes) cudaMemcpyAsync(h, dev, bytes, cudaMemcpyDeviceToHost, ctx->stream);
+  if (bytes) {
+    OutList& L = ctx->out_list;
+    if (L.n == OUT_MAX) {  // never with the fixed output set; flush and go on
+      mars_enqueue_gather_out(ctx->stream, L, ctx->h_out);
+      L.n = 0;
+    }
+    L.d[L.n++] = {dev, (unsigned long long)off, (unsigned long long)bytes};
+  }
   off += bytes;
   return h;
 }
 
 int mars_step_fetch(mars_ctx* ctx, mars_step_out* o) {
   if (!ctx || !o) return MARS_ERR_ARG;
+  ctx->out_list.n = 0;
   CK(cudaSetDevice(ctx->device));
   CK(cudaMemcpyAsync(ctx->h_work, ctx->work, sizeof(Work), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
@@ -837,6 +847,11 @@ int mars_step_fetch(mars_ctx* ctx, mars_step_out* o) {
   o->fin_benefit = (const double*)pull(ctx, off, b.fin_b, (size_t)w.n_finish * 8);
   o->fin_cost = (const double*)pull(ctx, off, b.fin_c, (size_t)w.n_finish * 8);
   o->fin_deadline = (const double*)pull(ctx, off, b.fin_d, (size_t)w.n_finish * 8);
+  {
+    int rc = mars_enqueue_gather_out(ctx->stream, ctx->out_list, ctx->h_out);
+    ctx->out_list.n = 0;
+    if (rc) return fail(ctx, MARS_ERR_CUDA, "fetch: %s", cudaGetErrorString((cudaError_t)rc));
+  }
   CK(cudaStreamSynchronize(ctx->stream));
   CK(cudaGetLastError());
   if (sharded && n_adm > 1) {
@@ -857,6 +872,13 @@ int mars_step_fetch(mars_ctx* ctx, mars_step_out* o) {
     ctx->q_upper -= w.take;
   }
   if (ctx->q_upper < 0) ctx->q_upper = 0;
+  return MARS_OK;
+}
+
+int mars_output_arena(mars_ctx* ctx, void** base, int64_t* bytes) {
+  if (!ctx || !base || !bytes) return MARS_ERR_ARG;
+  *base = ctx->h_out;
+  *bytes = (int64_t)ctx->h_out_bytes;
   return MARS_OK;
 }
 

@@ -3239,6 +3239,32 @@ __global__ void k_retention_batch(Cfg c, i64 n, const i32* ctx, const i32* kv, i
   }
 }
 
+// fetch: every output array of the step into the pinned host arena in one
+// launch (blockIdx.y = array), 16-byte stores where both sides allow
+__global__ void __launch_bounds__(256) k_gather_out(OutList L, unsigned char* dst) {
+  const OutDesc D = L.d[blockIdx.y];
+  const unsigned char* src = (const unsigned char*)D.src;
+  unsigned char* out = dst + D.dst_off;
+  const unsigned long long n16 =
+      (((uintptr_t)src | (uintptr_t)out) & 15) == 0 ? D.bytes / 16 : 0;
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n16;
+       i += (unsigned long long)gridDim.x * blockDim.x)
+    ((uint4*)out)[i] = __ldcg((const uint4*)src + i);
+  for (unsigned long long i = n16 * 16 + (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+       i < D.bytes; i += (unsigned long long)gridDim.x * blockDim.x)
+    out[i] = src[i];
+}
+
+int mars_enqueue_gather_out(cudaStream_t s, const OutList& L, unsigned char* host_dst) {
+  if (L.n <= 0) return 0;
+  unsigned long long mx = 0;
+  for (int i = 0; i < L.n; ++i) mx = L.d[i].bytes > mx ? L.d[i].bytes : mx;
+  unsigned long long gx = (mx / 16 + 255) / 256;
+  gx = gx < 1 ? 1 : (gx > 64 ? 64 : gx);
+  k_gather_out<<<dim3((unsigned)gx, (unsigned)L.n), 256, 0, s>>>(L, host_dst);
+  return (int)cudaGetLastError();
+}
+
 __global__ void k_flush(u8* p, i64 n, u32 salt) {
   u32* q = (u32*)p;
   i64 m = n / 4;

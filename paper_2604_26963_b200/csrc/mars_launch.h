@@ -42,6 +42,18 @@ int mars_enqueue_retention(const Cfg& c, cudaStream_t s, i64 n, const i32* ctx, 
                            i64 total, double usage, double ema, double now, u8* pin, double* bb,
                            double* cc, double* dd);
 int mars_enqueue_flush(cudaStream_t s, u8* p, i64 n, u32 salt);
+// the step's outputs -> the pinned host arena in one launch (the kernel
+// stores straight into the mapped host buffer; one descriptor per array)
+#define OUT_MAX 48
+struct OutDesc {
+  const void* src;
+  unsigned long long dst_off, bytes;
+};
+struct OutList {
+  OutDesc d[OUT_MAX];
+  int n;
+};
+int mars_enqueue_gather_out(cudaStream_t s, const OutList& L, unsigned char* host_dst);
 int mars_enqueue_resume(const Tab& t, const Cfg& c, mars_scalars* sc, cudaStream_t s, i64 n,
                         const i64* rows, const double* fin, const double* dur, const i32* newp,
                         const i32* dec, double now, int* counts, u8* o_kind, i32* o_blk,

@@ -110,6 +110,31 @@ class StepResult:
     diag: Dict[str, int] = field(default_factory=dict)
 
 
+# (array, count field, dtype) of every mars_step_out array, with the byte
+# offsets of its pointer (in 8-byte units) and count (4-byte units)
+_OUT_ARRAYS = [
+    ("expired_rows", "n_expired", np.uint32), ("expired_blocks", "n_expired", np.int32),
+    ("admitted_rows", "n_admitted", np.uint32), ("window_rows", "n_window", np.uint32),
+    ("decode_rows", "n_decode", np.uint32), ("prefill_rows", "n_prefill", np.uint32),
+    ("prefill_grants", "n_prefill", np.int32), ("evict_rows", "n_evict", np.uint32),
+    ("evict_kind", "n_evict", np.uint8), ("evict_blocks", "n_evict", np.int32),
+    ("journal_op", "n_journal", np.uint8), ("journal_row", "n_journal", np.uint32),
+    ("journal_n", "n_journal", np.int32), ("ret_rows", "n_retention", np.uint32),
+    ("ret_pin", "n_retention", np.uint8), ("ret_benefit", "n_retention", np.float64),
+    ("ret_cost", "n_retention", np.float64), ("ret_deadline", "n_retention", np.float64),
+    ("decode_level", "n_decode", np.uint8), ("prefill_level", "n_prefill", np.uint8),
+    ("fin_rows", "n_finish", np.uint32), ("fin_pin", "n_finish", np.uint8),
+    ("fin_benefit", "n_finish", np.float64), ("fin_cost", "n_finish", np.float64),
+    ("fin_deadline", "n_finish", np.float64), ("end_rows", "n_round_end", np.uint32),
+    ("end_kind", "n_round_end", np.uint8), ("end_blocks", "n_round_end", np.int32),
+    ("end_pin", "n_round_end", np.uint8), ("end_benefit", "n_round_end", np.float64),
+    ("end_cost", "n_round_end", np.float64), ("end_deadline", "n_round_end", np.float64),
+    ("prefill_done", "n_prefill", np.uint8),
+]
+_OUT_SPEC = [(a, getattr(N.MarsStepOut, a).offset // 8, getattr(N.MarsStepOut, c).offset // 4,
+              np.dtype(d), np.dtype(d).itemsize) for a, c, d in _OUT_ARRAYS]
+
+
 def _arr(p, n, dt):
     if n <= 0:
         return np.zeros(0, dtype=dt)
@@ -130,6 +155,7 @@ class MarsEngine:
                                      C.byref(ctx)))
         self.ctx = ctx
         self.n_rows = 0
+        self._out = None
 
     def close(self) -> None:
         if self.ctx:
@@ -266,6 +292,43 @@ class MarsEngine:
         self._check(self.lib.mars_step_enqueue(self.ctx, C.byref(si)))
 
     def fetch(self) -> StepResult:
+        if self._out is None:
+            self._fetch_setup()
+        o = self._out
+        self._check(self.lib.mars_step_fetch(self.ctx, C.byref(o)))
+        i32, p64, arena, base = self._out_i32, self._out_p64, self._arena, self._arena_base
+        arrs = {}
+        for name, po, co, dt, isz in _OUT_SPEC:
+            n = int(i32[co])
+            p = int(p64[po]) if n > 0 else 0
+            if p == 0:
+                arrs[name] = np.empty(0, dt)
+            else:
+                s0 = p - base
+                arrs[name] = arena[s0:s0 + n * isz].view(dt).copy()
+        return StepResult(
+            status=o.status, **arrs,
+            n_ready=o.n_ready, n_promoted=o.n_promoted, pack_mode=o.pack_mode,
+            total_tokens=o.total_tokens, free_after_expiry=o.free_after_expiry,
+            free_blocks=o.free_blocks, limit=o.limit, slots=o.slots,
+            diag={"n_window_cand": o.n_window_cand, "n_victim_cand": o.n_victim_cand,
+                  "walk_slow": o.walk_slow, "sort_path": o.sort_path,
+                  "n_round_end": o.n_round_end, "n_done": o.n_done})
+
+    def _fetch_setup(self) -> None:
+        base, size = C.c_void_p(), C.c_int64()
+        self._check(self.lib.mars_output_arena(self.ctx, C.byref(base), C.byref(size)))
+        self._arena_base = int(base.value)
+        self._arena = np.ctypeslib.as_array((C.c_uint8 * int(size.value)).from_address(
+            self._arena_base))
+        self._out = N.MarsStepOut()
+        raw = np.frombuffer(self._out, np.uint8)
+        self._out_i32 = raw[:len(raw) // 4 * 4].view(np.int32)
+        self._out_p64 = raw[:len(raw) // 8 * 8].view(np.uint64)
+
+    def fetch_reference(self) -> StepResult:
+        """The field-by-field conversion (kept for the tests that check the
+        fast path against it)."""
         o = N.MarsStepOut()
         self._check(self.lib.mars_step_fetch(self.ctx, C.byref(o)))
         return StepResult(

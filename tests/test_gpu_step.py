@@ -233,3 +233,26 @@ def test_step_reads_only_its_columns(pool):
         if k not in keep:
             got["state"][k] = want["state"][k]
     assert canon(got) == canon(want)
+
+
+@pytest.mark.parametrize("pool", ["headroom", "pressure"])
+def test_fast_fetch_matches_field_by_field(pool):
+    """engine.fetch (one gather launch into the pinned arena, arrays sliced
+    from one view of it) against the field-by-field conversion."""
+    from dataclasses import fields
+    snap = snapshot_v1(60_000, seed=11, pool=pool)
+    eng = MarsEngine(max_rows=snap.n, max_queue=len(snap.queue),
+                     config=make_config(initial_window=snap.initial_window))
+    eng.load_snapshot(snap)
+    si = eng.step_in(snap.now, True, snap.active_tools, snap.queued_tools, snap.worker_slots)
+    a = eng.step(si)
+    b = eng.fetch_reference()
+    for f in fields(a):
+        x, y = getattr(a, f.name), getattr(b, f.name)
+        if isinstance(x, np.ndarray):
+            assert x.dtype == y.dtype and np.array_equal(x, y), f.name
+        else:
+            assert x == y, f.name
+    assert len(a.ret_rows) > 0 and len(a.journal_op) > 0
+    assert pool == "pressure" or len(a.admitted_rows) > 0
+    eng.close()
