@@ -1010,6 +1010,10 @@ int mars_resume(mars_ctx* ctx, int64_t n, const int64_t* rows, const double* fin
   int rc = mars_enqueue_resume(ctx->tab, ctx->cfg, ctx->sc, ctx->stream, n, drows, dfin, ddur,
                                dnew, ddec, now, dcnt, o_kind, o_blk, o_ctx, o_need, o_proj);
   if (rc) return fail(ctx, MARS_ERR_CUDA, "resume: %s", cudaGetErrorString((cudaError_t)rc));
+  if (ctx->kv_on) {
+    rc = mars_kv_enqueue_resume_free(ctx->kv, ctx->stream, n, drows, o_kind);
+    if (rc) return fail(ctx, MARS_ERR_CUDA, "resume kv: %s", cudaGetErrorString((cudaError_t)rc));
+  }
   int hc[4] = {0, 0, 0, 0};
   CK(cudaMemcpyAsync(hc, dcnt, sizeof hc, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));

@@ -104,7 +104,10 @@ __global__ void __launch_bounds__(KV_TPB) k_kv_apply(Kv k, i64 n_ops, const u8* 
   }
 }
 
-// the step's own journal: expired pins (rank order) then k_walk's journal
+// the step's own journal: expired pins (rank order) then k_walk's journal,
+// then (MARS_MODE_ADVANCE) the tick tail's frees in decode order -- a finished
+// session's blocks (sim.py:243) and an unpinned boundary's (sim.py:269); a
+// pin keeps the table (ownership moves, the IDs stay)
 __global__ void __launch_bounds__(KV_TPB) k_kv_apply_step(Kv k, Work* w, Bufs b) {
   const int ne = w->n_exp;
   for (int i = 0; i < ne; ++i)
@@ -118,6 +121,25 @@ __global__ void __launch_bounds__(KV_TPB) k_kv_apply_step(Kv k, Work* w, Bufs b)
       if (!kv_op(k, MARS_KV_FREE, b.j_row[i], -1)) return;
     }
   }
+  if (w->in.mode & MARS_MODE_ADVANCE) {
+    const int nr = w->n_round_end;
+    for (int i = 0; i < nr; ++i)
+      if (b.end_kind[i] != 1 && !kv_op(k, MARS_KV_FREE, b.end_row[i], -1)) return;
+  }
+}
+
+// resume_from_tool's return-time release of an expired pin (sim.py:203-205),
+// in the tool plane's finish order (kind 2 of mars_resume_rows)
+__global__ void __launch_bounds__(KV_TPB) k_kv_resume_free(Kv k, i64 n, const i64* rows,
+                                                           const u8* kind) {
+  for (i64 i = 0; i < n; ++i)
+    if (kind[i] == 2 && !kv_op(k, MARS_KV_FREE, (u32)rows[i], -1)) return;
+}
+
+int mars_kv_enqueue_resume_free(const Kv& k, cudaStream_t s, i64 n, const i64* rows,
+                                const u8* kind) {
+  k_kv_resume_free<<<1, KV_TPB, 0, s>>>(k, n, rows, kind);
+  return (int)cudaGetLastError();
 }
 
 __global__ void k_kv_table(Kv k, u32 row, i64 cap, u32* out) {

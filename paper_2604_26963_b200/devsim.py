@@ -153,14 +153,18 @@ def run_device_simulation(traces: Sequence, total_blocks: int, tool_worker_slots
                           enable_coscheduler: bool = True, enable_control_plane: bool = True,
                           initial_window: Optional[float] = None, device: int = 0,
                           max_ticks: int = 5_000_000,
-                          log: Optional[EventLog] = None) -> Tuple[Dict[str, int], float]:
+                          log: Optional[EventLog] = None,
+                          kv_state: Optional[dict] = None) -> Tuple[Dict[str, int], float]:
     """``policy`` (a POLICY_KINDS name) over ``traces`` (objects with
     session_id, arrival_time_s and rounds of new_prefill_tokens /
     decode_tokens / tool_duration_s, as agentsched.workload.Trace).  MARS
     admits through its control plane unless ``enable_control_plane`` is off;
     the comparison policies admit at arrival (sim.py:116).  Returns
     (counters, final clock); fills ``log`` with the run's event log when
-    one is given."""
+    one is given.  With ``kv_state`` (a dict) the device block-ID manager
+    rides along (every alloc / free of the run applied to concrete block IDs
+    on the device, mars_kv) and its final free-stack order is stored there
+    as ``kv_state["top"]`` (with ``depth``, ``fresh``, ``status``)."""
     order = sorted(traces, key=lambda t: (t.arrival_time_s, t.session_id))
     n = len(order)
     cfg = make_config(enable_coordinator, enable_coscheduler, initial_window=initial_window,
@@ -174,8 +178,18 @@ def run_device_simulation(traces: Sequence, total_blocks: int, tool_worker_slots
     eng = MarsEngine(max_rows=max(n, 1), max_queue=max(n, 1), device=device, config=cfg)
     decides = (policy == "mars" and enable_coscheduler) or policy in ("static_ttl", "dynamic_ttl")
     try:
-        return _run(eng, cfg, order, total_blocks, tool_worker_slots, max_ticks, cfg_admission,
-                    policy, log, decides)
+        kv = None
+        if kv_state is not None:
+            from .kvstore import KvBlockManager
+            most = max((-(-sum(r.new_prefill_tokens + r.decode_tokens for r in tr.rounds) // bs)
+                        for tr in order), default=1)
+            kv = KvBlockManager(eng, total_blocks, max_blocks_per_row=max(most, 1))
+        out = _run(eng, cfg, order, total_blocks, tool_worker_slots, max_ticks, cfg_admission,
+                   policy, log, decides)
+        if kv is not None:
+            top, depth, fresh, status = kv.state(total_blocks)
+            kv_state.update(top=top, depth=depth, fresh=fresh, status=status)
+        return out
     finally:
         eng.close()
 

@@ -81,3 +81,34 @@ def test_device_simulation_without_log_matches():
     cnt, horizon = run_device_simulation(traces, spec["engine"]["total_blocks"],
                                          spec["engine"]["tool_worker_slots"])
     assert cnt == spec["counters"] and horizon == spec["horizon_s"]
+
+
+@pytest.mark.parametrize("key", ["small12/mars", "small12/mars-no-control", "demo64/mars",
+                                 "small12/static_ttl", "small12/fcfs"])
+def test_device_simulation_block_ids(key):
+    """The device block-ID manager riding along a whole device-resident run
+    (plan journal, expiries, the tail's frees, return-time releases) ends
+    with the free stack the block-ID restatement (oracle/block_ids.py) builds
+    from the run's event log -- itself byte-identical to the reference's."""
+    from oracle.block_ids import BlockIdPool
+    spec = SIM[key] if key in SIM else SIM_BASE[key]
+    traces = tracefile.load(os.path.join(GOLDEN, spec["trace"]))
+    variant = key.split("/")[1]
+    kw = dict(VARIANT_KW.get(variant, {}))
+    if key in SIM_BASE:
+        kw["policy"] = spec["policy"]
+    log, kv = EventLog(), {}
+    total = spec["engine"]["total_blocks"]
+    run_device_simulation(traces, total, spec["engine"]["tool_worker_slots"],
+                          enable_control_plane=spec["run"].get("enable_control_plane", True),
+                          log=log, kv_state=kv, **kw)
+    _check_log(key, spec, log)
+    pool = BlockIdPool(total)
+    n_ops = 0
+    for r in log.records:
+        if r["kind"] in ("alloc", "free", "pin", "unpin"):
+            pool.apply(r["kind"], r["session_id"], r["blocks"], r.get("from_pinned", False))
+            n_ops += 1
+    assert n_ops > 100
+    assert kv["status"] == 0
+    assert kv["top"].tolist() == pool.top(total)
