@@ -342,6 +342,7 @@ def advance_run(eng, snap, stream, flush, ticks):
         eng.restore()
         now, next_ctl = snap.now, snap.now
         out, evs = [], []
+        wall.clear()
         for _ in range(ticks):
             due = now >= next_ctl - 1e-9
             if due:
@@ -350,10 +351,13 @@ def advance_run(eng, snap, stream, flush, ticks):
                              N.MODE_ADVANCE)
             eng.flush_l2(flush)
             s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            w0 = time.perf_counter()
             s0.record(stream)
             eng.enqueue(si)
             s1.record(stream)
             r = eng.fetch()
+            wall.append(time.perf_counter() - w0)
             if r.status:
                 raise SystemExit(f"advance tick status {r.status}")
             evs.append((s0, s1))
@@ -361,6 +365,7 @@ def advance_run(eng, snap, stream, flush, ticks):
             now = now + tick
         return [a.elapsed_time(b) for a, b in evs], out
 
+    wall = []
     run(False)
     ms, out = run(True)
     eng.restore()
@@ -370,6 +375,9 @@ def advance_run(eng, snap, stream, flush, ticks):
             "ms_per_tick_control": (sum(ctl) / len(ctl)) if ctl else None,
             "ms_per_tick_no_control": (sum(plain) / len(plain)) if plain else None,
             "ticks_per_s": 1e3 * len(ms) / sum(ms),
+            # host view of the same ticks through the public API (step_in ->
+            # graph launch -> fetch of the plan, journal and decisions)
+            "wall_ms_per_tick": 1e3 * sum(wall) / len(wall),
             "tokens": sum(o[1] for o in out), "rounds_ended": sum(o[2] for o in out),
             "admitted": sum(o[3] for o in out),
             "timing": "CUDA events around each tick's graph launch, L2 flushed before each "

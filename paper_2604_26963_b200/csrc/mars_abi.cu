@@ -1085,7 +1085,6 @@ static void queue_arrays(mars_ctx* ctx, void** qp, size_t* qs) {
 int mars_checkpoint(mars_ctx* ctx) {
   if (!ctx) return MARS_ERR_ARG;
   CK(cudaSetDevice(ctx->device));
-  const i64 R = ctx->max_rows, Qc = ctx->max_queue;
   for (auto& cs : ctx->cols) {
     if (!cs.ckpt) CK(cudaMalloc(&cs.ckpt, (size_t)ctx->alloc_rows * cs.esz));
     CK(cudaMemcpyAsync(cs.ckpt, *cs.dev, (size_t)ctx->n_rows * cs.esz, cudaMemcpyDeviceToDevice,

@@ -1527,7 +1527,7 @@ __device__ void pack_small_cta(Work* w, Queue Q, Lsd L, mars_scalars* sc, i32* q
   if (mode == PACK_FF) {
     // first fit against available_kv, in current list order; fits, then deferred
     __shared__ long long s_cap;
-    __shared__ int s_cursor, s_found, s_nfit;
+    __shared__ int s_cursor, s_nfit;
     if (threadIdx.x == 0) {
       s_cap = w->adm_avail;
       s_nfit = 0;
@@ -1567,8 +1567,7 @@ __device__ void pack_small_cta(Work* w, Queue Q, Lsd L, mars_scalars* sc, i32* q
     for (int base = 0; base < qlen; base += blockDim.x) {
       int i = base + threadIdx.x;
       u32 isfit = (i < qlen) ? fit[i] : 0;
-      u32 isdef = (i < qlen) ? (1u - isfit) : 0;
-      // scan of isfit (and isdef = valid - isfit)
+      // scan of isfit (the deferred count is valid - isfit)
       shu[threadIdx.x] = isfit;
       __syncthreads();
       for (int off = 1; off < (int)blockDim.x; off <<= 1) {
@@ -1585,7 +1584,6 @@ __device__ void pack_small_cta(Work* w, Queue Q, Lsd L, mars_scalars* sc, i32* q
                         : (s_def_run + (int)(threadIdx.x + 1 - incl) - 1);
         L.v[0][pos] = (u32)i;
       }
-      (void)isdef;
       __syncthreads();
       if (threadIdx.x == 0) {
         s_fit_run += (int)tot;
@@ -2805,7 +2803,6 @@ __global__ void __launch_bounds__(WALK_TPB) k_walk(Tab t, Cfg c, Work* w, Bufs b
     long long budget = c.budget;
     long long lim_dec = c.max_dec < budget ? c.max_dec : budget;
     // decode eligibility counts
-    int base = 0;
     long long need_dec = 0;
     int selected_mask[4] = {0, 0, 0, 0};
     int cnt_before = 0;
@@ -2820,7 +2817,6 @@ __global__ void __launch_bounds__(WALK_TPB) k_walk(Tab t, Cfg c, Work* w, Bufs b
       if (sel && block_aligned(c, S.wkv[i])) need_dec += 1;
       cnt_before += __popc(m);
     }
-    (void)base;
     long long ndec = cnt_before < lim_dec ? cnt_before : lim_dec;
     need_dec = warp_sum<long long>(need_dec);
     PTIME(22);
@@ -3284,8 +3280,7 @@ __global__ void __launch_bounds__(1024) k_work_init(Work* w, const mars_step_in*
   uint4* p = (uint4*)w;
   const uint4 z = make_uint4(0, 0, 0, 0);
   for (size_t i = threadIdx.x; i < n16; i += blockDim.x) p[i] = z;
-  unsigned char* tail = (unsigned char*)w + n16 * 16;
-  for (size_t i = threadIdx.x; i < sizeof(Work) - n16 * 16; i += blockDim.x) tail[i] = 0;
+  static_assert(sizeof(Work) % 16 == 0, "Work is zeroed in 16-byte words");
   __syncthreads();
   {
     const unsigned int* src = (const unsigned int*)h_in;

@@ -26,13 +26,11 @@ __device__ __forceinline__ u32 kv_slot(const Kv& k, u32 row, i64 pos) {
 // (n = -1: the whole table).  Returns false on a contract break.
 __device__ bool kv_op(Kv& k, int op, u32 row, i64 n) {
   __shared__ i64 s_top, s_fresh, s_ctop, s_len;
-  __shared__ int s_ok;
   if (threadIdx.x == 0) {
     s_top = k.s->fs_top;
     s_fresh = k.s->fresh;
     s_ctop = k.s->cfs_top;
     s_len = k.len[row];
-    s_ok = 1;
   }
   __syncthreads();
   const i64 top = s_top, fresh = s_fresh, ctop = s_ctop, len = s_len;
