@@ -112,3 +112,69 @@ def test_device_simulation_block_ids(key):
     assert n_ops > 100
     assert kv["status"] == 0
     assert kv["top"].tolist() == pool.top(total)
+
+
+def _synthetic(n, seed):
+    """A larger seeded trace than the frozen ones: many sessions arriving
+    together into a tight pool, so preemptions, reclaims, pins and their
+    expiries all happen often."""
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(n):
+        k = int(rng.integers(1, 5))
+        rounds = []
+        for j in range(k):
+            tool = None if j == k - 1 else float(np.round(rng.uniform(0.05, 6.0), 3))
+            rounds.append(tracefile.RoundRec(int(rng.integers(100, 5000)),
+                                             int(rng.integers(1, 160)), tool))
+        out.append(tracefile.Trace(f"syn{i:04d}", float(np.round(rng.uniform(0, 15.0), 3)),
+                                   rounds))
+    return out
+
+
+SYN = {  # label: (policy, MARS switches, control plane, sessions, pool blocks, tool slots)
+    "mars": ("mars", {}, True, 160, 2500, 6),
+    "mars-600": ("mars", {}, True, 600, 6000, 16),
+    "mars-no-coordinator": ("mars", {"enable_coordinator": False}, True, 150, 2400, 6),
+    "mars-no-coscheduler": ("mars", {"enable_coscheduler": False}, True, 150, 2400, 6),
+    "mars-no-control": ("mars", {}, False, 120, 2000, 4),
+    "fcfs": ("fcfs", {}, True, 100, 2200, 4),
+    "program_priority": ("program_priority", {}, True, 100, 2200, 4),
+    "static_ttl": ("static_ttl", {}, True, 120, 2000, 4),
+    "dynamic_ttl": ("dynamic_ttl", {}, True, 120, 2000, 4),
+}
+
+
+@pytest.mark.parametrize("label", sorted(SYN))
+def test_device_simulation_synthetic_matches_oracle(label):
+    """Whole device-resident run of a synthetic trace against the oracle's
+    tick loop (oracle/loop.py, itself pinned to the reference's logs):
+    counters, final clock, the event log byte for byte and the block IDs."""
+    from oracle import loop
+    from oracle import policy as op
+    from oracle.block_ids import BlockIdPool
+    kind, sw, ctl_on, n, blocks, slots = SYN[label]
+    traces = _synthetic(n, seed=n + blocks)
+    pol = op.MarsOracle(**sw) if kind == "mars" else op.make_oracle_policy(kind)
+    ref = loop.run(traces, loop.Engine(blocks, tool_worker_slots=slots), pol,
+                   enable_control_plane=ctl_on)
+    assert ref.counters["preemptions"] > 0 and ref.counters["completed"] == n
+    log, kv = EventLog(), {}
+    cnt, horizon = run_device_simulation(traces, blocks, slots, policy=kind,
+                                         enable_control_plane=ctl_on, log=log, kv_state=kv,
+                                         **sw)
+    assert cnt == ref.counters
+    assert horizon == ref.horizon_s
+    got, want = log.jsonl_bytes(), ref.log.jsonl_bytes()
+    if got != want:
+        for i, (a, b) in enumerate(zip(log.records, ref.events)):
+            if json.dumps(a) != json.dumps(b):
+                pytest.fail(f"record {i + 1} differs\n  device: {json.dumps(a)}\n"
+                            f"  oracle: {json.dumps(b)}")
+        pytest.fail(f"{len(log.records)} records, the oracle has {len(ref.events)}")
+    pool = BlockIdPool(blocks)
+    for r in log.records:
+        if r["kind"] in ("alloc", "free", "pin", "unpin"):
+            pool.apply(r["kind"], r["session_id"], r["blocks"], r.get("from_pinned", False))
+    assert kv["status"] == 0 and kv["top"].tolist() == pool.top(blocks)
