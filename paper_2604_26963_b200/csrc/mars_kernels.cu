@@ -2798,117 +2798,129 @@ __global__ void __launch_bounds__(WALK_TPB) k_walk(Tab t, Cfg c, Work* w, Bufs b
 
   // 2. fast path (warp 0): no claim can fail when the free pool covers every
   //    allocation of the greedy plan -> prefix sums reproduce build_plan.
-  if (threadIdx.x < 32) {
-    int lane = threadIdx.x;
-    long long budget = c.budget;
-    long long lim_dec = c.max_dec < budget ? c.max_dec : budget;
-    // decode eligibility counts
-    long long need_dec = 0;
-    int selected_mask[4] = {0, 0, 0, 0};
-    int cnt_before = 0;
-    #pragma unroll 1
-    for (int q = 0; q < 4; ++q) {
-      int i = q * 32 + lane;
-      bool e = i < nwin && S.wph[i] == MARS_DECODE && S.wrem[i] >= 1;
-      u32 m = __ballot_sync(FULL, e);
-      int pos = cnt_before + __popc(m & ((1u << lane) - 1u));
-      bool sel = e && pos < lim_dec;
-      selected_mask[q] = sel;
-      if (sel && block_aligned(c, S.wkv[i])) need_dec += 1;
-      cnt_before += __popc(m);
+  //    Four warps, one per 32 window entries (WIN_MAX = 128), exchange their
+  //    per-warp counts through shared memory at three named barriers (the
+  //    other warps do not take part): each stage is one pass, not four.
+  if (threadIdx.x < WIN_MAX) {
+    __shared__ int s_wc[4][6];         // per warp: eligible, selected, decode allocs,
+                                       // granted, prefill allocs, (pad)
+    __shared__ long long s_wl[4][3];   // per warp: need_dec, rp total, need_pre / grants
+    const int lane = threadIdx.x & 31, q = threadIdx.x >> 5, i = threadIdx.x;
+    const u32 lt = (1u << lane) - 1u;
+    const long long budget = c.budget;
+    const long long lim_dec = c.max_dec < budget ? c.max_dec : budget;
+    const bool in = i < nwin;
+    const u8 ph = in ? S.wph[i] : (u8)0;
+    const i32 kv = in ? S.wkv[i] : 0;
+    // stage 1: decode eligibility (window order) and the prefill requests
+    const bool e = in && ph == MARS_DECODE && S.wrem[i] >= 1;
+    const u32 me = __ballot_sync(FULL, e);
+    const bool p = in && ph == MARS_PREFILL;
+    const long long rp = p ? ((long long)S.wctx[i] - kv) : 0;
+    const long long rpp = rp > 0 ? rp : 0;
+    long long incl = rpp;  // inclusive warp scan of the prefill requests
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long x = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += x;
     }
-    long long ndec = cnt_before < lim_dec ? cnt_before : lim_dec;
-    need_dec = warp_sum<long long>(need_dec);
+    if (lane == 31) {
+      s_wc[q][0] = __popc(me);
+      s_wl[q][1] = incl;
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(WIN_MAX) : "memory");
+    int e_before = 0, e_total = 0;
+    long long run = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      e_before += k < q ? s_wc[k][0] : 0;
+      e_total += s_wc[k][0];
+      run += k < q ? s_wl[k][1] : 0;
+    }
+    const int epos = e_before + __popc(me & lt);
+    const bool sel = e && epos < lim_dec;
+    const bool dneed = sel && block_aligned(c, kv);
+    const long long ndec = e_total < lim_dec ? e_total : lim_dec;
+    // stage 2: prefill grants S_j = min(P_j, left0), g_j = min(rp_j, left0 - S_j)
+    const long long left0 = budget - ndec;
+    const long long P = run + incl - rpp;
+    const long long Sj = P < left0 ? P : left0;
+    const long long lft = left0 - Sj;
+    long long g = 0;
+    if (p && lft >= 1 && rp >= 1) g = rp < lft ? rp : lft;
+    const long long nd = g > 0 ? blocks_ceil(c, kv + g) - blocks_ceil(c, kv) : 0;
+    const u32 msel = __ballot_sync(FULL, sel), mdn = __ballot_sync(FULL, dneed);
+    const u32 mg = __ballot_sync(FULL, g > 0), mpn = __ballot_sync(FULL, nd > 0);
+    const long long nd_w = warp_sum<long long>(nd), g_w = warp_sum<long long>(g);
+    if (lane == 0) {
+      s_wc[q][1] = __popc(msel);
+      s_wc[q][2] = __popc(mdn);
+      s_wc[q][3] = __popc(mg);
+      s_wc[q][4] = __popc(mpn);
+      s_wl[q][0] = nd_w;
+      s_wl[q][2] = g_w;
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(WIN_MAX) : "memory");
+    int dbefore = 0, dn_before = 0, dn_total = 0, gbefore = 0, pn_before = 0;
+    long long need_pre = 0, gsum = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const bool b4 = k < q;
+      dbefore += b4 ? s_wc[k][1] : 0;
+      dn_before += b4 ? s_wc[k][2] : 0;
+      dn_total += s_wc[k][2];
+      gbefore += b4 ? s_wc[k][3] : 0;
+      pn_before += b4 ? s_wc[k][4] : 0;
+      need_pre += s_wl[k][0];
+      gsum += s_wl[k][2];
+    }
+    const long long need_dec = dn_total;
     PTIME(22);
-    long long left0 = budget - ndec;
-    // prefill grants: S_j = min(P_j, left0), g_j = min(rp_j, left0 - S_j)
-    long long run = 0;  // P_j prefix over earlier PREFILL entries
-    long long need_pre = 0;
-    long long grant[4] = {0, 0, 0, 0};
-    #pragma unroll 1
-    for (int q = 0; q < 4; ++q) {
-      int i = q * 32 + lane;
-      bool p = i < nwin && S.wph[i] == MARS_PREFILL;
-      long long rp = p ? ((long long)S.wctx[i] - S.wkv[i]) : 0;
-      long long rpp = rp > 0 ? rp : 0;
-      // inclusive warp scan of rpp
-      long long incl = rpp;
-      for (int o = 1; o < 32; o <<= 1) {
-        long long x = __shfl_up_sync(FULL, incl, o);
-        if (lane >= o) incl += x;
-      }
-      long long P = run + incl - rpp;
-      long long Sj = P < left0 ? P : left0;
-      long long lft = left0 - Sj;
-      long long g = 0;
-      if (p && lft >= 1 && rp >= 1) g = rp < lft ? rp : lft;
-      grant[q] = g;
-      if (g > 0) need_pre += blocks_ceil(c, S.wkv[i] + g) - blocks_ceil(c, S.wkv[i]);
-      run += __shfl_sync(FULL, incl, 31);
-    }
-    need_pre = warp_sum<long long>(need_pre);
-    PTIME(23);
-    bool ok = S.freeb >= need_dec + need_pre;
+    const bool ok = S.freeb >= need_dec + need_pre;
     if (ok) {
-      // emit in window order: decode allocations, then prefill allocations
-      int dcount = 0, pcount = 0, jcount = 0;
-      #pragma unroll 1
-      for (int q = 0; q < 4; ++q) {
-        int i = q * 32 + lane;
-        bool sel = selected_mask[q];
-        u32 m = __ballot_sync(FULL, sel);
-        int pos = dcount + __popc(m & ((1u << lane) - 1u));
-        if (sel) {
-          b.dec_rows[pos] = S.wrow[i];
-          S.wplanned[i] = 1;
-        }
-        dcount += __popc(m);
-        bool need = sel && block_aligned(c, S.wkv[i]);
-        u32 mj = __ballot_sync(FULL, need);
-        int jp = jcount + __popc(mj & ((1u << lane) - 1u));
-        if (need) {
-          b.j_op[jp] = MARS_J_ALLOC;
-          b.j_row[jp] = S.wrow[i];
-          b.j_n[jp] = 1;
-        }
-        jcount += __popc(mj);
+      // stage 3: emit in window order -- decodes, their allocations, then
+      // prefill grants and their allocations after every decode allocation
+      const u32 r = in ? S.wrow[i] : 0u;
+      if (sel) {
+        b.dec_rows[dbefore + __popc(msel & lt)] = r;
+        S.wplanned[i] = 1;
       }
-      long long tot = ndec;
-      #pragma unroll 1
-      for (int q = 0; q < 4; ++q) {
-        int i = q * 32 + lane;
-        long long g = grant[q];
-        bool gp = g > 0;
-        u32 m = __ballot_sync(FULL, gp);
-        int pos = pcount + __popc(m & ((1u << lane) - 1u));
-        long long nd = gp ? blocks_ceil(c, S.wkv[i] + g) - blocks_ceil(c, S.wkv[i]) : 0;
-        if (gp) {
-          b.pre_rows[pos] = S.wrow[i];
-          b.pre_grant[pos] = (i32)g;
-          S.wplanned[i] = 1;
-        }
-        pcount += __popc(m);
-        bool hn = nd > 0;
-        u32 mj = __ballot_sync(FULL, hn);
-        int jp = jcount + __popc(mj & ((1u << lane) - 1u));
-        if (hn) {
-          b.j_op[jp] = MARS_J_ALLOC;
-          b.j_row[jp] = S.wrow[i];
-          b.j_n[jp] = (i32)nd;
-        }
-        jcount += __popc(mj);
-        tot += warp_sum<long long>(g);
+      if (dneed) {
+        const int jp = dn_before + __popc(mdn & lt);
+        b.j_op[jp] = MARS_J_ALLOC;
+        b.j_row[jp] = r;
+        b.j_n[jp] = 1;
       }
-      if (lane == 0) {
+      if (g > 0) {
+        const int pos = gbefore + __popc(mg & lt);
+        b.pre_rows[pos] = r;
+        b.pre_grant[pos] = (i32)g;
+        S.wplanned[i] = 1;
+      }
+      if (nd > 0) {
+        const int jp = dn_total + pn_before + __popc(mpn & lt);
+        b.j_op[jp] = MARS_J_ALLOC;
+        b.j_row[jp] = r;
+        b.j_n[jp] = (i32)nd;
+      }
+      if (threadIdx.x == 0) {
+        int dc = 0, pc = 0, pn = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          dc += s_wc[k][1];
+          pc += s_wc[k][3];
+          pn += s_wc[k][4];
+        }
         S.fast_ok = 1;
-        S.ndec = dcount;
-        S.npre = pcount;
-        S.nj = jcount;
-        S.total = tot;
+        S.ndec = dc;
+        S.npre = pc;
+        S.nj = dn_total + pn;
+        S.total = ndec + gsum;
         S.freeb -= need_dec + need_pre;
         S.request = REQ_DONE;
       }
     }
+    PTIME(23);
   }
   __syncthreads();
   PTIME(20);
