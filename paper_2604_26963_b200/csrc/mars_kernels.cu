@@ -2462,8 +2462,19 @@ __device__ int cta_select_sorted(const u64* ghi, const u64* glo, const u32* gpay
       l = glo[i];
       p = gpay[i];
     }
-    const u64 mn = block_min<u64>(h, s_mm, ~0ull);
-    const u64 mx = block_max<u64>(i < n ? h : 0ull, s_mm, 0ull);
+    // the candidates' hi range: one barrier, every warp folds the 32 partials
+    __shared__ u64 s_mx[32];
+    {
+      const u64 wmn = warp_min(h), wmx = warp_max(i < n ? h : 0ull);
+      if ((i & 31) == 0) {
+        s_mm[i >> 5] = wmn;
+        s_mx[i >> 5] = wmx;
+      }
+    }
+    __syncthreads();
+    const int nwarp = (int)(blockDim.x >> 5);
+    const u64 mn = warp_min((i & 31) < nwarp ? s_mm[i & 31] : ~0ull);
+    const u64 mx = warp_max((i & 31) < nwarp ? s_mx[i & 31] : 0ull);
     PTIME(36);
     const double span = (double)(mx - mn);
     const double inv = span > 0.0 ? 255.0 / span : 0.0;
@@ -2522,7 +2533,7 @@ __device__ int cta_select_sorted(const u64* ghi, const u64* glo, const u32* gpay
         gph = wg->phase[r];
       }
       // parts threads per survivor, each counting a slice of the others
-      const int parts = ns <= 256 ? 4 : 2;
+      const int parts = ns <= 128 ? 8 : ns <= 170 ? 6 : ns <= 256 ? 4 : 2;
       const int q = i / parts, part = i % parts;
       if (i < 512) s_rank[i] = 0;
       __syncthreads();
