@@ -143,6 +143,8 @@ struct Work {
   i32 walk_slow;
   i32 n_queued_kv;  // queued rows holding KV (admission then touches reclaim state)
   u32 admit_done;   // set by k_control after admission; k_walk may wait on it
+  u32 adm_ctas;     // k_control CTAs past admission (the last one publishes)
+  u32 adm_pad[3];   // (Work stays a whole number of 16-byte words)
   i32 n_finish;
   i32 sort_path;    // pack_queue: 1 grid LSD sort, 2 one CTA, 3 early grid LSD (k_pack)
   i32 n_round_end, n_done;  // MARS_MODE_ADVANCE: rounds that ended, sessions that finished

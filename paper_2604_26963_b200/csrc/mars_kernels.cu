@@ -1640,7 +1640,6 @@ __device__ void admit_grid(Tab t, Cfg c, Work* w, Bufs b, Queue Q, const u32* pe
                            mars_scalars* sc, i32* qsel_p, Queue G, Xchg x) {
   PTIME(12);
   __shared__ long long shl[32];
-  cg::grid_group grid = cg::this_grid();
   const double now = w->in.now;
   const i64 qlen = w->qlen;
   const bool sharded = (w->in.mode & MARS_MODE_SHARDED) != 0;
@@ -1796,9 +1795,16 @@ __device__ void admit_grid(Tab t, Cfg c, Work* w, Bufs b, Queue Q, const u32* pe
   }
   PTIME(14);
   long long ps = block_sum<long long>(proj, shl);
-  if (threadIdx.x == 0 && ps) atomicAdd((unsigned long long*)&w->projected, (unsigned long long)ps);
-  grid.sync();
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  // the last CTA past admission publishes (no grid barrier: the others exit)
+  __shared__ bool s_last;
+  if (threadIdx.x == 0) {
+    if (ps) atomicAdd((unsigned long long*)&w->projected, (unsigned long long)ps);
+    __threadfence();
+    s_last = atomicAdd(&w->adm_ctas, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    __threadfence();
     volatile Work* vw = w;
     sc->w_adm = wadm;
     sc->last_update = last;
@@ -1932,8 +1938,9 @@ __global__ void __launch_bounds__(1024, 1) k_control(Tab t, Cfg c, Work* w, Bufs
       if (w->pk_done && w->pk_mode != mode) atomicOr(&w->status, ST_QUEUE_MISMATCH);
     }
     if (early) {
+      // no barrier: admission reads none of block 0's fields above (mode and
+      // the seed flag are computed by every CTA; the key bound is k_pack's)
       cur = w->pk_cur;
-      grid.sync();  // (orders the published mode for admission, as the sort's barriers do)
     } else {
       cur = lsd_grid_sort<false>(L, lsd_view(w, 0), a, npass, (u32(*)[256])smem);
       if (npass == 0) grid.sync();  // (no sort barrier to order the published mode)
