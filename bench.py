@@ -398,6 +398,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--flush-mb", type=int, default=512)
     ap.add_argument("--no-kv", action="store_true", help="skip the KV evict/restore sweep")
+    ap.add_argument("--clock-load", type=int, default=100,
+                    help="untimed 20-step batches run under the clock sampler first (0 under ncu)")
     ap.add_argument("--advance-ticks", type=int, default=40,
                     help="consecutive device-resident ticks (MARS_MODE_ADVANCE) to time; 0 = off")
     ap.add_argument("--hbm-sweep", default="100000,4000000,16000000,64000000",
@@ -500,7 +502,7 @@ def main():
         # period: keep the GPU on the same restore / flush / step load first
         # (a fixed count, identical on every rank: the sharded step runs
         # collectives) so the clock samples are taken under it (untimed)
-        for _ in range(100):
+        for _ in range(a.clock_load):
             for _ in range(20):
                 eng.restore()
                 eng.flush_l2(flush)
