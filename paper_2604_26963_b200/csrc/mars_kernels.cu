@@ -72,6 +72,11 @@ __global__ void k_ptime_dump() {
 #define PTIME(k)
 #endif
 
+// one of a struct's two buffers by a runtime index, as a select: indexing a
+// kernel parameter's array with a runtime value makes the compiler copy the
+// whole parameter struct into local memory at kernel entry (every thread)
+#define PICK2(arr, i) ((i) ? (arr)[1] : (arr)[0])
+
 // ---------------------------------------------------------------------------
 // block utilities
 // ---------------------------------------------------------------------------
@@ -1190,10 +1195,10 @@ __device__ int lsd_grid_sort(Lsd L, LsdView v, LsdArgs a, int npass, u32 (*wc)[2
     }
     // the queue's first pass reads req[] straight from the admission list
     const bool rawp = raw != nullptr && pass == 0;
-    const u64* kin = L.k[cur];
-    const u32* vin = L.v[cur];
-    u64* kout = L.k[1 - cur];
-    u32* vout = L.v[1 - cur];
+    const u64* kin = PICK2(L.k, cur);
+    const u32* vin = PICK2(L.v, cur);
+    u64* kout = PICK2(L.k, 1 - cur);
+    u32* vout = PICK2(L.v, 1 - cur);
     // a chunk of <= 1024 entries (the usual case) stays in registers from
     // the histogram to the scatter: one load per entry per pass
     const bool one = e - s <= 1024;
@@ -1431,7 +1436,7 @@ __global__ void k_exp_gather(Work* w, Bufs b, Lsd L) {
   int n = w->xlsd_n;
   int cur = w->xlsd_cur;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    u32 j = L.v[cur][i];
+    u32 j = PICK2(L.v, cur)[i];
     b.exp_row_sorted[i] = b.exp_row[j];
     b.exp_blk_sorted[i] = b.exp_blk[j];
   }
@@ -1485,8 +1490,8 @@ __device__ void pack_small_cta(Work* w, Queue Q, Lsd L, mars_scalars* sc, i32* q
   if (qlen <= 0) return;
   const bool sharded = (w->in.mode & MARS_MODE_SHARDED) != 0;
   int sel = *qsel_p;
-  const i32* req = sharded ? G.req[0] : Q.req[sel];
-  const u8* lng = sharded ? G.lng[0] : Q.lng[sel];
+  const i32* req = sharded ? G.req[0] : PICK2(Q.req, sel);
+  const u8* lng = sharded ? G.lng[0] : PICK2(Q.lng, sel);
   __shared__ u32 shu[1024 + 32];
   __shared__ u32 hist[256];
   __shared__ int shr[32];
@@ -1635,7 +1640,7 @@ __device__ void pack_small_cta(Work* w, Queue Q, Lsd L, mars_scalars* sc, i32* q
 // K_AP: update_window + clamp + admit prefix + residual queue
 // ---------------------------------------------------------------------------
 
-__device__ void admit_grid(Tab t, Cfg c, Work* w, Bufs b, Queue Q, const u32* perm,
+__device__ __forceinline__ void admit_grid(Tab t, Cfg c, Work* w, Bufs b, Queue Q, const u32* perm,
                            const u64* sorted_keys, u64 keyc, int mode, bool need_seed,
                            mars_scalars* sc, i32* qsel_p, Queue G, Xchg x) {
   PTIME(12);
@@ -1645,9 +1650,9 @@ __device__ void admit_grid(Tab t, Cfg c, Work* w, Bufs b, Queue Q, const u32* pe
   const bool sharded = (w->in.mode & MARS_MODE_SHARDED) != 0;
   const int sel = *qsel_p;
   // packed source: the local list, or (sharded) the all-gathered global list
-  const u32* src_row = sharded ? G.row[0] : Q.row[sel];
-  const i32* src_req = sharded ? G.req[0] : Q.req[sel];
-  const u8* src_lng = sharded ? G.lng[0] : Q.lng[sel];
+  const u32* src_row = sharded ? G.row[0] : PICK2(Q.row, sel);
+  const i32* src_req = sharded ? G.req[0] : PICK2(Q.req, sel);
+  const u8* src_lng = sharded ? G.lng[0] : PICK2(Q.lng, sel);
   // balance_and_admit scalars (control.py:181-190), computed redundantly per CTA
   bool has_seed = sc->has_blocks_seed;
   double seed = sc->blocks_seed;
@@ -1773,9 +1778,9 @@ __device__ void admit_grid(Tab t, Cfg c, Work* w, Bufs b, Queue Q, const u32* pe
     if (!sharded) {
       if (j < nres) {
         u32 pos = perm[take + j];
-        Q.row[1 - sel][j] = Q.row[sel][pos];
-        Q.req[1 - sel][j] = Q.req[sel][pos];
-        Q.lng[1 - sel][j] = Q.lng[sel][pos];
+        PICK2(Q.row, 1 - sel)[j] = PICK2(Q.row, sel)[pos];
+        PICK2(Q.req, 1 - sel)[j] = PICK2(Q.req, sel)[pos];
+        PICK2(Q.lng, 1 - sel)[j] = PICK2(Q.lng, sel)[pos];
       }
       continue;
     }
@@ -1787,10 +1792,10 @@ __device__ void admit_grid(Tab t, Cfg c, Work* w, Bufs b, Queue Q, const u32* pe
     }
     int s = warp_append(&w->n_res_own, mine);
     if (s >= 0) {
-      Q.row[1 - sel][s] = src_row[pos];
-      Q.req[1 - sel][s] = src_req[pos];
-      Q.lng[1 - sel][s] = src_lng[pos];
-      Q.gpos[1 - sel][s] = (u32)j;
+      PICK2(Q.row, 1 - sel)[s] = src_row[pos];
+      PICK2(Q.req, 1 - sel)[s] = src_req[pos];
+      PICK2(Q.lng, 1 - sel)[s] = src_lng[pos];
+      PICK2(Q.gpos, 1 - sel)[s] = (u32)j;
     }
   }
   PTIME(14);
@@ -1864,7 +1869,7 @@ __global__ void __launch_bounds__(1024, 1) k_pack(Cfg c, Work* w, Queue Q, Lsd L
   const int qlen = (int)w->pre_queue_len;
   if (!w->in.control_due || qlen <= SORT_CAP || npass < 1 || npass > 3) return;  // grid-uniform
   const int sel = *qsel_p;
-  const i32* req = Q.req[sel];
+  const i32* req = PICK2(Q.req, sel);
   const int mode = cpu_overloaded_after_refresh(c, w) ? PACK_DESC : PACK_ASC;
   const u64 keyc = (1ull << (8 * npass)) - 1ull;  // > every req (host bound q_maxreq)
   LsdArgs a;
@@ -1898,7 +1903,7 @@ __global__ void __launch_bounds__(1024, 1) k_control(Tab t, Cfg c, Work* w, Bufs
   cg::grid_group grid = cg::this_grid();
   const int qlen = (int)w->qlen;
   const bool sharded = (w->in.mode & MARS_MODE_SHARDED) != 0;
-  const i32* req = sharded ? G.req[0] : Q.req[*qsel_p];
+  const i32* req = sharded ? G.req[0] : PICK2(Q.req, *qsel_p);
   // pack_queue's mode (control.py:109-122) from the queue statistics the table
   // scan (or the global-list build) reduced: computed by every CTA, so a big
   // queue goes straight into the grid-wide sort without a barrier
@@ -1946,7 +1951,7 @@ __global__ void __launch_bounds__(1024, 1) k_control(Tab t, Cfg c, Work* w, Bufs
       if (npass == 0) grid.sync();  // (no sort barrier to order the published mode)
     }
     // sorted keys exist when at least one pass ran (pass 0 always does)
-    if (npass > 0) lsd_keys = L.k[cur];
+    if (npass > 0) lsd_keys = PICK2(L.k, cur);
     if (early) lsd_keyc = (u64)w->pk_max_req;
   } else {
     // small queue, first fit, or a row-less queue: one CTA packs
@@ -1961,7 +1966,7 @@ __global__ void __launch_bounds__(1024, 1) k_control(Tab t, Cfg c, Work* w, Bufs
   // the median seed is taken only from a non-empty queue (pack_small_cta)
   const bool need_seed = qlen > 0 && !sc->has_ema_blocks && !sc->has_blocks_seed;
   // the grid LSD sort leaves the sorted keys next to the permutation
-  admit_grid(t, c, w, b, Q, L.v[cur], lsd_keys, lsd_keyc, mode, need_seed, sc, qsel_p, G, x);
+  admit_grid(t, c, w, b, Q, PICK2(L.v, cur), lsd_keys, lsd_keyc, mode, need_seed, sc, qsel_p, G, x);
 }
 
 // ---------------------------------------------------------------------------
@@ -1978,9 +1983,9 @@ __global__ void k_export_queue(Queue Q, const i32* qsel_p, mars_scalars* sc, Xch
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) x.xsend[0] = (u64)n;
   for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    u64 key = ((u64)Q.gpos[sel][i] << 32) | ((u64)(u32)Q.req[sel][i] << 1) | (u64)(Q.lng[sel][i] & 1);
+    u64 key = ((u64)PICK2(Q.gpos, sel)[i] << 32) | ((u64)(u32)PICK2(Q.req, sel)[i] << 1) | (u64)(PICK2(Q.lng, sel)[i] & 1);
     x.xsend[1 + 2 * i] = key;
-    x.xsend[2 + 2 * i] = (u64)Q.row[sel][i];
+    x.xsend[2 + 2 * i] = (u64)PICK2(Q.row, sel)[i];
   }
 }
 
