@@ -516,11 +516,6 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
       const u8 ph = B[SB_PH + lr];
       if (f & MARS_F_ACTIVE) n_active++;
       if (f & MARS_F_QUEUED) {
-        // the admission reads these three for every admitted row: start them
-        // toward L2 (k_scan does not stream them)
-        prefetch_l2(&t.r0p[r]);
-        prefetch_l2(&t.ctx[r]);
-        prefetch_l2(&t.r0d[r]);
         n_queued++;
         if (f & MARS_F_LONG) n_long++;
         if (((const i32*)(B + SB_KV))[lr] > 0) n_qkv++;
