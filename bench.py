@@ -550,17 +550,20 @@ def main():
     e2e_t = []
     d2h = 0
     e2e_warm = 3  # first copies out of freshly pinned pages are slower on some hosts
+    e2e_up = []
     for i in range(a.e2e_steps + e2e_warm):
         eng.restore()
         eng.flush_l2(flush)
         barrier()
         t0 = time.perf_counter()
         eng.upsert(pinned)
+        tu = time.perf_counter()
         enqueue_step()
         r = eng.fetch()
         t1 = time.perf_counter()
         if i >= e2e_warm:
             e2e_t.append(t1 - t0)
+            e2e_up.append(tu - t0)
         d2h = (r.expired_rows.nbytes * 2 + r.admitted_rows.nbytes + r.window_rows.nbytes
                + r.decode_rows.nbytes + r.prefill_rows.nbytes * 2 + r.evict_rows.nbytes * 3
                + r.journal_row.nbytes * 3 + r.ret_rows.nbytes * 7 + 4096)
@@ -599,7 +602,8 @@ def main():
                      "step_frac": step_bytes(snap) / (ms_per_step * 1e-3) / 1e9 / peak},
         "e2e": {"value": total_sessions / e2e_s, "unit": "sessions/s",
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "ms_per_step": e2e_s * 1e3},
+                "ms_per_step": e2e_s * 1e3,
+                "upload_ms": statistics.median(e2e_up) * 1e3},
         "gpu_launches": launches,
         "advance": adv,
         "kernel_ms_median": kernel_ms,

@@ -24,10 +24,12 @@ flat = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
 dflat = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
 
 
-def t(fn, n=10):
+def t(fn, n=10, flush=False):
     out = []
     for i in range(n + 1):
         eng.restore()
+        if flush:
+            eng.flush_l2(512 << 20)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         fn()
@@ -58,6 +60,9 @@ print(f"upsert            {t(lambda: eng.upsert(pinned)):.3f} ms")
 print(f"step+fetch        {t(step):.3f} ms")
 print(f"enqueue only      {t(lambda: eng.enqueue(si)):.3f} ms")
 print(f"upsert+step+fetch {t(full):.3f} ms")
+print(f"  same, L2 flushed before each {t(full, flush=True):.3f} ms")
+print(f"upsert, L2 flushed before each {t(lambda: eng.upsert(pinned), flush=True):.3f} ms")
+print(f"one pinned copy, L2 flushed    {t(raw, flush=True):.3f} ms")
 
 import ctypes as C
 
