@@ -36,7 +36,7 @@ extern "C" {
 #define MARS_ERR_CAPACITY 3
 #define MARS_ERR_ARG 4
 
-#define MARS_ABI_VERSION 4
+#define MARS_ABI_VERSION 5
 
 /* phase codes: agentsched/engine.py:250-256 */
 #define MARS_WAITING_ADMISSION 0
@@ -217,6 +217,11 @@ typedef struct mars_step_out {
   const uint8_t* end_pin;
   const double *end_benefit, *end_cost, *end_deadline;
   const uint8_t* prefill_done;
+  /* diagnostics (ABI v5): exact full-table reclaimer passes the walk took (0
+   * whenever the victim stream covered the step's claims), which candidate
+   * lists k_scan's grid radix refinement cut (bit 0 window, bit 1 victims),
+   * its rounds, and the refined lists' lengths */
+  int32_t n_fullscan, ref_flags, ref_rounds, n_window_ref, n_victim_ref;
 } mars_step_out;
 
 /* ---- lifecycle ------------------------------------------------------- */

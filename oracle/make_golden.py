@@ -175,14 +175,18 @@ PHASES = ("waiting_admission", "prefill", "decode", "tool", "waiting_resume", "d
 F_ACTIVE, F_QUEUED, F_PINNED, F_BOUNDARY, F_LONG = 1, 2, 4, 8, 16
 
 
-def ref_snapshot_step(A, snap, enable_coordinator=True, enable_coscheduler=True):
+def ref_snapshot_step(A, snap, enable_coordinator=True, enable_coscheduler=True, policy="mars",
+                      control_due=True):
+    """One scheduling step through the reference's own objects (any of its
+    policies, baselines.py:108-455), canonical output as oracle/snapshot_step.py."""
     import numpy as np
     from agentsched.scheduler import PinnedSession, PriorityState, RetentionConfig, decide_retention
     from agentsched.telemetry import refresh_pressure
 
     c = snap.cols
     n = snap.n
-    pol = A.make_policy("mars", enable_coordinator=enable_coordinator,
+    mars = policy == "mars"
+    pol = A.make_policy(policy, enable_coordinator=enable_coordinator,
                         enable_coscheduler=enable_coscheduler)
     pool = A.KvPool(total_blocks=snap.total_blocks)
     gpu = A.GpuModel()
@@ -212,10 +216,13 @@ def ref_snapshot_step(A, snap, enable_coordinator=True, enable_coscheduler=True)
         if f & F_ACTIVE:
             active[sid] = call
             lv = int(c["level"][i])
-            pol.states[sid] = PriorityState(level=lv, base_level=lv,
-                                            served_tokens_at_level=int(c["served"][i]),
-                                            wait_since=float(c["wait_since"][i]),
-                                            promotions=int(c["promos"][i]))
+            if mars:
+                pol.states[sid] = PriorityState(level=lv, base_level=lv,
+                                                served_tokens_at_level=int(c["served"][i]),
+                                                wait_since=float(c["wait_since"][i]),
+                                                promotions=int(c["promos"][i]))
+            else:  # Call.served_tokens (program_priority's key, baselines.py:170-171)
+                call.served_tokens = int(c["served"][i])
         if f & F_PINNED:
             call.pinned = True
             call.retention_deadline = float(c["deadline"][i])
@@ -223,7 +230,7 @@ def ref_snapshot_step(A, snap, enable_coordinator=True, enable_coscheduler=True)
             pool.pinned[sid] = pb
             used += pb
             pol.pinned[sid] = PinnedSession(sid, pb, 0.0, 0.0, float(c["deadline"][i]),
-                                            int(c["plevel"][i]))
+                                            int(c["plevel"][i]) if mars else 0)
         elif call.kv_tokens > 0:
             h = A.blocks_for_tokens(call.kv_tokens, 16)
             pool.allocated[sid] = h
@@ -270,44 +277,51 @@ def ref_snapshot_step(A, snap, enable_coordinator=True, enable_coscheduler=True)
     tel.probe(pool, Plane(), active_sessions=len(active))
     probe = dict(available_kv=tel.available_kv, usage=tel.kv_usage_ratio,
                  active_sessions=tel.active_sessions)
-    refresh_pressure(tel, pressure, snap.worker_slots)
-    clock = A.SimClock()
-    clock.now = now
-    log = A.EventLog()
-    admitted = A.balance_and_admit(queue, ctl, tel, snap.worker_slots, pressure, clock, log)
-    wu = log.records[-1]
-    for e in admitted:
-        call = e.call
-        call.admit_time = now
-        A.submit_round(call, now)
-        tel.record("gpu_submit", {"projected_blocks": call.incremental_blocks(
-            call.remaining_prefill, pool.block_size)})
-        active[call.session_id] = call
-        pol.on_admit(call, now)
-    control = dict(w_adm=ctl.w_adm, last_update=ctl.last_update, limit=wu["limit"],
-                   slots=wu["slots"], admitted=[row[e.call.session_id] for e in admitted],
-                   queue=[row[e.call.session_id] for e in queue],
-                   cpu_overloaded=tel.cpu_overloaded, kv_overloaded=tel.kv_overloaded,
-                   streaks=[tel.cpu_high_streak, tel.cpu_low_streak, tel.kv_high_streak,
-                            tel.kv_low_streak],
-                   blocks_seed=tel.blocks_seed, available_kv=tel.available_kv)
+    control = None
+    if control_due:
+        refresh_pressure(tel, pressure, snap.worker_slots)
+        clock = A.SimClock()
+        clock.now = now
+        log = A.EventLog()
+        admitted = A.balance_and_admit(queue, ctl, tel, snap.worker_slots, pressure, clock, log)
+        wu = log.records[-1]
+        for e in admitted:
+            call = e.call
+            call.admit_time = now
+            A.submit_round(call, now)
+            tel.record("gpu_submit", {"projected_blocks": call.incremental_blocks(
+                call.remaining_prefill, pool.block_size)})
+            active[call.session_id] = call
+            pol.on_admit(call, now)
+        control = dict(w_adm=ctl.w_adm, last_update=ctl.last_update, limit=wu["limit"],
+                       slots=wu["slots"], admitted=[row[e.call.session_id] for e in admitted],
+                       queue=[row[e.call.session_id] for e in queue],
+                       cpu_overloaded=tel.cpu_overloaded, kv_overloaded=tel.kv_overloaded,
+                       streaks=[tel.cpu_high_streak, tel.cpu_low_streak, tel.kv_high_streak,
+                                tel.kv_low_streak],
+                       blocks_seed=tel.blocks_seed, available_kv=tel.available_kv)
     ret = []
     for r in boundary:
-        d = decide_retention(sess[r], tel, pool, gpu, RetentionConfig(), pressure, now)
+        if mars:
+            d = decide_retention(sess[r], tel, pool, gpu, RetentionConfig(), pressure, now)
+        else:  # the policy's own rule; None = never pin (baselines.py:82-86)
+            d = pol.retention_decision(sess[r], pool, tel, gpu, now)
+            if d is None:
+                continue
         ret.append([r, d.pin, d.benefit_s, d.cost_s, d.retention_deadline])
     ready = sorted((x for x in active.values() if x.phase in (A.Phase.PREFILL, A.Phase.DECODE)),
                    key=lambda x: x.session_id)
     window_holder = []
-    orig_key = pol._order_key
 
-    # capture the window exactly as build_plan forms it (scheduler.py:310)
+    # capture the window exactly as build_plan forms it (scheduler.py:310, the
+    # scheduler module's only sorted() call)
     def plan_tick_capture():
         import agentsched.scheduler as S
         real_sorted = sorted
 
         def spy(seq, key=None):
             out = real_sorted(seq, key=key)
-            if key is orig_key or getattr(key, "__func__", None) is getattr(orig_key, "__func__", 0):
+            if not window_holder:
                 window_holder.append(out[:128])
             return out
         S.sorted = spy
@@ -335,7 +349,7 @@ def ref_snapshot_step(A, snap, enable_coordinator=True, enable_coscheduler=True)
         if call.session_id in pool.pinned:
             f |= F_PINNED
         cols["flags"].append(f)
-        p = pol.states.get(call.session_id)
+        p = pol.states.get(call.session_id) if mars else None
         if p is not None:
             cols["level"].append(p.level)
             cols["promos"].append(p.promotions)
@@ -390,6 +404,51 @@ def freeze_snapshots(A, out):
         print(f"  snapshot {case}: window {len(o['window'])} evictions {len(o['evictions'])} "
               f"admitted {len(o['control']['admitted'])}")
     out["snapshot_steps.json"] = res
+
+
+# heavy-reclaim and tick-gridded snapshots (tests/_variants.py): steps that
+# take dozens of victims per claim sequence, all five policies, exact time ties
+HEAVY_CASES = [
+    dict(n=30_000, seed=81, kind="reclaim_heavy", policy=p, grid=g)
+    for p in ("mars", "fcfs", "program_priority", "static_ttl", "dynamic_ttl")
+    for g in (False, True)
+] + [
+    dict(n=30_000, seed=82, kind="tick_grid", policy="mars", grid=True),
+    dict(n=30_000, seed=83, kind="reclaim_heavy", policy="mars", grid=True,
+         enable_coordinator=False),
+]
+
+
+def heavy_snapshot(case):
+    sys.path.insert(0, REPO)
+    from paper_2604_26963_b200.snapshot import snapshot_v1
+    from tests._variants import reclaim_heavy, tick_grid
+
+    if case["kind"] == "reclaim_heavy":
+        snap = reclaim_heavy(case["n"], case["seed"], case["policy"])
+    else:
+        snap = snapshot_v1(case["n"], seed=case["seed"], pool="pressure")
+    if case.get("grid"):
+        snap = tick_grid(snap, case["seed"])
+    return snap
+
+
+def heavy_kw(case):
+    kw = {k: case[k] for k in ("enable_coordinator", "enable_coscheduler") if k in case}
+    kw["policy"] = case["policy"]
+    kw["control_due"] = case["policy"] == "mars"
+    return kw
+
+
+def freeze_heavy(A, out):
+    res = []
+    for case in HEAVY_CASES:
+        snap = heavy_snapshot(case)
+        o = ref_snapshot_step(A, snap, **heavy_kw(case))
+        res.append(dict(case=case, out=json.loads(json.dumps(o))))
+        print(f"  heavy {case}: evictions {len(o['evictions'])} "
+              f"(pinned {sum(1 for e in o['evictions'] if e[1] == 'pinned')})")
+    out["heavy_steps.json"] = res
 
 
 # ---------------------------------------------------------------------------
@@ -566,6 +625,8 @@ def main(argv=None):
         freeze_snapshots(A, out)
     if not only or "kat" in only:
         freeze_kat(A, out)
+    if not only or "heavy" in only:
+        freeze_heavy(A, out)
     os.makedirs(GOLDEN, exist_ok=True)
     for name, obj in out.items():
         with open(os.path.join(GOLDEN, name), "w") as fh:

@@ -115,6 +115,8 @@ class MarsStepOut(C.Structure):
         ("end_rows", P(u32)), ("end_kind", P(u8)),
         ("end_blocks", P(i32)), ("end_pin", P(u8)), ("end_benefit", P(f64)),
         ("end_cost", P(f64)), ("end_deadline", P(f64)), ("prefill_done", P(u8)),
+        ("n_fullscan", i32), ("ref_flags", i32), ("ref_rounds", i32),
+        ("n_window_ref", i32), ("n_victim_ref", i32),
     ]
 
 

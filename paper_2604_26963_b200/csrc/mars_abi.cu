@@ -162,6 +162,17 @@ static Cfg make_cfg(const mars_config& h) {
     c.cosched = 0;
   }
   c.strict = (c.policy == POL_FCFS || c.policy == POL_STATIC_TTL || c.policy == POL_DYNAMIC_TTL);
+  // candidate-list refinement triggers and the victim stream length; tests
+  // shrink them (MARS_REF_TRIG_W / _V, MARS_VSTREAM) to drive the refinement
+  // and the exact full-table fallback on small tables
+  auto env_int = [](const char* k, int dflt) {
+    const char* v = getenv(k);
+    return (v && v[0]) ? atoi(v) : dflt;
+  };
+  c.ref_trig_w = env_int("MARS_REF_TRIG_W", REF_TRIG_W);
+  c.ref_trig_v = env_int("MARS_REF_TRIG_V", REF_TRIG_V);
+  c.stream_cap = env_int("MARS_VSTREAM", VSTREAM_CAP);
+  if (c.stream_cap < 1 || c.stream_cap > VSTREAM_CAP) c.stream_cap = VSTREAM_CAP;
   return c;
 }
 
@@ -330,10 +341,21 @@ int mars_create(const mars_config* hcfg, int device, int64_t max_rows, int64_t m
   ALLOC(b.wc_lo, R * 8);
   ALLOC(b.wc_row, R * 4);
   ALLOC(b.vc_key, R * 8);
+  ALLOC(b.vc_kl, R * 8);
   ALLOC(b.vc_whi, R * 8);
   ALLOC(b.vc_wlo, R * 8);
   ALLOC(b.vc_row, R * 4);
   ALLOC(b.vc_blk, R * 4);
+  // refined lists (k_scan phase 3): the window list can grow by admitted rows
+  ALLOC(b.wr_hi, R * 8);
+  ALLOC(b.wr_lo, R * 8);
+  ALLOC(b.wr_row, R * 4);
+  ALLOC(b.vr_key, (size_t)VR_CAP * 8);
+  ALLOC(b.vr_kl, (size_t)VR_CAP * 8);
+  ALLOC(b.vr_whi, (size_t)VR_CAP * 8);
+  ALLOC(b.vr_wlo, (size_t)VR_CAP * 8);
+  ALLOC(b.vr_row, (size_t)VR_CAP * 4);
+  ALLOC(b.vr_blk, (size_t)VR_CAP * 4);
   ALLOC(b.ret_row, R * 4);
   ALLOC(b.ret_pin, R);
   ALLOC(b.ret_b, R * 8);
@@ -441,7 +463,8 @@ int mars_destroy(mars_ctx* ctx) {
                 b.pre_rows, b.pre_grant, b.ev_row, b.ev_kind, b.ev_blk, b.j_op, b.j_row, b.j_n,
                 b.dec_level, b.pre_level, b.fin_row, b.fin_pin, b.fin_b, b.fin_c, b.fin_d,
                 b.flush, b.end_row, b.end_kind, b.end_blk, b.end_pin, b.end_b, b.end_c,
-                b.end_d, b.pre_done};
+                b.end_d, b.pre_done, b.vc_kl, b.wr_hi, b.wr_lo, b.wr_row, b.vr_key, b.vr_kl,
+                b.vr_whi, b.vr_wlo, b.vr_row, b.vr_blk};
   for (void* p : bs) cudaFree(p);
   cudaFree(ctx->d_stage);
   cudaFree(ctx->d_resume);
@@ -830,6 +853,11 @@ int mars_step_fetch(mars_ctx* ctx, mars_step_out* o) {
   o->n_victim_cand = w.n_vc;
   o->walk_slow = w.walk_slow;
   o->sort_path = w.sort_path;
+  o->n_fullscan = w.n_fullscan;
+  o->ref_flags = (w.ref_on[0] ? 1 : 0) | (w.ref_on[1] ? 2 : 0);
+  o->ref_rounds = w.ref_iters;
+  o->n_window_ref = w.n_wr;
+  o->n_victim_ref = w.n_vr;
   o->n_round_end = w.n_round_end;
   o->n_done = w.n_done;
   o->end_rows = (const uint32_t*)pull(ctx, off, b.end_row, (size_t)w.n_round_end * 4);

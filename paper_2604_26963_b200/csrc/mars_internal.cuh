@@ -17,8 +17,14 @@ typedef int64_t i64;
 #define HIST_BINS 4096
 #define WIN_MAX 128
 #define SORT_CAP 4096         // bitonic sort capacity of the single-CTA selector
-#define VSEL 256              // victim-stream target length (prefix of reclaim order)
-#define VSTREAM_CAP 2048      // victim stream entries kept in shared memory
+#define VSEL 512              // victim-stream target length (prefix of reclaim order): covers
+                              // every victim one step can take (<= max_dec + budget/bs + window)
+                              // plus the window rows a claim may skip
+#define VSTREAM_CAP 1024      // victim stream entries kept in shared memory
+#define REF_STOP 256          // grid radix refinement stops at a group this small
+#define REF_TRIG_W 1024       // window candidates beyond this are refined in k_scan
+#define REF_TRIG_V VSTREAM_CAP
+#define VR_CAP 4096           // refined victim list capacity (<= VSEL + REF_STOP used)
 #define LSD_G 592             // max CTAs of the cooperative LSD radix sort (>= #SMs)
 #define SCAN_RPT 4            // consecutive rows per thread in the table scans
 #define MAX_SCAN_CTAS 1024    // upper bound of k_scan's grid
@@ -54,6 +60,7 @@ struct Cfg {
   double tick_s, prefill_rate, promo_wait, slack, horizon, pw_clip;
   double cpu_hi, cpu_lo, kv_hi, kv_lo, ema_alpha, tool_prior;
   double ai, md, ctl_interval, init_window, oversub, reserve, long_frac;
+  i32 ref_trig_w, ref_trig_v, stream_cap;  // refinement triggers, victim stream length
 };
 
 // device column pointers (the session-state store, SoA in HBM)
@@ -145,6 +152,17 @@ struct Work {
   u32 admit_done;   // set by k_control after admission; k_walk may wait on it
   u32 adm_ctas;     // k_control CTAs past admission (the last one publishes)
   u32 adm_pad[3];   // (Work stays a whole number of 16-byte words)
+  // grid radix refinement of the candidate lists (k_scan phase 3): per list
+  // (0 window, 1 victims) the AND / OR of every emitted key (their common
+  // prefix), three rotating 256-bin histograms, and the final bound: the
+  // refined list holds the keys with (key >> ref_s) <= (ref_p >> ref_s)
+  unsigned long long ref_and[2][2], ref_or[2][2];
+  u32 ref_hist[2][3][256];
+  unsigned long long ref_p[2][2];
+  i32 ref_on[2], ref_s[2];
+  i32 n_wr, n_vr;     // refined list lengths
+  i32 n_fullscan;     // exact full-table reclaimer passes taken by the walk
+  i32 ref_iters;
   i32 n_finish;
   i32 sort_path;    // pack_queue: 1 grid LSD sort, 2 one CTA, 3 early grid LSD (k_pack)
   i32 n_round_end, n_done;  // MARS_MODE_ADVANCE: rounds that ended, sessions that finished
@@ -167,8 +185,12 @@ struct Bufs {
   u32 *exp_row_sorted; i32 *exp_blk_sorted;
   // window candidates
   u64 *wc_hi, *wc_lo; u32 *wc_row;
-  // victim candidates
-  u64 *vc_key, *vc_whi, *vc_wlo; u32 *vc_row; i32 *vc_blk;
+  // victim candidates: the policy's 128-bit reclaim key (vc_key, vc_kl), the
+  // window key of running rows (eligibility), row, blocks
+  u64 *vc_key, *vc_kl, *vc_whi, *vc_wlo; u32 *vc_row; i32 *vc_blk;
+  // the same two lists after the grid radix refinement (k_scan phase 3)
+  u64 *wr_hi, *wr_lo; u32 *wr_row;
+  u64 *vr_key, *vr_kl, *vr_whi, *vr_wlo; u32 *vr_row; i32 *vr_blk;
   // retention results
   u32 *ret_row; u8 *ret_pin; double *ret_b, *ret_c, *ret_d;
   // admission
@@ -278,6 +300,71 @@ __device__ __forceinline__ u64 victim_key(bool running, bool nonexp, u32 level, 
 __device__ __forceinline__ u32 victim_digit(bool running, bool nonexp, u32 level, i64 blocks) {
   return ((running ? 1u : 0u) << 11) | ((nonexp ? 1u : 0u) << 10) | ((3u - level) << 8) |
          (255u - blocks_bucket(blocks));
+}
+
+// monotone non-decreasing 11-bit bucket of a non-negative count: exact below
+// 64, then 64 sub-buckets per octave (values are clamped to 2^32 - 1)
+__device__ __forceinline__ u32 log_bucket11(i64 v) {
+  if (v <= 0) return 0;
+  const u64 x = v >= 0xffffffffll ? 0xffffffffull : (u64)v;
+  if (x < 64) return (u32)x;
+  const int e = 63 - __clzll((long long)x);
+  return 64u * (u32)(e - 5) + (u32)((x >> (e - 6)) & 63u);
+}
+
+// The policy's reclaim order as one unique 128-bit key (kh, kl), pinned
+// victims first (bit 127 clear):
+//  mars     pinned (expired first, -level, -blocks, sid), then running
+//           (-level, -blocks, sid)             scheduler.py:249-259
+//  fcfs/ttl running: latest arrival first      baselines.py:120-130, 288-298
+//  program_priority running: most service first baselines.py:176-186
+//  ttl      pinned (expired first, deadline, -blocks, sid)  baselines.py:268-287
+// `lv` is the row's MLFQ level (0 with the coordinator off).
+__device__ __forceinline__ void run_reclaim_key(int policy, u32 lv, i64 held, double arr,
+                                                i64 served, u32 rank, u64& kh, u64& kl) {
+  if (policy == POL_MARS) {
+    kh = victim_key(true, false, lv, held, rank);
+    kl = 0;
+  } else if (policy == POL_PP) {
+    const u64 su = served <= 0 ? 0ull : (u64)served;
+    kh = (1ull << 63) | (0x3fffffffffffffffull - (su & 0x3fffffffffffffffull));
+    kl = rank;
+  } else {
+    const u64 o = ~ord_f64(arr);
+    kh = (1ull << 63) | (o >> 1);
+    kl = ((o & 1ull) << 63) | (u64)rank;
+  }
+}
+
+__device__ __forceinline__ void pin_reclaim_key(int policy, bool nonexp, u32 plevel, i64 pb,
+                                                double dl, u32 rank, u64& kh, u64& kl) {
+  if (policy == POL_MARS) {
+    kh = victim_key(false, nonexp, plevel, pb, rank);
+    kl = 0;
+  } else {
+    const u64 o = ord_f64(dl);
+    const u64 bb = pb > (i64)MAXH ? MAXH : (u64)(pb < 0 ? 0 : pb);
+    kh = ((u64)(nonexp ? 1 : 0) << 62) | (o >> 2);
+    kl = ((o & 3ull) << 62) | ((MAXH - bb) << 32) | (u64)rank;
+  }
+}
+
+// 12-bit digits monotone in those keys (the k_scan histograms)
+__device__ __forceinline__ u32 pin_reclaim_digit(int policy, bool nonexp, u32 plevel, i64 pb,
+                                                 double dl, double now) {
+  if (policy == POL_MARS) return victim_digit(false, nonexp, plevel, pb);
+  const double y = (dl - now + 64.0) * 8.0;  // deadline, 1/8 s over now +- 64 s
+  const u32 b = (y >= 1023.0) ? 1023u : (y > 0.0 ? (u32)y : 0u);
+  return ((nonexp ? 1u : 0u) << 10) | b;
+}
+
+__device__ __forceinline__ u32 run_reclaim_digit(int policy, u32 lv, i64 held, double arr,
+                                                 i64 served, double ascale) {
+  if (policy == POL_MARS) return victim_digit(true, false, lv, held);
+  if (policy == POL_PP) return (1u << 11) | (2047u - log_bucket11(served));
+  const double y = arr * ascale;  // arrival over [0, now], 2048 buckets
+  const u32 b = (y >= 2047.0) ? 2047u : (y > 0.0 ? (u32)y : 0u);
+  return (1u << 11) | (2047u - b);
 }
 
 // 64-bit division kept out of line: the single-CTA kernels pay for every

@@ -391,6 +391,173 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, u32 bytes, 
       : "memory");
 }
 
+// ---- grid radix refinement of the candidate lists ------------------------
+typedef unsigned __int128 u128;
+__device__ __forceinline__ u128 mk128(u64 h, u64 l) { return ((u128)h << 64) | (u128)l; }
+__device__ __forceinline__ int clz128(u128 x) {
+  const u64 h = (u64)(x >> 64);
+  return h ? __clzll((long long)h) : 64 + __clzll((long long)(u64)x);
+}
+
+// Exact radix select over the emitted 128-bit keys of the window list (0)
+// and the victim list (1), by the whole cooperative grid: starting below the
+// keys' common prefix (the AND / OR folded during emission), each round
+// histograms the next 8 bits of the keys still sharing the prefix (CTA slices
+// of the list, shared-memory counts, one global add per bin), one grid
+// barrier, and every CTA derives the bin holding the k-th key from the same
+// counts.  It stops once that bin holds <= REF_STOP keys; the refined list is
+// every key whose bits above the bin's position are <= the prefix's: the
+// exact top k plus fewer than REF_STOP keys, compacted into wr_* / vr_*.
+// Called by every thread of every CTA after a grid barrier (the lists are
+// complete).  Keys are unique (session rank), so at most 16 rounds.
+__device__ void grid_refine(cg::grid_group& grid, Work* w, Bufs& b, bool on_w, bool on_v, int kw,
+                            int kv) {
+  __shared__ u32 sh[2][256];
+  __shared__ u32 s_ws[2][8];
+  const int G = gridDim.x, g = blockIdx.x, tid = threadIdx.x, bd = blockDim.x;
+  const int lane = tid & 31, wid = tid >> 5;
+  const int n[2] = {__ldcg(&w->n_wc), __ldcg(&w->n_vc)};
+  const u64* khp[2] = {b.wc_hi, b.vc_key};
+  const u64* klp[2] = {b.wc_lo, b.vc_kl};
+  const bool on[2] = {on_w, on_v};
+  bool act[2];
+  u128 P[2];
+  int top[2], fin_s[2];
+  u32 need[2] = {(u32)kw, (u32)kv};
+#pragma unroll
+  for (int l = 0; l < 2; ++l) {
+    act[l] = false;
+    P[l] = 0;
+    top[l] = -1;
+    fin_s[l] = 0;
+    if (!on[l]) continue;
+    const u128 A = mk128(__ldcg(&w->ref_and[l][0]), __ldcg(&w->ref_and[l][1]));
+    const u128 O = mk128(__ldcg(&w->ref_or[l][0]), __ldcg(&w->ref_or[l][1]));
+    const u128 x = A ^ O;
+    if (x == 0) {  // one distinct key: nothing to refine
+      P[l] = A;
+      continue;
+    }
+    top[l] = 127 - clz128(x);
+    P[l] = (top[l] >= 127) ? (u128)0 : ((A >> (top[l] + 1)) << (top[l] + 1));
+    act[l] = true;
+  }
+  int it = 0;
+  while (act[0] || act[1]) {  // grid-uniform: every CTA holds the same state
+    const int buf = it % 3;
+    for (int i = tid; i < 512; i += bd) (&sh[0][0])[i] = 0u;
+    __syncthreads();
+#pragma unroll
+    for (int l = 0; l < 2; ++l) {
+      if (!act[l]) continue;
+      const int lo_b = top[l] >= 7 ? top[l] - 7 : 0;
+      const u32 msk = (1u << (top[l] - lo_b + 1)) - 1u;
+      const int sft = top[l] + 1;
+      const u128 pp = sft >= 128 ? (u128)0 : (P[l] >> sft);
+      const i64 i0 = (i64)n[l] * g / G, i1 = (i64)n[l] * (g + 1) / G;
+      for (i64 i = i0 + tid; i < i1; i += bd) {
+        const u128 key = mk128(__ldcg(khp[l] + i), __ldcg(klp[l] + i));
+        if (sft < 128 && (key >> sft) != pp) continue;
+        atomicAdd(&sh[l][(u32)(key >> lo_b) & msk], 1u);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int l = 0; l < 2; ++l)
+      if (act[l])
+        for (int d = tid; d < 256; d += bd)
+          if (sh[l][d]) atomicAdd(&w->ref_hist[l][buf][d], sh[l][d]);
+    grid.sync();
+#pragma unroll
+    for (int l = 0; l < 2; ++l) {
+      if (!act[l]) continue;
+      // the bin holding the need-th key: a 256-entry scan on 8 warps
+      const u32 v = tid < 256 ? __ldcg(&w->ref_hist[l][buf][tid]) : 0u;
+      u32 incl = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const u32 x = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += x;
+      }
+      __shared__ int s_bin[2];
+      __shared__ u32 s_below[2], s_cntb[2];
+      if (tid < 256 && lane == 31) s_ws[l][wid] = incl;
+      if (tid == 0) {  // (need beyond the total cannot happen: the list holds > k keys)
+        s_bin[l] = 255;
+        s_below[l] = 0;
+        s_cntb[l] = 0;
+      }
+      __syncthreads();
+      u32 wb = 0;
+      if (tid < 256)
+        for (int q = 0; q < wid; ++q) wb += s_ws[l][q];
+      incl += wb;
+      if (tid < 256 && incl - v < need[l] && incl >= need[l]) {
+        s_bin[l] = tid;
+        s_below[l] = incl - v;
+        s_cntb[l] = v;
+      }
+      __syncthreads();
+      const int lo_b = top[l] >= 7 ? top[l] - 7 : 0;
+      need[l] -= s_below[l];
+      P[l] |= (u128)(u32)s_bin[l] << lo_b;
+      const u32 cnt = s_cntb[l];
+      top[l] = lo_b - 1;
+      if (cnt <= (u32)REF_STOP || top[l] < 0) {
+        act[l] = false;
+        fin_s[l] = lo_b;
+      }
+      __syncthreads();
+    }
+    // the buffer two rounds ahead was last read before this round's barrier
+    if (g == 0)
+      for (int i = tid; i < 512; i += bd) (&w->ref_hist[0][0][0])[((i >> 8) * 3 + (it + 2) % 3) * 256 + (i & 255)] = 0u;
+    ++it;
+  }
+  // compaction: the keys at or below the bound, in any order (the walk sorts)
+#pragma unroll
+  for (int l = 0; l < 2; ++l) {
+    if (!on[l]) continue;
+    const int sft = fin_s[l];
+    const u128 pp = P[l] >> sft;
+    const i64 i0 = (i64)n[l] * g / G, i1 = (i64)n[l] * (g + 1) / G;
+    for (i64 base = i0; base < i1; base += bd) {
+      const i64 i = base + tid;
+      bool pred = false;
+      if (i < i1) pred = (mk128(__ldcg(khp[l] + i), __ldcg(klp[l] + i)) >> sft) <= pp;
+      int slot = warp_append(l ? &w->n_vr : &w->n_wr, pred);
+      if (l == 1 && slot >= VR_CAP) {
+        w->status |= ST_WALK_OVERFLOW;
+        slot = -1;
+      }
+      if (slot >= 0) {
+        if (l == 0) {
+          b.wr_hi[slot] = __ldcg(&b.wc_hi[i]);
+          b.wr_lo[slot] = __ldcg(&b.wc_lo[i]);
+          b.wr_row[slot] = __ldcg(&b.wc_row[i]);
+        } else {
+          b.vr_key[slot] = __ldcg(&b.vc_key[i]);
+          b.vr_kl[slot] = __ldcg(&b.vc_kl[i]);
+          b.vr_whi[slot] = __ldcg(&b.vc_whi[i]);
+          b.vr_wlo[slot] = __ldcg(&b.vc_wlo[i]);
+          b.vr_row[slot] = __ldcg(&b.vc_row[i]);
+          b.vr_blk[slot] = __ldcg(&b.vc_blk[i]);
+        }
+      }
+    }
+  }
+  if (g == 0 && tid == 0) {
+#pragma unroll
+    for (int l = 0; l < 2; ++l) {
+      w->ref_on[l] = on[l] ? 1 : 0;
+      w->ref_p[l][0] = (u64)(P[l] >> 64);
+      w->ref_p[l][1] = (u64)P[l];
+      w->ref_s[l] = fin_s[l];
+    }
+    w->ref_iters = it;
+  }
+}
+
 // k_scan staging: one round = SCAN_TPB consecutive rows (one per thread),
 // every column k_scan reads arrives by TMA into one of SCAN_NBUF ring buffers.
 #define SCAN_R SCAN_TPB
@@ -475,9 +642,10 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
   const double now = w->in.now;
   const int mode = w->in.mode;
   const bool do_exp = !(mode & MARS_MODE_SKIP_EXPIRY) && policy_pins(c);
-  // the k_scan victim stream is MARS's reclaim order; the comparison policies
-  // reclaim through the walk's exact full-table search
-  const bool vic = c.policy == POL_MARS;
+  // the victim stream is the policy's reclaim order (run_reclaim_key /
+  // pin_reclaim_key); pins are victims of the policies that pin
+  const bool vic_pin = policy_pins(c);
+  const double ascale = (now > 0.0 && now < 1e300) ? 2048.0 / now : 0.0;
   // S2 at tool boundaries: MARS's economics or the TTL rule; fcfs and
   // program_priority never pin (retention_decision None, baselines.py:82-86)
   const bool ret_on = c.policy != POL_FCFS && c.policy != POL_PP;
@@ -533,8 +701,8 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
           exp_blocks += pbk;
           n_exp++;
           rv = DIG_EXP;
-        } else if (vic) {
-          rv = victim_digit(false, !exp_, B[SB_PL + lr], pbk);
+        } else if (vic_pin) {
+          rv = pin_reclaim_digit(c.policy, !exp_, B[SB_PL + lr], pbk, d, now);
           if (rv <= bv) atomicAdd(&hv[rv], 1u);
           n_vic++;
         }
@@ -556,8 +724,9 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
         } else {
           lv = 0;
         }
+        i64 sv = 0;
         if (c.policy == POL_PP) {
-          const i64 sv = t.served[r];
+          sv = t.served[r];
           if (sv > 0xffffffffll) w->status |= ST_BAD_INPUT;  // outside the packed key
           rw = pp_window_digit(sv, ((const double*)(B + SB_RS))[lr], scale);
           if (rw <= bw) atomicAdd(&hw[rw], 1u);
@@ -568,10 +737,11 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
           if (rw <= bw) atomicAdd(&hw[rw], 1u);
         }
         const i32 kvv = ((const i32*)(B + SB_KV))[lr];
-        if (kvv > 0 && vic) {
+        if (kvv > 0) {
           n_vic++;
           if (bv >= (1u << 11)) {  // running digits start at 1 << 11
-            rv = victim_digit(true, false, lv, held_blocks(c, kvv));
+            rv = run_reclaim_digit(c.policy, lv, held_blocks(c, kvv),
+                                   ((const double*)(B + SB_RS))[lr], sv, ascale);
             if (rv <= bv) atomicAdd(&hv[rv], 1u);
           } else {
             rv = DIG_ABOVE;
@@ -702,6 +872,10 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
   block_threshold_pair(hw, (u32)c.window, hv, (u32)VSEL, wsum, &gw, &wu, &gv, &vu);
   if (gw > (int)tmw) gw = (int)tmw;
   if (gv > (int)tmv) gv = (int)tmv;
+  // lists the digits cannot cut down to about their target (every CTA derives
+  // the same answer from the merged histogram): refined in phase 3
+  const bool ref_w = wu > (u32)max(c.ref_trig_w, c.window);
+  const bool ref_v = vu > (u32)max(c.ref_trig_v, VSEL);
 
   // the probe's view after the expiry evictions (telemetry.py:152-158): the
   // usage S2 prices retention with
@@ -811,8 +985,8 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
     const int ntot = nw + nv + nb + ne;
     const bool ro = (mode & MARS_MODE_RANK_ORDERED) != 0;
     u32* exp_rows = ro ? b.exp_row_sorted : b.exp_row;
-    // staging: CTA-local row lists (4 B) + one 32-byte record per entry
-    constexpr int STAGE_REC = 32;
+    // staging: CTA-local row lists (4 B) + one 48-byte record per entry
+    constexpr int STAGE_REC = 48;
     const bool staged = ((((size_t)ntot * 4 + 15) & ~(size_t)15) + (size_t)ntot * STAGE_REC) <=
                         (size_t)SCAN_NBUF * SB_BYTES;
     u32* lrow = (u32*)sdyn;                                       // [ntot]
@@ -887,7 +1061,10 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
     }
     __syncthreads();
     PTIME(41);
-    // (C) gathers; staged: records in shared memory, else straight to global
+    // (C) gathers; staged: records in shared memory, else straight to global.
+    // Lists that will be refined (phase 3) also fold every key into the
+    // AND / OR of the list: their common prefix, where the refinement starts.
+    u64 ka[2][2] = {{~0ull, ~0ull}, {~0ull, ~0ull}}, ko[2][2] = {{0ull, 0ull}, {0ull, 0ull}};
     for (int k = threadIdx.x; k < ntot; k += blockDim.x) {
       u32 r;
       if (staged) {
@@ -907,16 +1084,25 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
         const bool ready = (dig[(i64)r - cs] & DIG_NONE) == 0;
         const u32 rk = t.rank[r];
         u64 whi = 0, wlo = 0;
+        u32 lv = 0;
+        double arr = 0.0;
+        i64 sv = 0;
         if (ready) {  // post-aging level
           if (c.policy == POL_PP) {
-            pp_window_key(t.served[r], t.arr[r], rk, whi, wlo);
+            sv = t.served[r];
+            arr = t.arr[r];
+            pp_window_key(sv, arr, rk, whi, wlo);
           } else {
-            const u32 lv = c.coord ? (u32)t.level[r] : 0u;
-            const double tt = c.coord ? t.rs[r] : t.arr[r];
-            window_key(lv, tt, rk, whi, wlo);
+            lv = c.coord ? (u32)t.level[r] : 0u;
+            arr = c.coord ? t.rs[r] : t.arr[r];
+            window_key(lv, arr, rk, whi, wlo);
           }
         }
         if (is_w) {
+          if (ref_w) {
+            ka[0][0] &= whi; ka[0][1] &= wlo;
+            ko[0][0] |= whi; ko[0][1] |= wlo;
+          }
           if (staged) {
             ((u64*)R)[0] = whi;
             ((u64*)R)[1] = wlo;
@@ -925,26 +1111,32 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
             b.wc_lo[s_base[0] + k] = wlo;
           }
         } else {
-          u64 vk;
+          u64 vk, vkl;
           i32 blk;
           if (ready) {
             const i64 h = held_blocks(c, t.kv[r]);
-            vk = victim_key(true, false, c.coord ? (u32)t.level[r] : 0u, h, rk);
+            run_reclaim_key(c.policy, lv, h, arr, sv, rk, vk, vkl);
             blk = (i32)h;
           } else {  // pinned row
-            const bool nonexp = !(t.dl[r] < now);
+            const double dl = t.dl[r];
             const i32 pbk = t.pb[r];
-            vk = victim_key(false, nonexp, (u32)t.plevel[r], pbk, rk);
+            pin_reclaim_key(c.policy, !(dl < now), (u32)t.plevel[r], pbk, dl, rk, vk, vkl);
             blk = pbk;
+          }
+          if (ref_v) {
+            ka[1][0] &= vk; ka[1][1] &= vkl;
+            ko[1][0] |= vk; ko[1][1] |= vkl;
           }
           if (staged) {
             ((u64*)R)[0] = vk;
-            ((u64*)R)[1] = whi;
-            ((u64*)R)[2] = wlo;
-            ((i32*)R)[6] = blk;
+            ((u64*)R)[1] = vkl;
+            ((u64*)R)[2] = whi;
+            ((u64*)R)[3] = wlo;
+            ((i32*)R)[8] = blk;
           } else {
             const int slot = s_base[1] + k - nw;
             b.vc_key[slot] = vk;
+            b.vc_kl[slot] = vkl;
             b.vc_whi[slot] = whi;
             b.vc_wlo[slot] = wlo;
             b.vc_blk[slot] = blk;
@@ -977,6 +1169,35 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
         if (staged) exp_rows[slot] = r;
       }
     }
+    if (ref_w || ref_v) {  // grid-uniform: the CTA's AND / OR -> the list's
+      __shared__ unsigned long long s_ka[2][2], s_ko[2][2];
+      if (threadIdx.x < 4) {
+        s_ka[threadIdx.x >> 1][threadIdx.x & 1] = ~0ull;
+        s_ko[threadIdx.x >> 1][threadIdx.x & 1] = 0ull;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int l = 0; l < 2; ++l)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          u64 a = ka[l][h], o = ko[l][h];
+#pragma unroll
+          for (int q = 16; q > 0; q >>= 1) {
+            a &= __shfl_xor_sync(FULL, a, q);
+            o |= __shfl_xor_sync(FULL, o, q);
+          }
+          if (lane == 0) {
+            if (~a) atomicAnd(&s_ka[l][h], a);
+            if (o) atomicOr(&s_ko[l][h], o);
+          }
+        }
+      __syncthreads();
+      if (threadIdx.x < 4) {
+        const int l = threadIdx.x >> 1, h = threadIdx.x & 1;
+        if (~s_ka[l][h]) atomicAnd(&w->ref_and[l][h], s_ka[l][h]);
+        if (s_ko[l][h]) atomicOr(&w->ref_or[l][h], s_ko[l][h]);
+      }
+    }
     if (staged) {
       if (threadIdx.x == 0) {  // the reservations' results, first use
         s_base[0] = gb0;
@@ -998,9 +1219,10 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
           const int slot = bv + k - nw;
           b.vc_row[slot] = r;
           b.vc_key[slot] = ((const u64*)R)[0];
-          b.vc_whi[slot] = ((const u64*)R)[1];
-          b.vc_wlo[slot] = ((const u64*)R)[2];
-          b.vc_blk[slot] = ((const i32*)R)[6];
+          b.vc_kl[slot] = ((const u64*)R)[1];
+          b.vc_whi[slot] = ((const u64*)R)[2];
+          b.vc_wlo[slot] = ((const u64*)R)[3];
+          b.vc_blk[slot] = ((const i32*)R)[8];
         } else {
           const int slot = bb + k - nw - nv;
           b.ret_row[slot] = r;
@@ -1011,6 +1233,15 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
         }
       }
     }
+  }
+
+  // ---- phase 3: grid radix refinement (only when a candidate list is much
+  // longer than its target: coarse digits over tied keys, or huge tables)
+  if (ref_w || ref_v) {
+    grid.sync();
+    PTIME(43);
+    grid_refine(grid, w, b, ref_w, ref_v, (int)c.window, VSEL);
+    PTIME(44);
   }
 
   PTIME(4);
@@ -1705,6 +1936,9 @@ __device__ __forceinline__ void admit_grid(Tab t, Cfg c, Work* w, Bufs b, Queue 
   // admit() of the packed prefix (sim.py:148-166 + MarsPolicy.on_admit)
   const double scale = (now > 0.0 && now < 1e300) ? 1024.0 / now : 0.0;
   const u32 tw = (u32)w->t_win;
+  const bool ref_w = w->ref_on[0] != 0;
+  const int ref_sft = w->ref_s[0];
+  const u128 ref_pp = mk128(w->ref_p[0][0], w->ref_p[0][1]) >> ref_sft;
   long long proj = 0;
   const i64 stride = (i64)gridDim.x * blockDim.x;
   const i64 lim = ((take + 31) / 32) * 32;
@@ -1753,14 +1987,18 @@ __device__ __forceinline__ void admit_grid(Tab t, Cfg c, Work* w, Bufs b, Queue 
         t.served[row] = 0;
         proj += blocks_ceil(c, cn) - blocks_ceil(c, kvv);
         if (!sharded) b.admitted[i] = adm;
-        if (wc) window_key(kl, arr, rk, whi, wlo);
+        if (wc) {
+          window_key(kl, arr, rk, whi, wlo);
+          // k_scan refined the window list: join it only at or below its bound
+          if (ref_w) wc = (mk128(whi, wlo) >> ref_sft) <= ref_pp;
+        }
       }
     }
-    int s = warp_append(&w->n_wc, wc);
+    int s = warp_append(ref_w ? &w->n_wr : &w->n_wc, wc);
     if (s >= 0) {
-      b.wc_hi[s] = whi;
-      b.wc_lo[s] = wlo;
-      b.wc_row[s] = row;
+      (ref_w ? b.wr_hi : b.wc_hi)[s] = whi;
+      (ref_w ? b.wr_lo : b.wc_lo)[s] = wlo;
+      (ref_w ? b.wr_row : b.wc_row)[s] = row;
     }
     // sharded: this replica's admitted rows, tagged with their packed index
     s = warp_append(&w->n_adm_own, own);
@@ -2040,7 +2278,7 @@ __global__ void k_build_global_queue(Work* w, Xchg x) {
 
 // victim stream entry (prefix of the reclaim order, scheduler.py:259)
 struct VEnt {
-  u64 key, whi, wlo;
+  u64 key, kl, whi, wlo;
   u32 row;
   i32 blk;
   int16_t wi;   // window index or -1
@@ -2452,6 +2690,7 @@ struct WinGather {
 
 // select the `k` smallest (hi, lo) keys of a global candidate list into smem,
 // sorted.  Bitonic when n <= SORT_CAP, else MSD radix refinement first.
+#define GPAY(i) (gpay != nullptr ? gpay[i] : (u32)(i))
 __device__ int cta_select_sorted(const u64* ghi, const u64* glo, const u32* gpay, int n, int k,
                                  u64* kh, u64* kl, u32* pv, u32* hist /*256*/,
                                  WinGather* wg = nullptr) {
@@ -2472,7 +2711,7 @@ __device__ int cta_select_sorted(const u64* ghi, const u64* glo, const u32* gpay
     if (i < n) {
       h = ghi[i];
       l = glo[i];
-      p = gpay[i];
+      p = GPAY(i);
     }
     // the candidates' hi range: one barrier, every warp folds the 32 partials
     __shared__ u64 s_mx[32];
@@ -2590,7 +2829,7 @@ __device__ int cta_select_sorted(const u64* ghi, const u64* glo, const u32* gpay
     if (i < n) {
       h = ghi[i];
       l = glo[i];
-      p = gpay[i];
+      p = GPAY(i);
     }
     for (int kk = 2; kk <= n2; kk <<= 1) {
       for (int j = kk >> 1; j > 0; j >>= 1) {
@@ -2639,7 +2878,7 @@ __device__ int cta_select_sorted(const u64* ghi, const u64* glo, const u32* gpay
     for (int i = threadIdx.x; i < n2; i += blockDim.x) {
       kh[i] = i < n ? ghi[i] : ~0ull;
       kl[i] = i < n ? glo[i] : ~0ull;
-      pv[i] = i < n ? gpay[i] : 0xffffffffu;
+      pv[i] = i < n ? GPAY(i) : 0xffffffffu;
     }
     __syncthreads();
     bitonic_sort(kh, kl, pv, n2);
@@ -2701,7 +2940,7 @@ __device__ int cta_select_sorted(const u64* ghi, const u64* glo, const u32* gpay
       if (s < SORT_CAP) {
         kh[s] = h;
         kl[s] = l;
-        pv[s] = gpay[i];
+        pv[s] = GPAY(i);
       }
     }
   }
@@ -2762,7 +3001,8 @@ __global__ void __launch_bounds__(WALK_TPB) k_walk(Tab t, Cfg c, Work* w, Bufs b
   }
   // 1. window = top-k of the candidates (k_scan + admitted rows)
   PTIME(35);
-  int nwc = w->n_wc;
+  const bool ref_w = w->ref_on[0] != 0;  // k_scan refined the window list
+  int nwc = ref_w ? w->n_wr : w->n_wc;
   __shared__ WinGather wg;
   if (threadIdx.x == 0) {
     wg.kv = t.kv;
@@ -2776,7 +3016,8 @@ __global__ void __launch_bounds__(WALK_TPB) k_walk(Tab t, Cfg c, Work* w, Bufs b
     wg.done = 0;
   }
   __syncthreads();
-  int nwin = cta_select_sorted(b.wc_hi, b.wc_lo, b.wc_row, nwc, c.window, kh, kl, pv, hist, &wg);
+  int nwin = cta_select_sorted(ref_w ? b.wr_hi : b.wc_hi, ref_w ? b.wr_lo : b.wc_lo,
+                               ref_w ? b.wr_row : b.wc_row, nwc, c.window, kh, kl, pv, hist, &wg);
   PTIME(24);
   const bool gathered = wg.done != 0;
   for (int i = threadIdx.x; i < nwin; i += blockDim.x) {
@@ -2809,12 +3050,6 @@ __global__ void __launch_bounds__(WALK_TPB) k_walk(Tab t, Cfg c, Work* w, Bufs b
     S.fs_ready = 0;
     S.status = 0;
     S.fast_ok = 0;
-    if (c.policy != POL_MARS) {
-      // no k_scan victim stream (it is MARS's reclaim order): every claim
-      // that the free pool cannot cover goes to the exact full-table search
-      S.stream_ready = 1;
-      S.stream_complete = 0;
-    }
   }
   __syncthreads();
   PTIME(17);
@@ -2956,44 +3191,44 @@ __global__ void __launch_bounds__(WALK_TPB) k_walk(Tab t, Cfg c, Work* w, Bufs b
       int rq = S.request;
       if (rq == REQ_DONE) break;
       if (rq == REQ_SORT) {
-        // victim stream: the smallest VSTREAM_CAP reclaim keys among the candidates
-        int nvc = w->n_vc;
-        int len = cta_select_sorted(b.vc_key, b.vc_key /*lo unused*/, b.vc_row, nvc,
-                                    VSTREAM_CAP, kh, kl, pv, hist);
-        // kl holds vc_key again (lo == hi); payload = row; recover per-entry data by
-        // a second lookup: build index map row -> candidate slot
+        // victim stream: the policy's reclaim-order prefix k_scan selected
+        // (refined: the exact top VSEL plus < REF_STOP), sorted by the
+        // 128-bit key; payload = candidate index
+        const bool ref_v = w->ref_on[1] != 0;
+        const int nvc = ref_v ? w->n_vr : w->n_vc;
+        const u64* vkh = ref_v ? b.vr_key : b.vc_key;
+        const u64* vkl = ref_v ? b.vr_kl : b.vc_kl;
+        const int len = cta_select_sorted(vkh, vkl, nullptr, nvc, c.stream_cap, kh, kl, pv, hist);
         __syncthreads();
-        for (int q = threadIdx.x; q < nvc; q += blockDim.x) {
-          u64 key = b.vc_key[q];
-          // position of this key in the sorted prefix (binary search)
-          int lo = 0, hi = len;
-          while (lo < hi) {
-            int mid = (lo + hi) >> 1;
-            if (kh[mid] < key) lo = mid + 1; else hi = mid;
-          }
-          if (lo < len && kh[lo] == key) {
-            VEnt e;
-            e.key = key;
-            e.whi = b.vc_whi[q];
-            e.wlo = b.vc_wlo[q];
-            e.row = b.vc_row[q];
-            e.blk = b.vc_blk[q];
-            e.pinned = (key >> 63) == 0;
-            e.dead = 0;
-            e.wi = t.winpos[e.row];
-            st[lo] = e;
-          }
+        const u64* vwh = ref_v ? b.vr_whi : b.vc_whi;
+        const u64* vwl = ref_v ? b.vr_wlo : b.vc_wlo;
+        const u32* vrw = ref_v ? b.vr_row : b.vc_row;
+        const i32* vbk = ref_v ? b.vr_blk : b.vc_blk;
+        for (int q = threadIdx.x; q < len; q += blockDim.x) {
+          const u32 ci = pv[q];
+          VEnt e;
+          e.key = kh[q];
+          e.kl = kl[q];
+          e.whi = vwh[ci];
+          e.wlo = vwl[ci];
+          e.row = vrw[ci];
+          e.blk = vbk[ci];
+          e.pinned = (e.key >> 63) == 0;
+          e.dead = 0;
+          e.wi = t.winpos[e.row];
+          st[q] = e;
         }
         __syncthreads();
         if (threadIdx.x == 0) {
           S.stream_ready = 1;
           S.stream_len = len;
           S.stream_first = 0;
+          // the stream holds every potential victim of the step
           S.stream_complete = (len == nvc && nvc == w->n_victims) ? 1 : 0;
-          // entries already evicted this walk (none before the first sort)
         }
         __syncthreads();
       } else if (rq == REQ_FULLSCAN) {
+        if (threadIdx.x == 0) w->n_fullscan += 1;
         walk_fullscan(c, t, S, n_rows, now, fs_row, fs_pin, fs_blk);
       }
     }
@@ -3323,6 +3558,7 @@ __global__ void __launch_bounds__(1024) k_work_init(Work* w, const mars_step_in*
     static_assert(sizeof(mars_step_in) % 4 == 0, "step_in is word-sized");
     for (size_t i = threadIdx.x; i < sizeof(mars_step_in) / 4; i += blockDim.x) dst[i] = src[i];
   }
+  if (threadIdx.x < 4) (&w->ref_and[0][0])[threadIdx.x] = ~0ull;
   if (threadIdx.x == 0) {
     w->tmin_win = 0xffffffffu;
     w->tmin_vic = 0xffffffffu;

@@ -313,7 +313,10 @@ class MarsEngine:
             free_blocks=o.free_blocks, limit=o.limit, slots=o.slots,
             diag={"n_window_cand": o.n_window_cand, "n_victim_cand": o.n_victim_cand,
                   "walk_slow": o.walk_slow, "sort_path": o.sort_path,
-                  "n_round_end": o.n_round_end, "n_done": o.n_done})
+                  "n_round_end": o.n_round_end, "n_done": o.n_done,
+                  "n_fullscan": o.n_fullscan, "ref_flags": o.ref_flags,
+                  "ref_rounds": o.ref_rounds, "n_window_ref": o.n_window_ref,
+                  "n_victim_ref": o.n_victim_ref})
 
     def _fetch_setup(self) -> None:
         base, size = C.c_void_p(), C.c_int64()
@@ -371,7 +374,10 @@ class MarsEngine:
             free_blocks=o.free_blocks, limit=o.limit, slots=o.slots,
             diag={"n_window_cand": o.n_window_cand, "n_victim_cand": o.n_victim_cand,
                   "walk_slow": o.walk_slow, "sort_path": o.sort_path,
-                  "n_round_end": o.n_round_end, "n_done": o.n_done})
+                  "n_round_end": o.n_round_end, "n_done": o.n_done,
+                  "n_fullscan": o.n_fullscan, "ref_flags": o.ref_flags,
+                  "ref_rounds": o.ref_rounds, "n_window_ref": o.n_window_ref,
+                  "n_victim_ref": o.n_victim_ref})
 
     def step(self, si: N.MarsStepIn) -> StepResult:
         self.enqueue(si)

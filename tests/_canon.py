@@ -33,3 +33,16 @@ def _conv(o):
     if isinstance(o, np.ndarray):
         return o.tolist()
     raise TypeError(type(o))
+
+
+def digest(obj, limit=2048):
+    """Canonical form with every list longer than `limit` replaced by its
+    length and the SHA-256 of its compact JSON (large frozen fixtures)."""
+    if isinstance(obj, dict):
+        return {k: digest(v, limit) for k, v in obj.items()}
+    if isinstance(obj, list):
+        if len(obj) > limit:
+            h = hashlib.sha256(json.dumps(obj, separators=(",", ":")).encode()).hexdigest()
+            return {"len": len(obj), "sha256": h}
+        return [digest(v, limit) for v in obj]
+    return obj

@@ -135,3 +135,73 @@ def comparison_variant(n, seed, policy, pool):
         served[(u >= 0.08) & (u < 0.10)] = 4096
         c["served"][:] = served
     return s
+
+
+def tick_grid(snap, seed, tick=0.064, batch_frac=0.05):
+    """Times on the reference clock's tick grid (engine.py:71-74: the clock
+    advances by repeated `now + tick_duration`), so ready_since / wait_since /
+    arrival tie exactly across many sessions, and a batch of sessions admitted
+    together shares ready_since == now (sim.py:148-166)."""
+    c = snap.cols
+    n = snap.n
+    rng = np.random.default_rng(seed + 4242)
+    k_now = int(round(snap.now / tick))
+    grid = np.cumsum(np.full(k_now + 400, tick))          # sequential IEEE adds
+    now = float(grid[k_now - 1])
+    ir = rng.integers(0, k_now, size=n)
+    ir[rng.random(n) < batch_frac] = k_now - 1              # admitted at `now` together
+    iw = np.minimum(ir + rng.integers(0, 313, size=n), k_now - 1)
+    ia = (ir * rng.random(n)).astype(np.int64)
+    c["ready_since"][:] = grid[ir]
+    c["wait_since"][:] = grid[iw]
+    c["arrival"][:] = grid[ia]
+    pinned = (c["flags"] & F_PINNED) != 0
+    c["deadline"][pinned] += now - snap.now
+    snap.now = now
+    snap.meta = dict(snap.meta, tick_grid=True)
+    return snap
+
+
+def reclaim_heavy(n, seed, policy="mars", tiny_pins=40):
+    """A step that needs many victims (scheduler.py:228-267 returning long
+    prefixes): every running session holds 1-2 blocks, decodes are block
+    aligned (each needs one new block), prefills are whole chunks from a
+    block-aligned KV, and the pool has no free block.  Policies that pin keep
+    a few one-block pins (reclaimed first); fcfs / program_priority hold none."""
+    from paper_2604_26963_b200.snapshot import DECODE, PREFILL
+
+    s = snapshot_v1(n, seed=seed, pool="pressure")
+    c = s.cols
+    rng = np.random.default_rng(seed + 99)
+    dec = c["phase"] == DECODE
+    pre = c["phase"] == PREFILL
+    small = 16 * rng.integers(1, 3, size=n)
+    c["kv"][dec] = small[dec]
+    c["context"][dec] = small[dec]
+    c["kv"][pre] = 16 * rng.integers(0, 2, size=n)[pre]
+    pinned = (c["flags"] & F_PINNED) != 0
+    keep = np.zeros(n, dtype=bool)
+    if policy not in ("fcfs", "program_priority"):
+        keep[rng.permutation(np.nonzero(pinned)[0])[:tiny_pins]] = True
+    drop = pinned & ~keep
+    c["flags"][drop] &= ~np.uint8(F_PINNED)
+    c["kv"][drop] = 0
+    c["pinned_blocks"][drop] = 0
+    c["deadline"][drop] = 0.0
+    c["plevel"][drop] = 0
+    c["kv"][keep] = 16
+    c["pinned_blocks"][keep] = 1
+    held = -(-c["kv"].astype(np.int64) // 16)
+    s.total_blocks = int(held.sum())
+    s.free_blocks = 0
+    q = s.queue
+    long_ = c["req_blocks"][q] > 0.25 * s.total_blocks
+    c["flags"][q] = (c["flags"][q] & ~np.uint8(F_LONG)) | np.where(long_, F_LONG, 0).astype(np.uint8)
+    if policy == "program_priority":
+        served = rng.integers(0, 60_000, size=n)
+        u = rng.random(n)
+        served[u < 0.05] = 0
+        served[(u >= 0.05) & (u < 0.10)] = 4096
+        c["served"][:] = served
+    s.meta = dict(s.meta, variant="reclaim_heavy", policy=policy)
+    return s

@@ -140,3 +140,19 @@ def test_kat_levels_and_charges():
         for ch in r["charges"]:
             op.charge(st, ch, m)
         assert (st.level, st.served_tokens_at_level) == (r["level"], r["served"])
+
+
+HEAVY = _load("heavy_steps.json")
+
+
+@pytest.mark.parametrize("i", range(len(HEAVY)))
+def test_oracle_heavy_step_matches_reference(i):
+    """Heavy reclaim (dozens of victims, every policy) and tick-gridded ties:
+    the oracle against the reference's own step (oracle/make_golden.py
+    --only heavy)."""
+    from oracle.make_golden import heavy_kw, heavy_snapshot
+
+    case = HEAVY[i]["case"]
+    got = canon(run_step(heavy_snapshot(case), **heavy_kw(case)))
+    for k, v in HEAVY[i]["out"].items():
+        assert got[k] == v, k
