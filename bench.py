@@ -257,65 +257,162 @@ def hbm_sweep(device: int, sizes, steps: int = 5, warmup: int = 3, flush_mb: int
     return out
 
 
+def regime_sweep(device: int, n: int, steps: int = 10, warmup: int = 3, flush_mb: int = 512) -> list:
+    """The step on the regimes beyond the headroom snapshot, at 1M sessions
+    (SURVEY.md §8(d) pressure pool; VERDICT r1 task 1): heavy reclamation
+    (every running session holds 1-2 blocks, no free block: dozens of victims
+    per step) under MARS and a comparison policy, and tick-gridded ties
+    (every time on the 0.064 s grid, a batch admitted at `now`).  Same timing
+    as the headline (graph launch, L2 flushed, state restored, CUDA events)."""
+    import statistics as st
+
+    import torch
+
+    from paper_2604_26963_b200.engine import MarsEngine, make_config
+    from paper_2604_26963_b200.snapshot import snapshot_v1
+    from tests._variants import reclaim_heavy, tick_grid
+
+    cases = [("reclaim_heavy", "mars", lambda: reclaim_heavy(n, 91, "mars")),
+             ("reclaim_heavy_grid", "mars", lambda: tick_grid(reclaim_heavy(n, 92, "mars"), 92)),
+             ("reclaim_heavy_grid", "fcfs", lambda: tick_grid(reclaim_heavy(n, 93, "fcfs"), 93)),
+             ("reclaim_heavy", "program_priority", lambda: reclaim_heavy(n, 94, "program_priority")),
+             ("tick_grid_headroom", "mars", lambda: tick_grid(snapshot_v1(n, seed=111), 111))]
+    out = []
+    for name, policy, mk in cases:
+        snap = mk()
+        due = policy == "mars"
+        eng = MarsEngine(max_rows=snap.n, max_queue=max(len(snap.queue), 1), device=device,
+                         config=make_config(initial_window=snap.initial_window, policy=policy))
+        eng.load_snapshot(snap)
+        si = eng.step_in(snap.now, due, snap.active_tools, snap.queued_tools, snap.worker_slots)
+        stream = torch.cuda.Stream()
+        torch.cuda.set_stream(stream)
+        eng.lib.mars_set_stream(eng.ctx, stream.cuda_stream)
+        eng.checkpoint()
+        res = eng.step(si)
+        eng.restore()
+        eng.set_graph(True)
+        for _ in range(warmup):
+            eng.restore()
+            eng.enqueue(si)
+        torch.cuda.synchronize()
+        ms = []
+        for _ in range(steps):
+            eng.restore()
+            eng.flush_l2(flush_mb << 20)
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            eng.enqueue(si)
+            b.record(stream)
+            torch.cuda.synchronize()
+            ms.append(a.elapsed_time(b))
+        eng.set_graph(False)
+        eng.set_profiling(True)
+        kt = []
+        for _ in range(steps):
+            eng.restore()
+            eng.flush_l2(flush_mb << 20)
+            eng.enqueue(si)
+            kt.append(eng.kernel_times())
+        eng.set_profiling(False)
+        step_ms = st.median(ms)
+        out.append({"regime": name, "policy": policy, "sessions": n, "status": int(res.status),
+                    "ms_per_step": step_ms, "sessions_per_s": n / (step_ms * 1e-3),
+                    "evictions": int(len(res.evict_rows)), "tokens": int(res.total_tokens),
+                    "n_fullscan": res.diag["n_fullscan"], "ref_flags": res.diag["ref_flags"],
+                    "ref_rounds": res.diag["ref_rounds"],
+                    "k_scan_ms": st.median(k["k_scan"] for k in kt),
+                    "k_walk_ms": st.median(k["k_walk"] for k in kt),
+                    "k_control_ms": st.median(k["k_control"] for k in kt) if due else None})
+        eng.close()
+        del snap
+        torch.cuda.synchronize()
+    return out
+
+
 def cpu_reference(sessions: int, seed: int, reps: int = 1):
-    """Times the oracle port's full step (materialisation excluded)."""
-    from oracle.snapshot_step import World, run_step
+    """The reference's own step (agentsched from baseline/_ref, else the
+    oracle port) over snapshot_v1(sessions) on one core; materialisation
+    excluded."""
+    from oracle.ref_step import timed_step
     from paper_2604_26963_b200.snapshot import snapshot_v1
 
-    times = []
-    for r in range(reps):
-        snap = snapshot_v1(sessions, seed=seed + r, pool="headroom")
-        w = World(snap)
-        t0 = time.perf_counter()
-        run_step(snap, world=w)
-        times.append(time.perf_counter() - t0)
-        del w
-    return times
+    return [timed_step(snapshot_v1(sessions, seed=seed + r, pool="headroom")) for r in range(reps)]
 
 
-def _ref_worker(job):
-    n, seed = job
-    return cpu_reference(n, seed=seed)[0]
+_REF_SHARDS = []
+
+
+def _ref_worker(j):
+    from oracle.ref_step import timed_step
+    return timed_step(_REF_SHARDS[j])
+
+
+def workload_config(sessions: int, world: int) -> dict:
+    """The `config` of both arms' lines (identical keys and values)."""
+    return {"workload": "one MARS scheduling step over one global snapshot_v1 session table "
+                        "(pin expiry, probe, control-plane admission, MLFQ aging, window "
+                        "top-128, build_plan walk with reclamation, S2 retention)"
+                        + ("" if world == 1 else
+                           f"; rows sharded rank mod {world} over data-parallel replicas"),
+            "sessions": sessions, "pool": "headroom", "mix": "A",
+            "parallelism": "1 replica" if world == 1 else
+            f"{world} replicas: NCCL all-reduce of probe counters + all-gather of "
+            "top-slots admission candidates",
+            "l2": "flushed before every timed step (512 MiB scratch write); state restored "
+                  "from a device checkpoint (untimed)"}
 
 
 def run_reference_arm(a):
-    """The reference's CPU path on every host core it can use: the port is
-    single-threaded CPython, so P processes each run one full step over their
-    own n-session sample concurrently (data-parallel replicas, as the GPU
-    replicas are); a step's time is the slowest process's (materialisation
-    excluded), throughput = P x n / that time."""
+    """The reference's CPU path on every host core it can use, on the GPU
+    arm's workload: snapshot_v1(sessions) split into P row-shards (row r ->
+    shard r mod P), one process per shard running the real agentsched step
+    (baseline/_ref; the oracle port if it is missing) over its shard
+    concurrently; a step takes as long as the slowest shard (materialisation
+    excluded), throughput = sessions / that time."""
     import multiprocessing as mp
+
+    from oracle.ref_step import kind
+    from paper_2604_26963_b200.snapshot import snapshot_shard, snapshot_v1
 
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    n = a.ref_sample
+    world = int(os.environ.get("WORLD_SIZE", str(a.gpus)))
     try:
         cores = len(os.sched_getaffinity(0))
     except AttributeError:
         cores = os.cpu_count() or 1
     procs = max(1, min(a.ref_procs, cores)) if a.ref_procs > 0 else max(1, min(16, cores))
+    snap = snapshot_v1(a.sessions, seed=0, pool="headroom")
+    _REF_SHARDS[:] = [snapshot_shard(snap, procs, j) for j in range(procs)]
     times = []
     with mp.get_context("fork").Pool(procs) as pool:
         for i in range(a.warmup + a.steps):
-            ts = pool.map(_ref_worker, [(n, 100 + i * procs + j) for j in range(procs)])
+            ts = pool.map(_ref_worker, range(procs))
             if i >= a.warmup:
                 times.append(max(ts))
     per = sum(times) / len(times)
-    val = procs * n / per
+    val = a.sessions / per
+    k = kind()
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "sessions/s",
-        "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": per * 1e3,
-        "steps_per_s": 1.0 / per, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64+i64", "data": "synthetic (snapshot_v1, mix A)",
-        "config": {"workload": "one MARS scheduling step (expiry, probe, admission, aging, "
-                               "window top-128, build_plan walk, S2 retention)",
-                   "sessions": a.sessions, "pool": "headroom", "parallelism": "replicas"},
-        "cpu_baseline": {"value": val, "unit": "sessions/s", "cores": procs, "kind": "port",
-                         "sample": f"{procs} processes, each one full step over its own "
-                                   f"{n}-session snapshot_v1 (fresh seed per step) with the "
-                                   "object-level CPython restatement of agentsched (oracle/), "
-                                   "materialisation excluded; step time = slowest process",
+        "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": per * 1e3,
+        "steps_per_s": 1.0 / per, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "f64+i64", "data": "synthetic (snapshot_v1, mix A, seed 0)",
+        "config": workload_config(a.sessions, world),
+        "cpu_baseline": {"value": val, "unit": "sessions/s", "cores": procs, "kind": k,
+                         "sample": f"snapshot_v1({a.sessions}) in {procs} row-shards of "
+                                   f"~{a.sessions // procs} sessions, one process per shard "
+                                   "running " + ("the unmodified reference agentsched "
+                                                 "(baseline/_ref)" if k == "reference" else
+                                                 "the oracle port of agentsched")
+                                   + " step (expiry, probe, refresh_pressure, balance_and_admit"
+                                   " + admit, decide_retention on boundary rows, sorted ready "
+                                   "list, MarsPolicy.plan_tick with the evictor); "
+                                   "materialisation excluded; step time = slowest shard",
                          "host_cores": cores},
         "e2e": {"value": val, "unit": "sessions/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -391,13 +488,14 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--sessions", type=int, default=1_000_000)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--ref-sample", type=int, default=100_000)
     ap.add_argument("--ref-procs", type=int, default=0,
                     help="reference-arm processes (0: every host core, at most 16)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--flush-mb", type=int, default=512)
     ap.add_argument("--no-kv", action="store_true", help="skip the KV evict/restore sweep")
+    ap.add_argument("--no-regimes", dest="regimes", action="store_false",
+                    help="skip the heavy-reclaim / tick-grid regime sweep")
     ap.add_argument("--clock-load", type=int, default=100,
                     help="untimed 20-step batches run under the clock sampler first (0 under ncu)")
     ap.add_argument("--advance-ticks", type=int, default=40,
@@ -587,14 +685,7 @@ def main():
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_per_step,
         "steps_per_s": steps_per_s, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64+i64", "data": "synthetic (snapshot_v1 mix A, seed=rank)",
-        "config": {"workload": "one MARS scheduling step (expiry, probe, control-plane admission, "
-                               "aging, window top-128, build_plan walk, S2 retention) per replica",
-                   "sessions_per_gpu": a.sessions, "pool": "headroom",
-                   "parallelism": (f"replicas x{world}" if world == 1 else
-                                   f"sharded replicas x{world}: NCCL all-reduce of probe "
-                                   "counters + all-gather of the admission list"),
-                   "l2": f"flushed before every timed step ({a.flush_mb} MiB scratch write); "
-                         "state restored from a device checkpoint (untimed)"},
+        "config": workload_config(a.sessions, world),
         "roofline": {"bound": "hbm", "kernel": "k_scan", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": _ncu_traffic(),
                      "algorithmic_bytes": sb, "kernel_ms": scan_avg, "peak_source": peak_kind,
@@ -615,17 +706,25 @@ def main():
             line["kv"] = kv_sweep(local)
         except Exception as exc:  # the scheduler number stands on its own
             line["kv"] = {"error": repr(exc)[:300]}
+    if rank == 0 and world == 1 and a.regimes:
+        try:
+            line["regimes"] = regime_sweep(local, a.sessions)
+        except Exception as exc:  # the headline line stands on its own
+            line["regimes"] = {"error": repr(exc)[:300]}
     if rank == 0 and world == 1 and a.hbm_sweep:
         try:
             line["hbm_sweep"] = hbm_sweep(local, [int(x) for x in a.hbm_sweep.split(",") if x])
         except Exception as exc:  # the headline line stands on its own
             line["hbm_sweep"] = {"error": repr(exc)[:300]}
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        from oracle.ref_step import kind as ref_kind
         t_cpu = cpu_reference(a.sessions, seed=0)[0]
         line["cpu_baseline"] = {
-            "value": a.sessions / t_cpu, "unit": "sessions/s", "cores": 1, "kind": "port",
-            "sample": f"one full step over snapshot_v1({a.sessions}) on the oracle "
-                      "(object-level CPython restatement of agentsched), materialisation excluded",
+            "value": a.sessions / t_cpu, "unit": "sessions/s", "cores": 1, "kind": ref_kind(),
+            "sample": f"one full step over snapshot_v1({a.sessions}) (the same table) with "
+                      + ("the unmodified reference agentsched (baseline/_ref)"
+                         if ref_kind() == "reference" else "the oracle port of agentsched")
+                      + " on one core, materialisation excluded",
             "seconds": t_cpu}
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -166,3 +166,40 @@ def snapshot_v1(n: int, seed: int = 0, pool: str = "headroom", now: float = 1000
                     active_tools=int(tool.sum()), queued_tools=0,
                     initial_window=float(max(2 * n, 8)),
                     meta={"kind": "snapshot_v1", "n": n, "seed": seed, "pool": pool, "mix": "A"})
+
+
+def snapshot_shard(snap: Snapshot, G: int, g: int) -> Snapshot:
+    """Row shard ``g`` of ``G`` (rows ``r`` with ``r % G == g``, SURVEY.md
+    §8(e): session row -> replica ``sid_rank mod G``; ``snapshot_v1`` ranks
+    equal rows).  The shard is a replica of its own: its rows keep their
+    session ids (rank), its pool holds its own rows' blocks with the same
+    headroom rule (or the same +8 slack under pressure), its admission list is
+    its rows in the global list order, and the tool plane / admission window
+    scale with its size."""
+    if not (0 <= g < G):
+        raise ValueError((G, g))
+    rows = np.arange(g, snap.n, G)
+    c = {k: v[rows].copy() for k, v in snap.cols.items()}
+    n = len(rows)
+    held = -(-c["kv"].astype(np.int64) // BLOCK)
+    total_held = int(held.sum())
+    pool = snap.meta.get("pool", "headroom")
+    slack = snap.total_blocks - (snap.total_blocks - snap.free_blocks)
+    if pool == "headroom":
+        total = -(-total_held * 100 // 85)
+    else:
+        total = total_held + min(slack, 8)
+    total = max(total, 1)
+    q = snap.queue[snap.queue % G == g]
+    queue = (q // G).astype(np.uint32)
+    long_ = c["req_blocks"] > 0.25 * total
+    fl = c["flags"]
+    waiting = (fl & F_QUEUED) != 0
+    c["flags"][:] = (fl & ~np.uint8(F_LONG)) | np.where(waiting & long_, F_LONG, 0).astype(np.uint8)
+    meta = dict(snap.meta, shard=(G, g), n=n)
+    return Snapshot(cols=c, queue=queue, now=snap.now, total_blocks=int(total),
+                    free_blocks=int(total - total_held), worker_slots=max(2 * n, 1),
+                    active_tools=int((c["phase"] == TOOL).sum()), queued_tools=0,
+                    initial_window=float(max(2 * n, 8)), ema_tool=snap.ema_tool,
+                    ema_blocks=snap.ema_blocks, blocks_seed=snap.blocks_seed,
+                    telemetry=dict(snap.telemetry), meta=meta)

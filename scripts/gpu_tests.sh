@@ -10,7 +10,7 @@ import json
 d = json.loads(open("gpurun_out/bench_quick.json").read().strip().splitlines()[-1])
 print("ms_per_step", d["ms_per_step"], "min", d["step_ms_min"], "kernels", d["kernel_ms_median"],
       "frac", d["roofline"]["frac"], "e2e_ms", d["e2e"]["ms_per_step"])
-for k in ("pressure_1m", "hbm_sweep"):
+for k in ("regimes", "hbm_sweep"):
     v = d.get(k)
     if isinstance(v, list):
         for r in v: print({a: (round(b, 4) if isinstance(b, float) else b) for a, b in r.items()})
