@@ -356,6 +356,12 @@ int mars_create(const mars_config* hcfg, int device, int64_t max_rows, int64_t m
   ALLOC(b.vr_wlo, (size_t)VR_CAP * 8);
   ALLOC(b.vr_row, (size_t)VR_CAP * 4);
   ALLOC(b.vr_blk, (size_t)VR_CAP * 4);
+  ALLOC(b.vs_key, (size_t)VSTREAM_CAP * 8);
+  ALLOC(b.vs_kl, (size_t)VSTREAM_CAP * 8);
+  ALLOC(b.vs_whi, (size_t)VSTREAM_CAP * 8);
+  ALLOC(b.vs_wlo, (size_t)VSTREAM_CAP * 8);
+  ALLOC(b.vs_row, (size_t)VSTREAM_CAP * 4);
+  ALLOC(b.vs_blk, (size_t)VSTREAM_CAP * 4);
   ALLOC(b.ret_row, R * 4);
   ALLOC(b.ret_pin, R);
   ALLOC(b.ret_b, R * 8);
@@ -464,7 +470,8 @@ int mars_destroy(mars_ctx* ctx) {
                 b.dec_level, b.pre_level, b.fin_row, b.fin_pin, b.fin_b, b.fin_c, b.fin_d,
                 b.flush, b.end_row, b.end_kind, b.end_blk, b.end_pin, b.end_b, b.end_c,
                 b.end_d, b.pre_done, b.vc_kl, b.wr_hi, b.wr_lo, b.wr_row, b.vr_key, b.vr_kl,
-                b.vr_whi, b.vr_wlo, b.vr_row, b.vr_blk};
+                b.vr_whi, b.vr_wlo, b.vr_row, b.vr_blk, b.vs_key, b.vs_kl, b.vs_whi,
+                b.vs_wlo, b.vs_row, b.vs_blk};
   for (void* p : bs) cudaFree(p);
   cudaFree(ctx->d_stage);
   cudaFree(ctx->d_resume);

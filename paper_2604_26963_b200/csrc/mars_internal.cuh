@@ -153,16 +153,20 @@ struct Work {
   u32 adm_ctas;     // k_control CTAs past admission (the last one publishes)
   u32 adm_pad[3];   // (Work stays a whole number of 16-byte words)
   // grid radix refinement of the candidate lists (k_scan phase 3): per list
-  // (0 window, 1 victims) the AND / OR of every emitted key (their common
-  // prefix), three rotating 256-bin histograms, and the final bound: the
-  // refined list holds the keys with (key >> ref_s) <= (ref_p >> ref_s)
-  unsigned long long ref_and[2][2], ref_or[2][2];
+  // (0 window, 1 victims) three rotating 256-bin histograms and group AND /
+  // ORs, and the final bound: the refined list holds the keys with
+  // (key >> ref_s) <= (ref_p >> ref_s)
   u32 ref_hist[2][3][256];
+  unsigned long long ref_gand[2][3][2], ref_gor[2][3][2];  // per round: the group's AND / OR
   unsigned long long ref_p[2][2];
   i32 ref_on[2], ref_s[2];
   i32 n_wr, n_vr;     // refined list lengths
   i32 n_fullscan;     // exact full-table reclaimer passes taken by the walk
   i32 ref_iters;
+  i32 vic_on;         // k_scan built a victim stream (the free pool may not cover a plan)
+  i32 vs_on;          // ... and ranked it into the stream order (vs_*)
+  i32 ref_pad[2];
+  u32 ref_pad2[16];
   i32 n_finish;
   i32 sort_path;    // pack_queue: 1 grid LSD sort, 2 one CTA, 3 early grid LSD (k_pack)
   i32 n_round_end, n_done;  // MARS_MODE_ADVANCE: rounds that ended, sessions that finished
@@ -191,6 +195,8 @@ struct Bufs {
   // the same two lists after the grid radix refinement (k_scan phase 3)
   u64 *wr_hi, *wr_lo; u32 *wr_row;
   u64 *vr_key, *vr_kl, *vr_whi, *vr_wlo; u32 *vr_row; i32 *vr_blk;
+  // the victim stream in reclaim order (k_scan's grid rank), VSTREAM_CAP entries
+  u64 *vs_key, *vs_kl, *vs_whi, *vs_wlo; u32 *vs_row; i32 *vs_blk;
   // retention results
   u32 *ret_row; u8 *ret_pin; double *ret_b, *ret_c, *ret_d;
   // admission

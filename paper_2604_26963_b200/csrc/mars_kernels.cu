@@ -39,7 +39,7 @@ namespace cg = cooperative_groups;
 #ifdef MARS_PHASE_TIMING
 // Debug builds only (-DMARS_PHASE_TIMING): per-CTA %globaltimer stamps at
 // named points of the step, dumped as a timeline after each step.
-#define PT_SLOTS 48
+#define PT_SLOTS 64
 __device__ unsigned long long g_ptime[1024][PT_SLOTS];
 __device__ __forceinline__ void ptime(int k) {
   if (threadIdx.x == 0) {
@@ -400,12 +400,12 @@ __device__ __forceinline__ int clz128(u128 x) {
 }
 
 // Exact radix select over the emitted 128-bit keys of the window list (0)
-// and the victim list (1), by the whole cooperative grid: starting below the
-// keys' common prefix (the AND / OR folded during emission), each round
+// and the victim list (1), by the whole cooperative grid: each round
 // histograms the next 8 bits of the keys still sharing the prefix (CTA slices
-// of the list, shared-memory counts, one global add per bin), one grid
-// barrier, and every CTA derives the bin holding the k-th key from the same
-// counts.  It stops once that bin holds <= REF_STOP keys; the refined list is
+// of the list, shared-memory counts, one global add per bin) and folds their
+// AND / OR, one grid barrier, and every CTA derives the bin holding the k-th
+// key from the same counts -- or, when every key of the group shared the
+// digit, jumps to the group's first differing bit.  It stops once that bin holds <= REF_STOP keys; the refined list is
 // every key whose bits above the bin's position are <= the prefix's: the
 // exact top k plus fewer than REF_STOP keys, compacted into wr_* / vr_*.
 // Called by every thread of every CTA after a grid barrier (the lists are
@@ -414,6 +414,7 @@ __device__ void grid_refine(cg::grid_group& grid, Work* w, Bufs& b, bool on_w, b
                             int kv) {
   __shared__ u32 sh[2][256];
   __shared__ u32 s_ws[2][8];
+  __shared__ unsigned long long s_ga[2][2], s_go[2][2];
   const int G = gridDim.x, g = blockIdx.x, tid = threadIdx.x, bd = blockDim.x;
   const int lane = tid & 31, wid = tid >> 5;
   const int n[2] = {__ldcg(&w->n_wc), __ldcg(&w->n_vc)};
@@ -424,28 +425,24 @@ __device__ void grid_refine(cg::grid_group& grid, Work* w, Bufs& b, bool on_w, b
   u128 P[2];
   int top[2], fin_s[2];
   u32 need[2] = {(u32)kw, (u32)kv};
+  // the first round starts at the top byte; a round whose digit is common to
+  // the whole group jumps to the group's first differing bit (its AND / OR)
 #pragma unroll
   for (int l = 0; l < 2; ++l) {
-    act[l] = false;
+    act[l] = on[l];
     P[l] = 0;
-    top[l] = -1;
+    top[l] = 127;
     fin_s[l] = 0;
-    if (!on[l]) continue;
-    const u128 A = mk128(__ldcg(&w->ref_and[l][0]), __ldcg(&w->ref_and[l][1]));
-    const u128 O = mk128(__ldcg(&w->ref_or[l][0]), __ldcg(&w->ref_or[l][1]));
-    const u128 x = A ^ O;
-    if (x == 0) {  // one distinct key: nothing to refine
-      P[l] = A;
-      continue;
-    }
-    top[l] = 127 - clz128(x);
-    P[l] = (top[l] >= 127) ? (u128)0 : ((A >> (top[l] + 1)) << (top[l] + 1));
-    act[l] = true;
   }
   int it = 0;
   while (act[0] || act[1]) {  // grid-uniform: every CTA holds the same state
+    PTIME(48 + (it < 7 ? it : 7));
     const int buf = it % 3;
     for (int i = tid; i < 512; i += bd) (&sh[0][0])[i] = 0u;
+    if (tid < 4) {
+      (&s_ga[0][0])[tid] = ~0ull;
+      (&s_go[0][0])[tid] = 0ull;
+    }
     __syncthreads();
 #pragma unroll
     for (int l = 0; l < 2; ++l) {
@@ -455,18 +452,40 @@ __device__ void grid_refine(cg::grid_group& grid, Work* w, Bufs& b, bool on_w, b
       const int sft = top[l] + 1;
       const u128 pp = sft >= 128 ? (u128)0 : (P[l] >> sft);
       const i64 i0 = (i64)n[l] * g / G, i1 = (i64)n[l] * (g + 1) / G;
+      u64 ah = ~0ull, al = ~0ull, oh = 0ull, ol = 0ull;  // the group's AND / OR
       for (i64 i = i0 + tid; i < i1; i += bd) {
-        const u128 key = mk128(__ldcg(khp[l] + i), __ldcg(klp[l] + i));
+        const u64 kh_ = __ldcg(khp[l] + i), kl_ = __ldcg(klp[l] + i);
+        const u128 key = mk128(kh_, kl_);
         if (sft < 128 && (key >> sft) != pp) continue;
         atomicAdd(&sh[l][(u32)(key >> lo_b) & msk], 1u);
+        ah &= kh_;
+        al &= kl_;
+        oh |= kh_;
+        ol |= kl_;
+      }
+#pragma unroll
+      for (int q = 16; q > 0; q >>= 1) {
+        ah &= __shfl_xor_sync(FULL, ah, q);
+        al &= __shfl_xor_sync(FULL, al, q);
+        oh |= __shfl_xor_sync(FULL, oh, q);
+        ol |= __shfl_xor_sync(FULL, ol, q);
+      }
+      if (lane == 0) {
+        if (~ah) atomicAnd(&s_ga[l][0], ah);
+        if (~al) atomicAnd(&s_ga[l][1], al);
+        if (oh) atomicOr(&s_go[l][0], oh);
+        if (ol) atomicOr(&s_go[l][1], ol);
       }
     }
     __syncthreads();
 #pragma unroll
     for (int l = 0; l < 2; ++l)
-      if (act[l])
+      if (act[l]) {
         for (int d = tid; d < 256; d += bd)
           if (sh[l][d]) atomicAdd(&w->ref_hist[l][buf][d], sh[l][d]);
+        if (tid < 2 && ~s_ga[l][tid]) atomicAnd(&w->ref_gand[l][buf][tid], s_ga[l][tid]);
+        if (tid < 2 && s_go[l][tid]) atomicOr(&w->ref_gor[l][buf][tid], s_go[l][tid]);
+      }
     grid.sync();
 #pragma unroll
     for (int l = 0; l < 2; ++l) {
@@ -499,21 +518,46 @@ __device__ void grid_refine(cg::grid_group& grid, Work* w, Bufs& b, bool on_w, b
       }
       __syncthreads();
       const int lo_b = top[l] >= 7 ? top[l] - 7 : 0;
-      need[l] -= s_below[l];
-      P[l] |= (u128)(u32)s_bin[l] << lo_b;
-      const u32 cnt = s_cntb[l];
-      top[l] = lo_b - 1;
-      if (cnt <= (u32)REF_STOP || top[l] < 0) {
-        act[l] = false;
-        fin_s[l] = lo_b;
+      // the group's first differing bit: below this round's digit, every key
+      // of the group fell into one bin -- jump straight to that bit (ties in
+      // the leading key fields: equal times, equal levels and footprints)
+      const u128 ga = mk128(__ldcg(&w->ref_gand[l][buf][0]), __ldcg(&w->ref_gand[l][buf][1]));
+      const u128 go = mk128(__ldcg(&w->ref_gor[l][buf][0]), __ldcg(&w->ref_gor[l][buf][1]));
+      const u128 gx = ga ^ go;
+      const int dtop = gx ? 127 - clz128(gx) : -1;
+      if (dtop < lo_b) {
+        if (dtop < 0) {  // a single key left
+          P[l] = ga;
+          act[l] = false;
+          fin_s[l] = 0;
+        } else {
+          P[l] = (ga >> (dtop + 1)) << (dtop + 1);
+          top[l] = dtop;
+        }
+      } else {
+        need[l] -= s_below[l];
+        P[l] |= (u128)(u32)s_bin[l] << lo_b;
+        const u32 cnt = s_cntb[l];
+        top[l] = lo_b - 1;
+        if (cnt <= (u32)REF_STOP || top[l] < 0) {
+          act[l] = false;
+          fin_s[l] = lo_b;
+        }
       }
       __syncthreads();
     }
     // the buffer two rounds ahead was last read before this round's barrier
-    if (g == 0)
-      for (int i = tid; i < 512; i += bd) (&w->ref_hist[0][0][0])[((i >> 8) * 3 + (it + 2) % 3) * 256 + (i & 255)] = 0u;
+    if (g == 0) {
+      const int nb = (it + 2) % 3;
+      for (int i = tid; i < 512; i += bd) (&w->ref_hist[0][0][0])[((i >> 8) * 3 + nb) * 256 + (i & 255)] = 0u;
+      if (tid < 4) {
+        w->ref_gand[tid >> 1][nb][tid & 1] = ~0ull;
+        w->ref_gor[tid >> 1][nb][tid & 1] = 0ull;
+      }
+    }
     ++it;
   }
+  PTIME(56);
   // compaction: the keys at or below the bound, in any order (the walk sorts)
 #pragma unroll
   for (int l = 0; l < 2; ++l) {
@@ -556,6 +600,40 @@ __device__ void grid_refine(cg::grid_group& grid, Work* w, Bufs& b, bool on_w, b
     }
     w->ref_iters = it;
   }
+}
+
+// The victim list (<= REF_TRIG_V entries, or the refined list) in the
+// policy's reclaim order, by rank counting on the whole grid: every CTA
+// stages all keys in shared memory, each warp ranks one entry (keys are
+// unique) and the entry lands at its rank in the stream arrays (vs_*), the
+// first `cap` of them.  Called by every thread after the list is complete.
+__device__ void grid_rank_victims(Work* w, Bufs& b, bool ref_v, int cap, u64* sk /* smem */) {
+  const int n = ref_v ? __ldcg(&w->n_vr) : __ldcg(&w->n_vc);
+  const u64* kh = ref_v ? b.vr_key : b.vc_key;
+  const u64* kl = ref_v ? b.vr_kl : b.vc_kl;
+  const int m = n < 2 * VSTREAM_CAP ? n : 2 * VSTREAM_CAP;  // (the list never exceeds it)
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    sk[2 * i] = __ldcg(kh + i);
+    sk[2 * i + 1] = __ldcg(kl + i);
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (int i = gw; i < m; i += nw) {
+    const u64 h = sk[2 * i], l = sk[2 * i + 1];
+    int cnt = 0;
+    for (int j = lane; j < m; j += 32) cnt += key_lt(sk[2 * j], sk[2 * j + 1], h, l) ? 1 : 0;
+    const int r = __reduce_add_sync(FULL, cnt);
+    if (lane == 0 && r < cap) {
+      b.vs_key[r] = h;
+      b.vs_kl[r] = l;
+      b.vs_whi[r] = __ldcg((ref_v ? b.vr_whi : b.vc_whi) + i);
+      b.vs_wlo[r] = __ldcg((ref_v ? b.vr_wlo : b.vc_wlo) + i);
+      b.vs_row[r] = __ldcg((ref_v ? b.vr_row : b.vc_row) + i);
+      b.vs_blk[r] = __ldcg((ref_v ? b.vr_blk : b.vc_blk) + i);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) w->vs_on = m == n ? 1 : 0;
 }
 
 // k_scan staging: one round = SCAN_TPB consecutive rows (one per thread),
@@ -655,6 +733,13 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
   const i64 sc_total = sc->total_blocks, sc_free = sc->free_blocks;
   const double sc_usage = sc->kv_usage_ratio;
   const double ema = sc->has_ema_tool ? sc->ema_tool : c.tool_prior;
+  // The most blocks one plan can allocate: a block per decode slot plus the
+  // prefill chunks' blocks (sum of grants <= budget, one partial block per
+  // grant).  With that many blocks free before the step (expiry only adds to
+  // them) no claim can fail, the reclaimer never runs and the step needs no
+  // victim stream: the scan skips the victim digits and candidates.
+  const i64 alloc_bound = (i64)c.max_dec + ((i64)c.budget + c.bs - 1) / c.bs + c.window + 1;
+  const bool vic_on = sc_free < alloc_bound;
 
   long long exp_blocks = 0;
   int n_active = 0, n_queued = 0, n_long = 0, n_ready = 0, n_prom = 0, n_vic = 0, n_bnd = 0;
@@ -701,7 +786,7 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
           exp_blocks += pbk;
           n_exp++;
           rv = DIG_EXP;
-        } else if (vic_pin) {
+        } else if (vic_pin && vic_on) {
           rv = pin_reclaim_digit(c.policy, !exp_, B[SB_PL + lr], pbk, d, now);
           if (rv <= bv) atomicAdd(&hv[rv], 1u);
           n_vic++;
@@ -737,7 +822,7 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
           if (rw <= bw) atomicAdd(&hw[rw], 1u);
         }
         const i32 kvv = ((const i32*)(B + SB_KV))[lr];
-        if (kvv > 0) {
+        if (kvv > 0 && vic_on) {
           n_vic++;
           if (bv >= (1u << 11)) {  // running digits start at 1 << 11
             rv = run_reclaim_digit(c.policy, lv, held_blocks(c, kvv),
@@ -1061,10 +1146,7 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
     }
     __syncthreads();
     PTIME(41);
-    // (C) gathers; staged: records in shared memory, else straight to global.
-    // Lists that will be refined (phase 3) also fold every key into the
-    // AND / OR of the list: their common prefix, where the refinement starts.
-    u64 ka[2][2] = {{~0ull, ~0ull}, {~0ull, ~0ull}}, ko[2][2] = {{0ull, 0ull}, {0ull, 0ull}};
+    // (C) gathers; staged: records in shared memory, else straight to global
     for (int k = threadIdx.x; k < ntot; k += blockDim.x) {
       u32 r;
       if (staged) {
@@ -1099,10 +1181,6 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
           }
         }
         if (is_w) {
-          if (ref_w) {
-            ka[0][0] &= whi; ka[0][1] &= wlo;
-            ko[0][0] |= whi; ko[0][1] |= wlo;
-          }
           if (staged) {
             ((u64*)R)[0] = whi;
             ((u64*)R)[1] = wlo;
@@ -1122,10 +1200,6 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
             const i32 pbk = t.pb[r];
             pin_reclaim_key(c.policy, !(dl < now), (u32)t.plevel[r], pbk, dl, rk, vk, vkl);
             blk = pbk;
-          }
-          if (ref_v) {
-            ka[1][0] &= vk; ka[1][1] &= vkl;
-            ko[1][0] |= vk; ko[1][1] |= vkl;
           }
           if (staged) {
             ((u64*)R)[0] = vk;
@@ -1169,35 +1243,6 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
         if (staged) exp_rows[slot] = r;
       }
     }
-    if (ref_w || ref_v) {  // grid-uniform: the CTA's AND / OR -> the list's
-      __shared__ unsigned long long s_ka[2][2], s_ko[2][2];
-      if (threadIdx.x < 4) {
-        s_ka[threadIdx.x >> 1][threadIdx.x & 1] = ~0ull;
-        s_ko[threadIdx.x >> 1][threadIdx.x & 1] = 0ull;
-      }
-      __syncthreads();
-#pragma unroll
-      for (int l = 0; l < 2; ++l)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          u64 a = ka[l][h], o = ko[l][h];
-#pragma unroll
-          for (int q = 16; q > 0; q >>= 1) {
-            a &= __shfl_xor_sync(FULL, a, q);
-            o |= __shfl_xor_sync(FULL, o, q);
-          }
-          if (lane == 0) {
-            if (~a) atomicAnd(&s_ka[l][h], a);
-            if (o) atomicOr(&s_ko[l][h], o);
-          }
-        }
-      __syncthreads();
-      if (threadIdx.x < 4) {
-        const int l = threadIdx.x >> 1, h = threadIdx.x & 1;
-        if (~s_ka[l][h]) atomicAnd(&w->ref_and[l][h], s_ka[l][h]);
-        if (s_ko[l][h]) atomicOr(&w->ref_or[l][h], s_ko[l][h]);
-      }
-    }
     if (staged) {
       if (threadIdx.x == 0) {  // the reservations' results, first use
         s_base[0] = gb0;
@@ -1237,11 +1282,18 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
 
   // ---- phase 3: grid radix refinement (only when a candidate list is much
   // longer than its target: coarse digits over tied keys, or huge tables)
-  if (ref_w || ref_v) {
+  // the victim list (when the step may reclaim) is ranked grid-wide into the
+  // walk's stream order, so the single-CTA walk does not sort it
+  const bool vsort = vic_on && vu > 0u;
+  if (ref_w || ref_v || vsort) {
     grid.sync();
     PTIME(43);
-    grid_refine(grid, w, b, ref_w, ref_v, (int)c.window, VSEL);
+    if (ref_w || ref_v) grid_refine(grid, w, b, ref_w, ref_v, (int)c.window, VSEL);
     PTIME(44);
+    if (vsort) {
+      if (ref_v) grid.sync();  // the refined list is complete
+      grid_rank_victims(w, b, ref_v, c.stream_cap, (u64*)sdyn);
+    }
   }
 
   PTIME(4);
@@ -1261,6 +1313,7 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
   const mars_step_in in = w->in;
   w->t_win = gw;
   w->t_vic = gv;
+  w->vic_on = vic_on ? 1 : 0;
   w->n_win_cand_expected = (i32)wu;
   w->n_vic_cand_expected = (i32)vu;
   w->n_exp = n_exp_all;
@@ -2283,6 +2336,8 @@ struct VEnt {
   i32 blk;
   int16_t wi;   // window index or -1
   u8 pinned, dead;
+  u8 phase, flags;  // the row's phase and flags when the stream was built
+  i32 pre;          // and its preemption count
 };
 
 enum { REQ_NONE = 0, REQ_DONE = 1, REQ_SORT = 2, REQ_FULLSCAN = 3 };
@@ -2308,37 +2363,52 @@ struct WalkShared {
   int fast_ok;
 };
 
-__device__ __forceinline__ void jpush(Bufs& b, WalkShared& S, u8 op, u32 row, i32 n) {
-  int j = S.nj++;
+struct WalkReg {
+  int pass, idx, sub, ndec, npre, nev, nj, status, nwin;
+  int stream_first, stream_len, stream_ready, stream_complete;
+  long long total, freeb;
+};
+
+__device__ __forceinline__ void jpush(Bufs& b, WalkReg& R, u8 op, u32 row, i32 n) {
+  int j = R.nj++;
   if (j < b.j_cap) {
     b.j_op[j] = op;
     b.j_row[j] = row;
     b.j_n[j] = n;
   } else {
-    S.status |= ST_WALK_OVERFLOW;
+    R.status |= ST_WALK_OVERFLOW;
   }
 }
 
-// evict one victim (sim.py:168-188) -- thread 0 only
-__device__ void walk_evict(Tab& t, Bufs& b, WalkShared& S, u32 row, bool pinned, i32 blk) {
+// evict one victim (sim.py:168-188) -- thread 0 only.  Stream entries carry
+// the row's phase, flags and window index (gathered by the whole CTA when the
+// stream is built), so their eviction is stores only; the full-table
+// fallback's victims pass ph < 0 and are read here.
+__device__ void walk_evict(Tab& t, Bufs& b, WalkShared& S, WalkReg& R, u32 row, bool pinned, i32 blk,
+                           int ph = -1, int fl = 0, int wi = -2, int pre = 0) {
+  if (ph < 0) {
+    ph = t.phase[row];
+    fl = t.flags[row];
+    wi = t.winpos[row];
+    pre = t.pre[row];
+  }
   if (pinned) {
-    t.flags[row] = t.flags[row] & ~MARS_F_PINNED;
+    t.flags[row] = (u8)(fl & ~MARS_F_PINNED);
   } else {
-    t.pre[row] = t.pre[row] + 1;
-    if (t.phase[row] == MARS_DECODE) t.phase[row] = MARS_PREFILL;
+    t.pre[row] = pre + 1;  // (an atomic here would be a blocking round trip)
+    if (ph == MARS_DECODE) t.phase[row] = MARS_PREFILL;
   }
   t.kv[row] = 0;
-  S.freeb += blk;
-  int e = S.nev++;
+  R.freeb += blk;
+  int e = R.nev++;
   if (e < b.ev_cap) {
     b.ev_row[e] = row;
     b.ev_kind[e] = pinned ? 1 : 0;
     b.ev_blk[e] = blk;
   } else {
-    S.status |= ST_WALK_OVERFLOW;
+    R.status |= ST_WALK_OVERFLOW;
   }
-  jpush(b, S, pinned ? MARS_J_EVICT_PINNED : MARS_J_EVICT_RUNNING, row, blk);
-  int wi = t.winpos[row];
+  jpush(b, R, pinned ? MARS_J_EVICT_PINNED : MARS_J_EVICT_RUNNING, row, blk);
   if (wi >= 0) {
     S.wkv[wi] = 0;
     if (S.wph[wi] == MARS_DECODE) S.wph[wi] = MARS_PREFILL;
@@ -2361,25 +2431,25 @@ __device__ __forceinline__ bool run_eligible(const Cfg& c, const WalkShared& S, 
 }
 
 // claim_blocks (scheduler.py:313-324) via the MARS reclaimer -- thread 0
-__device__ int walk_claim(const Cfg& c, Tab& t, Bufs& b, WalkShared& S, VEnt* st, u32* fs_row,
+__device__ int walk_claim(const Cfg& c, Tab& t, Bufs& b, WalkShared& S, WalkReg& R, VEnt* st, u32* fs_row,
                           u8* fs_pin, i32* fs_blk, long long need, int bi) {
-  if (S.freeb >= need) return CL_TRUE;
+  if (R.freeb >= need) return CL_TRUE;
   if (S.fs_ready && S.fs_need == need && S.fs_b == bi) {
     S.fs_ready = 0;
     if (S.fs_n == 0) return CL_FALSE;
     for (int k = 0; k < S.fs_n; ++k) {
-      walk_evict(t, b, S, fs_row[k], fs_pin[k] != 0, fs_blk[k]);
-      for (int q = 0; q < S.stream_len; ++q)
+      walk_evict(t, b, S, R, fs_row[k], fs_pin[k] != 0, fs_blk[k]);
+      for (int q = 0; q < R.stream_len; ++q)
         if (st[q].row == fs_row[k]) st[q].dead = 1;
     }
-    return S.freeb >= need ? CL_TRUE : CL_FALSE;
+    return R.freeb >= need ? CL_TRUE : CL_FALSE;
   }
-  if (!S.stream_ready) return CL_NEED_SORT;
+  if (!R.stream_ready) return CL_NEED_SORT;
   // scan the stream prefix for the shortest sufficient eligible prefix
   long long freed = 0;
   int nch = 0;
   bool found = false;
-  for (int q = S.stream_first; q < S.stream_len; ++q) {
+  for (int q = R.stream_first; q < R.stream_len; ++q) {
     VEnt& e = st[q];
     if (e.dead) continue;
     if (!e.pinned) {
@@ -2389,7 +2459,7 @@ __device__ int walk_claim(const Cfg& c, Tab& t, Bufs& b, WalkShared& S, VEnt* st
     fs_row[nch] = (u32)q;  // temporarily stream indices
     nch++;
     freed += e.blk;
-    if (S.freeb + freed >= need) {
+    if (R.freeb + freed >= need) {
       found = true;
       break;
     }
@@ -2398,126 +2468,175 @@ __device__ int walk_claim(const Cfg& c, Tab& t, Bufs& b, WalkShared& S, VEnt* st
     for (int k = 0; k < nch; ++k) {
       VEnt& e = st[fs_row[k]];
       e.dead = 1;
-      walk_evict(t, b, S, e.row, e.pinned != 0, e.blk);
+      walk_evict(t, b, S, R, e.row, e.pinned != 0, e.blk, e.phase, e.flags, e.wi, e.pre);
     }
-    while (S.stream_first < S.stream_len && st[S.stream_first].dead) S.stream_first++;
+    while (R.stream_first < R.stream_len && st[R.stream_first].dead) R.stream_first++;
     return CL_TRUE;
   }
-  if (S.stream_complete) return CL_FALSE;  // reclaim_for returns [] (scheduler.py:267)
+  if (R.stream_complete) return CL_FALSE;  // reclaim_for returns [] (scheduler.py:267)
   S.fs_need = need;
   S.fs_b = bi;
   return CL_NEED_FULL;
 }
 
 // try_fit (scheduler.py:136-157) -- thread 0; allocates on success
-__device__ long long walk_try_fit(const Cfg& c, Bufs& b, WalkShared& S, int wi, long long desired) {
+__device__ long long walk_try_fit(const Cfg& c, Bufs& b, WalkShared& S, WalkReg& R, int wi, long long desired) {
   long long kvv = S.wkv[wi];
   long long held = blocks_ceil(c, kvv);
-  long long room = (held + S.freeb) * c.bs - kvv;
+  long long room = (held + R.freeb) * c.bs - kvv;
   long long g = desired <= room ? desired : blocks_floor_tokens(c, room);
   if (g < 1) return 0;
   long long need = blocks_ceil(c, kvv + g) - held;
   if (need > 0) {
-    S.freeb -= need;
-    jpush(b, S, MARS_J_ALLOC, S.wrow[wi], (i32)need);
+    R.freeb -= need;
+    jpush(b, R, MARS_J_ALLOC, S.wrow[wi], (i32)need);
   }
   return g;
 }
 
 // the sequential walk; returns a request code when it needs the whole CTA
-__device__ int walk_run(const Cfg& c, Tab& t, Bufs& b, WalkShared& S, VEnt* st, u32* fs_row,
-                        u8* fs_pin, i32* fs_blk) {
+__device__ int walk_run_r(const Cfg& c, Tab& t, Bufs& b, WalkShared& S, WalkReg& R, VEnt* st,
+                          u32* fs_row, u8* fs_pin, i32* fs_blk) {
   const long long budget = c.budget;
   while (true) {
-    if (S.pass == 0) {
-      if (S.idx >= S.nwin) {
-        S.pass = 1;
-        S.idx = 0;
-        S.sub = 0;
+    if (R.pass == 0) {
+      if (R.idx >= R.nwin) {
+        R.pass = 1;
+        R.idx = 0;
+        R.sub = 0;
         continue;
       }
-      int i = S.idx;
+      int i = R.idx;
       if (S.wph[i] != MARS_DECODE || S.wrem[i] < 1) {
-        S.idx++;
+        R.idx++;
         continue;
       }
-      if (S.total >= budget || S.ndec >= c.max_dec) {
-        S.idx++;
+      if (R.total >= budget || R.ndec >= c.max_dec) {
+        R.idx++;
         continue;
       }
       long long need = block_aligned(c, S.wkv[i]) ? 1 : 0;
       if (need > 0) {
-        int r = walk_claim(c, t, b, S, st, fs_row, fs_pin, fs_blk, need, i);
+        int r = walk_claim(c, t, b, S, R, st, fs_row, fs_pin, fs_blk, need, i);
         if (r == CL_NEED_SORT) return REQ_SORT;
         if (r == CL_NEED_FULL) return REQ_FULLSCAN;
         if (r == CL_FALSE) {
-          S.idx++;
+          R.idx++;
           continue;
         }
-        S.freeb -= need;
-        jpush(b, S, MARS_J_ALLOC, S.wrow[i], (i32)need);
+        R.freeb -= need;
+        jpush(b, R, MARS_J_ALLOC, S.wrow[i], (i32)need);
       }
-      b.dec_rows[S.ndec] = S.wrow[i];
-      S.ndec++;
+      b.dec_rows[R.ndec] = S.wrow[i];
+      R.ndec++;
       S.wplanned[i] = 1;
-      S.total += 1;
-      S.idx++;
+      R.total += 1;
+      R.idx++;
     } else {
-      if (S.idx >= S.nwin) return REQ_DONE;
-      int i = S.idx;
+      if (R.idx >= R.nwin) return REQ_DONE;
+      int i = R.idx;
       if (S.wph[i] != MARS_PREFILL) {
-        S.idx++;
+        R.idx++;
         continue;
       }
-      long long left = budget - S.total;
+      long long left = budget - R.total;
       if (left < 1) return REQ_DONE;
       long long rp = (long long)S.wctx[i] - S.wkv[i];
       long long desired = rp < left ? rp : left;
       if (desired < 1) {
-        S.idx++;
+        R.idx++;
         continue;
       }
       long long g = 0;
       long long kvv = S.wkv[i];
       long long incr = blocks_ceil(c, kvv + desired) - blocks_ceil(c, kvv);
       if (c.cosched) {
-        if (S.sub == 0) {
-          g = walk_try_fit(c, b, S, i, desired);
-          if (g == 0) S.sub = 1;
+        if (R.sub == 0) {
+          g = walk_try_fit(c, b, S, R, i, desired);
+          if (g == 0) R.sub = 1;
         }
-        if (S.sub == 1) {
-          int r = walk_claim(c, t, b, S, st, fs_row, fs_pin, fs_blk, incr, i);
+        if (R.sub == 1) {
+          int r = walk_claim(c, t, b, S, R, st, fs_row, fs_pin, fs_blk, incr, i);
           if (r == CL_NEED_SORT) return REQ_SORT;
           if (r == CL_NEED_FULL) return REQ_FULLSCAN;
-          S.sub = 0;
-          g = (r == CL_TRUE) ? walk_try_fit(c, b, S, i, desired) : 0;
+          R.sub = 0;
+          g = (r == CL_TRUE) ? walk_try_fit(c, b, S, R, i, desired) : 0;
         }
       } else {
         if (incr == 0) {
           g = desired;
         } else {
-          int r = walk_claim(c, t, b, S, st, fs_row, fs_pin, fs_blk, incr, i);
+          int r = walk_claim(c, t, b, S, R, st, fs_row, fs_pin, fs_blk, incr, i);
           if (r == CL_NEED_SORT) return REQ_SORT;
           if (r == CL_NEED_FULL) return REQ_FULLSCAN;
           if (r == CL_TRUE) {
-            S.freeb -= incr;
-            jpush(b, S, MARS_J_ALLOC, S.wrow[i], (i32)incr);
+            R.freeb -= incr;
+            jpush(b, R, MARS_J_ALLOC, S.wrow[i], (i32)incr);
             g = desired;
           }
         }
       }
       if (g > 0) {
-        b.pre_rows[S.npre] = S.wrow[i];
-        b.pre_grant[S.npre] = (i32)g;
-        S.npre++;
+        b.pre_rows[R.npre] = S.wrow[i];
+        b.pre_grant[R.npre] = (i32)g;
+        R.npre++;
         S.wplanned[i] = 1;
-        S.total += g;
+        R.total += g;
       } else if (c.strict) {
         return REQ_DONE;  // head-of-line blocking (scheduler.py:369-370)
       }
-      S.idx++;
+      R.idx++;
     }
   }
+}
+
+
+// The walk's scalar state lives in thread 0's registers while it runs (every
+// field of WalkShared is a shared-memory round trip, and the claim / evict /
+// journal chain is strictly sequential); it is written back whenever the walk
+// hands control to the whole CTA (stream sort, full-table search) or ends.
+__device__ __forceinline__ void wreg_load(WalkReg& R, const WalkShared& S) {
+  R.pass = S.pass;
+  R.idx = S.idx;
+  R.sub = S.sub;
+  R.ndec = S.ndec;
+  R.npre = S.npre;
+  R.nev = S.nev;
+  R.nj = S.nj;
+  R.status = S.status;
+  R.nwin = S.nwin;
+  R.stream_first = S.stream_first;
+  R.stream_len = S.stream_len;
+  R.stream_ready = S.stream_ready;
+  R.stream_complete = S.stream_complete;
+  R.total = S.total;
+  R.freeb = S.freeb;
+}
+__device__ __forceinline__ void wreg_store(WalkShared& S, const WalkReg& R) {
+  S.pass = R.pass;
+  S.idx = R.idx;
+  S.sub = R.sub;
+  S.ndec = R.ndec;
+  S.npre = R.npre;
+  S.nev = R.nev;
+  S.nj = R.nj;
+  S.status = R.status;
+  S.nwin = R.nwin;
+  S.stream_first = R.stream_first;
+  S.stream_len = R.stream_len;
+  S.stream_ready = R.stream_ready;
+  S.stream_complete = R.stream_complete;
+  S.total = R.total;
+  S.freeb = R.freeb;
+}
+
+__device__ int walk_run(const Cfg& c, Tab& t, Bufs& b, WalkShared& S, VEnt* st, u32* fs_row,
+                        u8* fs_pin, i32* fs_blk) {
+  WalkReg R;
+  wreg_load(R, S);
+  const int rq = walk_run_r(c, t, b, S, R, st, fs_row, fs_pin, fs_blk);
+  wreg_store(S, R);
+  return rq;
 }
 
 // Row r's place in the policy's reclaim order, if it is an eligible victim
@@ -2957,6 +3076,198 @@ __device__ int cta_select_sorted(const u64* ghi, const u64* glo, const u32* gpay
   return m < k ? m : k;
 }
 
+// The victim stream (whole CTA): the policy's reclaim-order prefix k_scan
+// selected (refined: the exact top VSEL plus < REF_STOP), sorted by the
+// 128-bit key, with each entry's row state gathered once (phase, flags,
+// window index) so that evicting it is stores only.
+__device__ void walk_build_stream(const Cfg& c, Tab& t, Work* w, Bufs& b, WalkShared& S, VEnt* st,
+                                  u64* kh, u64* kl, u32* pv, u32* hist) {
+  PTIME(38);
+  const bool ref_v = w->ref_on[1] != 0;
+  const int nvc = ref_v ? w->n_vr : w->n_vc;
+  const bool presorted = w->vs_on != 0;  // k_scan ranked the candidates (grid-wide)
+  const u64* vkh = presorted ? b.vs_key : (ref_v ? b.vr_key : b.vc_key);
+  const u64* vkl = presorted ? b.vs_kl : (ref_v ? b.vr_kl : b.vc_kl);
+  int len;
+  if (presorted) {
+    len = nvc < c.stream_cap ? nvc : c.stream_cap;
+  } else {
+    len = cta_select_sorted(vkh, vkl, nullptr, nvc, c.stream_cap, kh, kl, pv, hist);
+    __syncthreads();
+  }
+  PTIME(57);
+  const u64* vwh = presorted ? b.vs_whi : (ref_v ? b.vr_whi : b.vc_whi);
+  const u64* vwl = presorted ? b.vs_wlo : (ref_v ? b.vr_wlo : b.vc_wlo);
+  const u32* vrw = presorted ? b.vs_row : (ref_v ? b.vr_row : b.vc_row);
+  const i32* vbk = presorted ? b.vs_blk : (ref_v ? b.vr_blk : b.vc_blk);
+  for (int q = threadIdx.x; q < len; q += blockDim.x) {
+    const u32 ci = presorted ? (u32)q : pv[q];
+    VEnt e;
+    e.key = presorted ? vkh[q] : kh[q];
+    e.kl = presorted ? vkl[q] : kl[q];
+    e.whi = vwh[ci];
+    e.wlo = vwl[ci];
+    e.row = vrw[ci];
+    e.blk = vbk[ci];
+    e.pinned = (e.key >> 63) == 0;
+    e.dead = 0;
+    e.wi = t.winpos[e.row];
+    e.phase = t.phase[e.row];
+    e.flags = t.flags[e.row];
+    e.pre = t.pre[e.row];
+    st[q] = e;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    S.stream_ready = 1;
+    S.stream_len = len;
+    S.stream_first = 0;
+    // the stream holds every potential victim of the step
+    S.stream_complete = (len == nvc && nvc == w->n_victims) ? 1 : 0;
+  }
+  __syncthreads();
+  PTIME(39);
+}
+
+// build_plan's decode pass with its claims (scheduler.py:326-341, claim_blocks
+// :313-324) on the whole CTA.  The pass selects the first min(max_decode,
+// budget) decode-ready window rows, each allocating one block when its KV is
+// block aligned; a claim evicts the shortest prefix of the eligible reclaim
+// order that covers the shortfall.  When every stream entry those claims
+// consume is outside the window and eligible for the last claiming decode
+// (eligibility only narrows along the window order), the claims are plain
+// prefix sums: with B(v) the blocks of the first v stream entries and N_i the
+// block needs through decode i, decode i's claim evicts the entries
+// [v(N_i - 1), v(N_i)) where v(x) = min{v : free + B(v) >= x}, and the journal
+// interleaves them with the allocations in the same order the sequential walk
+// would.  Otherwise (a window row among them, a tie-ineligible entry, a short
+// stream) nothing is touched and the sequential walk runs the pass.
+__device__ void walk_decode_claims(const Cfg& c, Tab& t, Bufs& b, WalkShared& S, VEnt* st,
+                                   long long* B /* [len + 1] */) {
+  __shared__ int s_e[4], s_n[4], s_s[4];
+  __shared__ int s_ilast, s_vstar, s_ok;
+  __shared__ long long s_wsum[32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const u32 lt = (1u << lane) - 1u;
+  const int nwin = S.nwin, len = S.stream_len;
+  const long long free0 = S.freeb;
+  const long long lim_dec = c.max_dec < c.budget ? c.max_dec : c.budget;
+  const bool win = tid < WIN_MAX && tid < nwin;
+  const bool e = win && S.wph[tid] == MARS_DECODE && S.wrem[tid] >= 1;
+  const u32 me = __ballot_sync(FULL, e);
+  if (tid < WIN_MAX && lane == 0) s_e[wid] = __popc(me);
+  if (tid == 0) {
+    s_ilast = -1;
+    s_vstar = 0;
+    s_ok = 1;
+  }
+  __syncthreads();
+  int eb = 0;
+  if (tid < WIN_MAX)
+    for (int k = 0; k < wid; ++k) eb += s_e[k];
+  const bool sel = e && (eb + __popc(me & lt)) < lim_dec;
+  const bool dn = sel && block_aligned(c, S.wkv[tid]);
+  const u32 ms = __ballot_sync(FULL, sel), mn = __ballot_sync(FULL, dn);
+  if (tid < WIN_MAX && lane == 0) {
+    s_s[wid] = __popc(ms);
+    s_n[wid] = __popc(mn);
+  }
+  __syncthreads();
+  int sb = 0, nb = 0, Nd = 0, nsel = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const bool before = tid < WIN_MAX && k < wid;
+    sb += before ? s_s[k] : 0;
+    nb += before ? s_n[k] : 0;
+    Nd += s_n[k];
+    nsel += s_s[k];
+  }
+  const int Ni = nb + __popc(mn & lt) + (dn ? 1 : 0);  // needs through this decode
+  if (dn && Ni == Nd) s_ilast = tid;                      // the last claiming beneficiary
+  // stream prefix sums B(v) (no entry is dead yet)
+  const long long blk = tid < len ? (long long)st[tid].blk : 0;
+  long long incl = blk;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long x = __shfl_up_sync(FULL, incl, o);
+    if (lane >= o) incl += x;
+  }
+  if (lane == 31) s_wsum[wid] = incl;
+  __syncthreads();
+  for (int k = 0; k < wid; ++k) incl += s_wsum[k];
+  if (tid < len) B[tid + 1] = incl;
+  if (tid == 0) B[0] = 0;
+  const long long need_total = (long long)Nd - free0;  // blocks the claims must free
+  if (need_total > 0 && tid < len && incl - blk < need_total && incl >= need_total)
+    s_vstar = tid + 1;
+  __syncthreads();
+  const int vstar = s_vstar;
+  if (need_total > 0 && vstar == 0) s_ok = 0;  // the stream cannot cover the pass
+  __syncthreads();
+  if (!s_ok) return;
+  // every consumed entry: outside the window, eligible for the last claimer
+  bool good = true;
+  if (tid < vstar) {
+    const VEnt& v = st[tid];
+    good = v.wi < 0 && !v.dead && v.blk > 0 &&
+           (v.pinned || run_eligible(c, S, v.row, v.whi, v.wlo, v.wi, s_ilast));
+  }
+  if (!__syncthreads_and(good)) return;
+  PTIME(58);
+  // apply: decodes, their claims' evictions and the interleaved journal
+  if (sel) {
+    b.dec_rows[sb + __popc(ms & lt)] = S.wrow[tid];
+    S.wplanned[tid] = 1;
+  }
+  if (dn) {
+    auto vof = [&](long long x) {  // min{v in [0, vstar] : free0 + B(v) >= x}
+      int lo = 0, hi = vstar;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (free0 + B[mid] >= x) hi = mid; else lo = mid + 1;
+      }
+      return lo;
+    };
+    const int v1 = vof(Ni), v0 = vof(Ni - 1);
+    for (int q = v0; q < v1; ++q) {
+      VEnt& v = st[q];
+      v.dead = 1;
+      const u32 r = v.row;
+      if (v.pinned) {
+        t.flags[r] = (u8)(v.flags & ~MARS_F_PINNED);
+      } else {
+        t.pre[r] = v.pre + 1;
+        if (v.phase == MARS_DECODE) t.phase[r] = MARS_PREFILL;
+      }
+      t.kv[r] = 0;
+      b.ev_row[q] = r;
+      b.ev_kind[q] = v.pinned ? 1 : 0;
+      b.ev_blk[q] = v.blk;
+      const int js = q + Ni - 1;
+      b.j_op[js] = v.pinned ? MARS_J_EVICT_PINNED : MARS_J_EVICT_RUNNING;
+      b.j_row[js] = r;
+      b.j_n[js] = v.blk;
+    }
+    const int ja = v1 + Ni - 1;
+    b.j_op[ja] = MARS_J_ALLOC;
+    b.j_row[ja] = S.wrow[tid];
+    b.j_n[ja] = 1;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    S.ndec = nsel;
+    S.total = nsel;
+    S.freeb = free0 + B[vstar] - Nd;
+    S.nev = vstar;
+    S.nj = vstar + Nd;
+    S.stream_first = vstar;
+    S.pass = 1;
+    S.idx = 0;
+    S.sub = 0;
+  }
+  __syncthreads();
+}
+
 __global__ void __launch_bounds__(WALK_TPB) k_walk(Tab t, Cfg c, Work* w, Bufs b,
                                                    mars_scalars* sc, i64 n_rows,
                                                    int admit_async) {
@@ -3050,6 +3361,13 @@ __global__ void __launch_bounds__(WALK_TPB) k_walk(Tab t, Cfg c, Work* w, Bufs b
     S.fs_ready = 0;
     S.status = 0;
     S.fast_ok = 0;
+    if (!w->vic_on) {
+      // the free pool covers every allocation a plan can make, so k_scan built
+      // no victim stream; a claim cannot fail (were one to, the exact
+      // full-table reclaimer would serve it)
+      S.stream_ready = 1;
+      S.stream_complete = 0;
+    }
   }
   __syncthreads();
   PTIME(17);
@@ -3183,56 +3501,28 @@ __global__ void __launch_bounds__(WALK_TPB) k_walk(Tab t, Cfg c, Work* w, Bufs b
   __syncthreads();
   PTIME(20);
 
-  // 3. sequential walk with on-demand help from the whole CTA
+  // 3. the victim stream and the decode pass with its claims on the whole
+  //    CTA, then the sequential walk (the prefill pass, or everything when the
+  //    parallel decode pass does not apply) with on-demand help from the CTA
   if (!S.fast_ok) {
+    if (!S.stream_ready) {
+      walk_build_stream(c, t, w, b, S, st, kh, kl, pv, hist);
+      walk_decode_claims(c, t, b, S, st, (long long*)kh);
+    }
     while (true) {
       if (threadIdx.x == 0) S.request = walk_run(c, t, b, S, st, fs_row, fs_pin, fs_blk);
       __syncthreads();
       int rq = S.request;
       if (rq == REQ_DONE) break;
       if (rq == REQ_SORT) {
-        // victim stream: the policy's reclaim-order prefix k_scan selected
-        // (refined: the exact top VSEL plus < REF_STOP), sorted by the
-        // 128-bit key; payload = candidate index
-        const bool ref_v = w->ref_on[1] != 0;
-        const int nvc = ref_v ? w->n_vr : w->n_vc;
-        const u64* vkh = ref_v ? b.vr_key : b.vc_key;
-        const u64* vkl = ref_v ? b.vr_kl : b.vc_kl;
-        const int len = cta_select_sorted(vkh, vkl, nullptr, nvc, c.stream_cap, kh, kl, pv, hist);
-        __syncthreads();
-        const u64* vwh = ref_v ? b.vr_whi : b.vc_whi;
-        const u64* vwl = ref_v ? b.vr_wlo : b.vc_wlo;
-        const u32* vrw = ref_v ? b.vr_row : b.vc_row;
-        const i32* vbk = ref_v ? b.vr_blk : b.vc_blk;
-        for (int q = threadIdx.x; q < len; q += blockDim.x) {
-          const u32 ci = pv[q];
-          VEnt e;
-          e.key = kh[q];
-          e.kl = kl[q];
-          e.whi = vwh[ci];
-          e.wlo = vwl[ci];
-          e.row = vrw[ci];
-          e.blk = vbk[ci];
-          e.pinned = (e.key >> 63) == 0;
-          e.dead = 0;
-          e.wi = t.winpos[e.row];
-          st[q] = e;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-          S.stream_ready = 1;
-          S.stream_len = len;
-          S.stream_first = 0;
-          // the stream holds every potential victim of the step
-          S.stream_complete = (len == nvc && nvc == w->n_victims) ? 1 : 0;
-        }
-        __syncthreads();
+        walk_build_stream(c, t, w, b, S, st, kh, kl, pv, hist);
       } else if (rq == REQ_FULLSCAN) {
         if (threadIdx.x == 0) w->n_fullscan += 1;
         walk_fullscan(c, t, S, n_rows, now, fs_row, fs_pin, fs_blk);
       }
     }
   }
+  PTIME(18);
   __syncthreads();
 
   // 4. drop-in epilogues on the planned rows: charge_service at tick end
@@ -3558,7 +3848,7 @@ __global__ void __launch_bounds__(1024) k_work_init(Work* w, const mars_step_in*
     static_assert(sizeof(mars_step_in) % 4 == 0, "step_in is word-sized");
     for (size_t i = threadIdx.x; i < sizeof(mars_step_in) / 4; i += blockDim.x) dst[i] = src[i];
   }
-  if (threadIdx.x < 4) (&w->ref_and[0][0])[threadIdx.x] = ~0ull;
+  if (threadIdx.x < 12) (&w->ref_gand[0][0][0])[threadIdx.x] = ~0ull;
   if (threadIdx.x == 0) {
     w->tmin_win = 0xffffffffu;
     w->tmin_vic = 0xffffffffu;

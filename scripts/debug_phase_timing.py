@@ -10,15 +10,21 @@ from paper_2604_26963_b200.engine import MarsEngine, make_config  # noqa: E402
 from paper_2604_26963_b200.snapshot import snapshot_v1  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000
-snap = snapshot_v1(n, seed=0)
-eng = MarsEngine(max_rows=snap.n, max_queue=len(snap.queue),
-                 config=make_config(initial_window=snap.initial_window))
+variant = sys.argv[2] if len(sys.argv) > 2 else "headroom"
+policy = sys.argv[3] if len(sys.argv) > 3 else "mars"
+if variant == "headroom":
+    snap = snapshot_v1(n, seed=0)
+else:
+    from tests._variants import reclaim_heavy
+    snap = reclaim_heavy(n, 91, policy)
+eng = MarsEngine(max_rows=snap.n, max_queue=max(len(snap.queue), 1),
+                 config=make_config(initial_window=snap.initial_window, policy=policy))
 stream = torch.cuda.Stream()
 torch.cuda.set_stream(stream)
 eng.lib.mars_set_stream(eng.ctx, stream.cuda_stream)
 eng.load_snapshot(snap)
 eng.checkpoint()
-si = eng.step_in(snap.now, True, snap.active_tools, 0, snap.worker_slots)
+si = eng.step_in(snap.now, policy == 'mars', snap.active_tools, 0, snap.worker_slots)
 eng.set_profiling(True)
 for it in range(4):
     eng.restore()
