@@ -309,8 +309,13 @@ typedef struct mars_kv_config {
 int mars_kv_init(mars_ctx* ctx, const mars_kv_config* cfg);
 int mars_kv_apply(mars_ctx* ctx, int64_t n_ops, const uint8_t* op, const uint32_t* row,
                   const int32_t* n);                                              /* sync */
+/* initial tables from a fresh pool (no free segment yet): row[i] (distinct)
+ * gets the next cnt[i] never-used IDs, as cnt[i] sequential allocs in list
+ * order would (the bench's 1M-session tables) */
+int mars_kv_bulk_alloc(mars_ctx* ctx, int64_t n, const uint32_t* row, const int32_t* cnt); /* sync */
 int mars_kv_table(mars_ctx* ctx, uint32_t row, int64_t cap, uint32_t* ids, int64_t* n); /* sync */
-/* next `k` IDs the stack would pop, plus its depth (explicit, fresh) */
+/* next `k` IDs the stack would pop (UINT32_MAX past the last free block),
+ * plus its depth (IDs on the explicit stack, next fresh ID) */
 int mars_kv_state(mars_ctx* ctx, int64_t k, uint32_t* top_ids, int64_t* explicit_depth,
                   int64_t* fresh, int32_t* status);                               /* sync */
 /* evict (HBM -> host slots [slot0, slot0+n)) / restore (host -> HBM) block data.
@@ -347,7 +352,8 @@ int mars_last_launch_count(mars_ctx* ctx);
 /* per-kernel device times of the last step, recorded with CUDA events on the
  * stream each kernel runs on: [scan, expired-sort, control, walk] in ms
  * (-1 = not launched).  Profiling must be enabled before the step. */
-#define MARS_NUM_KTIMES 5  /* k_scan, expired sort, k_control, k_walk, k_pack */
+#define MARS_NUM_KTIMES 7  /* k_scan, expired sort, k_control, k_walk, k_pack,
+                              S5 expired-pin frees (k_kv_exp_*), S5 journal (k_kv_apply_step) */
 int mars_set_profiling(mars_ctx* ctx, int on);
 int mars_kernel_times(mars_ctx* ctx, float* ms, int n);   /* sync */
 

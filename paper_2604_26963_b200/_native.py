@@ -148,6 +148,7 @@ _SIGS = {
     "mars_kv_init": (i32, [C.c_void_p, C.c_void_p]),
     "mars_kv_apply": (i32, [C.c_void_p, i64, C.c_void_p, C.c_void_p, C.c_void_p]),
     "mars_kv_table": (i32, [C.c_void_p, u32, i64, C.c_void_p, P(i64)]),
+    "mars_kv_bulk_alloc": (i32, [C.c_void_p, i64, C.c_void_p, C.c_void_p]),
     "mars_kv_state": (i32, [C.c_void_p, i64, C.c_void_p, P(i64), P(i64), P(i32)]),
     "mars_kv_evict": (i32, [C.c_void_p, i64, C.c_void_p, i64, C.c_int]),
     "mars_kv_restore": (i32, [C.c_void_p, i64, C.c_void_p, i64, C.c_int]),
@@ -168,7 +169,8 @@ _SIGS = {
     "mars_kernel_times": (i32, [C.c_void_p, P(C.c_float), C.c_int]),
 }
 
-KTIME_NAMES = ("k_scan", "k_expired_sort", "k_control", "k_walk", "k_pack")
+KTIME_NAMES = ("k_scan", "k_expired_sort", "k_control", "k_walk", "k_pack", "k_kv_exp_free",
+               "k_kv_apply_step")
 
 EXPORTS = tuple(_SIGS)
 

@@ -33,6 +33,7 @@ struct mars_ctx {
   i64 last_resume_n = 0;
   bool own_stream = true;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_head = nullptr, ev_pack = nullptr;
+  cudaEvent_t ev_kvfork = nullptr, ev_kvjoin = nullptr;
   int pack_ctas = 20;
   mars_config hcfg;
   Cfg cfg;
@@ -85,6 +86,8 @@ struct mars_ctx {
   std::string err;
   // S5 block manager + host tier (mars_kv_init)
   bool kv_on = false;
+  void* ck_kv[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  bool have_kv_ckpt = false;
   Kv kv = {};
   void* kv_host = nullptr;          // pinned, mapped
   unsigned char* kv_stage = nullptr; // device staging for op streams / ids
@@ -269,6 +272,8 @@ int mars_create(const mars_config* hcfg, int device, int64_t max_rows, int64_t m
   CK(cudaStreamCreateWithFlags(&ctx->side2, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&ctx->ev_head, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&ctx->ev_pack, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ctx->ev_kvfork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ctx->ev_kvjoin, cudaEventDisableTiming));
   {
     const char* e = getenv("MARS_PACK_CTAS");  // tuning knob: 0 disables the early pack
     if (e) ctx->pack_ctas = atoi(e);
@@ -479,6 +484,7 @@ int mars_destroy(mars_ctx* ctx) {
   for (auto& cs : ctx->cols) cudaFree(cs.ckpt);
   for (void* p : ctx->ck_q) cudaFree(p);
   cudaFree(ctx->ck_sc);
+  for (void* p : ctx->ck_kv) cudaFree(p);
   cudaFree(ctx->ck_qsel);
   cudaFreeHost(ctx->h_in);
   cudaFreeHost(ctx->h_work);
@@ -486,7 +492,8 @@ int mars_destroy(mars_ctx* ctx) {
   cudaFreeHost(ctx->h_out);
   {
     Kv& k = ctx->kv;
-    void* kp[] = {k.fs, k.chunks, k.cfs, k.dir, k.len, k.s, k.data, ctx->kv_stage, ctx->kv_dstage};
+    void* kp[] = {k.seg, k.chunks, k.cfs, k.dir, k.len, k.s, k.data, ctx->kv_stage,
+                  ctx->kv_dstage, k.xoff, k.xlen, k.xbase, k.arena, k.xaoff, k.xroff};
     for (void* p : kp) cudaFree(p);
     if (ctx->kv_host) cudaFreeHost(ctx->kv_host);
   }
@@ -503,6 +510,8 @@ int mars_destroy(mars_ctx* ctx) {
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->ev_head) cudaEventDestroy(ctx->ev_head);
   if (ctx->ev_pack) cudaEventDestroy(ctx->ev_pack);
+  if (ctx->ev_kvfork) cudaEventDestroy(ctx->ev_kvfork);
+  if (ctx->ev_kvjoin) cudaEventDestroy(ctx->ev_kvjoin);
   if (ctx->side2) cudaStreamDestroy(ctx->side2);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->side) cudaStreamDestroy(ctx->side);
@@ -656,6 +665,8 @@ static LaunchArgs launch_args(mars_ctx* ctx, const mars_step_in* in) {
   a.side2 = ctx->side2;
   a.ev_head = ctx->ev_head;
   a.ev_pack = ctx->ev_pack;
+  a.ev_kvfork = ctx->ev_kvfork;
+  a.ev_kvjoin = ctx->ev_kvjoin;
   a.tab = ctx->tab;
   a.cfg = ctx->cfg;
   a.work = ctx->work;
@@ -1136,6 +1147,18 @@ int mars_checkpoint(mars_ctx* ctx) {
   if (!ctx->ck_qsel) CK(cudaMalloc((void**)&ctx->ck_qsel, sizeof(i32)));
   CK(cudaMemcpyAsync(ctx->ck_sc, ctx->sc, sizeof(mars_scalars), cudaMemcpyDeviceToDevice, ctx->stream));
   CK(cudaMemcpyAsync(ctx->ck_qsel, ctx->qsel, sizeof(i32), cudaMemcpyDeviceToDevice, ctx->stream));
+  if (ctx->kv_on) {  // the block manager's state with the table
+    Kv& k = ctx->kv;
+    const size_t kb[7] = {(size_t)k.rows * 4, (size_t)k.rows * k.D * 4,
+                          (size_t)k.nchunks * KV_CH * 4, (size_t)k.seg_cap * 8,
+                          (size_t)k.nchunks * 4, sizeof(KvScal), (size_t)k.total * 4};
+    void* kp[7] = {k.len, k.dir, k.chunks, k.seg, k.cfs, k.s, k.arena};
+    for (int i = 0; i < 7; ++i) {
+      if (!ctx->ck_kv[i]) CK(cudaMalloc(&ctx->ck_kv[i], kb[i]));
+      CK(cudaMemcpyAsync(ctx->ck_kv[i], kp[i], kb[i], cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    ctx->have_kv_ckpt = true;
+  }
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->ck_q_upper = ctx->q_upper;
   ctx->ck_q_maxreq = ctx->q_maxreq;
@@ -1161,6 +1184,15 @@ int mars_restore(mars_ctx* ctx) {
   CK(cudaMemcpyAsync(ctx->qsel, ctx->ck_qsel, sizeof(i32), cudaMemcpyDeviceToDevice, ctx->stream));
   ctx->q_upper = ctx->ck_q_upper;
   ctx->q_maxreq = ctx->ck_q_maxreq;
+  if (ctx->kv_on && ctx->have_kv_ckpt) {
+    Kv& k = ctx->kv;
+    const size_t kb[7] = {(size_t)k.rows * 4, (size_t)k.rows * k.D * 4,
+                          (size_t)k.nchunks * KV_CH * 4, (size_t)k.seg_cap * 8,
+                          (size_t)k.nchunks * 4, sizeof(KvScal), (size_t)k.total * 4};
+    void* kp[7] = {k.len, k.dir, k.chunks, k.seg, k.cfs, k.s, k.arena};
+    for (int i = 0; i < 7; ++i)
+      CK(cudaMemcpyAsync(kp[i], ctx->ck_kv[i], kb[i], cudaMemcpyDeviceToDevice, ctx->stream));
+  }
   return MARS_OK;
 }
 
@@ -1233,12 +1265,20 @@ int mars_kv_init(mars_ctx* ctx, const mars_kv_config* kc) {
   k.total = kc->total_blocks;
   k.D = (kc->max_blocks_per_row + KV_CH - 1) / KV_CH;
   k.rows = ctx->alloc_rows;
-  k.nchunks = (k.total + KV_CH - 1) / KV_CH + k.rows;
+  // table chunks (<= total/64 + rows) plus whole chunks on the free stack
+  k.nchunks = 2 * ((k.total + KV_CH - 1) / KV_CH) + k.rows + 64;
+  k.seg_cap = (k.total + KV_CH - 1) / KV_CH + 4 * k.rows + 65536;
   k.layers = layers;
   k.block_bytes = kc->block_bytes;
   k.host_blocks = kc->host_blocks;
-  CK(cudaMalloc((void**)&k.fs, (size_t)k.total * 4));
+  CK(cudaMalloc((void**)&k.seg, (size_t)k.seg_cap * 8));
+  CK(cudaMalloc((void**)&k.arena, (size_t)k.total * 4));
+  CK(cudaMalloc((void**)&k.xaoff, (size_t)k.rows * 8));
+  CK(cudaMalloc((void**)&k.xroff, (size_t)k.rows * 8));
   CK(cudaMalloc((void**)&k.chunks, (size_t)k.nchunks * KV_CH * 4));
+  CK(cudaMalloc((void**)&k.xoff, (size_t)k.rows * 8));
+  CK(cudaMalloc((void**)&k.xlen, (size_t)k.rows * 4));
+  CK(cudaMalloc((void**)&k.xbase, 32));
   CK(cudaMalloc((void**)&k.cfs, (size_t)k.nchunks * 4));
   CK(cudaMalloc((void**)&k.dir, (size_t)k.rows * k.D * 4));
   CK(cudaMalloc((void**)&k.len, (size_t)k.rows * 4));
@@ -1249,7 +1289,7 @@ int mars_kv_init(mars_ctx* ctx, const mars_kv_config* kc) {
     for (i64 i = 0; i < k.nchunks; ++i) iota[i] = (u32)(k.nchunks - 1 - i);  // pops 0,1,2,..
     CK(cudaMemcpy(k.cfs, iota.data(), (size_t)k.nchunks * 4, cudaMemcpyHostToDevice));
   }
-  KvScal s0 = {0, 0, k.nchunks, 0};
+  KvScal s0 = {0, 0, 0, 0, k.nchunks, 0};
   CK(cudaMemcpy(k.s, &s0, sizeof s0, cudaMemcpyHostToDevice));
   if (k.block_bytes > 0) {
     CK(cudaMalloc((void**)&k.data, (size_t)k.total * k.block_bytes));
@@ -1289,6 +1329,36 @@ int mars_kv_apply(mars_ctx* ctx, int64_t n, const uint8_t* op, const uint32_t* r
   return MARS_OK;
 }
 
+int mars_kv_bulk_alloc(mars_ctx* ctx, int64_t n, const uint32_t* row, const int32_t* cnt) {
+  if (!ctx || n < 0) return MARS_ERR_ARG;
+  if (!ctx->kv_on) return fail(ctx, MARS_ERR_ARG, "kv manager not initialised");
+  if (n == 0) return MARS_OK;
+  for (int64_t i = 0; i < n; ++i) {
+    if ((i64)row[i] >= ctx->kv.rows) return fail(ctx, MARS_ERR_CAPACITY, "kv row out of range");
+    if (cnt[i] < 0) return fail(ctx, MARS_ERR_ARG, "negative block count");
+  }
+  {  // rows must be distinct (each row's IDs are one contiguous fresh range)
+    std::vector<uint32_t> r(row, row + n);
+    std::sort(r.begin(), r.end());
+    if (std::adjacent_find(r.begin(), r.end()) != r.end())
+      return fail(ctx, MARS_ERR_ARG, "bulk alloc rows must be distinct");
+  }
+  CK(cudaSetDevice(ctx->device));
+  int rc = kv_stage(ctx, n * 8 + 64);
+  if (rc) return rc;
+  u32* drow = (u32*)ctx->kv_stage;
+  i32* dn = (i32*)(drow + n);
+  CK(cudaMemcpyAsync(drow, row, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(dn, cnt, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+  rc = mars_kv_enqueue_bulk(ctx->kv, ctx->stream, n, drow, dn, ctx->num_sms * 8);
+  if (rc) return fail(ctx, MARS_ERR_CUDA, "kv bulk: %s", cudaGetErrorString((cudaError_t)rc));
+  KvScal s;
+  CK(cudaMemcpyAsync(&s, ctx->kv.s, sizeof s, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (s.status) return fail(ctx, MARS_ERR_CONTRACT, "kv bulk alloc needs a fresh pool (status %d)", s.status);
+  return MARS_OK;
+}
+
 int mars_kv_table(mars_ctx* ctx, uint32_t row, int64_t cap, uint32_t* ids, int64_t* n) {
   if (!ctx || !n) return MARS_ERR_ARG;
   if (!ctx->kv_on) return fail(ctx, MARS_ERR_ARG, "kv manager not initialised");
@@ -1325,7 +1395,7 @@ int mars_kv_state(mars_ctx* ctx, int64_t k, uint32_t* top_ids, int64_t* explicit
     CK(cudaMemcpyAsync(top_ids, ctx->kv_stage, k * 4, cudaMemcpyDeviceToHost, ctx->stream));
   }
   CK(cudaStreamSynchronize(ctx->stream));
-  if (explicit_depth) *explicit_depth = s.fs_top;
+  if (explicit_depth) *explicit_depth = s.fs_ids;
   if (fresh) *fresh = s.fresh;
   if (status) *status = s.status;
   return MARS_OK;

@@ -4075,6 +4075,18 @@ int mars_enqueue_step(const LaunchArgs* a) {
     }
     mark(1, 1, s);
   }
+  if (a->kv) {
+    // S5, expired pins: their tables return to the free stack (segment pushes
+    // by the whole grid) on the second side stream, concurrently with the
+    // control plane and the walk; the journal apply after the join waits
+    cudaEventRecord(a->ev_kvfork, s);
+    cudaStreamWaitEvent(a->side2, a->ev_kvfork, 0);
+    mark(5, 0, a->side2);
+    mars_kv_enqueue_exp_free(*a->kv, a->side2, a->work, a->bufs, nsm);
+    mark(5, 1, a->side2);
+    cudaEventRecord(a->ev_kvjoin, a->side2);
+    launches += 2;
+  }
   if (a->control_possible) {
     i64 lgq = (a->queue_upper + a->ctl_per_cta - 1) / a->ctl_per_cta;  // list entries per CTA
     int lg = (int)(lgq < 1 ? 1 : (lgq > nsm - 1 ? nsm - 1 : lgq));  // the walk keeps one SM
@@ -4103,7 +4115,10 @@ int mars_enqueue_step(const LaunchArgs* a) {
     launches++;
   }
   if (a->kv) {
+    cudaStreamWaitEvent(s, a->ev_kvjoin, 0);
+    mark(6, 0, s);
     mars_kv_enqueue_apply_step(*a->kv, s, a->work, a->bufs);
+    mark(6, 1, s);
     launches++;
   }
 #ifdef MARS_PHASE_TIMING

@@ -3,126 +3,502 @@
 // Block IDs follow the written-down policy of oracle/block_ids.py (the
 // reference KvPool only counts, engine.py:116-221): a LIFO free stack whose
 // pops first yield 0,1,2,..., alloc appends pops to the session's table,
-// free pushes the table tail back in reverse.  The stack is an explicit
-// array on top of an implicit "fresh" range, and tables are chunked (64 IDs
-// per chunk, per-row chunk directory), so the pool can hold millions of
-// blocks without materialising them up front.
+// free pushes the table tail back in reverse (so the first freed ID is on
+// top and an immediate re-allocation returns the same IDs in order).
 //
-// Ops of one journal are applied in order by one CTA; every op is parallel
-// over its IDs (coalesced pushes/pops).
+// Layout: a session's table is a directory of 64-ID chunks.  The free stack
+// is a stack of *segments* over an implicit "fresh" range of never-used IDs.
+// A chunk segment is a whole 64-ID chunk handed over by a freed table (IDs
+// pop forward from `start`); an arena segment holds < 64 loose IDs (a table's
+// partial last chunk, a partial free's boundary part, the rest of a chunk a
+// run popped partly) copied to the top of a LIFO ID arena (they pop from the
+// segment's end).  Freeing a table is O(its chunks), not O(its IDs): the
+// 1M-session step frees ~7K expired pins holding ~11M blocks by ~180K
+// segment pushes and < 64 copied IDs per table.  Chunk segments are always
+// full, so chunks in use stay below 2 * total/64 + rows.
+//
+// Ops apply in runs of one kind (frees or allocs, distinct rows within a
+// run): a run is parallel over its ops via prefix sums (one CTA for the
+// step's journal, the whole grid for the expired pins).
 #include <cuda_runtime.h>
 
 #include "mars_internal.cuh"
 #include "mars_kv.h"
 
 #define KV_TPB 1024
+#define FULL32 0xffffffffu
+#define SEG_ARENA (1ull << 63)
 
-__device__ __forceinline__ u32 kv_slot(const Kv& k, u32 row, i64 pos) {
-  u32 ch = k.dir[(i64)row * k.D + pos / KV_CH];
-  return k.chunks[(i64)ch * KV_CH + pos % KV_CH];
+__device__ __forceinline__ u64 seg_chunk_make(u32 ch, u32 start, u32 cnt) {
+  return ((u64)ch << 16) | ((u64)start << 8) | (u64)cnt;
+}
+__device__ __forceinline__ u64 seg_arena_make(i64 base, u32 cnt) {
+  return SEG_ARENA | ((u64)base << 16) | (u64)cnt;
+}
+__device__ __forceinline__ bool seg_is_arena(u64 s) { return (s & SEG_ARENA) != 0; }
+__device__ __forceinline__ u64 seg_index(u64 s) { return (s >> 16) & 0xffffffffffull; }
+__device__ __forceinline__ u32 seg_start(u64 s) { return (u32)(s >> 8) & 0xffu; }
+__device__ __forceinline__ u32 seg_count(u64 s) { return (u32)s & 0xffu; }
+
+// the q-th ID a segment pops
+__device__ __forceinline__ u32 seg_id(const Kv& k, u64 sg, i64 q) {
+  if (seg_is_arena(sg)) return k.arena[(i64)seg_index(sg) + seg_count(sg) - 1 - q];
+  return k.chunks[(i64)seg_index(sg) * KV_CH + seg_start(sg) + q];
 }
 
-// one pool op, executed by the whole CTA.  op: MARS_KV_ALLOC / MARS_KV_FREE
-// (n = -1: the whole table).  Returns false on a contract break.
-__device__ bool kv_op(Kv& k, int op, u32 row, i64 n) {
-  __shared__ i64 s_top, s_fresh, s_ctop, s_len;
-  if (threadIdx.x == 0) {
-    s_top = k.s->fs_top;
-    s_fresh = k.s->fresh;
-    s_ctop = k.s->cfs_top;
-    s_len = k.len[row];
+__device__ __forceinline__ u32* kv_slot_ptr(const Kv& k, u32 row, i64 pos) {
+  const u32 ch = k.dir[(i64)row * k.D + pos / KV_CH];
+  return &k.chunks[(i64)ch * KV_CH + pos % KV_CH];
+}
+
+// block-wide exclusive scan of one i64 per thread (blockDim.x == KV_TPB);
+// returns the exclusive prefix, *total the sum
+__device__ i64 kv_scan(i64 v, i64* total) {
+  __shared__ i64 s_w[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  i64 incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const i64 x = __shfl_up_sync(FULL32, incl, o);
+    if (lane >= o) incl += x;
   }
   __syncthreads();
-  const i64 top = s_top, fresh = s_fresh, ctop = s_ctop, len = s_len;
-  if (op == MARS_KV_ALLOC) {
-    if (n <= 0) return true;
-    if (len + n > (i64)k.D * KV_CH || n > top + (k.total - fresh)) {
-      if (threadIdx.x == 0) k.s->status |= 1;
-      __syncthreads();
-      return false;
+  if (lane == 31) s_w[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    i64 t = s_w[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const i64 x = __shfl_up_sync(FULL32, t, o);
+      if (lane >= o) t += x;
     }
-    const i64 c0 = (len + KV_CH - 1) / KV_CH, c1 = (len + n + KV_CH - 1) / KV_CH;
-    const i64 nc = c1 - c0;
-    if (nc > ctop) {
-      if (threadIdx.x == 0) k.s->status |= 2;
-      __syncthreads();
-      return false;
-    }
-    for (i64 j = threadIdx.x; j < nc; j += blockDim.x)
-      k.dir[(i64)row * k.D + c0 + j] = k.cfs[ctop - 1 - j];
-    __syncthreads();
-    for (i64 q = threadIdx.x; q < n; q += blockDim.x) {
-      u32 id = (q < top) ? k.fs[top - 1 - q] : (u32)(fresh + (q - top));
-      i64 p = len + q;
-      u32 ch = k.dir[(i64)row * k.D + p / KV_CH];
-      k.chunks[(i64)ch * KV_CH + p % KV_CH] = id;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      i64 from_stack = n < top ? n : top;
-      k.s->fs_top = top - from_stack;
-      k.s->fresh = fresh + (n - from_stack);
-      k.s->cfs_top = ctop - nc;
-      k.len[row] = (i32)(len + n);
-    }
-    __syncthreads();
-    return true;
+    s_w[lane] = t;
   }
-  // free: the last n IDs, pushed in reverse table order
-  if (n < 0) n = len;
-  if (n > len) {
+  __syncthreads();
+  const i64 before = wid ? s_w[wid - 1] : 0;
+  *total = s_w[31];
+  __syncthreads();
+  return before + incl - v;
+}
+
+// Pieces of freeing table positions [keep, L) (bottom -> top of the pushes):
+// the tail T = [tb, L) of a partial last chunk (to the arena, its chunk back
+// to the pool), the whole chunks between (chunk segments), the head
+// H = [keep, hb) of a kept boundary chunk (to the arena).
+struct FreePlan {
+  i64 keep, L, hb, tb, f0, f1;  // full chunks [f0, f1)
+  i64 nh, nt;                   // |H|, |T|
+  bool tail_chunk;              // T's chunk returns to the pool
+};
+
+__device__ __forceinline__ FreePlan free_plan(i64 L, i64 keep) {
+  FreePlan f;
+  f.keep = keep;
+  f.L = L;
+  const i64 up = (keep + KV_CH - 1) / KV_CH * KV_CH;  // keep rounded up
+  const i64 dn = L / KV_CH * KV_CH;                   // L rounded down
+  if (up >= L) {  // one chunk, or nothing: all of it to the arena
+    f.hb = L;
+    f.tb = L;
+    f.nh = L - keep;
+    f.nt = 0;
+    f.f0 = f.f1 = 0;
+    f.tail_chunk = (keep % KV_CH) == 0 && L > keep;  // the chunk leaves the row
+  } else {
+    f.hb = up;
+    f.nh = up - keep;
+    f.tb = dn > up ? dn : up;
+    f.nt = L - f.tb;
+    f.f0 = up / KV_CH;
+    f.f1 = f.tb / KV_CH;
+    f.tail_chunk = f.nt > 0;
+  }
+  return f;
+}
+
+// arena segment holding table positions [p0, p0 + c) of `row` in pop order
+__device__ __forceinline__ void arena_fill(const Kv& k, u32 row, i64 p0, i64 c, i64 base) {
+  for (i64 j = 0; j < c; ++j) k.arena[base + c - 1 - j] = *kv_slot_ptr(k, row, p0 + j);
+}
+
+// One run of frees (distinct rows; n < 0: the whole table), <= KV_TPB ops,
+// one per thread, on the whole CTA.  Free i pushes its segments above those of
+// frees 0..i-1; its first freed ID ends on top.
+__device__ bool kv_free_run(Kv& k, int m, const u32* rows, const i32* ns) {
+  const int i = threadIdx.x;
+  u32 row = 0;
+  i64 L = 0, n = 0;
+  if (i < m) {
+    row = rows[i];
+    L = k.len[row];
+    n = (ns == nullptr || ns[i] < 0) ? L : ns[i];
+  }
+  const bool bad = i < m && n > L;
+  if (__syncthreads_or(bad)) {
     if (threadIdx.x == 0) k.s->status |= 4;
-    __syncthreads();
     return false;
   }
-  if (n == 0) return true;
-  for (i64 q = threadIdx.x; q < n; q += blockDim.x) k.fs[top + q] = kv_slot(k, row, len - 1 - q);
-  const i64 c_keep = (len - n + KV_CH - 1) / KV_CH, c_all = (len + KV_CH - 1) / KV_CH;
-  __syncthreads();
-  for (i64 j = threadIdx.x; j < c_all - c_keep; j += blockDim.x)
-    k.cfs[ctop + j] = k.dir[(i64)row * k.D + c_all - 1 - j];
+  FreePlan f = free_plan(L, L - n);
+  if (n == 0) f.nh = f.nt = f.f0 = f.f1 = 0, f.tail_chunk = false;
+  const i64 nseg = (f.nt > 0) + (f.f1 - f.f0) + (f.nh > 0);
+  i64 S, A, R, N;
+  const i64 soff = kv_scan(nseg, &S);
+  const i64 aoff = kv_scan(f.nh + f.nt, &A);
+  const i64 roff = kv_scan(f.tail_chunk ? 1 : 0, &R);
+  kv_scan(n, &N);
+  const i64 s0 = k.s->seg_top, a0 = k.s->arena_top, c0 = k.s->cfs_top;
+  if (s0 + S > k.seg_cap) {
+    if (threadIdx.x == 0) k.s->status |= 32;
+    return false;
+  }
+  if (n > 0) {
+    i64 sp = s0 + soff, ap = a0 + aoff;
+    if (f.nt > 0) {
+      arena_fill(k, row, f.tb, f.nt, ap);
+      k.seg[sp++] = seg_arena_make(ap, (u32)f.nt);
+      ap += f.nt;
+    }
+    for (i64 j = f.f1 - 1; j >= f.f0; --j)
+      k.seg[sp++] = seg_chunk_make(k.dir[(i64)row * k.D + j], 0, KV_CH);
+    if (f.nh > 0) {
+      arena_fill(k, row, f.keep, f.nh, ap);
+      k.seg[sp++] = seg_arena_make(ap, (u32)f.nh);
+    }
+    if (f.tail_chunk) k.cfs[c0 + roff] = k.dir[(i64)row * k.D + (L - 1) / KV_CH];
+    k.len[row] = (i32)f.keep;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
-    k.s->fs_top = top + n;
-    k.s->cfs_top = ctop + (c_all - c_keep);
-    k.len[row] = (i32)(len - n);
+    k.s->seg_top = s0 + S;
+    k.s->arena_top = a0 + A;
+    k.s->fs_ids += N;
+    k.s->cfs_top = c0 + R;
   }
   __syncthreads();
   return true;
 }
 
-// host journal: ordered (op, row, n)
-__global__ void __launch_bounds__(KV_TPB) k_kv_apply(Kv k, i64 n_ops, const u8* op, const u32* row,
-                                                     const i32* n) {
-  for (i64 i = 0; i < n_ops; ++i) {
-    int o = op[i];
-    if (o == MARS_KV_ALLOC || o == MARS_KV_FREE) {
-      if (!kv_op(k, o, row[i], o == MARS_KV_FREE && n[i] < 0 ? -1 : n[i])) return;
+// After a run popped F IDs from the touched top segments (top first, `cum`
+// their prefix counts): emptied chunks return to the pool, an emptied arena
+// segment lowers the arena top, and a partly popped chunk segment leaves its
+// rest in the arena (chunk segments stay whole).  Thread 0.
+__device__ void kv_settle(Kv& k, const u64* segs, const i64* cum, int nseg, i64 F, i64 top,
+                          i64 ctop) {
+  i64 a = k.s->arena_top, cf = ctop;
+  int full = 0;
+  u64 last = 0;
+  bool keep_last = false;
+  for (int j = 0; j < nseg; ++j) {
+    const u64 sg = segs[j];
+    const i64 c = seg_count(sg), used = F - cum[j] < c ? F - cum[j] : c;
+    if (used == c) {  // emptied
+      ++full;
+      if (seg_is_arena(sg)) a = (i64)seg_index(sg);
+      else k.cfs[cf++] = (u32)seg_index(sg);
+    } else if (seg_is_arena(sg)) {
+      last = seg_arena_make((i64)seg_index(sg), (u32)(c - used));
+      a = (i64)seg_index(sg) + (c - used);
+      keep_last = true;
+    } else {  // partly popped chunk: its rest to the arena, the chunk back
+      const i64 r = c - used;
+      for (i64 q = 0; q < r; ++q)
+        k.arena[a + r - 1 - q] = k.chunks[(i64)seg_index(sg) * KV_CH + seg_start(sg) + used + q];
+      last = seg_arena_make(a, (u32)r);
+      a += r;
+      k.cfs[cf++] = (u32)seg_index(sg);
+      keep_last = true;
     }
+  }
+  i64 nt = top - full - (keep_last ? 1 : 0);
+  if (keep_last) k.seg[nt++] = last;
+  k.s->seg_top = nt;
+  k.s->arena_top = a;
+  k.s->cfs_top = cf;
+}
+
+// One run of allocs (distinct rows), <= KV_TPB ops, on the whole CTA: the
+// run's N IDs are the next N pops (segments from the top, then fresh IDs),
+// alloc i taking pops [off_i, off_i + n_i) onto its table's tail.  The top
+// KV_TPB segments are staged in shared memory with their prefix counts; a run
+// reaching deeper (only a host replay popping > KV_TPB small segments at
+// once) pops one ID at a time on thread 0.
+__device__ bool kv_alloc_run(Kv& k, int m, const u32* rows, const i32* ns) {
+  __shared__ i64 s_cum[KV_TPB];
+  __shared__ u64 s_seg[KV_TPB];
+  const int i = threadIdx.x;
+  u32 row = 0;
+  i64 L = 0, n = 0;
+  if (i < m) {
+    row = rows[i];
+    L = k.len[row];
+    n = ns[i] > 0 ? ns[i] : 0;
+  }
+  const i64 cnew = n > 0 ? (L + n + KV_CH - 1) / KV_CH - (L + KV_CH - 1) / KV_CH : 0;
+  const bool bad = i < m && (L + n > (i64)k.D * KV_CH);
+  i64 N, Cn;
+  const i64 noff = kv_scan(n, &N);
+  const i64 coff = kv_scan(cnew, &Cn);
+  const i64 top = k.s->seg_top, ids = k.s->fs_ids, fresh = k.s->fresh, ctop = k.s->cfs_top;
+  if (__syncthreads_or(bad) || N > ids + (k.total - fresh) || Cn > ctop) {
+    if (threadIdx.x == 0) k.s->status |= 1;
+    return false;
+  }
+  if (N == 0) return true;
+  const i64 F = N < ids ? N : ids;  // pops served by segments
+  // new table chunks for the allocating rows (popped before any release)
+  if (n > 0) {
+    const i64 c0 = (L + KV_CH - 1) / KV_CH;
+    for (i64 j = 0; j < cnew; ++j)
+      k.dir[(i64)row * k.D + c0 + j] = k.cfs[ctop - 1 - (coff + j)];
+  }
+  // the top segments and the IDs before each
+  const u64 sg = (i < top) ? k.seg[top - 1 - i] : 0ull;
+  i64 staged;
+  const i64 ex = kv_scan((i < top) ? (i64)seg_count(sg) : 0, &staged);
+  s_seg[i] = sg;
+  s_cum[i] = ex;
+  __syncthreads();
+  if (staged >= F) {
+    i64 t;
+    kv_scan((i < top && ex < F) ? 1 : 0, &t);
+    const int nseg = (int)t;  // segments touched: those starting before F
+    if (n > 0) {
+      for (i64 q = 0; q < n; ++q) {
+        const i64 p = noff + q;
+        u32 id;
+        if (p < F) {
+          int lo = 0, hi = nseg - 1;
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (s_cum[mid] <= p) lo = mid; else hi = mid - 1;
+          }
+          id = seg_id(k, s_seg[lo], p - s_cum[lo]);
+        } else {
+          id = (u32)(fresh + (p - F));
+        }
+        *kv_slot_ptr(k, row, L + q) = id;
+      }
+      k.len[row] = (i32)(L + n);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      kv_settle(k, s_seg, s_cum, nseg, F, top, ctop - Cn);
+      k.s->fs_ids = ids - F;
+      k.s->fresh = fresh + (N - F);
+    }
+  } else {
+    // deep run: sequential pops (thread 0), in the run's order
+    __syncthreads();
+    s_cum[i] = (i < m) ? n : 0;  // reuse: per-op counts / rows
+    s_seg[i] = row;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      i64 st = top, cf = ctop - Cn, fr = fresh, left = ids, a = k.s->arena_top;
+      for (int o = 0; o < m; ++o) {
+        const u32 r = (u32)s_seg[o];
+        const i64 la = k.len[r], na = s_cum[o];
+        for (i64 q = 0; q < na; ++q) {
+          u32 id;
+          if (left > 0) {
+            const u64 g = k.seg[st - 1];
+            id = seg_id(k, g, 0);
+            const u32 c = seg_count(g);
+            if (c == 1) {
+              if (seg_is_arena(g)) a = (i64)seg_index(g);
+              else k.cfs[cf++] = (u32)seg_index(g);
+              --st;
+            } else if (seg_is_arena(g)) {
+              k.seg[st - 1] = seg_arena_make((i64)seg_index(g), c - 1);
+              a = (i64)seg_index(g) + c - 1;
+            } else {
+              k.seg[st - 1] = seg_chunk_make((u32)seg_index(g), seg_start(g) + 1, c - 1);
+            }
+            --left;
+          } else {
+            id = (u32)(fr++);
+          }
+          *kv_slot_ptr(k, r, la + q) = id;
+        }
+        k.len[r] = (i32)(la + na);
+      }
+      // a partly popped chunk on top leaves its rest in the arena
+      if (st > 0 && !seg_is_arena(k.seg[st - 1]) && seg_count(k.seg[st - 1]) < KV_CH) {
+        const u64 g = k.seg[st - 1];
+        const i64 r = seg_count(g);
+        for (i64 q = 0; q < r; ++q)
+          k.arena[a + r - 1 - q] = k.chunks[(i64)seg_index(g) * KV_CH + seg_start(g) + q];
+        k.seg[st - 1] = seg_arena_make(a, (u32)r);
+        a += r;
+        k.cfs[cf++] = (u32)seg_index(g);
+      }
+      k.s->seg_top = st;
+      k.s->fs_ids = left;
+      k.s->fresh = fr;
+      k.s->cfs_top = cf;
+      k.s->arena_top = a;
+    }
+  }
+  __syncthreads();
+  return true;
+}
+
+// An ordered op list (op, row, n) on one CTA: maximal runs of frees or of
+// allocs with distinct rows, <= KV_TPB ops each, applied run by run.  PIN /
+// UNPIN move ownership only (no table change).  `journal`: the ops are the
+// step journal's codes (MARS_J_ALLOC, or a whole-table free).
+__device__ void kv_apply_list(Kv& k, i64 n_ops, const u8* op, const u32* row, const i32* n,
+                              bool journal) {
+  __shared__ u32 s_row[KV_TPB];
+  __shared__ i32 s_n[KV_TPB];
+  __shared__ int s_m, s_kind;
+  i64 i = 0;
+  while (i < n_ops) {
+    if (threadIdx.x == 0) {
+      // extend the run while the kind matches and rows stay distinct (a
+      // linear check: runs are short)
+      int kind = -1, m = 0;
+      while (i + m < n_ops && m < KV_TPB) {
+        const int o = op[i + m];
+        int kd;
+        if (journal) kd = (o == MARS_J_ALLOC) ? 1 : 2;
+        else kd = (o == MARS_KV_ALLOC) ? 1 : (o == MARS_KV_FREE ? 2 : 0);
+        if (kd == 0) {  // pin / unpin: ends a run, skipped
+          if (m == 0) {
+            kind = 0;
+            m = 1;
+          }
+          break;
+        }
+        if (kind < 0) kind = kd;
+        if (kd != kind) break;
+        const u32 r = row[i + m];
+        bool dup = false;
+        for (int q = 0; q < m; ++q) dup |= s_row[q] == r;
+        if (dup) break;
+        s_row[m] = r;
+        s_n[m] = (journal && kd == 2) ? -1 : n[i + m];
+        ++m;
+      }
+      s_m = m;
+      s_kind = kind;
+    }
+    __syncthreads();
+    const int m = s_m, kind = s_kind;
+    bool ok = true;
+    if (kind == 1) ok = kv_alloc_run(k, m, s_row, s_n);
+    else if (kind == 2) ok = kv_free_run(k, m, s_row, s_n);
+    if (!ok) return;
+    i += m;
+    __syncthreads();
   }
 }
 
-// the step's own journal: expired pins (rank order) then k_walk's journal,
-// then (MARS_MODE_ADVANCE) the tick tail's frees in decode order -- a finished
-// session's blocks (sim.py:243) and an unpinned boundary's (sim.py:269); a
-// pin keeps the table (ownership moves, the IDs stay)
-__global__ void __launch_bounds__(KV_TPB) k_kv_apply_step(Kv k, Work* w, Bufs b) {
+// host journal: ordered (op, row, n)
+__global__ void __launch_bounds__(KV_TPB) k_kv_apply(Kv k, i64 n_ops, const u8* op, const u32* row,
+                                                     const i32* n) {
+  kv_apply_list(k, n_ops, op, row, n, false);
+}
+
+// The step's expired pins (rank order), freed as one run by the whole grid:
+// k_kv_exp_scan (one CTA) computes every table's segment / arena / chunk
+// offsets and moves the scalars, k_kv_exp_push writes the segments (one
+// thread each; the thread of a table's tail segment also copies its < 64
+// loose IDs to the arena and returns the chunk).
+__global__ void __launch_bounds__(KV_TPB) k_kv_exp_scan(Kv k, const Work* w, Bufs b) {
   const int ne = w->n_exp;
-  for (int i = 0; i < ne; ++i)
-    if (!kv_op(k, MARS_KV_FREE, b.exp_row_sorted[i], -1)) return;
-  const int nj = w->n_journal;
-  for (int i = 0; i < nj; ++i) {
-    int o = b.j_op[i];
-    if (o == MARS_J_ALLOC) {
-      if (!kv_op(k, MARS_KV_ALLOC, b.j_row[i], b.j_n[i])) return;
-    } else {
-      if (!kv_op(k, MARS_KV_FREE, b.j_row[i], -1)) return;
-    }
+  const int per = (ne + KV_TPB - 1) / KV_TPB;
+  const int i0 = threadIdx.x * per, i1 = min(ne, i0 + per);
+  i64 segs = 0, ids = 0, ar = 0, rc = 0;
+  for (int i = i0; i < i1; ++i) {
+    const i64 L = k.len[b.exp_row_sorted[i]];
+    k.xlen[i] = (i32)L;
+    segs += L / KV_CH + ((L % KV_CH) ? 1 : 0);
+    ar += L % KV_CH;
+    rc += (L % KV_CH) ? 1 : 0;
+    ids += L;
   }
-  if (w->in.mode & MARS_MODE_ADVANCE) {
+  i64 S, N, A, R;
+  i64 so = kv_scan(segs, &S);
+  i64 ao = kv_scan(ar, &A);
+  i64 ro = kv_scan(rc, &R);
+  kv_scan(ids, &N);
+  for (int i = i0; i < i1; ++i) {
+    const i64 L = k.xlen[i];
+    k.xoff[i] = so;
+    k.xaoff[i] = ao;
+    k.xroff[i] = ro;
+    so += L / KV_CH + ((L % KV_CH) ? 1 : 0);
+    ao += L % KV_CH;
+    ro += (L % KV_CH) ? 1 : 0;
+    k.len[b.exp_row_sorted[i]] = 0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const i64 s0 = k.s->seg_top;
+    if (s0 + S > k.seg_cap) {
+      k.s->status |= 32;
+      k.xbase[1] = 0;
+      return;
+    }
+    k.xbase[0] = s0;
+    k.xbase[1] = S;
+    k.xbase[2] = k.s->arena_top;
+    k.xbase[3] = k.s->cfs_top;
+    k.s->seg_top = s0 + S;
+    k.s->arena_top += A;
+    k.s->cfs_top += R;
+    k.s->fs_ids += N;
+  }
+}
+
+__global__ void k_kv_exp_push(Kv k, const Work* w, Bufs b) {
+  const int ne = w->n_exp;
+  const i64 base = k.xbase[0], S = k.xbase[1], a0 = k.xbase[2], c0 = k.xbase[3];
+  for (i64 g = (i64)blockIdx.x * blockDim.x + threadIdx.x; g < S;
+       g += (i64)gridDim.x * blockDim.x) {
+    int lo = 0, hi = ne - 1;  // the free owning segment g: last xoff <= g
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (k.xoff[mid] <= g) lo = mid; else hi = mid - 1;
+    }
+    const u32 row = b.exp_row_sorted[lo];
+    const i64 L = k.xlen[lo], tail = L % KV_CH, full = L / KV_CH;
+    i64 j = g - k.xoff[lo];  // 0 = bottom
+    if (tail) {
+      if (j == 0) {  // the partial last chunk: loose IDs to the arena
+        const i64 ap = a0 + k.xaoff[lo];
+        arena_fill(k, row, full * KV_CH, tail, ap);
+        k.seg[base + g] = seg_arena_make(ap, (u32)tail);
+        k.cfs[c0 + k.xroff[lo]] = k.dir[(i64)row * k.D + full];
+        continue;
+      }
+      --j;
+    }
+    k.seg[base + g] = seg_chunk_make(k.dir[(i64)row * k.D + (full - 1 - j)], 0, KV_CH);
+  }
+}
+
+// the rest of the step's journal on one CTA: k_walk's alloc / evict ops in
+// plan order, then (MARS_MODE_ADVANCE) the tick tail's frees in decode order
+// -- a finished session's blocks (sim.py:243) and an unpinned boundary's
+// (sim.py:269); a pin keeps the table (ownership moves, the IDs stay)
+__global__ void __launch_bounds__(KV_TPB) k_kv_apply_step(Kv k, Work* w, Bufs b) {
+  if (k.s->status) return;
+  kv_apply_list(k, w->n_journal, b.j_op, b.j_row, b.j_n, true);
+  if ((w->in.mode & MARS_MODE_ADVANCE) && k.s->status == 0) {
+    __shared__ u32 s_r[KV_TPB];
+    __shared__ int s_m;
     const int nr = w->n_round_end;
-    for (int i = 0; i < nr; ++i)
-      if (b.end_kind[i] != 1 && !kv_op(k, MARS_KV_FREE, b.end_row[i], -1)) return;
+    for (int i0 = 0; i0 < nr; i0 += KV_TPB) {
+      if (threadIdx.x == 0) {
+        int m = 0;
+        for (int i = i0; i < nr && i < i0 + KV_TPB; ++i)
+          if (b.end_kind[i] != 1) s_r[m++] = b.end_row[i];
+        s_m = m;
+      }
+      __syncthreads();
+      if (!kv_free_run(k, s_m, s_r, nullptr)) return;
+    }
   }
 }
 
@@ -130,8 +506,102 @@ __global__ void __launch_bounds__(KV_TPB) k_kv_apply_step(Kv k, Work* w, Bufs b)
 // in the tool plane's finish order (kind 2 of mars_resume_rows)
 __global__ void __launch_bounds__(KV_TPB) k_kv_resume_free(Kv k, i64 n, const i64* rows,
                                                            const u8* kind) {
-  for (i64 i = 0; i < n; ++i)
-    if (kind[i] == 2 && !kv_op(k, MARS_KV_FREE, (u32)rows[i], -1)) return;
+  __shared__ u32 s_r[KV_TPB];
+  __shared__ int s_m;
+  for (i64 i0 = 0; i0 < n; i0 += KV_TPB) {
+    if (threadIdx.x == 0) {
+      int m = 0;
+      for (i64 i = i0; i < n && i < i0 + KV_TPB; ++i)
+        if (kind[i] == 2) s_r[m++] = (u32)rows[i];
+      s_m = m;
+    }
+    __syncthreads();
+    if (!kv_free_run(k, s_m, s_r, nullptr)) return;
+  }
+}
+
+// bulk table initialisation from a fresh pool (no free segment): row i of the
+// list gets the next n_i IDs of the fresh range, exactly as n_i sequential
+// allocs in list order would.  k_kv_bulk_scan (one CTA) + k_kv_bulk_fill.
+__global__ void __launch_bounds__(KV_TPB) k_kv_bulk_scan(Kv k, i64 n, const u32* rows,
+                                                         const i32* cnt) {
+  const i64 per = (n + KV_TPB - 1) / KV_TPB;
+  const i64 i0 = threadIdx.x * per, i1 = (i0 + per < n) ? i0 + per : n;
+  i64 ids = 0, chs = 0;
+  for (i64 i = i0; i < i1; ++i) {
+    const i64 L = k.len[rows[i]], c = cnt[i];
+    ids += c;
+    chs += (L + c + KV_CH - 1) / KV_CH - (L + KV_CH - 1) / KV_CH;
+  }
+  i64 N, C;
+  i64 io = kv_scan(ids, &N);
+  i64 co = kv_scan(chs, &C);
+  const i64 fresh = k.s->fresh, ctop = k.s->cfs_top;
+  if (k.s->fs_ids != 0 || N > k.total - fresh || C > ctop) {
+    if (threadIdx.x == 0) k.s->status |= 16;
+    return;
+  }
+  for (i64 i = i0; i < i1; ++i) {
+    const i64 L = k.len[rows[i]], c = cnt[i];
+    const i64 c0 = (L + KV_CH - 1) / KV_CH, cn = (L + c + KV_CH - 1) / KV_CH - c0;
+    for (i64 j = 0; j < cn; ++j) k.dir[(i64)rows[i] * k.D + c0 + j] = k.cfs[ctop - 1 - (co + j)];
+    k.xoff[i] = fresh + io;  // first ID of this row
+    io += c;
+    co += cn;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    k.s->fresh = fresh + N;
+    k.s->cfs_top = ctop - C;
+  }
+}
+
+__global__ void k_kv_bulk_fill(Kv k, i64 n, const u32* rows, const i32* cnt) {
+  // one warp per row: consecutive IDs onto its table tail, then the length
+  const int lane = threadIdx.x & 31;
+  for (i64 i = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n;
+       i += ((i64)gridDim.x * blockDim.x) >> 5) {
+    const u32 r = rows[i];
+    const i64 L = k.len[r], c = cnt[i], id0 = k.xoff[i];
+    for (i64 q = lane; q < c; q += 32) *kv_slot_ptr(k, r, L + q) = (u32)(id0 + q);
+    __syncwarp();
+    if (lane == 0) k.len[r] = (i32)(L + c);
+  }
+}
+
+__global__ void k_kv_table(Kv k, u32 row, i64 cap, u32* out) {
+  i64 len = k.len[row];
+  if (len > cap) len = cap;
+  for (i64 p = blockIdx.x * blockDim.x + threadIdx.x; p < len; p += gridDim.x * blockDim.x)
+    out[p] = *kv_slot_ptr(k, row, p);
+}
+
+// the next `cnt` IDs pops would return (segments from the top, then fresh)
+__global__ void k_kv_top(Kv k, i64 cnt, u32* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  i64 q = 0;
+  for (i64 j = k.s->seg_top - 1; j >= 0 && q < cnt; --j) {
+    const u64 sg = k.seg[j];
+    for (u32 t = 0; t < seg_count(sg) && q < cnt; ++t) out[q++] = seg_id(k, sg, t);
+  }
+  for (i64 f = k.s->fresh; q < cnt; ++f) out[q++] = f < k.total ? (u32)f : 0xffffffffu;
+}
+
+int mars_kv_enqueue_apply(const Kv& k, cudaStream_t s, i64 n_ops, const u8* op, const u32* row,
+                          const i32* n) {
+  k_kv_apply<<<1, KV_TPB, 0, s>>>(k, n_ops, op, row, n);
+  return (int)cudaGetLastError();
+}
+
+int mars_kv_enqueue_exp_free(const Kv& k, cudaStream_t s, Work* w, const Bufs& b, int grid) {
+  k_kv_exp_scan<<<1, KV_TPB, 0, s>>>(k, w, b);
+  k_kv_exp_push<<<grid, 256, 0, s>>>(k, w, b);
+  return (int)cudaGetLastError();
+}
+
+int mars_kv_enqueue_apply_step(const Kv& k, cudaStream_t s, Work* w, const Bufs& b) {
+  k_kv_apply_step<<<1, KV_TPB, 0, s>>>(k, w, b);
+  return (int)cudaGetLastError();
 }
 
 int mars_kv_enqueue_resume_free(const Kv& k, cudaStream_t s, i64 n, const i64* rows,
@@ -140,17 +610,21 @@ int mars_kv_enqueue_resume_free(const Kv& k, cudaStream_t s, i64 n, const i64* r
   return (int)cudaGetLastError();
 }
 
-__global__ void k_kv_table(Kv k, u32 row, i64 cap, u32* out) {
-  i64 len = k.len[row];
-  if (len > cap) len = cap;
-  for (i64 p = blockIdx.x * blockDim.x + threadIdx.x; p < len; p += gridDim.x * blockDim.x)
-    out[p] = kv_slot(k, row, p);
+int mars_kv_enqueue_bulk(const Kv& k, cudaStream_t s, i64 n, const u32* rows, const i32* cnt,
+                         int grid) {
+  k_kv_bulk_scan<<<1, KV_TPB, 0, s>>>(k, n, rows, cnt);
+  k_kv_bulk_fill<<<grid, 256, 0, s>>>(k, n, rows, cnt);
+  return (int)cudaGetLastError();
 }
 
-__global__ void k_kv_top(Kv k, i64 cnt, u32* out) {
-  i64 top = k.s->fs_top, fresh = k.s->fresh;
-  for (i64 q = blockIdx.x * blockDim.x + threadIdx.x; q < cnt; q += gridDim.x * blockDim.x)
-    out[q] = (q < top) ? k.fs[top - 1 - q] : (u32)(fresh + (q - top));
+int mars_kv_enqueue_table(const Kv& k, cudaStream_t s, u32 row, i64 cap, u32* out) {
+  k_kv_table<<<16, 256, 0, s>>>(k, row, cap, out);
+  return (int)cudaGetLastError();
+}
+
+int mars_kv_enqueue_top(const Kv& k, cudaStream_t s, i64 cnt, u32* out) {
+  k_kv_top<<<1, 32, 0, s>>>(k, cnt, out);
+  return (int)cudaGetLastError();
 }
 
 // SM-driven block copy (zero-copy pinned host memory): one CTA per block piece,
@@ -170,27 +644,6 @@ __global__ void __launch_bounds__(512) k_kv_copy(const Kv k, const u32* ids, i64
     const i64 m = piece / 16;
     for (i64 j = threadIdx.x; j < m; j += blockDim.x) d4[j] = s4[j];
   }
-}
-
-int mars_kv_enqueue_apply(const Kv& k, cudaStream_t s, i64 n_ops, const u8* op, const u32* row,
-                          const i32* n) {
-  k_kv_apply<<<1, KV_TPB, 0, s>>>(k, n_ops, op, row, n);
-  return (int)cudaGetLastError();
-}
-
-int mars_kv_enqueue_apply_step(const Kv& k, cudaStream_t s, Work* w, const Bufs& b) {
-  k_kv_apply_step<<<1, KV_TPB, 0, s>>>(k, w, b);
-  return (int)cudaGetLastError();
-}
-
-int mars_kv_enqueue_table(const Kv& k, cudaStream_t s, u32 row, i64 cap, u32* out) {
-  k_kv_table<<<16, 256, 0, s>>>(k, row, cap, out);
-  return (int)cudaGetLastError();
-}
-
-int mars_kv_enqueue_top(const Kv& k, cudaStream_t s, i64 cnt, u32* out) {
-  k_kv_top<<<16, 256, 0, s>>>(k, cnt, out);
-  return (int)cudaGetLastError();
 }
 
 int mars_kv_enqueue_copy(const Kv& k, cudaStream_t s, const u32* ids, i64 n, i64 slot0, int dir,

@@ -59,6 +59,27 @@ class KvBlockManager:
                                            row.ctypes.data_as(C.c_void_p),
                                            n.ctypes.data_as(C.c_void_p)))
 
+    def bulk_alloc(self, rows, counts) -> None:
+        """Initial tables from a fresh pool: rows[i] (distinct) gets the next
+        counts[i] never-used IDs, as sequential allocs in list order would."""
+        r = np.ascontiguousarray(rows, np.uint32)
+        c = np.ascontiguousarray(counts, np.int32)
+        self._check(self.lib.mars_kv_bulk_alloc(self.eng.ctx, len(r), r.ctypes.data_as(C.c_void_p),
+                                                c.ctypes.data_as(C.c_void_p)))
+
+    def load_snapshot_tables(self, snap) -> int:
+        """Tables for every session of a snapshot that holds KV (a running
+        session's held blocks, a pin's pinned blocks), rows in session-id
+        (rank) order; returns the blocks handed out."""
+        from .snapshot import F_PINNED
+        c = snap.cols
+        held = -(-c["kv"].astype(np.int64) // 16)
+        blocks = np.where((c["flags"] & F_PINNED) != 0, c["pinned_blocks"], held)
+        rows = np.nonzero(blocks > 0)[0]
+        rows = rows[np.argsort(c["rank"][rows], kind="stable")]
+        self.bulk_alloc(rows, blocks[rows])
+        return int(blocks[rows].sum())
+
     def table(self, row: int) -> np.ndarray:
         n = C.c_int64()
         self._check(self.lib.mars_kv_table(self.eng.ctx, row, 0, None, C.byref(n)))
@@ -73,7 +94,8 @@ class KvBlockManager:
         depth, fresh, status = C.c_int64(), C.c_int64(), C.c_int32()
         self._check(self.lib.mars_kv_state(self.eng.ctx, k, top.ctypes.data_as(C.c_void_p),
                                            C.byref(depth), C.byref(fresh), C.byref(status)))
-        return top[:k], depth.value, fresh.value, status.value
+        top = top[:k]
+        return top[top != 0xFFFFFFFF], depth.value, fresh.value, status.value
 
     def free_count(self) -> int:
         _, depth, fresh, _ = self.state(0)

@@ -205,3 +205,32 @@ def reclaim_heavy(n, seed, policy="mars", tiny_pins=40):
         c["served"][:] = served
     s.meta = dict(s.meta, variant="reclaim_heavy", policy=policy)
     return s
+
+
+def kv_small(n, seed):
+    """The headroom mix with small KV footprints (1-4 blocks per session), so
+    the CPU block-ID restatement (oracle/block_ids.py) can follow a 1M-session
+    table: running and pinned sessions hold 16-64 tokens, prefills 0-63, the
+    pool keeps the headroom rule and ~8% of the pins expire this step."""
+    from paper_2604_26963_b200.snapshot import DECODE, PREFILL
+
+    s = snapshot_v1(n, seed=seed, pool="headroom")
+    c = s.cols
+    rng = np.random.default_rng(seed + 5)
+    dec = c["phase"] == DECODE
+    pre = c["phase"] == PREFILL
+    pinned = (c["flags"] & F_PINNED) != 0
+    small = 16 * rng.integers(1, 5, size=n)
+    c["kv"][dec | pinned] = small[dec | pinned]
+    c["context"][dec] = small[dec]
+    c["kv"][pre] = rng.integers(0, 64, size=n)[pre]
+    c["pinned_blocks"][pinned] = small[pinned] // 16
+    held = np.where(pinned, c["pinned_blocks"], -(-c["kv"].astype(np.int64) // 16))
+    total_held = int(held.sum())
+    s.total_blocks = -(-total_held * 100 // 85)
+    s.free_blocks = s.total_blocks - total_held
+    q = s.queue
+    long_ = c["req_blocks"][q] > 0.25 * s.total_blocks
+    c["flags"][q] = (c["flags"][q] & ~np.uint8(F_LONG)) | np.where(long_, F_LONG, 0).astype(np.uint8)
+    s.meta = dict(s.meta, variant="kv_small")
+    return s

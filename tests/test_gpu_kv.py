@@ -37,7 +37,7 @@ def test_fuzzed_op_stream_matches_the_restatement():
     ref = BlockIdPool(total)
     alloc, pinned, rows = {}, {}, {}
     ops = []
-    for step in range(20_000):
+    for step in range(100_000):
         choices = ["alloc_new"]
         if alloc:
             choices += ["alloc_more", "free_some", "free_all", "pin"]
@@ -162,3 +162,84 @@ def test_dropin_block_ids_follow_the_reference_op_stream(key):
     rows = {sid: pol._row[sid] for sid in pol._row}
     _same_state(pol.kv, ref, rows)
     pol.close()
+
+
+def _ref_tables(snap):
+    """The restatement holding every session's initial table: sequential
+    allocs in session-id order (what mars_kv_bulk_alloc reproduces)."""
+    c = snap.cols
+    held = -(-c["kv"].astype(np.int64) // 16)
+    blocks = np.where((c["flags"] & F_PINNED) != 0, c["pinned_blocks"], held)
+    ref = BlockIdPool(snap.total_blocks)
+    for r in np.argsort(c["rank"], kind="stable"):
+        if blocks[r] > 0:
+            ref.apply("alloc", snap.sid(int(r)), int(blocks[r]))
+    return ref
+
+
+def test_bulk_alloc_matches_sequential_allocs():
+    from tests._variants import kv_small
+    snap = kv_small(30_000, 61)
+    eng = MarsEngine(max_rows=snap.n, max_queue=len(snap.queue),
+                     config=make_config(initial_window=snap.initial_window))
+    eng.load_snapshot(snap)
+    kv = KvBlockManager(eng, snap.total_blocks, max_blocks_per_row=1 << 10)
+    kv.load_snapshot_tables(snap)
+    ref = _ref_tables(snap)
+    rows = {snap.sid(r): r for r in range(0, snap.n, 97)}
+    _same_state(kv, ref, {s: r for s, r in rows.items() if s in ref.tables})
+    eng.close()
+
+
+@pytest.mark.parametrize("n,kind", [(1_000_000, "kv_small"), (200_000, "reclaim_heavy"),
+                                    (100_000, "pressure_small")])
+def test_step_with_block_ids_at_scale_matches_the_restatement(n, kind):
+    """The whole step with S5 attached (expired pins' tables back on the stack
+    grid-wide, then the plan's alloc / evict journal) against the
+    restatement replaying the oracle's op stream."""
+    from tests._variants import kv_small, reclaim_heavy, with_free
+    if kind == "kv_small":
+        snap = kv_small(n, 62)
+    elif kind == "reclaim_heavy":
+        snap = reclaim_heavy(n, 63, "mars")
+    else:
+        snap = with_free(kv_small(n, 64), 3)
+    eng = MarsEngine(max_rows=snap.n, max_queue=len(snap.queue),
+                     config=make_config(initial_window=snap.initial_window))
+    eng.load_snapshot(snap)
+    kv = KvBlockManager(eng, snap.total_blocks, max_blocks_per_row=1 << 10)
+    kv.load_snapshot_tables(snap)
+    eng.set_graph(True)
+    res = eng.step(eng.step_in(snap.now, True, snap.active_tools, 0, snap.worker_slots))
+    assert res.status == 0
+    ref = _ref_tables(snap)
+    out = run_step(snap.copy())
+    for op, r, k, from_pinned in out["expiry_journal"] + out["journal"]:
+        ref.apply(op, snap.sid(r), k)
+    touched = {snap.sid(r) for _, r, _, _ in out["expiry_journal"] + out["journal"]}
+    assert touched
+    _same_state(kv, ref, {s: int(s[1:]) for s in touched if int(s[1:]) < snap.n})
+    top, depth, fresh, status = kv.state(4096)
+    assert top.tolist() == ref.top(4096)
+    eng.close()
+
+
+def test_deep_alloc_run_pops_many_small_segments():
+    """An alloc popping more than 1024 one-ID segments at once (the
+    sequential fallback of the run kernel)."""
+    eng = MarsEngine(max_rows=4096, max_queue=1)
+    total = 8192
+    kv = KvBlockManager(eng, total, max_blocks_per_row=4096)
+    ref = BlockIdPool(total)
+    ops = []
+    for r in range(3000):
+        ops.append((N.KV_ALLOC, r, 2))
+        ref.apply("alloc", f"s{r}", 2)
+    for r in range(3000):
+        ops.append((N.KV_FREE, r, 1))
+        ref.apply("free", f"s{r}", 1)
+    ops.append((N.KV_ALLOC, 3500, 2500))
+    ref.apply("alloc", "s3500", 2500)
+    kv.apply(ops)
+    _same_state(kv, ref, {"s3500": 3500, "s17": 17, "s2999": 2999})
+    eng.close()
