@@ -10,8 +10,11 @@ reclamation, and S2 retention for the boundary rows.  Every timed step starts
 from the same snapshot (device-side restore, untimed) with L2 flushed, so each
 step repeats the identical decisions.
 
-Multi-GPU (torchrun): data-parallel engine replicas, each rank owns its own
-1M-session shard (weak scaling); time = max over ranks.
+Multi-GPU (torchrun): ONE global 1M-session snapshot,
+rows sharded rank mod N over data-parallel engine replicas (strong scaling);
+global admission exchanges the probe counters (NCCL all-reduce) and the
+admission entries (all-gather); time = max over ranks, value = the global
+table's sessions per second.
 
 ``--impl reference`` times the reference CPU path (the oracle port of
 agentsched, single-threaded CPython) on the same workload and prints the same
@@ -331,6 +334,68 @@ def regime_sweep(device: int, n: int, steps: int = 10, warmup: int = 3, flush_mb
     return out
 
 
+def dropin_sweep(keys=("demo64/mars", "faceoff200/mars", "openhands_heavy40/mars")) -> list:
+    """SURVEY.md §8(d) configs (1) and (5), the full loop: the reference's own
+    ``agentsched.sim.run_simulation`` (baseline/_ref) on a frozen reference
+    trace, once with the reference MarsPolicy and once with the INTEGRATION.md
+    binding (GpuMarsPolicy + the B200 balance_and_admit).  Wall time of the
+    whole run on the host clock, scheduling steps (plan_tick calls) per second
+    for both arms, and whether the drop-in's event log is byte-identical to
+    the reference's (the frozen SHA-256)."""
+    import hashlib
+
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(ref_dir) and ref_dir not in sys.path:
+        sys.path.insert(1, ref_dir)
+    try:
+        from agentsched import baselines, control, sim, workload
+    except ImportError:
+        return [{"error": "agentsched (baseline/_ref) not importable"}]
+    with open(os.path.join(ROOT, "tests", "golden", "sim_logs.json")) as fh:
+        SIM = json.load(fh)
+
+    from paper_2604_26963_b200.admission import balance_and_admit as gpu_bna
+    from paper_2604_26963_b200.policy import GpuMarsPolicy
+
+    out = []
+    for key in keys:
+        spec = SIM[key]
+        traces = workload.load_trace(os.path.join(ROOT, "tests", "golden", spec["trace"]))
+        params = sim.EngineParams(**spec["engine"])
+        run = dict(spec["run"])
+        if "controller" in run:
+            run["controller"] = control.ControllerConfig(**run["controller"])
+        row = {"trace": key, "sessions": len(traces)}
+        for arm in ("reference", "b200"):
+            pol = baselines.make_policy("mars") if arm == "reference" else GpuMarsPolicy()
+            ticks = [0]
+            inner = pol.plan_tick
+
+            def counted(*a, _inner=inner, _t=ticks, **k):
+                _t[0] += 1
+                return _inner(*a, **k)
+
+            pol.plan_tick = counted
+            orig = sim.balance_and_admit
+            if arm == "b200":
+                sim.balance_and_admit = gpu_bna
+            try:
+                t0 = time.perf_counter()
+                res = sim.run_simulation(traces, params, pol, **run)
+                dt = time.perf_counter() - t0
+            finally:
+                sim.balance_and_admit = orig
+                if arm == "b200":
+                    pol.close()
+            data = b"".join(json.dumps(r, separators=(",", ":")).encode() + b"\n"
+                            for r in res.events)
+            row[arm] = {"wall_s": dt, "steps": ticks[0], "steps_per_s": ticks[0] / dt,
+                        "log_identical": hashlib.sha256(data).hexdigest() == spec["sha256"]}
+        row["b200_over_reference"] = row["b200"]["steps_per_s"] / row["reference"]["steps_per_s"]
+        out.append(row)
+    return out
+
+
 def cpu_reference(sessions: int, seed: int, reps: int = 1):
     """The reference's own step (agentsched from baseline/_ref, else the
     oracle port) over snapshot_v1(sessions) on one core; materialisation
@@ -353,7 +418,9 @@ def workload_config(sessions: int, world: int) -> dict:
     """The `config` of both arms' lines (identical keys and values)."""
     return {"workload": "one MARS scheduling step over one global snapshot_v1 session table "
                         "(pin expiry, probe, control-plane admission, MLFQ aging, window "
-                        "top-128, build_plan walk with reclamation, S2 retention)"
+                        "top-128, build_plan walk with reclamation, S2 retention, S5: the "
+                        "pool ops of the step -- expired pins freed, the plan's allocs and "
+                        "evictions; the B200 arm keeps every block's ID)"
                         + ("" if world == 1 else
                            f"; rows sharded rank mod {world} over data-parallel replicas"),
             "sessions": sessions, "pool": "headroom", "mix": "A",
@@ -494,6 +561,10 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--flush-mb", type=int, default=512)
     ap.add_argument("--no-kv", action="store_true", help="skip the KV evict/restore sweep")
+    ap.add_argument("--no-s5", dest="s5", action="store_false",
+                    help="step without the block-ID manager (S5) attached")
+    ap.add_argument("--no-dropin", dest="dropin", action="store_false",
+                    help="skip the full-loop drop-in runs (configs 1 and 5)")
     ap.add_argument("--no-regimes", dest="regimes", action="store_false",
                     help="skip the heavy-reclaim / tick-grid regime sweep")
     ap.add_argument("--clock-load", type=int, default=100,
@@ -536,7 +607,13 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    snap = snapshot_v1(a.sessions, seed=rank, pool="headroom")
+    # ONE global snapshot; with N ranks every rank
+    # owns the rows r with r mod N == rank (strong scaling, the value counts
+    # the global table's sessions once)
+    snap = snapshot_v1(a.sessions, seed=0, pool="headroom")
+    if world > 1:
+        from paper_2604_26963_b200.snapshot import snapshot_shard
+        snap = snapshot_shard(snap, world, rank, box_global=True)
     qcap = max(len(snap.queue), 1)
     qlens = [len(snap.queue)]
     if dist is not None:
@@ -550,6 +627,17 @@ def main():
     eng = MarsEngine(max_rows=snap.n, max_queue=qcap, device=local,
                      config=make_config(initial_window=snap.initial_window))
     eng.load_snapshot(snap)
+    s5_blocks = None
+    if a.s5:
+        # S5 in the step: every session holding KV gets its block table (IDs
+        # from a fresh pool, rank order); each step then frees the expired
+        # pins' tables and applies the plan's alloc / evict journal on the
+        # device (k_kv_exp_scan/push, k_kv_apply_step), state restored with
+        # the table between steps
+        from paper_2604_26963_b200.kvstore import KvBlockManager
+        per_row = int(-(-(int(snap.cols["context"].max()) + 4096) // 16))
+        kvm = KvBlockManager(eng, snap.total_blocks, max_blocks_per_row=per_row)
+        s5_blocks = kvm.load_snapshot_tables(snap)
     si = eng.step_in(snap.now, True, snap.active_tools, snap.queued_tools, snap.worker_slots)
     flush = a.flush_mb << 20
     if world == 1:
@@ -565,9 +653,9 @@ def main():
     else:
         # sharded replicas: every rank owns a 1M-session shard, the control
         # plane runs on NCCL-reduced counters and the all-gathered union list
-        from paper_2604_26963_b200.dist import COUNTERS, ShardedEngine, exchange, interleaved_gpos
+        from paper_2604_26963_b200.dist import COUNTERS, ShardedEngine, exchange
 
-        gpos = interleaved_gpos(qlens)[rank]
+        gpos = snap.meta["gpos"]
         sh = ShardedEngine(eng, world=world, rank=rank)
         stream = sh.stream
         torch.cuda.set_stream(stream)
@@ -677,15 +765,19 @@ def main():
     peak, peak_kind = _peaks()
     sb = scan_bytes(snap)
     achieved = sb / (scan_avg * 1e-3) / 1e9
-    total_sessions = a.sessions * world
+    total_sessions = a.sessions
     steps_per_s = 1e3 / ms_per_step
     value = total_sessions * steps_per_s
     line = {
         "metric": METRIC, "value": value, "unit": "sessions/s", "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_per_step,
-        "steps_per_s": steps_per_s, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64+i64", "data": "synthetic (snapshot_v1 mix A, seed=rank)",
+        "steps_per_s": steps_per_s, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "f64+i64",
+        "data": "synthetic (snapshot_v1 mix A, seed 0" + (
+            f", rows sharded rank mod {world})" if world > 1 else ")"),
         "config": workload_config(a.sessions, world),
+        "s5_block_ids": s5_blocks,
         "roofline": {"bound": "hbm", "kernel": "k_scan", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": _ncu_traffic(),
                      "algorithmic_bytes": sb, "kernel_ms": scan_avg, "peak_source": peak_kind,
@@ -711,6 +803,11 @@ def main():
             line["regimes"] = regime_sweep(local, a.sessions)
         except Exception as exc:  # the headline line stands on its own
             line["regimes"] = {"error": repr(exc)[:300]}
+    if rank == 0 and world == 1 and a.dropin:
+        try:
+            line["dropin"] = dropin_sweep()
+        except Exception as exc:  # the headline line stands on its own
+            line["dropin"] = [{"error": repr(exc)[:300]}]
     if rank == 0 and world == 1 and a.hbm_sweep:
         try:
             line["hbm_sweep"] = hbm_sweep(local, [int(x) for x in a.hbm_sweep.split(",") if x])

@@ -36,7 +36,7 @@ extern "C" {
 #define MARS_ERR_CAPACITY 3
 #define MARS_ERR_ARG 4
 
-#define MARS_ABI_VERSION 5
+#define MARS_ABI_VERSION 6
 
 /* phase codes: agentsched/engine.py:250-256 */
 #define MARS_WAITING_ADMISSION 0
@@ -222,6 +222,10 @@ typedef struct mars_step_out {
    * lists k_scan's grid radix refinement cut (bit 0 window, bit 1 victims),
    * its rounds, and the refined lists' lengths */
   int32_t n_fullscan, ref_flags, ref_rounds, n_window_ref, n_victim_ref;
+  /* MARS_MODE_SERVICE (ABI v6): per planned row (decodes, then prefills) its
+   * MLFQ state before the tick-end charge, (served_tokens_at_level << 8) |
+   * level, so a host that charges a different amount can undo the prediction */
+  const int64_t* plan_pre_charge;
 } mars_step_out;
 
 /* ---- lifecycle ------------------------------------------------------- */
@@ -258,6 +262,10 @@ int mars_output_arena(mars_ctx* ctx, void** base, int64_t* bytes);
 /* capture the whole step (both streams) as one CUDA graph; re-captured only
  * when the launch shape (rows, queue bucket, mode) changes */
 int mars_set_graph(mars_ctx* ctx, int on);
+/* replace the context's configuration (same policy): the reference builds its
+ * engine parameters per run (sim.py:90-110, GpuModel token_budget_per_tick /
+ * tick_duration_s, engine.py:24-29); drops the captured step graphs */
+int mars_set_config(mars_ctx* ctx, const mars_config* cfg);
 
 /* decide_retention (scheduler.py:190-213) for explicit inputs; elementwise f64
  * on the device, bit-exact (no FMA contraction). */

@@ -116,7 +116,7 @@ class MarsStepOut(C.Structure):
         ("end_blocks", P(i32)), ("end_pin", P(u8)), ("end_benefit", P(f64)),
         ("end_cost", P(f64)), ("end_deadline", P(f64)), ("prefill_done", P(u8)),
         ("n_fullscan", i32), ("ref_flags", i32), ("ref_rounds", i32),
-        ("n_window_ref", i32), ("n_victim_ref", i32),
+        ("n_window_ref", i32), ("n_victim_ref", i32), ("plan_pre_charge", P(i64)),
     ]
 
 
@@ -138,6 +138,7 @@ _SIGS = {
     "mars_step_enqueue": (i32, [C.c_void_p, P(MarsStepIn)]),
     "mars_step_fetch": (i32, [C.c_void_p, P(MarsStepOut)]),
     "mars_set_graph": (i32, [C.c_void_p, C.c_int]),
+    "mars_set_config": (i32, [C.c_void_p, C.c_void_p]),
     "mars_sync": (i32, [C.c_void_p]),
     "mars_shard_init": (i32, [C.c_void_p, C.c_int, C.c_int]),
     "mars_shard_buffers": (i32, [C.c_void_p, P(C.c_void_p), P(C.c_void_p), P(C.c_void_p),

@@ -33,7 +33,6 @@ struct mars_ctx {
   i64 last_resume_n = 0;
   bool own_stream = true;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_head = nullptr, ev_pack = nullptr;
-  cudaEvent_t ev_kvfork = nullptr, ev_kvjoin = nullptr;
   int pack_ctas = 20;
   mars_config hcfg;
   Cfg cfg;
@@ -272,8 +271,6 @@ int mars_create(const mars_config* hcfg, int device, int64_t max_rows, int64_t m
   CK(cudaStreamCreateWithFlags(&ctx->side2, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&ctx->ev_head, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&ctx->ev_pack, cudaEventDisableTiming));
-  CK(cudaEventCreateWithFlags(&ctx->ev_kvfork, cudaEventDisableTiming));
-  CK(cudaEventCreateWithFlags(&ctx->ev_kvjoin, cudaEventDisableTiming));
   {
     const char* e = getenv("MARS_PACK_CTAS");  // tuning knob: 0 disables the early pack
     if (e) ctx->pack_ctas = atoi(e);
@@ -379,6 +376,7 @@ int mars_create(const mars_config* hcfg, int device, int64_t max_rows, int64_t m
   ALLOC(b.pre_grant, WIN_MAX * 4);
   ALLOC(b.dec_level, WIN_MAX);
   ALLOC(b.pre_level, WIN_MAX);
+  ALLOC(b.svc_pre, WIN_MAX * 8);
   ALLOC(b.fin_row, WIN_MAX * 4);
   ALLOC(b.fin_pin, WIN_MAX);
   ALLOC(b.fin_b, WIN_MAX * 8);
@@ -472,7 +470,7 @@ int mars_destroy(mars_ctx* ctx) {
                 b.wc_lo, b.wc_row, b.vc_key, b.vc_whi, b.vc_wlo, b.vc_row, b.vc_blk, b.ret_row,
                 b.ret_pin, b.ret_b, b.ret_c, b.ret_d, b.admitted, b.win_rows, b.dec_rows,
                 b.pre_rows, b.pre_grant, b.ev_row, b.ev_kind, b.ev_blk, b.j_op, b.j_row, b.j_n,
-                b.dec_level, b.pre_level, b.fin_row, b.fin_pin, b.fin_b, b.fin_c, b.fin_d,
+                b.dec_level, b.pre_level, b.svc_pre, b.fin_row, b.fin_pin, b.fin_b, b.fin_c, b.fin_d,
                 b.flush, b.end_row, b.end_kind, b.end_blk, b.end_pin, b.end_b, b.end_c,
                 b.end_d, b.pre_done, b.vc_kl, b.wr_hi, b.wr_lo, b.wr_row, b.vr_key, b.vr_kl,
                 b.vr_whi, b.vr_wlo, b.vr_row, b.vr_blk, b.vs_key, b.vs_kl, b.vs_whi,
@@ -510,8 +508,6 @@ int mars_destroy(mars_ctx* ctx) {
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->ev_head) cudaEventDestroy(ctx->ev_head);
   if (ctx->ev_pack) cudaEventDestroy(ctx->ev_pack);
-  if (ctx->ev_kvfork) cudaEventDestroy(ctx->ev_kvfork);
-  if (ctx->ev_kvjoin) cudaEventDestroy(ctx->ev_kvjoin);
   if (ctx->side2) cudaStreamDestroy(ctx->side2);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->side) cudaStreamDestroy(ctx->side);
@@ -665,8 +661,6 @@ static LaunchArgs launch_args(mars_ctx* ctx, const mars_step_in* in) {
   a.side2 = ctx->side2;
   a.ev_head = ctx->ev_head;
   a.ev_pack = ctx->ev_pack;
-  a.ev_kvfork = ctx->ev_kvfork;
-  a.ev_kvjoin = ctx->ev_kvjoin;
   a.tab = ctx->tab;
   a.cfg = ctx->cfg;
   a.work = ctx->work;
@@ -796,6 +790,28 @@ int mars_set_graph(mars_ctx* ctx, int on) {
   return MARS_OK;
 }
 
+int mars_set_config(mars_ctx* ctx, const mars_config* hcfg) {
+  if (!ctx || !hcfg) return MARS_ERR_ARG;
+  if (hcfg->policy != ctx->hcfg.policy)
+    return fail(ctx, MARS_ERR_ARG, "mars_set_config cannot change the policy");
+  if (hcfg->window_size < 1 || hcfg->window_size > WIN_MAX || hcfg->num_levels < 1 ||
+      hcfg->num_levels > 4 || hcfg->block_size < 1 || hcfg->token_budget < 1 ||
+      hcfg->max_decode_slots < 0)
+    return fail(ctx, MARS_ERR_ARG, "invalid mars_config");
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(ctx->stream));
+  // the captured step graphs carry the old configuration as kernel parameters
+  for (auto& g : ctx->graph_exec)
+    if (g) {
+      cudaGraphExecDestroy(g);
+      g = nullptr;
+    }
+  memset(ctx->graph_key, 0, sizeof ctx->graph_key);
+  ctx->hcfg = *hcfg;
+  ctx->cfg = make_cfg(*hcfg);
+  return MARS_OK;
+}
+
 // place a device array in the pinned arena (copied by the one k_gather_out
 // launch of the fetch) and return its host address
 static const void* pull(mars_ctx* ctx, size_t& off, const void* dev, size_t bytes) {
@@ -866,6 +882,8 @@ int mars_step_fetch(mars_ctx* ctx, mars_step_out* o) {
   o->ret_deadline = (const double*)pull(ctx, off, b.ret_d, (size_t)w.n_ret * 8);
   o->decode_level = (const uint8_t*)pull(ctx, off, b.dec_level, (size_t)w.n_dec);
   o->prefill_level = (const uint8_t*)pull(ctx, off, b.pre_level, (size_t)w.n_pre);
+  if ((ctx->h_in->mode & MARS_MODE_SERVICE) && ctx->cfg.coord)
+    o->plan_pre_charge = (const int64_t*)pull(ctx, off, b.svc_pre, (size_t)(w.n_dec + w.n_pre) * 8);
   o->n_finish = w.n_finish;
   o->n_window_cand = w.n_wc;
   o->n_victim_cand = w.n_vc;

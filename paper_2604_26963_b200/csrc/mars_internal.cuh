@@ -204,6 +204,7 @@ struct Bufs {
   // plan outputs
   u32 *win_rows, *dec_rows, *pre_rows; i32 *pre_grant;
   u8 *dec_level, *pre_level;
+  i64* svc_pre;                // (served << 8) | level before the tick-end charge
   u32 *fin_row; u8 *fin_pin; double *fin_b, *fin_c, *fin_d;
   u32 *end_row; u8 *end_kind;  // MARS_MODE_ADVANCE: rounds that ended, decode order
   i32 *end_blk; u8 *end_pin; double *end_b, *end_c, *end_d;  // blocks pinned/freed, decision

@@ -3542,7 +3542,9 @@ __global__ void __launch_bounds__(WALK_TPB) k_walk(Tab t, Cfg c, Work* w, Bufs b
       i64 tokens = dec ? 1 : b.pre_grant[i - nd];
       u32 lv = t.level[r];
       if ((mode & MARS_MODE_SERVICE) && c.coord) {
-        i64 served = t.served[r] + tokens;
+        const i64 served0 = t.served[r];
+        b.svc_pre[i] = (served0 << 8) | (i64)lv;
+        i64 served = served0 + tokens;
         if (served > c.quotas[lv] && (int)lv < c.num_levels - 1) {
           lv += 1;
           served = 0;
@@ -4075,18 +4077,6 @@ int mars_enqueue_step(const LaunchArgs* a) {
     }
     mark(1, 1, s);
   }
-  if (a->kv) {
-    // S5, expired pins: their tables return to the free stack (segment pushes
-    // by the whole grid) on the second side stream, concurrently with the
-    // control plane and the walk; the journal apply after the join waits
-    cudaEventRecord(a->ev_kvfork, s);
-    cudaStreamWaitEvent(a->side2, a->ev_kvfork, 0);
-    mark(5, 0, a->side2);
-    mars_kv_enqueue_exp_free(*a->kv, a->side2, a->work, a->bufs, nsm);
-    mark(5, 1, a->side2);
-    cudaEventRecord(a->ev_kvjoin, a->side2);
-    launches += 2;
-  }
   if (a->control_possible) {
     i64 lgq = (a->queue_upper + a->ctl_per_cta - 1) / a->ctl_per_cta;  // list entries per CTA
     int lg = (int)(lgq < 1 ? 1 : (lgq > nsm - 1 ? nsm - 1 : lgq));  // the walk keeps one SM
@@ -4109,13 +4099,24 @@ int mars_enqueue_step(const LaunchArgs* a) {
     mark(2, 1, s);
     launches++;
   }
+  if (a->kv) {
+    // S5, expired pins: their tables return to the free stack (segment pushes
+    // by the whole grid) after the control plane, while the walk -- the longer
+    // branch -- is still running.  (Not on a third stream beside the control
+    // plane: the walk may spin on the admission's completion flag, and with
+    // the early pack on the second side stream that arrangement was seen to
+    // starve k_control, r2.)
+    mark(5, 0, s);
+    mars_kv_enqueue_exp_free(*a->kv, s, a->work, a->bufs, nsm);
+    mark(5, 1, s);
+    launches += 2;
+  }
   cudaStreamWaitEvent(s, a->ev_join, 0);
   if (a->advance) {
     k_advance<<<1, 1024, 0, s>>>(a->tab, a->cfg, a->work, a->bufs, a->sc);
     launches++;
   }
   if (a->kv) {
-    cudaStreamWaitEvent(s, a->ev_kvjoin, 0);
     mark(6, 0, s);
     mars_kv_enqueue_apply_step(*a->kv, s, a->work, a->bufs);
     mark(6, 1, s);

@@ -116,15 +116,58 @@ __device__ __forceinline__ FreePlan free_plan(i64 L, i64 keep) {
   return f;
 }
 
-// arena segment holding table positions [p0, p0 + c) of `row` in pop order
-__device__ __forceinline__ void arena_fill(const Kv& k, u32 row, i64 p0, i64 c, i64 base) {
-  for (i64 j = 0; j < c; ++j) k.arena[base + c - 1 - j] = *kv_slot_ptr(k, row, p0 + j);
+// one per-block scratch area shared by the run kernels (a static __shared__
+// inside a device function is one allocation per CTA, whatever the call site)
+#define KV_SCRATCH (KV_TPB * 32)
+__device__ __forceinline__ unsigned char* kv_scratch() {
+  __shared__ __align__(16) unsigned char buf[KV_SCRATCH];
+  return buf;
 }
 
-// One run of frees (distinct rows; n < 0: the whole table), <= KV_TPB ops,
-// one per thread, on the whole CTA.  Free i pushes its segments above those of
-// frees 0..i-1; its first freed ID ends on top.
+// Freeing table positions [keep, L) of `row` (FreePlan f), on one warp: the
+// segments go to seg[sp..] bottom -> top (T's arena segment, the whole chunks
+// from the last one down, H's arena segment), the loose IDs of T and H to the
+// arena at ap.. (each segment pops from its end), T's chunk back to the pool
+// at cfs[cf] (cf < 0: none); the lanes copy IDs / write segments in parallel.
+__device__ __forceinline__ void kv_free_warp(const Kv& k, u32 row, const FreePlan& f, i64 sp,
+                                             i64 ap, i64 cf, int lane) {
+  const u32* dr = k.dir + (i64)row * k.D;
+  if (f.nt > 0) {
+    for (i64 j = lane; j < f.nt; j += 32) {
+      const i64 p = f.tb + j;
+      k.arena[ap + f.nt - 1 - j] = k.chunks[(i64)dr[p / KV_CH] * KV_CH + p % KV_CH];
+    }
+    if (lane == 0) k.seg[sp] = seg_arena_make(ap, (u32)f.nt);
+    ++sp;
+    ap += f.nt;
+  }
+  const i64 nf = f.f1 - f.f0;
+  for (i64 j = lane; j < nf; j += 32) k.seg[sp + j] = seg_chunk_make(dr[f.f1 - 1 - j], 0, KV_CH);
+  sp += nf;
+  if (f.nh > 0) {
+    for (i64 j = lane; j < f.nh; j += 32) {
+      const i64 p = f.keep + j;
+      k.arena[ap + f.nh - 1 - j] = k.chunks[(i64)dr[p / KV_CH] * KV_CH + p % KV_CH];
+    }
+    if (lane == 0) k.seg[sp] = seg_arena_make(ap, (u32)f.nh);
+  }
+  if (lane == 0) {
+    if (cf >= 0) k.cfs[cf] = dr[(f.L - 1) / KV_CH];
+    k.len[row] = (i32)f.keep;
+  }
+}
+
+// One run of frees (distinct rows; n < 0: the whole table), <= KV_TPB ops, on
+// the whole CTA.  Free i pushes its segments above those of frees 0..i-1; its
+// first freed ID ends on top.  Thread i plans op i (prefix sums give every
+// op's segment / arena / chunk-pool offsets), then one warp per op writes it.
 __device__ bool kv_free_run(Kv& k, int m, const u32* rows, const i32* ns) {
+  u32* o_row = (u32*)kv_scratch();
+  i32* o_L = (i32*)(o_row + KV_TPB);
+  i32* o_keep = o_L + KV_TPB;
+  u32* o_so = (u32*)(o_keep + KV_TPB);
+  u32* o_ao = o_so + KV_TPB;
+  i32* o_ro = (i32*)(o_ao + KV_TPB);
   const int i = threadIdx.x;
   u32 row = 0;
   i64 L = 0, n = 0;
@@ -151,21 +194,22 @@ __device__ bool kv_free_run(Kv& k, int m, const u32* rows, const i32* ns) {
     if (threadIdx.x == 0) k.s->status |= 32;
     return false;
   }
-  if (n > 0) {
-    i64 sp = s0 + soff, ap = a0 + aoff;
-    if (f.nt > 0) {
-      arena_fill(k, row, f.tb, f.nt, ap);
-      k.seg[sp++] = seg_arena_make(ap, (u32)f.nt);
-      ap += f.nt;
-    }
-    for (i64 j = f.f1 - 1; j >= f.f0; --j)
-      k.seg[sp++] = seg_chunk_make(k.dir[(i64)row * k.D + j], 0, KV_CH);
-    if (f.nh > 0) {
-      arena_fill(k, row, f.keep, f.nh, ap);
-      k.seg[sp++] = seg_arena_make(ap, (u32)f.nh);
-    }
-    if (f.tail_chunk) k.cfs[c0 + roff] = k.dir[(i64)row * k.D + (L - 1) / KV_CH];
-    k.len[row] = (i32)f.keep;
+  if (i < m) {
+    o_row[i] = row;
+    o_L[i] = (i32)L;
+    o_keep[i] = (i32)(n > 0 ? L - n : L);
+    o_so[i] = (u32)soff;
+    o_ao[i] = (u32)aoff;
+    o_ro[i] = f.tail_chunk ? (i32)roff : -1;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  for (int o = threadIdx.x >> 5; o < m; o += KV_TPB / 32) {
+    const i64 Lo = o_L[o], ko = o_keep[o];
+    if (ko == Lo) continue;  // nothing freed
+    FreePlan g = free_plan(Lo, ko);
+    kv_free_warp(k, o_row[o], g, s0 + o_so[o], a0 + o_ao[o], o_ro[o] < 0 ? -1 : c0 + o_ro[o],
+                 lane);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -223,8 +267,11 @@ __device__ void kv_settle(Kv& k, const u64* segs, const i64* cum, int nseg, i64 
 // reaching deeper (only a host replay popping > KV_TPB small segments at
 // once) pops one ID at a time on thread 0.
 __device__ bool kv_alloc_run(Kv& k, int m, const u32* rows, const i32* ns) {
-  __shared__ i64 s_cum[KV_TPB];
-  __shared__ u64 s_seg[KV_TPB];
+  i64* s_cum = (i64*)kv_scratch();
+  u64* s_seg = (u64*)(s_cum + KV_TPB);
+  i64* s_noff = (i64*)(s_seg + KV_TPB);
+  u32* s_orow = (u32*)(s_noff + KV_TPB);
+  i32* s_oL = (i32*)(s_orow + KV_TPB);
   const int i = threadIdx.x;
   u32 row = 0;
   i64 L = 0, n = 0;
@@ -262,24 +309,34 @@ __device__ bool kv_alloc_run(Kv& k, int m, const u32* rows, const i32* ns) {
     i64 t;
     kv_scan((i < top && ex < F) ? 1 : 0, &t);
     const int nseg = (int)t;  // segments touched: those starting before F
-    if (n > 0) {
-      for (i64 q = 0; q < n; ++q) {
-        const i64 p = noff + q;
-        u32 id;
-        if (p < F) {
-          int lo = 0, hi = nseg - 1;
-          while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (s_cum[mid] <= p) lo = mid; else hi = mid - 1;
-          }
-          id = seg_id(k, s_seg[lo], p - s_cum[lo]);
-        } else {
-          id = (u32)(fresh + (p - F));
-        }
-        *kv_slot_ptr(k, row, L + q) = id;
-      }
-      k.len[row] = (i32)(L + n);
+    if (i < m) {
+      s_noff[i] = noff;
+      s_orow[i] = row;
+      s_oL[i] = (i32)L;
     }
+    __syncthreads();  // (the new chunks' directory entries are written too)
+    // pop p of the run -> alloc op (last op starting at or before p; ops
+    // with n = 0 start where the next one does) -> its table slot
+    for (i64 p = threadIdx.x; p < N; p += KV_TPB) {
+      int lo = 0, hi = m - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s_noff[mid] <= p) lo = mid; else hi = mid - 1;
+      }
+      u32 id;
+      if (p < F) {
+        int a = 0, b2 = nseg - 1;
+        while (a < b2) {
+          const int mid = (a + b2 + 1) >> 1;
+          if (s_cum[mid] <= p) a = mid; else b2 = mid - 1;
+        }
+        id = seg_id(k, s_seg[a], p - s_cum[a]);
+      } else {
+        id = (u32)(fresh + (p - F));
+      }
+      *kv_slot_ptr(k, s_orow[lo], (i64)s_oL[lo] + (p - s_noff[lo])) = id;
+    }
+    if (n > 0) k.len[row] = (i32)(L + n);
     __syncthreads();
     if (threadIdx.x == 0) {
       kv_settle(k, s_seg, s_cum, nseg, F, top, ctop - Cn);
@@ -350,40 +407,38 @@ __device__ void kv_apply_list(Kv& k, i64 n_ops, const u8* op, const u32* row, co
                               bool journal) {
   __shared__ u32 s_row[KV_TPB];
   __shared__ i32 s_n[KV_TPB];
-  __shared__ int s_m, s_kind;
+  __shared__ u8 s_kd[KV_TPB];
+  __shared__ int s_m;
+  const int t = threadIdx.x;
   i64 i = 0;
   while (i < n_ops) {
-    if (threadIdx.x == 0) {
-      // extend the run while the kind matches and rows stay distinct (a
-      // linear check: runs are short)
-      int kind = -1, m = 0;
-      while (i + m < n_ops && m < KV_TPB) {
-        const int o = op[i + m];
-        int kd;
-        if (journal) kd = (o == MARS_J_ALLOC) ? 1 : 2;
-        else kd = (o == MARS_KV_ALLOC) ? 1 : (o == MARS_KV_FREE ? 2 : 0);
-        if (kd == 0) {  // pin / unpin: ends a run, skipped
-          if (m == 0) {
-            kind = 0;
-            m = 1;
-          }
-          break;
-        }
-        if (kind < 0) kind = kd;
-        if (kd != kind) break;
-        const u32 r = row[i + m];
-        bool dup = false;
-        for (int q = 0; q < m; ++q) dup |= s_row[q] == r;
-        if (dup) break;
-        s_row[m] = r;
-        s_n[m] = (journal && kd == 2) ? -1 : n[i + m];
-        ++m;
+    // the next window of ops, one per thread
+    const bool valid = i + t < n_ops;
+    int kd = 3;  // past the end
+    if (valid) {
+      const int o = op[i + t];
+      if (journal) kd = (o == MARS_J_ALLOC) ? 1 : 2;
+      else kd = (o == MARS_KV_ALLOC) ? 1 : (o == MARS_KV_FREE ? 2 : 0);
+      s_row[t] = row[i + t];
+      s_n[t] = (journal && kd == 2) ? -1 : n[i + t];
+    }
+    s_kd[t] = (u8)kd;
+    if (t == 0) s_m = KV_TPB;
+    __syncthreads();
+    // the run is the longest prefix of one kind (alloc or free) with distinct
+    // rows; a pin / unpin (no table change) is a run of its own, skipped.
+    // Every thread tests whether its op ends the run (in parallel).
+    const int kind = s_kd[0];
+    if (t > 0) {
+      bool stop = kind == 0 || kd != kind;
+      if (!stop) {
+        const u32 r = s_row[t];
+        for (int q = 0; q < t && !stop; ++q) stop = s_row[q] == r;
       }
-      s_m = m;
-      s_kind = kind;
+      if (stop) atomicMin(&s_m, t);
     }
     __syncthreads();
-    const int m = s_m, kind = s_kind;
+    const int m = s_m;
     bool ok = true;
     if (kind == 1) ok = kv_alloc_run(k, m, s_row, s_n);
     else if (kind == 2) ok = kv_free_run(k, m, s_row, s_n);
@@ -401,16 +456,18 @@ __global__ void __launch_bounds__(KV_TPB) k_kv_apply(Kv k, i64 n_ops, const u8* 
 
 // The step's expired pins (rank order), freed as one run by the whole grid:
 // k_kv_exp_scan (one CTA) computes every table's segment / arena / chunk
-// offsets and moves the scalars, k_kv_exp_push writes the segments (one
-// thread each; the thread of a table's tail segment also copies its < 64
-// loose IDs to the arena and returns the chunk).
+// offsets and moves the scalars, k_kv_exp_push writes each table's segments
+// and loose IDs with one warp per table.
 __global__ void __launch_bounds__(KV_TPB) k_kv_exp_scan(Kv k, const Work* w, Bufs b) {
   const int ne = w->n_exp;
   const int per = (ne + KV_TPB - 1) / KV_TPB;
   const int i0 = threadIdx.x * per, i1 = min(ne, i0 + per);
+  // a pinned session's table is exactly its pinned blocks (a pin moves the
+  // whole table, engine.py:190-200): the lengths come with the expired list
+  // (coalesced), k_kv_exp_push checks them against the tables
   i64 segs = 0, ids = 0, ar = 0, rc = 0;
   for (int i = i0; i < i1; ++i) {
-    const i64 L = k.len[b.exp_row_sorted[i]];
+    const i64 L = __ldcg(&b.exp_blk_sorted[i]);
     k.xlen[i] = (i32)L;
     segs += L / KV_CH + ((L % KV_CH) ? 1 : 0);
     ar += L % KV_CH;
@@ -430,14 +487,13 @@ __global__ void __launch_bounds__(KV_TPB) k_kv_exp_scan(Kv k, const Work* w, Buf
     so += L / KV_CH + ((L % KV_CH) ? 1 : 0);
     ao += L % KV_CH;
     ro += (L % KV_CH) ? 1 : 0;
-    k.len[b.exp_row_sorted[i]] = 0;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     const i64 s0 = k.s->seg_top;
     if (s0 + S > k.seg_cap) {
       k.s->status |= 32;
-      k.xbase[1] = 0;
+      k.xbase[1] = -1;
       return;
     }
     k.xbase[0] = s0;
@@ -451,30 +507,31 @@ __global__ void __launch_bounds__(KV_TPB) k_kv_exp_scan(Kv k, const Work* w, Buf
   }
 }
 
+// a whole table: T = its partial last chunk (loose IDs to the arena, the
+// chunk back to the pool), then its full chunks from the last one down
 __global__ void k_kv_exp_push(Kv k, const Work* w, Bufs b) {
   const int ne = w->n_exp;
-  const i64 base = k.xbase[0], S = k.xbase[1], a0 = k.xbase[2], c0 = k.xbase[3];
-  for (i64 g = (i64)blockIdx.x * blockDim.x + threadIdx.x; g < S;
-       g += (i64)gridDim.x * blockDim.x) {
-    int lo = 0, hi = ne - 1;  // the free owning segment g: last xoff <= g
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (k.xoff[mid] <= g) lo = mid; else hi = mid - 1;
-    }
-    const u32 row = b.exp_row_sorted[lo];
-    const i64 L = k.xlen[lo], tail = L % KV_CH, full = L / KV_CH;
-    i64 j = g - k.xoff[lo];  // 0 = bottom
-    if (tail) {
-      if (j == 0) {  // the partial last chunk: loose IDs to the arena
-        const i64 ap = a0 + k.xaoff[lo];
-        arena_fill(k, row, full * KV_CH, tail, ap);
-        k.seg[base + g] = seg_arena_make(ap, (u32)tail);
-        k.cfs[c0 + k.xroff[lo]] = k.dir[(i64)row * k.D + full];
-        continue;
-      }
-      --j;
-    }
-    k.seg[base + g] = seg_chunk_make(k.dir[(i64)row * k.D + (full - 1 - j)], 0, KV_CH);
+  if (__ldcg(&k.xbase[1]) < 0) return;  // the stack overflowed (status set)
+  const i64 base = k.xbase[0], a0 = k.xbase[2], c0 = k.xbase[3];
+  const int lane = threadIdx.x & 31;
+  for (int e = (int)(((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5); e < ne;
+       e += (int)(((i64)gridDim.x * blockDim.x) >> 5)) {
+    const u32 row = b.exp_row_sorted[e];
+    const i64 L = k.xlen[e];
+    if (lane == 0 && k.len[row] != L) k.s->status |= 64;  // table != pinned blocks
+    const i64 tail = L % KV_CH, full = L / KV_CH;
+    FreePlan f;
+    f.keep = 0;
+    f.L = L;
+    f.nh = 0;
+    f.f0 = 0;
+    f.f1 = full;
+    f.tb = full * KV_CH;
+    f.nt = tail;
+    f.hb = 0;
+    f.tail_chunk = tail > 0;
+    kv_free_warp(k, row, f, base + k.xoff[e], a0 + k.xaoff[e],
+                 tail > 0 ? c0 + k.xroff[e] : -1, lane);
   }
 }
 
@@ -595,7 +652,8 @@ int mars_kv_enqueue_apply(const Kv& k, cudaStream_t s, i64 n_ops, const u8* op, 
 
 int mars_kv_enqueue_exp_free(const Kv& k, cudaStream_t s, Work* w, const Bufs& b, int grid) {
   k_kv_exp_scan<<<1, KV_TPB, 0, s>>>(k, w, b);
-  k_kv_exp_push<<<grid, 256, 0, s>>>(k, w, b);
+  // small CTAs: they also fit beside the walk's CTA, which may still run
+  k_kv_exp_push<<<4 * grid, 256, 0, s>>>(k, w, b);
   return (int)cudaGetLastError();
 }
 

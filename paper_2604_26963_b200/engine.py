@@ -99,6 +99,7 @@ class StepResult:
     end_cost: np.ndarray
     end_deadline: np.ndarray
     prefill_done: np.ndarray   # MARS_MODE_ADVANCE: the grant finished the prefill
+    plan_pre_charge: np.ndarray  # MARS_MODE_SERVICE: (served << 8) | level before the charge
     n_ready: int
     n_promoted: int
     pack_mode: int
@@ -285,6 +286,11 @@ class MarsEngine:
         si.mode = int(mode) | (N.MODE_RANK_ORDERED if self.rank_ordered else 0)
         return si
 
+    def set_config(self, cfg: N.MarsConfig) -> None:
+        """Replaces the configuration (same policy) of a live context."""
+        self._check(self.lib.mars_set_config(self.ctx, C.byref(cfg)))
+        self.cfg = cfg
+
     def set_graph(self, on: bool) -> None:
         self._check(self.lib.mars_set_graph(self.ctx, int(bool(on))))
 
@@ -306,6 +312,12 @@ class MarsEngine:
             else:
                 s0 = p - base
                 arrs[name] = arena[s0:s0 + n * isz].view(dt).copy()
+        npc = int(o.n_decode) + int(o.n_prefill)
+        if o.plan_pre_charge and npc:
+            s0 = int(C.cast(o.plan_pre_charge, C.c_void_p).value) - base
+            arrs["plan_pre_charge"] = arena[s0:s0 + npc * 8].view(np.int64).copy()
+        else:
+            arrs["plan_pre_charge"] = np.empty(0, np.int64)
         return StepResult(
             status=o.status, **arrs,
             n_ready=o.n_ready, n_promoted=o.n_promoted, pack_mode=o.pack_mode,
@@ -369,6 +381,8 @@ class MarsEngine:
             end_cost=_arr(o.end_cost, o.n_round_end, np.float64),
             end_deadline=_arr(o.end_deadline, o.n_round_end, np.float64),
             prefill_done=_arr(o.prefill_done, o.n_prefill if o.prefill_done else 0, np.uint8),
+            plan_pre_charge=_arr(o.plan_pre_charge,
+                                 (o.n_decode + o.n_prefill) if o.plan_pre_charge else 0, np.int64),
             n_ready=o.n_ready, n_promoted=o.n_promoted, pack_mode=o.pack_mode,
             total_tokens=o.total_tokens, free_after_expiry=o.free_after_expiry,
             free_blocks=o.free_blocks, limit=o.limit, slots=o.slots,

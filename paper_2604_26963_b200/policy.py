@@ -41,7 +41,7 @@ def _i64(x) -> int:
     return 2**63 - 1 if x == math.inf else int(x)
 
 
-class Victim:
+class _Victim:
     """scheduler.py:221-225 (fields read by the sim's evictor, sim.py:186-188)."""
 
     __slots__ = ("session_id", "kind", "blocks")
@@ -53,7 +53,7 @@ class Victim:
         return f"Victim({self.session_id!r}, {self.kind!r}, {self.blocks})"
 
 
-class TickPlan:
+class _TickPlan:
     """scheduler.py:275-280."""
 
     def __init__(self) -> None:
@@ -63,7 +63,7 @@ class TickPlan:
         self.total_tokens = 0
 
 
-class RetentionDecision:
+class _RetentionDecision:
     """scheduler.py:175-180."""
 
     __slots__ = ("pin", "benefit_s", "cost_s", "retention_deadline")
@@ -71,6 +71,18 @@ class RetentionDecision:
     def __init__(self, pin: bool, benefit_s: float, cost_s: float, retention_deadline: float):
         self.pin, self.benefit_s, self.cost_s = pin, benefit_s, cost_s
         self.retention_deadline = retention_deadline
+
+
+# Inside the reference's own process (agentsched importable) the drop-ins ARE
+# PolicyBase plugins and hand back the reference's plan / victim / decision
+# types (baselines.py:56-101, scheduler.py:175-180, 221-225, 275-280);
+# standalone they use the field-compatible classes above.
+try:
+    from agentsched.baselines import PolicyBase as _PolicyBase
+    from agentsched.scheduler import RetentionDecision, TickPlan, Victim
+except ImportError:  # the reference package is not installed
+    _PolicyBase = object
+    RetentionDecision, TickPlan, Victim = _RetentionDecision, _TickPlan, _Victim
 
 
 def config_from(mlfq=None, retention=None, pressure=None, controller=None,
@@ -111,8 +123,9 @@ def config_from(mlfq=None, retention=None, pressure=None, controller=None,
     return cfg
 
 
-class GpuMarsPolicy:
-    """B200 drop-in for MarsPolicy (baselines.py:318-455)."""
+class GpuMarsPolicy(_PolicyBase):
+    """B200 drop-in for MarsPolicy (baselines.py:318-455); a PolicyBase
+    subclass whenever the reference package is importable."""
 
     name = "mars"
     uses_admission_control = True
@@ -146,7 +159,8 @@ class GpuMarsPolicy:
         self._levels: Dict[str, int] = {}       # sid -> MLFQ level (device value)
         self._admitted: set = set()
         self._fin: Dict[str, tuple] = {}        # sid -> (ctx, kv, now, usage, ema, decision)
-        self._service: Dict[str, tuple] = {}    # sid -> (tokens, tick_end) charged on device
+        # sid -> (tokens, tick_end, level, served before the charge): charged on device
+        self._service: Dict[str, tuple] = {}
         self._replaying = False
         self.last_window: List[str] = []
         b = getattr(mlfq, "level_boundaries_tokens", (4_000, 32_000, 128_000, math.inf))
@@ -157,17 +171,17 @@ class GpuMarsPolicy:
     # -- device context ---------------------------------------------------------
 
     def _engine(self, gpu=None) -> MarsEngine:
-        if self.eng is not None:
-            if gpu is not None and (gpu.token_budget_per_tick, gpu.tick_duration_s) != (
-                    self.eng.cfg.token_budget, self.eng.cfg.tick_duration_s):
-                if self._sid:
-                    raise ContractViolation("GpuModel changed after sessions were registered")
-                self.eng.close()
-                self.eng = None
         if self.eng is None:
             cfg = config_from(gpu=gpu, **self._cfg_args)
+            self._gpu_key = (cfg.token_budget, cfg.tick_duration_s)
             self.eng = MarsEngine(max_rows=self._max, max_queue=1, device=self._device,
                                   config=cfg)
+        elif gpu is not None and (gpu.token_budget_per_tick, gpu.tick_duration_s) != self._gpu_key:
+            # the sim registers and admits sessions before the first plan_tick
+            # hands over the GpuModel (sim.py:165, :297, :342): the engine
+            # parameters change in place, the registered rows stay
+            self._gpu_key = (gpu.token_budget_per_tick, gpu.tick_duration_s)
+            self.eng.set_config(config_from(gpu=gpu, **self._cfg_args))
         return self.eng
 
     def close(self) -> None:
@@ -198,8 +212,8 @@ class GpuMarsPolicy:
                     "flags": np.zeros(1, np.uint8), "rank": np.array([r], np.uint32),
                     "arrival": np.array([call.arrival_time], np.float64)},
                    rows=np.array([r]))
-        if self._ranks_dirty:
-            self._sync_ranks()
+        # ranks only order the device step's keys: one re-rank in the next
+        # plan_tick covers every out-of-order registration before it
 
     def _sync_ranks(self) -> None:
         order = sorted(range(len(self._sid)), key=self._sid.__getitem__)
@@ -237,14 +251,18 @@ class GpuMarsPolicy:
         if session_id not in self._admitted or not self.enable_coordinator:
             return
         exp = self._service.pop(session_id, None)
-        if exp is not None and exp == (tokens, now):
+        if exp is not None and exp[:2] == (tokens, now):
             return  # already charged by the device step at tick end
-        # a charge the plan did not predict: apply it to the device row
-        r = self._row[session_id]
-        st = self._engine().read(["level", "served"], rows=np.array([r]))
-        lv, served = int(st["level"][0]), int(st["served"][0]) + int(tokens)
         if tokens < 0:
             raise ContractViolation("cannot charge negative service")
+        r = self._row[session_id]
+        if exp is not None:
+            # the device charged its prediction: charge this amount from the
+            # state before it instead (scheduler.py:100-108)
+            lv, served = exp[2], exp[3] + int(tokens)
+        else:  # a charge the plan did not predict: apply it to the device row
+            st = self._engine().read(["level", "served"], rows=np.array([r]))
+            lv, served = int(st["level"][0]), int(st["served"][0]) + int(tokens)
         q = list(getattr(self.mlfq, "level_quotas_tokens", (2_000, 8_000, 32_000, math.inf)))
         if served > q[lv] and lv < self._levels_n - 1:
             lv, served = lv + 1, 0
@@ -254,9 +272,12 @@ class GpuMarsPolicy:
         self._levels[session_id] = lv
 
     def level_of(self, call) -> int:
+        """The MLFQ level now (baselines.py:370-372): the device row, which
+        the step's promote_waiting and charges keep current."""
         if not self.enable_coordinator:
             return 0
-        return self._levels[call.session_id]
+        r = self._row[call.session_id]
+        return int(self._engine().read(["level"], rows=np.array([r]))["level"][0])
 
     def retention_decision(self, call, pool, telemetry, gpu, now):
         if not self.enable_coscheduler:
@@ -277,7 +298,9 @@ class GpuMarsPolicy:
     def note_pin(self, call, decision, blocks: int, now: float) -> None:
         sid = call.session_id
         r = self._row[sid]
-        lv = self.level_of(call)
+        # the round that ends here was planned this tick, so its post-charge
+        # level came back with the step (no device read)
+        lv = self._levels[sid] if self.enable_coordinator else 0
         self._engine().upsert({"flags": np.array([F_ACTIVE | F_PINNED], np.uint8),
                                "deadline": np.array([decision.retention_deadline], np.float64),
                                "pinned_blocks": np.array([blocks], np.int32),
@@ -397,13 +420,18 @@ class GpuMarsPolicy:
         plan.total_tokens = int(res.total_tokens)
         tick_end = now + gpu.tick_duration_s
         self._service.clear()
-        for r, lv in zip(res.decode_rows.tolist(), res.decode_level.tolist()):
+        pre = res.plan_pre_charge.tolist()
+        if not pre:
+            pre = [0] * (len(res.decode_rows) + len(res.prefill_rows))
+        nd = len(res.decode_rows)
+        for i, (r, lv) in enumerate(zip(res.decode_rows.tolist(), res.decode_level.tolist())):
             self._levels[sid[r]] = lv
-            self._service[sid[r]] = (1, tick_end)
-        for (r, g), lv in zip(zip(res.prefill_rows.tolist(), res.prefill_grants.tolist()),
-                              res.prefill_level.tolist()):
+            self._service[sid[r]] = (1, tick_end, pre[i] & 0xff, pre[i] >> 8)
+        for i, ((r, g), lv) in enumerate(zip(zip(res.prefill_rows.tolist(),
+                                                 res.prefill_grants.tolist()),
+                                             res.prefill_level.tolist())):
             self._levels[sid[r]] = lv
-            self._service[sid[r]] = (g, tick_end)
+            self._service[sid[r]] = (g, tick_end, pre[nd + i] & 0xff, pre[nd + i] >> 8)
         self._fin.clear()
         ema_v = self._tool_prior if ema is None else ema
         for r, p, b, c, d in zip(res.fin_rows.tolist(), res.fin_pin.tolist(),

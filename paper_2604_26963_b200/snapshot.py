@@ -168,14 +168,19 @@ def snapshot_v1(n: int, seed: int = 0, pool: str = "headroom", now: float = 1000
                     meta={"kind": "snapshot_v1", "n": n, "seed": seed, "pool": pool, "mix": "A"})
 
 
-def snapshot_shard(snap: Snapshot, G: int, g: int) -> Snapshot:
+def snapshot_shard(snap: Snapshot, G: int, g: int, box_global: bool = False) -> Snapshot:
     """Row shard ``g`` of ``G`` (rows ``r`` with ``r % G == g``, SURVEY.md
     §8(e): session row -> replica ``sid_rank mod G``; ``snapshot_v1`` ranks
-    equal rows).  The shard is a replica of its own: its rows keep their
-    session ids (rank), its pool holds its own rows' blocks with the same
-    headroom rule (or the same +8 slack under pressure), its admission list is
-    its rows in the global list order, and the tool plane / admission window
-    scale with its size."""
+    equal rows).  Its rows keep their session ids (rank), its pool holds its
+    own rows' blocks with the same headroom rule (or the same +8 slack under
+    pressure), its admission list is its rows in the global list order, and
+    ``meta["gpos"]`` holds each of those entries' position in the global list.
+
+    ``box_global=False``: the shard is an independent replica (the tool plane
+    and admission window scale with its size).  ``box_global=True``: one
+    replica of a sharded engine (config 3): the tool-plane counters, worker
+    slots and the admission window stay the box's (identical on every rank),
+    as the sharded control plane sees them (oracle/multi.py)."""
     if not (0 <= g < G):
         raise ValueError((G, g))
     rows = np.arange(g, snap.n, G)
@@ -196,10 +201,17 @@ def snapshot_shard(snap: Snapshot, G: int, g: int) -> Snapshot:
     fl = c["flags"]
     waiting = (fl & F_QUEUED) != 0
     c["flags"][:] = (fl & ~np.uint8(F_LONG)) | np.where(waiting & long_, F_LONG, 0).astype(np.uint8)
-    meta = dict(snap.meta, shard=(G, g), n=n)
+    meta = dict(snap.meta, shard=(G, g), n=n,
+                gpos=np.nonzero(snap.queue % G == g)[0].astype(np.uint32))
+    if box_global:
+        slots, tools, qtools, win = (snap.worker_slots, snap.active_tools, snap.queued_tools,
+                                     snap.initial_window)
+    else:
+        slots, tools, qtools, win = (max(2 * n, 1), int((c["phase"] == TOOL).sum()), 0,
+                                     float(max(2 * n, 8)))
     return Snapshot(cols=c, queue=queue, now=snap.now, total_blocks=int(total),
-                    free_blocks=int(total - total_held), worker_slots=max(2 * n, 1),
-                    active_tools=int((c["phase"] == TOOL).sum()), queued_tools=0,
-                    initial_window=float(max(2 * n, 8)), ema_tool=snap.ema_tool,
+                    free_blocks=int(total - total_held), worker_slots=slots,
+                    active_tools=tools, queued_tools=qtools,
+                    initial_window=win, ema_tool=snap.ema_tool,
                     ema_blocks=snap.ema_blocks, blocks_seed=snap.blocks_seed,
                     telemetry=dict(snap.telemetry), meta=meta)

@@ -23,23 +23,29 @@ from oracle.multi import run_multi_step
 from oracle.snapshot_step import ToolCounts, World
 from paper_2604_26963_b200.dist import (COUNTERS, decode_gathered, encode_queue, exchange,
                                         interleaved_gpos)
-from paper_2604_26963_b200.snapshot import snapshot_v1
+from paper_2604_26963_b200.snapshot import snapshot_shard, snapshot_v1
 
 N_PER_RANK = 1500
 WORLD = 2
 
 
-def shards():
+def shards(kind="independent"):
+    if kind == "global":
+        # config (3): ONE global snapshot, rows sharded rank mod G, every
+        # admission entry at its position in the global list
+        glob = snapshot_v1(WORLD * N_PER_RANK, seed=95, pool="headroom")
+        snaps = [snapshot_shard(glob, WORLD, g, box_global=True) for g in range(WORLD)]
+        return snaps, [s.meta["gpos"].tolist() for s in snaps]
     snaps = [snapshot_v1(N_PER_RANK, seed=90 + g, pool="headroom") for g in range(WORLD)]
     gpos = interleaved_gpos([len(s.queue) for s in snaps])
     return snaps, gpos
 
 
-def _worker(rank, port, out):
+def _worker(rank, port, out, kind="independent"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=WORLD)
-    snaps, gpos = shards()
+    snaps, gpos = shards(kind)
     snap = snaps[rank]
     w = World(snap)
     # replica-local expiry + probe (what k_scan leaves in xc)
@@ -83,12 +89,13 @@ def _free_port():
     return p
 
 
-def test_two_rank_exchange_reproduces_the_sharded_oracle():
-    snaps, gpos = shards()
+@pytest.mark.parametrize("kind", ["independent", "global"])
+def test_two_rank_exchange_reproduces_the_sharded_oracle(kind):
+    snaps, gpos = shards(kind)
     want = run_multi_step([s.copy() for s in snaps], gpos)["control"]
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(_free_port(), out), nprocs=WORLD, join=True)
+    mp.spawn(_worker, args=(_free_port(), out, kind), nprocs=WORLD, join=True)
     for rank in range(WORLD):
         got, qlen, w_adm = out[rank]
         assert got == [tuple(x) for x in want["admitted_global"]]

@@ -14,7 +14,7 @@ import torch
 from oracle.multi import run_multi_step
 from paper_2604_26963_b200.dist import COUNTERS, ShardedEngine, interleaved_gpos
 from paper_2604_26963_b200.engine import MarsEngine, canonical, make_config
-from paper_2604_26963_b200.snapshot import F_LONG, snapshot_v1
+from paper_2604_26963_b200.snapshot import F_LONG, snapshot_shard, snapshot_v1
 from tests._canon import canon
 
 pytestmark = pytest.mark.gpu
@@ -53,12 +53,25 @@ def test_world_one_sharded_step_equals_the_single_step(pool):
     eng2.close()
 
 
-def test_two_replicas_on_one_gpu_match_the_sharded_oracle():
-    snaps = [snapshot_v1(30_000, seed=70 + g, pool="headroom") for g in range(2)]
-    gpos = interleaved_gpos([len(s.queue) for s in snaps])
+@pytest.mark.parametrize("kind,world", [("independent", 2), ("global", 2), ("global", 4)])
+def test_replicas_on_one_gpu_match_the_sharded_oracle(kind, world):
+    """Replica contexts on one GPU, the collectives done by hand.  "global":
+    config (3) -- ONE snapshot_v1 sharded rank mod G with box-global tool
+    counters, every admission entry at its global list position."""
+    if kind == "global":
+        glob = snapshot_v1(30_000 * world, seed=77, pool="headroom")
+        # a window that admits part of the union list: the residual's global
+        # order (packed order, dense positions) is exercised
+        glob.initial_window = 2000.0
+        glob.worker_slots = 4000
+        snaps = [snapshot_shard(glob, world, g, box_global=True) for g in range(world)]
+        gpos = [s.meta["gpos"] for s in snaps]
+    else:
+        snaps = [snapshot_v1(30_000, seed=70 + g, pool="headroom") for g in range(world)]
+        gpos = interleaved_gpos([len(s.queue) for s in snaps])
     want = run_multi_step([s.copy() for s in snaps], gpos)
     cap = 2 * max(len(s.queue) for s in snaps)
-    reps = [_replica(s, 2, g, gpos[g], cap) for g, s in enumerate(snaps)]
+    reps = [_replica(s, world, g, gpos[g], cap) for g, s in enumerate(snaps)]
     sis = [e.step_in(s.now, True, s.active_tools, 0, s.worker_slots) for (e, _), s in
            zip(reps, snaps)]
     for (e, sh), si in zip(reps, sis):
