@@ -184,7 +184,8 @@ struct Work {
 struct Bufs {
   // expired pins: row order (k_scan), rank order (k_exp_*)
   i32 *tile_cnt;             // per-k_scan-CTA expired counts
-  u32 *row_dig;              // k_scan digit record when it exceeds shared memory
+  u32 *row_dig;              // k_scan: per CTA, the compacted rows' digit records
+  u32 *cand_row;             // k_scan: per CTA, the compacted rows (row order)
   u32 *exp_row; i32 *exp_blk; u32 *exp_rank;
   u32 *exp_row_sorted; i32 *exp_blk_sorted;
   // window candidates

@@ -270,7 +270,6 @@ __device__ void refresh_pressure(const Cfg& c, mars_scalars* sc, int worker_slot
 #define DIG_BND 0x4000u
 #define DIG_EXP 0x4000u
 #define DIG_ABOVE 0x7fffu  // victim digit above every threshold (not computed)
-#define DIG_SMEM_MAX (64 * 1024)  // record kept in shared memory up to this size
 
 // For two HIST_BINS shared histograms at once: the smallest bin d with
 // cumsum(h[0..d]) >= k (HIST_BINS-1 if the total is below k), and
@@ -638,6 +637,7 @@ __device__ void grid_rank_victims(Work* w, Bufs& b, bool ref_v, int cap, u64* sk
 
 // k_scan staging: one round = SCAN_TPB consecutive rows (one per thread),
 // every column k_scan reads arrives by TMA into one of SCAN_NBUF ring buffers.
+// (the queued rows' req_blocks come from the admission list itself)
 #define SCAN_R SCAN_TPB
 #define SCAN_NBUF 3
 #define SB_RS 0                       // f64 ready_since (or arrival when coordinator off)
@@ -645,14 +645,13 @@ __device__ void grid_rank_victims(Work* w, Bufs& b, bool ref_v, int cap, u64* sk
 #define SB_DL (SB_WS + 8 * SCAN_R)    // f64 pin deadline
 #define SB_KV (SB_DL + 8 * SCAN_R)    // i32 kv tokens
 #define SB_PB (SB_KV + 4 * SCAN_R)    // i32 pinned blocks
-#define SB_REQ (SB_PB + 4 * SCAN_R)   // i32 queued req blocks
-#define SB_FL (SB_REQ + 4 * SCAN_R)   // u8 flags
+#define SB_FL (SB_PB + 4 * SCAN_R)    // u8 flags
 #define SB_PH (SB_FL + SCAN_R)        // u8 phase
 #define SB_LV (SB_PH + SCAN_R)        // u8 level
 #define SB_PR (SB_LV + SCAN_R)        // u8 promotions
 #define SB_PL (SB_PR + SCAN_R)        // u8 pinned level
-#define SB_BYTES (SB_PL + SCAN_R)     // 41 bytes per row
-#define SCAN_ROW_BYTES 41
+#define SB_BYTES (SB_PL + SCAN_R)     // 37 bytes per row
+#define SCAN_ROW_BYTES 37
 
 static size_t scan_stage_bytes() { return (size_t)SCAN_NBUF * SB_BYTES; }
 
@@ -673,11 +672,13 @@ static size_t scan_stage_bytes() { return (size_t)SCAN_NBUF * SB_BYTES; }
 //           probe / refresh scalars.
 __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Bufs b,
                                                       mars_scalars* sc, i64 n_rows, i64* xc,
-                                                      i64 chunk, int dig_in_smem) {
+                                                      i64 chunk, Queue Q, const i32* qsel_p,
+                                                      int no_stage) {
   extern __shared__ __align__(128) unsigned char sdyn[];
   __shared__ u32 hw[HIST_BINS];
   __shared__ u32 hv[HIST_BINS];
   __shared__ u32 wsum[64];
+  __shared__ u32 s_wc[32];  // per-warp kept-row counts of the current round
   __shared__ u32 s_bw, s_bv;  // running histogram bounds (digits above are not counted)
   __shared__ __align__(8) u64 bars[SCAN_NBUF];
   cg::grid_group grid = cg::this_grid();
@@ -703,7 +704,6 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
     bulk_g2s(B + SB_DL, t.dl + rb, n16 * 8, bar);
     bulk_g2s(B + SB_KV, t.kv + rb, n16 * 4, bar);
     bulk_g2s(B + SB_PB, t.pb + rb, n16 * 4, bar);
-    bulk_g2s(B + SB_REQ, t.req + rb, n16 * 4, bar);
     bulk_g2s(B + SB_FL, t.flags + rb, n16, bar);
     bulk_g2s(B + SB_PH, t.phase + rb, n16, bar);
     bulk_g2s(B + SB_LV, t.level + rb, n16, bar);
@@ -728,7 +728,13 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
   // program_priority never pin (retention_decision None, baselines.py:82-86)
   const bool ret_on = c.policy != POL_FCFS && c.policy != POL_PP;
   const double scale = (now > 0.0 && now < 1e300) ? 1024.0 / now : 0.0;
-  u32* dig = dig_in_smem ? (u32*)(sdyn + (size_t)SCAN_NBUF * SB_BYTES) : b.row_dig + cs;
+  // Phase 1 compacts, in row order, every row phase 2 may emit (a digit at
+  // or below the CTA's running bound -- the final thresholds are never above
+  // it --, a boundary row, an expired pin) with its digit record into the
+  // CTA's segment of cand_row / row_dig; phase 2 reads only that list.
+  u32* lrow_g = b.cand_row + cs;
+  u32* ldig = b.row_dig + cs;
+  u32 lbase = 0;  // the list's length (uniform)
   // pre-step scalars: CTA 0 rewrites *sc after the grid barrier
   const i64 sc_total = sc->total_blocks, sc_free = sc->free_blocks;
   const double sc_usage = sc->kv_usage_ratio;
@@ -746,6 +752,19 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
   int n_exp = 0, n_qkv = 0;
   int max_req = 0, min_req = 0x7fffffff;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  // pack_queue's key range (control.py:109-122) over the admission list
+  // itself: CTA g reduces its slice (coalesced; the loads overlap the first
+  // TMA round trip)
+  {
+    const i64 qn = sc->queue_len;
+    const i32* qreq = PICK2(Q.req, *qsel_p);
+    const i64 q0 = qn * me / gridDim.x, q1 = qn * (me + 1) / gridDim.x;
+    for (i64 i = q0 + threadIdx.x; i < q1; i += SCAN_TPB) {
+      const i32 q = __ldcg(qreq + i);
+      max_req = q > max_req ? q : max_req;
+      min_req = q < min_req ? q : min_req;
+    }
+  }
   __syncthreads();
 
   // ---- phase 1 ---------------------------------------------------------------
@@ -755,8 +774,7 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
   // stay above every threshold (DIG_ABOVE, or the level's largest digit).
   int buf = 0;
   u32 par = 0;
-  u32* dig_rd = dig;
-  for (int rd = 0; rd < nrounds; ++rd, dig_rd += SCAN_R) {
+  for (int rd = 0; rd < nrounds; ++rd) {
     const unsigned char* B = sdyn + (size_t)buf * SB_BYTES;
     mbar_wait(&bars[buf], par);
     const int lr = threadIdx.x;
@@ -764,6 +782,7 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
     const bool valid = lr < (int)(ce - (cs + (i64)rd * SCAN_R));
     const u32 bw = s_bw, bv = s_bv;
     u32 rw = DIG_NONE, rv = DIG_NONE;
+    bool keep = false;
     if (valid) {
       const u8 f = B[SB_FL + lr];
       const u8 ph = B[SB_PH + lr];
@@ -772,9 +791,6 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
         n_queued++;
         if (f & MARS_F_LONG) n_long++;
         if (((const i32*)(B + SB_KV))[lr] > 0) n_qkv++;
-        const i32 q = ((const i32*)(B + SB_REQ))[lr];
-        max_req = q > max_req ? q : max_req;
-        min_req = q < min_req ? q : min_req;
       }
       if (f & MARS_F_PINNED) {
         const double d = ((const double*)(B + SB_DL))[lr];
@@ -837,14 +853,27 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
         n_bnd++;
         rw |= DIG_BND;
       }
-      dig_rd[lr] = rw | (rv << 16);
+      keep = ((rw & ~DIG_BND) <= bw) || rv <= bv || (rw & DIG_BND) || rv == DIG_EXP;
     }
+    const u32 kbal = __ballot_sync(FULL, keep);
+    if (lane == 0) s_wc[wid] = __popc(kbal);
     if (++buf == SCAN_NBUF) {
       buf = 0;
       par ^= 1u;
     }
     // every thread is done with this round's buffer: refill it
     __syncthreads();
+    {  // append the kept rows at their row-order positions
+      const u32 cw = s_wc[lane];
+      const u32 before = __reduce_add_sync(FULL, lane < wid ? cw : 0u);
+      const u32 tot = __reduce_add_sync(FULL, cw);
+      if (keep) {
+        const u32 k = lbase + before + __popc(kbal & ((1u << lane) - 1u));
+        lrow_g[k] = (u32)r;
+        ldig[k] = rw | (rv << 16);
+      }
+      lbase += tot;
+    }
     if (threadIdx.x == 0 && rd + SCAN_NBUF < nrounds) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue(rd + SCAN_NBUF);
@@ -1003,31 +1032,27 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
     __shared__ unsigned long long s_scan[32];
     __shared__ u32 s_escan[32];
     __shared__ int s_base[3], s_tot[4];
-    // Two layouts of the CTA's rows over its threads.  Digit record in
-    // shared memory: thread t owns a contiguous run (sequential, conflict-free
-    // reads).  Record in global memory (large tables): warp w owns the rows
-    // [w*S, (w+1)*S), read 32 consecutive rows at a time (coalesced).  Either
-    // way thread / warp order is row order.
-    const bool tr = dig_in_smem != 0;
-    const i64 len = ce - cs;
+    // The compacted list over the warps: warp w owns the entries
+    // [w*S, (w+1)*S), read 32 consecutive entries at a time (coalesced), so
+    // warp order is row order.
+    const i64 len = lbase;
     const i64 per = (len + SCAN_TPB - 1) / SCAN_TPB;
-    const i64 r0 = tr ? (i64)threadIdx.x * per : (i64)wid * per * 32 + lane;
-    const i64 rlim = tr ? r0 + per : (i64)(wid + 1) * per * 32;
+    const i64 r0 = (i64)wid * per * 32 + lane;
+    const i64 rlim = (i64)(wid + 1) * per * 32;
     const i64 r1 = rlim < len ? rlim : len;
-    const i64 step = tr ? 1 : 32;
+    const i64 step = 32;
     constexpr int FB = 21;  // count field width (chunk < 2^21 rows)
     constexpr unsigned long long FM = (1ull << FB) - 1;
     unsigned long long cnt = 0;
     u32 ecnt = 0;
     for (i64 i = r0; i < r1; i += step) {
-      const u32 rc = dig[i];
+      const u32 rc = ldig[i];
       const u32 rw = rc & 0xffffu, rv = rc >> 16;
       cnt += ((rw & ~DIG_BND) <= (u32)gw ? 1ull : 0ull) + ((rv <= (u32)gv ? 1ull : 0ull) << FB) +
              ((rw & DIG_BND) ? (1ull << (2 * FB)) : 0ull);
       ecnt += rv == DIG_EXP ? 1u : 0u;
     }
-    // thread-level inclusive scan (fields never carry: each < 2^21); the
-    // warp layout needs only the warp totals (lane 31's inclusive value)
+    // warp totals (lane 31's inclusive value; fields never carry: each < 2^21)
     unsigned long long incl = cnt;
     u32 eincl = ecnt;
 #pragma unroll
@@ -1070,12 +1095,15 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
     const int ntot = nw + nv + nb + ne;
     const bool ro = (mode & MARS_MODE_RANK_ORDERED) != 0;
     u32* exp_rows = ro ? b.exp_row_sorted : b.exp_row;
-    // staging: CTA-local row lists (4 B) + one 48-byte record per entry
+    // staging: CTA-local row lists (4 B), their digit records (4 B) and one
+    // 48-byte record per entry
     constexpr int STAGE_REC = 48;
-    const bool staged = ((((size_t)ntot * 4 + 15) & ~(size_t)15) + (size_t)ntot * STAGE_REC) <=
-                        (size_t)SCAN_NBUF * SB_BYTES;
+    const size_t lrow_bytes = ((size_t)ntot * 8 + 15) & ~(size_t)15;
+    const bool staged =
+        !no_stage && lrow_bytes + (size_t)ntot * STAGE_REC <= (size_t)SCAN_NBUF * SB_BYTES;
     u32* lrow = (u32*)sdyn;                                       // [ntot]
-    unsigned char* rec = sdyn + (((size_t)ntot * 4 + 15) & ~(size_t)15);  // [ntot][32]
+    u32* lrec = lrow + ntot;                                      // [ntot]
+    unsigned char* rec = sdyn + lrow_bytes;                       // [ntot][48]
     // (A') global list reservations, issued now, consumed in (D)
     int gb0 = 0, gb1 = 0, gb2 = 0;
     if (threadIdx.x == 0) {
@@ -1093,11 +1121,11 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
     // (B) row ids: local lists (staged) or the global lists
     const unsigned long long wtot = __shfl_sync(FULL, incl, 31);
     const u32 wetot = __shfl_sync(FULL, eincl, 31);
-    if (tr ? (cnt | ecnt) != 0 : (wtot | wetot) != 0) {
-      const unsigned long long ex = (tr ? incl - cnt : 0ull) + (wid ? s_scan[wid - 1] : 0ull);
+    if ((wtot | wetot) != 0) {
+      const unsigned long long ex = wid ? s_scan[wid - 1] : 0ull;
       int pw = (int)(ex & FM), pv = nw + (int)((ex >> FB) & FM);
       int pr = nw + nv + (int)(ex >> (2 * FB));
-      int pe = nw + nv + nb + (int)((tr ? eincl - ecnt : 0u) + (wid ? s_escan[wid - 1] : 0u));
+      int pe = nw + nv + nb + (int)(wid ? s_escan[wid - 1] : 0u);
       u32* ow = lrow;
       u32* ov = lrow;
       u32* orr = lrow;
@@ -1112,29 +1140,25 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
         orr = b.ret_row;
         oe = exp_rows;
       }
-      if (tr) {
-        for (i64 i = r0; i < r1; ++i) {
-          const u32 rc = dig[i];
-          const u32 rw = rc & 0xffffu, rv = rc >> 16;
-          const u32 r = (u32)(cs + i);
-          if ((rw & ~DIG_BND) <= (u32)gw) ow[pw++] = r;
-          if (rv <= (u32)gv) ov[pv++] = r;
-          if (rw & DIG_BND) orr[pr++] = r;
-          if (rv == DIG_EXP) oe[pe++] = r;
-        }
-      } else {  // 32 consecutive rows per ballot, lane order = row order
+      {  // 32 consecutive entries per ballot, lane order = row order
         const u32 lt = (1u << lane) - 1u;
         for (i64 c0 = r0 - lane; c0 < r1; c0 += 32) {
           const i64 i = c0 + lane;
-          const u32 rc = i < r1 ? dig[i] : (DIG_NONE | (DIG_NONE << 16));
+          const u32 rc = i < r1 ? ldig[i] : (DIG_NONE | (DIG_NONE << 16));
           const u32 rw = rc & 0xffffu, rv = rc >> 16;
-          const u32 r = (u32)(cs + i);
+          const u32 r = i < r1 ? lrow_g[i] : 0u;
           const bool qw = (rw & ~DIG_BND) <= (u32)gw, qv = rv <= (u32)gv;
           const bool qb = (rw & DIG_BND) != 0, qe = rv == DIG_EXP;
           const u32 mw = __ballot_sync(FULL, qw), mv = __ballot_sync(FULL, qv);
           const u32 mb = __ballot_sync(FULL, qb), me_ = __ballot_sync(FULL, qe);
-          if (qw) ow[pw + __popc(mw & lt)] = r;
-          if (qv) ov[pv + __popc(mv & lt)] = r;
+          if (qw) {
+            ow[pw + __popc(mw & lt)] = r;
+            if (staged) lrec[pw + __popc(mw & lt)] = rc;
+          }
+          if (qv) {
+            ov[pv + __popc(mv & lt)] = r;
+            if (staged) lrec[pv + __popc(mv & lt)] = rc;
+          }
           if (qb) orr[pr + __popc(mb & lt)] = r;
           if (qe) oe[pe + __popc(me_ & lt)] = r;
           pw += __popc(mw);
@@ -1163,7 +1187,14 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
       unsigned char* R = rec + (size_t)k * STAGE_REC;
       if (k < nw + nv) {
         const bool is_w = k < nw;
-        const bool ready = (dig[(i64)r - cs] & DIG_NONE) == 0;
+        // a ready row (window digit computed) or, for a victim, a pin
+        bool ready;
+        if (staged) {
+          ready = (lrec[k] & DIG_NONE) == 0;
+        } else {
+          const u8 fl = t.flags[r], ph = t.phase[r];
+          ready = (fl & MARS_F_ACTIVE) && (ph == MARS_PREFILL || ph == MARS_DECODE);
+        }
         const u32 rk = t.rank[r];
         u64 whi = 0, wlo = 0;
         u32 lv = 0;
@@ -3927,9 +3958,9 @@ static void lchk(const char* name) {
   if (e != cudaSuccess) fprintf(stderr, "mars: launch of %s failed: %s\n", name, cudaGetErrorString(e));
 }
 
-static int g_dig_global = 0;  // MARS_DIG_GLOBAL=1: digit record in global memory (tests)
+static int g_no_stage = 0;  // MARS_SCAN_NO_STAGE=1: k_scan emits without staging (tests)
 
-static void scan_geometry(i64 n, int nsm, int* grid, i64* chunk, int* in_smem) {
+static void scan_geometry(i64 n, int nsm, int* grid, i64* chunk) {
   i64 g = (n + SCAN_TILE - 1) / SCAN_TILE;
   if (g > nsm) g = nsm;
   if (g > SCAN_TPB) g = SCAN_TPB;
@@ -3937,13 +3968,12 @@ static void scan_geometry(i64 n, int nsm, int* grid, i64* chunk, int* in_smem) {
   i64 units = (n + 15) / 16;  // TMA rounds start 16-row (16-byte) aligned
   *grid = (int)g;
   *chunk = ((units + g - 1) / g) * 16;
-  *in_smem = (*chunk * 4 <= DIG_SMEM_MAX && !g_dig_global) ? 1 : 0;
 }
 
 static void launch_scan(const LaunchArgs* a, int nsm, cudaStream_t s) {
-  int grid, in_smem;
+  int grid;
   i64 chunk;
-  scan_geometry(a->n_rows, nsm, &grid, &chunk, &in_smem);
+  scan_geometry(a->n_rows, nsm, &grid, &chunk);
   Tab t = a->tab;
   Cfg c = a->cfg;
   Work* w = a->work;
@@ -3951,21 +3981,24 @@ static void launch_scan(const LaunchArgs* a, int nsm, cudaStream_t s) {
   mars_scalars* sc = a->sc;
   i64 n = a->n_rows;
   i64* xc = a->x.xc;
-  void* args[] = {&t, &c, &w, &b, &sc, &n, &xc, &chunk, &in_smem};
+  Queue Q = a->queue;
+  const i32* qsel = a->qsel;
+  int no_stage = g_no_stage;
+  void* args[] = {&t, &c, &w, &b, &sc, &n, &xc, &chunk, &Q, &qsel, &no_stage};
   cudaLaunchCooperativeKernel((const void*)k_scan, dim3(grid), dim3(SCAN_TPB), args,
-                              scan_stage_bytes() + (in_smem ? (size_t)chunk * 4 : 0), s);
+                              scan_stage_bytes(), s);
 }
 
 int mars_kernels_init() {
   {
-    const char* v = getenv("MARS_DIG_GLOBAL");
-    g_dig_global = (v && v[0] == '1') ? 1 : 0;
+    const char* v = getenv("MARS_SCAN_NO_STAGE");
+    g_no_stage = (v && v[0] == '1') ? 1 : 0;
     const char* d = getenv("MARS_DEBUG_LAUNCH");
     g_debug_launch = (d && d[0] == '1') ? 1 : 0;
   }
   cudaError_t e;
   e = cudaFuncSetAttribute(k_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)(scan_stage_bytes() + DIG_SMEM_MAX));
+                           (int)scan_stage_bytes());
   if (e != cudaSuccess) return (int)e;
   e = cudaFuncSetAttribute(k_walk, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)walk_smem_bytes());

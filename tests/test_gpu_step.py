@@ -150,11 +150,11 @@ def test_comparison_policy_step_matches_oracle(policy, pool, n, seed):
         assert want["evictions"], "the pressure case must exercise the reclaimer"
 
 
-def test_digit_record_in_global_memory_matches_oracle(monkeypatch):
-    """Tables whose per-CTA digit record exceeds shared memory (> 2.4M rows)
-    keep it in HBM and emit with the coalesced warp layout; forced here on a
-    smaller table."""
-    monkeypatch.setenv("MARS_DIG_GLOBAL", "1")
+def test_unstaged_emission_matches_oracle(monkeypatch):
+    """A CTA whose emitted entries exceed k_scan's staging area writes its
+    row lists straight to the global lists and gathers from there (forced
+    here with MARS_SCAN_NO_STAGE=1; read at context creation)."""
+    monkeypatch.setenv("MARS_SCAN_NO_STAGE", "1")
     for kind, n, seed in (("headroom", 200_000, 61), ("expired_big", 150_000, 62)):
         snap = variant(n, seed, kind)
         assert_same(device_step(snap.copy()), run_step(snap.copy()))
