@@ -333,6 +333,7 @@ int mars_create(const mars_config* hcfg, int device, int64_t max_rows, int64_t m
   Bufs& b = ctx->bufs;
   memset(&b, 0, sizeof b);
   ALLOC(b.tile_cnt, (R / 4096 + 2) * 4);
+  ALLOC(b.tile_kv, (R / 4096 + 2) * 3 * 8);
   ALLOC(b.row_dig, R * 4);
   ALLOC(b.cand_row, R * 4);
   ALLOC(b.exp_row, R * 4);
@@ -467,7 +468,7 @@ int mars_destroy(mars_ctx* ctx) {
   cudaFree(ctx->sc);
   cudaFree(ctx->qsel);
   Bufs& b = ctx->bufs;
-  void* bs[] = {b.tile_cnt, b.row_dig, b.cand_row, b.exp_row, b.exp_blk, b.exp_rank, b.exp_row_sorted, b.exp_blk_sorted, b.wc_hi,
+  void* bs[] = {b.tile_cnt, b.tile_kv, b.row_dig, b.cand_row, b.exp_row, b.exp_blk, b.exp_rank, b.exp_row_sorted, b.exp_blk_sorted, b.wc_hi,
                 b.wc_lo, b.wc_row, b.vc_key, b.vc_whi, b.vc_wlo, b.vc_row, b.vc_blk, b.ret_row,
                 b.ret_pin, b.ret_b, b.ret_c, b.ret_d, b.admitted, b.win_rows, b.dec_rows,
                 b.pre_rows, b.pre_grant, b.ev_row, b.ev_kind, b.ev_blk, b.j_op, b.j_row, b.j_n,

@@ -184,6 +184,7 @@ struct Work {
 struct Bufs {
   // expired pins: row order (k_scan), rank order (k_exp_*)
   i32 *tile_cnt;             // per-k_scan-CTA expired counts
+  i64 *tile_kv;              // per-k_scan-CTA S5 sums of the expired tables: segments, loose IDs, tail chunks
   u32 *row_dig;              // k_scan: per CTA, the compacted rows' digit records
   u32 *cand_row;             // k_scan: per CTA, the compacted rows (row order)
   u32 *exp_row; i32 *exp_blk; u32 *exp_rank;

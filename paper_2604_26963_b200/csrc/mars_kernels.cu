@@ -26,6 +26,7 @@
 
 #include <cooperative_groups.h>
 #include <stdlib.h>
+#include <string.h>
 #include <cuda_runtime.h>
 #include <stdio.h>
 
@@ -86,6 +87,34 @@ __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
   return v;
+}
+
+// block-wide exclusive scan of one i64 per thread (blockDim.x == 1024, every
+// thread calls it); *total = the block's sum
+__device__ __forceinline__ long long block_excl_scan_i64(long long v, long long* total) {
+  __shared__ long long s_ws[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  long long incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long x = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += x;
+  }
+  __syncthreads();
+  if (lane == 31) s_ws[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    long long t = s_ws[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long x = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += x;
+    }
+    s_ws[lane] = t;
+  }
+  __syncthreads();
+  *total = s_ws[31];
+  return (wid ? s_ws[wid - 1] : 0ll) + incl - v;
 }
 
 template <typename T>
@@ -673,18 +702,24 @@ static size_t scan_stage_bytes() { return (size_t)SCAN_NBUF * SB_BYTES; }
 __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Bufs b,
                                                       mars_scalars* sc, i64 n_rows, i64* xc,
                                                       i64 chunk, Queue Q, const i32* qsel_p,
-                                                      int no_stage) {
+                                                      int no_stage, Kv kv, int kv_fused) {
   extern __shared__ __align__(128) unsigned char sdyn[];
   __shared__ u32 hw[HIST_BINS];
   __shared__ u32 hv[HIST_BINS];
   __shared__ u32 wsum[64];
   __shared__ u32 s_wc[32];  // per-warp kept-row counts of the current round
+  // S5 with a rank-ordered table (kv_fused): the expired pins' tables go back
+  // to the free stack in row order, so this scan also lays out their frees
+  // (segment / loose-ID / tail-chunk offsets, as k_kv_exp_scan would) and
+  // k_kv_exp_push runs right after it
+  __shared__ unsigned long long s_kv[3];
   __shared__ u32 s_bw, s_bv;  // running histogram bounds (digits above are not counted)
   __shared__ __align__(8) u64 bars[SCAN_NBUF];
   cg::grid_group grid = cg::this_grid();
 
   PTIME(0);
   for (int i = threadIdx.x; i < HIST_BINS; i += blockDim.x) hw[i] = hv[i] = 0;
+  if (threadIdx.x < 3) s_kv[threadIdx.x] = 0;
   const int me = blockIdx.x;
   const i64 cs = (i64)me * chunk;
   const i64 ce = (cs + chunk < n_rows) ? cs + chunk : n_rows;
@@ -799,6 +834,13 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
         if (do_exp && exp_) {
           t.flags[r] = f & ~MARS_F_PINNED;
           t.kv[r] = 0;
+          if (kv_fused) {  // (rare rows: shared atomics cost nothing here)
+            atomicAdd(&s_kv[0], (unsigned long long)(pbk / KV_CH + (pbk % KV_CH ? 1 : 0)));
+            if (pbk % KV_CH) {
+              atomicAdd(&s_kv[1], (unsigned long long)(pbk % KV_CH));
+              atomicAdd(&s_kv[2], 1ull);
+            }
+          }
           exp_blocks += pbk;
           n_exp++;
           rv = DIG_EXP;
@@ -932,6 +974,7 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
       atomicMin(&s_cnt[8], mn);
     }
     __syncthreads();
+    if (threadIdx.x < 3 && kv_fused) b.tile_kv[3 * me + threadIdx.x] = (i64)s_kv[threadIdx.x];
     if (threadIdx.x == 0) {
       b.tile_cnt[me] = s_cnt[9];
       atomicAdd(&w->exp_blocks, s_eb);
@@ -959,6 +1002,10 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
   // window top-k sits at level 0, the victim top-k among the pinned rows).
   const u32 tmw = __ldcg(&w->tmin_win), tmv = __ldcg(&w->tmin_vic);
   const int tile_cnt_g = (int)threadIdx.x < (int)gridDim.x ? __ldcg(&b.tile_cnt[threadIdx.x]) : 0;
+  long long tkv[3] = {0, 0, 0};  // S5 (kv_fused): CTA t's sums, in flight with the rest
+  if (kv_fused && (int)threadIdx.x < (int)gridDim.x)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) tkv[q] = __ldcg(&b.tile_kv[3 * threadIdx.x + q]);
   const unsigned long long exp_total = __ldcg(&w->exp_blocks);
   {
     constexpr int HALF = HIST_BINS / 2 / SCAN_TPB;
@@ -1307,6 +1354,77 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
           b.ret_d[slot] = ((const double*)R)[2];
           b.ret_pin[slot] = R[24];
         }
+      }
+    }
+  }
+
+  // S5 (kv_fused): per expired table, in row order, its segment / loose-ID /
+  // tail-chunk offsets on the free stack (k_kv_exp_push's inputs); CTA 0
+  // moves the stack scalars.  The lengths are the pinned blocks (a pin moves
+  // the whole table) gathered above into exp_blk_sorted.
+  if (kv_fused) {
+    // this CTA's bases (sums over the CTAs before it) and the totals
+    __shared__ long long s_kr[6][32];
+    __shared__ i64 s_kb[3], s_kt[3];
+    {
+      long long v[6];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        v[q] = warp_sum<long long>((int)threadIdx.x < me ? tkv[q] : 0ll);
+        v[3 + q] = warp_sum<long long>(tkv[q]);
+      }
+      if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < 6; ++q) s_kr[q][wid] = v[q];
+      __syncthreads();
+      if (wid == 0) {
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+          const long long x = warp_sum<long long>(s_kr[q][lane]);
+          if (lane == 0) {
+            if (q < 3) s_kb[q] = x; else s_kt[q - 3] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+    i64 so = s_kb[0], ao = s_kb[1], ro = s_kb[2];
+    const int ne_cta = __ldcg(&b.tile_cnt[me]);
+    for (int e0 = 0; e0 < ne_cta; e0 += SCAN_TPB) {
+      const int e = e0 + (int)threadIdx.x;
+      i64 L = 0;
+      if (e < ne_cta) L = __ldcg(&b.exp_blk_sorted[exp_off + e]);
+      // one scan of the three fields packed 21 bits apart (a 1024-table chunk
+      // sums to < 2^21 in each: <= 8K blocks per table)
+      constexpr int KB = 21;
+      constexpr long long KM = (1ll << KB) - 1;
+      const long long pk = (L / KV_CH + (L % KV_CH ? 1 : 0)) | ((L % KV_CH) << KB) |
+                           ((long long)(L % KV_CH ? 1 : 0) << (2 * KB));
+      long long tot;
+      const long long x = block_excl_scan_i64(pk, &tot);
+      if (e < ne_cta) {
+        kv.xoff[exp_off + e] = so + (x & KM);
+        kv.xaoff[exp_off + e] = ao + ((x >> KB) & KM);
+        kv.xroff[exp_off + e] = ro + (x >> (2 * KB));
+      }
+      so += tot & KM;
+      ao += (tot >> KB) & KM;
+      ro += tot >> (2 * KB);
+    }
+    if (me == 0 && threadIdx.x == 0) {
+      const i64 s0 = kv.s->seg_top;
+      if (s0 + s_kt[0] > kv.seg_cap) {
+        kv.s->status |= 32;
+        kv.xbase[1] = -1;
+      } else {
+        kv.xbase[0] = s0;
+        kv.xbase[1] = s_kt[0];
+        kv.xbase[2] = kv.s->arena_top;
+        kv.xbase[3] = kv.s->cfs_top;
+        kv.s->seg_top = s0 + s_kt[0];
+        kv.s->arena_top += s_kt[1];
+        kv.s->cfs_top += s_kt[2];
+        kv.s->fs_ids += (i64)exp_total;
       }
     }
   }
@@ -3984,7 +4102,12 @@ static void launch_scan(const LaunchArgs* a, int nsm, cudaStream_t s) {
   Queue Q = a->queue;
   const i32* qsel = a->qsel;
   int no_stage = g_no_stage;
-  void* args[] = {&t, &c, &w, &b, &sc, &n, &xc, &chunk, &Q, &qsel, &no_stage};
+  // S5 expiry offsets laid out by the scan itself when the expired list is
+  // already in rank order (no sort after the scan)
+  int kv_fused = (a->kv && !a->exp_sort && !a->exp_may_be_big) ? 1 : 0;
+  Kv kv;
+  if (a->kv) kv = *a->kv; else memset(&kv, 0, sizeof kv);
+  void* args[] = {&t, &c, &w, &b, &sc, &n, &xc, &chunk, &Q, &qsel, &no_stage, &kv, &kv_fused};
   cudaLaunchCooperativeKernel((const void*)k_scan, dim3(grid), dim3(SCAN_TPB), args,
                               scan_stage_bytes(), s);
 }
@@ -4140,9 +4263,10 @@ int mars_enqueue_step(const LaunchArgs* a) {
     // the early pack on the second side stream that arrangement was seen to
     // starve k_control, r2.)
     mark(5, 0, s);
-    mars_kv_enqueue_exp_free(*a->kv, s, a->work, a->bufs, nsm);
+    const bool fused = !a->exp_sort && !a->exp_may_be_big;
+    mars_kv_enqueue_exp_free(*a->kv, s, a->work, a->bufs, nsm, /*offsets_done=*/fused);
     mark(5, 1, s);
-    launches += 2;
+    launches += fused ? 1 : 2;
   }
   cudaStreamWaitEvent(s, a->ev_join, 0);
   if (a->advance) {

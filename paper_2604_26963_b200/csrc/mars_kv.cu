@@ -225,9 +225,12 @@ __device__ bool kv_free_run(Kv& k, int m, const u32* rows, const i32* ns) {
 // After a run popped F IDs from the touched top segments (top first, `cum`
 // their prefix counts): emptied chunks return to the pool, an emptied arena
 // segment lowers the arena top, and a partly popped chunk segment leaves its
-// rest in the arena (chunk segments stay whole).  Thread 0.
+// rest in the arena (chunk segments stay whole).  Thread 0; that rest's copy
+// (< 64 IDs from chunk position cp[0] to arena position cp[1], cp[2] of them,
+// in reverse) is left to the caller's threads.
 __device__ void kv_settle(Kv& k, const u64* segs, const i64* cum, int nseg, i64 F, i64 top,
-                          i64 ctop) {
+                          i64 ctop, i64* cp) {
+  cp[2] = 0;
   i64 a = k.s->arena_top, cf = ctop;
   int full = 0;
   u64 last = 0;
@@ -245,8 +248,9 @@ __device__ void kv_settle(Kv& k, const u64* segs, const i64* cum, int nseg, i64 
       keep_last = true;
     } else {  // partly popped chunk: its rest to the arena, the chunk back
       const i64 r = c - used;
-      for (i64 q = 0; q < r; ++q)
-        k.arena[a + r - 1 - q] = k.chunks[(i64)seg_index(sg) * KV_CH + seg_start(sg) + used + q];
+      cp[0] = (i64)seg_index(sg) * KV_CH + seg_start(sg) + used;
+      cp[1] = a;
+      cp[2] = r;
       last = seg_arena_make(a, (u32)r);
       a += r;
       k.cfs[cf++] = (u32)seg_index(sg);
@@ -338,11 +342,15 @@ __device__ bool kv_alloc_run(Kv& k, int m, const u32* rows, const i32* ns) {
     }
     if (n > 0) k.len[row] = (i32)(L + n);
     __syncthreads();
+    __shared__ i64 s_cp[3];
     if (threadIdx.x == 0) {
-      kv_settle(k, s_seg, s_cum, nseg, F, top, ctop - Cn);
+      kv_settle(k, s_seg, s_cum, nseg, F, top, ctop - Cn, s_cp);
       k.s->fs_ids = ids - F;
       k.s->fresh = fresh + (N - F);
     }
+    __syncthreads();
+    for (i64 q = threadIdx.x; q < s_cp[2]; q += KV_TPB)
+      k.arena[s_cp[1] + s_cp[2] - 1 - q] = k.chunks[s_cp[0] + q];
   } else {
     // deep run: sequential pops (thread 0), in the run's order
     __syncthreads();
@@ -463,31 +471,39 @@ __global__ void __launch_bounds__(KV_TPB) k_kv_exp_scan(Kv k, const Work* w, Buf
   const int per = (ne + KV_TPB - 1) / KV_TPB;
   const int i0 = threadIdx.x * per, i1 = min(ne, i0 + per);
   // a pinned session's table is exactly its pinned blocks (a pin moves the
-  // whole table, engine.py:190-200): the lengths come with the expired list
-  // (coalesced), k_kv_exp_push checks them against the tables
+  // whole table, engine.py:190-200): the lengths come with the expired list,
+  // all in flight at once (k_kv_exp_push checks them against the tables)
+  constexpr int PR = 8;  // entries per thread held in registers (ne <= 8K; then loads)
+  i32 Lr[PR];
+#pragma unroll
+  for (int q = 0; q < PR; ++q) Lr[q] = (i0 + q < i1) ? __ldcg(&b.exp_blk_sorted[i0 + q]) : 0;
   i64 segs = 0, ids = 0, ar = 0, rc = 0;
-  for (int i = i0; i < i1; ++i) {
-    const i64 L = __ldcg(&b.exp_blk_sorted[i]);
-    k.xlen[i] = (i32)L;
+  auto add = [&](i64 L) {
     segs += L / KV_CH + ((L % KV_CH) ? 1 : 0);
     ar += L % KV_CH;
     rc += (L % KV_CH) ? 1 : 0;
     ids += L;
-  }
+  };
+#pragma unroll
+  for (int q = 0; q < PR; ++q) add(Lr[q]);  // (0 past the run)
+  for (int i = i0 + PR; i < i1; ++i) add(__ldcg(&b.exp_blk_sorted[i]));
   i64 S, N, A, R;
   i64 so = kv_scan(segs, &S);
   i64 ao = kv_scan(ar, &A);
   i64 ro = kv_scan(rc, &R);
   kv_scan(ids, &N);
-  for (int i = i0; i < i1; ++i) {
-    const i64 L = k.xlen[i];
+  auto put = [&](int i, i64 L) {
     k.xoff[i] = so;
     k.xaoff[i] = ao;
     k.xroff[i] = ro;
     so += L / KV_CH + ((L % KV_CH) ? 1 : 0);
     ao += L % KV_CH;
     ro += (L % KV_CH) ? 1 : 0;
-  }
+  };
+#pragma unroll
+  for (int q = 0; q < PR; ++q)
+    if (i0 + q < i1) put(i0 + q, Lr[q]);
+  for (int i = i0 + PR; i < i1; ++i) put(i, __ldcg(&b.exp_blk_sorted[i]));
   __syncthreads();
   if (threadIdx.x == 0) {
     const i64 s0 = k.s->seg_top;
@@ -517,7 +533,7 @@ __global__ void k_kv_exp_push(Kv k, const Work* w, Bufs b) {
   for (int e = (int)(((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5); e < ne;
        e += (int)(((i64)gridDim.x * blockDim.x) >> 5)) {
     const u32 row = b.exp_row_sorted[e];
-    const i64 L = k.xlen[e];
+    const i64 L = b.exp_blk_sorted[e];
     if (lane == 0 && k.len[row] != L) k.s->status |= 64;  // table != pinned blocks
     const i64 tail = L % KV_CH, full = L / KV_CH;
     FreePlan f;
@@ -650,10 +666,11 @@ int mars_kv_enqueue_apply(const Kv& k, cudaStream_t s, i64 n_ops, const u8* op, 
   return (int)cudaGetLastError();
 }
 
-int mars_kv_enqueue_exp_free(const Kv& k, cudaStream_t s, Work* w, const Bufs& b, int grid) {
-  k_kv_exp_scan<<<1, KV_TPB, 0, s>>>(k, w, b);
+int mars_kv_enqueue_exp_free(const Kv& k, cudaStream_t s, Work* w, const Bufs& b, int grid,
+                             bool offsets_done) {
+  if (!offsets_done) k_kv_exp_scan<<<1, KV_TPB, 0, s>>>(k, w, b);
   // small CTAs: they also fit beside the walk's CTA, which may still run
-  k_kv_exp_push<<<4 * grid, 256, 0, s>>>(k, w, b);
+  k_kv_exp_push<<<8 * grid, 256, 0, s>>>(k, w, b);
   return (int)cudaGetLastError();
 }
 

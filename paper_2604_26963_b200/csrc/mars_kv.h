@@ -45,7 +45,9 @@ struct Kv {
 int mars_kv_enqueue_apply(const Kv& k, cudaStream_t s, i64 n_ops, const u8* op, const u32* row,
                           const i32* n);
 int mars_kv_enqueue_apply_step(const Kv& k, cudaStream_t s, Work* w, const Bufs& b);
-int mars_kv_enqueue_exp_free(const Kv& k, cudaStream_t s, Work* w, const Bufs& b, int grid);
+// the step's expired pins' frees; offsets_done: k_scan laid out the offsets
+int mars_kv_enqueue_exp_free(const Kv& k, cudaStream_t s, Work* w, const Bufs& b, int grid,
+                             bool offsets_done);
 int mars_kv_enqueue_bulk(const Kv& k, cudaStream_t s, i64 n, const u32* rows, const i32* cnt,
                          int grid);
 int mars_kv_enqueue_resume_free(const Kv& k, cudaStream_t s, i64 n, const i64* rows,

@@ -1,4 +1,4 @@
-"""One headroom step at N sessions (argv[1]) for an ncu capture of k_scan:
+"""One headroom step at N sessions (argv[1]; argv[2] == "s5": with S5) for ncu:
 launch 1 warms up, launch 2 is the one to capture (ncu -k regex:k_scan -s 1 -c 1)."""
 import os
 import sys
@@ -12,6 +12,11 @@ snap = snapshot_v1(n, seed=7, pool="headroom")
 eng = MarsEngine(max_rows=snap.n, max_queue=max(len(snap.queue), 1),
                  config=make_config(initial_window=snap.initial_window))
 eng.load_snapshot(snap)
+if len(sys.argv) > 2 and sys.argv[2] == "s5":  # the block-ID manager attached
+    from paper_2604_26963_b200.kvstore import KvBlockManager
+    kvm = KvBlockManager(eng, snap.total_blocks,
+                         max_blocks_per_row=int(-(-(int(snap.cols["context"].max()) + 4096) // 16)))
+    kvm.load_snapshot_tables(snap)
 si = eng.step_in(snap.now, True, snap.active_tools, snap.queued_tools, snap.worker_slots)
 eng.checkpoint()
 for _ in range(2):
