@@ -33,6 +33,7 @@ struct mars_ctx {
   i64 last_resume_n = 0;
   bool own_stream = true;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_head = nullptr, ev_pack = nullptr;
+  cudaEvent_t ev_kvx = nullptr;
   int pack_ctas = 20;
   mars_config hcfg;
   Cfg cfg;
@@ -271,6 +272,7 @@ int mars_create(const mars_config* hcfg, int device, int64_t max_rows, int64_t m
   CK(cudaStreamCreateWithFlags(&ctx->side2, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&ctx->ev_head, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&ctx->ev_pack, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ctx->ev_kvx, cudaEventDisableTiming));
   {
     const char* e = getenv("MARS_PACK_CTAS");  // tuning knob: 0 disables the early pack
     if (e) ctx->pack_ctas = atoi(e);
@@ -510,6 +512,7 @@ int mars_destroy(mars_ctx* ctx) {
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->ev_head) cudaEventDestroy(ctx->ev_head);
   if (ctx->ev_pack) cudaEventDestroy(ctx->ev_pack);
+  if (ctx->ev_kvx) cudaEventDestroy(ctx->ev_kvx);
   if (ctx->side2) cudaStreamDestroy(ctx->side2);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->side) cudaStreamDestroy(ctx->side);
@@ -663,6 +666,7 @@ static LaunchArgs launch_args(mars_ctx* ctx, const mars_step_in* in) {
   a.side2 = ctx->side2;
   a.ev_head = ctx->ev_head;
   a.ev_pack = ctx->ev_pack;
+  a.ev_kvx = ctx->ev_kvx;
   a.tab = ctx->tab;
   a.cfg = ctx->cfg;
   a.work = ctx->work;

@@ -713,6 +713,7 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
   // (segment / loose-ID / tail-chunk offsets, as k_kv_exp_scan would) and
   // k_kv_exp_push runs right after it
   __shared__ unsigned long long s_kv[3];
+  __shared__ i64 s_kvb[3];  // the free stack's pre-step tops (segments, arena, chunk pool)
   __shared__ u32 s_bw, s_bv;  // running histogram bounds (digits above are not counted)
   __shared__ __align__(8) u64 bars[SCAN_NBUF];
   cg::grid_group grid = cg::this_grid();
@@ -720,6 +721,11 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
   PTIME(0);
   for (int i = threadIdx.x; i < HIST_BINS; i += blockDim.x) hw[i] = hv[i] = 0;
   if (threadIdx.x < 3) s_kv[threadIdx.x] = 0;
+  if (kv_fused && threadIdx.x == 0) {  // read before the grid barrier (CTA 0 moves them after)
+    s_kvb[0] = kv.s->seg_top;
+    s_kvb[1] = kv.s->arena_top;
+    s_kvb[2] = kv.s->cfs_top;
+  }
   const int me = blockIdx.x;
   const i64 cs = (i64)me * chunk;
   const i64 ce = (cs + chunk < n_rows) ? cs + chunk : n_rows;
@@ -1358,10 +1364,12 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
     }
   }
 
-  // S5 (kv_fused): per expired table, in row order, its segment / loose-ID /
-  // tail-chunk offsets on the free stack (k_kv_exp_push's inputs); CTA 0
-  // moves the stack scalars.  The lengths are the pinned blocks (a pin moves
-  // the whole table) gathered above into exp_blk_sorted.
+  // S5 (kv_fused): per expired table, in row order (= rank order, the order
+  // expired_pins() evicts them, baselines.py:396-399), its segment / loose-ID
+  // / tail-chunk positions on the free stack (prefix over the CTAs before it
+  // and a block scan): k_kv_exp_push's inputs, no separate scan kernel.  CTA
+  // 0 moves the stack scalars.  The lengths are the pinned blocks (a pin
+  // moves the whole table) gathered above.
   if (kv_fused) {
     // this CTA's bases (sums over the CTAs before it) and the totals
     __shared__ long long s_kr[6][32];
@@ -1389,7 +1397,8 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
       __syncthreads();
     }
     i64 so = s_kb[0], ao = s_kb[1], ro = s_kb[2];
-    const int ne_cta = __ldcg(&b.tile_cnt[me]);
+    const bool kv_room = s_kvb[0] + s_kt[0] <= kv.seg_cap;  // (else: status 32, no frees)
+    const int ne_cta = kv_room ? __ldcg(&b.tile_cnt[me]) : 0;
     for (int e0 = 0; e0 < ne_cta; e0 += SCAN_TPB) {
       const int e = e0 + (int)threadIdx.x;
       i64 L = 0;
@@ -1402,28 +1411,24 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
                            ((long long)(L % KV_CH ? 1 : 0) << (2 * KB));
       long long tot;
       const long long x = block_excl_scan_i64(pk, &tot);
-      if (e < ne_cta) {
-        kv.xoff[exp_off + e] = so + (x & KM);
-        kv.xaoff[exp_off + e] = ao + ((x >> KB) & KM);
-        kv.xroff[exp_off + e] = ro + (x >> (2 * KB));
+      if (e < ne_cta) {  // absolute positions on the stack / arena / chunk pool
+        kv.xoff[exp_off + e] = s_kvb[0] + so + (x & KM);
+        kv.xaoff[exp_off + e] = s_kvb[1] + ao + ((x >> KB) & KM);
+        kv.xroff[exp_off + e] = s_kvb[2] + ro + (x >> (2 * KB));
       }
       so += tot & KM;
       ao += (tot >> KB) & KM;
       ro += tot >> (2 * KB);
     }
     if (me == 0 && threadIdx.x == 0) {
-      const i64 s0 = kv.s->seg_top;
-      if (s0 + s_kt[0] > kv.seg_cap) {
-        kv.s->status |= 32;
-        kv.xbase[1] = -1;
+      kv.xbase[1] = kv_room ? 1 : -1;  // k_kv_exp_push: offsets absolute (or overflow)
+      kv.xbase[0] = kv.xbase[2] = kv.xbase[3] = 0;
+      if (!kv_room) {
+        atomicOr(&kv.s->status, 32);
       } else {
-        kv.xbase[0] = s0;
-        kv.xbase[1] = s_kt[0];
-        kv.xbase[2] = kv.s->arena_top;
-        kv.xbase[3] = kv.s->cfs_top;
-        kv.s->seg_top = s0 + s_kt[0];
-        kv.s->arena_top += s_kt[1];
-        kv.s->cfs_top += s_kt[2];
+        kv.s->seg_top = s_kvb[0] + s_kt[0];
+        kv.s->arena_top = s_kvb[1] + s_kt[1];
+        kv.s->cfs_top = s_kvb[2] + s_kt[2];
         kv.s->fs_ids += (i64)exp_total;
       }
     }
@@ -4206,6 +4211,7 @@ int mars_enqueue_step(const LaunchArgs* a) {
   // then waits for the admission's completion flag (k_walk, admit_async).
   // The KV journal apply needs the walk's journal and the rank-ordered
   // expired pins: after the join.
+  const bool kv_fused = a->kv && !a->exp_sort && !a->exp_may_be_big;
   cudaEventRecord(a->ev_fork, s);
   cudaStreamWaitEvent(s2, a->ev_fork, 0);
   mark(3, 0, s2);
@@ -4214,6 +4220,22 @@ int mars_enqueue_step(const LaunchArgs* a) {
   lchk("k_walk");
   launches++;
   mark(3, 1, s2);
+  if (kv_fused) {
+    // S5, expired list in rank order (k_scan laid out the frees): the expired
+    // tables go back to the free stack on the main stream beside the walk
+    // (small CTAs: they never need the walk's SM), then the walk's journal
+    // applies on the walk's stream behind both, beside the control plane
+    mark(5, 0, s);
+    mars_kv_enqueue_exp_free(*a->kv, s, a->work, a->bufs, nsm, /*offsets_done=*/true);
+    mark(5, 1, s);
+    launches++;
+    cudaEventRecord(a->ev_kvx, s);
+    cudaStreamWaitEvent(s2, a->ev_kvx, 0);
+    mark(6, 0, s2);
+    mars_kv_enqueue_apply_step(*a->kv, s2, a->work, a->bufs, 1);
+    mark(6, 1, s2);
+    launches++;
+  }
   cudaEventRecord(a->ev_join, s2);
   // the early pack's SMs return before any other grid-wide kernel starts
   if (a->pack_early) cudaStreamWaitEvent(s, a->ev_pack, 0);
@@ -4255,28 +4277,26 @@ int mars_enqueue_step(const LaunchArgs* a) {
     mark(2, 1, s);
     launches++;
   }
-  if (a->kv) {
-    // S5, expired pins: their tables return to the free stack (segment pushes
-    // by the whole grid) after the control plane, while the walk -- the longer
-    // branch -- is still running.  (Not on a third stream beside the control
-    // plane: the walk may spin on the admission's completion flag, and with
-    // the early pack on the second side stream that arrangement was seen to
-    // starve k_control, r2.)
+  if (a->kv && !kv_fused) {
+    // S5, expired list sorted after the scan: the expired tables return to
+    // the free stack (segment pushes by the whole grid) after the control
+    // plane, while the walk is still running.  (Not on a third stream beside the control plane: the walk may
+    // spin on the admission's completion flag, and with the early pack on the
+    // second side stream that arrangement was seen to starve k_control, r2.)
     mark(5, 0, s);
-    const bool fused = !a->exp_sort && !a->exp_may_be_big;
-    mars_kv_enqueue_exp_free(*a->kv, s, a->work, a->bufs, nsm, /*offsets_done=*/fused);
+    mars_kv_enqueue_exp_free(*a->kv, s, a->work, a->bufs, nsm, /*offsets_done=*/false);
     mark(5, 1, s);
-    launches += fused ? 1 : 2;
+    launches += 2;
   }
   cudaStreamWaitEvent(s, a->ev_join, 0);
   if (a->advance) {
     k_advance<<<1, 1024, 0, s>>>(a->tab, a->cfg, a->work, a->bufs, a->sc);
     launches++;
   }
-  if (a->kv) {
-    mark(6, 0, s);
-    mars_kv_enqueue_apply_step(*a->kv, s, a->work, a->bufs);
-    mark(6, 1, s);
+  if (a->kv && (!kv_fused || a->advance)) {  // (fused: only the tick tail's frees are left)
+    if (!kv_fused) mark(6, 0, s);
+    mars_kv_enqueue_apply_step(*a->kv, s, a->work, a->bufs, kv_fused ? 2 : 3);
+    if (!kv_fused) mark(6, 1, s);
     launches++;
   }
 #ifdef MARS_PHASE_TIMING

@@ -27,18 +27,6 @@
 
 #define KV_TPB 1024
 #define FULL32 0xffffffffu
-#define SEG_ARENA (1ull << 63)
-
-__device__ __forceinline__ u64 seg_chunk_make(u32 ch, u32 start, u32 cnt) {
-  return ((u64)ch << 16) | ((u64)start << 8) | (u64)cnt;
-}
-__device__ __forceinline__ u64 seg_arena_make(i64 base, u32 cnt) {
-  return SEG_ARENA | ((u64)base << 16) | (u64)cnt;
-}
-__device__ __forceinline__ bool seg_is_arena(u64 s) { return (s & SEG_ARENA) != 0; }
-__device__ __forceinline__ u64 seg_index(u64 s) { return (s >> 16) & 0xffffffffffull; }
-__device__ __forceinline__ u32 seg_start(u64 s) { return (u32)(s >> 8) & 0xffu; }
-__device__ __forceinline__ u32 seg_count(u64 s) { return (u32)s & 0xffu; }
 
 // the q-th ID a segment pops
 __device__ __forceinline__ u32 seg_id(const Kv& k, u64 sg, i64 q) {
@@ -81,40 +69,6 @@ __device__ i64 kv_scan(i64 v, i64* total) {
   return before + incl - v;
 }
 
-// Pieces of freeing table positions [keep, L) (bottom -> top of the pushes):
-// the tail T = [tb, L) of a partial last chunk (to the arena, its chunk back
-// to the pool), the whole chunks between (chunk segments), the head
-// H = [keep, hb) of a kept boundary chunk (to the arena).
-struct FreePlan {
-  i64 keep, L, hb, tb, f0, f1;  // full chunks [f0, f1)
-  i64 nh, nt;                   // |H|, |T|
-  bool tail_chunk;              // T's chunk returns to the pool
-};
-
-__device__ __forceinline__ FreePlan free_plan(i64 L, i64 keep) {
-  FreePlan f;
-  f.keep = keep;
-  f.L = L;
-  const i64 up = (keep + KV_CH - 1) / KV_CH * KV_CH;  // keep rounded up
-  const i64 dn = L / KV_CH * KV_CH;                   // L rounded down
-  if (up >= L) {  // one chunk, or nothing: all of it to the arena
-    f.hb = L;
-    f.tb = L;
-    f.nh = L - keep;
-    f.nt = 0;
-    f.f0 = f.f1 = 0;
-    f.tail_chunk = (keep % KV_CH) == 0 && L > keep;  // the chunk leaves the row
-  } else {
-    f.hb = up;
-    f.nh = up - keep;
-    f.tb = dn > up ? dn : up;
-    f.nt = L - f.tb;
-    f.f0 = up / KV_CH;
-    f.f1 = f.tb / KV_CH;
-    f.tail_chunk = f.nt > 0;
-  }
-  return f;
-}
 
 // one per-block scratch area shared by the run kernels (a static __shared__
 // inside a device function is one allocation per CTA, whatever the call site)
@@ -124,38 +78,6 @@ __device__ __forceinline__ unsigned char* kv_scratch() {
   return buf;
 }
 
-// Freeing table positions [keep, L) of `row` (FreePlan f), on one warp: the
-// segments go to seg[sp..] bottom -> top (T's arena segment, the whole chunks
-// from the last one down, H's arena segment), the loose IDs of T and H to the
-// arena at ap.. (each segment pops from its end), T's chunk back to the pool
-// at cfs[cf] (cf < 0: none); the lanes copy IDs / write segments in parallel.
-__device__ __forceinline__ void kv_free_warp(const Kv& k, u32 row, const FreePlan& f, i64 sp,
-                                             i64 ap, i64 cf, int lane) {
-  const u32* dr = k.dir + (i64)row * k.D;
-  if (f.nt > 0) {
-    for (i64 j = lane; j < f.nt; j += 32) {
-      const i64 p = f.tb + j;
-      k.arena[ap + f.nt - 1 - j] = k.chunks[(i64)dr[p / KV_CH] * KV_CH + p % KV_CH];
-    }
-    if (lane == 0) k.seg[sp] = seg_arena_make(ap, (u32)f.nt);
-    ++sp;
-    ap += f.nt;
-  }
-  const i64 nf = f.f1 - f.f0;
-  for (i64 j = lane; j < nf; j += 32) k.seg[sp + j] = seg_chunk_make(dr[f.f1 - 1 - j], 0, KV_CH);
-  sp += nf;
-  if (f.nh > 0) {
-    for (i64 j = lane; j < f.nh; j += 32) {
-      const i64 p = f.keep + j;
-      k.arena[ap + f.nh - 1 - j] = k.chunks[(i64)dr[p / KV_CH] * KV_CH + p % KV_CH];
-    }
-    if (lane == 0) k.seg[sp] = seg_arena_make(ap, (u32)f.nh);
-  }
-  if (lane == 0) {
-    if (cf >= 0) k.cfs[cf] = dr[(f.L - 1) / KV_CH];
-    k.len[row] = (i32)f.keep;
-  }
-}
 
 // One run of frees (distinct rows; n < 0: the whole table), <= KV_TPB ops, on
 // the whole CTA.  Free i pushes its segments above those of frees 0..i-1; its
@@ -535,19 +457,7 @@ __global__ void k_kv_exp_push(Kv k, const Work* w, Bufs b) {
     const u32 row = b.exp_row_sorted[e];
     const i64 L = b.exp_blk_sorted[e];
     if (lane == 0 && k.len[row] != L) k.s->status |= 64;  // table != pinned blocks
-    const i64 tail = L % KV_CH, full = L / KV_CH;
-    FreePlan f;
-    f.keep = 0;
-    f.L = L;
-    f.nh = 0;
-    f.f0 = 0;
-    f.f1 = full;
-    f.tb = full * KV_CH;
-    f.nt = tail;
-    f.hb = 0;
-    f.tail_chunk = tail > 0;
-    kv_free_warp(k, row, f, base + k.xoff[e], a0 + k.xaoff[e],
-                 tail > 0 ? c0 + k.xroff[e] : -1, lane);
+    kv_free_table_warp(k, row, L, base + k.xoff[e], a0 + k.xaoff[e], c0 + k.xroff[e], lane);
   }
 }
 
@@ -555,10 +465,11 @@ __global__ void k_kv_exp_push(Kv k, const Work* w, Bufs b) {
 // plan order, then (MARS_MODE_ADVANCE) the tick tail's frees in decode order
 // -- a finished session's blocks (sim.py:243) and an unpinned boundary's
 // (sim.py:269); a pin keeps the table (ownership moves, the IDs stay)
-__global__ void __launch_bounds__(KV_TPB) k_kv_apply_step(Kv k, Work* w, Bufs b) {
+// parts: 1 the journal, 2 the tick tail's frees, 3 both
+__global__ void __launch_bounds__(KV_TPB) k_kv_apply_step(Kv k, Work* w, Bufs b, int parts) {
   if (k.s->status) return;
-  kv_apply_list(k, w->n_journal, b.j_op, b.j_row, b.j_n, true);
-  if ((w->in.mode & MARS_MODE_ADVANCE) && k.s->status == 0) {
+  if (parts & 1) kv_apply_list(k, w->n_journal, b.j_op, b.j_row, b.j_n, true);
+  if ((parts & 2) && (w->in.mode & MARS_MODE_ADVANCE) && k.s->status == 0) {
     __shared__ u32 s_r[KV_TPB];
     __shared__ int s_m;
     const int nr = w->n_round_end;
@@ -674,8 +585,8 @@ int mars_kv_enqueue_exp_free(const Kv& k, cudaStream_t s, Work* w, const Bufs& b
   return (int)cudaGetLastError();
 }
 
-int mars_kv_enqueue_apply_step(const Kv& k, cudaStream_t s, Work* w, const Bufs& b) {
-  k_kv_apply_step<<<1, KV_TPB, 0, s>>>(k, w, b);
+int mars_kv_enqueue_apply_step(const Kv& k, cudaStream_t s, Work* w, const Bufs& b, int parts) {
+  k_kv_apply_step<<<1, KV_TPB, 0, s>>>(k, w, b, parts);
   return (int)cudaGetLastError();
 }
 

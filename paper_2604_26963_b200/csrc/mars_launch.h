@@ -6,7 +6,7 @@
 
 struct LaunchArgs {
   cudaStream_t stream, side, side2;
-  cudaEvent_t ev_fork, ev_join, ev_head, ev_pack;
+  cudaEvent_t ev_fork, ev_join, ev_head, ev_pack, ev_kvx;
   Tab tab;
   Cfg cfg;
   Work* work;

@@ -1,5 +1,5 @@
 set -x
-timeout 1500 python -m pytest tests/test_gpu_kv.py tests/test_gpu_devsim.py -m gpu -q -p no:cacheprovider -x -k "block_ids or kv or fuzz or journal or deep or scale" 2>&1 | tail -4
+timeout 1500 python -m pytest tests/test_gpu_kv.py tests/test_gpu_devsim.py tests/test_gpu_ticks.py -m gpu -q -p no:cacheprovider -x -k "block_ids or kv or fuzz or journal or deep or scale or ticks" 2>&1 | tail -4
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/l_s5.csv python scripts/prof_scan.py 1000000 s5 > /dev/null 2>&1
 python - <<'PY'
 import csv
