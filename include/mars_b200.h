@@ -334,6 +334,25 @@ int mars_kv_evict(mars_ctx* ctx, int64_t n, const uint32_t* block_ids, int64_t s
 int mars_kv_restore(mars_ctx* ctx, int64_t n, const uint32_t* block_ids, int64_t slot0,
                     int method);
 int mars_kv_host_ptr(mars_ctx* ctx, void** host, void** device);
+
+/* The host tier driven by the step's decisions (no host tier in the
+ * reference; decision-neutral: the pool counts stay the
+ * reference's).  With capture on, every step records the IDs of the tables
+ * that a running session's eviction (scheduler.py:228-267 via sim.py:168-188)
+ * or an unpinned tool boundary (sim.py:266-272) frees; offload_captured copies
+ * those blocks to the next slots of the pinned host ring (returns the count,
+ * the first slot, and optionally the IDs in slot order).  offload_rows copies
+ * whole tables of rows (a pin at a tool boundary, sim.py:261-265) to the ring
+ * (row i at slot0 + counts[0..i)); restore_rows copies them back into the
+ * rows' current tables (a warm resume, sim.py:193-200).  counts[i] must be
+ * row i's table length. */
+int mars_kv_capture(mars_ctx* ctx, int on);
+int mars_kv_offload_captured(mars_ctx* ctx, int64_t* n_blocks, int64_t* slot0, uint32_t* ids,
+                             int64_t ids_cap);
+int mars_kv_offload_rows(mars_ctx* ctx, int64_t n, const int64_t* rows, const int32_t* counts,
+                         int64_t* slot0);
+int mars_kv_restore_rows(mars_ctx* ctx, int64_t n, const int64_t* rows, const int32_t* counts,
+                         const int64_t* slots);
 /* pinned cudaMemcpyAsync peak of the host link: best of `reps` per direction */
 int mars_host_link_peak(mars_ctx* ctx, int64_t bytes, int reps, double* d2h_gbs, double* h2d_gbs,
                         double* bidir_gbs);

@@ -154,6 +154,10 @@ _SIGS = {
     "mars_kv_evict": (i32, [C.c_void_p, i64, C.c_void_p, i64, C.c_int]),
     "mars_kv_restore": (i32, [C.c_void_p, i64, C.c_void_p, i64, C.c_int]),
     "mars_kv_host_ptr": (i32, [C.c_void_p, P(C.c_void_p), P(C.c_void_p)]),
+    "mars_kv_capture": (i32, [C.c_void_p, C.c_int]),
+    "mars_kv_offload_captured": (i32, [C.c_void_p, P(i64), P(i64), C.c_void_p, i64]),
+    "mars_kv_offload_rows": (i32, [C.c_void_p, i64, C.c_void_p, C.c_void_p, P(i64)]),
+    "mars_kv_restore_rows": (i32, [C.c_void_p, i64, C.c_void_p, C.c_void_p, C.c_void_p]),
     "mars_host_link_peak": (i32, [C.c_void_p, i64, C.c_int, P(f64), P(f64), P(f64)]),
     "mars_resume": (i32, [C.c_void_p, i64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                           C.c_void_p, f64, C.c_void_p]),

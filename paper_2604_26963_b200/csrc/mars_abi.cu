@@ -93,6 +93,10 @@ struct mars_ctx {
   unsigned char* kv_stage = nullptr; // device staging for op streams / ids
   i64 kv_stage_bytes = 0;
   u8* kv_dstage = nullptr;           // HBM staging for the staged host-tier path
+  i64 kv_dstage_blocks = 0;
+  i64 kv_ring = 0;                   // next host-tier slot (decision-driven tier, a ring)
+  u32* kv_ids = nullptr;             // device ID list of the row offload / restore
+  i64 kv_ids_cap = 0;
   // sharded replica (mars_shard_init)
   Xchg x = {};
 };
@@ -279,6 +283,8 @@ int mars_create(const mars_config* hcfg, int device, int64_t max_rows, int64_t m
   }
   {
     int rc = mars_kernels_init();
+    if (!rc) rc = mars_kernels_preload();
+    if (!rc) rc = mars_kv_preload();
     if (rc) return fail(ctx, MARS_ERR_CUDA, "kernel init: %s", cudaGetErrorString((cudaError_t)rc));
   }
   const i64 R = ctx->alloc_rows, Qc = ctx->max_queue;
@@ -495,7 +501,8 @@ int mars_destroy(mars_ctx* ctx) {
   {
     Kv& k = ctx->kv;
     void* kp[] = {k.seg, k.chunks, k.cfs, k.dir, k.len, k.s, k.data, ctx->kv_stage,
-                  ctx->kv_dstage, k.xoff, k.xlen, k.xbase, k.arena, k.xaoff, k.xroff};
+                  ctx->kv_dstage, k.xoff, k.xlen, k.xbase, k.arena, k.xaoff, k.xroff, k.cap,
+                  ctx->kv_ids};
     for (void* p : kp) cudaFree(p);
     if (ctx->kv_host) cudaFreeHost(ctx->kv_host);
   }
@@ -1449,7 +1456,10 @@ static int kv_move(mars_ctx* ctx, int64_t n, const uint32_t* ids, int64_t slot0,
     if (rc) return rc;
     CK(cudaMemcpyAsync(ctx->kv_stage, ids, n * 4, cudaMemcpyHostToDevice, ctx->stream));
     const i64 chunk = KV_STAGE_BLOCKS;
-    if (!ctx->kv_dstage) CK(cudaMalloc((void**)&ctx->kv_dstage, (size_t)chunk * k.block_bytes));
+    if (!ctx->kv_dstage) {
+      CK(cudaMalloc((void**)&ctx->kv_dstage, (size_t)chunk * k.block_bytes));
+      ctx->kv_dstage_blocks = chunk;
+    }
     u8* hbase = (u8*)ctx->kv_host;
     for (i64 c0 = 0; c0 < n; c0 += chunk) {
       const i64 m = (n - c0) < chunk ? (n - c0) : chunk;
@@ -1480,6 +1490,187 @@ static int kv_move(mars_ctx* ctx, int64_t n, const uint32_t* ids, int64_t slot0,
     }
   }
   CK(cudaStreamSynchronize(ctx->stream));
+  return MARS_OK;
+}
+
+// ---- host tier driven by the step's decisions ------
+// Staged copies between scattered pool blocks and consecutive host slots
+// [slot0, slot0 + n): gather / scatter kernels into an HBM staging area and
+// one copy-engine DMA per ~128 MiB.
+static int kv_stage_copy(mars_ctx* ctx, const u32* d_ids, i64 n, i64 slot0, int dir) {
+  Kv& k = ctx->kv;
+  const i64 chunk = std::max<i64>(KV_STAGE_BLOCKS, ((i64)128 << 20) / k.block_bytes);
+  if (ctx->kv_dstage_blocks < chunk) {
+    if (ctx->kv_dstage) cudaFree(ctx->kv_dstage);
+    ctx->kv_dstage = nullptr;
+    ctx->kv_dstage_blocks = 0;
+    CK(cudaMalloc((void**)&ctx->kv_dstage, (size_t)chunk * k.block_bytes));
+    ctx->kv_dstage_blocks = chunk;
+  }
+  u8* hbase = (u8*)ctx->kv_host;
+  for (i64 c0 = 0; c0 < n; c0 += chunk) {
+    const i64 m = (n - c0) < chunk ? (n - c0) : chunk;
+    const size_t bytes = (size_t)m * k.block_bytes;
+    u8* hp = hbase + (size_t)(slot0 + c0) * k.block_bytes;
+    int rc;
+    if (dir == 0) {
+      rc = mars_kv_enqueue_stage(k, ctx->stream, d_ids + c0, m, ctx->kv_dstage, 0, ctx->num_sms * 4);
+      if (rc) return fail(ctx, MARS_ERR_CUDA, "kv stage: %s", cudaGetErrorString((cudaError_t)rc));
+      CK(cudaMemcpyAsync(hp, ctx->kv_dstage, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    } else {
+      CK(cudaMemcpyAsync(ctx->kv_dstage, hp, bytes, cudaMemcpyHostToDevice, ctx->stream));
+      rc = mars_kv_enqueue_stage(k, ctx->stream, d_ids + c0, m, ctx->kv_dstage, 1, ctx->num_sms * 4);
+      if (rc) return fail(ctx, MARS_ERR_CUDA, "kv stage: %s", cudaGetErrorString((cudaError_t)rc));
+    }
+  }
+  return MARS_OK;
+}
+
+// n IDs to the ring (wrapping); returns the first slot
+static int kv_ring_put(mars_ctx* ctx, const u32* d_ids, i64 n, i64* slot0) {
+  Kv& k = ctx->kv;
+  if (n > k.host_blocks) return fail(ctx, MARS_ERR_CAPACITY, "host tier smaller than one offload");
+  if (ctx->kv_ring + n > k.host_blocks) ctx->kv_ring = 0;
+  *slot0 = ctx->kv_ring;
+  int rc = kv_stage_copy(ctx, d_ids, n, ctx->kv_ring, 0);
+  if (rc) return rc;
+  ctx->kv_ring += n;
+  return MARS_OK;
+}
+
+static int kv_tier_ready(mars_ctx* ctx) {
+  if (!ctx) return MARS_ERR_ARG;
+  if (!ctx->kv_on || !ctx->kv.data || !ctx->kv.host) return fail(ctx, MARS_ERR_ARG, "no kv data tier");
+  return MARS_OK;
+}
+
+int mars_kv_capture(mars_ctx* ctx, int on) {
+  int rc = kv_tier_ready(ctx);
+  if (rc) return rc;
+  Kv& k = ctx->kv;
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (on && !k.cap) CK(cudaMalloc((void**)&k.cap, (size_t)k.total * 4));
+  if (!on && k.cap) {
+    cudaFree(k.cap);
+    k.cap = nullptr;
+  }
+  // the step graphs carry the Kv struct as a kernel parameter
+  for (auto& g : ctx->graph_exec)
+    if (g) {
+      cudaGraphExecDestroy(g);
+      g = nullptr;
+    }
+  memset(ctx->graph_key, 0, sizeof ctx->graph_key);
+  return MARS_OK;
+}
+
+int mars_kv_offload_captured(mars_ctx* ctx, int64_t* n_blocks, int64_t* slot0, uint32_t* ids,
+                             int64_t ids_cap) {
+  int rc = kv_tier_ready(ctx);
+  if (rc) return rc;
+  Kv& k = ctx->kv;
+  if (!k.cap) return fail(ctx, MARS_ERR_ARG, "capture is off");
+  CK(cudaSetDevice(ctx->device));
+  KvScal s;
+  CK(cudaMemcpyAsync(&s, k.s, sizeof s, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (s.status & 128) return fail(ctx, MARS_ERR_CAPACITY, "capture list overflow");
+  i64 s0 = -1;
+  if (s.cap_n > 0) {
+    rc = kv_ring_put(ctx, k.cap, s.cap_n, &s0);
+    if (rc) return rc;
+    if (ids && ids_cap > 0)
+      CK(cudaMemcpyAsync(ids, k.cap, (size_t)std::min<i64>(ids_cap, s.cap_n) * 4,
+                         cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemsetAsync(&k.s->cap_n, 0, sizeof(i64), ctx->stream));
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (n_blocks) *n_blocks = s.cap_n;
+  if (slot0) *slot0 = s0;
+  return MARS_OK;
+}
+
+// the tables of n rows (row i holds counts[i] IDs) -> one device ID list
+static int kv_rows_ids(mars_ctx* ctx, int64_t n, const int64_t* rows, const int32_t* counts,
+                       i64* total) {
+  Kv& k = ctx->kv;
+  std::vector<i64> off((size_t)n + 1, 0);
+  for (int64_t i = 0; i < n; ++i) {
+    if (rows[i] < 0 || rows[i] >= k.rows || counts[i] < 0) return MARS_ERR_ARG;
+    off[i + 1] = off[i] + counts[i];
+  }
+  *total = off[n];
+  if (off[n] > ctx->kv_ids_cap) {
+    if (ctx->kv_ids) cudaFree(ctx->kv_ids);
+    ctx->kv_ids = nullptr;
+    ctx->kv_ids_cap = 0;
+    CK(cudaMalloc((void**)&ctx->kv_ids, (size_t)off[n] * 4 + 4));
+    ctx->kv_ids_cap = off[n];
+  }
+  // rows (u32) and offsets (i64) through the op staging buffer
+  int rc = kv_stage(ctx, n * 4 + (n + 1) * 8 + 16);
+  if (rc) return rc;
+  std::vector<u32> r32((size_t)n);
+  for (int64_t i = 0; i < n; ++i) r32[i] = (u32)rows[i];
+  i64* doff = (i64*)(ctx->kv_stage + (((size_t)n * 4 + 15) & ~(size_t)15));
+  CK(cudaMemcpyAsync(ctx->kv_stage, r32.data(), (size_t)n * 4, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(doff, off.data(), (size_t)(n + 1) * 8, cudaMemcpyHostToDevice, ctx->stream));
+  rc = mars_kv_enqueue_gather_ids(k, ctx->stream, n, (const u32*)ctx->kv_stage, doff, ctx->kv_ids,
+                                  ctx->num_sms * 4);
+  if (rc) return fail(ctx, MARS_ERR_CUDA, "kv gather ids: %s", cudaGetErrorString((cudaError_t)rc));
+  CK(cudaStreamSynchronize(ctx->stream));  // (the staging buffer is reused next)
+  return MARS_OK;
+}
+
+int mars_kv_offload_rows(mars_ctx* ctx, int64_t n, const int64_t* rows, const int32_t* counts,
+                         int64_t* slot0) {
+  int rc = kv_tier_ready(ctx);
+  if (rc) return rc;
+  if (n < 0 || (n > 0 && (!rows || !counts))) return MARS_ERR_ARG;
+  CK(cudaSetDevice(ctx->device));
+  i64 tot = 0, s0 = -1;
+  if (n > 0) {
+    rc = kv_rows_ids(ctx, n, rows, counts, &tot);
+    if (rc) return rc;
+    if (tot > 0) {
+      rc = kv_ring_put(ctx, ctx->kv_ids, tot, &s0);
+      if (rc) return rc;
+    }
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  KvScal s;
+  CK(cudaMemcpy(&s, ctx->kv.s, sizeof s, cudaMemcpyDeviceToHost));
+  if (s.status & 256) return fail(ctx, MARS_ERR_CONTRACT, "row table length != count");
+  if (slot0) *slot0 = s0;
+  return MARS_OK;
+}
+
+int mars_kv_restore_rows(mars_ctx* ctx, int64_t n, const int64_t* rows, const int32_t* counts,
+                         const int64_t* slots) {
+  int rc = kv_tier_ready(ctx);
+  if (rc) return rc;
+  if (n < 0 || (n > 0 && (!rows || !counts || !slots))) return MARS_ERR_ARG;
+  CK(cudaSetDevice(ctx->device));
+  i64 tot = 0;
+  if (n > 0) {
+    rc = kv_rows_ids(ctx, n, rows, counts, &tot);
+    if (rc) return rc;
+    i64 o = 0;
+    for (int64_t i = 0; i < n; ++i) {  // every row from its own slots
+      if (slots[i] < 0 || slots[i] + counts[i] > ctx->kv.host_blocks)
+        return fail(ctx, MARS_ERR_ARG, "host slots");
+      if (counts[i] > 0) {
+        rc = kv_stage_copy(ctx, ctx->kv_ids + o, counts[i], slots[i], 1);
+        if (rc) return rc;
+      }
+      o += counts[i];
+    }
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  KvScal s;
+  CK(cudaMemcpy(&s, ctx->kv.s, sizeof s, cudaMemcpyDeviceToHost));
+  if (s.status & 256) return fail(ctx, MARS_ERR_CONTRACT, "row table length != count");
   return MARS_OK;
 }
 

@@ -4220,23 +4220,21 @@ int mars_enqueue_step(const LaunchArgs* a) {
   lchk("k_walk");
   launches++;
   mark(3, 1, s2);
+  // Host enqueue order matters beyond the streams' own order: streams can
+  // share a hardware work queue (CUDA_DEVICE_MAX_CONNECTIONS), and there an
+  // entry that waits for the walk would block everything queued after it --
+  // the control plane the walk may be waiting for included.  So nothing that
+  // depends on the walk is enqueued before the control plane is.
   if (kv_fused) {
     // S5, expired list in rank order (k_scan laid out the frees): the expired
     // tables go back to the free stack on the main stream beside the walk
-    // (small CTAs: they never need the walk's SM), then the walk's journal
-    // applies on the walk's stream behind both, beside the control plane
+    // (small CTAs: they never need the walk's SM)
     mark(5, 0, s);
     mars_kv_enqueue_exp_free(*a->kv, s, a->work, a->bufs, nsm, /*offsets_done=*/true);
     mark(5, 1, s);
     launches++;
     cudaEventRecord(a->ev_kvx, s);
-    cudaStreamWaitEvent(s2, a->ev_kvx, 0);
-    mark(6, 0, s2);
-    mars_kv_enqueue_apply_step(*a->kv, s2, a->work, a->bufs, 1);
-    mark(6, 1, s2);
-    launches++;
   }
-  cudaEventRecord(a->ev_join, s2);
   // the early pack's SMs return before any other grid-wide kernel starts
   if (a->pack_early) cudaStreamWaitEvent(s, a->ev_pack, 0);
   if (a->exp_sort || a->exp_may_be_big) {
@@ -4288,6 +4286,16 @@ int mars_enqueue_step(const LaunchArgs* a) {
     mark(5, 1, s);
     launches += 2;
   }
+  // the walk's stream, behind the walk: (S5, fused) its journal, after the
+  // expired tables' pushes, beside the control plane; then the join
+  if (kv_fused) {
+    cudaStreamWaitEvent(s2, a->ev_kvx, 0);
+    mark(6, 0, s2);
+    mars_kv_enqueue_apply_step(*a->kv, s2, a->work, a->bufs, 1);
+    mark(6, 1, s2);
+    launches++;
+  }
+  cudaEventRecord(a->ev_join, s2);
   cudaStreamWaitEvent(s, a->ev_join, 0);
   if (a->advance) {
     k_advance<<<1, 1024, 0, s>>>(a->tab, a->cfg, a->work, a->bufs, a->sc);
@@ -4320,4 +4328,24 @@ int mars_enqueue_flush(cudaStream_t s, u8* p, i64 n, u32 salt) {
   if (prior != cudaSuccess) return 1000 + (int)prior;  // an earlier call left an error
   k_flush<<<1184, 256, 0, s>>>(p, n, salt);
   return (int)cudaGetLastError();
+}
+
+// Every kernel of this file loaded now (CUDA loads modules lazily by default):
+// a kernel first launched while the walk spins on the control plane's flag
+// must not wait on its own loading (which can wait for the device).
+int mars_kernels_preload() {
+  cudaFuncAttributes fa;
+  const void* fns[] = {(const void*)k_advance, (const void*)k_build_global_queue,
+                       (const void*)k_control, (const void*)k_exp_gather,
+                       (const void*)k_exp_small, (const void*)k_export_queue,
+                       (const void*)k_flush, (const void*)k_gather, (const void*)k_gather_out,
+                       (const void*)k_global_control, (const void*)k_lsd_coop,
+                       (const void*)k_pack, (const void*)k_resume,
+                       (const void*)k_retention_batch, (const void*)k_scan,
+                       (const void*)k_scatter, (const void*)k_walk, (const void*)k_work_init};
+  for (const void* f : fns) {
+    cudaError_t e = cudaFuncGetAttributes(&fa, f);
+    if (e != cudaSuccess) return (int)e;
+  }
+  return 0;
 }

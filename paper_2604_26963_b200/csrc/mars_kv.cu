@@ -83,7 +83,9 @@ __device__ __forceinline__ unsigned char* kv_scratch() {
 // the whole CTA.  Free i pushes its segments above those of frees 0..i-1; its
 // first freed ID ends on top.  Thread i plans op i (prefix sums give every
 // op's segment / arena / chunk-pool offsets), then one warp per op writes it.
-__device__ bool kv_free_run(Kv& k, int m, const u32* rows, const i32* ns) {
+// capm (nullable): per op, 1 if the freed IDs go to the host-tier capture
+__device__ bool kv_free_run(Kv& k, int m, const u32* rows, const i32* ns,
+                            const u8* capm = nullptr) {
   u32* o_row = (u32*)kv_scratch();
   i32* o_L = (i32*)(o_row + KV_TPB);
   i32* o_keep = o_L + KV_TPB;
@@ -131,7 +133,7 @@ __device__ bool kv_free_run(Kv& k, int m, const u32* rows, const i32* ns) {
     if (ko == Lo) continue;  // nothing freed
     FreePlan g = free_plan(Lo, ko);
     kv_free_warp(k, o_row[o], g, s0 + o_so[o], a0 + o_ao[o], o_ro[o] < 0 ? -1 : c0 + o_ro[o],
-                 lane);
+                 lane, capm != nullptr && capm[o] != 0);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -338,6 +340,7 @@ __device__ void kv_apply_list(Kv& k, i64 n_ops, const u8* op, const u32* row, co
   __shared__ u32 s_row[KV_TPB];
   __shared__ i32 s_n[KV_TPB];
   __shared__ u8 s_kd[KV_TPB];
+  __shared__ u8 s_cap[KV_TPB];  // host-tier capture: a running session's eviction
   __shared__ int s_m;
   const int t = threadIdx.x;
   i64 i = 0;
@@ -351,6 +354,7 @@ __device__ void kv_apply_list(Kv& k, i64 n_ops, const u8* op, const u32* row, co
       else kd = (o == MARS_KV_ALLOC) ? 1 : (o == MARS_KV_FREE ? 2 : 0);
       s_row[t] = row[i + t];
       s_n[t] = (journal && kd == 2) ? -1 : n[i + t];
+      s_cap[t] = (journal && o == MARS_J_EVICT_RUNNING) ? 1 : 0;
     }
     s_kd[t] = (u8)kd;
     if (t == 0) s_m = KV_TPB;
@@ -371,7 +375,7 @@ __device__ void kv_apply_list(Kv& k, i64 n_ops, const u8* op, const u32* row, co
     const int m = s_m;
     bool ok = true;
     if (kind == 1) ok = kv_alloc_run(k, m, s_row, s_n);
-    else if (kind == 2) ok = kv_free_run(k, m, s_row, s_n);
+    else if (kind == 2) ok = kv_free_run(k, m, s_row, s_n, s_cap);
     if (!ok) return;
     i += m;
     __syncthreads();
@@ -471,17 +475,21 @@ __global__ void __launch_bounds__(KV_TPB) k_kv_apply_step(Kv k, Work* w, Bufs b,
   if (parts & 1) kv_apply_list(k, w->n_journal, b.j_op, b.j_row, b.j_n, true);
   if ((parts & 2) && (w->in.mode & MARS_MODE_ADVANCE) && k.s->status == 0) {
     __shared__ u32 s_r[KV_TPB];
+    __shared__ u8 s_c[KV_TPB];
     __shared__ int s_m;
     const int nr = w->n_round_end;
     for (int i0 = 0; i0 < nr; i0 += KV_TPB) {
       if (threadIdx.x == 0) {
         int m = 0;
         for (int i = i0; i < nr && i < i0 + KV_TPB; ++i)
-          if (b.end_kind[i] != 1) s_r[m++] = b.end_row[i];
+          if (b.end_kind[i] != 1) {
+            s_c[m] = b.end_kind[i] == 2 ? 1 : 0;  // an unpinned boundary (not a finished session)
+            s_r[m++] = b.end_row[i];
+          }
         s_m = m;
       }
       __syncthreads();
-      if (!kv_free_run(k, s_m, s_r, nullptr)) return;
+      if (!kv_free_run(k, s_m, s_r, nullptr, s_c)) return;
     }
   }
 }
@@ -603,6 +611,27 @@ int mars_kv_enqueue_bulk(const Kv& k, cudaStream_t s, i64 n, const u32* rows, co
   return (int)cudaGetLastError();
 }
 
+// the tables of n rows into one list (row i's IDs at out[off[i]..off[i+1]),
+// one warp per row; a table whose length is not off[i+1] - off[i] sets
+// status bit 256
+__global__ void k_kv_gather_ids(Kv k, i64 n, const u32* rows, const i64* off, u32* out) {
+  const int lane = threadIdx.x & 31;
+  for (i64 i = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n;
+       i += ((i64)gridDim.x * blockDim.x) >> 5) {
+    const u32 r = rows[i];
+    const i64 o = off[i], c = off[i + 1] - o;
+    if (lane == 0 && (i64)k.len[r] != c) atomicOr(&k.s->status, 256);
+    const u32* dr = k.dir + (i64)r * k.D;
+    for (i64 p = lane; p < c; p += 32) out[o + p] = k.chunks[(i64)dr[p / KV_CH] * KV_CH + p % KV_CH];
+  }
+}
+
+int mars_kv_enqueue_gather_ids(const Kv& k, cudaStream_t s, i64 n, const u32* rows, const i64* off,
+                               u32* out, int grid) {
+  k_kv_gather_ids<<<grid, 256, 0, s>>>(k, n, rows, off, out);
+  return (int)cudaGetLastError();
+}
+
 int mars_kv_enqueue_table(const Kv& k, cudaStream_t s, u32 row, i64 cap, u32* out) {
   k_kv_table<<<16, 256, 0, s>>>(k, row, cap, out);
   return (int)cudaGetLastError();
@@ -660,4 +689,20 @@ int mars_kv_enqueue_stage(const Kv& k, cudaStream_t s, const u32* ids, i64 n, u8
                           int grid) {
   k_kv_stage<<<grid, 512, 0, s>>>(k, ids, n, stage, dir);
   return (int)cudaGetLastError();
+}
+
+// every kernel of this file loaded now (see mars_kernels_preload)
+int mars_kv_preload() {
+  cudaFuncAttributes fa;
+  const void* fns[] = {(const void*)k_kv_apply, (const void*)k_kv_apply_step,
+                       (const void*)k_kv_bulk_fill, (const void*)k_kv_bulk_scan,
+                       (const void*)k_kv_copy, (const void*)k_kv_exp_push,
+                       (const void*)k_kv_exp_scan, (const void*)k_kv_gather_ids,
+                       (const void*)k_kv_resume_free, (const void*)k_kv_stage,
+                       (const void*)k_kv_table, (const void*)k_kv_top};
+  for (const void* f : fns) {
+    cudaError_t e = cudaFuncGetAttributes(&fa, f);
+    if (e != cudaSuccess) return (int)e;
+  }
+  return 0;
 }

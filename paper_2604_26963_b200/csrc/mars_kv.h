@@ -13,6 +13,8 @@ struct KvScal {
   i64 fresh;    // next never-used block ID (implicit stack bottom)
   i64 cfs_top;  // free table chunks
   i32 status;   // contract-break bits
+  i32 pad_;
+  i64 cap_n;    // IDs captured for the host tier since the last offload
 };
 
 struct Kv {
@@ -40,6 +42,10 @@ struct Kv {
   i64 block_bytes;
   i32 layers;
   i64 host_blocks;
+  // host tier driven by the step's decisions: the IDs of the tables that
+  // running-session evictions and unpinned tool boundaries free are captured
+  // here (any order), to be copied to host memory after the step
+  u32* cap;       // [total] or null (capture off)
 };
 
 
@@ -99,8 +105,23 @@ __device__ __forceinline__ FreePlan free_plan(i64 L, i64 keep) {
 // arena at ap.. (each segment pops from its end), T's chunk back to the pool
 // at cfs[cf] (cf < 0: none); the lanes copy IDs / write segments in parallel.
 __device__ __forceinline__ void kv_free_warp(const Kv& k, u32 row, const FreePlan& f, i64 sp,
-                                             i64 ap, i64 cf, int lane) {
+                                             i64 ap, i64 cf, int lane, bool cap = false) {
   const u32* dr = k.dir + (i64)row * k.D;
+  if (cap && k.cap != nullptr && f.L > f.keep) {
+    // the freed IDs (table positions [keep, L)) to the capture list first
+    const i64 n = f.L - f.keep;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd((unsigned long long*)&k.s->cap_n, (unsigned long long)n);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if ((i64)base + n > k.total) {
+      if (lane == 0) atomicOr(&k.s->status, 128);
+    } else {
+      for (i64 j = lane; j < n; j += 32) {
+        const i64 p = f.keep + j;
+        k.cap[base + j] = k.chunks[(i64)dr[p / KV_CH] * KV_CH + p % KV_CH];
+      }
+    }
+  }
   if (f.nt > 0) {
     for (i64 j = lane; j < f.nt; j += 32) {
       const i64 p = f.tb + j;
@@ -144,6 +165,7 @@ __device__ __forceinline__ void kv_free_table_warp(const Kv& k, u32 row, i64 L, 
   kv_free_warp(k, row, f, sp, ap, tail > 0 ? cf : -1, lane);
 }
 
+int mars_kv_preload();
 int mars_kv_enqueue_apply(const Kv& k, cudaStream_t s, i64 n_ops, const u8* op, const u32* row,
                           const i32* n);
 // the step's journal (parts & 1) and the tick tail's frees (parts & 2)
@@ -156,6 +178,8 @@ int mars_kv_enqueue_bulk(const Kv& k, cudaStream_t s, i64 n, const u32* rows, co
 int mars_kv_enqueue_resume_free(const Kv& k, cudaStream_t s, i64 n, const i64* rows,
                                 const u8* kind);
 int mars_kv_enqueue_table(const Kv& k, cudaStream_t s, u32 row, i64 cap, u32* out);
+int mars_kv_enqueue_gather_ids(const Kv& k, cudaStream_t s, i64 n, const u32* rows, const i64* off,
+                               u32* out, int grid);
 int mars_kv_enqueue_top(const Kv& k, cudaStream_t s, i64 cnt, u32* out);
 int mars_kv_enqueue_copy(const Kv& k, cudaStream_t s, const u32* ids, i64 n, i64 slot0, int dir,
                          int grid);

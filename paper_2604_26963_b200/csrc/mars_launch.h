@@ -37,6 +37,7 @@ struct LaunchArgs {
 };
 
 int mars_kernels_init();
+int mars_kernels_preload();
 int mars_enqueue_step(const LaunchArgs* a);
 int mars_enqueue_retention(const Cfg& c, cudaStream_t s, i64 n, const i32* ctx, const i32* kv,
                            i64 total, double usage, double ema, double now, u8* pin, double* bb,

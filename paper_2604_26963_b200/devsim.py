@@ -154,7 +154,8 @@ def run_device_simulation(traces: Sequence, total_blocks: int, tool_worker_slots
                           initial_window: Optional[float] = None, device: int = 0,
                           max_ticks: int = 5_000_000,
                           log: Optional[EventLog] = None,
-                          kv_state: Optional[dict] = None) -> Tuple[Dict[str, int], float]:
+                          kv_state: Optional[dict] = None,
+                          kv_tier: Optional[dict] = None) -> Tuple[Dict[str, int], float]:
     """``policy`` (a POLICY_KINDS name) over ``traces`` (objects with
     session_id, arrival_time_s and rounds of new_prefill_tokens /
     decode_tokens / tool_duration_s, as agentsched.workload.Trace).  MARS
@@ -164,7 +165,17 @@ def run_device_simulation(traces: Sequence, total_blocks: int, tool_worker_slots
     one is given.  With ``kv_state`` (a dict) the device block-ID manager
     rides along (every alloc / free of the run applied to concrete block IDs
     on the device, mars_kv) and its final free-stack order is stored there
-    as ``kv_state["top"]`` (with ``depth``, ``fresh``, ``status``)."""
+    as ``kv_state["top"]`` (with ``depth``, ``fresh``, ``status``).
+
+    ``kv_tier`` (a dict, with ``kv_state``): the KV bytes follow the run's
+    decisions through a pinned host ring (``block_bytes``, ``host_blocks``;
+    decision-neutral, the reference has no host tier): a pin
+    copies the session's table to the host (sim.py:261-265), a warm resume
+    copies it back (sim.py:193-200), and a running session's eviction or an
+    unpinned tool boundary copies the freed blocks out (captured on the
+    device as the step frees them).  Blocks, bytes and copy times per
+    direction are stored back into the dict; ``verify=True`` also records
+    which block every host slot holds (``slot_ids``)."""
     order = sorted(traces, key=lambda t: (t.arrival_time_s, t.session_id))
     n = len(order)
     cfg = make_config(enable_coordinator, enable_coscheduler, initial_window=initial_window,
@@ -183,15 +194,136 @@ def run_device_simulation(traces: Sequence, total_blocks: int, tool_worker_slots
             from .kvstore import KvBlockManager
             most = max((-(-sum(r.new_prefill_tokens + r.decode_tokens for r in tr.rounds) // bs)
                         for tr in order), default=1)
-            kv = KvBlockManager(eng, total_blocks, max_blocks_per_row=max(most, 1))
+            if kv_tier is not None:
+                kv = KvBlockManager(eng, total_blocks, max_blocks_per_row=max(most, 1),
+                                    block_bytes=int(kv_tier["block_bytes"]), layers=1,
+                                    host_blocks=int(kv_tier.get("host_blocks", 2 * total_blocks)))
+                if kv_tier.get("pattern"):
+                    _fill_pattern(kv)
+                kv.capture(True)
+            else:
+                kv = KvBlockManager(eng, total_blocks, max_blocks_per_row=max(most, 1))
+        tier = _HostTier(kv, kv_tier) if kv_tier is not None else None
         out = _run(eng, cfg, order, total_blocks, tool_worker_slots, max_ticks, cfg_admission,
-                   policy, log, decides)
+                   policy, log, decides, tier)
+        if tier is not None:
+            tier.finish()
         if kv is not None:
             top, depth, fresh, status = kv.state(total_blocks)
             kv_state.update(top=top, depth=depth, fresh=fresh, status=status)
         return out
     finally:
         eng.close()
+
+
+def block_pattern(ids, block_bytes: int) -> np.ndarray:
+    """Test content of pool blocks: block `id` holds its id (u32) followed
+    by the byte id % 251."""
+    ids = np.asarray(ids, np.uint32)
+    out = np.empty((len(ids), block_bytes), np.uint8)
+    out[:] = (ids % 251).astype(np.uint8)[:, None]
+    out[:, :4] = ids.view(np.uint8).reshape(-1, 4)
+    return out
+
+
+def _fill_pattern(kv) -> None:
+    """Every pool block gets block_pattern (through the host tier)."""
+    host = kv.host_view()
+    n = min(kv.total_blocks, kv.host_blocks)
+    for a in range(0, kv.total_blocks, n):
+        ids = np.arange(a, min(a + n, kv.total_blocks), dtype=np.uint32)
+        host[:len(ids)] = block_pattern(ids, kv.block_bytes)
+        kv.restore(ids, 0, 2)
+
+
+class _HostTier:
+    """The KV bytes the run's decisions imply, through the host ring."""
+
+    def __init__(self, kv, stats: dict) -> None:
+        import time
+        self._time = time.perf_counter
+        self.kv, self.st = kv, stats
+        self.verify = bool(stats.get("verify"))
+        self.slots: Dict[int, Tuple[int, int]] = {}   # pinned row -> (first slot, blocks)
+        self.slot_ids: Dict[int, int] = {}            # (verify) host slot -> block id
+        for k in ("evict_blocks", "pin_blocks", "restore_blocks", "d2h_s", "h2d_s"):
+            stats[k] = 0
+        self.bb = kv.block_bytes
+
+    def _guard(self, s0: int, n: int) -> None:
+        # a ring write over a pinned session's host copy would break its restore
+        for r, (a, m) in self.slots.items():
+            if s0 < a + m and a < s0 + n:
+                raise RuntimeError(f"host tier too small: pinned row {r}'s copy overwritten")
+
+    def after_step(self, res) -> None:
+        t0 = self._time()
+        n, s0, ids = self.kv.offload_captured(want_ids=self.verify)
+        if n:
+            self._guard(s0, n)
+            self.st["evict_blocks"] += n
+            if self.verify:
+                self.slot_ids.update(zip(range(s0, s0 + n), ids.tolist()))
+        pins = [(int(r), int(b)) for r, k, b in zip(res.end_rows.tolist(), res.end_kind.tolist(),
+                                                     res.end_blocks.tolist()) if k == 1 and b > 0]
+        if pins:
+            rows = [r for r, _ in pins]
+            cnts = [b for _, b in pins]
+            if self.verify:
+                tabs = [self.kv.table(r) for r in rows]
+            s0 = self.kv.offload_rows(rows, cnts)
+            self._guard(s0, sum(cnts))
+            a = s0
+            for i, (r, b) in enumerate(pins):
+                self.slots[r] = (a, b)
+                if self.verify:
+                    self.slot_ids.update(zip(range(a, a + b), tabs[i].tolist()))
+                a += b
+            self.st["pin_blocks"] += sum(cnts)
+        self.st["d2h_s"] += self._time() - t0
+
+    def after_resume(self, rows, kinds, blocks) -> None:
+        warm = [(int(r), int(b)) for r, k, b in zip(rows, kinds, blocks) if k == 0 and b > 0]
+        for r, k in zip(rows, kinds):
+            if k != 0:
+                self.slots.pop(int(r), None)   # an expired pin: its host copy is dropped
+        if not warm:
+            return
+        t0 = self._time()
+        slots = []
+        for r, b in warm:
+            a, m = self.slots.pop(r)
+            if m != b:
+                raise RuntimeError(f"warm resume of row {r}: {b} blocks, {m} offloaded")
+            slots.append(a)
+        self.kv.restore_rows([r for r, _ in warm], [b for _, b in warm], slots)
+        self.st["restore_blocks"] += sum(b for _, b in warm)
+        self.st["h2d_s"] += self._time() - t0
+
+    def finish(self) -> None:
+        st, bb = self.st, self.bb
+        st["d2h_bytes"] = (st["evict_blocks"] + st["pin_blocks"]) * bb
+        st["h2d_bytes"] = st["restore_blocks"] * bb
+        st["d2h_gbs"] = st["d2h_bytes"] / st["d2h_s"] / 1e9 if st["d2h_s"] else None
+        st["h2d_gbs"] = st["h2d_bytes"] / st["h2d_s"] / 1e9 if st["h2d_s"] else None
+        if self.verify and st.get("pattern"):
+            # every host slot holds the block it was given, and the pool blocks
+            # (pinned tables restored in place) still hold their own content
+            host = self.kv.host_view()
+            slots = np.fromiter(self.slot_ids.keys(), np.int64, len(self.slot_ids))
+            ids = np.fromiter(self.slot_ids.values(), np.int64, len(self.slot_ids))
+            bad = 0
+            for a in range(0, len(slots), 4096):
+                s_, i_ = slots[a:a + 4096], ids[a:a + 4096]
+                bad += int((host[s_] != block_pattern(i_, bb)).any(axis=1).sum())
+            st["host_slots_checked"], st["host_slots_bad"] = len(slots), bad
+            pool_bad = 0
+            n = min(self.kv.total_blocks, self.kv.host_blocks)
+            for a in range(0, self.kv.total_blocks, n):
+                i_ = np.arange(a, min(a + n, self.kv.total_blocks), dtype=np.uint32)
+                self.kv.evict(i_, 0, 2)
+                pool_bad += int((host[:len(i_)] != block_pattern(i_, bb)).any(axis=1).sum())
+            st["pool_blocks_bad"] = pool_bad
 
 
 def _initial_level(tokens: int, cfg) -> int:  # scheduler.py:87-97
@@ -202,7 +334,8 @@ def _initial_level(tokens: int, cfg) -> int:  # scheduler.py:87-97
 
 
 def _run(eng: MarsEngine, cfg, order, total_blocks: int, slots: int, max_ticks: int,
-         admission: bool, policy: str, log: Optional[EventLog], decides: bool):
+         admission: bool, policy: str, log: Optional[EventLog], decides: bool,
+         tier: Optional[_HostTier] = None):
     n = len(order)
     bs = int(cfg.block_size)
     sid_rank = {sid: i for i, sid in enumerate(sorted(t.session_id for t in order))}
@@ -312,8 +445,10 @@ def _run(eng: MarsEngine, cfg, order, total_blocks: int, slots: int, max_ticks: 
             cnt["cold_resumes"] += c["cold"]
             cnt["evictions"] += c["evicted"]
             pinned -= c["warm"] + c["evicted"]
+            rr = eng.resume_rows(len(rows)) if (log is not None or tier is not None) else None
+            if tier is not None:   # warm resumes: their tables back from the host tier
+                tier.after_resume(rows, rr["kind"].tolist(), rr["blocks"].tolist())
             if log is not None:
-                rr = eng.resume_rows(len(rows))
                 for i, d in enumerate(done):
                     r = d.row
                     log.emit(d.finish_time, "tool_end", sid[r], duration_s=d.duration_s,
@@ -340,6 +475,8 @@ def _run(eng: MarsEngine, cfg, order, total_blocks: int, slots: int, max_ticks: 
         res = eng.step(si)
         if res.status:
             raise RuntimeError(f"device step status {res.status}")
+        if tier is not None:   # evicted / unpinned blocks and new pins to the host tier
+            tier.after_step(res)
         if log is not None:
             for r, b in zip(res.expired_rows.tolist(), res.expired_blocks.tolist()):
                 evict_log(r, b, "pinned", "pin_expired", now)   # sim.py:324-325

@@ -112,6 +112,42 @@ class KvBlockManager:
                                              ids.ctypes.data_as(C.c_void_p), int(slot0),
                                              int(method)))
 
+    # -- the host tier driven by the step's decisions (mars_kv_capture ...) ----
+
+    def capture(self, on: bool = True) -> None:
+        """Record the IDs that running-session evictions and unpinned tool
+        boundaries free during the engine's steps (for offload_captured)."""
+        self._check(self.lib.mars_kv_capture(self.eng.ctx, int(bool(on))))
+
+    def offload_captured(self, want_ids: bool = False):
+        """Copies the captured blocks to the next host-ring slots:
+        (n_blocks, first slot or -1, the IDs in slot order or None)."""
+        n, s0 = C.c_int64(), C.c_int64()
+        ids = np.zeros(self.total_blocks if want_ids else 1, np.uint32)
+        self._check(self.lib.mars_kv_offload_captured(
+            self.eng.ctx, C.byref(n), C.byref(s0), ids.ctypes.data_as(C.c_void_p) if want_ids
+            else None, len(ids) if want_ids else 0))
+        return n.value, s0.value, (ids[:n.value].copy() if want_ids else None)
+
+    def offload_rows(self, rows, counts) -> int:
+        """Whole tables of `rows` (counts[i] = row i's table length) to the
+        host ring; row i lands at the returned slot + sum(counts[:i])."""
+        r = np.ascontiguousarray(rows, np.int64)
+        c = np.ascontiguousarray(counts, np.int32)
+        s0 = C.c_int64()
+        self._check(self.lib.mars_kv_offload_rows(self.eng.ctx, len(r), r.ctypes.data_as(C.c_void_p),
+                                                  c.ctypes.data_as(C.c_void_p), C.byref(s0)))
+        return s0.value
+
+    def restore_rows(self, rows, counts, slots) -> None:
+        """The rows' tables back from their host slots (slots[i] = row i's first)."""
+        r = np.ascontiguousarray(rows, np.int64)
+        c = np.ascontiguousarray(counts, np.int32)
+        s = np.ascontiguousarray(slots, np.int64)
+        self._check(self.lib.mars_kv_restore_rows(self.eng.ctx, len(r), r.ctypes.data_as(C.c_void_p),
+                                                  c.ctypes.data_as(C.c_void_p),
+                                                  s.ctypes.data_as(C.c_void_p)))
+
     def host_view(self) -> np.ndarray:
         """The pinned host tier as a uint8 array [host_blocks, block_bytes]."""
         h, d = C.c_void_p(), C.c_void_p()

@@ -243,3 +243,36 @@ def test_deep_alloc_run_pops_many_small_segments():
     kv.apply(ops)
     _same_state(kv, ref, {"s3500": 3500, "s17": 17, "s2999": 2999})
     eng.close()
+
+
+@pytest.mark.parametrize("key", ["openhands_heavy40/mars", "demo64/mars", "small12/mars-no-coscheduler"])
+def test_host_tier_follows_the_decisions(key):
+    """the KV bytes move as the run's decisions imply
+    -- a pin copies the table to the host ring, a warm resume copies it back,
+    a running session's eviction and an unpinned tool boundary copy the freed
+    blocks out (captured on the device while the step frees them) -- while
+    the event log stays the reference's byte for byte.  Every host slot holds
+    the block it was given and no pool block is corrupted by the restores."""
+    from oracle import tracefile
+    from paper_2604_26963_b200.devsim import EventLog, run_device_simulation
+    from tests._sim import SIM, VARIANT_KW
+    from tests.conftest import GOLDEN
+    import hashlib
+    import os
+    spec = SIM[key]
+    traces = tracefile.load(os.path.join(GOLDEN, spec["trace"]))
+    log, kv = EventLog(), {}
+    tier = {"block_bytes": 1024, "pattern": True, "verify": True}
+    run_device_simulation(traces, spec["engine"]["total_blocks"], spec["engine"]["tool_worker_slots"],
+                          enable_control_plane=spec["run"].get("enable_control_plane", True),
+                          log=log, kv_state=kv, kv_tier=tier, **VARIANT_KW[key.split("/")[1]])
+    assert hashlib.sha256(log.jsonl_bytes()).hexdigest() == spec["sha256"]
+    assert kv["status"] == 0
+    recs = log.records
+    out = sum(r["blocks"] for r in recs if r["kind"] == "evict" and r["victim"] in ("running", "boundary"))
+    assert tier["evict_blocks"] == out
+    assert tier["pin_blocks"] == sum(r["blocks"] for r in recs if r["kind"] == "pin")
+    assert tier["restore_blocks"] == sum(r["blocks"] for r in recs if r["kind"] == "unpin")
+    assert tier["evict_blocks"] + tier["pin_blocks"] > 0
+    assert tier["host_slots_checked"] > 0 and tier["host_slots_bad"] == 0
+    assert tier["pool_blocks_bad"] == 0
