@@ -193,6 +193,43 @@ def kv_sweep(device: int, batches=(1, 16, 256, 2048), reps: int = 3) -> dict:
             "sweep": sweep}
 
 
+def kv_tier_run(block_bytes: int = 16384, key: str = "openhands_heavy40/mars") -> dict:
+    """SURVEY.md §8(d) config (5), the KV path: the OpenHands-style heavy
+    trace run whole on the device (devsim, event log byte-identical to the
+    reference's) with the host tier following its decisions -- pins copied
+    to pinned host memory, warm resumes copied back, running-session
+    evictions and unpinned boundaries copied out -- at `block_bytes` per
+    16-token block (the Llama-3-8B 2 MiB block would need 340 GB of HBM for
+    this pool).  GB/s = bytes / time of the copy calls (synchronous, staged
+    DMA), against the pinned-copy peak of the link measured here."""
+    from paper_2604_26963_b200.devsim import EventLog, load_trace, run_device_simulation
+    from paper_2604_26963_b200.engine import MarsEngine
+    from paper_2604_26963_b200.kvstore import host_link_peak
+
+    ref_dir = os.path.join(ROOT, "tests", "golden")
+    with open(os.path.join(ref_dir, "sim_logs.json")) as fh:
+        spec = json.load(fh)[key]
+    traces = load_trace(os.path.join(ref_dir, spec["trace"]))
+    total = spec["engine"]["total_blocks"]
+    log, kv = EventLog(), {}
+    tier = {"block_bytes": block_bytes, "host_blocks": 2 * total}
+    t0 = time.perf_counter()
+    run_device_simulation(traces, total, spec["engine"]["tool_worker_slots"], log=log,
+                          kv_state=kv, kv_tier=tier)
+    wall = time.perf_counter() - t0
+    import hashlib
+    same = hashlib.sha256(log.jsonl_bytes()).hexdigest() == spec["sha256"]
+    eng = MarsEngine(max_rows=64, max_queue=1)
+    d2h, h2d, _ = host_link_peak(eng, 1 << 30, 5)
+    eng.close()
+    out = {k: tier[k] for k in ("evict_blocks", "pin_blocks", "restore_blocks", "d2h_bytes",
+                                "h2d_bytes", "d2h_s", "h2d_s", "d2h_gbs", "h2d_gbs")}
+    out.update(trace=key, block_bytes=block_bytes, log_identical=same, run_wall_s=wall,
+               peak_d2h_gbs=d2h, peak_h2d_gbs=h2d,
+               d2h_frac=(tier["d2h_gbs"] or 0) / d2h, h2d_frac=(tier["h2d_gbs"] or 0) / h2d)
+    return out
+
+
 def hbm_sweep(device: int, sizes, steps: int = 5, warmup: int = 3, flush_mb: int = 512) -> list:
     """the step and its scan kernel on tables far beyond the
     126 MB L2 (L2 flushed before every step), where the 1M-session step's
@@ -798,6 +835,11 @@ def main():
             line["kv"] = kv_sweep(local)
         except Exception as exc:  # the scheduler number stands on its own
             line["kv"] = {"error": repr(exc)[:300]}
+        if rank == 0 and world == 1:
+            try:
+                line["kv_tier"] = kv_tier_run()
+            except Exception as exc:
+                line["kv_tier"] = {"error": repr(exc)[:300]}
     if rank == 0 and world == 1 and a.regimes:
         try:
             line["regimes"] = regime_sweep(local, a.sessions)

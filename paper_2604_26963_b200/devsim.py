@@ -28,7 +28,7 @@ import heapq
 import json
 import math
 from dataclasses import dataclass
-from typing import Dict, List, Optional, Sequence, Tuple
+from typing import Dict, List, NamedTuple, Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -216,6 +216,36 @@ def run_device_simulation(traces: Sequence, total_blocks: int, tool_worker_slots
         eng.close()
 
 
+class TraceRound(NamedTuple):
+    new_prefill_tokens: int
+    decode_tokens: int
+    tool_duration_s: Optional[float]
+
+
+class SessionTrace(NamedTuple):
+    session_id: str
+    arrival_time_s: float
+    rounds: Tuple[TraceRound, ...]
+
+
+def load_trace(path: str) -> List[SessionTrace]:
+    """A JSONL session-trace file in the reference's format
+    (agentsched/workload.py:276-330: session_id, arrival_time_s, rounds of
+    new_prefill_tokens / decode_tokens / tool_duration_s)."""
+    out = []
+    with open(path, "r", encoding="utf-8") as fh:
+        for line in fh:
+            if not line.strip():
+                continue
+            rec = json.loads(line)
+            out.append(SessionTrace(
+                str(rec["session_id"]), float(rec["arrival_time_s"]),
+                tuple(TraceRound(int(r["new_prefill_tokens"]), int(r["decode_tokens"]),
+                                 None if r["tool_duration_s"] is None else float(r["tool_duration_s"]))
+                      for r in rec["rounds"])))
+    return out
+
+
 def block_pattern(ids, block_bytes: int) -> np.ndarray:
     """Test content of pool blocks: block `id` holds its id (u32) followed
     by the byte id % 251."""
@@ -257,9 +287,11 @@ class _HostTier:
                 raise RuntimeError(f"host tier too small: pinned row {r}'s copy overwritten")
 
     def after_step(self, res) -> None:
+        # (copy times: the calls that moved blocks, each synchronous)
         t0 = self._time()
         n, s0, ids = self.kv.offload_captured(want_ids=self.verify)
         if n:
+            self.st["d2h_s"] += self._time() - t0
             self._guard(s0, n)
             self.st["evict_blocks"] += n
             if self.verify:
@@ -271,7 +303,9 @@ class _HostTier:
             cnts = [b for _, b in pins]
             if self.verify:
                 tabs = [self.kv.table(r) for r in rows]
+            t0 = self._time()
             s0 = self.kv.offload_rows(rows, cnts)
+            self.st["d2h_s"] += self._time() - t0
             self._guard(s0, sum(cnts))
             a = s0
             for i, (r, b) in enumerate(pins):
@@ -280,7 +314,6 @@ class _HostTier:
                     self.slot_ids.update(zip(range(a, a + b), tabs[i].tolist()))
                 a += b
             self.st["pin_blocks"] += sum(cnts)
-        self.st["d2h_s"] += self._time() - t0
 
     def after_resume(self, rows, kinds, blocks) -> None:
         warm = [(int(r), int(b)) for r, k, b in zip(rows, kinds, blocks) if k == 0 and b > 0]
