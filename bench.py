@@ -48,15 +48,19 @@ def _peaks():
 
 
 def _ncu_traffic():
-    p = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
-    if not os.path.exists(p):
-        return None
+    """k_scan's DRAM bytes per launch (dram__bytes_read + write) from the
+    newest committed ncu capture of this bench command (profiles/, written by
+    scripts/ncu_summary.py; ncu cannot run inside the timed process)."""
+    import glob
+    caps = sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_summary_r*.json")))
+    if not caps:
+        return None, None
     try:
-        with open(p) as fh:
+        with open(caps[-1]) as fh:
             d = json.load(fh)
-        return d.get("k_scan", {}).get("dram_bytes_per_launch")
+        return d.get("k_scan", {}).get("dram_bytes_per_launch"), os.path.basename(caps[-1])
     except Exception:
-        return None
+        return None, None
 
 
 class Clocks:
@@ -816,7 +820,8 @@ def main():
         "config": workload_config(a.sessions, world),
         "s5_block_ids": s5_blocks,
         "roofline": {"bound": "hbm", "kernel": "k_scan", "achieved": achieved, "peak": peak,
-                     "unit": "GB/s", "frac": achieved / peak, "traffic": _ncu_traffic(),
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": _ncu_traffic()[0],
+                     "traffic_source": _ncu_traffic()[1],
                      "algorithmic_bytes": sb, "kernel_ms": scan_avg, "peak_source": peak_kind,
                      "step_algorithmic_bytes": step_bytes(snap),
                      "step_frac": step_bytes(snap) / (ms_per_step * 1e-3) / 1e9 / peak},
