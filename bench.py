@@ -437,6 +437,56 @@ def dropin_sweep(keys=("demo64/mars", "faceoff200/mars", "openhands_heavy40/mars
     return out
 
 
+def dropin_scale(sizes=(64, 512, 4096, 32768), ticks: int = 40) -> list:
+    """The drop-in crossover: the reference's own
+    run_simulation over n sessions that all arrive at once (one long decode
+    round each, no tools, a pool that holds them all, an admission window of
+    n), so every tick plans over ~n ready sessions; `ticks` ticks
+    (run_simulation's max_ticks guard ends the run) with MarsPolicy, then
+    with the INTEGRATION.md binding.  ms per tick = wall / ticks."""
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(ref_dir) and ref_dir not in sys.path:
+        sys.path.insert(1, ref_dir)
+    try:
+        from agentsched import baselines, control, sim, workload
+    except ImportError:
+        return [{"error": "agentsched (baseline/_ref) not importable"}]
+    from paper_2604_26963_b200.admission import balance_and_admit as gpu_bna
+    from paper_2604_26963_b200.policy import GpuMarsPolicy
+
+    out = []
+    for n in sizes:
+        cfg = workload.RegimeConfig(mean_prompt_volume=2_000.0,
+                                    prompt_volume_range=(1_000.0, 4_000.0), rounds_range=(1, 1),
+                                    arrival_rate=1e6, request_count=n, seed=11,
+                                    tool_duration_distribution=None,
+                                    decode_tokens_range=(20_000, 30_000))
+        traces = workload.generate_workload(cfg)
+        params = sim.EngineParams(total_blocks=2_300 * n, tool_worker_slots=max(8, n))
+        row = {"sessions": n, "ticks": ticks}
+        for arm in ("reference", "b200"):
+            pol = baselines.make_policy("mars") if arm == "reference" else \
+                GpuMarsPolicy(max_sessions=max(n, 64))
+            orig = sim.balance_and_admit
+            if arm == "b200":
+                sim.balance_and_admit = gpu_bna
+            t0 = time.perf_counter()
+            try:
+                sim.run_simulation(traces, params, pol,
+                                   controller=control.ControllerConfig(initial_window=float(n)),
+                                   max_ticks=ticks)
+            except sim.SimulationStall:
+                pass
+            dt = time.perf_counter() - t0
+            sim.balance_and_admit = orig
+            if arm == "b200":
+                pol.close()
+            row[arm + "_ms_per_tick"] = dt * 1e3 / (ticks + 1)
+        row["b200_over_reference"] = row["reference_ms_per_tick"] / row["b200_ms_per_tick"]
+        out.append(row)
+    return out
+
+
 def cpu_reference(sessions: int, seed: int, reps: int = 1):
     """The reference's own step (agentsched from baseline/_ref, else the
     oracle port) over snapshot_v1(sessions) on one core; materialisation
@@ -853,6 +903,7 @@ def main():
     if rank == 0 and world == 1 and a.dropin:
         try:
             line["dropin"] = dropin_sweep()
+            line["dropin_scale"] = dropin_scale()
         except Exception as exc:  # the headline line stands on its own
             line["dropin"] = [{"error": repr(exc)[:300]}]
     if rank == 0 and world == 1 and a.hbm_sweep:

@@ -6,7 +6,9 @@ the triple clamp (control.py:130-163), admits the packed prefix, leaves the
 residual in packed order in ``queue`` (mutated in place), emits one
 ``window_update`` event and folds it into the telemetry.  The packing,
 median seed, window arithmetic and the admit/residual split run on the
-device (k_pack_small / k_lsd_* / k_admit_apply); the reference's sim binds
+device in one ``k_control`` launch (MARS_MODE_NO_ROWS: the one-CTA pack of a
+small list or the grid LSD sort of a big one, update_window + the triple
+clamp, the packed prefix and the residual list); the reference's sim binds
 the function by import (sim.py:29), so the drop-in swaps
 ``agentsched.sim.balance_and_admit`` (INTEGRATION.md).
 """

@@ -25,7 +25,7 @@ import numpy as np
 
 from . import _native as N
 from .engine import MarsEngine, make_config
-from .snapshot import DECODE, F_ACTIVE, F_PINNED, PHASE_NAMES, PREFILL
+from .snapshot import COLUMNS, DECODE, F_ACTIVE, F_PINNED, PHASE_NAMES, PREFILL
 
 ContractViolation = N.ContractViolation
 _PHASE_CODE = {p: i for i, p in enumerate(PHASE_NAMES)}
@@ -125,7 +125,24 @@ def config_from(mlfq=None, retention=None, pressure=None, controller=None,
 
 class GpuMarsPolicy(_PolicyBase):
     """B200 drop-in for MarsPolicy (baselines.py:318-455); a PolicyBase
-    subclass whenever the reference package is importable."""
+    subclass whenever the reference package is importable.
+
+    Device writes are batched: every hook records its row's new values on the
+    host and the next plan_tick uploads them, one call per hook kind, in the
+    order the hooks fire between two ticks (the previous tick's service
+    charges and pins, then arrivals, tool returns, evictions, admissions), and
+    only the ready rows whose Call changed since the last tick (new in the
+    ready list, planned or evicted by the last plan, touched by a hook) are
+    re-uploaded."""
+
+    # hook kind -> the columns it sets, in the order hooks fire between ticks
+    _PENDING = (("service", ("level", "served", "wait_since")),
+                ("pin", ("flags", "deadline", "pinned_blocks", "plevel")),
+                ("register", ("phase", "flags", "rank", "arrival")),
+                ("resume", ("wait_since",)),
+                ("evicted", ("flags", "kv")),
+                ("admit", ("level", "promos", "served", "wait_since", "flags")),
+                ("admit_base", ("level", "promos", "served", "flags")))
 
     name = "mars"
     uses_admission_control = True
@@ -154,7 +171,6 @@ class GpuMarsPolicy(_PolicyBase):
         self._sid: List[str] = []
         self._max_sid: Optional[str] = None
         self._ranks_dirty = False
-        self._dev_ready: set = set()
         self._pins: Dict[str, float] = {}       # sid -> retention deadline (registry view)
         self._levels: Dict[str, int] = {}       # sid -> MLFQ level (device value)
         self._admitted: set = set()
@@ -167,6 +183,10 @@ class GpuMarsPolicy(_PolicyBase):
         self._bounds = tuple(b)
         self._levels_n = getattr(mlfq, "num_levels", 4)
         self._tool_prior = getattr(pressure, "initial_tool_estimate_s", 5.0)
+        self._pend: Dict[str, Dict[int, tuple]] = {k: {} for k, _ in self._PENDING}
+        self._in_ready = np.zeros(self._max, bool)   # rows of the last uploaded ready list
+        self._dirty = np.zeros(self._max, bool)      # rows whose Call changed since
+        self._ready_rows = np.zeros(0, np.int64)
 
     # -- device context ---------------------------------------------------------
 
@@ -176,6 +196,7 @@ class GpuMarsPolicy(_PolicyBase):
             self._gpu_key = (cfg.token_budget, cfg.tick_duration_s)
             self.eng = MarsEngine(max_rows=self._max, max_queue=1, device=self._device,
                                   config=cfg)
+            self.eng.set_graph(True)  # one CUDA-graph launch per plan_tick
         elif gpu is not None and (gpu.token_budget_per_tick, gpu.tick_duration_s) != self._gpu_key:
             # the sim registers and admits sessions before the first plan_tick
             # hands over the GpuModel (sim.py:165, :297, :342): the engine
@@ -207,13 +228,28 @@ class GpuMarsPolicy(_PolicyBase):
         else:
             self._max_sid = sid
         self._sid.append(sid)
-        eng = self._engine()
-        eng.upsert({"phase": np.array([_phase_code(call.phase)], np.uint8),
-                    "flags": np.zeros(1, np.uint8), "rank": np.array([r], np.uint32),
-                    "arrival": np.array([call.arrival_time], np.float64)},
-                   rows=np.array([r]))
+        self._engine()
+        self._queue("register", r, (_phase_code(call.phase), 0, r, call.arrival_time))
         # ranks only order the device step's keys: one re-rank in the next
         # plan_tick covers every out-of-order registration before it
+
+    def _queue(self, kind: str, row: int, vals: tuple) -> None:
+        self._pend[kind][row] = vals
+        self._dirty[row] = True
+
+    def _flush(self) -> None:
+        """Uploads the hooks' pending row values (one call per hook kind)."""
+        eng = None
+        for kind, cols in self._PENDING:
+            d = self._pend[kind]
+            if not d:
+                continue
+            eng = eng or self._engine()
+            rows = np.fromiter(d.keys(), np.int64, len(d))
+            vals = list(zip(*d.values()))
+            eng.upsert({c: np.asarray(v, dtype=COLUMNS[c]) for c, v in zip(cols, vals)},
+                       rows=rows)
+            d.clear()
 
     def _sync_ranks(self) -> None:
         order = sorted(range(len(self._sid)), key=self._sid.__getitem__)
@@ -234,18 +270,14 @@ class GpuMarsPolicy(_PolicyBase):
         sid = call.session_id
         lv = self._initial_level(call.rounds[0].new_prefill_tokens)
         r = self._row[sid]
-        self._engine().upsert({"level": np.array([lv], np.uint8), "promos": np.zeros(1, np.uint8),
-                               "served": np.zeros(1, np.int64),
-                               "wait_since": np.array([now], np.float64),
-                               "flags": np.array([F_ACTIVE], np.uint8)}, rows=np.array([r]))
+        self._queue("admit", r, (lv, 0, 0, now, F_ACTIVE))
         self._levels[sid] = lv
         self._admitted.add(sid)
 
     def on_resume(self, call, now: float) -> None:
         sid = call.session_id
         if sid in self._admitted:
-            self._engine().upsert({"wait_since": np.array([now], np.float64)},
-                                  rows=np.array([self._row[sid]]))
+            self._queue("resume", self._row[sid], (now,))
 
     def on_service(self, session_id: str, tokens: int, now: float) -> None:
         if session_id not in self._admitted or not self.enable_coordinator:
@@ -261,14 +293,13 @@ class GpuMarsPolicy(_PolicyBase):
             # state before it instead (scheduler.py:100-108)
             lv, served = exp[2], exp[3] + int(tokens)
         else:  # a charge the plan did not predict: apply it to the device row
+            self._flush()
             st = self._engine().read(["level", "served"], rows=np.array([r]))
             lv, served = int(st["level"][0]), int(st["served"][0]) + int(tokens)
         q = list(getattr(self.mlfq, "level_quotas_tokens", (2_000, 8_000, 32_000, math.inf)))
         if served > q[lv] and lv < self._levels_n - 1:
             lv, served = lv + 1, 0
-        self._engine().upsert({"level": np.array([lv], np.uint8),
-                               "served": np.array([served], np.int64),
-                               "wait_since": np.array([now], np.float64)}, rows=np.array([r]))
+        self._queue("service", r, (lv, served, now))
         self._levels[session_id] = lv
 
     def level_of(self, call) -> int:
@@ -277,6 +308,7 @@ class GpuMarsPolicy(_PolicyBase):
         if not self.enable_coordinator:
             return 0
         r = self._row[call.session_id]
+        self._flush()
         return int(self._engine().read(["level"], rows=np.array([r]))["level"][0])
 
     def retention_decision(self, call, pool, telemetry, gpu, now):
@@ -301,11 +333,7 @@ class GpuMarsPolicy(_PolicyBase):
         # the round that ends here was planned this tick, so its post-charge
         # level came back with the step (no device read)
         lv = self._levels[sid] if self.enable_coordinator else 0
-        self._engine().upsert({"flags": np.array([F_ACTIVE | F_PINNED], np.uint8),
-                               "deadline": np.array([decision.retention_deadline], np.float64),
-                               "pinned_blocks": np.array([blocks], np.int32),
-                               "plevel": np.array([lv], np.uint8)},
-                              rows=np.array([r]))
+        self._queue("pin", r, (F_ACTIVE | F_PINNED, decision.retention_deadline, blocks, lv))
         self._pins[sid] = decision.retention_deadline
 
     def expired_pins(self, now: float) -> List[str]:
@@ -319,12 +347,11 @@ class GpuMarsPolicy(_PolicyBase):
         r = self._row[session_id]
         call = self.calls[session_id]
         flags = F_ACTIVE if session_id in self._admitted else 0
-        self._engine().upsert({"flags": np.array([flags], np.uint8),
-                               "kv": np.array([call.kv_tokens], np.int32)}, rows=np.array([r]))
+        self._queue("evicted", r, (flags, call.kv_tokens))
 
     # -- the tick ---------------------------------------------------------------------
 
-    def _extra_cols(self, ready: Sequence, n: int) -> dict:
+    def _extra_cols(self, calls: Sequence, n: int) -> dict:
         return {}
 
     # -- S5 block IDs: tee of the caller's pool op stream -------------------------
@@ -357,29 +384,38 @@ class GpuMarsPolicy(_PolicyBase):
         if self._kv_enabled and self.kv is None:
             self._kv_attach(pool, gpu)
         self.kv_flush()
+        self._flush()
         if self._ranks_dirty:
             self._sync_ranks()
-        rows = np.fromiter((self._row[c.session_id] for c in ready), dtype=np.int64,
-                           count=len(ready))
-        ready_set = set(rows.tolist())
-        gone = sorted(self._dev_ready - ready_set)
-        n = len(ready)
-        cols = {
-            "phase": np.fromiter((_phase_code(c.phase) for c in ready), np.uint8, n),
-            "flags": np.full(n, F_ACTIVE, np.uint8),
-            "kv": np.fromiter((c.kv_tokens for c in ready), np.int32, n),
-            "context": np.fromiter((c.context_tokens for c in ready), np.int32, n),
-            "rem_decode": np.fromiter((c.remaining_decode for c in ready), np.int32, n),
-            "ready_since": np.fromiter((c.ready_since for c in ready), np.float64, n),
-            "arrival": np.fromiter((c.arrival_time for c in ready), np.float64, n),
-        }
-        cols.update(self._extra_cols(ready, n))
+        rid = self._row
+        rows = np.fromiter((rid[c.session_id] for c in ready), dtype=np.int64, count=len(ready))
+        # re-upload only the ready rows whose Call can have changed: new in the
+        # ready list, planned or evicted by the last plan, touched by a hook
+        # (the sim changes a Call's phase / kv / context / decode / ready_since
+        # only through those, engine.py:320-330, :459-514, sim.py:168-279)
+        sel = np.nonzero(~self._in_ready[rows] | self._dirty[rows])[0]
+        self._in_ready[self._ready_rows] = False
+        self._in_ready[rows] = True
+        gone = self._ready_rows[~self._in_ready[self._ready_rows]]
+        self._ready_rows = rows
+        n = len(sel)
         if n:
-            eng.upsert(cols, rows=rows)
-        if gone:
+            calls = [ready[i] for i in sel.tolist()]
+            cols = {
+                "phase": np.fromiter((_phase_code(c.phase) for c in calls), np.uint8, n),
+                "flags": np.full(n, F_ACTIVE, np.uint8),
+                "kv": np.fromiter((c.kv_tokens for c in calls), np.int32, n),
+                "context": np.fromiter((c.context_tokens for c in calls), np.int32, n),
+                "rem_decode": np.fromiter((c.remaining_decode for c in calls), np.int32, n),
+                "ready_since": np.fromiter((c.ready_since for c in calls), np.float64, n),
+                "arrival": np.fromiter((c.arrival_time for c in calls), np.float64, n),
+            }
+            cols.update(self._extra_cols(calls, n))
+            eng.upsert(cols, rows=rows[sel])
+        if len(gone):
             eng.upsert({"phase": np.array([_phase_code(self.calls[self._sid[r]].phase)
-                                           for r in gone], np.uint8)},
-                       rows=np.array(gone, np.int64))
+                                           for r in gone.tolist()], np.uint8)}, rows=gone)
+        self._dirty[:] = False
         s = N.MarsScalars()
         s.total_blocks = pool.total_blocks
         s.free_blocks = pool.free_blocks
@@ -395,7 +431,10 @@ class GpuMarsPolicy(_PolicyBase):
         res = eng.step(si)
         if res.status:
             raise RuntimeError(f"device step status {res.status}")
-        self._dev_ready = ready_set
+        # the plan's rows change in step_gpu / the evictor before the next tick
+        self._dirty[res.decode_rows] = True
+        self._dirty[res.prefill_rows] = True
+        self._dirty[res.journal_row] = True
         sid = self._sid
         plan = TickPlan()
         self.last_window = [sid[r] for r in res.window_rows]
@@ -512,8 +551,8 @@ class GpuProgramPriorityPolicy(_GpuComparisonPolicy):
 
     name = "program_priority"
 
-    def _extra_cols(self, ready: Sequence, n: int) -> dict:
-        return {"served": np.fromiter((c.served_tokens for c in ready), np.int64, n)}
+    def _extra_cols(self, calls: Sequence, n: int) -> dict:
+        return {"served": np.fromiter((c.served_tokens for c in calls), np.int64, n)}
 
 
 class GpuTtlPolicy(_GpuComparisonPolicy):
