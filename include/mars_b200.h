@@ -246,6 +246,23 @@ int mars_read_rows(mars_ctx* ctx, int64_t n, const int64_t* rows, mars_cols* out
 int mars_set_queue(mars_ctx* ctx, int64_t n, const uint32_t* rows, const int32_t* req_blocks,
                    const uint8_t* is_long);
 int mars_get_queue(mars_ctx* ctx, int64_t cap, uint32_t* rows, int64_t* n);          /* sync */
+/* arrivals appended to the end of the device admission list (sim.py:289-301
+ * + control.py:76-93 make_queue_entry), without a host round trip of the list */
+int mars_queue_append(mars_ctx* ctx, int64_t n, const uint32_t* rows, const int32_t* req,
+                      const uint8_t* lng);
+/* The drop-in's per-session MLFQ hooks, batched (rows distinct): on_admit
+ * (baselines.py:351-360, initial_level scheduler.py:87-97 of the first
+ * round's new prefill) and on_service (baselines.py:362-367, charge_service
+ * scheduler.py:100-108) from the device state, or -- pre_charge non-null --
+ * from the given (served << 8) | level (undoing a predicted charge).
+ * MARS_ERR_CONTRACT for a prefill < 1 or negative tokens. */
+int mars_on_admit(mars_ctx* ctx, int64_t n, const int64_t* rows, const int32_t* r0_prefill,
+                  const double* now);
+/* MarsPolicy.expired_pins (baselines.py:396-399): the pinned rows whose
+ * deadline is before now, in no particular order (*n = how many) */
+int mars_expired_pins(mars_ctx* ctx, double now, int64_t cap, uint32_t* rows, int64_t* n);
+int mars_on_service(mars_ctx* ctx, int64_t n, const int64_t* rows, const int64_t* tokens,
+                    const double* now, const int64_t* pre_charge);
 int mars_set_scalars(mars_ctx* ctx, const mars_scalars* s);
 int mars_get_scalars(mars_ctx* ctx, mars_scalars* s);                               /* sync */
 

@@ -132,6 +132,10 @@ _SIGS = {
     "mars_read_rows": (i32, [C.c_void_p, i64, C.c_void_p, P(MarsCols)]),
     "mars_set_queue": (i32, [C.c_void_p, i64, C.c_void_p, C.c_void_p, C.c_void_p]),
     "mars_get_queue": (i32, [C.c_void_p, i64, C.c_void_p, P(i64)]),
+    "mars_queue_append": (i32, [C.c_void_p, i64, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "mars_on_admit": (i32, [C.c_void_p, i64, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "mars_expired_pins": (i32, [C.c_void_p, f64, i64, C.c_void_p, P(i64)]),
+    "mars_on_service": (i32, [C.c_void_p, i64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "mars_set_scalars": (i32, [C.c_void_p, P(MarsScalars)]),
     "mars_get_scalars": (i32, [C.c_void_p, P(MarsScalars)]),
     "mars_step": (i32, [C.c_void_p, P(MarsStepIn), P(MarsStepOut)]),

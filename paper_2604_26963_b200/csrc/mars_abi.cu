@@ -57,6 +57,7 @@ struct mars_ctx {
   // device staging for row scatter/gather
   unsigned char* d_stage = nullptr;
   i64* d_rows = nullptr;
+  int* d_hook_st = nullptr;          // contract bits of the drop-in hook kernels
   // checkpoint
   bool have_ckpt = false;
   void* ck_q[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -410,6 +411,8 @@ int mars_create(const mars_config* hcfg, int device, int64_t max_rows, int64_t m
   ALLOC(b.j_n, b.j_cap * 4);
   ALLOC(ctx->d_stage, R * 8);
   ALLOC(ctx->d_rows, R * 8);
+  ALLOC(ctx->d_hook_st, 16);
+  CK(cudaMemset(ctx->d_hook_st, 0, 16));
   // host pinned
   CK(cudaMallocHost((void**)&ctx->h_in, sizeof(mars_step_in)));
   CK(cudaMallocHost((void**)&ctx->h_work, sizeof(Work)));
@@ -489,6 +492,7 @@ int mars_destroy(mars_ctx* ctx) {
   cudaFree(ctx->d_stage);
   cudaFree(ctx->d_resume);
   cudaFree(ctx->d_rows);
+  cudaFree(ctx->d_hook_st);
   for (auto& cs : ctx->cols) cudaFree(cs.ckpt);
   for (void* p : ctx->ck_q) cudaFree(p);
   cudaFree(ctx->ck_sc);
@@ -623,6 +627,111 @@ int mars_set_queue(mars_ctx* ctx, int64_t n, const uint32_t* rows, const int32_t
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->q_upper = n;
   ctx->q_maxreq = mx;
+  return MARS_OK;
+}
+
+int mars_queue_append(mars_ctx* ctx, int64_t n, const uint32_t* rows, const int32_t* req,
+                      const uint8_t* lng) {
+  if (!ctx || n < 0 || (n > 0 && (!rows || !req || !lng))) return MARS_ERR_ARG;
+  if (n == 0) return MARS_OK;
+  if (ctx->q_upper + n > ctx->max_queue)
+    return fail(ctx, MARS_ERR_CAPACITY, "queue %lld + %lld > %lld", (long long)ctx->q_upper,
+                (long long)n, (long long)ctx->max_queue);
+  if (n * 9 > ctx->alloc_rows * 8) return fail(ctx, MARS_ERR_CAPACITY, "append batch too large");
+  int mx = ctx->q_maxreq;
+  for (int64_t i = 0; i < n; ++i) {
+    if (req[i] < 1) return fail(ctx, MARS_ERR_CONTRACT, "queue entry needs req_blocks >= 1");
+    if (req[i] > mx) mx = req[i];
+    if ((i64)rows[i] >= ctx->max_rows) return fail(ctx, MARS_ERR_CAPACITY, "row out of range");
+  }
+  CK(cudaSetDevice(ctx->device));
+  u8* st = ctx->d_stage;
+  CK(cudaMemcpyAsync(st, rows, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(st + n * 4, req, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(st + n * 8, lng, n, cudaMemcpyHostToDevice, ctx->stream));
+  int rc = mars_enqueue_queue_append(ctx->stream, ctx->queue, ctx->qsel, ctx->sc, n, (const u32*)st,
+                                     (const i32*)(st + n * 4), st + n * 8);
+  if (rc) return fail(ctx, MARS_ERR_CUDA, "queue append: %s", cudaGetErrorString((cudaError_t)rc));
+  CK(cudaStreamSynchronize(ctx->stream));  // (the staging buffer is reused next)
+  ctx->q_upper += n;
+  ctx->q_maxreq = mx;
+  return MARS_OK;
+}
+
+// the drop-in's batched MLFQ hooks (k_admit_rows / k_service_rows); the
+// work area's status carries a contract break back
+static int hook_rows_check(mars_ctx* ctx, int64_t n, const int64_t* rows) {
+  if (!ctx || n < 0 || (n > 0 && !rows)) return MARS_ERR_ARG;
+  for (int64_t i = 0; i < n; ++i)
+    if (rows[i] < 0 || rows[i] >= ctx->max_rows) return fail(ctx, MARS_ERR_CAPACITY, "row out of range");
+  if (n * 24 > ctx->alloc_rows * 8) return fail(ctx, MARS_ERR_CAPACITY, "hook batch too large");
+  return MARS_OK;
+}
+
+static int hook_status(mars_ctx* ctx) {
+  int32_t st = 0;
+  CK(cudaMemcpyAsync(&st, ctx->d_hook_st, sizeof st, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemsetAsync(ctx->d_hook_st, 0, sizeof(int32_t), ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (st & ST_BAD_INPUT) return fail(ctx, MARS_ERR_CONTRACT, "hook input violates the contract");
+  return MARS_OK;
+}
+
+int mars_on_admit(mars_ctx* ctx, int64_t n, const int64_t* rows, const int32_t* r0_prefill,
+                  const double* now) {
+  int rc = hook_rows_check(ctx, n, rows);
+  if (rc || n == 0) return rc;
+  CK(cudaSetDevice(ctx->device));
+  u8* st = ctx->d_stage;
+  CK(cudaMemcpyAsync(st, rows, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(st + n * 8, now, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(st + n * 16, r0_prefill, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+  rc = mars_enqueue_admit_rows(ctx->stream, ctx->tab, ctx->cfg, n, (const i64*)st,
+                               (const i32*)(st + n * 16), (const double*)(st + n * 8),
+                               ctx->d_hook_st);
+  if (rc) return fail(ctx, MARS_ERR_CUDA, "admit rows: %s", cudaGetErrorString((cudaError_t)rc));
+  return hook_status(ctx);
+}
+
+int mars_on_service(mars_ctx* ctx, int64_t n, const int64_t* rows, const int64_t* tokens,
+                    const double* now, const int64_t* pre_charge) {
+  int rc = hook_rows_check(ctx, n, rows);
+  if (rc || n == 0) return rc;
+  CK(cudaSetDevice(ctx->device));
+  u8* st = ctx->d_stage;
+  CK(cudaMemcpyAsync(st, rows, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(st + n * 8, tokens, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(st + n * 16, now, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  const i64* pre = nullptr;
+  if (pre_charge) {
+    // (the rows' staging slot is reused: pre-charge states go to the upsert index buffer)
+    CK(cudaMemcpyAsync(ctx->d_rows, pre_charge, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+    pre = ctx->d_rows;
+  }
+  rc = mars_enqueue_service_rows(ctx->stream, ctx->tab, ctx->cfg, n, (const i64*)st,
+                                 (const i64*)(st + n * 8), (const double*)(st + n * 16), pre,
+                                 ctx->d_hook_st);
+  if (rc) return fail(ctx, MARS_ERR_CUDA, "service rows: %s", cudaGetErrorString((cudaError_t)rc));
+  return hook_status(ctx);
+}
+
+int mars_expired_pins(mars_ctx* ctx, double now, int64_t cap, uint32_t* rows, int64_t* n) {
+  if (!ctx || !n || cap < 0 || (cap > 0 && !rows)) return MARS_ERR_ARG;
+  CK(cudaSetDevice(ctx->device));
+  u8* st = ctx->d_stage;  // [count][rows...]
+  const i64 room = std::min<i64>(cap, (ctx->alloc_rows * 8 - 16) / 4);
+  int rc = mars_enqueue_expired_rows(ctx->stream, ctx->tab, ctx->n_rows, now, (u32*)(st + 16),
+                                     room, (int*)st, ctx->num_sms * 4);
+  if (rc) return fail(ctx, MARS_ERR_CUDA, "expired rows: %s", cudaGetErrorString((cudaError_t)rc));
+  int cnt = 0;
+  CK(cudaMemcpyAsync(&cnt, st, sizeof cnt, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  *n = cnt;
+  if (cnt > room) return fail(ctx, MARS_ERR_CAPACITY, "%d expired pins > %lld", cnt, (long long)room);
+  if (cnt > 0) {
+    CK(cudaMemcpyAsync(rows, st + 16, (size_t)cnt * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
   return MARS_OK;
 }
 

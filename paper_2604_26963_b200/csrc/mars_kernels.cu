@@ -4040,6 +4040,108 @@ __global__ void k_gather(u8* dst, const u8* src, const i64* rows, i64 n, int esz
   }
 }
 
+// arrivals appended to the admission list on the device (sim.py:289-301: the
+// queue keeps its packed order, new entries go to the end); one CTA
+__global__ void __launch_bounds__(1024) k_queue_append(Queue Q, const i32* qsel_p, mars_scalars* sc,
+                                                       i64 n, const u32* rows, const i32* req,
+                                                       const u8* lng) {
+  __shared__ i64 s_len;
+  if (threadIdx.x == 0) s_len = sc->queue_len;
+  __syncthreads();
+  const int sel = *qsel_p;
+  u32* qr = PICK2(Q.row, sel);
+  i32* qq = PICK2(Q.req, sel);
+  u8* ql = PICK2(Q.lng, sel);
+  for (i64 i = threadIdx.x; i < n; i += blockDim.x) {
+    qr[s_len + i] = rows[i];
+    qq[s_len + i] = req[i];
+    ql[s_len + i] = lng[i];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) sc->queue_len = s_len + n;
+}
+
+int mars_enqueue_queue_append(cudaStream_t s, const Queue& Q, const i32* qsel, mars_scalars* sc,
+                              i64 n, const u32* rows, const i32* req, const u8* lng) {
+  k_queue_append<<<1, 1024, 0, s>>>(Q, qsel, sc, n, rows, req, lng);
+  return (int)cudaGetLastError();
+}
+
+// The drop-in's per-session MLFQ hooks on the device, batched per tick:
+// MarsPolicy.on_admit (baselines.py:351-360: level = initial_level of the
+// first round's new prefill, scheduler.py:87-97; no promotions, nothing
+// served, wait_since = now, the session active) and on_service
+// (baselines.py:362-367 -> charge_service scheduler.py:100-108, wait_since =
+// tick end) from the device state, or from a given state (undoing the step's
+// predicted charge).  Rows are distinct within a batch.
+__global__ void k_admit_rows(Tab t, Cfg c, i64 n, const i64* rows, const i32* r0p,
+                             const double* now, int* st) {
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+    const i64 r = rows[i];
+    if (r0p[i] < 1) {  // initial_level's ContractViolation
+      atomicOr(st, ST_BAD_INPUT);
+      continue;
+    }
+    t.level[r] = (u8)initial_level(c, r0p[i]);
+    t.promos[r] = 0;
+    t.served[r] = 0;
+    t.ws[r] = now[i];
+    t.flags[r] = (u8)(t.flags[r] | MARS_F_ACTIVE);
+  }
+}
+
+__global__ void k_service_rows(Tab t, Cfg c, i64 n, const i64* rows, const i64* tokens,
+                               const double* now, const i64* pre /* (served << 8) | level, or null */,
+                               int* st) {
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+    const i64 r = rows[i];
+    if (tokens[i] < 0) {  // charge_service's ContractViolation
+      atomicOr(st, ST_BAD_INPUT);
+      continue;
+    }
+    u32 lv = pre ? (u32)(pre[i] & 0xff) : (u32)t.level[r];
+    i64 served = (pre ? (pre[i] >> 8) : t.served[r]) + tokens[i];
+    if (served > c.quotas[lv] && (int)lv < c.num_levels - 1) {
+      lv += 1;
+      served = 0;
+    }
+    t.level[r] = (u8)lv;
+    t.served[r] = served;
+    t.ws[r] = now[i];
+  }
+}
+
+// MarsPolicy.expired_pins (baselines.py:396-399): the pinned rows whose
+// deadline passed (any order; the caller sorts by session id); *cnt counts
+// every match, rows past `cap` are not stored
+__global__ void k_expired_rows(Tab t, i64 n_rows, double now, u32* out, i64 cap, int* cnt) {
+  for (i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x; r < n_rows; r += (i64)gridDim.x * blockDim.x) {
+    if ((t.flags[r] & MARS_F_PINNED) && t.dl[r] < now) {
+      const int k = atomicAdd(cnt, 1);
+      if (k < cap) out[k] = (u32)r;
+    }
+  }
+}
+
+int mars_enqueue_expired_rows(cudaStream_t s, const Tab& t, i64 n_rows, double now, u32* out,
+                              i64 cap, int* cnt, int grid) {
+  cudaMemsetAsync(cnt, 0, sizeof(int), s);
+  k_expired_rows<<<grid, 256, 0, s>>>(t, n_rows, now, out, cap, cnt);
+  return (int)cudaGetLastError();
+}
+
+int mars_enqueue_admit_rows(cudaStream_t s, const Tab& t, const Cfg& c, i64 n, const i64* rows,
+                            const i32* r0p, const double* now, int* st) {
+  k_admit_rows<<<(int)((n + 255) / 256), 256, 0, s>>>(t, c, n, rows, r0p, now, st);
+  return (int)cudaGetLastError();
+}
+
+int mars_enqueue_service_rows(cudaStream_t s, const Tab& t, const Cfg& c, i64 n, const i64* rows,
+                              const i64* tokens, const double* now, const i64* pre, int* st) {
+  k_service_rows<<<(int)((n + 255) / 256), 256, 0, s>>>(t, c, n, rows, tokens, now, pre, st);
+  return (int)cudaGetLastError();
+}
+
 int mars_enqueue_scatter(cudaStream_t s, void* dst, const void* src, const i64* rows, i64 n,
                          int esz) {
   if (n <= 0) return 0;
@@ -4342,7 +4444,9 @@ int mars_kernels_preload() {
                        (const void*)k_global_control, (const void*)k_lsd_coop,
                        (const void*)k_pack, (const void*)k_resume,
                        (const void*)k_retention_batch, (const void*)k_scan,
-                       (const void*)k_scatter, (const void*)k_walk, (const void*)k_work_init};
+                       (const void*)k_scatter, (const void*)k_walk, (const void*)k_work_init,
+                       (const void*)k_queue_append, (const void*)k_admit_rows,
+                       (const void*)k_service_rows, (const void*)k_expired_rows};
   for (const void* f : fns) {
     cudaError_t e = cudaFuncGetAttributes(&fa, f);
     if (e != cudaSuccess) return (int)e;

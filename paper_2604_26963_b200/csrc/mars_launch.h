@@ -38,6 +38,14 @@ struct LaunchArgs {
 
 int mars_kernels_init();
 int mars_kernels_preload();
+int mars_enqueue_expired_rows(cudaStream_t s, const Tab& t, i64 n_rows, double now, u32* out,
+                              i64 cap, int* cnt, int grid);
+int mars_enqueue_admit_rows(cudaStream_t s, const Tab& t, const Cfg& c, i64 n, const i64* rows,
+                            const i32* r0p, const double* now, int* st);
+int mars_enqueue_service_rows(cudaStream_t s, const Tab& t, const Cfg& c, i64 n, const i64* rows,
+                              const i64* tokens, const double* now, const i64* pre, int* st);
+int mars_enqueue_queue_append(cudaStream_t s, const Queue& Q, const i32* qsel, mars_scalars* sc,
+                              i64 n, const u32* rows, const i32* req, const u8* lng);
 int mars_enqueue_step(const LaunchArgs* a);
 int mars_enqueue_retention(const Cfg& c, cudaStream_t s, i64 n, const i32* ctx, const i32* kv,
                            i64 total, double usage, double ema, double now, u8* pin, double* bb,

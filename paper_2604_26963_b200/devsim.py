@@ -359,13 +359,6 @@ class _HostTier:
             st["pool_blocks_bad"] = pool_bad
 
 
-def _initial_level(tokens: int, cfg) -> int:  # scheduler.py:87-97
-    for i in range(cfg.num_levels):
-        if tokens <= cfg.level_bounds[i]:
-            return i
-    return cfg.num_levels - 1
-
-
 def _run(eng: MarsEngine, cfg, order, total_blocks: int, slots: int, max_ticks: int,
          admission: bool, policy: str, log: Optional[EventLog], decides: bool,
          tier: Optional[_HostTier] = None):
@@ -445,17 +438,17 @@ def _run(eng: MarsEngine, cfg, order, total_blocks: int, slots: int, max_ticks: 
                        rows=rows)
             queue += new
             # appended to the device list, whose residual keeps the packed order
-            q = np.concatenate([np.asarray(eng.get_queue(), np.int64), rows])
-            eng.set_queue(q.astype(np.uint32), req[q].astype(np.int32), long_[q])
+            eng.queue_append(rows, req[rows], long_[rows])
         elif new:
             # admit() at arrival (sim.py:148-166): submit_round + on_admit
             rows = np.array(new, np.int64)
             k = len(new)
-            lv = [_initial_level(int(r0p[r]), cfg) if policy == "mars" else 0 for r in new]
             eng.upsert({"phase": np.full(k, 1, np.uint8), "flags": np.ones(k, np.uint8),
                         "context": r0p[rows], "rem_decode": dec0[rows],
                         "ready_since": np.full(k, now), "wait_since": np.full(k, now),
-                        "level": np.array(lv, np.uint8)}, rows=rows)
+                        "level": np.zeros(k, np.uint8)}, rows=rows)
+            if policy == "mars":  # on_admit: initial_level on the device
+                eng.on_admit(rows, r0p[rows], now)
             cnt["admitted"] += k
             active += k
             if log is not None:

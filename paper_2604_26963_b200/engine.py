@@ -224,6 +224,24 @@ class MarsEngine:
                                             q.ctypes.data_as(C.c_void_p),
                                             lg.ctypes.data_as(C.c_void_p)))
 
+    def queue_append(self, rows: np.ndarray, req: np.ndarray, is_long: np.ndarray) -> None:
+        """Arrivals to the end of the device admission list."""
+        r = np.ascontiguousarray(rows, np.uint32)
+        q = np.ascontiguousarray(req, np.int32)
+        lg = np.ascontiguousarray(is_long, np.uint8)
+        self._check(self.lib.mars_queue_append(self.ctx, len(r), r.ctypes.data_as(C.c_void_p),
+                                               q.ctypes.data_as(C.c_void_p),
+                                               lg.ctypes.data_as(C.c_void_p)))
+
+    def on_admit(self, rows, r0_prefill, now) -> None:
+        """MarsPolicy.on_admit for a batch of rows, on the device (mars_on_admit)."""
+        r = np.ascontiguousarray(rows, np.int64)
+        p = np.ascontiguousarray(r0_prefill, np.int32)
+        t = np.ascontiguousarray(np.broadcast_to(np.asarray(now, np.float64), r.shape))
+        self._check(self.lib.mars_on_admit(self.ctx, len(r), r.ctypes.data_as(C.c_void_p),
+                                           p.ctypes.data_as(C.c_void_p),
+                                           t.ctypes.data_as(C.c_void_p)))
+
     def get_queue(self) -> np.ndarray:
         n = C.c_int64()
         self._check(self.lib.mars_get_queue(self.ctx, 0, None, C.byref(n)))

@@ -18,6 +18,7 @@ values (engine.py:503-512), and handed back when the sim asks for them.
 
 from __future__ import annotations
 
+import ctypes as C
 import math
 from typing import Dict, List, Optional, Sequence, Tuple
 
@@ -136,12 +137,14 @@ class GpuMarsPolicy(_PolicyBase):
     re-uploaded."""
 
     # hook kind -> the columns it sets, in the order hooks fire between ticks
-    _PENDING = (("service", ("level", "served", "wait_since")),
+    # (kinds with no columns run a device hook kernel: mars_on_service /
+    # mars_on_admit, the reference's MLFQ arithmetic never restated on the host)
+    _PENDING = (("service", ()), ("service_pre", ()),
                 ("pin", ("flags", "deadline", "pinned_blocks", "plevel")),
                 ("register", ("phase", "flags", "rank", "arrival")),
                 ("resume", ("wait_since",)),
                 ("evicted", ("flags", "kv")),
-                ("admit", ("level", "promos", "served", "wait_since", "flags")),
+                ("admit", ()),
                 ("admit_base", ("level", "promos", "served", "flags")))
 
     name = "mars"
@@ -179,9 +182,6 @@ class GpuMarsPolicy(_PolicyBase):
         self._service: Dict[str, tuple] = {}
         self._replaying = False
         self.last_window: List[str] = []
-        b = getattr(mlfq, "level_boundaries_tokens", (4_000, 32_000, 128_000, math.inf))
-        self._bounds = tuple(b)
-        self._levels_n = getattr(mlfq, "num_levels", 4)
         self._tool_prior = getattr(pressure, "initial_tool_estimate_s", 5.0)
         self._pend: Dict[str, Dict[int, tuple]] = {k: {} for k, _ in self._PENDING}
         self._in_ready = np.zeros(self._max, bool)   # rows of the last uploaded ready list
@@ -247,9 +247,23 @@ class GpuMarsPolicy(_PolicyBase):
             eng = eng or self._engine()
             rows = np.fromiter(d.keys(), np.int64, len(d))
             vals = list(zip(*d.values()))
-            eng.upsert({c: np.asarray(v, dtype=COLUMNS[c]) for c, v in zip(cols, vals)},
-                       rows=rows)
             d.clear()
+            P = C.c_void_p
+            if kind == "admit":       # (first round's new prefill, now)
+                r0 = np.asarray(vals[0], np.int32)
+                now = np.asarray(vals[1], np.float64)
+                eng._check(eng.lib.mars_on_admit(eng.ctx, len(rows), rows.ctypes.data_as(P),
+                                                 r0.ctypes.data_as(P), now.ctypes.data_as(P)))
+            elif kind in ("service", "service_pre"):   # (tokens, now[, pre-charge state])
+                tok = np.asarray(vals[0], np.int64)
+                now = np.asarray(vals[1], np.float64)
+                pre = np.asarray(vals[2], np.int64) if kind == "service_pre" else None
+                eng._check(eng.lib.mars_on_service(
+                    eng.ctx, len(rows), rows.ctypes.data_as(P), tok.ctypes.data_as(P),
+                    now.ctypes.data_as(P), pre.ctypes.data_as(P) if pre is not None else None))
+            else:
+                eng.upsert({c: np.asarray(v, dtype=COLUMNS[c]) for c, v in zip(cols, vals)},
+                           rows=rows)
 
     def _sync_ranks(self) -> None:
         order = sorted(range(len(self._sid)), key=self._sid.__getitem__)
@@ -258,20 +272,13 @@ class GpuMarsPolicy(_PolicyBase):
         self._engine().upsert({"rank": rank}, rows=np.arange(len(order)))
         self._ranks_dirty = False
 
-    def _initial_level(self, tokens: int) -> int:  # scheduler.py:87-97
-        if tokens < 1:
-            raise ContractViolation("context_tokens must be >= 1")
-        for i, b in enumerate(self._bounds):
-            if tokens <= b:
-                return i
-        return self._levels_n - 1
-
     def on_admit(self, call, now: float) -> None:
         sid = call.session_id
-        lv = self._initial_level(call.rounds[0].new_prefill_tokens)
-        r = self._row[sid]
-        self._queue("admit", r, (lv, 0, 0, now, F_ACTIVE))
-        self._levels[sid] = lv
+        tokens = call.rounds[0].new_prefill_tokens
+        if tokens < 1:  # initial_level's precondition (scheduler.py:93-94)
+            raise ContractViolation("context_tokens must be >= 1")
+        # the level itself: initial_level on the device at the next upload
+        self._queue("admit", self._row[sid], (tokens, now))
         self._admitted.add(sid)
 
     def on_resume(self, call, now: float) -> None:
@@ -285,22 +292,15 @@ class GpuMarsPolicy(_PolicyBase):
         exp = self._service.pop(session_id, None)
         if exp is not None and exp[:2] == (tokens, now):
             return  # already charged by the device step at tick end
-        if tokens < 0:
+        if tokens < 0:  # charge_service's precondition (scheduler.py:102-103)
             raise ContractViolation("cannot charge negative service")
         r = self._row[session_id]
         if exp is not None:
             # the device charged its prediction: charge this amount from the
-            # state before it instead (scheduler.py:100-108)
-            lv, served = exp[2], exp[3] + int(tokens)
-        else:  # a charge the plan did not predict: apply it to the device row
-            self._flush()
-            st = self._engine().read(["level", "served"], rows=np.array([r]))
-            lv, served = int(st["level"][0]), int(st["served"][0]) + int(tokens)
-        q = list(getattr(self.mlfq, "level_quotas_tokens", (2_000, 8_000, 32_000, math.inf)))
-        if served > q[lv] and lv < self._levels_n - 1:
-            lv, served = lv + 1, 0
-        self._queue("service", r, (lv, served, now))
-        self._levels[session_id] = lv
+            # state before it instead (charge_service on the device)
+            self._queue("service_pre", r, (int(tokens), now, (exp[3] << 8) | exp[2]))
+        else:  # a charge the plan did not predict: from the device row's state
+            self._queue("service", r, (int(tokens), now))
 
     def level_of(self, call) -> int:
         """The MLFQ level now (baselines.py:370-372): the device row, which
@@ -337,7 +337,19 @@ class GpuMarsPolicy(_PolicyBase):
         self._pins[sid] = decision.retention_deadline
 
     def expired_pins(self, now: float) -> List[str]:
-        return sorted(sid for sid, dl in self._pins.items() if dl < now)
+        """The pins whose deadline passed, in session-id order (baselines.py:
+        396-399), found on the device from the table's pin flags and
+        deadlines (the pending hook writes go up first)."""
+        if not self._pins:
+            return []
+        self._flush()
+        eng = self._engine()
+        out = np.zeros(len(self._pins), np.uint32)
+        n = C.c_int64()
+        eng._check(eng.lib.mars_expired_pins(eng.ctx, float(now), len(out),
+                                             out.ctypes.data_as(C.c_void_p), C.byref(n)))
+        sid = self._sid
+        return sorted(sid[r] for r in out[:n.value].tolist())
 
     def on_evicted(self, session_id: str) -> None:
         if self._pins.pop(session_id, None) is None:
