@@ -1624,7 +1624,11 @@ __device__ int lsd_grid_sort(Lsd L, LsdView v, LsdArgs a, int npass, u32 (*wc)[2
   const i32* raw = a.raw;
   const bool asc = a.asc;
   const i32 mr = a.mr;
-  int cur = a.cur;
+  // the current buffer is block-uniform: kept in shared memory (a register
+  // for it across the passes' grid barriers spilled to local memory)
+  __shared__ int s_cur;
+  if (tid == 0) s_cur = a.cur;
+  __syncthreads();
   for (int pass = 0; pass < npass; ++pass) {
     const int shift = 8 * pass;
     if (pass > 0 && (maxkey >> shift) == 0) {
@@ -1633,6 +1637,7 @@ __device__ int lsd_grid_sort(Lsd L, LsdView v, LsdArgs a, int npass, u32 (*wc)[2
     }
     // the queue's first pass reads req[] straight from the admission list
     const bool rawp = raw != nullptr && pass == 0;
+    const int cur = s_cur;
     const u64* kin = PICK2(L.k, cur);
     const u32* vin = PICK2(L.v, cur);
     u64* kout = PICK2(L.k, 1 - cur);
@@ -1811,11 +1816,14 @@ __device__ int lsd_grid_sort(Lsd L, LsdView v, LsdArgs a, int npass, u32 (*wc)[2
       v.skip[pass] = 0;
       v.in[pass] = cur;
     }
-    cur = 1 - cur;
+    __syncthreads();  // (every thread has read s_cur)
+    if (tid == 0) s_cur = 1 - cur;
+    __syncthreads();
     if (pass == 0) PTIME(9);
     grid.sync();  // the next pass reads this pass' output and rewrites L.cnt
   }
   PTIME(10);
+  const int cur = s_cur;
   if (me == 0 && tid == 0) *v.cur = cur;
   return cur;
 }
@@ -2324,11 +2332,14 @@ __global__ void __launch_bounds__(1024, 1) k_pack(Cfg c, Work* w, Queue Q, Lsd L
   a.asc = mode == PACK_ASC;
   a.mr = (i32)keyc;
   a.cur = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // (before the sort: nothing live across it)
+    w->pk_mode = mode;
+    w->pk_max_req = (i32)keyc;  // the descending keys' constant
+  }
   const int cur = lsd_grid_sort<true>(L, lsd_view(w, 0), a, npass, (u32(*)[256])smem);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    w->pk_mode = mode;
     w->pk_cur = cur;
-    w->pk_max_req = (i32)keyc;  // the descending keys' constant
+    __threadfence();
     w->pk_done = 1;
   }
   PTIME(34);

@@ -38,9 +38,9 @@ def test_dropin_event_log_is_byte_identical(key):
     assert out.counters == SIM[key]["counters"]
 
 
-# demo64/program_priority (173K records) replays ~10x longer than the rest;
-# its CPU oracle replay is pinned in tests/test_oracle_golden.py
-BASE_KEYS = sorted(k for k in SIM_BASE if k != "demo64/program_priority")
+# every frozen comparison-policy run, demo64/program_priority's 173K-record
+# log included
+BASE_KEYS = sorted(SIM_BASE)
 
 
 @pytest.mark.parametrize("key", BASE_KEYS)
