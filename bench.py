@@ -850,6 +850,36 @@ def main():
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_s = float(te.item())
 
+    # e2e_resident: the table stays in HBM between steps (as a serving
+    # scheduler keeps it); every step uploads from pinned host memory the
+    # rows that changed since the previous one -- modelled as 1 % of the
+    # sessions, every column the step reads -- then runs the step and fetches
+    # the plan / journal / decisions, all through the public API
+    rng = np.random.default_rng(5)
+    dn = max(1, snap.n // 100)
+    drows = torch.from_numpy(np.sort(rng.choice(snap.n, dn, replace=False)).astype(np.int64)
+                             ).pin_memory().numpy()
+    dcols = {k: torch.from_numpy(np.ascontiguousarray(v[drows])).pin_memory().numpy()
+             for k, v in pinned.items()}
+    dh2d = sum(v.nbytes for v in dcols.values()) + drows.nbytes
+    res_t = []
+    for i in range(a.e2e_steps + e2e_warm):
+        eng.restore()
+        eng.flush_l2(flush)
+        barrier()
+        t0 = time.perf_counter()
+        eng.upsert(dcols, rows=drows)
+        enqueue_step()
+        r = eng.fetch()
+        t1 = time.perf_counter()
+        if i >= e2e_warm:
+            res_t.append(t1 - t0)
+    res_s = statistics.median(res_t)
+    tr_ = torch.tensor([res_s], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(tr_, op=dist.ReduceOp.MAX)
+    res_s = float(tr_.item())
+
     adv = advance_run(eng, snap, stream, flush, a.advance_ticks) if (
         world == 1 and a.advance_ticks > 0) else None
 
@@ -878,7 +908,13 @@ def main():
         "e2e": {"value": total_sessions / e2e_s, "unit": "sessions/s",
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "ms_per_step": e2e_s * 1e3,
-                "upload_ms": statistics.median(e2e_up) * 1e3},
+                "upload_ms": statistics.median(e2e_up) * 1e3,
+                "inputs": "every column the step reads, all rows, uploaded each step"},
+        "e2e_resident": {"value": total_sessions / res_s, "unit": "sessions/s",
+                         "h2d_bytes_per_step": int(dh2d), "d2h_bytes_per_step": int(d2h),
+                         "ms_per_step": res_s * 1e3,
+                         "inputs": "table resident in HBM; 1 % of the rows (every column the "
+                                   "step reads) uploaded each step"},
         "gpu_launches": launches,
         "advance": adv,
         "kernel_ms_median": kernel_ms,

@@ -341,8 +341,9 @@ int mars_create(const mars_config* hcfg, int device, int64_t max_rows, int64_t m
   CK(cudaMemset(ctx->qsel, 0, sizeof(i32)));
   Bufs& b = ctx->bufs;
   memset(&b, 0, sizeof b);
-  ALLOC(b.tile_cnt, (R / 4096 + 2) * 4);
-  ALLOC(b.tile_kv, (R / 4096 + 2) * 3 * 8);
+  // one entry per k_scan CTA (<= the scan's block size, mars_kernels.cu)
+  ALLOC(b.tile_cnt, 1024 * 4);
+  ALLOC(b.tile_kv, 1024 * 3 * 8);
   ALLOC(b.row_dig, R * 4);
   ALLOC(b.cand_row, R * 4);
   ALLOC(b.exp_row, R * 4);

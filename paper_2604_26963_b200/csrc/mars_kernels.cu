@@ -89,11 +89,11 @@ __device__ __forceinline__ T warp_sum(T v) {
   return v;
 }
 
-// block-wide exclusive scan of one i64 per thread (blockDim.x == 1024, every
-// thread calls it); *total = the block's sum
+// block-wide exclusive scan of one i64 per thread (blockDim.x a multiple of
+// 32, every thread calls it); *total = the block's sum
 __device__ __forceinline__ long long block_excl_scan_i64(long long v, long long* total) {
   __shared__ long long s_ws[32];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   long long incl = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -104,7 +104,7 @@ __device__ __forceinline__ long long block_excl_scan_i64(long long v, long long*
   if (lane == 31) s_ws[wid] = incl;
   __syncthreads();
   if (wid == 0) {
-    long long t = s_ws[lane];
+    long long t = lane < nw ? s_ws[lane] : 0ll;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const long long x = __shfl_up_sync(0xffffffffu, t, o);
@@ -289,6 +289,10 @@ __device__ void refresh_pressure(const Cfg& c, mars_scalars* sc, int worker_slot
 // ---------------------------------------------------------------------------
 
 #define SCAN_TPB 1024
+// resident k_scan CTAs per SM (two 512-thread CTAs per SM measured the same
+// as one 1024-thread CTA at 1M and 64M rows, r2; the block-level helpers
+// take any SCAN_TPB that is a multiple of 32)
+#define SCAN_CTAS_PER_SM 1
 #define SCAN_TILE (SCAN_TPB * SCAN_RPT)  // rows per tile (4096)
 
 // Per-row digit record written by phase 1 and read by phase 2 of k_scan:
@@ -307,6 +311,7 @@ __device__ void refresh_pressure(const Cfg& c, mars_scalars* sc, int worker_slot
 __device__ void block_threshold_pair(const u32* ha, u32 ka, const u32* hb, u32 kb, u32* wsum2,
                                      int* da, u32* ua, int* db, u32* ub) {
   constexpr int PER = HIST_BINS / SCAN_TPB;
+  constexpr int NW = SCAN_TPB / 32;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int base = threadIdx.x * PER;
   u32 va[PER], vb[PER];
@@ -339,7 +344,7 @@ __device__ void block_threshold_pair(const u32* ha, u32 ka, const u32* hb, u32 k
   }
   __syncthreads();
   if (wid < 2) {
-    u32 t = wsum2[wid * 32 + lane];
+    u32 t = lane < NW ? wsum2[wid * 32 + lane] : 0u;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       u32 x = __shfl_up_sync(FULL, t, o);
@@ -699,7 +704,7 @@ static size_t scan_stage_bytes() { return (size_t)SCAN_NBUF * SB_BYTES; }
 //           record, the S2 retention of its boundary rows and its expired
 //           pins at their place in the row-ordered list; CTA 0 finalises the
 //           probe / refresh scalars.
-__global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Bufs b,
+__global__ void __launch_bounds__(SCAN_TPB, SCAN_CTAS_PER_SM) k_scan(Tab t, Cfg c, Work* w, Bufs b,
                                                       mars_scalars* sc, i64 n_rows, i64* xc,
                                                       i64 chunk, Queue Q, const i32* qsel_p,
                                                       int no_stage, Kv kv, int kv_fused) {
@@ -912,7 +917,7 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
     // every thread is done with this round's buffer: refill it
     __syncthreads();
     {  // append the kept rows at their row-order positions
-      const u32 cw = s_wc[lane];
+      const u32 cw = lane < SCAN_TPB / 32 ? s_wc[lane] : 0u;
       const u32 before = __reduce_add_sync(FULL, lane < wid ? cw : 0u);
       const u32 tot = __reduce_add_sync(FULL, cw);
       if (keep) {
@@ -1065,8 +1070,9 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
       s_a[wid] = as;
     }
     __syncthreads();
-    exp_off = __reduce_add_sync(FULL, s_b[lane]);
-    n_exp_all = __reduce_add_sync(FULL, s_a[lane]);
+    const int nw = SCAN_TPB / 32;
+    exp_off = __reduce_add_sync(FULL, lane < nw ? s_b[lane] : 0);
+    n_exp_all = __reduce_add_sync(FULL, lane < nw ? s_a[lane] : 0);
   }
   PTIME(3);
 
@@ -1123,8 +1129,8 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
     }
     __syncthreads();
     if (wid == 0) {
-      unsigned long long v = s_scan[lane];
-      u32 e = s_escan[lane];
+      unsigned long long v = lane < SCAN_TPB / 32 ? s_scan[lane] : 0ull;
+      u32 e = lane < SCAN_TPB / 32 ? s_escan[lane] : 0u;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const unsigned long long x = __shfl_up_sync(FULL, v, o);
@@ -1388,7 +1394,7 @@ __global__ void __launch_bounds__(SCAN_TPB, 1) k_scan(Tab t, Cfg c, Work* w, Buf
       if (wid == 0) {
 #pragma unroll
         for (int q = 0; q < 6; ++q) {
-          const long long x = warp_sum<long long>(s_kr[q][lane]);
+          const long long x = warp_sum<long long>(lane < SCAN_TPB / 32 ? s_kr[q][lane] : 0ll);
           if (lane == 0) {
             if (q < 3) s_kb[q] = x; else s_kt[q - 3] = x;
           }
@@ -4209,7 +4215,7 @@ static void scan_geometry(i64 n, int nsm, int* grid, i64* chunk) {
 static void launch_scan(const LaunchArgs* a, int nsm, cudaStream_t s) {
   int grid;
   i64 chunk;
-  scan_geometry(a->n_rows, nsm, &grid, &chunk);
+  scan_geometry(a->n_rows, nsm * SCAN_CTAS_PER_SM, &grid, &chunk);
   Tab t = a->tab;
   Cfg c = a->cfg;
   Work* w = a->work;
