@@ -717,7 +717,7 @@ __global__ void __launch_bounds__(SCAN_TPB, SCAN_CTAS_PER_SM) k_scan(Tab t, Cfg 
   // to the free stack in row order, so this scan also lays out their frees
   // (segment / loose-ID / tail-chunk offsets, as k_kv_exp_scan would) and
   // k_kv_exp_push runs right after it
-  __shared__ unsigned long long s_kv[3];
+  __shared__ u32 s_kv[3];  // (per-CTA sums fit 32 bits: < rows x 128 segments)
   __shared__ i64 s_kvb[3];  // the free stack's pre-step tops (segments, arena, chunk pool)
   __shared__ u32 s_bw, s_bv;  // running histogram bounds (digits above are not counted)
   __shared__ __align__(8) u64 bars[SCAN_NBUF];
@@ -846,10 +846,10 @@ __global__ void __launch_bounds__(SCAN_TPB, SCAN_CTAS_PER_SM) k_scan(Tab t, Cfg 
           t.flags[r] = f & ~MARS_F_PINNED;
           t.kv[r] = 0;
           if (kv_fused) {  // (rare rows: shared atomics cost nothing here)
-            atomicAdd(&s_kv[0], (unsigned long long)(pbk / KV_CH + (pbk % KV_CH ? 1 : 0)));
+            atomicAdd(&s_kv[0], (u32)(pbk / KV_CH + (pbk % KV_CH ? 1 : 0)));
             if (pbk % KV_CH) {
-              atomicAdd(&s_kv[1], (unsigned long long)(pbk % KV_CH));
-              atomicAdd(&s_kv[2], 1ull);
+              atomicAdd(&s_kv[1], (u32)(pbk % KV_CH));
+              atomicAdd(&s_kv[2], 1u);
             }
           }
           exp_blocks += pbk;

@@ -455,12 +455,13 @@ __global__ void k_kv_exp_push(Kv k, const Work* w, Bufs b) {
   const int ne = w->n_exp;
   if (__ldcg(&k.xbase[1]) < 0) return;  // the stack overflowed (status set)
   const i64 base = k.xbase[0], a0 = k.xbase[2], c0 = k.xbase[3];
+  // one warp per table (a half warp per table measured the same, r2)
   const int lane = threadIdx.x & 31;
   for (int e = (int)(((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5); e < ne;
        e += (int)(((i64)gridDim.x * blockDim.x) >> 5)) {
     const u32 row = b.exp_row_sorted[e];
     const i64 L = b.exp_blk_sorted[e];
-    if (lane == 0 && k.len[row] != L) k.s->status |= 64;  // table != pinned blocks
+    if (lane == 0 && k.len[row] != L) atomicOr(&k.s->status, 64);  // table != pinned blocks
     kv_free_table_warp(k, row, L, base + k.xoff[e], a0 + k.xaoff[e], c0 + k.xroff[e], lane);
   }
 }

@@ -104,6 +104,8 @@ __device__ __forceinline__ FreePlan free_plan(i64 L, i64 keep) {
 // from the last one down, H's arena segment), the loose IDs of T and H to the
 // arena at ap.. (each segment pops from its end), T's chunk back to the pool
 // at cfs[cf] (cf < 0: none); the lanes copy IDs / write segments in parallel.
+// (W lanes per free: a warp, or a half warp for the many small expired tables)
+template <int W = 32>
 __device__ __forceinline__ void kv_free_warp(const Kv& k, u32 row, const FreePlan& f, i64 sp,
                                              i64 ap, i64 cf, int lane, bool cap = false) {
   const u32* dr = k.dir + (i64)row * k.D;
@@ -112,18 +114,18 @@ __device__ __forceinline__ void kv_free_warp(const Kv& k, u32 row, const FreePla
     const i64 n = f.L - f.keep;
     unsigned long long base = 0;
     if (lane == 0) base = atomicAdd((unsigned long long*)&k.s->cap_n, (unsigned long long)n);
-    base = __shfl_sync(0xffffffffu, base, 0);
+    base = __shfl_sync(0xffffffffu, base, 0, W);
     if ((i64)base + n > k.total) {
       if (lane == 0) atomicOr(&k.s->status, 128);
     } else {
-      for (i64 j = lane; j < n; j += 32) {
+      for (i64 j = lane; j < n; j += W) {
         const i64 p = f.keep + j;
         k.cap[base + j] = k.chunks[(i64)dr[p / KV_CH] * KV_CH + p % KV_CH];
       }
     }
   }
   if (f.nt > 0) {
-    for (i64 j = lane; j < f.nt; j += 32) {
+    for (i64 j = lane; j < f.nt; j += W) {
       const i64 p = f.tb + j;
       k.arena[ap + f.nt - 1 - j] = k.chunks[(i64)dr[p / KV_CH] * KV_CH + p % KV_CH];
     }
@@ -132,10 +134,10 @@ __device__ __forceinline__ void kv_free_warp(const Kv& k, u32 row, const FreePla
     ap += f.nt;
   }
   const i64 nf = f.f1 - f.f0;
-  for (i64 j = lane; j < nf; j += 32) k.seg[sp + j] = seg_chunk_make(dr[f.f1 - 1 - j], 0, KV_CH);
+  for (i64 j = lane; j < nf; j += W) k.seg[sp + j] = seg_chunk_make(dr[f.f1 - 1 - j], 0, KV_CH);
   sp += nf;
   if (f.nh > 0) {
-    for (i64 j = lane; j < f.nh; j += 32) {
+    for (i64 j = lane; j < f.nh; j += W) {
       const i64 p = f.keep + j;
       k.arena[ap + f.nh - 1 - j] = k.chunks[(i64)dr[p / KV_CH] * KV_CH + p % KV_CH];
     }
@@ -149,6 +151,7 @@ __device__ __forceinline__ void kv_free_warp(const Kv& k, u32 row, const FreePla
 
 // a whole table of L IDs (an expired pin's): T = its partial last chunk, then
 // its full chunks from the last one down
+template <int W = 32>
 __device__ __forceinline__ void kv_free_table_warp(const Kv& k, u32 row, i64 L, i64 sp, i64 ap,
                                                    i64 cf, int lane) {
   const i64 tail = L % KV_CH, full = L / KV_CH;
@@ -162,7 +165,7 @@ __device__ __forceinline__ void kv_free_table_warp(const Kv& k, u32 row, i64 L, 
   f.nt = tail;
   f.hb = 0;
   f.tail_chunk = tail > 0;
-  kv_free_warp(k, row, f, sp, ap, tail > 0 ? cf : -1, lane);
+  kv_free_warp<W>(k, row, f, sp, ap, tail > 0 ? cf : -1, lane);
 }
 
 int mars_kv_preload();
