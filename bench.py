@@ -758,6 +758,19 @@ def main():
             exchange(sh.xc[:len(COUNTERS)], sh.xsend, sh.xrecv)
             sh.phase(si, 2)
     eng.checkpoint()
+    sharded_graph = None
+    if world > 1 and os.environ.get("MARS_BENCH_BACKEND", "nccl") == "nccl":
+        # the whole sharded step (phase 1, NCCL all-reduce + all-gather,
+        # phase 2) as one CUDA graph; eager launches if the capture fails
+        try:
+            sh.capture(si)
+            eng.restore()
+            enqueue_step = sh.replay  # noqa: F811
+            sharded_graph = True
+        except Exception as exc:  # (reported in the line)
+            sharded_graph = "eager: " + repr(exc)[:120]
+            torch.cuda.synchronize()
+            eng.restore()
 
     # correctness guard: one fetched step must succeed with status 0
     enqueue_step()
@@ -916,6 +929,7 @@ def main():
                          "inputs": "table resident in HBM; 1 % of the rows (every column the "
                                    "step reads) uploaded each step"},
         "gpu_launches": launches,
+        "sharded_graph": sharded_graph,
         "advance": adv,
         "kernel_ms_median": kernel_ms,
         "clocks": clk.summary(),

@@ -157,3 +157,32 @@ class ShardedEngine:
             exchange(self.xc[:len(COUNTERS)], self.xsend, self.xrecv, self.group)
         self.phase(si, 2)
         return self.eng.fetch()
+
+    def capture(self, si) -> None:
+        """The whole sharded step -- phase 1, the NCCL all-reduce and
+        all-gather, phase 2 -- as ONE CUDA graph on the replica's stream
+        (torch.cuda.graph captures the collectives; the library's kernels are
+        stream-ordered launches with no host synchronisation).  ``replay``
+        then launches it; ``si`` is the step the graph repeats (its host copy
+        is read by the graph's first kernel at every replay)."""
+        import torch
+
+        si.mode |= N.MODE_SHARDED
+        self._si = si
+        lib, ctx = self.eng.lib, self.eng.ctx
+        # one eager step first: NCCL communicators and every kernel exist
+        self.step(si)
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=self.stream):
+            N.check(lib.mars_step_phase(ctx, C.byref(si), 1), ctx)
+            exchange(self.xc[:len(COUNTERS)], self.xsend, self.xrecv, self.group)
+            N.check(lib.mars_step_phase(ctx, C.byref(si), 2), ctx)
+
+    def replay(self) -> None:
+        import torch
+
+        # (a graph replays on the current stream: the replica's, so it is
+        # ordered with the library's own copies and the fetch)
+        with torch.cuda.stream(self.stream):
+            self.graph.replay()

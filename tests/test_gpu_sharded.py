@@ -104,3 +104,24 @@ def test_replicas_on_one_gpu_match_the_sharded_oracle(kind, world):
         for k in mine["state"]:
             assert np.array_equal(got["state"][k], mine["state"][k]), k
         e.close()
+
+
+def test_sharded_step_as_one_cuda_graph_replays_the_eager_step():
+    """phase 1 + the exchange + phase 2 captured as ONE CUDA graph
+    (ShardedEngine.capture; the bench's multi-GPU step) and replayed from a
+    restored state give the eager sharded step's outputs (world 1: the
+    exchange is the device copy the collectives reduce to)."""
+    snap = snapshot_v1(30_000, seed=81, pool="headroom")
+    eng, sh = _replica(snap, 1, 0, np.arange(len(snap.queue)))
+    si = eng.step_in(snap.now, True, snap.active_tools, 0, snap.worker_slots)
+    eng.checkpoint()
+    want = canon(canonical(sh.step(si), eng, snap))
+    eng.restore()
+    sh.capture(si)
+    for _ in range(2):
+        eng.restore()
+        sh.replay()
+        got = canon(canonical(eng.fetch(), eng, snap))
+        for k in want:
+            assert got[k] == want[k], k
+    eng.close()
