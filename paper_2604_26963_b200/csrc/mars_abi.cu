@@ -638,7 +638,14 @@ int mars_queue_append(mars_ctx* ctx, int64_t n, const uint32_t* rows, const int3
   if (ctx->q_upper + n > ctx->max_queue)
     return fail(ctx, MARS_ERR_CAPACITY, "queue %lld + %lld > %lld", (long long)ctx->q_upper,
                 (long long)n, (long long)ctx->max_queue);
-  if (n * 9 > ctx->alloc_rows * 8) return fail(ctx, MARS_ERR_CAPACITY, "append batch too large");
+  if (n * 9 > ctx->alloc_rows * 8) {  // through the staging buffer in chunks, in order
+    const int64_t m = ctx->alloc_rows * 8 / 9;
+    for (int64_t o = 0; o < n; o += m) {
+      int rc = mars_queue_append(ctx, std::min(m, n - o), rows + o, req + o, lng + o);
+      if (rc) return rc;
+    }
+    return MARS_OK;
+  }
   int mx = ctx->q_maxreq;
   for (int64_t i = 0; i < n; ++i) {
     if (req[i] < 1) return fail(ctx, MARS_ERR_CONTRACT, "queue entry needs req_blocks >= 1");
@@ -665,9 +672,11 @@ static int hook_rows_check(mars_ctx* ctx, int64_t n, const int64_t* rows) {
   if (!ctx || n < 0 || (n > 0 && !rows)) return MARS_ERR_ARG;
   for (int64_t i = 0; i < n; ++i)
     if (rows[i] < 0 || rows[i] >= ctx->max_rows) return fail(ctx, MARS_ERR_CAPACITY, "row out of range");
-  if (n * 24 > ctx->alloc_rows * 8) return fail(ctx, MARS_ERR_CAPACITY, "hook batch too large");
   return MARS_OK;
 }
+
+// entries per pass through the row staging buffer (24 bytes each at most)
+static int64_t hook_chunk(const mars_ctx* ctx) { return ctx->alloc_rows * 8 / 24; }
 
 static int hook_status(mars_ctx* ctx) {
   int32_t st = 0;
@@ -682,6 +691,14 @@ int mars_on_admit(mars_ctx* ctx, int64_t n, const int64_t* rows, const int32_t* 
                   const double* now) {
   int rc = hook_rows_check(ctx, n, rows);
   if (rc || n == 0) return rc;
+  const int64_t m = hook_chunk(ctx);
+  if (n > m) {  // (rows are distinct: the chunks are independent)
+    for (int64_t o = 0; o < n; o += m) {
+      rc = mars_on_admit(ctx, std::min(m, n - o), rows + o, r0_prefill + o, now + o);
+      if (rc) return rc;
+    }
+    return MARS_OK;
+  }
   CK(cudaSetDevice(ctx->device));
   u8* st = ctx->d_stage;
   CK(cudaMemcpyAsync(st, rows, n * 8, cudaMemcpyHostToDevice, ctx->stream));
@@ -698,6 +715,15 @@ int mars_on_service(mars_ctx* ctx, int64_t n, const int64_t* rows, const int64_t
                     const double* now, const int64_t* pre_charge) {
   int rc = hook_rows_check(ctx, n, rows);
   if (rc || n == 0) return rc;
+  const int64_t m = hook_chunk(ctx);
+  if (n > m) {
+    for (int64_t o = 0; o < n; o += m) {
+      rc = mars_on_service(ctx, std::min(m, n - o), rows + o, tokens + o, now + o,
+                           pre_charge ? pre_charge + o : nullptr);
+      if (rc) return rc;
+    }
+    return MARS_OK;
+  }
   CK(cudaSetDevice(ctx->device));
   u8* st = ctx->d_stage;
   CK(cudaMemcpyAsync(st, rows, n * 8, cudaMemcpyHostToDevice, ctx->stream));

@@ -276,3 +276,27 @@ def test_host_tier_follows_the_decisions(key):
     assert tier["evict_blocks"] + tier["pin_blocks"] > 0
     assert tier["host_slots_checked"] > 0 and tier["host_slots_bad"] == 0
     assert tier["pool_blocks_bad"] == 0
+
+
+def test_batched_hooks_larger_than_the_staging_buffer():
+    """mars_on_admit / mars_queue_append take batches of any size (passed
+    through the row staging buffer in chunks)."""
+    from paper_2604_26963_b200.snapshot import initial_level_np
+    n = 2000
+    eng = MarsEngine(max_rows=n, max_queue=n)
+    rng = np.random.default_rng(3)
+    rows = rng.permutation(n)[:1900].astype(np.int64)
+    r0 = rng.integers(1, 200_000, size=len(rows)).astype(np.int32)
+    eng.upsert({"level": np.full(n, 9, np.uint8), "promos": np.full(n, 2, np.uint8),
+                "served": np.full(n, 7, np.int64), "flags": np.zeros(n, np.uint8)})
+    eng.on_admit(rows, r0, 12.5)
+    st = eng.read(["level", "promos", "served", "wait_since", "flags"], rows=rows)
+    assert st["level"].tolist() == initial_level_np(r0.astype(np.int64)).tolist()
+    assert not st["promos"].any() and not st["served"].any()
+    assert (st["wait_since"] == 12.5).all() and (st["flags"] & 1).all()
+    q = rng.permutation(n)[:1800].astype(np.uint32)
+    req = rng.integers(1, 500, size=len(q)).astype(np.int32)
+    eng.set_queue(q[:5], req[:5], np.zeros(5, bool))
+    eng.queue_append(q[5:], req[5:], np.zeros(len(q) - 5, bool))
+    assert eng.get_queue().tolist() == q.tolist()
+    eng.close()
