@@ -4005,34 +4005,49 @@ __global__ void k_flush(u8* p, i64 n, u32 salt) {
 // Step head in one node: zero the work area, take this step's inputs
 // straight from the pinned host copy (mapped, UVA: a ~100-byte PCIe read, no
 // separate memset / memcpy graph nodes) and seed the min/max accumulators.
+// The step's work area: zeroed (16-byte stores), the step input copied from
+// its mapped pinned host copy and the pre-step scalars the early pack needs
+// taken -- every load issued before the zeroing and stored after it, so the
+// PCIe round trip of the host read overlaps the zeroing.
 __global__ void __launch_bounds__(1024) k_work_init(Work* w, const mars_step_in* h_in,
                                                    const mars_scalars* sc) {
   PTIME(32);
-  static_assert(sizeof(Work) % 16 == 0 || true, "");
+  static_assert(sizeof(Work) % 16 == 0, "Work is zeroed in 16-byte words");
+  static_assert(sizeof(mars_step_in) % 4 == 0 && sizeof(mars_step_in) / 4 <= 1024,
+                "step_in is a few words");
+  constexpr int NIN = (int)(sizeof(mars_step_in) / 4);
+  unsigned int in_word = 0;
+  int pre[5] = {0, 0, 0, 0, 0};
+  long long pre_q = 0;
+  if (threadIdx.x < NIN) in_word = ((const volatile unsigned int*)h_in)[threadIdx.x];
+  if (threadIdx.x == 32) {  // (another warp than the host read's)
+    pre[0] = sc->cpu_overloaded;
+    pre[1] = sc->cpu_high_streak;
+    pre[2] = sc->cpu_low_streak;
+    pre[3] = sc->active_tools;
+    pre[4] = sc->queued_tools;
+    pre_q = sc->queue_len;
+  }
   const size_t n16 = sizeof(Work) / 16;
   uint4* p = (uint4*)w;
   const uint4 z = make_uint4(0, 0, 0, 0);
   for (size_t i = threadIdx.x; i < n16; i += blockDim.x) p[i] = z;
-  static_assert(sizeof(Work) % 16 == 0, "Work is zeroed in 16-byte words");
   __syncthreads();
-  {
-    const unsigned int* src = (const unsigned int*)h_in;
-    unsigned int* dst = (unsigned int*)&w->in;
-    static_assert(sizeof(mars_step_in) % 4 == 0, "step_in is word-sized");
-    for (size_t i = threadIdx.x; i < sizeof(mars_step_in) / 4; i += blockDim.x) dst[i] = src[i];
-  }
+  if (threadIdx.x < NIN) ((unsigned int*)&w->in)[threadIdx.x] = in_word;
   if (threadIdx.x < 12) (&w->ref_gand[0][0][0])[threadIdx.x] = ~0ull;
   if (threadIdx.x == 0) {
     w->tmin_win = 0xffffffffu;
     w->tmin_vic = 0xffffffffu;
     w->min_req = 0x7fffffff;
     w->pk_min_req = 0x7fffffff;
-    w->pre_cpu_overloaded = sc->cpu_overloaded;
-    w->pre_cpu_high_streak = sc->cpu_high_streak;
-    w->pre_cpu_low_streak = sc->cpu_low_streak;
-    w->pre_active_tools = sc->active_tools;
-    w->pre_queued_tools = sc->queued_tools;
-    w->pre_queue_len = sc->queue_len;
+  }
+  if (threadIdx.x == 32) {
+    w->pre_cpu_overloaded = pre[0];
+    w->pre_cpu_high_streak = pre[1];
+    w->pre_cpu_low_streak = pre[2];
+    w->pre_active_tools = pre[3];
+    w->pre_queued_tools = pre[4];
+    w->pre_queue_len = pre_q;
   }
 }
 
