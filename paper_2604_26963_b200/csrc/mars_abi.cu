@@ -566,12 +566,45 @@ int mars_upsert_rows(mars_ctx* ctx, int64_t n, const int64_t* rows, const mars_c
         return fail(ctx, MARS_ERR_CAPACITY, "row %lld out of range", (long long)rows[i]);
     if (n > ctx->max_rows) return MARS_ERR_CAPACITY;
     CK(cudaMemcpyAsync(ctx->d_rows, rows, (size_t)n * 8, cudaMemcpyHostToDevice, ctx->stream));
+    // every given column staged side by side, then ONE scatter launch; a
+    // batch larger than the staging buffer goes column by column
+    ScatterCols L;
+    L.n = 0;
+    size_t off = 0;
+    bool fits = true;
     for (auto& cs : ctx->cols) {
       const void* hp = *(void* const*)((const char*)cols + cs.host_off);
       if (!hp) continue;
-      CK(cudaMemcpyAsync(ctx->d_stage, hp, (size_t)n * cs.esz, cudaMemcpyHostToDevice, ctx->stream));
-      int rc = mars_enqueue_scatter(ctx->stream, *cs.dev, ctx->d_stage, ctx->d_rows, n, cs.esz);
+      off = (off + 15) & ~(size_t)15;
+      if (off + (size_t)n * cs.esz > (size_t)ctx->alloc_rows * 8 || L.n == SCATTER_MAX_COLS) {
+        fits = false;
+        break;
+      }
+      L.dst[L.n] = *cs.dev;
+      L.off[L.n] = (long long)off;
+      L.esz[L.n] = cs.esz;
+      ++L.n;
+      off += (size_t)n * cs.esz;
+    }
+    if (fits) {
+      int k = 0;
+      for (auto& cs : ctx->cols) {
+        const void* hp = *(void* const*)((const char*)cols + cs.host_off);
+        if (!hp) continue;
+        CK(cudaMemcpyAsync(ctx->d_stage + L.off[k], hp, (size_t)n * cs.esz, cudaMemcpyHostToDevice,
+                           ctx->stream));
+        ++k;
+      }
+      int rc = mars_enqueue_scatter_cols(ctx->stream, L, ctx->d_stage, ctx->d_rows, n);
       if (rc) return fail(ctx, MARS_ERR_CUDA, "scatter: %s", cudaGetErrorString((cudaError_t)rc));
+    } else {
+      for (auto& cs : ctx->cols) {
+        const void* hp = *(void* const*)((const char*)cols + cs.host_off);
+        if (!hp) continue;
+        CK(cudaMemcpyAsync(ctx->d_stage, hp, (size_t)n * cs.esz, cudaMemcpyHostToDevice, ctx->stream));
+        int rc = mars_enqueue_scatter(ctx->stream, *cs.dev, ctx->d_stage, ctx->d_rows, n, cs.esz);
+        if (rc) return fail(ctx, MARS_ERR_CUDA, "scatter: %s", cudaGetErrorString((cudaError_t)rc));
+      }
     }
     for (int64_t i = 0; i < n; ++i)
       if (rows[i] + 1 > ctx->n_rows) ctx->n_rows = rows[i] + 1;

@@ -4174,6 +4174,31 @@ int mars_enqueue_service_rows(cudaStream_t s, const Tab& t, const Cfg& c, i64 n,
   return (int)cudaGetLastError();
 }
 
+// every column of an upsert in one launch: column c's values sit at
+// src + L.off[c] (n entries of L.esz[c] bytes), row i goes to rows[i]
+__global__ void k_scatter_cols(ScatterCols L, const u8* src, const i64* rows, i64 n) {
+  for (i64 j = (i64)blockIdx.x * blockDim.x + threadIdx.x; j < n * L.n;
+       j += (i64)gridDim.x * blockDim.x) {
+    const int c = (int)(j / n);
+    const i64 i = j - (i64)c * n, r = rows[i];
+    const u8* sp = src + L.off[c];
+    u8* dp = (u8*)L.dst[c];
+    const int esz = L.esz[c];
+    if (esz == 1) dp[r] = sp[i];
+    else if (esz == 4) ((u32*)dp)[r] = ((const u32*)sp)[i];
+    else ((u64*)dp)[r] = ((const u64*)sp)[i];
+  }
+}
+
+int mars_enqueue_scatter_cols(cudaStream_t s, const ScatterCols& L, const void* src,
+                              const i64* rows, i64 n) {
+  if (n <= 0 || L.n <= 0) return 0;
+  i64 g = (n * L.n + 255) / 256;
+  if (g > 1184) g = 1184;
+  k_scatter_cols<<<(int)g, 256, 0, s>>>(L, (const u8*)src, rows, n);
+  return (int)cudaGetLastError();
+}
+
 int mars_enqueue_scatter(cudaStream_t s, void* dst, const void* src, const i64* rows, i64 n,
                          int esz) {
   if (n <= 0) return 0;
@@ -4478,7 +4503,8 @@ int mars_kernels_preload() {
                        (const void*)k_retention_batch, (const void*)k_scan,
                        (const void*)k_scatter, (const void*)k_walk, (const void*)k_work_init,
                        (const void*)k_queue_append, (const void*)k_admit_rows,
-                       (const void*)k_service_rows, (const void*)k_expired_rows};
+                       (const void*)k_service_rows, (const void*)k_expired_rows,
+                       (const void*)k_scatter_cols};
   for (const void* f : fns) {
     cudaError_t e = cudaFuncGetAttributes(&fa, f);
     if (e != cudaSuccess) return (int)e;

@@ -38,6 +38,15 @@ struct LaunchArgs {
 
 int mars_kernels_init();
 int mars_kernels_preload();
+#define SCATTER_MAX_COLS 32
+struct ScatterCols {  // the columns of one upsert (k_scatter_cols)
+  int n;
+  void* dst[SCATTER_MAX_COLS];
+  long long off[SCATTER_MAX_COLS];
+  int esz[SCATTER_MAX_COLS];
+};
+int mars_enqueue_scatter_cols(cudaStream_t s, const ScatterCols& L, const void* src,
+                              const i64* rows, i64 n);
 int mars_enqueue_expired_rows(cudaStream_t s, const Tab& t, i64 n_rows, double now, u32* out,
                               i64 cap, int* cnt, int grid);
 int mars_enqueue_admit_rows(cudaStream_t s, const Tab& t, const Cfg& c, i64 n, const i64* rows,
