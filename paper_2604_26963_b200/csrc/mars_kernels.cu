@@ -54,6 +54,7 @@ __global__ void k_ptime_dump() {
   for (int i = 0; i < 1024; ++i)
     if (g_ptime[i][0]) t0 = min(t0, g_ptime[i][0]);
   if (g_ptime[0][32]) t0 = min(t0, g_ptime[0][32]);  // k_work_init
+  printf("t0 %llu\n", t0);
   for (int k = 0; k < PT_SLOTS; ++k) {
     unsigned long long mn = ~0ull, mx = 0;
     int cnt = 0;
@@ -712,7 +713,7 @@ __global__ void __launch_bounds__(SCAN_TPB, SCAN_CTAS_PER_SM) k_scan(Tab t, Cfg 
   __shared__ u32 hw[HIST_BINS];
   __shared__ u32 hv[HIST_BINS];
   __shared__ u32 wsum[64];
-  __shared__ u32 s_wc[32];  // per-warp kept-row counts of the current round
+  __shared__ u32 s_wc[64];  // per-warp kept-row counts of the current round (x2)
   // S5 with a rank-ordered table (kv_fused): the expired pins' tables go back
   // to the free stack in row order, so this scan also lays out their frees
   // (segment / loose-ID / tail-chunk offsets, as k_kv_exp_scan would) and
@@ -763,6 +764,10 @@ __global__ void __launch_bounds__(SCAN_TPB, SCAN_CTAS_PER_SM) k_scan(Tab t, Cfg 
     for (int rd = 0; rd < nrounds && rd < SCAN_NBUF; ++rd) issue(rd);
   }
 
+  // Launched as k_work_init's programmatic dependent: everything above (the
+  // ring's first fill included) overlaps the step head; the work area and
+  // the step input are read only past this point
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const double now = w->in.now;
   const int mode = w->in.mode;
   const bool do_exp = !(mode & MARS_MODE_SKIP_EXPIRY) && policy_pins(c);
@@ -800,7 +805,8 @@ __global__ void __launch_bounds__(SCAN_TPB, SCAN_CTAS_PER_SM) k_scan(Tab t, Cfg 
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   // pack_queue's key range (control.py:109-122) over the admission list
   // itself: CTA g reduces its slice (coalesced; the loads overlap the first
-  // TMA round trip)
+  // TMA round trip.  Folding a part per round instead -- loads in flight
+  // across the row work -- was measured slower: they queue behind the ring)
   {
     const i64 qn = sc->queue_len;
     const i32* qreq = PICK2(Q.req, *qsel_p);
@@ -812,6 +818,7 @@ __global__ void __launch_bounds__(SCAN_TPB, SCAN_CTAS_PER_SM) k_scan(Tab t, Cfg 
     }
   }
   __syncthreads();
+  PTIME(45);
 
   // ---- phase 1 ---------------------------------------------------------------
   // Running-victim digits and the window digit's f64 part are skipped once the
@@ -823,6 +830,7 @@ __global__ void __launch_bounds__(SCAN_TPB, SCAN_CTAS_PER_SM) k_scan(Tab t, Cfg 
   for (int rd = 0; rd < nrounds; ++rd) {
     const unsigned char* B = sdyn + (size_t)buf * SB_BYTES;
     mbar_wait(&bars[buf], par);
+    if (rd == 0) PTIME(46);
     const int lr = threadIdx.x;
     const i64 r = cs + (i64)rd * SCAN_R + lr;
     const bool valid = lr < (int)(ce - (cs + (i64)rd * SCAN_R));
@@ -909,15 +917,19 @@ __global__ void __launch_bounds__(SCAN_TPB, SCAN_CTAS_PER_SM) k_scan(Tab t, Cfg 
       keep = ((rw & ~DIG_BND) <= bw) || rv <= bv || (rw & DIG_BND) || rv == DIG_EXP;
     }
     const u32 kbal = __ballot_sync(FULL, keep);
-    if (lane == 0) s_wc[wid] = __popc(kbal);
+    // (per-warp counts double-buffered by round parity: a warp may run one
+    // round ahead -- there is no barrier at a round's end -- but not two)
+    u32* wc_ = s_wc + (rd & 1) * 32;
+    if (lane == 0) wc_[wid] = __popc(kbal);
     if (++buf == SCAN_NBUF) {
       buf = 0;
       par ^= 1u;
     }
     // every thread is done with this round's buffer: refill it
     __syncthreads();
+    if (rd == 0) PTIME(47);
     {  // append the kept rows at their row-order positions
-      const u32 cw = lane < SCAN_TPB / 32 ? s_wc[lane] : 0u;
+      const u32 cw = lane < SCAN_TPB / 32 ? wc_[lane] : 0u;
       const u32 before = __reduce_add_sync(FULL, lane < wid ? cw : 0u);
       const u32 tot = __reduce_add_sync(FULL, cw);
       if (keep) {
@@ -931,7 +943,9 @@ __global__ void __launch_bounds__(SCAN_TPB, SCAN_CTAS_PER_SM) k_scan(Tab t, Cfg 
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue(rd + SCAN_NBUF);
     }
-    // tighten the histogram bounds to the CTA's running top-k bins
+    // tighten the histogram bounds to the CTA's running top-k bins (the
+    // only rounds that end at a barrier: the next round reads the bounds)
+    if (rd == 0) PTIME(59);
     if ((rd == 0 || rd == 2) && rd + 1 < nrounds) {
       int tw, tv;
       u32 up, upv;
@@ -940,10 +954,11 @@ __global__ void __launch_bounds__(SCAN_TPB, SCAN_CTAS_PER_SM) k_scan(Tab t, Cfg 
         s_bw = (u32)tw;
         s_bv = (u32)tv;
       }
+      __syncthreads();
     }
-    __syncthreads();
     if (rd < 7) PTIME(25 + rd);
   }
+  __syncthreads();
 
   // local thresholds: only bins at or below them can hold a global top-k key
   {
@@ -1005,6 +1020,9 @@ __global__ void __launch_bounds__(SCAN_TPB, SCAN_CTAS_PER_SM) k_scan(Tab t, Cfg 
   PTIME(1);
   grid.sync();
   PTIME(2);
+  // the kernel after the scan (S5's expired-table push, launched as a
+  // programmatic dependent) may become resident now and wait for this grid
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   // ---- phase 2 ---------------------------------------------------------------
   // Every load that does not depend on another is issued at once: the CTA
@@ -4012,6 +4030,9 @@ __global__ void k_flush(u8* p, i64 n, u32 salt) {
 __global__ void __launch_bounds__(1024) k_work_init(Work* w, const mars_step_in* h_in,
                                                    const mars_scalars* sc) {
   PTIME(32);
+  // k_scan may launch now: it waits (griddepcontrol.wait) for this grid's
+  // completion before touching the work area
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   static_assert(sizeof(Work) % 16 == 0, "Work is zeroed in 16-byte words");
   static_assert(sizeof(mars_step_in) % 4 == 0 && sizeof(mars_step_in) / 4 <= 1024,
                 "step_in is a few words");
@@ -4240,6 +4261,7 @@ static void lchk(const char* name) {
   if (e != cudaSuccess) fprintf(stderr, "mars: launch of %s failed: %s\n", name, cudaGetErrorString(e));
 }
 
+static int g_no_pdl = 0;    // MARS_NO_PDL=1: plain stream order between the step head and k_scan
 static int g_no_stage = 0;  // MARS_SCAN_NO_STAGE=1: k_scan emits without staging (tests)
 
 static void scan_geometry(i64 n, int nsm, int* grid, i64* chunk) {
@@ -4272,14 +4294,29 @@ static void launch_scan(const LaunchArgs* a, int nsm, cudaStream_t s) {
   Kv kv;
   if (a->kv) kv = *a->kv; else memset(&kv, 0, sizeof kv);
   void* args[] = {&t, &c, &w, &b, &sc, &n, &xc, &chunk, &Q, &qsel, &no_stage, &kv, &kv_fused};
-  cudaLaunchCooperativeKernel((const void*)k_scan, dim3(grid), dim3(SCAN_TPB), args,
-                              scan_stage_bytes(), s);
+  // cooperative, and a programmatic dependent of the kernel before it on the
+  // stream (k_work_init): its head and first ring fill overlap the step head
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(SCAN_TPB);
+  cfg.dynamicSmemBytes = scan_stage_bytes();
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = g_no_pdl ? 1 : 2;
+  cudaLaunchKernelExC(&cfg, (const void*)k_scan, args);
 }
 
 int mars_kernels_init() {
   {
     const char* v = getenv("MARS_SCAN_NO_STAGE");
     g_no_stage = (v && v[0] == '1') ? 1 : 0;
+    const char* pd = getenv("MARS_NO_PDL");
+    g_no_pdl = (pd && pd[0] == '1') ? 1 : 0;
     const char* d = getenv("MARS_DEBUG_LAUNCH");
     g_debug_launch = (d && d[0] == '1') ? 1 : 0;
   }
@@ -4386,10 +4423,14 @@ int mars_enqueue_step(const LaunchArgs* a) {
   // depends on the walk is enqueued before the control plane is.
   if (kv_fused) {
     // S5, expired list in rank order (k_scan laid out the frees): the expired
-    // tables go back to the free stack on the main stream beside the walk
-    // (small CTAs: they never need the walk's SM)
+    // tables go back to the free stack on the main stream beside the walk, as
+    // a programmatic dependent of the scan (resident and waiting before the
+    // scan ends).  On the pack's stream instead -- beside the control plane
+    // rather than in front of it -- both slowed down (r2: 73.0 vs 71.6 us):
+    // the push and the admission are latency-bound on the same memory.
     mark(5, 0, s);
-    mars_kv_enqueue_exp_free(*a->kv, s, a->work, a->bufs, nsm, /*offsets_done=*/true);
+    mars_kv_enqueue_exp_free(*a->kv, s, a->work, a->bufs, nsm, /*offsets_done=*/true,
+                             /*pdl=*/!g_no_pdl);
     mark(5, 1, s);
     launches++;
     cudaEventRecord(a->ev_kvx, s);
@@ -4441,7 +4482,8 @@ int mars_enqueue_step(const LaunchArgs* a) {
     // spin on the admission's completion flag, and with the early pack on the
     // second side stream that arrangement was seen to starve k_control, r2.)
     mark(5, 0, s);
-    mars_kv_enqueue_exp_free(*a->kv, s, a->work, a->bufs, nsm, /*offsets_done=*/false);
+    mars_kv_enqueue_exp_free(*a->kv, s, a->work, a->bufs, nsm, /*offsets_done=*/false,
+                             /*pdl=*/false);
     mark(5, 1, s);
     launches += 2;
   }
@@ -4468,6 +4510,7 @@ int mars_enqueue_step(const LaunchArgs* a) {
   }
 #ifdef MARS_PHASE_TIMING
   k_ptime_dump<<<1, 1, 0, s>>>();
+  mars_kv_ptime_dump(s);
 #endif
   return launches;
 }

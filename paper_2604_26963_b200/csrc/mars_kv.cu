@@ -383,6 +383,32 @@ __device__ void kv_apply_list(Kv& k, i64 n_ops, const u8* op, const u32* row, co
 }
 
 // host journal: ordered (op, row, n)
+#ifdef MARS_PHASE_TIMING
+#include <cstdio>
+// debug builds only: first CTA start (even slots) / last CTA end (odd slots)
+__device__ unsigned long long g_kvt[8];
+__device__ __forceinline__ unsigned long long kvt_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define KVT_BEGIN(k) \
+  if (threadIdx.x == 0) atomicMin(&g_kvt[2 * (k)], kvt_now())
+#define KVT_END(k) \
+  if (threadIdx.x == 0) atomicMax(&g_kvt[2 * (k) + 1], kvt_now())
+__global__ void k_kvt_dump() {
+  for (int k = 0; k < 4; ++k) {
+    if (g_kvt[2 * k + 1]) printf("kvt %d %llu %llu\n", k, g_kvt[2 * k], g_kvt[2 * k + 1]);
+    g_kvt[2 * k] = ~0ull;
+    g_kvt[2 * k + 1] = 0;
+  }
+}
+void mars_kv_ptime_dump(cudaStream_t s) { k_kvt_dump<<<1, 1, 0, s>>>(); }
+#else
+#define KVT_BEGIN(k)
+#define KVT_END(k)
+#endif
+
 __global__ void __launch_bounds__(KV_TPB) k_kv_apply(Kv k, i64 n_ops, const u8* op, const u32* row,
                                                      const i32* n) {
   kv_apply_list(k, n_ops, op, row, n, false);
@@ -452,6 +478,10 @@ __global__ void __launch_bounds__(KV_TPB) k_kv_exp_scan(Kv k, const Work* w, Buf
 // a whole table: T = its partial last chunk (loose IDs to the arena, the
 // chunk back to the pool), then its full chunks from the last one down
 __global__ void k_kv_exp_push(Kv k, const Work* w, Bufs b) {
+  // (a programmatic dependent of k_scan when the scan laid out the offsets:
+  // resident early, it waits here for the scan's completion; a no-op else)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  KVT_BEGIN(0);
   const int ne = w->n_exp;
   if (__ldcg(&k.xbase[1]) < 0) return;  // the stack overflowed (status set)
   const i64 base = k.xbase[0], a0 = k.xbase[2], c0 = k.xbase[3];
@@ -464,6 +494,7 @@ __global__ void k_kv_exp_push(Kv k, const Work* w, Bufs b) {
     if (lane == 0 && k.len[row] != L) atomicOr(&k.s->status, 64);  // table != pinned blocks
     kv_free_table_warp(k, row, L, base + k.xoff[e], a0 + k.xaoff[e], c0 + k.xroff[e], lane);
   }
+  KVT_END(0);
 }
 
 // the rest of the step's journal on one CTA: k_walk's alloc / evict ops in
@@ -472,8 +503,10 @@ __global__ void k_kv_exp_push(Kv k, const Work* w, Bufs b) {
 // (sim.py:269); a pin keeps the table (ownership moves, the IDs stay)
 // parts: 1 the journal, 2 the tick tail's frees, 3 both
 __global__ void __launch_bounds__(KV_TPB) k_kv_apply_step(Kv k, Work* w, Bufs b, int parts) {
+  KVT_BEGIN(1);
   if (k.s->status) return;
   if (parts & 1) kv_apply_list(k, w->n_journal, b.j_op, b.j_row, b.j_n, true);
+  KVT_END(1);
   if ((parts & 2) && (w->in.mode & MARS_MODE_ADVANCE) && k.s->status == 0) {
     __shared__ u32 s_r[KV_TPB];
     __shared__ u8 s_c[KV_TPB];
@@ -587,10 +620,22 @@ int mars_kv_enqueue_apply(const Kv& k, cudaStream_t s, i64 n_ops, const u8* op, 
 }
 
 int mars_kv_enqueue_exp_free(const Kv& k, cudaStream_t s, Work* w, const Bufs& b, int grid,
-                             bool offsets_done) {
+                             bool offsets_done, bool pdl) {
   if (!offsets_done) k_kv_exp_scan<<<1, KV_TPB, 0, s>>>(k, w, b);
-  // small CTAs: they also fit beside the walk's CTA, which may still run
-  k_kv_exp_push<<<8 * grid, 256, 0, s>>>(k, w, b);
+  // small CTAs, one wave of at most 1024 threads per SM: resident beside
+  // k_scan's CTA while they wait for it (programmatic launch), they leave
+  // the scan's slot to the walk, which launches when the scan ends (8 per SM
+  // queued CTAs ahead of the walk and delayed its start by ~7 us at 1M, r2)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(4 * grid);
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, k_kv_exp_push, k, (const Work*)w, b);
   return (int)cudaGetLastError();
 }
 

@@ -169,13 +169,17 @@ __device__ __forceinline__ void kv_free_table_warp(const Kv& k, u32 row, i64 L, 
 }
 
 int mars_kv_preload();
+#ifdef MARS_PHASE_TIMING
+void mars_kv_ptime_dump(cudaStream_t s);  // first start / last end of the S5 kernels
+#endif
 int mars_kv_enqueue_apply(const Kv& k, cudaStream_t s, i64 n_ops, const u8* op, const u32* row,
                           const i32* n);
 // the step's journal (parts & 1) and the tick tail's frees (parts & 2)
 int mars_kv_enqueue_apply_step(const Kv& k, cudaStream_t s, Work* w, const Bufs& b, int parts);
-// the step's expired pins' frees; offsets_done: k_scan laid out the offsets
+// the step's expired pins' frees; offsets_done: k_scan laid out the offsets;
+// pdl: the push is a programmatic dependent of the kernel before it (k_scan)
 int mars_kv_enqueue_exp_free(const Kv& k, cudaStream_t s, Work* w, const Bufs& b, int grid,
-                             bool offsets_done);
+                             bool offsets_done, bool pdl);
 int mars_kv_enqueue_bulk(const Kv& k, cudaStream_t s, i64 n, const u32* rows, const i32* cnt,
                          int grid);
 int mars_kv_enqueue_resume_free(const Kv& k, cudaStream_t s, i64 n, const i64* rows,

@@ -23,6 +23,11 @@ stream = torch.cuda.Stream()
 torch.cuda.set_stream(stream)
 eng.lib.mars_set_stream(eng.ctx, stream.cuda_stream)
 eng.load_snapshot(snap)
+if "s5" in sys.argv[4:]:  # the block-ID manager attached (the bench's default step)
+    from paper_2604_26963_b200.kvstore import KvBlockManager
+    kvm = KvBlockManager(eng, snap.total_blocks,
+                         max_blocks_per_row=int(-(-(int(snap.cols["context"].max()) + 4096) // 16)))
+    kvm.load_snapshot_tables(snap)
 eng.checkpoint()
 si = eng.step_in(snap.now, policy == 'mars', snap.active_tools, 0, snap.worker_slots)
 eng.set_profiling(True)

@@ -6,5 +6,5 @@ nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo --fmad=false -std=c++
   -Xcompiler -fPIC -shared -DMARS_PHASE_TIMING -o ../libmars_b200.so \
   mars_kernels.cu mars_kv.cu mars_abi.cu
 cd ../..
-python scripts/debug_phase_timing.py ${1:-1000000} ${2:-headroom} ${3:-mars} 2>&1
+python scripts/debug_phase_timing.py ${1:-1000000} ${2:-headroom} ${3:-mars} ${4:-} 2>&1
 [ -n "$MICRO" ] && nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/mc scripts/micro_coop.cu && /tmp/mc
