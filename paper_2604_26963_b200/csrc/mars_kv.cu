@@ -343,32 +343,51 @@ __device__ void kv_apply_list(Kv& k, i64 n_ops, const u8* op, const u32* row, co
   __shared__ u8 s_cap[KV_TPB];  // host-tier capture: a running session's eviction
   __shared__ int s_m;
   const int t = threadIdx.x;
+  // the window's rows -> their first position (open addressing in the run
+  // scratch, which is free between runs): a repeated row ends the run
+  constexpr int HS = 2 * KV_TPB;
+  u32* h_key = (u32*)kv_scratch();
+  int* h_first = (int*)(h_key + HS);
+  static_assert(HS * 8 <= KV_SCRATCH, "row hash fits the run scratch");
   i64 i = 0;
   while (i < n_ops) {
     // the next window of ops, one per thread
     const bool valid = i + t < n_ops;
     int kd = 3;  // past the end
+    u32 r = 0;
     if (valid) {
       const int o = op[i + t];
       if (journal) kd = (o == MARS_J_ALLOC) ? 1 : 2;
       else kd = (o == MARS_KV_ALLOC) ? 1 : (o == MARS_KV_FREE ? 2 : 0);
-      s_row[t] = row[i + t];
+      r = row[i + t];
+      s_row[t] = r;
       s_n[t] = (journal && kd == 2) ? -1 : n[i + t];
       s_cap[t] = (journal && o == MARS_J_EVICT_RUNNING) ? 1 : 0;
     }
     s_kd[t] = (u8)kd;
+    for (int q = t; q < HS; q += KV_TPB) {
+      h_key[q] = 0xffffffffu;
+      h_first[q] = 0x7fffffff;
+    }
     if (t == 0) s_m = KV_TPB;
+    __syncthreads();
+    int slot = 0;
+    if (valid) {
+      slot = (int)((r * 2654435761u) >> 21) & (HS - 1);
+      for (;;) {
+        const u32 prev = atomicCAS(&h_key[slot], 0xffffffffu, r);
+        if (prev == 0xffffffffu || prev == r) break;
+        slot = (slot + 1) & (HS - 1);
+      }
+      atomicMin(&h_first[slot], t);
+    }
     __syncthreads();
     // the run is the longest prefix of one kind (alloc or free) with distinct
     // rows; a pin / unpin (no table change) is a run of its own, skipped.
     // Every thread tests whether its op ends the run (in parallel).
     const int kind = s_kd[0];
     if (t > 0) {
-      bool stop = kind == 0 || kd != kind;
-      if (!stop) {
-        const u32 r = s_row[t];
-        for (int q = 0; q < t && !stop; ++q) stop = s_row[q] == r;
-      }
+      const bool stop = kind == 0 || kd != kind || h_first[slot] < t;
       if (stop) atomicMin(&s_m, t);
     }
     __syncthreads();
