@@ -315,7 +315,10 @@ class MarsEngine:
     def enqueue(self, si: N.MarsStepIn) -> None:
         self._check(self.lib.mars_step_enqueue(self.ctx, C.byref(si)))
 
-    def fetch(self) -> StepResult:
+    def fetch(self, copy: bool = True) -> StepResult:
+        """The step's outputs.  ``copy=False``: the arrays are views of the
+        pinned output arena the device wrote (no host memcpy), valid until
+        the next fetch overwrites it."""
         if self._out is None:
             self._fetch_setup()
         o = self._out
@@ -329,11 +332,13 @@ class MarsEngine:
                 arrs[name] = np.empty(0, dt)
             else:
                 s0 = p - base
-                arrs[name] = arena[s0:s0 + n * isz].view(dt).copy()
+                v = arena[s0:s0 + n * isz].view(dt)
+                arrs[name] = v.copy() if copy else v
         npc = int(o.n_decode) + int(o.n_prefill)
         if o.plan_pre_charge and npc:
             s0 = int(C.cast(o.plan_pre_charge, C.c_void_p).value) - base
-            arrs["plan_pre_charge"] = arena[s0:s0 + npc * 8].view(np.int64).copy()
+            v = arena[s0:s0 + npc * 8].view(np.int64)
+            arrs["plan_pre_charge"] = v.copy() if copy else v
         else:
             arrs["plan_pre_charge"] = np.empty(0, np.int64)
         return StepResult(

@@ -87,3 +87,7 @@ t0 = time.perf_counter()
 for _ in range(20):
     eng.fetch()
 print(f"  fetch() x1      {(time.perf_counter() - t0) / 20 * 1e3:.3f} ms")
+t0 = time.perf_counter()
+for _ in range(20):
+    eng.fetch(copy=False)
+print(f"  fetch(copy=False) x1 {(time.perf_counter() - t0) / 20 * 1e3:.3f} ms")
