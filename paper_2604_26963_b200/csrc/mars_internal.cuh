@@ -151,7 +151,8 @@ struct Work {
   i32 n_queued_kv;  // queued rows holding KV (admission then touches reclaim state)
   u32 admit_done;   // set by k_control after admission; k_walk may wait on it
   u32 adm_ctas;     // k_control CTAs past admission (the last one publishes)
-  u32 adm_pad[3];   // (Work stays a whole number of 16-byte words)
+  u32 adm_next;     // admission: next 1024-entry chunk of the packed prefix to take
+  u32 adm_pad[2];   // (Work stays a whole number of 16-byte words)
   // grid radix refinement of the candidate lists (k_scan phase 3): per list
   // (0 window, 1 victims) three rotating 256-bin histograms and group AND /
   // ORs, and the final bound: the refined list holds the keys with

@@ -2179,78 +2179,97 @@ __device__ __forceinline__ void admit_grid(Tab t, Cfg c, Work* w, Bufs b, Queue 
   const int ref_sft = w->ref_s[0];
   const u128 ref_pp = mk128(w->ref_p[0][0], w->ref_p[0][1]) >> ref_sft;
   long long proj = 0;
-  const i64 stride = (i64)gridDim.x * blockDim.x;
   const i64 lim = ((take + 31) / 32) * 32;
   // the whole list is admitted: apply admit() in list order (row writes stay
   // sequential for a row-ordered list) -- the admitted set is the same
   const bool in_order = !sharded && !(w->in.mode & MARS_MODE_NO_ROWS) && take == qlen;
-  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < lim; i += stride) {
-    bool valid = i < take;
-    bool wc = false, own = false;
-    u64 whi = 0, wlo = 0;
-    u32 row = 0;
-    if (valid && (w->in.mode & MARS_MODE_NO_ROWS)) {
-      b.admitted[i] = src_row[perm[i]];
-    } else if (valid) {
-      // every load is issued before the first table store (the stores may
-      // alias them as far as the compiler knows): two dependent round trips
-      const u32 pi = perm[i];
-      const u32 pos = in_order ? (u32)i : pi;
-      row = src_row[pos];
-      const u32 adm = in_order ? src_row[pi] : row;
-      if (sharded && row == XQ_NONE) {
-        // another replica's session: a fresh queued session projects exactly
-        // req_blocks (context 0, kv 0: control.py:86-87 vs sim.py:162)
-        proj += src_req[pos];
-      } else {
-        own = sharded;
-        const i32 r0p = t.r0p[row];
-        const i32 kvv = t.kv[row];
-        const i32 ctx0 = t.ctx[row];
-        const i32 r0d = t.r0d[row];
-        const u8 fl = t.flags[row];
-        const double arr = c.coord ? now : t.arr[row];
-        const i64 cn = (i64)ctx0 + r0p;
-        const u32 lv = initial_level(c, r0p);
-        const u32 kl = c.coord ? lv : 0u;
-        wc = window_digit(kl, arr, scale) <= tw;
-        const u32 rk = wc ? t.rank[row] : 0u;
-        t.ctx[row] = (i32)cn;
-        t.rem[row] = r0d;
-        t.rs[row] = now;
-        t.ws[row] = now;
-        t.phase[row] = MARS_PREFILL;
-        t.flags[row] = (fl | MARS_F_ACTIVE) & ~MARS_F_QUEUED;
-        t.level[row] = (u8)lv;
-        t.promos[row] = 0;
-        t.served[row] = 0;
-        proj += blocks_ceil(c, cn) - blocks_ceil(c, kvv);
-        if (!sharded) b.admitted[i] = adm;
-        if (wc) {
-          window_key(kl, arr, rk, whi, wlo);
-          // k_scan refined the window list: join it only at or below its bound
-          if (ref_w) wc = (mk128(whi, wlo) >> ref_sft) <= ref_pp;
+  // The packed prefix is handed out in 1024-entry chunks by a counter, not
+  // strided over a fixed grid: admit() is a chain of scattered table
+  // accesses and CTAs progress unevenly (64M: the last CTA finished 240 us
+  // after the first).  The next chunk's grab is in flight during the
+  // current one; entries are independent (the candidate appends are atomic
+  // and the projected-block sum commutes), so the order does not matter.
+  // (CTA g's first chunk is chunk g: no grab before the first entry)
+  __shared__ long long s_c0;
+  i64 c0 = (i64)blockIdx.x * blockDim.x;
+  for (;;) {
+    if (c0 >= lim) break;  // (block-uniform)
+    u32 nxt = 0;
+    if (threadIdx.x == 0) nxt = gridDim.x + atomicAdd(&w->adm_next, 1u);
+    const i64 i = c0 + threadIdx.x;
+    if (i < lim) {  // (whole warps: lim and c0 are multiples of 32)
+      bool valid = i < take;
+      bool wc = false, own = false;
+      u64 whi = 0, wlo = 0;
+      u32 row = 0;
+      if (valid && (w->in.mode & MARS_MODE_NO_ROWS)) {
+        b.admitted[i] = src_row[perm[i]];
+      } else if (valid) {
+        // every load is issued before the first table store (the stores may
+        // alias them as far as the compiler knows): two dependent round trips
+        const u32 pi = perm[i];
+        const u32 pos = in_order ? (u32)i : pi;
+        row = src_row[pos];
+        const u32 adm = in_order ? src_row[pi] : row;
+        if (sharded && row == XQ_NONE) {
+          // another replica's session: a fresh queued session projects exactly
+          // req_blocks (context 0, kv 0: control.py:86-87 vs sim.py:162)
+          proj += src_req[pos];
+        } else {
+          own = sharded;
+          const i32 r0p = t.r0p[row];
+          const i32 kvv = t.kv[row];
+          const i32 ctx0 = t.ctx[row];
+          const i32 r0d = t.r0d[row];
+          const u8 fl = t.flags[row];
+          const double arr = c.coord ? now : t.arr[row];
+          const i64 cn = (i64)ctx0 + r0p;
+          const u32 lv = initial_level(c, r0p);
+          const u32 kl = c.coord ? lv : 0u;
+          wc = window_digit(kl, arr, scale) <= tw;
+          const u32 rk = wc ? t.rank[row] : 0u;
+          t.ctx[row] = (i32)cn;
+          t.rem[row] = r0d;
+          t.rs[row] = now;
+          t.ws[row] = now;
+          t.phase[row] = MARS_PREFILL;
+          t.flags[row] = (fl | MARS_F_ACTIVE) & ~MARS_F_QUEUED;
+          t.level[row] = (u8)lv;
+          t.promos[row] = 0;
+          t.served[row] = 0;
+          proj += blocks_ceil(c, cn) - blocks_ceil(c, kvv);
+          if (!sharded) b.admitted[i] = adm;
+          if (wc) {
+            window_key(kl, arr, rk, whi, wlo);
+            // k_scan refined the window list: join it only at or below its bound
+            if (ref_w) wc = (mk128(whi, wlo) >> ref_sft) <= ref_pp;
+          }
         }
       }
+      int s = warp_append(ref_w ? &w->n_wr : &w->n_wc, wc);
+      if (s >= 0) {
+        (ref_w ? b.wr_hi : b.wc_hi)[s] = whi;
+        (ref_w ? b.wr_lo : b.wc_lo)[s] = wlo;
+        (ref_w ? b.wr_row : b.wc_row)[s] = row;
+      }
+      // sharded: this replica's admitted rows, tagged with their packed index
+      s = warp_append(&w->n_adm_own, own);
+      if (s >= 0) {
+        b.admitted[s] = row;
+        x.adm_idx[s] = (u32)i;
+      }
     }
-    int s = warp_append(ref_w ? &w->n_wr : &w->n_wc, wc);
-    if (s >= 0) {
-      (ref_w ? b.wr_hi : b.wc_hi)[s] = whi;
-      (ref_w ? b.wr_lo : b.wc_lo)[s] = wlo;
-      (ref_w ? b.wr_row : b.wc_row)[s] = row;
-    }
-    // sharded: this replica's admitted rows, tagged with their packed index
-    s = warp_append(&w->n_adm_own, own);
-    if (s >= 0) {
-      b.admitted[s] = row;
-      x.adm_idx[s] = (u32)i;
-    }
+    if (threadIdx.x == 0) s_c0 = (long long)nxt * blockDim.x;
+    __syncthreads();
+    c0 = s_c0;
+    __syncthreads();  // (every thread has read s_c0 before the next store)
   }
   PTIME(13);
   // residual queue in packed order (control.py:190); sharded: this replica's
   // entries only, each with its new dense global position
   const i64 nres = qlen - take;
   const i64 rlim = ((nres + 31) / 32) * 32;
+  const i64 stride = (i64)gridDim.x * blockDim.x;
   for (i64 j = (i64)blockIdx.x * blockDim.x + threadIdx.x; j < rlim; j += stride) {
     if (!sharded) {
       if (j < nres) {
