@@ -1576,6 +1576,7 @@ __device__ __forceinline__ int next_pow2(int n) {
 // ---------------------------------------------------------------------------
 // generic multi-CTA stable LSD radix sort (u64 keys, u32 values, 8-bit digits)
 #define LSD_SEG_J (PACK_SEG_ENTRIES / 1024)  // entries per lane of the warp-segment ranking
+#define LSD_B 4  // entries per lane per batch of a long chunk's scatter
 // control words live in Work (queue: lsd_*, expired: xlsd_*)
 // ---------------------------------------------------------------------------
 
@@ -1799,22 +1800,60 @@ __device__ int lsd_grid_sort(Lsd L, LsdView v, LsdArgs a, int npass, u32 (*wc)[2
         vout[pos] = sv[j];
       }
     }
-    for (int base = s; base < e && !seg; base += 1024) {
-      int i = base + tid;
-      bool valid = i < e;
-      u64 k = 0;
-      u32 val = 0;
-      if (one) {
-        k = k1;
-        val = v1;
-      } else if (valid) {
-        k = rawp ? (u64)(asc ? raw[i] : mr - raw[i]) : kin[i];
-        val = rawp ? (u32)i : vin[i];
-      }
-      u32 dig = valid ? (u32)((k >> shift) & 255u) : (256u + (u32)lane);
+    if (one) {  // the chunk is in registers: one batch
+      u32 dig = has1 ? (u32)((k1 >> shift) & 255u) : (256u + (u32)lane);
       u32 peers = __match_any_sync(FULL, dig);
       u32 rk = __popc(peers & ((1u << lane) - 1u));
-      if (valid && rk == 0) wc[wid][dig] = __popc(peers);
+      if (has1 && rk == 0) wc[wid][dig] = __popc(peers);
+      __syncthreads();
+      if (tid < 256) {
+        u32 acc = 0;
+        for (int q = 0; q < 32; ++q) {
+          u32 x = wc[q][tid];
+          wc[q][tid] = acc;
+          acc += x;
+        }
+      }
+      __syncthreads();
+      if (has1) {
+        u32 pos = off[dig] + wc[wid][dig] + rk;
+        kout[pos] = k1;
+        vout[pos] = v1;
+      }
+    }
+    // longer chunks: batches of LSD_B x 1024 entries; warp w ranks the LSD_B
+    // groups of 32 consecutive entries [base + (w*LSD_B + j)*32, ...) in order
+    // with running per-warp digit counts, so one column scan over the warps
+    // (and four barriers) serve 4096 entries instead of 1024
+    for (int base = s; base < e && !seg && !one; base += LSD_B * 1024) {
+      u64 bk[LSD_B];
+      u32 bv[LSD_B], br[LSD_B];
+#pragma unroll
+      for (int j = 0; j < LSD_B; ++j) {  // every load in flight first
+        const int i = base + (wid * LSD_B + j) * 32 + lane;
+        bk[j] = 0;
+        bv[j] = 0;
+        if (i < e) {
+          bk[j] = rawp ? (u64)(asc ? raw[i] : mr - raw[i]) : kin[i];
+          bv[j] = rawp ? (u32)i : vin[i];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < LSD_B; ++j) {
+        const int i = base + (wid * LSD_B + j) * 32 + lane;
+        const bool valid = i < e;
+        const u32 dig = valid ? (u32)((bk[j] >> shift) & 255u) : (256u + (u32)lane);
+        const u32 peers = __match_any_sync(FULL, dig);
+        const int leader = __ffs(peers) - 1;
+        u32 b0 = 0;
+        if (valid && lane == leader) {
+          b0 = wc[wid][dig];
+          wc[wid][dig] = b0 + __popc(peers);
+        }
+        b0 = __shfl_sync(FULL, b0, leader);
+        __syncwarp();
+        br[j] = valid ? ((dig << 16) | (b0 + __popc(peers & ((1u << lane) - 1u)))) : 0xffffffffu;
+      }
       __syncthreads();
       if (tid < 256) {
         u32 acc = 0;
@@ -1826,10 +1865,13 @@ __device__ int lsd_grid_sort(Lsd L, LsdView v, LsdArgs a, int npass, u32 (*wc)[2
         tt[tid] = acc;
       }
       __syncthreads();
-      if (valid) {
-        u32 pos = off[dig] + wc[wid][dig] + rk;
-        kout[pos] = k;
-        vout[pos] = val;
+#pragma unroll
+      for (int j = 0; j < LSD_B; ++j) {
+        if (br[j] == 0xffffffffu) continue;
+        const u32 dg = br[j] >> 16;
+        const u32 pos = off[dg] + wc[wid][dg] + (br[j] & 0xffffu);
+        kout[pos] = bk[j];
+        vout[pos] = bv[j];
       }
       __syncthreads();
       if (tid < 256) off[tid] += tt[tid];
