@@ -76,6 +76,11 @@ struct mars_ctx {
   static constexpr int NGRAPH = 4;
   static constexpr int NKEY = 11;
   cudaGraphExec_t graph_exec[NGRAPH] = {};
+  // the captured graph (kept: its k_work_init node takes each step's input
+  // as a kernel parameter, cudaGraphExecKernelNodeSetParams before a launch)
+  cudaGraph_t graph_g[NGRAPH] = {};
+  cudaGraphNode_t init_node[NGRAPH] = {};
+  cudaKernelNodeParams init_params[NGRAPH] = {};
   long long graph_key[NGRAPH][NKEY] = {};
   int graph_launches[NGRAPH] = {};
   unsigned long long graph_used[NGRAPH] = {};
@@ -520,6 +525,8 @@ int mars_destroy(mars_ctx* ctx) {
     if (e) cudaEventDestroy(e);
   for (auto& g : ctx->graph_exec)
     if (g) cudaGraphExecDestroy(g);
+  for (auto& g : ctx->graph_g)
+    if (g) cudaGraphDestroy(g);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->ev_head) cudaEventDestroy(ctx->ev_head);
@@ -897,6 +904,15 @@ static LaunchArgs launch_args(mars_ctx* ctx, const mars_step_in* in) {
   return a;
 }
 
+// one cached step graph dropped (exec, the captured graph it came from)
+static void drop_graph(mars_ctx* ctx, int i) {
+  if (ctx->graph_exec[i]) cudaGraphExecDestroy(ctx->graph_exec[i]);
+  if (ctx->graph_g[i]) cudaGraphDestroy(ctx->graph_g[i]);
+  ctx->graph_exec[i] = nullptr;
+  ctx->graph_g[i] = nullptr;
+  ctx->init_node[i] = nullptr;
+}
+
 int mars_step_enqueue(mars_ctx* ctx, const mars_step_in* in) {
   if (!ctx || !in) return MARS_ERR_ARG;
   if (in->control_due && ctx->cfg.policy != POL_MARS)  // PolicyBase.uses_admission_control
@@ -931,10 +947,7 @@ int mars_step_enqueue(mars_ctx* ctx, const mars_step_in* in) {
       }
       if (ctx->graph_used[i] < ctx->graph_used[gi]) gi = i;
     }
-    if (ctx->graph_exec[gi]) {
-      cudaGraphExecDestroy(ctx->graph_exec[gi]);
-      ctx->graph_exec[gi] = nullptr;
-    }
+    drop_graph(ctx, gi);
     cudaGraph_t g = nullptr;
     if (ctx->stream == nullptr || ctx->stream == cudaStreamLegacy ||
         ctx->stream == cudaStreamPerThread)
@@ -947,10 +960,37 @@ int mars_step_enqueue(mars_ctx* ctx, const mars_step_in* in) {
       return fail(ctx, MARS_ERR_CUDA, "graph capture failed: %s", cudaGetErrorString(ce));
     }
     CK(cudaGraphInstantiate(&ctx->graph_exec[gi], g, 0));
-    cudaGraphDestroy(g);
+    ctx->graph_g[gi] = g;
+    // the step head's node: this step's input goes in as its parameter
+    size_t nn = 0;
+    CK(cudaGraphGetNodes(g, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    CK(cudaGraphGetNodes(g, nodes.data(), &nn));
+    for (size_t i = 0; i < nn; ++i) {
+      cudaGraphNodeType ty;
+      CK(cudaGraphNodeGetType(nodes[i], &ty));
+      if (ty != cudaGraphNodeTypeKernel) continue;
+      cudaKernelNodeParams kp;
+      CK(cudaGraphKernelNodeGetParams(nodes[i], &kp));
+      if (kp.func == mars_work_init_fn()) {
+        ctx->init_node[gi] = nodes[i];
+        ctx->init_params[gi] = kp;
+      }
+    }
+    if (!ctx->init_node[gi]) return fail(ctx, MARS_ERR_CUDA, "step graph without its head node");
     memcpy(ctx->graph_key[gi], key, sizeof key);
   }
   ctx->graph_used[gi] = ++ctx->graph_clock;
+  {
+    cudaKernelNodeParams kp = ctx->init_params[gi];
+    Work* w = ctx->work;
+    mars_step_in v = *ctx->h_in;
+    const mars_scalars* sc = ctx->sc;
+    void* args[] = {&w, &v, &sc};
+    kp.kernelParams = args;
+    kp.extra = nullptr;
+    CK(cudaGraphExecKernelNodeSetParams(ctx->graph_exec[gi], ctx->init_node[gi], &kp));
+  }
   CK(cudaGraphLaunch(ctx->graph_exec[gi], ctx->stream));
   ctx->last_launches = ctx->graph_launches[gi];
   return MARS_OK;
@@ -983,11 +1023,7 @@ int mars_set_config(mars_ctx* ctx, const mars_config* hcfg) {
   CK(cudaSetDevice(ctx->device));
   CK(cudaStreamSynchronize(ctx->stream));
   // the captured step graphs carry the old configuration as kernel parameters
-  for (auto& g : ctx->graph_exec)
-    if (g) {
-      cudaGraphExecDestroy(g);
-      g = nullptr;
-    }
+  for (int i = 0; i < mars_ctx::NGRAPH; ++i) drop_graph(ctx, i);
   memset(ctx->graph_key, 0, sizeof ctx->graph_key);
   ctx->hcfg = *hcfg;
   ctx->cfg = make_cfg(*hcfg);
@@ -1725,11 +1761,7 @@ int mars_kv_capture(mars_ctx* ctx, int on) {
     k.cap = nullptr;
   }
   // the step graphs carry the Kv struct as a kernel parameter
-  for (auto& g : ctx->graph_exec)
-    if (g) {
-      cudaGraphExecDestroy(g);
-      g = nullptr;
-    }
+  for (int i = 0; i < mars_ctx::NGRAPH; ++i) drop_graph(ctx, i);
   memset(ctx->graph_key, 0, sizeof ctx->graph_key);
   return MARS_OK;
 }

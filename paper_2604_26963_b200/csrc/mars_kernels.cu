@@ -4081,28 +4081,23 @@ __global__ void k_flush(u8* p, i64 n, u32 salt) {
     q[i] = (u32)i ^ salt;
 }
 
-// Step head in one node: zero the work area, take this step's inputs
-// straight from the pinned host copy (mapped, UVA: a ~100-byte PCIe read, no
-// separate memset / memcpy graph nodes) and seed the min/max accumulators.
-// The step's work area: zeroed (16-byte stores), the step input copied from
-// its mapped pinned host copy and the pre-step scalars the early pack needs
-// taken -- every load issued before the zeroing and stored after it, so the
-// PCIe round trip of the host read overlaps the zeroing.
-__global__ void __launch_bounds__(1024) k_work_init(Work* w, const mars_step_in* h_in,
+// Step head in one node: zero the work area, store this step's input and
+// seed the min/max accumulators.  The input arrives as a by-value kernel
+// parameter (the graph's node parameters are set before each launch,
+// cudaGraphExecKernelNodeSetParams): no PCIe round trip to a mapped host
+// copy (round 1-2 read it over PCIe: ~2 us on the step's critical path),
+// no memcpy node.  The pre-step scalars the early pack needs are taken
+// before the zeroing, stored after it.
+__global__ void __launch_bounds__(1024) k_work_init(Work* w, const mars_step_in in,
                                                    const mars_scalars* sc) {
   PTIME(32);
   // k_scan may launch now: it waits (griddepcontrol.wait) for this grid's
   // completion before touching the work area
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   static_assert(sizeof(Work) % 16 == 0, "Work is zeroed in 16-byte words");
-  static_assert(sizeof(mars_step_in) % 4 == 0 && sizeof(mars_step_in) / 4 <= 1024,
-                "step_in is a few words");
-  constexpr int NIN = (int)(sizeof(mars_step_in) / 4);
-  unsigned int in_word = 0;
   int pre[5] = {0, 0, 0, 0, 0};
   long long pre_q = 0;
-  if (threadIdx.x < NIN) in_word = ((const volatile unsigned int*)h_in)[threadIdx.x];
-  if (threadIdx.x == 32) {  // (another warp than the host read's)
+  if (threadIdx.x == 32) {
     pre[0] = sc->cpu_overloaded;
     pre[1] = sc->cpu_high_streak;
     pre[2] = sc->cpu_low_streak;
@@ -4115,7 +4110,7 @@ __global__ void __launch_bounds__(1024) k_work_init(Work* w, const mars_step_in*
   const uint4 z = make_uint4(0, 0, 0, 0);
   for (size_t i = threadIdx.x; i < n16; i += blockDim.x) p[i] = z;
   __syncthreads();
-  if (threadIdx.x < NIN) ((unsigned int*)&w->in)[threadIdx.x] = in_word;
+  if (threadIdx.x == 0) w->in = in;  // (constant-bank loads, no local copy)
   if (threadIdx.x < 12) (&w->ref_gand[0][0][0])[threadIdx.x] = ~0ull;
   if (threadIdx.x == 0) {
     w->tmin_win = 0xffffffffu;
@@ -4414,7 +4409,7 @@ int mars_enqueue_step(const LaunchArgs* a) {
     // ---- head: reset, k_scan (+ sharded: export the local admission list)
     if (a->prof)
       for (int k = 0; k < MARS_NUM_KTIMES; ++k) a->prof_used[k] = 0;
-    k_work_init<<<1, 1024, 0, s>>>(a->work, a->host_in, a->sc);
+    k_work_init<<<1, 1024, 0, s>>>(a->work, *a->host_in, a->sc);
     lchk("k_work_init");
     launches++;
     int scan_sms = nsm;
@@ -4596,6 +4591,8 @@ int mars_enqueue_flush(cudaStream_t s, u8* p, i64 n, u32 salt) {
 // Every kernel of this file loaded now (CUDA loads modules lazily by default):
 // a kernel first launched while the walk spins on the control plane's flag
 // must not wait on its own loading (which can wait for the device).
+const void* mars_work_init_fn() { return (const void*)k_work_init; }
+
 int mars_kernels_preload() {
   cudaFuncAttributes fa;
   const void* fns[] = {(const void*)k_advance, (const void*)k_build_global_queue,

@@ -38,6 +38,8 @@ struct LaunchArgs {
 
 int mars_kernels_init();
 int mars_kernels_preload();
+// the step head kernel (its graph node takes each step's input as a parameter)
+const void* mars_work_init_fn();
 #define SCATTER_MAX_COLS 32
 struct ScatterCols {  // the columns of one upsert (k_scatter_cols)
   int n;

@@ -163,8 +163,9 @@ class ShardedEngine:
         all-gather, phase 2 -- as ONE CUDA graph on the replica's stream
         (torch.cuda.graph captures the collectives; the library's kernels are
         stream-ordered launches with no host synchronisation).  ``replay``
-        then launches it; ``si`` is the step the graph repeats (its host copy
-        is read by the graph's first kernel at every replay)."""
+        then launches it; ``si`` is the step the graph repeats (the step
+        input is a by-value parameter of the graph's head kernel, fixed at
+        capture: capture again for another input)."""
         import torch
 
         si.mode |= N.MODE_SHARDED
