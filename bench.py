@@ -712,7 +712,7 @@ def main():
     qcap = max(len(snap.queue), 1)
     qlens = [len(snap.queue)]
     if dist is not None:
-        # the exchange buffers (1 + 2 x queue capacity words) must have the
+        # the exchange buffers (1 + queue capacity words) must have the
         # same size on every rank: size them by the longest shard list
         ql = torch.tensor([len(snap.queue)], dtype=torch.int64, device="cuda")
         allq = [torch.zeros_like(ql) for _ in range(world)]

@@ -378,8 +378,10 @@ int mars_host_link_peak(mars_ctx* ctx, int64_t bytes, int reps, double* d2h_gbs,
  * replicas; S1/S2/S4/S5 replica-local, the control plane global.
  * A step is mars_step_phase(1) -> all-reduce(sum) of the XC_N int64 counters
  * at `xc` -> all-gather of `send_words` uint64 from `xsend` into `xrecv`
- * (rank-major) -> mars_step_phase(2) -> mars_step_fetch.  The collectives
- * are the caller's (NCCL through torch.distributed), on the same stream. */
+ * (rank-major; word 0 the entry count, then one gpos<<32 | req<<1 | long
+ * word per local admission entry) -> mars_step_phase(2) -> mars_step_fetch.
+ * The collectives are the caller's (NCCL through torch.distributed), on the
+ * same stream. */
 int mars_shard_init(mars_ctx* ctx, int world, int rank);
 int mars_shard_buffers(mars_ctx* ctx, void** xc, void** xsend, void** xrecv, int64_t* send_words);
 /* global list positions of the local admission entries (dense over the union) */

@@ -1182,7 +1182,7 @@ int mars_shard_init(mars_ctx* ctx, int world, int rank) {
   x.world = world;
   x.rank = rank;
   x.cap = ctx->max_queue;
-  const i64 words = 1 + 2 * x.cap;
+  const i64 words = 1 + x.cap;  // count, then one word per entry
   CK(cudaMalloc((void**)&x.xc, XC_N * 8));
   CK(cudaMemset(x.xc, 0, XC_N * 8));
   CK(cudaMalloc((void**)&x.xsend, words * 8));
@@ -1211,7 +1211,7 @@ int mars_shard_buffers(mars_ctx* ctx, void** xc, void** xsend, void** xrecv, int
   if (xc) *xc = ctx->x.xc;
   if (xsend) *xsend = ctx->x.xsend;
   if (xrecv) *xrecv = ctx->x.xrecv;
-  if (send_words) *send_words = 1 + 2 * ctx->x.cap;
+  if (send_words) *send_words = 1 + ctx->x.cap;
   return MARS_OK;
 }
 

@@ -89,8 +89,8 @@ struct Queue {
 #define XQ_NONE 0xffffffffu
 struct Xchg {
   i64* xc;            // [XC_N] local, then (after the all-reduce) global sums
-  u64* xsend;         // [1 + cap] : header count, then (gpos<<32 | req<<1 | long, row) pairs
-  u64* xrecv;         // [world][1 + cap] pairs
+  u64* xsend;         // [1 + cap] : header count, then one gpos<<32 | req<<1 | long per entry
+  u64* xrecv;         // [world][1 + cap]
   u32* gq_row;        // global queue by gpos: own local row or XQ_NONE
   i32* gq_req;
   u8* gq_lng;

@@ -2523,11 +2523,11 @@ __global__ void k_export_queue(Queue Q, const i32* qsel_p, mars_scalars* sc, Xch
     n = x.cap;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) x.xsend[0] = (u64)n;
-  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    u64 key = ((u64)PICK2(Q.gpos, sel)[i] << 32) | ((u64)(u32)PICK2(Q.req, sel)[i] << 1) | (u64)(PICK2(Q.lng, sel)[i] & 1);
-    x.xsend[1 + 2 * i] = key;
-    x.xsend[2 + 2 * i] = (u64)PICK2(Q.row, sel)[i];
-  }
+  // one 8-byte word per entry: the row stays home (only the owner needs it;
+  // k_build_global_queue takes it from the local list, entry k <-> word k)
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    x.xsend[1 + i] = ((u64)PICK2(Q.gpos, sel)[i] << 32) |
+                     ((u64)(u32)PICK2(Q.req, sel)[i] << 1) | (u64)(PICK2(Q.lng, sel)[i] & 1);
 }
 
 // all-reduced counters -> pooled telemetry; refresh_pressure on the pooled view
@@ -2546,9 +2546,11 @@ __global__ void k_global_control(Cfg c, Work* w, mars_scalars* sc, Xchg x) {
     refresh_pressure(c, sc, w->in.worker_slots, w->adm_usage);
 }
 
-// all-gathered entries -> the global list indexed by global position
-__global__ void k_build_global_queue(Work* w, Xchg x) {
-  const i64 stride1 = 1 + 2 * x.cap;
+// all-gathered entries -> the global list indexed by global position (this
+// replica's own entries with their rows from the local list)
+__global__ void k_build_global_queue(Work* w, Xchg x, Queue Q, const i32* qsel_p) {
+  const i64 stride1 = 1 + x.cap;
+  const u32* own_row = PICK2(Q.row, *qsel_p);
   const i64 total = (i64)x.world * x.cap;
   const i64 qlen = w->qlen;
   for (i64 f = (i64)blockIdx.x * blockDim.x + threadIdx.x; f < total;
@@ -2556,7 +2558,7 @@ __global__ void k_build_global_queue(Work* w, Xchg x) {
     i64 g = f / x.cap, k = f % x.cap;
     i64 cnt = (i64)x.xrecv[g * stride1];
     if (k >= cnt) continue;
-    u64 key = x.xrecv[g * stride1 + 1 + 2 * k];
+    u64 key = x.xrecv[g * stride1 + 1 + k];
     u32 gp = (u32)(key >> 32);
     if ((i64)gp >= qlen) {
       w->status |= ST_BAD_INPUT;
@@ -2565,7 +2567,7 @@ __global__ void k_build_global_queue(Work* w, Xchg x) {
     i32 rq = (i32)((key >> 1) & 0x7fffffffu);
     x.gq_req[gp] = rq;
     x.gq_lng[gp] = (u8)(key & 1);
-    x.gq_row[gp] = (g == x.rank) ? (u32)x.xrecv[g * stride1 + 2 + 2 * k] : XQ_NONE;
+    x.gq_row[gp] = (g == x.rank) ? own_row[k] : XQ_NONE;
     // statistics of the union list for pack_queue's mode (pack_small_cta)
     if (key & 1) atomicAdd(&w->tab_long_q, 1);
     atomicMax(&w->tab_max_req, rq);
@@ -4449,7 +4451,7 @@ int mars_enqueue_step(const LaunchArgs* a) {
   // ---- tail (sharded: after the counter all-reduce and the list all-gather)
   if (sharded) {
     k_global_control<<<1, 32, 0, s>>>(a->cfg, a->work, a->sc, a->x);
-    k_build_global_queue<<<nsm, 256, 0, s>>>(a->work, a->x);
+    k_build_global_queue<<<nsm, 256, 0, s>>>(a->work, a->x, a->queue, a->qsel);
     lchk("k_global_control / k_build_global_queue");
     launches += 2;
   }

@@ -16,8 +16,9 @@ only exchange, once per step:
    replica admits its own winners and keeps its own residual (new dense global
    positions), then the replica-local plan.
 
-Wire format of one admission entry (two uint64): ``gpos << 32 | req << 1 |
-is_long`` and the local row.  ``xsend[0]`` is the entry count.
+Wire format of one admission entry: ONE uint64, ``gpos << 32 | req << 1 |
+is_long``; ``xsend[0]`` is the entry count.  The row stays home: only its
+owner needs it, and entry k of the owner's list is word k of its block.
 Semantics and oracle: ``oracle/multi.py``.
 """
 
@@ -42,39 +43,43 @@ def interleaved_gpos(lengths):
     return [[pos[(k, g)] for k in range(n)] for g, n in enumerate(lengths)]
 
 
-def encode_queue(gpos, req, is_long, rows, cap: int) -> np.ndarray:
-    """Host restatement of k_export_queue's wire format (1 + 2*cap uint64)."""
+XQ_NONE = 0xFFFFFFFF  # another replica's entry: its row is not sent
+
+
+def encode_queue(gpos, req, is_long, cap: int) -> np.ndarray:
+    """Host restatement of k_export_queue's wire format (1 + cap uint64)."""
     n = len(gpos)
     if n > cap:
         raise ValueError("queue larger than the exchange capacity")
-    buf = np.zeros(1 + 2 * cap, np.uint64)
+    buf = np.zeros(1 + cap, np.uint64)
     buf[0] = n
-    key = (np.asarray(gpos, np.uint64) << np.uint64(32)) | \
+    buf[1:1 + n] = (np.asarray(gpos, np.uint64) << np.uint64(32)) | \
         (np.asarray(req, np.uint64) << np.uint64(1)) | (np.asarray(is_long, np.uint64) & np.uint64(1))
-    buf[1:1 + 2 * n:2] = key
-    buf[2:2 + 2 * n:2] = np.asarray(rows, np.uint64)
     return buf
 
 
-def decode_gathered(recv: np.ndarray, world: int, cap: int, rank: int):
+def decode_gathered(recv: np.ndarray, world: int, cap: int, rank: int, own_rows):
     """Host restatement of k_build_global_queue: the union list by global
-    position -> (req, is_long, owner, row) arrays of length sum(counts)."""
-    words = 1 + 2 * cap
+    position -> (req, is_long, owner, row) arrays of length sum(counts); row
+    is this rank's local row for its own entries (``own_rows[k]`` for its
+    k-th entry) and XQ_NONE for the others'."""
+    words = 1 + cap
     recv = np.asarray(recv, np.uint64).reshape(world, words)
     counts = recv[:, 0].astype(np.int64)
     q = int(counts.sum())
     req = np.zeros(q, np.int64)
     lng = np.zeros(q, np.uint8)
     owner = np.zeros(q, np.int64)
-    row = np.zeros(q, np.int64)
+    row = np.full(q, XQ_NONE, np.int64)
     for g in range(world):
         n = int(counts[g])
-        key = recv[g, 1:1 + 2 * n:2]
+        key = recv[g, 1:1 + n]
         gp = (key >> np.uint64(32)).astype(np.int64)
         req[gp] = ((key >> np.uint64(1)) & np.uint64(0x7FFFFFFF)).astype(np.int64)
         lng[gp] = (key & np.uint64(1)).astype(np.uint8)
         owner[gp] = g
-        row[gp] = recv[g, 2:2 + 2 * n:2].astype(np.int64)
+        if g == rank:
+            row[gp] = np.asarray(own_rows, np.int64)[:n]
     return req, lng, owner, row
 
 

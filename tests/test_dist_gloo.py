@@ -21,7 +21,7 @@ from oracle import admission as oa
 from oracle import core as oc
 from oracle.multi import run_multi_step
 from oracle.snapshot_step import ToolCounts, World
-from paper_2604_26963_b200.dist import (COUNTERS, decode_gathered, encode_queue, exchange,
+from paper_2604_26963_b200.dist import (COUNTERS, XQ_NONE, decode_gathered, encode_queue, exchange,
                                         interleaved_gpos)
 from paper_2604_26963_b200.snapshot import snapshot_shard, snapshot_v1
 
@@ -58,10 +58,10 @@ def _worker(rank, port, out, kind="independent"):
     q = snap.queue
     cap = 2048
     send = torch.from_numpy(encode_queue(gpos[rank], snap.cols["req_blocks"][q],
-                                         (snap.cols["flags"][q] & 16) != 0, q, cap).view(np.int64))
+                                         (snap.cols["flags"][q] & 16) != 0, cap).view(np.int64))
     recv = torch.zeros(WORLD * send.numel(), dtype=torch.int64)
     exchange(xc[:len(COUNTERS)], send, recv, None)
-    req, lng, owner, row = decode_gathered(recv.numpy().view(np.uint64), WORLD, cap, rank)
+    req, lng, owner, row = decode_gathered(recv.numpy().view(np.uint64), WORLD, cap, rank, q)
     # global admission over the union list with pooled telemetry
     avail, total, active = int(xc[0]), int(xc[1]), int(xc[2])
     T = oa.Counters(total)
@@ -98,6 +98,8 @@ def test_two_rank_exchange_reproduces_the_sharded_oracle(kind):
     mp.spawn(_worker, args=(_free_port(), out, kind), nprocs=WORLD, join=True)
     for rank in range(WORLD):
         got, qlen, w_adm = out[rank]
-        assert got == [tuple(x) for x in want["admitted_global"]]
+        # the same winners in the same order on every rank; a rank knows the
+        # rows of its own entries only (the wire carries no rows)
+        assert got == [(o, r if o == rank else XQ_NONE) for o, r in want["admitted_global"]]
         assert qlen == sum(len(s.queue) for s in snaps)
         assert w_adm == want["w_adm"]
