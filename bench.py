@@ -521,7 +521,7 @@ def workload_config(sessions: int, world: int) -> dict:
             "sessions": sessions, "pool": "headroom", "mix": "A",
             "parallelism": "1 replica" if world == 1 else
             f"{world} replicas: NCCL all-reduce of probe counters + all-gather of "
-            "top-slots admission candidates",
+            "every admission entry (8 B each)",
             "l2": "flushed before every timed step (512 MiB scratch write); state restored "
                   "from a device checkpoint (untimed)"}
 
