@@ -12,6 +12,8 @@
 #include <vector>
 
 #include "mars_internal.cuh"
+
+#define UP_ARENA (256 << 10)  // small upserts: rows + columns in one pinned copy
 #include "mars_launch.h"
 
 namespace {
@@ -34,6 +36,8 @@ struct mars_ctx {
   bool own_stream = true;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_head = nullptr, ev_pack = nullptr;
   cudaEvent_t ev_kvx = nullptr;
+  cudaEvent_t ev_up = nullptr;         // the small-upsert arena's last copy
+  unsigned char* h_up = nullptr;       // pinned arena of small upserts (UP_ARENA bytes)
   int pack_ctas = 20;
   mars_config hcfg;
   Cfg cfg;
@@ -283,6 +287,8 @@ int mars_create(const mars_config* hcfg, int device, int64_t max_rows, int64_t m
   CK(cudaEventCreateWithFlags(&ctx->ev_head, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&ctx->ev_pack, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&ctx->ev_kvx, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ctx->ev_up, cudaEventDisableTiming));
+  CK(cudaMallocHost((void**)&ctx->h_up, UP_ARENA));
   {
     const char* e = getenv("MARS_PACK_CTAS");  // tuning knob: 0 disables the early pack
     if (e) ctx->pack_ctas = atoi(e);
@@ -532,6 +538,8 @@ int mars_destroy(mars_ctx* ctx) {
   if (ctx->ev_head) cudaEventDestroy(ctx->ev_head);
   if (ctx->ev_pack) cudaEventDestroy(ctx->ev_pack);
   if (ctx->ev_kvx) cudaEventDestroy(ctx->ev_kvx);
+  if (ctx->ev_up) cudaEventDestroy(ctx->ev_up);
+  if (ctx->h_up) cudaFreeHost(ctx->h_up);
   if (ctx->side2) cudaStreamDestroy(ctx->side2);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->side) cudaStreamDestroy(ctx->side);
@@ -572,7 +580,6 @@ int mars_upsert_rows(mars_ctx* ctx, int64_t n, const int64_t* rows, const mars_c
       if (rows[i] < 0 || rows[i] >= ctx->max_rows)
         return fail(ctx, MARS_ERR_CAPACITY, "row %lld out of range", (long long)rows[i]);
     if (n > ctx->max_rows) return MARS_ERR_CAPACITY;
-    CK(cudaMemcpyAsync(ctx->d_rows, rows, (size_t)n * 8, cudaMemcpyHostToDevice, ctx->stream));
     // every given column staged side by side, then ONE scatter launch; a
     // batch larger than the staging buffer goes column by column
     ScatterCols L;
@@ -593,6 +600,32 @@ int mars_upsert_rows(mars_ctx* ctx, int64_t n, const int64_t* rows, const mars_c
       ++L.n;
       off += (size_t)n * cs.esz;
     }
+    const size_t rows_off = (off + 15) & ~(size_t)15;
+    const size_t small = rows_off + (size_t)n * 8;
+    if (fits && small <= UP_ARENA && small <= (size_t)ctx->alloc_rows * 8) {
+      // a small batch (the drop-in's per-tick writes): rows and columns
+      // packed into a pinned host arena, ONE copy, ONE scatter, no wait --
+      // the caller's arrays are copied before the return, the arena is
+      // reused only once its previous copy completed (ev_up)
+      CK(cudaEventSynchronize(ctx->ev_up));
+      int k = 0;
+      for (auto& cs : ctx->cols) {
+        const void* hp = *(void* const*)((const char*)cols + cs.host_off);
+        if (!hp) continue;
+        memcpy(ctx->h_up + L.off[k], hp, (size_t)n * cs.esz);
+        ++k;
+      }
+      memcpy(ctx->h_up + rows_off, rows, (size_t)n * 8);
+      CK(cudaMemcpyAsync(ctx->d_stage, ctx->h_up, small, cudaMemcpyHostToDevice, ctx->stream));
+      CK(cudaEventRecord(ctx->ev_up, ctx->stream));
+      int rc = mars_enqueue_scatter_cols(ctx->stream, L, ctx->d_stage,
+                                         (const i64*)(ctx->d_stage + rows_off), n);
+      if (rc) return fail(ctx, MARS_ERR_CUDA, "scatter: %s", cudaGetErrorString((cudaError_t)rc));
+      for (int64_t i = 0; i < n; ++i)
+        if (rows[i] + 1 > ctx->n_rows) ctx->n_rows = rows[i] + 1;
+      return MARS_OK;
+    }
+    CK(cudaMemcpyAsync(ctx->d_rows, rows, (size_t)n * 8, cudaMemcpyHostToDevice, ctx->stream));
     if (fits) {
       int k = 0;
       for (auto& cs : ctx->cols) {
