@@ -36,7 +36,7 @@ extern "C" {
 #define MARS_ERR_CAPACITY 3
 #define MARS_ERR_ARG 4
 
-#define MARS_ABI_VERSION 6
+#define MARS_ABI_VERSION 7
 
 /* phase codes: agentsched/engine.py:250-256 */
 #define MARS_WAITING_ADMISSION 0
@@ -242,6 +242,16 @@ int mars_set_stream(mars_ctx* ctx, void* cuda_stream);
 int mars_set_rows(mars_ctx* ctx, int64_t n_rows);                 /* live row count */
 int mars_upsert_rows(mars_ctx* ctx, int64_t n, const int64_t* rows, const mars_cols* cols);
 int mars_read_rows(mars_ctx* ctx, int64_t n, const int64_t* rows, mars_cols* out);   /* sync */
+/* Zero-copy input staging for whole-table uploads: a pinned host arena laid
+ * out like the device table (one slab, columns grouped by element size).
+ * *base / *bytes describe it; cols (optional) receives each column's host
+ * address (max_rows rows).  Allocated on the first call, owned by the context. */
+int mars_input_arena(mars_ctx* ctx, void** base, int64_t* bytes, mars_cols* cols);
+/* rows [0, n) of the columns in `mask` (bit i = the i-th mars_cols field)
+ * from the input arena to the table: one pitched copy per run of adjacent
+ * columns of one element size (3 copies for a default step's 17 columns,
+ * instead of 17); sync (the arena may be rewritten after the return) */
+int mars_upsert_arena(mars_ctx* ctx, int64_t n, uint64_t mask);
 /* admission list (sim.py:132 admission_queue; control.py:190 persistent order) */
 int mars_set_queue(mars_ctx* ctx, int64_t n, const uint32_t* rows, const int32_t* req_blocks,
                    const uint8_t* is_long);

@@ -129,6 +129,8 @@ _SIGS = {
     "mars_set_stream": (i32, [C.c_void_p, C.c_void_p]),
     "mars_set_rows": (i32, [C.c_void_p, i64]),
     "mars_upsert_rows": (i32, [C.c_void_p, i64, C.c_void_p, P(MarsCols)]),
+    "mars_input_arena": (i32, [C.c_void_p, P(C.c_void_p), P(i64), P(MarsCols)]),
+    "mars_upsert_arena": (i32, [C.c_void_p, i64, C.c_uint64]),
     "mars_read_rows": (i32, [C.c_void_p, i64, C.c_void_p, P(MarsCols)]),
     "mars_set_queue": (i32, [C.c_void_p, i64, C.c_void_p, C.c_void_p, C.c_void_p]),
     "mars_get_queue": (i32, [C.c_void_p, i64, C.c_void_p, P(i64)]),

@@ -23,6 +23,7 @@ struct ColSpec {
   void** dev;       // address of the device pointer inside Tab
   int esz;
   void* ckpt;       // checkpoint copy
+  size_t slab_off;  // the column's offset in the table slab (and the input arena)
 };
 
 }  // namespace
@@ -56,6 +57,12 @@ struct mars_ctx {
   Work* h_work = nullptr;
   mars_scalars* h_sc = nullptr;
   unsigned char* h_out = nullptr;  // pinned output arena
+  // the session table: every column in ONE device slab, grouped by element
+  // size (u8 x5 | f64/i64 x5 | 4-byte x10, each column alloc_rows long), and
+  // a pinned host input arena with the same layout (mars_input_arena)
+  unsigned char* slab = nullptr;
+  size_t slab_bytes = 0;
+  unsigned char* h_in_arena = nullptr;
   OutList out_list{};              // the fetch's pending array copies
   size_t h_out_bytes = 0;
   // device staging for row scatter/gather
@@ -303,26 +310,30 @@ int mars_create(const mars_config* hcfg, int device, int64_t max_rows, int64_t m
   Tab& t = ctx->tab;
   memset(&t, 0, sizeof t);
   t.cap = R;
-  ALLOC(t.phase, R);
-  ALLOC(t.flags, R);
-  ALLOC(t.level, R);
-  ALLOC(t.promos, R);
-  ALLOC(t.plevel, R);
-  ALLOC(t.rs, R * 8);
-  ALLOC(t.ws, R * 8);
-  ALLOC(t.dl, R * 8);
-  ALLOC(t.arr, R * 8);
-  ALLOC(t.ctx, R * 4);
-  ALLOC(t.kv, R * 4);
-  ALLOC(t.rem, R * 4);
-  ALLOC(t.pb, R * 4);
-  ALLOC(t.req, R * 4);
-  ALLOC(t.r0p, R * 4);
-  ALLOC(t.r0d, R * 4);
-  ALLOC(t.pre, R * 4);
-  ALLOC(t.served, R * 8);
-  ALLOC(t.rank, R * 4);
-  ALLOC(t.rleft, R * 4);
+  {
+    // slab order: adjacent columns of one element size form one 2D copy in
+    // mars_upsert_arena; the columns a default step does not read (arrival,
+    // served, rounds_left) close their groups
+    struct {
+      void** p;
+      int esz;
+    } lay[] = {{(void**)&t.phase, 1}, {(void**)&t.flags, 1}, {(void**)&t.level, 1},
+               {(void**)&t.promos, 1}, {(void**)&t.plevel, 1}, {(void**)&t.rs, 8},
+               {(void**)&t.ws, 8},     {(void**)&t.dl, 8},     {(void**)&t.arr, 8},
+               {(void**)&t.served, 8}, {(void**)&t.ctx, 4},    {(void**)&t.kv, 4},
+               {(void**)&t.rem, 4},    {(void**)&t.pb, 4},     {(void**)&t.req, 4},
+               {(void**)&t.r0p, 4},    {(void**)&t.r0d, 4},    {(void**)&t.pre, 4},
+               {(void**)&t.rank, 4},   {(void**)&t.rleft, 4}};
+    size_t tot = 0;
+    for (auto& l : lay) tot += (size_t)R * l.esz;
+    ALLOC(ctx->slab, tot);
+    ctx->slab_bytes = tot;
+    size_t off = 0;
+    for (auto& l : lay) {
+      *l.p = ctx->slab + off;
+      off += (size_t)R * l.esz;
+    }
+  }
   CK(cudaMemset(t.rleft, 0, R * 4));
   ALLOC(t.winpos, R * 2);
   CK(cudaMemset(t.winpos, 0xff, R * 2));
@@ -441,7 +452,9 @@ int mars_create(const mars_config* hcfg, int device, int64_t max_rows, int64_t m
   s0.w_adm = hcfg->initial_window;
   CK(cudaMemcpy(ctx->sc, &s0, sizeof s0, cudaMemcpyHostToDevice));
   // column table
-  auto add = [&](size_t off, void** dev, int esz) { ctx->cols.push_back({off, dev, esz, nullptr}); };
+  auto add = [&](size_t off, void** dev, int esz) {
+    ctx->cols.push_back({off, dev, esz, nullptr, (size_t)((unsigned char*)*dev - ctx->slab)});
+  };
   add(offsetof(mars_cols, phase), (void**)&t.phase, 1);
   add(offsetof(mars_cols, flags), (void**)&t.flags, 1);
   add(offsetof(mars_cols, level), (void**)&t.level, 1);
@@ -472,9 +485,9 @@ int mars_destroy(mars_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   Tab& t = ctx->tab;
-  void* ps[] = {t.phase, t.flags, t.level, t.promos, t.plevel, t.rs, t.ws, t.dl, t.arr, t.ctx,
-                t.kv, t.rem, t.pb, t.req, t.r0p, t.r0d, t.pre, t.served, t.rank, t.winpos};
-  for (void* p : ps) cudaFree(p);
+  cudaFree(ctx->slab);  // every table column
+  cudaFree(t.winpos);
+  if (ctx->h_in_arena) cudaFreeHost(ctx->h_in_arena);
   for (int i = 0; i < 2; ++i) {
     cudaFree(ctx->queue.row[i]);
     cudaFree(ctx->queue.req[i]);
@@ -649,6 +662,49 @@ int mars_upsert_rows(mars_ctx* ctx, int64_t n, const int64_t* rows, const mars_c
     for (int64_t i = 0; i < n; ++i)
       if (rows[i] + 1 > ctx->n_rows) ctx->n_rows = rows[i] + 1;
   }
+  CK(cudaStreamSynchronize(ctx->stream));
+  return MARS_OK;
+}
+
+int mars_input_arena(mars_ctx* ctx, void** base, int64_t* bytes, mars_cols* cols) {
+  if (!ctx || !base || !bytes) return MARS_ERR_ARG;
+  CK(cudaSetDevice(ctx->device));
+  if (!ctx->h_in_arena) {
+    CK(cudaMallocHost((void**)&ctx->h_in_arena, ctx->slab_bytes));
+    memset(ctx->h_in_arena, 0, ctx->slab_bytes);
+  }
+  *base = ctx->h_in_arena;
+  *bytes = (int64_t)ctx->slab_bytes;
+  if (cols)
+    for (auto& cs : ctx->cols)
+      *(void**)((char*)cols + cs.host_off) = ctx->h_in_arena + cs.slab_off;
+  return MARS_OK;
+}
+
+int mars_upsert_arena(mars_ctx* ctx, int64_t n, uint64_t mask) {
+  if (!ctx || n < 0) return MARS_ERR_ARG;
+  if (!ctx->h_in_arena) return fail(ctx, MARS_ERR_ARG, "mars_upsert_arena before mars_input_arena");
+  if (n > ctx->max_rows) return fail(ctx, MARS_ERR_CAPACITY, "upsert %lld rows", (long long)n);
+  if (n == 0 || mask == 0) return MARS_OK;
+  CK(cudaSetDevice(ctx->device));
+  // the masked columns in slab order; a run of slab-adjacent columns of one
+  // element size is one pitched copy (rows [0, n) of each)
+  std::vector<std::pair<size_t, int>> sel;  // (slab offset, esz)
+  for (size_t i = 0; i < ctx->cols.size(); ++i)
+    if (mask >> i & 1) sel.push_back({ctx->cols[i].slab_off, ctx->cols[i].esz});
+  std::sort(sel.begin(), sel.end());
+  const size_t R = (size_t)ctx->alloc_rows;
+  for (size_t i = 0; i < sel.size();) {
+    size_t j = i + 1;
+    while (j < sel.size() && sel[j].second == sel[i].second &&
+           sel[j].first == sel[j - 1].first + R * (size_t)sel[i].second)
+      ++j;
+    const size_t pitch = R * (size_t)sel[i].second;
+    CK(cudaMemcpy2DAsync(ctx->slab + sel[i].first, pitch, ctx->h_in_arena + sel[i].first, pitch,
+                         (size_t)n * sel[i].second, j - i, cudaMemcpyHostToDevice, ctx->stream));
+    i = j;
+  }
+  if (n > ctx->n_rows) ctx->n_rows = n;
   CK(cudaStreamSynchronize(ctx->stream));
   return MARS_OK;
 }

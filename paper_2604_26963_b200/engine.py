@@ -201,6 +201,35 @@ class MarsEngine:
             if n:
                 self.n_rows = max(self.n_rows, int(r.max()) + 1)
 
+    def input_arena(self) -> Dict[str, np.ndarray]:
+        """The library's pinned input arena (mars_input_arena): one writable
+        numpy view per column (``max_rows`` rows), laid out like the device
+        table, for callers that keep the whole table on the host and upload
+        it every step (``upsert_arena``)."""
+        if getattr(self, "_in_views", None) is None:
+            base, size = C.c_void_p(), C.c_int64()
+            mc = N.MarsCols()
+            self._check(self.lib.mars_input_arena(self.ctx, C.byref(base), C.byref(size),
+                                                  C.byref(mc)))
+            views = {}
+            for name, field in N.COL_FIELDS.items():
+                dt = np.dtype(COLUMNS[name])
+                addr = C.cast(getattr(mc, field), C.c_void_p).value
+                buf = (C.c_uint8 * (self.max_rows * dt.itemsize)).from_address(addr)
+                views[name] = np.frombuffer(buf, dtype=dt)
+            self._in_views = views
+        return self._in_views
+
+    def upsert_arena(self, n: int, names) -> None:
+        """Rows [0, n) of the named columns from the input arena to the table
+        (mars_upsert_arena: one pitched copy per run of adjacent columns)."""
+        mask = 0
+        for i, name in enumerate(N.COL_FIELDS):
+            if name in names:
+                mask |= 1 << i
+        self._check(self.lib.mars_upsert_arena(self.ctx, int(n), mask))
+        self.n_rows = max(self.n_rows, int(n))
+
     def read(self, names=None, rows: Optional[np.ndarray] = None) -> Dict[str, np.ndarray]:
         names = list(names or N.COL_FIELDS)
         n = self.n_rows if rows is None else len(rows)

@@ -1,9 +1,12 @@
 """Where the e2e step's time goes (1M sessions): column upload, step, fetch,
 against one contiguous pinned copy of the same bytes."""
+import os
 import statistics
+import sys
 import time
 
-import torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
 
 from paper_2604_26963_b200.engine import MarsEngine, make_config, step_columns
 from paper_2604_26963_b200.snapshot import snapshot_v1
@@ -91,3 +94,42 @@ t0 = time.perf_counter()
 for _ in range(20):
     eng.fetch(copy=False)
 print(f"  fetch(copy=False) x1 {(time.perf_counter() - t0) / 20 * 1e3:.3f} ms")
+
+
+# host-side return time of each piece (no synchronize inside): is the column
+# upload asynchronous from the host's point of view?
+def host_times(n=10):
+    out = {"upsert": [], "enqueue": [], "fetch": [], "total": []}
+    for i in range(n + 1):
+        eng.restore()
+        eng.flush_l2(512 << 20)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        eng.upsert(pinned)
+        t1 = time.perf_counter()
+        eng.enqueue(si)
+        t2 = time.perf_counter()
+        eng.fetch()
+        t3 = time.perf_counter()
+        if i:
+            out["upsert"].append((t1 - t0) * 1e3)
+            out["enqueue"].append((t2 - t1) * 1e3)
+            out["fetch"].append((t3 - t2) * 1e3)
+            out["total"].append((t3 - t0) * 1e3)
+    return {k: round(statistics.median(v), 3) for k, v in out.items()}
+
+
+print("host return times (ms):", host_times())
+# the same bytes as ONE pinned copy through the library's stream
+ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+for name, fn in (("13 column copies", lambda: eng.upsert(pinned)), ("one flat copy", raw)):
+    ts = []
+    for i in range(6):
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        fn()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if i:
+            ts.append(ev0.elapsed_time(ev1))
+    print(f"device time {name}: {statistics.median(ts):.3f} ms")

@@ -39,7 +39,7 @@ def test_library_exports_every_declared_symbol(lib):
 
 
 def test_abi_version(lib):
-    assert lib.mars_abi_version() == 6
+    assert lib.mars_abi_version() == 7
 
 
 def test_default_config_matches_reference_constants(lib):
