@@ -13,7 +13,7 @@
 
 #include "mars_internal.cuh"
 
-#define UP_ARENA (256 << 10)  // small upserts: rows + columns in one pinned copy
+#define UP_ARENA (8 << 20)  // row batches up to 8 MiB: rows + columns in one pinned copy
 #include "mars_launch.h"
 
 namespace {
