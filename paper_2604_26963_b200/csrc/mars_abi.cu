@@ -63,7 +63,6 @@ struct mars_ctx {
   unsigned char* slab = nullptr;
   size_t slab_bytes = 0;
   unsigned char* h_in_arena = nullptr;
-  OutList out_list{};              // the fetch's pending array copies
   size_t h_out_bytes = 0;
   // device staging for row scatter/gather
   unsigned char* d_stage = nullptr;
@@ -440,7 +439,8 @@ int mars_create(const mars_config* hcfg, int device, int64_t max_rows, int64_t m
   CK(cudaMallocHost((void**)&ctx->h_in, sizeof(mars_step_in)));
   CK(cudaMallocHost((void**)&ctx->h_work, sizeof(Work)));
   CK(cudaMallocHost((void**)&ctx->h_sc, sizeof(mars_scalars)));
-  ctx->h_out_bytes = (size_t)R * 48 + (size_t)Qc * 4 + (size_t)b.j_cap * 9 + 4 * WIN_MAX * 4 + WIN_MAX * 80 + 8192;
+  ctx->h_out_bytes = (size_t)OUT_HDR + (size_t)R * 48 + (size_t)Qc * 4 + (size_t)b.j_cap * 9 +
+                     4 * WIN_MAX * 4 + WIN_MAX * 80 + 8192;
   CK(cudaMallocHost((void**)&ctx->h_out, ctx->h_out_bytes));
   memset(ctx->h_in, 0, sizeof(mars_step_in));
   // scalars: empty pool of one block until mars_set_scalars
@@ -1119,35 +1119,43 @@ int mars_set_config(mars_ctx* ctx, const mars_config* hcfg) {
   return MARS_OK;
 }
 
-// place a device array in the pinned arena (copied by the one k_gather_out
-// launch of the fetch) and return its host address
-static const void* pull(mars_ctx* ctx, size_t& off, const void* dev, size_t bytes) {
-  off = (off + 15) & ~(size_t)15;
-  if (off + bytes > ctx->h_out_bytes) return nullptr;
-  void* h = ctx->h_out + off;
-  if (bytes) {
-    OutList& L = ctx->out_list;
-    if (L.n == OUT_MAX) {  // never with the fixed output set; flush and go on
-      mars_enqueue_gather_out(ctx->stream, L, ctx->h_out);
-      L.n = 0;
-    }
-    L.d[L.n++] = {dev, (unsigned long long)off, (unsigned long long)bytes};
-  }
-  off += bytes;
-  return h;
-}
-
 int mars_step_fetch(mars_ctx* ctx, mars_step_out* o) {
   if (!ctx || !o) return MARS_ERR_ARG;
-  ctx->out_list.n = 0;
   CK(cudaSetDevice(ctx->device));
-  CK(cudaMemcpyAsync(ctx->h_work, ctx->work, sizeof(Work), cudaMemcpyDeviceToHost, ctx->stream));
+  // ONE kernel behind the step writes the final Work and every output array
+  // into the mapped arena (laid out on the device from the counts), then ONE
+  // synchronize: no host round trip for the counts first
+  const Bufs& b = ctx->bufs;
+  OutSrc S;
+  {
+    const void* src[OS_N] = {b.exp_row_sorted, b.exp_blk_sorted, b.admitted, ctx->x.adm_idx,
+                             b.win_rows, b.dec_rows, b.pre_rows, b.pre_grant, b.ev_row,
+                             b.ev_kind, b.ev_blk, b.j_op, b.j_row, b.j_n, b.ret_row, b.ret_pin,
+                             b.ret_b, b.ret_c, b.ret_d, b.dec_level, b.pre_level, b.svc_pre,
+                             b.end_row, b.end_kind, b.end_blk, b.end_pin, b.end_b, b.end_c,
+                             b.end_d, b.pre_done, b.fin_row, b.fin_pin, b.fin_b, b.fin_c,
+                             b.fin_d};
+    memcpy(S.p, src, sizeof src);
+    S.ev_cap = b.ev_cap;
+    S.j_cap = b.j_cap;
+    S.coord = ctx->cfg.coord;
+  }
+  {
+    int rc = mars_enqueue_out_fold(ctx->stream, ctx->work, S, ctx->h_out,
+                                   (long long)ctx->h_out_bytes);
+    if (rc) return fail(ctx, MARS_ERR_CUDA, "fetch: %s", cudaGetErrorString((cudaError_t)rc));
+  }
   CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaGetLastError());
+  memcpy(ctx->h_work, ctx->h_out, sizeof(Work));
   const Work& w = *ctx->h_work;
+  OutLay L;
+  out_layout(w, S, (long long)ctx->h_out_bytes, &L);
+  auto at = [&](int k) -> const void* { return L.off[k] < 0 ? nullptr : ctx->h_out + L.off[k]; };
   memset(o, 0, sizeof *o);
   o->status = w.status;
   o->n_expired = w.n_exp;
-  const bool sharded = (ctx->h_in->mode & MARS_MODE_SHARDED) != 0;
+  const bool sharded = (w.in.mode & MARS_MODE_SHARDED) != 0;
   const i64 n_adm = sharded ? (i64)w.n_adm_own : w.take;
   o->n_admitted = (int32_t)n_adm;
   o->n_window = w.n_window;
@@ -1163,34 +1171,28 @@ int mars_step_fetch(mars_ctx* ctx, mars_step_out* o) {
   o->free_after_expiry = w.free_after_expiry;
   o->limit = w.limit;
   o->slots = w.slots;
-  const Bufs& b = ctx->bufs;
-  size_t off = 0;
-  o->expired_rows = (const uint32_t*)pull(ctx, off, b.exp_row_sorted, (size_t)w.n_exp * 4);
-  o->expired_blocks = (const int32_t*)pull(ctx, off, b.exp_blk_sorted, (size_t)w.n_exp * 4);
-  o->admitted_rows = (const uint32_t*)pull(ctx, off, b.admitted, (size_t)n_adm * 4);
-  const uint32_t* adm_idx = nullptr;
-  if (sharded) adm_idx = (const uint32_t*)pull(ctx, off, ctx->x.adm_idx, (size_t)n_adm * 4);
-  o->window_rows = (const uint32_t*)pull(ctx, off, b.win_rows, (size_t)w.n_window * 4);
-  o->decode_rows = (const uint32_t*)pull(ctx, off, b.dec_rows, (size_t)w.n_dec * 4);
-  o->prefill_rows = (const uint32_t*)pull(ctx, off, b.pre_rows, (size_t)w.n_pre * 4);
-  o->prefill_grants = (const int32_t*)pull(ctx, off, b.pre_grant, (size_t)w.n_pre * 4);
-  int ne = w.n_evict < b.ev_cap ? w.n_evict : (int)b.ev_cap;
-  o->evict_rows = (const uint32_t*)pull(ctx, off, b.ev_row, (size_t)ne * 4);
-  o->evict_kind = (const uint8_t*)pull(ctx, off, b.ev_kind, (size_t)ne);
-  o->evict_blocks = (const int32_t*)pull(ctx, off, b.ev_blk, (size_t)ne * 4);
-  int nj = w.n_journal < b.j_cap ? w.n_journal : (int)b.j_cap;
-  o->journal_op = (const uint8_t*)pull(ctx, off, b.j_op, (size_t)nj);
-  o->journal_row = (const uint32_t*)pull(ctx, off, b.j_row, (size_t)nj * 4);
-  o->journal_n = (const int32_t*)pull(ctx, off, b.j_n, (size_t)nj * 4);
-  o->ret_rows = (const uint32_t*)pull(ctx, off, b.ret_row, (size_t)w.n_ret * 4);
-  o->ret_pin = (const uint8_t*)pull(ctx, off, b.ret_pin, (size_t)w.n_ret);
-  o->ret_benefit = (const double*)pull(ctx, off, b.ret_b, (size_t)w.n_ret * 8);
-  o->ret_cost = (const double*)pull(ctx, off, b.ret_c, (size_t)w.n_ret * 8);
-  o->ret_deadline = (const double*)pull(ctx, off, b.ret_d, (size_t)w.n_ret * 8);
-  o->decode_level = (const uint8_t*)pull(ctx, off, b.dec_level, (size_t)w.n_dec);
-  o->prefill_level = (const uint8_t*)pull(ctx, off, b.pre_level, (size_t)w.n_pre);
-  if ((ctx->h_in->mode & MARS_MODE_SERVICE) && ctx->cfg.coord)
-    o->plan_pre_charge = (const int64_t*)pull(ctx, off, b.svc_pre, (size_t)(w.n_dec + w.n_pre) * 8);
+  o->expired_rows = (const uint32_t*)at(OS_EXP_ROW);
+  o->expired_blocks = (const int32_t*)at(OS_EXP_BLK);
+  o->admitted_rows = (const uint32_t*)at(OS_ADM);
+  const uint32_t* adm_idx = (const uint32_t*)at(OS_ADM_IDX);
+  o->window_rows = (const uint32_t*)at(OS_WIN);
+  o->decode_rows = (const uint32_t*)at(OS_DEC);
+  o->prefill_rows = (const uint32_t*)at(OS_PRE);
+  o->prefill_grants = (const int32_t*)at(OS_PRE_GRANT);
+  o->evict_rows = (const uint32_t*)at(OS_EV_ROW);
+  o->evict_kind = (const uint8_t*)at(OS_EV_KIND);
+  o->evict_blocks = (const int32_t*)at(OS_EV_BLK);
+  o->journal_op = (const uint8_t*)at(OS_J_OP);
+  o->journal_row = (const uint32_t*)at(OS_J_ROW);
+  o->journal_n = (const int32_t*)at(OS_J_N);
+  o->ret_rows = (const uint32_t*)at(OS_RET_ROW);
+  o->ret_pin = (const uint8_t*)at(OS_RET_PIN);
+  o->ret_benefit = (const double*)at(OS_RET_B);
+  o->ret_cost = (const double*)at(OS_RET_C);
+  o->ret_deadline = (const double*)at(OS_RET_D);
+  o->decode_level = (const uint8_t*)at(OS_DEC_LEVEL);
+  o->prefill_level = (const uint8_t*)at(OS_PRE_LEVEL);
+  if (L.bytes[OS_SVC_PRE]) o->plan_pre_charge = (const int64_t*)at(OS_SVC_PRE);
   o->n_finish = w.n_finish;
   o->n_window_cand = w.n_wc;
   o->n_victim_cand = w.n_vc;
@@ -1203,28 +1205,19 @@ int mars_step_fetch(mars_ctx* ctx, mars_step_out* o) {
   o->n_victim_ref = w.n_vr;
   o->n_round_end = w.n_round_end;
   o->n_done = w.n_done;
-  o->end_rows = (const uint32_t*)pull(ctx, off, b.end_row, (size_t)w.n_round_end * 4);
-  o->end_kind = (const uint8_t*)pull(ctx, off, b.end_kind, (size_t)w.n_round_end);
-  o->end_blocks = (const int32_t*)pull(ctx, off, b.end_blk, (size_t)w.n_round_end * 4);
-  o->end_pin = (const uint8_t*)pull(ctx, off, b.end_pin, (size_t)w.n_round_end);
-  o->end_benefit = (const double*)pull(ctx, off, b.end_b, (size_t)w.n_round_end * 8);
-  o->end_cost = (const double*)pull(ctx, off, b.end_c, (size_t)w.n_round_end * 8);
-  o->end_deadline = (const double*)pull(ctx, off, b.end_d, (size_t)w.n_round_end * 8);
-  o->prefill_done = (w.in.mode & MARS_MODE_ADVANCE)
-                        ? (const uint8_t*)pull(ctx, off, b.pre_done, (size_t)w.n_pre)
-                        : nullptr;
-  o->fin_rows = (const uint32_t*)pull(ctx, off, b.fin_row, (size_t)w.n_finish * 4);
-  o->fin_pin = (const uint8_t*)pull(ctx, off, b.fin_pin, (size_t)w.n_finish);
-  o->fin_benefit = (const double*)pull(ctx, off, b.fin_b, (size_t)w.n_finish * 8);
-  o->fin_cost = (const double*)pull(ctx, off, b.fin_c, (size_t)w.n_finish * 8);
-  o->fin_deadline = (const double*)pull(ctx, off, b.fin_d, (size_t)w.n_finish * 8);
-  {
-    int rc = mars_enqueue_gather_out(ctx->stream, ctx->out_list, ctx->h_out);
-    ctx->out_list.n = 0;
-    if (rc) return fail(ctx, MARS_ERR_CUDA, "fetch: %s", cudaGetErrorString((cudaError_t)rc));
-  }
-  CK(cudaStreamSynchronize(ctx->stream));
-  CK(cudaGetLastError());
+  o->end_rows = (const uint32_t*)at(OS_END_ROW);
+  o->end_kind = (const uint8_t*)at(OS_END_KIND);
+  o->end_blocks = (const int32_t*)at(OS_END_BLK);
+  o->end_pin = (const uint8_t*)at(OS_END_PIN);
+  o->end_benefit = (const double*)at(OS_END_B);
+  o->end_cost = (const double*)at(OS_END_C);
+  o->end_deadline = (const double*)at(OS_END_D);
+  o->prefill_done = (w.in.mode & MARS_MODE_ADVANCE) ? (const uint8_t*)at(OS_PRE_DONE) : nullptr;
+  o->fin_rows = (const uint32_t*)at(OS_FIN_ROW);
+  o->fin_pin = (const uint8_t*)at(OS_FIN_PIN);
+  o->fin_benefit = (const double*)at(OS_FIN_B);
+  o->fin_cost = (const double*)at(OS_FIN_C);
+  o->fin_deadline = (const double*)at(OS_FIN_D);
   if (sharded && n_adm > 1) {
     // this replica's admitted rows in global packed order
     std::vector<std::pair<uint32_t, uint32_t>> pr((size_t)n_adm);

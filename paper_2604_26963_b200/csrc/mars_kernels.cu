@@ -4051,29 +4051,38 @@ __global__ void k_retention_batch(Cfg c, i64 n, const i32* ctx, const i32* kv, i
 
 // fetch: every output array of the step into the pinned host arena in one
 // launch (blockIdx.y = array), 16-byte stores where both sides allow
-__global__ void __launch_bounds__(256) k_gather_out(OutList L, unsigned char* dst) {
-  const OutDesc D = L.d[blockIdx.y];
-  const unsigned char* src = (const unsigned char*)D.src;
-  unsigned char* out = dst + D.dst_off;
-  const unsigned long long n16 =
-      (((uintptr_t)src | (uintptr_t)out) & 15) == 0 ? D.bytes / 16 : 0;
-  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n16;
-       i += (unsigned long long)gridDim.x * blockDim.x)
-    ((uint4*)out)[i] = __ldcg((const uint4*)src + i);
-  for (unsigned long long i = n16 * 16 + (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
-       i < D.bytes; i += (unsigned long long)gridDim.x * blockDim.x)
-    out[i] = src[i];
+
+// The step's outputs into the mapped host arena, launched by the fetch behind
+// the step (no host round trip for the counts first): every CTA lays them out
+// from the final Work (out_layout) and copies its share of each array and of
+// the Work struct itself (the arena's header).
+__global__ void __launch_bounds__(256) k_out_fold(const Work* w, OutSrc S, unsigned char* dst,
+                                                  long long cap) {
+  __shared__ OutLay L;
+  if (threadIdx.x == 0) out_layout(*w, S, cap, &L);
+  __syncthreads();
+  const unsigned long long nt = (unsigned long long)gridDim.x * blockDim.x;
+  const unsigned long long t0 = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int k = 0; k <= OS_N; ++k) {
+    const unsigned char* src;
+    unsigned char* out;
+    unsigned long long bytes;
+    if (k == OS_N) {  // the header, last: the host reads it after the synchronize
+      src = (const unsigned char*)w;
+      out = dst;
+      bytes = sizeof(Work);
+    } else {
+      if (L.off[k] < 0 || L.bytes[k] == 0) continue;
+      src = (const unsigned char*)S.p[k];
+      out = dst + L.off[k];
+      bytes = (unsigned long long)L.bytes[k];
+    }
+    const unsigned long long n16 = (((uintptr_t)src | (uintptr_t)out) & 15) == 0 ? bytes / 16 : 0;
+    for (unsigned long long i = t0; i < n16; i += nt) ((uint4*)out)[i] = __ldcg((const uint4*)src + i);
+    for (unsigned long long i = n16 * 16 + t0; i < bytes; i += nt) out[i] = src[i];
+  }
 }
 
-int mars_enqueue_gather_out(cudaStream_t s, const OutList& L, unsigned char* host_dst) {
-  if (L.n <= 0) return 0;
-  unsigned long long mx = 0;
-  for (int i = 0; i < L.n; ++i) mx = L.d[i].bytes > mx ? L.d[i].bytes : mx;
-  unsigned long long gx = (mx / 16 + 255) / 256;
-  gx = gx < 1 ? 1 : (gx > 64 ? 64 : gx);
-  k_gather_out<<<dim3((unsigned)gx, (unsigned)L.n), 256, 0, s>>>(L, host_dst);
-  return (int)cudaGetLastError();
-}
 
 __global__ void k_flush(u8* p, i64 n, u32 salt) {
   u32* q = (u32*)p;
@@ -4573,6 +4582,12 @@ int mars_enqueue_step(const LaunchArgs* a) {
   return launches;
 }
 
+int mars_enqueue_out_fold(cudaStream_t s, const Work* w, const OutSrc& S, unsigned char* arena,
+                          long long cap) {
+  k_out_fold<<<64, 256, 0, s>>>(w, S, arena, cap);
+  return (int)cudaGetLastError();
+}
+
 int mars_enqueue_retention(const Cfg& c, cudaStream_t s, i64 n, const i32* ctx, const i32* kv,
                            i64 total, double usage, double ema, double now, u8* pin, double* bb,
                            double* cc, double* dd) {
@@ -4598,9 +4613,10 @@ const void* mars_work_init_fn() { return (const void*)k_work_init; }
 int mars_kernels_preload() {
   cudaFuncAttributes fa;
   const void* fns[] = {(const void*)k_advance, (const void*)k_build_global_queue,
+                       (const void*)k_out_fold,
                        (const void*)k_control, (const void*)k_exp_gather,
                        (const void*)k_exp_small, (const void*)k_export_queue,
-                       (const void*)k_flush, (const void*)k_gather, (const void*)k_gather_out,
+                       (const void*)k_flush, (const void*)k_gather,
                        (const void*)k_global_control, (const void*)k_lsd_coop,
                        (const void*)k_pack, (const void*)k_resume,
                        (const void*)k_retention_batch, (const void*)k_scan,

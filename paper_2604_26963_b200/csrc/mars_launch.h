@@ -4,6 +4,53 @@
 #include "mars_internal.cuh"
 #include "mars_kv.h"
 
+// The step's outputs in the pinned host arena, laid out by the device
+// (k_out_fold, launched by mars_step_fetch behind the step) and parsed by the
+// host after one stream synchronize: the Work struct at offset 0, then every
+// output array, 16-byte aligned, in this slot order.  The same function runs
+// on both sides.
+enum {
+  OS_EXP_ROW, OS_EXP_BLK, OS_ADM, OS_ADM_IDX, OS_WIN, OS_DEC, OS_PRE, OS_PRE_GRANT,
+  OS_EV_ROW, OS_EV_KIND, OS_EV_BLK, OS_J_OP, OS_J_ROW, OS_J_N, OS_RET_ROW, OS_RET_PIN,
+  OS_RET_B, OS_RET_C, OS_RET_D, OS_DEC_LEVEL, OS_PRE_LEVEL, OS_SVC_PRE, OS_END_ROW,
+  OS_END_KIND, OS_END_BLK, OS_END_PIN, OS_END_B, OS_END_C, OS_END_D, OS_PRE_DONE,
+  OS_FIN_ROW, OS_FIN_PIN, OS_FIN_B, OS_FIN_C, OS_FIN_D, OS_N
+};
+struct OutSrc {
+  const void* p[OS_N];  // device sources per slot
+  long long ev_cap, j_cap;
+  int coord;
+};
+struct OutLay {
+  long long off[OS_N];    // byte offset in the arena (-1: the arena is too small)
+  long long bytes[OS_N];
+};
+#define OUT_HDR (((long long)sizeof(Work) + 15) & ~15ll)
+
+__host__ __device__ inline void out_layout(const Work& w, const OutSrc& S, long long cap,
+                                           OutLay* L) {
+  const int mode = w.in.mode;
+  const bool sharded = (mode & MARS_MODE_SHARDED) != 0;
+  const long long n_adm = sharded ? (long long)w.n_adm_own : (long long)w.take;
+  const long long ne = w.n_evict < S.ev_cap ? w.n_evict : S.ev_cap;
+  const long long nj = w.n_journal < S.j_cap ? w.n_journal : S.j_cap;
+  const long long ret = w.n_ret, ren = w.n_round_end, fin = w.n_finish;
+  const long long dec = w.n_dec, pre = w.n_pre, ex = w.n_exp;
+  const long long sz[OS_N] = {
+      ex * 4, ex * 4, n_adm * 4, sharded ? n_adm * 4 : 0, (long long)w.n_window * 4, dec * 4,
+      pre * 4, pre * 4, ne * 4, ne, ne * 4, nj, nj * 4, nj * 4, ret * 4, ret, ret * 8, ret * 8,
+      ret * 8, dec, pre, ((mode & MARS_MODE_SERVICE) && S.coord) ? (dec + pre) * 8 : 0, ren * 4,
+      ren, ren * 4, ren, ren * 8, ren * 8, ren * 8, (mode & MARS_MODE_ADVANCE) ? pre : 0,
+      fin * 4, fin, fin * 8, fin * 8, fin * 8};
+  long long off = OUT_HDR;
+  for (int i = 0; i < OS_N; ++i) {
+    off = (off + 15) & ~15ll;
+    L->bytes[i] = sz[i];
+    L->off[i] = off + sz[i] <= cap ? off : -1;
+    off += sz[i];
+  }
+}
+
 struct LaunchArgs {
   cudaStream_t stream, side, side2;
   cudaEvent_t ev_fork, ev_join, ev_head, ev_pack, ev_kvx;
@@ -35,6 +82,8 @@ struct LaunchArgs {
   Xchg x;                // sharded exchange buffers
   Queue gq;              // view of the all-gathered global admission list
 };
+int mars_enqueue_out_fold(cudaStream_t s, const Work* w, const OutSrc& S, unsigned char* arena,
+                          long long cap);
 
 int mars_kernels_init();
 int mars_kernels_preload();
@@ -62,18 +111,6 @@ int mars_enqueue_retention(const Cfg& c, cudaStream_t s, i64 n, const i32* ctx, 
                            i64 total, double usage, double ema, double now, u8* pin, double* bb,
                            double* cc, double* dd);
 int mars_enqueue_flush(cudaStream_t s, u8* p, i64 n, u32 salt);
-// the step's outputs -> the pinned host arena in one launch (the kernel
-// stores straight into the mapped host buffer; one descriptor per array)
-#define OUT_MAX 48
-struct OutDesc {
-  const void* src;
-  unsigned long long dst_off, bytes;
-};
-struct OutList {
-  OutDesc d[OUT_MAX];
-  int n;
-};
-int mars_enqueue_gather_out(cudaStream_t s, const OutList& L, unsigned char* host_dst);
 int mars_enqueue_resume(const Tab& t, const Cfg& c, mars_scalars* sc, cudaStream_t s, i64 n,
                         const i64* rows, const double* fin, const double* dur, const i32* newp,
                         const i32* dec, double now, int* counts, u8* o_kind, i32* o_blk,
