@@ -74,6 +74,7 @@ for name, ds in per.items():
     summary[name] = d0
 
 # launch list: shares of the step
+SETUP = ("k_flush", "k_scatter", "k_gather", "k_scatter_cols", "k_kv_bulk_scan", "k_kv_bulk_fill")
 shares = defaultdict(float)
 total = 0.0
 if os.path.exists(launches):
@@ -89,7 +90,9 @@ if os.path.exists(launches):
             k = r[ki].split("(")[0]
             v = float(r[vi].replace(",", ""))
             fh.write(f"{k},{v}\n")
-            if k.startswith("k_") and k not in ("k_flush", "k_scatter", "k_gather"):
+            # one-time setup (the block tables' bulk fill, the snapshot's
+            # column scatter) and the L2 flush are not part of a step
+            if k.startswith("k_") and k not in SETUP:
                 shares[k] += v
                 total += v
 summary["_step_share_cold_serialised"] = {k: round(v / total, 4) for k, v in
