@@ -25,6 +25,10 @@ def _ptr(a: np.ndarray, ct):
     return a.ctypes.data_as(C.POINTER(ct))
 
 
+_COL_INDEX = {name: i for i, name in enumerate(N.COL_FIELDS)}  # mars_cols field order
+assert [f for f, _ in N.MarsCols._fields_] == list(N.COL_FIELDS.values())
+_P_COLS = C.POINTER(N.MarsCols)
+
 _CT = {np.uint8: C.c_uint8, np.uint32: C.c_uint32, np.int32: C.c_int32, np.int64: C.c_int64,
        np.float64: C.c_double}
 
@@ -175,29 +179,33 @@ class MarsEngine:
     # -- session-state store -------------------------------------------------
 
     def upsert(self, cols: Dict[str, np.ndarray], rows: Optional[np.ndarray] = None) -> None:
+        # the mars_cols struct as a raw array of 20 pointers (the drop-in calls
+        # this every tick: no ctypes pointer objects per column)
+        ptrs = np.zeros(len(_COL_INDEX), np.uint64)
         keep = []
-        mc = N.MarsCols()
         n = None
-        for name, field in N.COL_FIELDS.items():
-            if name not in cols:
+        for name, v in cols.items():
+            ci = _COL_INDEX.get(name)
+            if ci is None:
                 continue
-            a = np.ascontiguousarray(cols[name], dtype=COLUMNS[name])
+            a = np.ascontiguousarray(v, dtype=COLUMNS[name])
             keep.append(a)
-            setattr(mc, field, _ptr(a, _CT[COLUMNS[name]]))
-            n = len(a) if n is None else n
-            if len(a) != n:
+            ptrs[ci] = a.ctypes.data
+            if n is None:
+                n = len(a)
+            elif len(a) != n:
                 raise ValueError("column lengths differ")
         if n is None:
             return
+        mc = ptrs.ctypes.data_as(_P_COLS)
         if rows is None:
-            self._check(self.lib.mars_upsert_rows(self.ctx, n, None, C.byref(mc)))
+            self._check(self.lib.mars_upsert_rows(self.ctx, n, None, mc))
             self.n_rows = max(self.n_rows, n)
         else:
             r = np.ascontiguousarray(rows, dtype=np.int64)
             if len(r) != n:
                 raise ValueError("rows / column length mismatch")
-            self._check(self.lib.mars_upsert_rows(self.ctx, n, r.ctypes.data_as(C.c_void_p),
-                                                  C.byref(mc)))
+            self._check(self.lib.mars_upsert_rows(self.ctx, n, r.ctypes.data, mc))
             if n:
                 self.n_rows = max(self.n_rows, int(r.max()) + 1)
 
