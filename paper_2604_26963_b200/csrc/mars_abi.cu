@@ -38,6 +38,7 @@ struct mars_ctx {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_head = nullptr, ev_pack = nullptr;
   cudaEvent_t ev_kvx = nullptr;
   cudaEvent_t ev_up = nullptr;         // the small-upsert arena's last copy
+  cudaEvent_t ev_sc = nullptr;         // the scalars' staging copy's last upload
   unsigned char* h_up = nullptr;       // pinned arena of small upserts (UP_ARENA bytes)
   int pack_ctas = 20;
   mars_config hcfg;
@@ -294,6 +295,7 @@ int mars_create(const mars_config* hcfg, int device, int64_t max_rows, int64_t m
   CK(cudaEventCreateWithFlags(&ctx->ev_pack, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&ctx->ev_kvx, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&ctx->ev_up, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ctx->ev_sc, cudaEventDisableTiming));
   CK(cudaMallocHost((void**)&ctx->h_up, UP_ARENA));
   {
     const char* e = getenv("MARS_PACK_CTAS");  // tuning knob: 0 disables the early pack
@@ -552,6 +554,7 @@ int mars_destroy(mars_ctx* ctx) {
   if (ctx->ev_pack) cudaEventDestroy(ctx->ev_pack);
   if (ctx->ev_kvx) cudaEventDestroy(ctx->ev_kvx);
   if (ctx->ev_up) cudaEventDestroy(ctx->ev_up);
+  if (ctx->ev_sc) cudaEventDestroy(ctx->ev_sc);
   if (ctx->h_up) cudaFreeHost(ctx->h_up);
   if (ctx->side2) cudaStreamDestroy(ctx->side2);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -913,9 +916,12 @@ int mars_set_scalars(mars_ctx* ctx, const mars_scalars* s) {
   if (s->total_blocks < 1 || s->free_blocks < 0 || s->free_blocks > s->total_blocks)
     return fail(ctx, MARS_ERR_CONTRACT, "bad pool counters");
   CK(cudaSetDevice(ctx->device));
+  // stream-ordered, no host wait: the pinned staging copy is rewritten only
+  // once its previous upload completed (ev_sc)
+  CK(cudaEventSynchronize(ctx->ev_sc));
   *ctx->h_sc = *s;
   CK(cudaMemcpyAsync(ctx->sc, ctx->h_sc, sizeof(mars_scalars), cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaEventRecord(ctx->ev_sc, ctx->stream));
   ctx->q_upper = s->queue_len;
   return MARS_OK;
 }
