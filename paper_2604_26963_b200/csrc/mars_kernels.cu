@@ -4330,6 +4330,7 @@ static void lchk(const char* name) {
 
 static int g_no_pdl = 0;    // MARS_NO_PDL=1: plain stream order between the step head and k_scan
 static int g_no_stage = 0;  // MARS_SCAN_NO_STAGE=1: k_scan emits without staging (tests)
+static int g_no_ctl_pdl = 0;  // MARS_NO_CTL_PDL=1: k_control in plain stream order behind the push
 
 static void scan_geometry(i64 n, int nsm, int* grid, i64* chunk) {
   i64 g = (n + SCAN_TILE - 1) / SCAN_TILE;
@@ -4382,6 +4383,8 @@ int mars_kernels_init() {
   {
     const char* v = getenv("MARS_SCAN_NO_STAGE");
     g_no_stage = (v && v[0] == '1') ? 1 : 0;
+    const char* cp = getenv("MARS_NO_CTL_PDL");
+    g_no_ctl_pdl = (cp && cp[0] == '1') ? 1 : 0;
     const char* pd = getenv("MARS_NO_PDL");
     g_no_pdl = (pd && pd[0] == '1') ? 1 : 0;
     const char* d = getenv("MARS_DEBUG_LAUNCH");
@@ -4536,8 +4539,25 @@ int mars_enqueue_step(const LaunchArgs* a) {
     int npass = a->queue_passes;
     void* args[] = {&t, &c, &w, &b, &Q, &L, &sc, &qsel, &G, &x, &npass};
     mark(2, 0, s);
-    cudaLaunchCooperativeKernel((const void*)k_control, dim3(lg), dim3(1024), args,
-                                sort_smem_bytes(), s);
+    // right behind the S5 push: a programmatic dependent of it (launched once
+    // every push CTA is past its wait for the scan, so the scan's results are
+    // visible; the control plane reads nothing the push writes), its CTAs
+    // placed as the push's drain instead of after the push's end
+    const bool ctl_pdl = kv_fused && !a->exp_sort && !a->exp_may_be_big && !g_no_pdl &&
+                         !g_no_ctl_pdl && !a->prof;
+    cudaLaunchConfig_t cc = {};
+    cc.gridDim = dim3(lg);
+    cc.blockDim = dim3(1024);
+    cc.dynamicSmemBytes = sort_smem_bytes();
+    cc.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cc.attrs = at;
+    cc.numAttrs = ctl_pdl ? 2 : 1;
+    cudaLaunchKernelExC(&cc, (const void*)k_control, args);
     lchk("k_control");
     mark(2, 1, s);
     launches++;

@@ -500,6 +500,9 @@ __global__ void k_kv_exp_push(Kv k, const Work* w, Bufs b) {
   // (a programmatic dependent of k_scan when the scan laid out the offsets:
   // resident early, it waits here for the scan's completion; a no-op else)
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  // the scan is complete: the control plane behind (a programmatic dependent
+  // that shares no data with the push) may take SMs as they free up
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   KVT_BEGIN(0);
   const int ne = w->n_exp;
   if (__ldcg(&k.xbase[1]) < 0) return;  // the stack overflowed (status set)
