@@ -4604,7 +4604,13 @@ int mars_enqueue_step(const LaunchArgs* a) {
 
 int mars_enqueue_out_fold(cudaStream_t s, const Work* w, const OutSrc& S, unsigned char* arena,
                           long long cap) {
-  k_out_fold<<<64, 256, 0, s>>>(w, S, arena, cap);
+  static int ctas = -1;
+  if (ctas < 0) {
+    const char* v = getenv("MARS_FOLD_CTAS");
+    ctas = v ? atoi(v) : 296;
+    if (ctas < 1) ctas = 1;
+  }
+  k_out_fold<<<ctas, 256, 0, s>>>(w, S, arena, cap);
   return (int)cudaGetLastError();
 }
 
