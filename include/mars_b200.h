@@ -248,9 +248,10 @@ int mars_read_rows(mars_ctx* ctx, int64_t n, const int64_t* rows, mars_cols* out
  * address (max_rows rows).  Allocated on the first call, owned by the context. */
 int mars_input_arena(mars_ctx* ctx, void** base, int64_t* bytes, mars_cols* cols);
 /* rows [0, n) of the columns in `mask` (bit i = the i-th mars_cols field)
- * from the input arena to the table: one pitched copy per run of adjacent
- * columns of one element size (3 copies for a default step's 17 columns,
- * instead of 17); sync (the arena may be rewritten after the return) */
+ * from the input arena to the table: n == max_rows and slab-contiguous
+ * columns (a default step's 17 are) -> ONE linear copy; else one pitched
+ * copy per run of adjacent columns of one element size; sync (the arena may
+ * be rewritten after the return) */
 int mars_upsert_arena(mars_ctx* ctx, int64_t n, uint64_t mask);
 /* admission list (sim.py:132 admission_queue; control.py:190 persistent order) */
 int mars_set_queue(mars_ctx* ctx, int64_t n, const uint32_t* rows, const int32_t* req_blocks,

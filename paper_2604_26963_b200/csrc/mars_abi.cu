@@ -312,19 +312,20 @@ int mars_create(const mars_config* hcfg, int device, int64_t max_rows, int64_t m
   memset(&t, 0, sizeof t);
   t.cap = R;
   {
-    // slab order: adjacent columns of one element size form one 2D copy in
-    // mars_upsert_arena; the columns a default step does not read (arrival,
-    // served, rounds_left) close their groups
+    // slab order: a default step's 17 columns first (u8 x5, f64 x3, 4-byte
+    // x9: one contiguous range, one linear copy of the whole table in
+    // mars_upsert_arena), then rounds_left, arrival, served; adjacent columns
+    // of one element size form one pitched copy otherwise
     struct {
       void** p;
       int esz;
     } lay[] = {{(void**)&t.phase, 1}, {(void**)&t.flags, 1}, {(void**)&t.level, 1},
                {(void**)&t.promos, 1}, {(void**)&t.plevel, 1}, {(void**)&t.rs, 8},
-               {(void**)&t.ws, 8},     {(void**)&t.dl, 8},     {(void**)&t.arr, 8},
-               {(void**)&t.served, 8}, {(void**)&t.ctx, 4},    {(void**)&t.kv, 4},
-               {(void**)&t.rem, 4},    {(void**)&t.pb, 4},     {(void**)&t.req, 4},
-               {(void**)&t.r0p, 4},    {(void**)&t.r0d, 4},    {(void**)&t.pre, 4},
-               {(void**)&t.rank, 4},   {(void**)&t.rleft, 4}};
+               {(void**)&t.ws, 8},     {(void**)&t.dl, 8},     {(void**)&t.ctx, 4},
+               {(void**)&t.kv, 4},     {(void**)&t.rem, 4},    {(void**)&t.pb, 4},
+               {(void**)&t.req, 4},    {(void**)&t.r0p, 4},    {(void**)&t.r0d, 4},
+               {(void**)&t.pre, 4},    {(void**)&t.rank, 4},   {(void**)&t.rleft, 4},
+               {(void**)&t.arr, 8},    {(void**)&t.served, 8}};
     size_t tot = 0;
     for (auto& l : lay) tot += (size_t)R * l.esz;
     ALLOC(ctx->slab, tot);
@@ -675,6 +676,11 @@ int mars_input_arena(mars_ctx* ctx, void** base, int64_t* bytes, mars_cols* cols
   if (!ctx->h_in_arena) {
     CK(cudaMallocHost((void**)&ctx->h_in_arena, ctx->slab_bytes));
     memset(ctx->h_in_arena, 0, ctx->slab_bytes);
+    // the capacity padding rows [max_rows, alloc_rows) hold the device's
+    // initial values (a whole-table upload copies them along)
+    const i64 R = ctx->alloc_rows, M = ctx->max_rows;
+    memset(ctx->h_in_arena + (size_t)((unsigned char*)ctx->tab.phase - ctx->slab) + M, MARS_EMPTY,
+           (size_t)(R - M));
   }
   *base = ctx->h_in_arena;
   *bytes = (int64_t)ctx->slab_bytes;
@@ -697,6 +703,21 @@ int mars_upsert_arena(mars_ctx* ctx, int64_t n, uint64_t mask) {
     if (mask >> i & 1) sel.push_back({ctx->cols[i].slab_off, ctx->cols[i].esz});
   std::sort(sel.begin(), sel.end());
   const size_t R = (size_t)ctx->alloc_rows;
+  if (n == ctx->max_rows) {
+    // the whole table of slab-contiguous columns: ONE linear copy (the padding
+    // rows past max_rows carry the device's initial values, set above)
+    bool contiguous = true;
+    for (size_t i = 1; i < sel.size(); ++i)
+      contiguous &= sel[i].first == sel[i - 1].first + R * (size_t)sel[i - 1].second;
+    if (contiguous) {
+      const size_t a = sel.front().first, b = sel.back().first + R * (size_t)sel.back().second;
+      CK(cudaMemcpyAsync(ctx->slab + a, ctx->h_in_arena + a, b - a, cudaMemcpyHostToDevice,
+                         ctx->stream));
+      if (n > ctx->n_rows) ctx->n_rows = n;
+      CK(cudaStreamSynchronize(ctx->stream));
+      return MARS_OK;
+    }
+  }
   for (size_t i = 0; i < sel.size();) {
     size_t j = i + 1;
     while (j < sel.size() && sel[j].second == sel[i].second &&
